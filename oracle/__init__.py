@@ -1,0 +1,244 @@
+"""ORACLE — test infrastructure only.
+
+numpy/ctypes front-end over two CPU checkers of the hot path
+(`Pipeline::train_microbatch`, /root/reference/proj/src/pipeline.cpp:97-141):
+
+* ``Oracle("c")``   -> oracle/liboracle.so, the plain-C fp64 restatement
+  (oracle/parl_oracle.c);
+* ``Oracle("ref")`` -> oracle/_ref/libparl_ref.so, the reference's own sources
+  compiled by oracle/Makefile behind oracle/ref_shim.cpp.
+
+Both expose the same methods, so tests can pin one against the other.  Only
+tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg import this
+package; the product path (paper_2511_18871_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_C = os.path.join(HERE, "liboracle.so")
+LIB_REF = os.path.join(HERE, "_ref", "libparl_ref.so")
+REF_SRC = "/root/reference/proj"
+
+
+def build(ref: bool = True) -> None:
+    """Compile the C restatement, and the reference shim when the reference is mounted."""
+    subprocess.check_call(["make", "-s", "-C", HERE, "liboracle.so"])
+    if ref and os.path.isdir(REF_SRC):
+        subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "ref"])
+
+
+@dataclass(frozen=True)
+class Cfg:
+    """ModelConfig, proj/include/parl/model.hpp:26-36."""
+
+    vocab: int = 64
+    d_model: int = 32
+    n_layers: int = 2
+    n_heads: int = 2
+    d_ff: int = 64
+    max_seq: int = 256
+
+    def c(self):
+        return (C.c_int * 6)(self.vocab, self.d_model, self.n_layers, self.n_heads, self.d_ff, self.max_seq)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        names = {1: "ConfigError", 2: "ShapeError", 3: "VocabError", 4: "LifecycleError", 5: "NumericError"}
+        self.code = code
+        self.kind = names.get(code, "Error")
+        super().__init__(f"{self.kind} in {what}")
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+class Oracle:
+    def __init__(self, kind: str = "c"):
+        self.kind = kind
+        path = LIB_C if kind == "c" else LIB_REF
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.lib = C.CDLL(path)
+        self.px = "orc_" if kind == "c" else "ref_"
+        for name in ("clipped_term", "kl_term"):
+            f = getattr(self.lib, self.px + name)
+            f.restype = C.c_double
+            f.argtypes = [C.c_double] * (4 if name == "clipped_term" else 2)
+        if kind == "ref":
+            self.lib.ref_bench_microbatch.restype = C.c_double
+            self.lib.ref_bench_microbatch.argtypes = [C.c_void_p, C.c_ulonglong] + [C.c_int] * 5
+            self.lib.ref_param_count.restype = C.c_long
+        else:
+            self.lib.orc_param_count.restype = C.c_size_t
+        self.lib[self.px + "init_params"].argtypes = [C.c_void_p, C.c_ulonglong, C.c_void_p]
+
+    def _f(self, name):
+        return getattr(self.lib, self.px + name)
+
+    @staticmethod
+    def _chk(rc, what):
+        if rc < 0:
+            raise OracleError(-rc, what)
+        return rc
+
+    def param_count(self, cfg: Cfg) -> int:
+        c = cfg.c()
+        return int(self._f("param_count")(C.byref(c)))
+
+    def init_params(self, cfg: Cfg, seed: int) -> np.ndarray:
+        w = np.zeros(self.param_count(cfg), dtype=np.float64)
+        c = cfg.c()
+        self._chk(self._f("init_params")(C.byref(c), C.c_ulonglong(seed), _p(w)), "init_params")
+        return w
+
+    def pack(self, prompt, responses, max_seq):
+        prompt = _i32(prompt)
+        lens = _i32([len(r) for r in responses])
+        flat = _i32(np.concatenate([np.asarray(r, dtype=np.int32) for r in responses]) if len(responses) else [])
+        T = len(prompt) + int(lens.sum())
+        out = {k: np.zeros(max(T, 1), dtype=np.int32) for k in ("tokens", "labels", "positions", "seg", "pred")}
+        spans = np.zeros(max(len(responses), 1), dtype=np.int32)
+        if self.kind == "c":
+            rc = self.lib.orc_pack(_p(prompt), len(prompt), _p(flat), _p(lens), len(responses), max_seq,
+                                   _p(out["tokens"]), _p(out["labels"]), _p(out["positions"]), _p(spans),
+                                   _p(out["seg"]), _p(out["pred"]))
+        else:
+            rc = self.lib.ref_pack(_p(prompt), len(prompt), _p(flat), _p(lens), len(responses), max_seq,
+                                   _p(out["tokens"]), _p(out["labels"]), _p(out["positions"]), _p(spans))
+        self._chk(rc, "pack")
+        res = {k: v[:rc] for k, v in out.items()}
+        res["span_start"] = spans[: len(responses)]
+        res["lens"] = lens
+        if self.kind != "c":
+            res.pop("seg")
+            res.pop("pred")
+        return res
+
+    def forward(self, cfg: Cfg, w, tokens, positions, labels, prompt_len=0, resp_lens=(), upstream=None,
+                grad_acc=None):
+        """forward_logprobs (+ backward into grad_acc when upstream is given)."""
+        tokens, positions, labels = _i32(tokens), _i32(positions), _i32(labels)
+        lens = _i32(resp_lens if len(resp_lens) else [0])
+        T = len(tokens)
+        lp = np.zeros(max(T, 1), dtype=np.float64)
+        c = cfg.c()
+        w = _f64(w)
+        up = _f64(upstream) if upstream is not None else None
+        if up is not None and grad_acc is None:
+            grad_acc = np.zeros(len(w), dtype=np.float64)
+        if self.kind == "c":
+            rc = self.lib.orc_forward(C.byref(c), _p(w), _p(tokens), _p(positions), T, prompt_len, _p(lens),
+                                      len(resp_lens), _p(labels), _p(lp), None, _p(up), _p(grad_acc), None)
+        else:
+            rc = self.lib.ref_forward(C.byref(c), _p(w), _p(tokens), _p(positions), T, prompt_len, _p(lens),
+                                      len(resp_lens), _p(labels), _p(lp), _p(up), _p(grad_acc))
+        self._chk(rc, "forward")
+        return (lp[:rc], grad_acc) if up is not None else lp[:rc]
+
+    def logprob_rows(self, cfg: Cfg, w, tokens, positions, prompt_len=0, resp_lens=()):
+        tokens, positions = _i32(tokens), _i32(positions)
+        lens = _i32(resp_lens if len(resp_lens) else [0])
+        T = len(tokens)
+        rows = np.zeros(T * cfg.vocab, dtype=np.float64)
+        c = cfg.c()
+        w = _f64(w)
+        if self.kind == "c":
+            rc = self.lib.orc_forward(C.byref(c), _p(w), _p(tokens), _p(positions), T, prompt_len, _p(lens),
+                                      len(resp_lens), None, None, None, None, None, _p(rows))
+        else:
+            rc = self.lib.ref_logprob_rows(C.byref(c), _p(w), _p(tokens), _p(positions), T, prompt_len,
+                                           _p(lens), len(resp_lens), _p(rows))
+        self._chk(rc, "logprob_rows")
+        return rows.reshape(T, cfg.vocab)
+
+    def group_advantages(self, rewards, mean_only=False):
+        r = _f64(rewards)
+        a = np.zeros(len(r), dtype=np.float64)
+        self._chk(self._f("group_advantages")(_p(r), len(r), int(mean_only), _p(a)), "group_advantages")
+        return a
+
+    def clipped_term(self, lp, old, adv, eps):
+        return self._f("clipped_term")(lp, old, adv, eps)
+
+    def kl_term(self, lp, ref):
+        return self._f("kl_term")(lp, ref)
+
+    def sample_terms(self, lp, old, ref, adv, eps, beta, granularity=0):
+        lp, old, ref = _f64(lp), _f64(old), _f64(ref)
+        up = np.zeros(len(lp), dtype=np.float64)
+        out4 = np.zeros(4, dtype=np.float64)
+        self._chk(self._f("sample_terms")(_p(lp), _p(old), _p(ref), len(lp), C.c_double(adv), C.c_double(eps),
+                                          C.c_double(beta), granularity, _p(up), _p(out4)), "sample_terms")
+        return {"clip_term": out4[0], "kl": out4[1], "clipped_units": int(out4[2]), "total_units": int(out4[3]),
+                "upstream": up}
+
+    def train_microbatch(self, cfg: Cfg, w_pol, w_old, w_ref, prompt, responses, advantages, eps=0.2,
+                         beta=0.04, granularity=0, grad_acc=None):
+        """Pipeline::train_microbatch shared-prompt branch.  Returns (grad, stats5, lp3[3,S])."""
+        prompt = _i32(prompt)
+        lens = _i32([len(r) for r in responses])
+        flat = _i32(np.concatenate([np.asarray(r, dtype=np.int32) for r in responses]))
+        adv = _f64(advantages)
+        S = int(lens.sum())
+        if grad_acc is None:
+            grad_acc = np.zeros(len(w_pol), dtype=np.float64)
+        stats = np.zeros(5, dtype=np.float64)
+        lp3 = np.zeros(3 * S, dtype=np.float64)
+        c = cfg.c()
+        w_pol, w_old, w_ref = _f64(w_pol), _f64(w_old), _f64(w_ref)
+        rc = self._f("train_microbatch")(C.byref(c), _p(w_pol), _p(w_old), _p(w_ref), _p(prompt), len(prompt),
+                                         _p(flat), _p(lens), len(responses), _p(adv), *(
+                                             [None] if self.kind == "c" else []),
+                                         C.c_double(eps), C.c_double(beta), granularity, _p(grad_acc), _p(stats),
+                                         _p(lp3))
+        self._chk(rc, "train_microbatch")
+        return grad_acc, stats, lp3.reshape(3, S)
+
+    def bench_microbatch(self, cfg: Cfg, seed, P, G, R, reps, threads) -> float:
+        assert self.kind == "ref"
+        c = cfg.c()
+        return float(self.lib.ref_bench_microbatch(C.byref(c), C.c_ulonglong(seed), P, G, R, reps, threads))
+
+
+def layout(cfg: Cfg):
+    """Named (offset, rows, cols) slices of the flat parameter array, model.cpp:86-114."""
+    d, F, V = cfg.d_model, cfg.d_ff, cfg.vocab
+    out = []
+    o = 0
+
+    def add(name, r, c):
+        nonlocal o
+        out.append((name, o, r, c))
+        o += r * c
+
+    add("tok_emb", V, d)
+    add("pos_emb", cfg.max_seq, d)
+    for l in range(cfg.n_layers):
+        p = f"layers.{l}."
+        for n, r, c in (("ln1.gamma", 1, d), ("ln1.beta", 1, d), ("attn.wq", d, d), ("attn.bq", 1, d),
+                        ("attn.wk", d, d), ("attn.bk", 1, d), ("attn.wv", d, d), ("attn.bv", 1, d),
+                        ("attn.wo", d, d), ("attn.bo", 1, d), ("ln2.gamma", 1, d), ("ln2.beta", 1, d),
+                        ("ffn.w1", d, F), ("ffn.b1", 1, F), ("ffn.w2", F, d), ("ffn.b2", 1, d)):
+            add(p + n, r, c)
+    add("ln_f.gamma", 1, d)
+    add("ln_f.beta", 1, d)
+    add("head.w", d, V)
+    add("head.b", 1, V)
+    return out

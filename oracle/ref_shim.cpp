@@ -1,0 +1,275 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" shim over the UNMODIFIED reference sources (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libparl_ref.so).
+// It is used (a) to pin the C restatement in parl_oracle.c, (b) to generate
+// the golden fixtures in tests/golden/, and (c) as the CPU baseline in
+// bench.py (`cpu_baseline.kind = "reference"`).  Nothing here is product code.
+#include <chrono>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "parl/grpo.hpp"
+#include "parl/model.hpp"
+#include "parl/packing.hpp"
+#include "parl/pipeline.hpp"
+#include "parl/rng.hpp"
+
+using namespace parl;
+
+namespace {
+
+struct CCfg {
+    int vocab, d_model, n_layers, n_heads, d_ff, max_seq;
+};
+
+ModelConfig to_cfg(const CCfg* c) {
+    ModelConfig m;
+    m.vocab_size = c->vocab;
+    m.d_model = c->d_model;
+    m.n_layers = c->n_layers;
+    m.n_heads = c->n_heads;
+    m.d_ff = c->d_ff;
+    m.max_seq_len = c->max_seq;
+    return m;
+}
+
+// Error convention of the C-ABI: errors.hpp types -> small positive codes.
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const ConfigError&) {
+        return -1;
+    } catch (const ShapeError&) {
+        return -2;
+    } catch (const VocabError&) {
+        return -3;
+    } catch (const LifecycleError&) {
+        return -4;
+    } catch (const NumericError&) {
+        return -5;
+    } catch (...) {
+        return -99;
+    }
+}
+
+ModelParams params_from(const CCfg* c, const double* w) {
+    ModelParams p = ModelParams::init(to_cfg(c), 0);
+    if (w) std::memcpy(p.flat_mut().data(), w, p.flat().size() * sizeof(double));
+    return p;
+}
+
+AttentionMaskSpec mask_from(int P, const int* lens, int G) {
+    if (P <= 0) return AttentionMaskSpec::causal();
+    return AttentionMaskSpec::shared_prompt(P, std::vector<int>(lens, lens + G));
+}
+
+}  // namespace
+
+extern "C" {
+
+long ref_param_count(const CCfg* c) {
+    return guarded([&] { return (int)ModelParams::init(to_cfg(c), 0).flat().size(); });
+}
+
+int ref_init_params(const CCfg* c, unsigned long long seed, double* out) {
+    return guarded([&] {
+        ModelParams p = ModelParams::init(to_cfg(c), seed);
+        std::memcpy(out, p.flat().data(), p.flat().size() * sizeof(double));
+        return 0;
+    });
+}
+
+// pack_group (packing.cpp:7-45).  Returns T.
+int ref_pack(const int* prompt, int P, const int* resp_flat, const int* lens, int G, int max_seq,
+             int* tokens, int* labels, int* positions, int* span_start) {
+    return guarded([&] {
+        std::vector<TokenId> pr(prompt, prompt + P);
+        std::vector<std::vector<TokenId>> rs;
+        int off = 0;
+        for (int g = 0; g < G; ++g) {
+            rs.emplace_back(resp_flat + off, resp_flat + off + lens[g]);
+            off += lens[g];
+        }
+        PackedGroup pg = pack_group(pr, rs, max_seq);
+        std::copy(pg.tokens.begin(), pg.tokens.end(), tokens);
+        std::copy(pg.labels.begin(), pg.labels.end(), labels);
+        std::copy(pg.positions.begin(), pg.positions.end(), positions);
+        for (size_t g = 0; g < pg.spans.size(); ++g) span_start[g] = pg.spans[g].start;
+        return (int)pg.tokens.size();
+    });
+}
+
+// forward_logprobs (+ backward when upstream != nullptr; grad ADDED to grad_acc).
+int ref_forward(const CCfg* c, const double* w, const int* tokens, const int* positions, int T,
+                int P, const int* lens, int G, const int* labels, double* lp_out,
+                const double* upstream, double* grad_acc) {
+    return guarded([&] {
+        ModelParams p = params_from(c, w);
+        auto mask = mask_from(P, lens, G);
+        std::span<const TokenId> tk(tokens, T);
+        std::span<const int> ps(positions, T);
+        std::span<const std::int32_t> lb(labels, T);
+        ForwardResult f = forward_logprobs(p, tk, ps, mask, lb, upstream != nullptr);
+        std::copy(f.logprobs.begin(), f.logprobs.end(), lp_out);
+        if (upstream) {
+            GradBuffer g = backward(p, f, std::span<const double>(upstream, f.logprobs.size()));
+            for (size_t i = 0; i < g.flat().size(); ++i) grad_acc[i] += g.flat()[i];
+        }
+        return (int)f.logprobs.size();
+    });
+}
+
+int ref_logprob_rows(const CCfg* c, const double* w, const int* tokens, const int* positions,
+                     int T, int P, const int* lens, int G, double* rows) {
+    return guarded([&] {
+        ModelParams p = params_from(c, w);
+        auto r = forward_logprob_rows(p, std::span<const TokenId>(tokens, T),
+                                      std::span<const int>(positions, T), mask_from(P, lens, G));
+        std::copy(r.begin(), r.end(), rows);
+        return 0;
+    });
+}
+
+int ref_group_advantages(const double* r, int G, int mean_only, double* a) {
+    return guarded([&] {
+        auto v = mean_only ? group_advantages_mean_only(std::span<const double>(r, G))
+                           : group_advantages(std::span<const double>(r, G));
+        std::copy(v.begin(), v.end(), a);
+        return 0;
+    });
+}
+
+int ref_sample_terms(const double* lp, const double* old, const double* ref, int n, double A,
+                     double eps, double beta, int gran, double* upstream, double* out4) {
+    return guarded([&] {
+        Sample s;
+        s.response.assign(n, 4);
+        s.old_logprobs.assign(old, old + n);
+        s.ref_logprobs.assign(ref, ref + n);
+        s.advantage = A;
+        SampleTerms st = per_sample_terms(s, std::span<const double>(lp, n), eps, beta,
+                                          gran ? LossGranularity::sequence : LossGranularity::token);
+        std::copy(st.upstream.begin(), st.upstream.end(), upstream);
+        out4[0] = st.clip_term;
+        out4[1] = st.kl;
+        out4[2] = st.clipped_units;
+        out4[3] = st.total_units;
+        return 0;
+    });
+}
+
+double ref_clipped_term(double lp, double old, double A, double eps) {
+    return clipped_term(lp, old, A, eps);
+}
+double ref_kl_term(double lp, double r) { return kl_term(lp, r); }
+
+}  // extern "C"
+
+namespace {
+
+// Pipeline::train_microbatch shared-prompt branch (pipeline.cpp:97-141),
+// replayed through the reference's public operator API.
+void microbatch(TriModel& tm, const std::vector<TokenId>& prompt,
+                const std::vector<std::vector<TokenId>>& responses,
+                const std::vector<double>& advantages, double eps, double beta,
+                LossGranularity gran, GradBuffer& grads, double* stats5, double* lp3) {
+    PackedGroup packed = pack_group(prompt, responses, tm.policy.config().max_seq_len);
+    TriForwardResult tri =
+        trimodel_forward(tm, packed.tokens, packed.positions, packed.mask, packed.labels);
+    auto pol = extract_response_logprobs(tri.policy.logprobs, packed);
+    auto ref = extract_response_logprobs(tri.ref_logprobs, packed);
+    auto old = extract_response_logprobs(tri.old_logprobs, packed);
+    std::vector<double> upstream;
+    for (size_t j = 0; j < responses.size(); ++j) {
+        Sample s;
+        s.prompt = prompt;
+        s.response = responses[j];
+        s.advantage = advantages[j];
+        s.old_logprobs = old[j];
+        s.ref_logprobs = ref[j];
+        SampleTerms st = per_sample_terms(s, pol[j], eps, beta, gran);
+        if (stats5) {
+            stats5[0] += st.clip_term - beta * st.kl;
+            stats5[1] += st.clip_term;
+            stats5[2] += st.kl;
+            stats5[3] += st.clipped_units;
+            stats5[4] += st.total_units;
+        }
+        for (double u : st.upstream) upstream.push_back(-u);
+    }
+    GradBuffer gb = backward(tm.policy, tri.policy, upstream);
+    grads.accumulate(gb);
+    if (lp3) {
+        size_t S = tri.policy.logprobs.size();
+        std::copy(tri.policy.logprobs.begin(), tri.policy.logprobs.end(), lp3);
+        std::copy(tri.old_logprobs.begin(), tri.old_logprobs.end(), lp3 + S);
+        std::copy(tri.ref_logprobs.begin(), tri.ref_logprobs.end(), lp3 + 2 * S);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+// One shared-prompt micro-batch through the reference.  grad_acc += gradient.
+int ref_train_microbatch(const CCfg* c, const double* w_pol, const double* w_old,
+                         const double* w_ref, const int* prompt, int P, const int* resp_flat,
+                         const int* lens, int G, const double* adv, double eps, double beta,
+                         int gran, double* grad_acc, double* stats5, double* lp3) {
+    return guarded([&] {
+        TriModel tm = TriModel::init(to_cfg(c), 0);
+        const size_t n = tm.policy.flat().size();
+        std::memcpy(tm.policy.flat_mut().data(), w_pol, n * sizeof(double));
+        std::memcpy(tm.old_policy.flat_mut().data(), w_old, n * sizeof(double));
+        std::memcpy(tm.reference.flat_mut().data(), w_ref, n * sizeof(double));
+        std::vector<TokenId> pr(prompt, prompt + P);
+        std::vector<std::vector<TokenId>> rs;
+        int off = 0;
+        for (int g = 0; g < G; ++g) {
+            rs.emplace_back(resp_flat + off, resp_flat + off + lens[g]);
+            off += lens[g];
+        }
+        GradBuffer grads(tm.policy);
+        microbatch(tm, pr, rs, std::vector<double>(adv, adv + G), eps, beta,
+                   gran ? LossGranularity::sequence : LossGranularity::token, grads, stats5, lp3);
+        for (size_t i = 0; i < n; ++i) grad_acc[i] += grads.flat()[i];
+        return (int)(P + off);
+    });
+}
+
+// CPU baseline: `threads` independent workers, each with its own TriModel
+// (SPEC.md:113 allows distinct instances concurrently), each running `reps`
+// shared-prompt micro-batches of P + G x R tokens with random tokens in
+// [4, V).  Returns wall seconds for the whole job (all threads).
+double ref_bench_microbatch(const CCfg* c, unsigned long long seed, int P, int G, int R, int reps,
+                            int threads) {
+    std::vector<std::thread> pool;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int th = 0; th < threads; ++th) {
+        pool.emplace_back([=] {
+            ModelConfig mc = to_cfg(c);
+            TriModel tm = TriModel::init(mc, seed);
+            Rng rng(mix_seed(seed, 123 + th));
+            for (int rep = 0; rep < reps; ++rep) {
+                std::vector<TokenId> prompt(P);
+                for (auto& t : prompt) t = rng.uniform_int(4, mc.vocab_size - 1);
+                std::vector<std::vector<TokenId>> rs(G, std::vector<TokenId>(R));
+                for (auto& r : rs)
+                    for (auto& t : r) t = rng.uniform_int(4, mc.vocab_size - 1);
+                std::vector<double> rewards(G);
+                for (auto& r : rewards) r = rng.uniform();
+                std::vector<double> adv = group_advantages(rewards);
+                GradBuffer grads(tm.policy);
+                microbatch(tm, prompt, rs, adv, 0.2, 0.04, LossGranularity::token, grads, nullptr,
+                           nullptr);
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"
