@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: packed tokens/s of tri-model log-prob + GRPO loss
+(+ policy backward, + gradient allreduce at N>1) on shared-prompt packed groups.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+A step = every rank processes `groups_per_rank` prompt groups (pack -> tri-model
+forward -> GRPO loss -> policy backward -> accumulate), then the gradient and the
+loss scalars are allreduced over NCCL (N>1).  Weak scaling: per-GPU work is fixed.
+
+Prints ONE JSON line (rank 0).  `value` = device-resident inputs, CUDA-event
+timed; `e2e` = the same through the public C-ABI from pinned host buffers with
+H2D/D2H inside the timed region; `roofline` = dominant kernel class timed with
+CUDA events on its launch stream during the timed region; `cpu_baseline` = the
+reference (oracle/_ref, built from the reference's own sources) on a bounded
+sample, FLOP-scaled to this workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[0]: tiny decoder, fp32 (CPU-runnable oracle case)
+    "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=4),
+    # BASELINE.json configs[1]: Qwen2.5-0.5B-shaped random-init tri-model, G=8, 512+1k, bf16, single B200
+    "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=2),
+}
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def flops_per_group(c, P, lens, reference_head=False):
+    """Algorithmic FLOPs of one micro-step:
+    fwd = 2 T L (4d^2 + 2dF) + 4 pairs d L + 2 rows d V; tri-model = 3 fwd;
+    policy bwd = 2x GEMM terms + 2.5x attention term + 2x head term."""
+    d, L, F, V = c["d"], c["L"], c["F"], c["vocab"]
+    T = P + sum(lens)
+    pairs = P * (P + 1) / 2 + sum(r * P + r * (r + 1) / 2 for r in lens)
+    rows = T if reference_head else 1 + sum(r - 1 for r in lens)
+    gemm = 2.0 * T * L * (4 * d * d + 2 * d * F)
+    attn = 4.0 * pairs * d * L
+    head = 2.0 * rows * d * V
+    return 3 * (gemm + attn + head) + 2 * gemm + 2.5 * attn + 2 * head
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            m = json.load(f)
+        return m["hbm_gbs"], m["bf16_tflops"], m.get("bf16_tflops_sustained", m["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                self.samples.append(p)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist
+    return world, rank, local, pg
+
+
+def allmax(pg, v: float) -> float:
+    if pg is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def cpu_threads(per_thread_bytes: float) -> int:
+    cores = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable"))
+    except Exception:
+        avail = 16 << 30
+    return max(1, min(cores, int(0.6 * avail / per_thread_bytes)))
+
+
+def reference_sample(c, reps=1, threads=None):
+    """Time the reference (oracle/_ref) on a bounded sample with the workload's
+    model dims; return (tokens/s scaled to the workload by the FLOP model, info)."""
+    from oracle import Cfg, Oracle
+
+    try:
+        ref = Oracle("ref")
+    except FileNotFoundError:
+        return None
+    # C2 dims with a tiny packed group: P=2, G=2, R=1 per worker (T=4)
+    sP, sG, sR = (2, 2, 1) if c["vocab"] > 10000 else (c["P"], c["G"], c["R"])
+    cfg = Cfg(c["vocab"], c["d"], c["L"], c["H"], c["F"], max(sP + sG * sR, 8))
+    n_params = ref.param_count(cfg)
+    thr = threads or cpu_threads(6.0 * 8 * n_params)
+    secs = ref.bench_microbatch(cfg, 7, sP, sG, sR, reps, thr)
+    T_s = sP + sG * sR
+    fl_s = flops_per_group(c, sP, [sR] * sG, reference_head=True)
+    fl_w = flops_per_group(c, c["P"], [c["R"]] * c["G"], reference_head=True)
+    T_w = c["P"] + c["G"] * c["R"]
+    tok_s_sample = thr * reps * T_s / secs
+    scaled = tok_s_sample * (fl_s / T_s) / (fl_w / T_w)
+    info = {"cores": thr, "sample": f"reference train_microbatch (shared-prompt) at {c['name']} model dims, "
+                                    f"P={sP},G={sG},R={sR} (T={T_s}) x {reps} per thread, {thr} threads, "
+                                    f"{secs:.1f}s wall; {tok_s_sample:.3f} tok/s on the sample, scaled by "
+                                    f"FLOPs/token to T={T_w}",
+            "secs": secs, "sample_tok_s": tok_s_sample}
+    return scaled, info
+
+
+def run_reference(args, c):
+    world, rank, local, pg = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    c["name"] = args.config
+    T_w = c["P"] + c["G"] * c["R"]
+    from oracle import Oracle
+
+    try:
+        Oracle("ref")
+    except FileNotFoundError:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparl_ref.so not built"}))
+        return
+    for _ in range(args.warmup):
+        reference_sample(c)
+    vals, infos = [], []
+    for _ in range(args.steps):
+        v, info = reference_sample(c)
+        vals.append(v)
+        infos.append(info)
+    value = float(np.mean(vals))
+    out = {"metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref", "value": value,
+           "unit": "packed tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1000.0 * T_w / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
+                                  f"P={c['P']} G={c['G']} R={c['R']} (T={T_w}) per group"},
+           "cpu_baseline": {"value": value, "unit": "packed tokens/s", "cores": infos[0]["cores"],
+                            "kind": "reference", "sample": infos[0]["sample"]},
+           "e2e": {"value": value, "unit": "packed tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def run_ours(args, c):
+    world, rank, local, pg = dist_setup(args.gpus)
+    from paper_2511_18871_b200 import parl as P
+
+    prec = P.PREC_BF16 if c["prec"] == "bf16" else P.PREC_FP32
+    ctx = P.Context(local, prec)
+    if world > 1:
+        uid = P.Context.comm_unique_id() if rank == 0 else b""
+        import torch.distributed as dist
+
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(obj[0], rank, world)
+
+    cfg = P.ModelConfig(c["vocab"], c["d"], c["L"], c["H"], c["F"], c["max_seq"])
+    pol = P.ModelParams.init_device(cfg, 7, ctx)
+    old = pol.clone(seed=11, noise=0.01)
+    ref = pol.clone()
+    tm = P.TriModel(pol, old, ref)
+    grads = P.GradBuffer(pol)
+    hyper = P.HyperParams(0.2, 0.04, "token")
+
+    Pn, G, R, ng = c["P"], c["G"], c["R"], args.groups or c["groups"]
+    T = Pn + G * R
+    rng = np.random.default_rng(123 + rank)
+    prompts = [rng.integers(4, c["vocab"], Pn).astype(np.int32) for _ in range(ng)]
+    resps = [rng.integers(4, c["vocab"], G * R).astype(np.int32) for _ in range(ng)]
+    rewards = [rng.random(G) for _ in range(ng)]
+    lens = np.full(G, R, np.int32)
+    group = P.Group(T, G, ctx)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+    d_prompts = [torch.from_numpy(p).cuda(local) for p in prompts]
+    d_resps = [torch.from_numpy(r).cuda(local) for r in resps]
+    torch.cuda.synchronize(local)
+
+    def step_device():
+        grads.reset()
+        for i in range(ng):
+            group.pack_device(d_prompts[i].data_ptr(), Pn, d_resps[i].data_ptr(), lens, c["max_seq"])
+            P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=False)
+        if world > 1:
+            grads.allreduce()
+            ctx.stats_allreduce()
+
+    # pinned host inputs for the end-to-end leg
+    h_prompts = [torch.from_numpy(p).pin_memory().numpy() for p in prompts]
+    h_resps = [torch.from_numpy(r).pin_memory().numpy() for r in resps]
+
+    def step_e2e():
+        grads.reset()
+        st = None
+        for i in range(ng):
+            group.pack(h_prompts[i], [h_resps[i][k * R:(k + 1) * R] for k in range(G)], c["max_seq"])
+            st = P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=True)
+        if world > 1:
+            grads.allreduce()
+            ctx.stats_allreduce()
+        ctx.sync()
+        return st
+
+    for _ in range(args.warmup):
+        step_device()
+    ctx.sync()
+
+    # ---- device-resident timed region (CUDA events on the library's stream)
+    l0 = ctx.launches
+    ctx.profile(True)
+    barrier(pg)
+    ctx.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        ctx.sync()
+    ctx.profile(False)
+    launches = (ctx.launches - l0) // max(args.steps, 1)
+    ms = e0.elapsed_time(e1)
+    barrier(pg)
+    ms_max = allmax(pg, ms)
+    prof = {k: ctx.profile_read(k) for k in ctx.KC}
+
+    # ---- end-to-end through the public API with host buffers
+    for _ in range(2):
+        step_e2e()
+    barrier(pg)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    e2e_s = time.perf_counter() - t0
+    e2e_max = allmax(pg, e2e_s)
+
+    if rank != 0:
+        return
+    tokens_per_step = world * ng * T
+    value = tokens_per_step * args.steps / (ms_max / 1000.0)
+    e2e_val = tokens_per_step * args.steps / e2e_max
+    hbm, bf16, bf16_sus, src = peaks()
+    # dominant tensor-core class
+    tc = {k: v for k, v in prof.items() if k in ("gemm", "head", "attn_fwd", "attn_bwd") and v["ms"] > 0}
+    dom = max(tc, key=lambda k: tc[k]["ms"]) if tc else "gemm"
+    dp = prof[dom]
+    achieved = dp["work"] / (dp["ms"] / 1000.0) / 1e12 if dp["ms"] > 0 else 0.0
+    step_ms = ms_max / args.steps
+    share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
+    c["name"] = args.config
+    cpu = reference_sample(c) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    out = {
+        "metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref",
+        "value": value, "unit": "packed tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": c["prec"], "data": "synthetic (random-init weights, uniform tokens in [4,V), U[0,1) rewards)",
+        "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
+                               f"P={Pn} G={G} R={R} (T={T}) x {ng} groups per rank per step",
+                   "groups_per_rank": ng, "packed_tokens_per_group": T,
+                   "l2": "working set (weights+activations, GBs) exceeds the 126 MB L2; no explicit flush",
+                   "parallelism": f"dp{world} over prompt groups"},
+        "e2e": {"value": e2e_val, "unit": "packed tokens/s", "h2d_bytes_per_step": ng * (T * 4 + G * 8),
+                "d2h_bytes_per_step": ng * 40},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved, "peak": bf16_sus,
+                     "unit": "TFLOP/s", "frac": achieved / bf16_sus, "peak_kind": f"{src} bf16 sustained",
+                     "traffic": None, "share_of_step": share},
+        "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                               "achieved": (v["work"] / (v["ms"] / 1e3) / (1e12 if k in tc else 1e9))
+                               if v["ms"] > 0 else None,
+                               "unit": "TFLOP/s" if k in ("gemm", "head", "attn_fwd", "attn_bwd") else "GB/s"}
+                           for k, v in prof.items()},
+        "flops_per_group": flops_per_group(c, Pn, [R] * G),
+        "model_tflops": flops_per_group(c, Pn, [R] * G) * ng * world / (step_ms / 1e3) / 1e12,
+        "clocks": clk.summary(),
+    }
+    if cpu is not None:
+        v, info = cpu
+        out["cpu_baseline"] = {"value": v, "unit": "packed tokens/s", "cores": info["cores"], "kind": "reference",
+                               "sample": info["sample"]}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--groups", type=int, default=0, help="prompt groups per rank per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    c = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        run_reference(args, c)
+    else:
+        run_ours(args, c)
+
+
+if __name__ == "__main__":
+    main()

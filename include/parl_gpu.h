@@ -1,0 +1,204 @@
+/*
+ * parl_gpu.h — C-ABI of the B200-native hot path of arXiv 2511.18871:
+ * shared-prompt packing -> tri-model log-prob -> GRPO loss -> policy backward
+ * -> gradient accumulate (+ NCCL allreduce across ranks).
+ *
+ * Plain C types only (no torch, no C++).  Every entry point returns a
+ * parl_status; the codes map 1:1 onto the reference's exception types
+ * (proj/include/parl/errors.hpp:9-46) plus CUDA/NCCL failures, and
+ * parl_last_error() returns the message.  The C++ drop-in layer
+ * (include/parl_gpu.hpp) converts them back into the same exception types.
+ *
+ * Each function cites the reference interface it replaces.  Device buffers
+ * stay resident: weights are uploaded once per version, and only per-token
+ * vectors and scalars cross host<->device on the measured path.
+ */
+#ifndef PARL_GPU_H
+#define PARL_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PARL_OK = 0,
+    PARL_E_CONFIG = 1,    /* ConfigError    errors.hpp:9  */
+    PARL_E_SHAPE = 2,     /* ShapeError     errors.hpp:14 */
+    PARL_E_VOCAB = 3,     /* VocabError     errors.hpp:19 */
+    PARL_E_LIFECYCLE = 4, /* LifecycleError errors.hpp:24 */
+    PARL_E_NUMERIC = 5,   /* NumericError   errors.hpp:29 */
+    PARL_E_BARRIER = 6,   /* BarrierError   errors.hpp:34 */
+    PARL_E_STALL = 7,     /* StallError     errors.hpp:39 */
+    PARL_E_IO = 8,        /* IoError        errors.hpp:44 */
+    PARL_E_CUDA = 9,
+    PARL_E_NCCL = 10
+} parl_status;
+
+/* Arithmetic of the device path.  FP32: fp32 storage, FFMA contractions
+ * (the BASELINE configs[0] precision).  BF16: bf16 operands on tcgen05
+ * tensor cores with fp32 accumulation, fp32 residual stream/statistics. */
+typedef enum { PARL_PREC_FP32 = 0, PARL_PREC_BF16 = 1 } parl_precision;
+
+/* ModelConfig, proj/include/parl/model.hpp:26-36 */
+typedef struct {
+    int vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len;
+} parl_config;
+
+/* HyperParams subset used by the loss, proj/include/parl/pipeline.hpp:29-37 */
+typedef struct {
+    double epsilon;         /* clip range, (0,1) */
+    double beta;            /* KL weight, >= 0 */
+    int granularity;        /* 0 = token, 1 = sequence (LossGranularity) */
+    int advantage_mean_only;/* 0 = (r-mean)/std_pop, 1 = r-mean (grpo.cpp:24-48) */
+} parl_hyper;
+
+/* Pipeline::MicrobatchStats, proj/include/parl/pipeline.hpp:109-116 */
+typedef struct {
+    double objective_sum, clip_sum, kl_sum, clipped_units, total_units;
+} parl_loss_stats;
+
+typedef struct parl_ctx_s* parl_ctx_t;     /* device, stream, workspaces, optional NCCL comm */
+typedef struct parl_model_s* parl_model_t; /* one device weight set (ModelParams) */
+typedef struct parl_group_s* parl_group_t; /* one packed sequence (PackedGroup + K1 outputs) */
+typedef struct parl_act_s* parl_act_t;     /* policy activations (ForwardResult::cache) */
+typedef struct parl_grad_s* parl_grad_t;   /* fp32 gradient accumulator (GradBuffer) */
+
+/* ---- context ------------------------------------------------------------ */
+parl_status parl_ctx_create(int device, parl_precision prec, parl_ctx_t* out);
+parl_status parl_ctx_destroy(parl_ctx_t ctx);
+const char* parl_last_error(parl_ctx_t ctx);
+parl_status parl_ctx_sync(parl_ctx_t ctx);
+/* cudaStream_t the context launches on (for callers timing with events). */
+void* parl_ctx_stream(parl_ctx_t ctx);
+/* Number of kernels this context launched since creation (bench evidence). */
+uint64_t parl_ctx_launches(parl_ctx_t ctx);
+const char* parl_version(void);
+
+/* Kernel-class profiler (bench evidence): when enabled, every launch of the
+ * classes below is bracketed by CUDA events on the context stream and its
+ * algorithmic work (FLOPs or bytes) is recorded.  Reading syncs the stream. */
+typedef enum {
+    PARL_KC_GEMM = 0,      /* all tensor-core / FFMA contractions */
+    PARL_KC_HEAD = 1,      /* LM-head forward contraction (+LSE epilogue) */
+    PARL_KC_ATTN_FWD = 2,
+    PARL_KC_ATTN_BWD = 3,
+    PARL_KC_LOSS = 4,      /* K7 GRPO loss */
+    PARL_KC_PACK = 5,      /* K1 packer */
+    PARL_KC_NORM = 6,      /* LayerNorm fwd/bwd, embeddings, reductions */
+    PARL_KC_COUNT = 7
+} parl_kernel_class;
+parl_status parl_ctx_profile(parl_ctx_t ctx, int enable);
+/* ms = summed event time, work = summed algorithmic FLOPs (or bytes for HBM
+ * classes), launches = count; then resets the class. */
+parl_status parl_ctx_profile_read(parl_ctx_t ctx, int kernel_class, double* ms, double* work, long* launches);
+
+/* ---- models: ModelParams (model.hpp:64-106) ---------------------------- */
+parl_status parl_model_create(parl_ctx_t ctx, const parl_config* cfg, parl_model_t* out);
+parl_status parl_model_destroy(parl_model_t m);
+/* Replaces ModelParams::flat() as the weight source: fp64 flat array in the
+ * reference layout (model.cpp:86-114).  `version` keys staleness. */
+parl_status parl_model_upload(parl_model_t m, const double* flat, size_t n, uint64_t version);
+/* ModelParams::init (model.cpp:142-164) bit-exact on the host, then upload. */
+parl_status parl_model_init(parl_model_t m, uint64_t seed);
+/* Device-side random init (Philox; same distribution, not the same stream)
+ * for the large configs whose fp64 host copy is impractical. */
+parl_status parl_model_init_device(parl_model_t m, uint64_t seed, double scale);
+/* dst <- src (+ scale * N(0,1) from seed when scale != 0): snapshot_old_policy,
+ * pipeline.cpp:20 / model copies for synthetic old/ref weights. */
+parl_status parl_model_copy(parl_model_t dst, parl_model_t src, uint64_t seed, double scale);
+/* Download weights into the reference fp64 layout (checkpoint path). */
+parl_status parl_model_download(parl_model_t m, double* flat, size_t n);
+size_t parl_param_count(const parl_config* cfg);
+uint64_t parl_model_version(parl_model_t m);
+
+/* ---- packing: pack_group (packing.cpp:7-45) + segments/predecessors
+ *      (model.cpp:230-253), K1 on the device ------------------------------ */
+parl_status parl_group_create(parl_ctx_t ctx, int max_tokens, int max_responses, parl_group_t* out);
+parl_status parl_group_destroy(parl_group_t g);
+/* Host inputs: prompt[P], responses concatenated in resp_flat with lengths
+ * resp_lens[G].  Same validation and errors as pack_group. */
+parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_t* resp_flat,
+                      const int32_t* resp_lens, int G, int max_seq_len);
+/* Device-resident inputs (same meaning; pointers are device pointers). */
+parl_status parl_pack_device(parl_group_t g, const int32_t* d_prompt, int P,
+                             const int32_t* d_resp_flat, const int32_t* resp_lens_host, int G,
+                             int max_seq_len);
+/* General forward_logprobs input (model.hpp:153-158): arbitrary tokens,
+ * positions and self-aligned labels (-1 = unscored) under a causal mask
+ * (prompt_len == 0) or a shared-prompt mask (prompt_len, resp_lens[G]).
+ * Validation order and errors follow validate_forward_inputs (model.cpp:404-426). */
+parl_status parl_set_sequence(parl_group_t g, const int32_t* tokens, const int32_t* positions,
+                              const int32_t* labels, int T, int prompt_len,
+                              const int32_t* resp_lens, int G, int vocab_size, int max_seq_len);
+/* Packed outputs back to the host (any pointer may be NULL). */
+parl_status parl_group_download(parl_group_t g, int32_t* tokens, int32_t* labels,
+                                int32_t* positions, int32_t* seg, int32_t* pred,
+                                int32_t* span_start, int32_t* scored_pos);
+int parl_group_tokens(parl_group_t g);
+int parl_group_scored(parl_group_t g);
+
+/* ---- forward: forward_logprobs (model.cpp:534-567), trimodel_forward
+ *      (pipeline.cpp:22-30) -------------------------------------------------
+ * slot: 0 = policy, 1 = old, 2 = reference.  Log-probs stay on the device in
+ * the group (slot-indexed) unless copied out with parl_group_logprobs. */
+parl_status parl_forward(parl_ctx_t ctx, parl_model_t m, parl_group_t g, int slot,
+                         parl_act_t* act_out /* NULL = no activation cache */);
+/* old == NULL: rollout_weights mode (pipeline.cpp:113-119); old log-probs
+ * come from parl_group_set_logprobs(slot 1). */
+parl_status parl_trimodel_forward(parl_ctx_t ctx, parl_model_t pol, parl_model_t old,
+                                  parl_model_t ref, parl_group_t g, parl_act_t* act_out);
+parl_status parl_group_logprobs(parl_group_t g, int slot, double* out /* [scored] */);
+parl_status parl_group_set_logprobs(parl_group_t g, int slot, const double* in);
+/* forward_logprob_rows (model.cpp:569-585): [T x V] log-softmax rows. */
+parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, double* rows);
+parl_status parl_act_destroy(parl_act_t a);
+
+/* ---- GRPO loss: group_advantages (grpo.cpp:24-48) + per_sample_terms
+ *      (grpo.cpp:111-151) over every response of the group --------------
+ * rewards[G] (host) -> advantages on the device, or advantages given
+ * directly (rewards == NULL).  Writes the backward seed upstream = -g
+ * (pipeline.cpp:138) into the group and ADDS this micro-batch's stats. */
+parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards,
+                           const double* advantages, const parl_hyper* hp,
+                           parl_loss_stats* stats_out /* NULL = keep on device */);
+parl_status parl_group_upstream(parl_group_t g, double* out);
+parl_status parl_group_set_upstream(parl_group_t g, const double* in);
+/* Device-side running stats (accumulated by parl_grpo_loss). */
+parl_status parl_stats_download(parl_ctx_t ctx, parl_loss_stats* out);
+parl_status parl_stats_reset(parl_ctx_t ctx);
+
+/* ---- backward: backward (model.cpp:587-838) + GradBuffer::accumulate
+ *      (model.cpp:189-194); uses the group's upstream seed --------------- */
+parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out);
+parl_status parl_grad_destroy(parl_grad_t gr);
+parl_status parl_grad_reset(parl_grad_t gr);
+parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl_group_t g,
+                          parl_grad_t gr);
+parl_status parl_grad_download(parl_grad_t gr, double* flat, size_t n);
+int parl_grad_micro_steps(parl_grad_t gr);
+
+/* ---- whole micro-step: Pipeline::train_microbatch shared-prompt branch
+ *      (pipeline.cpp:97-141) in one call ------------------------------------ */
+parl_status parl_train_microbatch(parl_ctx_t ctx, parl_model_t pol, parl_model_t old,
+                                  parl_model_t ref, parl_group_t g, const double* rewards,
+                                  const double* advantages, const parl_hyper* hp,
+                                  parl_grad_t gr, parl_loss_stats* stats_out);
+
+/* ---- apply_update (model.cpp:202-219) on the device: W -= lr*g/count,
+ *      refusing non-finite gradients/results (weights untouched). ---------- */
+parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr);
+
+/* ---- multi-GPU: data parallel over prompt groups (NCCL over NVLink) -------- */
+#define PARL_NCCL_ID_BYTES 128
+parl_status parl_comm_unique_id(char id[PARL_NCCL_ID_BYTES]);
+parl_status parl_comm_init(parl_ctx_t ctx, const char id[PARL_NCCL_ID_BYTES], int rank, int nranks);
+parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr);
+parl_status parl_stats_allreduce(parl_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARL_GPU_H */

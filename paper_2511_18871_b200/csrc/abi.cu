@@ -1,0 +1,1406 @@
+// C-ABI implementation: context, device-resident models, packed groups,
+// activation handles, gradient accumulators, and the orchestration of the
+// hot path (forward_logprobs / trimodel_forward / GRPO loss / backward /
+// accumulate) over the kernels in k_*.cu.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <type_traits>
+#include <vector>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace parl_gpu {
+uint64_t g_launches = 0;
+}
+
+using namespace parl_gpu;
+
+// ---------------------------------------------------------------------------
+// device memory: grow-only named buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            PARL_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t n) { return static_cast<T*>(get(std::max<size_t>(n, 1) * sizeof(T))); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    const char* (*getErrorString)(int) = nullptr;
+};
+
+struct parl_ctx_s {
+    int device = 0;
+    parl_precision prec = PARL_PREC_FP32;
+    cudaStream_t st = nullptr;
+    std::string err;
+    // forward/backward workspaces
+    DevBuf x0, x1, xmid, a, qkv, ctxo, bn, pre, actv, mean1, rstd1, mean2, rstd2, lse_attn;
+    DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head, part, target;
+    DevBuf dx, dx2, dx_act, dpre, dbn, dmid, dmid_act, dctx, dqkv, da, dsum, dhf, dxg, dz;
+    DevBuf stats, per_sample, staging, flags;
+    // kernel-class profiler (parl_ctx_profile)
+    struct ProfRec {
+        int cls;
+        cudaEvent_t a, b;
+        double work;
+    };
+    bool prof_on = false;
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[PARL_KC_COUNT] = {}, prof_work[PARL_KC_COUNT] = {};
+    long prof_n[PARL_KC_COUNT] = {};
+    cudaEvent_t ev() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            PARL_CUDA(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    void prof_collect() {
+        if (prof_pending.empty()) return;
+        PARL_CUDA(cudaStreamSynchronize(st));
+        for (auto& r : prof_pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            prof_ms[r.cls] += ms;
+            prof_work[r.cls] += r.work;
+            prof_n[r.cls] += 1;
+            ev_pool.push_back(r.a);
+            ev_pool.push_back(r.b);
+        }
+        prof_pending.clear();
+    }
+    // lifetime: objects created on this context keep it alive
+    int refs = 0;
+    bool closing = false;
+    // NCCL (data-parallel over prompt groups)
+    void* comm = nullptr;
+    int rank = 0, nranks = 1;
+};
+
+struct parl_model_s {
+    parl_ctx_s* ctx = nullptr;
+    parl_config cfg{};
+    FlatLayout L{};
+    ModelW W{};
+    std::vector<LayerW> layers;
+    DevBuf f32, act, master;
+    bool has_master = false;
+    uint64_t version = 0, forward_gen = 0;
+};
+
+struct parl_group_s {
+    parl_ctx_s* ctx = nullptr;
+    int max_T = 0, max_G = 0;
+    int T = 0, P = 0, G = 0, S = 0, n_samples = 0;
+    int Peff = 0;  // end of segment 0 (prompt, or the whole causal sequence)
+    double pairs = 0;  // allowed attention pairs (algorithmic attention work)
+    uint64_t epoch = 0;
+    PackedDev pk{};
+    DevBuf ints, seg_se, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
+    DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp;
+    uint64_t sorted_epoch = ~0ull;
+    std::vector<int> lens, span_start, cu;
+    int max_seq = 0, vocab = 0;
+};
+
+struct parl_act_s {
+    parl_model_s* owner = nullptr;
+    parl_group_s* group = nullptr;
+    uint64_t version = 0, gen = 0, epoch = 0;
+    int T = 0, S = 0;
+    DevBuf xs, xmid, a, qkv, ctxo, bn, pre, actv, stats, lse_attn;  // per-layer stacks
+    DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
+};
+
+struct parl_grad_s {
+    parl_ctx_s* ctx = nullptr;
+    parl_config cfg{};
+    FlatLayout L{};
+    DevBuf g;
+    int micro_steps = 0;
+};
+
+static void ctx_release(parl_ctx_s* ctx) {
+    if (--ctx->refs > 0 || !ctx->closing) return;
+    cudaStreamSynchronize(ctx->st);
+    cudaStreamDestroy(ctx->st);
+    delete ctx;
+}
+
+// RAII: bracket the launches of one kernel class with events when profiling.
+struct ProfScope {
+    parl_ctx_s* c;
+    int cls;
+    double work;
+    cudaEvent_t a = nullptr;
+    ProfScope(parl_ctx_s* c_, int cls_, double work_) : c(c_), cls(cls_), work(work_) {
+        if (c->prof_on) {
+            a = c->ev();
+            cudaEventRecord(a, c->st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = c->ev();
+            cudaEventRecord(b, c->st);
+            c->prof_pending.push_back({cls, a, b, work});
+            if (c->prof_pending.size() > 4096) c->prof_collect();
+        }
+    }
+};
+
+namespace {
+
+thread_local std::string tl_err;
+
+template <class F>
+parl_status guarded(parl_ctx_s* c, F&& f) {
+    try {
+        f();
+        return PARL_OK;
+    } catch (const Error& e) {
+        if (c) c->err = e.msg;
+        tl_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (c) c->err = e.what();
+        tl_err = e.what();
+        return PARL_E_CUDA;
+    }
+}
+
+void check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error{PARL_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+void validate_config(const parl_config& c) {  // ModelConfig::validate, model.cpp:19-31
+    if (c.vocab_size < 4)
+        throw Error{PARL_E_CONFIG, "vocab_size must be >= 4 (ids 0..3 are reserved), got " + std::to_string(c.vocab_size)};
+    if (c.d_model <= 0) throw Error{PARL_E_CONFIG, "d_model must be positive"};
+    if (c.n_layers <= 0) throw Error{PARL_E_CONFIG, "n_layers must be positive"};
+    if (c.n_heads <= 0) throw Error{PARL_E_CONFIG, "n_heads must be positive"};
+    if (c.d_ff <= 0) throw Error{PARL_E_CONFIG, "d_ff must be positive"};
+    if (c.max_seq_len <= 0) throw Error{PARL_E_CONFIG, "max_seq_len must be positive"};
+    if (c.d_model % c.n_heads != 0)
+        throw Error{PARL_E_CONFIG, "d_model (" + std::to_string(c.d_model) + ") not divisible by n_heads (" +
+                                       std::to_string(c.n_heads) + ")"};
+    if (c.d_model / c.n_heads > 128) throw Error{PARL_E_CONFIG, "head dim > 128 not supported by the device path"};
+}
+
+bool same_cfg(const parl_config& a, const parl_config& b) { return std::memcmp(&a, &b, sizeof(a)) == 0; }
+
+size_t act_size(parl_precision p) { return p == PARL_PREC_BF16 ? 2 : 4; }
+
+// One weight tensor's place in the compute copy.
+struct TensorMap {
+    size_t src_off;  // offset in the reference flat layout
+    int rows, cols;  // reference shape
+    bool matrix;     // act dtype, stored transposed ([cols x rows])
+    void* dst;       // f32 (vector/embedding) or act-dtype destination
+    long ldd;
+    int kind;        // 0 normal(0.08), 1 ones, 2 zeros  (model.cpp:152-162)
+};
+
+std::vector<TensorMap> tensor_maps(parl_model_s* m) {
+    const auto& c = m->cfg;
+    const int d = c.d_model, F = c.d_ff, V = c.vocab_size;
+    std::vector<TensorMap> v;
+    const size_t es = act_size(m->ctx->prec);
+    auto actp = [&](void* base, size_t elems) { return static_cast<char*>(base) + elems * es; };
+    v.push_back({m->L.tok_emb, V, d, false, m->W.tok_emb, d, 0});
+    v.push_back({m->L.pos_emb, c.max_seq_len, d, false, m->W.pos_emb, d, 0});
+    for (int l = 0; l < c.n_layers; ++l) {
+        auto o = m->L.layer(l, d, F);
+        LayerW& w = m->layers[l];
+        v.push_back({o.ln1g, 1, d, false, w.ln1_g, d, 1});
+        v.push_back({o.ln1b, 1, d, false, w.ln1_b, d, 2});
+        v.push_back({o.wq, d, d, true, actp(w.wqkv_t, 0), d, 0});
+        v.push_back({o.bq, 1, d, false, w.bqkv, d, 2});
+        v.push_back({o.wk, d, d, true, actp(w.wqkv_t, (size_t)d * d), d, 0});
+        v.push_back({o.bk, 1, d, false, w.bqkv + d, d, 2});
+        v.push_back({o.wv, d, d, true, actp(w.wqkv_t, (size_t)2 * d * d), d, 0});
+        v.push_back({o.bv, 1, d, false, w.bqkv + 2 * d, d, 2});
+        v.push_back({o.wo, d, d, true, w.wo_t, d, 0});
+        v.push_back({o.bo, 1, d, false, w.bo, d, 2});
+        v.push_back({o.ln2g, 1, d, false, w.ln2_g, d, 1});
+        v.push_back({o.ln2b, 1, d, false, w.ln2_b, d, 2});
+        v.push_back({o.w1, d, F, true, w.w1_t, d, 0});
+        v.push_back({o.b1, 1, F, false, w.b1, F, 2});
+        v.push_back({o.w2, F, d, true, w.w2_t, F, 0});
+        v.push_back({o.b2, 1, d, false, w.b2, d, 2});
+    }
+    v.push_back({m->L.lnf_g, 1, d, false, m->W.lnf_g, d, 1});
+    v.push_back({m->L.lnf_b, 1, d, false, m->W.lnf_b, d, 2});
+    v.push_back({m->L.head_w, d, V, true, m->W.head_w_t, d, 0});
+    v.push_back({m->L.head_b, 1, V, false, m->W.head_b, V, 2});
+    return v;
+}
+
+void convert_tensor(parl_model_s* m, const TensorMap& t, const double* dsrc) {
+    cudaStream_t st = m->ctx->st;
+    if (!t.matrix) {
+        launch_convert_w<float>(dsrc, t.rows, t.cols, static_cast<float*>(t.dst), t.cols, 0, st);
+    } else if (m->ctx->prec == PARL_PREC_BF16) {
+        launch_convert_w<bf16>(dsrc, t.rows, t.cols, static_cast<bf16*>(t.dst), t.ldd, 1, st);
+    } else {
+        launch_convert_w<float>(dsrc, t.rows, t.cols, static_cast<float*>(t.dst), t.ldd, 1, st);
+    }
+}
+
+// Rebuild the compute copy from the device fp64 master.
+void convert_from_master(parl_model_s* m) {
+    const double* base = static_cast<const double*>(m->master.p);
+    for (const auto& t : tensor_maps(m)) convert_tensor(m, t, base + t.src_off);
+    check_launch();
+}
+
+template <class T>
+void gemm(parl_ctx_s* c, const GemmArgs& g, int cls = PARL_KC_GEMM) {
+    ProfScope ps(c, cls, 2.0 * g.M * (double)g.N * g.K);
+    if constexpr (std::is_same_v<T, bf16>) {
+        if (gemm_tc(g, c->st)) return;
+    }
+    gemm_simt<T>(g, c->st);
+}
+
+GemmArgs mk(int M, int N, int K, const void* A, long sam, long sak, const void* B, long sbn, long sbk) {
+    GemmArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.sam = sam; g.sak = sak;
+    g.B = B; g.sbn = sbn; g.sbk = sbk;
+    return g;
+}
+
+void ensure_sorted(parl_group_s* g) {
+    if (g->sorted_epoch == g->epoch) return;
+    cudaStream_t st = g->ctx->st;
+    const int T = g->T;
+    int32_t* iota = g->iota.as<int32_t>(T);
+    launch_iota(iota, T, st);
+    const size_t tb = sort_temp_bytes(T);
+    void* tmp = g->sort_tmp.get(std::max<size_t>(tb, 16));
+    auto bits = [](int n) {
+        int b = 1;
+        while ((1L << b) < n) ++b;
+        return b;
+    };
+    launch_sort_pairs(tmp, tb, g->pk.tokens, g->tok_keys.as<int32_t>(T), iota, g->tok_idx.as<int32_t>(T), T,
+                      bits(g->vocab), st);
+    launch_sort_pairs(tmp, tb, g->pk.positions, g->pos_keys.as<int32_t>(T), iota, g->pos_idx.as<int32_t>(T), T,
+                      bits(g->max_seq), st);
+    g->sorted_epoch = g->epoch;
+}
+
+// ---------------------------------------------------------------------------
+// forward (forward_logprobs, model.cpp:534-567; run_forward 430-521)
+template <class T>
+void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, parl_act_s* act) {
+    cudaStream_t st = c->st;
+    const auto& cf = m->cfg;
+    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
+    const int NL = cf.n_layers;
+    const size_t TD = (size_t)Tn * D, TF = (size_t)Tn * F;
+
+    float* xs;   // residual stream stack: layer inputs x_0..x_L
+    float* xmid; // per-layer x_mid
+    T *a, *qkv, *ctxo, *bn, *pre, *actv;
+    float *stats, *lse_attn;
+    if (act) {
+        xs = act->xs.as<float>(TD * (NL + 1));
+        xmid = act->xmid.as<float>(TD * NL);
+        a = act->a.as<T>(TD * NL);
+        qkv = act->qkv.as<T>(3 * TD * NL);
+        ctxo = act->ctxo.as<T>(TD * NL);
+        bn = act->bn.as<T>(TD * NL);
+        pre = act->pre.as<T>(TF * NL);
+        actv = act->actv.as<T>(TF * NL);
+        stats = act->stats.as<float>((size_t)4 * Tn * NL);
+        lse_attn = act->lse_attn.as<float>((size_t)H * Tn * NL);
+    } else {
+        xs = c->x0.as<float>(TD * 2);
+        xmid = c->xmid.as<float>(TD);
+        a = c->a.as<T>(TD);
+        qkv = c->qkv.as<T>(3 * TD);
+        ctxo = c->ctxo.as<T>(TD);
+        bn = c->bn.as<T>(TD);
+        pre = c->pre.as<T>(TF);
+        actv = c->actv.as<T>(TF);
+        stats = c->mean1.as<float>((size_t)4 * Tn);
+        lse_attn = c->lse_attn.as<float>((size_t)H * Tn);
+    }
+    auto lay = [&](size_t per, int l) { return act ? per * (size_t)l : 0; };
+    auto xin_of = [&](int l) { return xs + (act ? TD * l : TD * (l & 1)); };
+
+    AttnArgs aa;
+    aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
+    aa.seg = g->pk.seg;
+    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
+    aa.seg_end = aa.seg_start + (g->max_G + 1);
+    aa.scale = 1.0f / std::sqrt((float)Dh);
+
+    launch_embed(m->W.tok_emb, m->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(0), st);
+    for (int l = 0; l < NL; ++l) {
+        const LayerW& w = m->layers[l];
+        float* xin = xin_of(l);
+        float* xout = xin_of(l + 1);
+        float* xm = xmid + lay(TD, l);
+        T* al = a + lay(TD, l);
+        T* ql = qkv + lay(3 * TD, l);
+        T* cl = ctxo + lay(TD, l);
+        T* bl = bn + lay(TD, l);
+        T* pl = pre + lay(TF, l);
+        T* vl = actv + lay(TF, l);
+        float* st4 = stats + lay((size_t)4 * Tn, l);
+        float* la = lse_attn + lay((size_t)H * Tn, l);
+
+        launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, st4, st4 + Tn, st);
+        {  // fused Q|K|V projection (model.cpp:464-466)
+            GemmArgs ga = mk(Tn, 3 * D, D, al, D, 1, w.wqkv_t, D, 1);
+            ga.epi = EPI_ACT; ga.bias = w.bqkv; ga.Ca = ql; ga.ldca = 3 * D;
+            gemm<T>(c, ga);
+        }
+        {
+            ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D);
+            launch_attn_fwd<T>(aa, ql, cl, la, st);
+        }
+        {  // O projection + residual (model.cpp:504-506)
+            GemmArgs ga = mk(Tn, D, D, cl, D, 1, w.wo_t, D, 1);
+            ga.epi = EPI_RESID; ga.bias = w.bo; ga.resid = xin; ga.Cf = xm; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, st4 + 2 * Tn, st4 + 3 * Tn, st);
+        {  // W1 + bias + GELU (model.cpp:509-511)
+            GemmArgs ga = mk(Tn, F, D, bl, D, 1, w.w1_t, D, 1);
+            ga.epi = EPI_GELU; ga.bias = w.b1; ga.Ca = pl; ga.Caux = vl; ga.ldca = F;
+            gemm<T>(c, ga);
+        }
+        {  // W2 + bias + residual (model.cpp:513-515)
+            GemmArgs ga = mk(Tn, D, F, vl, F, 1, w.w2_t, F, 1);
+            ga.epi = EPI_RESID; ga.bias = w.b2; ga.resid = xm; ga.Cf = xout; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+    }
+    float* xfin = xin_of(NL);
+    // final LN + head only on the scored tokens' predecessor rows (model.cpp:518-556)
+    T* hf = act ? act->hf.as<T>((size_t)S * D) : c->hf.as<T>((size_t)S * D);
+    float* lnf_mean = act ? act->lnf_mean.as<float>(S) : c->lnf_mean.as<float>(S);
+    float* lnf_rstd = act ? act->lnf_rstd.as<float>(S) : c->lnf_rstd.as<float>(S);
+    float* lse_head = act ? act->lse_head.as<float>(S) : c->lse_head.as<float>(S);
+    float* logits = act ? act->logits.as<float>((size_t)S * V) : c->logits.as<float>((size_t)S * V);
+    float* lp = static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T;
+    if (S > 0) {
+        launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, lnf_mean, lnf_rstd, st);
+        GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
+        ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
+        gemm<T>(c, ga, PARL_KC_HEAD);
+        launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
+    }
+    check_launch();
+}
+
+// backward (model.cpp:587-838) + GradBuffer::accumulate (model.cpp:189-194)
+template <class T>
+void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s* g, parl_grad_s* gr) {
+    cudaStream_t st = c->st;
+    const auto& cf = m->cfg;
+    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
+    const int NL = cf.n_layers;
+    const size_t TD = (size_t)Tn * D, TF = (size_t)Tn * F;
+    float* G = static_cast<float*>(gr->g.p);
+    const FlatLayout& L = gr->L;
+    const float* u = static_cast<const float*>(g->upstream.p);
+
+    float* dx = c->dx.as<float>(TD);
+    if (S > 0) {
+        // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
+        float* logits = static_cast<float*>(act->logits.p);
+        T* dz = c->dz.as<T>((size_t)S * V);
+        launch_softmax_bwd<float, T>(logits, V, dz, V, S, V, static_cast<float*>(act->lse_head.p), u,
+                                     g->pk.scored_label, st);
+        launch_colsum<T>(dz, V, S, V, G + L.head_b, st);
+        T* hf = static_cast<T*>(act->hf.p);
+        float* dhf = c->dhf.as<float>((size_t)S * D);
+        {  // dH = dZ W_head^T (model.cpp:654-666)
+            GemmArgs ga = mk(S, D, V, dz, V, 1, m->W.head_w_t, 1, D);
+            ga.epi = EPI_F32; ga.Cf = dhf; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        {  // dW_head += H^T dZ
+            GemmArgs ga = mk(D, V, S, hf, 1, D, dz, 1, V);
+            ga.epi = EPI_F32_ACC; ga.Cf = G + L.head_w; ga.ldc = V;
+            gemm<T>(c, ga);
+        }
+        // final LN backward on the gathered rows, then scatter to positions
+        float* dxg = c->dxg.as<float>((size_t)S * D);
+        float* xfin = static_cast<float*>(act->xs.p) + TD * NL;
+        launch_layernorm_bwd(dhf, xfin, g->pk.pred_pos, static_cast<float*>(act->lnf_mean.p),
+                             static_cast<float*>(act->lnf_rstd.p), m->W.lnf_g, S, D, nullptr, dxg, G + L.lnf_g,
+                             G + L.lnf_b, st);
+        launch_scatter_rows(dxg, g->pk.row_ptr, g->pk.row_idx, Tn, D, dx, st);
+    } else {
+        PARL_CUDA(cudaMemsetAsync(dx, 0, TD * sizeof(float), st));
+    }
+
+    T* dx_act = c->dx_act.as<T>(TD);
+    T* dpre = c->dpre.as<T>(TF);
+    float* dbn = c->dbn.as<float>(TD);
+    float* dmid = c->dmid.as<float>(TD);
+    T* dmid_act = c->dmid_act.as<T>(TD);
+    T* dctx = c->dctx.as<T>(TD);
+    T* dqkv = c->dqkv.as<T>(3 * TD);
+    float* da = c->da.as<float>(TD);
+    float* dsum = c->dsum.as<float>((size_t)H * Tn);
+    float* dx2 = c->dx2.as<float>(TD);
+
+    AttnArgs aa;
+    aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
+    aa.seg = g->pk.seg;
+    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
+    aa.seg_end = aa.seg_start + (g->max_G + 1);
+    aa.scale = 1.0f / std::sqrt((float)Dh);
+
+    for (int l = NL - 1; l >= 0; --l) {
+        const LayerW& w = m->layers[l];
+        const auto o = L.layer(l, D, F);
+        float* xin = static_cast<float*>(act->xs.p) + TD * l;
+        float* xm = static_cast<float*>(act->xmid.p) + TD * l;
+        T* al = static_cast<T*>(act->a.p) + TD * l;
+        T* ql = static_cast<T*>(act->qkv.p) + 3 * TD * l;
+        T* cl = static_cast<T*>(act->ctxo.p) + TD * l;
+        T* bl = static_cast<T*>(act->bn.p) + TD * l;
+        T* pl = static_cast<T*>(act->pre.p) + TF * l;
+        T* vl = static_cast<T*>(act->actv.p) + TF * l;
+        float* st4 = static_cast<float*>(act->stats.p) + (size_t)4 * Tn * l;
+        float* la = static_cast<float*>(act->lse_attn.p) + (size_t)H * Tn * l;
+
+        // FFN (model.cpp:688-727)
+        launch_f32_to_act<T>(dx, dx_act, TD, st);
+        {
+            GemmArgs ga = mk(Tn, F, D, dx_act, D, 1, w.w2_t, 1, F);
+            ga.epi = EPI_GELU_BWD; ga.aux_in = pl; ga.Ca = dpre; ga.ldca = F;
+            gemm<T>(c, ga);
+        }
+        {
+            GemmArgs ga = mk(F, D, Tn, vl, 1, F, dx_act, 1, D);
+            ga.epi = EPI_F32_ACC; ga.Cf = G + o.w2; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        launch_colsum<float>(dx, D, Tn, D, G + o.b2, st);
+        {
+            GemmArgs ga = mk(Tn, D, F, dpre, F, 1, w.w1_t, 1, D);
+            ga.epi = EPI_F32; ga.Cf = dbn; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        {
+            GemmArgs ga = mk(D, F, Tn, bl, 1, D, dpre, 1, F);
+            ga.epi = EPI_F32_ACC; ga.Cf = G + o.w1; ga.ldc = F;
+            gemm<T>(c, ga);
+        }
+        launch_colsum<T>(dpre, F, Tn, F, G + o.b1, st);
+        // LN2 (model.cpp:729-730)
+        launch_layernorm_bwd(dbn, xm, nullptr, st4 + 2 * Tn, st4 + 3 * Tn, w.ln2_g, Tn, D, dx, dmid, G + o.ln2g,
+                             G + o.ln2b, st);
+        // O projection (model.cpp:733-749)
+        launch_f32_to_act<T>(dmid, dmid_act, TD, st);
+        {
+            GemmArgs ga = mk(Tn, D, D, dmid_act, D, 1, w.wo_t, 1, D);
+            ga.epi = EPI_ACT; ga.Ca = dctx; ga.ldca = D;
+            gemm<T>(c, ga);
+        }
+        {
+            GemmArgs ga = mk(D, D, Tn, cl, 1, D, dmid_act, 1, D);
+            ga.epi = EPI_F32_ACC; ga.Cf = G + o.wo; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        launch_colsum<float>(dmid, D, Tn, D, G + o.bo, st);
+        // attention (model.cpp:752-786)
+        {
+            ProfScope ps(c, PARL_KC_ATTN_BWD, 10.0 * g->pairs * D);
+            launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
+        }
+        // Q/K/V projections (model.cpp:789-817)
+        {
+            GemmArgs ga = mk(Tn, D, 3 * D, dqkv, 3 * D, 1, w.wqkv_t, 1, D);
+            ga.epi = EPI_F32; ga.Cf = da; ga.ldc = D;
+            gemm<T>(c, ga);
+        }
+        const size_t woff[3] = {o.wq, o.wk, o.wv}, boff[3] = {o.bq, o.bk, o.bv};
+        for (int p = 0; p < 3; ++p) {
+            GemmArgs ga = mk(D, D, Tn, al, 1, D, dqkv + (size_t)p * D, 1, 3 * D);
+            ga.epi = EPI_F32_ACC; ga.Cf = G + woff[p]; ga.ldc = D;
+            gemm<T>(c, ga);
+            launch_colsum<T>(dqkv + (size_t)p * D, 3 * D, Tn, D, G + boff[p], st);
+        }
+        // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da)
+        launch_layernorm_bwd(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, G + o.ln1g, G + o.ln1b, st);
+        std::swap(dx, dx2);
+    }
+    // embeddings (model.cpp:826-834), deterministic segmented sums
+    ensure_sorted(g);
+    launch_embed_grad(static_cast<int32_t*>(g->tok_keys.p), static_cast<int32_t*>(g->tok_idx.p), Tn, dx, D,
+                      G + L.tok_emb, st);
+    launch_embed_grad(static_cast<int32_t*>(g->pos_keys.p), static_cast<int32_t*>(g->pos_idx.p), Tn, dx, D,
+                      G + L.pos_emb, st);
+    check_launch();
+    gr->micro_steps += 1;
+}
+
+void alloc_group_arrays(parl_group_s* g) {
+    const int T = g->max_T, G = g->max_G;
+    // tokens labels positions seg pred [T] ; scored_pos scored_label pred_pos sample_of [T];
+    // row_ptr [T+1]; row_idx [T]
+    int32_t* base = g->ints.as<int32_t>((size_t)T * 10 + 1);
+    g->pk.tokens = base;
+    g->pk.labels = base + T;
+    g->pk.positions = base + 2 * (size_t)T;
+    g->pk.seg = base + 3 * (size_t)T;
+    g->pk.pred = base + 4 * (size_t)T;
+    g->pk.scored_pos = base + 5 * (size_t)T;
+    g->pk.scored_label = base + 6 * (size_t)T;
+    g->pk.pred_pos = base + 7 * (size_t)T;
+    g->pk.sample_of = base + 8 * (size_t)T;
+    g->pk.row_idx = base + 9 * (size_t)T;
+    g->seg_se.as<int32_t>(2 * (size_t)(G + 1));               // segment [start, end) bounds
+    g->pk.row_ptr = g->cu_d.as<int32_t>((size_t)T + 1 + (G + 1));  // row_ptr [T+1] | cu [G+1]
+    g->lp.as<float>((size_t)3 * T);
+    g->upstream.as<float>(T);
+    g->rewards.as<double>(G);
+    g->adv.as<double>(G);
+}
+
+int32_t* group_cu(parl_group_s* g) { return static_cast<int32_t*>(g->cu_d.p) + g->max_T + 1; }
+
+// upload segment bounds / response offsets computed on the host
+void upload_meta(parl_group_s* g) {
+    std::vector<int32_t> se(2 * (size_t)(g->max_G + 1), 0);
+    se[0] = 0;
+    se[g->max_G + 1] = g->Peff;
+    for (int k = 0; k < g->G; ++k) {
+        se[k + 1] = g->span_start[k];
+        se[g->max_G + 1 + k + 1] = g->span_start[k] + g->lens[k];
+    }
+    PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
+    PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
+}
+
+void check_pack_inputs(parl_group_s* g, int P, const int32_t* lens, int G, int max_seq) {
+    if (P < 1) throw Error{PARL_E_SHAPE, "pack_group: empty prompt"};          // packing.cpp:9
+    if (G < 1) throw Error{PARL_E_SHAPE, "pack_group: no responses"};          // packing.cpp:10
+    long total = P;
+    for (int k = 0; k < G; ++k) {
+        if (lens[k] < 1) throw Error{PARL_E_SHAPE, "pack_group: empty response"};
+        total += lens[k];
+    }
+    if (total > max_seq)                                                         // packing.cpp:16-19
+        throw Error{PARL_E_SHAPE, "pack_group: packed length " + std::to_string(total) + " for group of " +
+                                      std::to_string(G) + " responses exceeds max_seq_len " + std::to_string(max_seq)};
+    if (total > g->max_T || G > g->max_G)
+        throw Error{PARL_E_SHAPE, "packed group exceeds the capacity this group was created with"};
+}
+
+void set_pack_meta(parl_group_s* g, int P, const int32_t* lens, int G, int max_seq) {
+    g->P = P;
+    g->G = G;
+    g->n_samples = G;
+    g->lens.assign(lens, lens + G);
+    g->span_start.resize(G);
+    g->cu.assign(G + 1, 0);
+    int t = P;
+    for (int k = 0; k < G; ++k) {
+        g->span_start[k] = t;
+        g->cu[k + 1] = g->cu[k] + lens[k];
+        t += lens[k];
+    }
+    g->T = t;
+    g->S = t - P;
+    g->Peff = P;
+    g->pairs = 0.5 * P * (P + 1.0);
+    for (int k = 0; k < G; ++k) g->pairs += (double)lens[k] * P + 0.5 * lens[k] * (lens[k] + 1.0);
+    g->max_seq = max_seq;
+    g->epoch++;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* parl_version(void) { return "parl_gpu 0.1 (sm_100a)"; }
+
+const char* parl_last_error(parl_ctx_t ctx) { return ctx ? ctx->err.c_str() : tl_err.c_str(); }
+
+parl_status parl_ctx_create(int device, parl_precision prec, parl_ctx_t* out) {
+    return guarded(nullptr, [&] {
+        auto c = std::make_unique<parl_ctx_s>();
+        c->device = device;
+        c->prec = prec;
+        PARL_CUDA(cudaSetDevice(device));
+        PARL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        double* s = c->stats.as<double>(8);
+        PARL_CUDA(cudaMemsetAsync(s, 0, 8 * sizeof(double), c->st));
+        *out = c.release();
+    });
+}
+
+
+parl_status parl_ctx_destroy(parl_ctx_t ctx) {
+    if (!ctx) return PARL_OK;
+    ctx->closing = true;
+    ctx->refs++;
+    ctx_release(ctx);
+    return PARL_OK;
+}
+
+parl_status parl_ctx_sync(parl_ctx_t ctx) {
+    return guarded(ctx, [&] { PARL_CUDA(cudaStreamSynchronize(ctx->st)); });
+}
+
+void* parl_ctx_stream(parl_ctx_t ctx) { return ctx ? (void*)ctx->st : nullptr; }
+
+parl_status parl_ctx_profile(parl_ctx_t ctx, int enable) {
+    return guarded(ctx, [&] {
+        ctx->prof_collect();
+        ctx->prof_on = enable != 0;
+    });
+}
+
+parl_status parl_ctx_profile_read(parl_ctx_t ctx, int cls, double* ms, double* work, long* n) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(cls >= 0 && cls < PARL_KC_COUNT, PARL_E_CONFIG, "unknown kernel class");
+        ctx->prof_collect();
+        if (ms) *ms = ctx->prof_ms[cls];
+        if (work) *work = ctx->prof_work[cls];
+        if (n) *n = ctx->prof_n[cls];
+        ctx->prof_ms[cls] = ctx->prof_work[cls] = 0;
+        ctx->prof_n[cls] = 0;
+    });
+}
+uint64_t parl_ctx_launches(parl_ctx_t) { return g_launches; }
+
+size_t parl_param_count(const parl_config* cfg) { return make_layout(*cfg).total; }
+
+parl_status parl_model_create(parl_ctx_t ctx, const parl_config* cfg, parl_model_t* out) {
+    return guarded(ctx, [&] {
+        validate_config(*cfg);
+        auto m = std::make_unique<parl_model_s>();
+        m->ctx = ctx;
+        ctx->refs++;
+        m->cfg = *cfg;
+        m->L = make_layout(*cfg);
+        const size_t d = cfg->d_model, F = cfg->d_ff, V = cfg->vocab_size, NL = cfg->n_layers;
+        const size_t n32 = V * d + (size_t)cfg->max_seq_len * d + NL * (4 * d + 3 * d + d + F + d) + 2 * d + V;
+        const size_t nact = NL * (3 * d * d + d * d + F * d + d * F) + V * d;
+        float* f = m->f32.as<float>(n32);
+        char* a = static_cast<char*>(m->act.get(std::max<size_t>(nact, 1) * act_size(ctx->prec)));
+        const size_t es = act_size(ctx->prec);
+        auto takef = [&](size_t n) { float* p = f; f += n; return p; };
+        auto takea = [&](size_t n) { void* p = a; a += n * es; return p; };
+        m->W.tok_emb = takef(V * d);
+        m->W.pos_emb = takef((size_t)cfg->max_seq_len * d);
+        m->layers.resize(NL);
+        for (auto& w : m->layers) {
+            w.ln1_g = takef(d); w.ln1_b = takef(d); w.ln2_g = takef(d); w.ln2_b = takef(d);
+            w.bqkv = takef(3 * d); w.bo = takef(d); w.b1 = takef(F); w.b2 = takef(d);
+            w.wqkv_t = takea(3 * d * d); w.wo_t = takea(d * d); w.w1_t = takea(F * d); w.w2_t = takea(d * F);
+        }
+        m->W.lnf_g = takef(d);
+        m->W.lnf_b = takef(d);
+        m->W.head_b = takef(V);
+        m->W.head_w_t = takea(V * d);
+        m->W.layers = m->layers.data();
+        // fp64 master copy (apply_update / snapshots) when it fits comfortably
+        m->has_master = m->L.total * sizeof(double) <= (size_t)24 << 30;
+        if (m->has_master) m->master.as<double>(m->L.total);
+        *out = m.release();
+    });
+}
+
+parl_status parl_model_destroy(parl_model_t m) {
+    if (m) {
+        parl_ctx_s* c = m->ctx;
+        cudaStreamSynchronize(c->st);
+        delete m;
+        ctx_release(c);
+    }
+    return PARL_OK;
+}
+
+uint64_t parl_model_version(parl_model_t m) { return m->version; }
+
+parl_status parl_model_upload(parl_model_t m, const double* flat, size_t n, uint64_t version) {
+    return guarded(m->ctx, [&] {
+        PARL_REQUIRE(n == m->L.total, PARL_E_SHAPE, "weight array size does not match the model layout");
+        cudaStream_t st = m->ctx->st;
+        if (m->has_master) {
+            PARL_CUDA(cudaMemcpyAsync(m->master.p, flat, n * sizeof(double), cudaMemcpyHostToDevice, st));
+            convert_from_master(m);
+        } else {
+            for (const auto& t : tensor_maps(m)) {
+                const size_t cnt = (size_t)t.rows * t.cols;
+                double* stg = m->ctx->staging.as<double>(cnt);
+                PARL_CUDA(cudaMemcpyAsync(stg, flat + t.src_off, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+                convert_tensor(m, t, stg);
+            }
+        }
+        PARL_CUDA(cudaStreamSynchronize(st));
+        m->version = version;
+    });
+}
+
+parl_status parl_model_init(parl_model_t m, uint64_t seed) {
+    // ModelParams::init (model.cpp:142-164) with the reference RNG
+    // (rng.hpp: splitmix64-whitened std::mt19937_64, Box-Muller normals).
+    std::vector<double> w;
+    parl_status s = guarded(m->ctx, [&] {
+        auto sm64 = [](uint64_t x) {
+            x += 0x9e3779b97f4a7c15ull;
+            x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+            x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+            return x ^ (x >> 31);
+        };
+        const uint64_t mixed = sm64(sm64(seed) ^ (0x9e3779b97f4a7c15ull + 0x6d6f64656cull));
+        std::mt19937_64 eng(sm64(mixed));
+        bool has_spare = false;
+        double spare = 0.0;
+        auto normal = [&]() {
+            if (has_spare) {
+                has_spare = false;
+                return spare;
+            }
+            const double u1 = 1.0 - (double)(eng() >> 11) * 0x1.0p-53;
+            const double u2 = (double)(eng() >> 11) * 0x1.0p-53;
+            const double r = std::sqrt(-2.0 * std::log(u1)), a = 6.283185307179586476925286766559 * u2;
+            spare = r * std::sin(a);
+            has_spare = true;
+            return r * std::cos(a);
+        };
+        w.assign(m->L.total, 0.0);
+        for (const auto& t : tensor_maps(m)) {
+            double* dst = w.data() + t.src_off;
+            const size_t cnt = (size_t)t.rows * t.cols;
+            if (t.kind == 1) std::fill(dst, dst + cnt, 1.0);
+            else if (t.kind == 0)
+                for (size_t i = 0; i < cnt; ++i) dst[i] = 0.08 * normal();
+        }
+    });
+    if (s != PARL_OK) return s;
+    // tensor_maps lists tensors in layout order, so draws follow model.cpp:153-162
+    return parl_model_upload(m, w.data(), w.size(), 0);
+}
+
+parl_status parl_model_init_device(parl_model_t m, uint64_t seed, double scale) {
+    return guarded(m->ctx, [&] {
+        cudaStream_t st = m->ctx->st;
+        uint32_t stream = 0;
+        for (const auto& t : tensor_maps(m)) {
+            const size_t cnt = (size_t)t.rows * t.cols;
+            double* dst = m->has_master ? static_cast<double*>(m->master.p) + t.src_off
+                                        : m->ctx->staging.as<double>(cnt);
+            if (t.kind == 0) launch_randn(dst, (long)cnt, seed, stream++, scale, nullptr, st);
+            else launch_fill_f64(dst, (long)cnt, t.kind == 1 ? 1.0 : 0.0, st);
+            if (!m->has_master) convert_tensor(m, t, dst);
+        }
+        if (m->has_master) convert_from_master(m);
+        check_launch();
+        PARL_CUDA(cudaStreamSynchronize(st));
+        m->version = 0;
+    });
+}
+
+parl_status parl_model_copy(parl_model_t dst, parl_model_t src, uint64_t seed, double scale) {
+    return guarded(dst->ctx, [&] {
+        PARL_REQUIRE(same_cfg(dst->cfg, src->cfg), PARL_E_SHAPE, "model copy between different configs");
+        cudaStream_t st = dst->ctx->st;
+        if (src->has_master && dst->has_master) {
+            if (scale != 0.0)
+                launch_randn(static_cast<double*>(dst->master.p), (long)dst->L.total, seed, 0xC0FFEEu, scale,
+                             static_cast<const double*>(src->master.p), st);
+            else
+                PARL_CUDA(cudaMemcpyAsync(dst->master.p, src->master.p, dst->L.total * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, st));
+            convert_from_master(dst);
+        } else {
+            PARL_REQUIRE(scale == 0.0, PARL_E_CONFIG, "perturbed copy needs an fp64 master copy");
+            PARL_CUDA(cudaMemcpyAsync(dst->f32.p, src->f32.p, src->f32.bytes, cudaMemcpyDeviceToDevice, st));
+            PARL_CUDA(cudaMemcpyAsync(dst->act.p, src->act.p, src->act.bytes, cudaMemcpyDeviceToDevice, st));
+        }
+        PARL_CUDA(cudaStreamSynchronize(st));
+        dst->version = src->version;
+    });
+}
+
+parl_status parl_model_download(parl_model_t m, double* flat, size_t n) {
+    return guarded(m->ctx, [&] {
+        PARL_REQUIRE(n == m->L.total, PARL_E_SHAPE, "weight array size does not match the model layout");
+        cudaStream_t st = m->ctx->st;
+        if (m->has_master) {
+            PARL_CUDA(cudaMemcpyAsync(flat, m->master.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        } else {
+            for (const auto& t : tensor_maps(m)) {
+                const size_t cnt = (size_t)t.rows * t.cols;
+                double* stg = m->ctx->staging.as<double>(cnt);
+                if (!t.matrix) launch_export_w<float>(static_cast<float*>(t.dst), t.cols, t.rows, t.cols, 0, stg, st);
+                else if (m->ctx->prec == PARL_PREC_BF16)
+                    launch_export_w<bf16>(static_cast<bf16*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
+                else launch_export_w<float>(static_cast<float*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
+                PARL_CUDA(cudaMemcpyAsync(flat + t.src_off, stg, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+                PARL_CUDA(cudaStreamSynchronize(st));
+            }
+        }
+        PARL_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// ---- groups -----------------------------------------------------------------
+parl_status parl_group_create(parl_ctx_t ctx, int max_tokens, int max_responses, parl_group_t* out) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(max_tokens > 0 && max_responses > 0, PARL_E_CONFIG, "group capacity must be positive");
+        auto g = std::make_unique<parl_group_s>();
+        g->ctx = ctx;
+        ctx->refs++;
+        g->max_T = max_tokens;
+        g->max_G = max_responses;
+        alloc_group_arrays(g.get());
+        *out = g.release();
+    });
+}
+
+parl_status parl_group_destroy(parl_group_t g) {
+    if (g) {
+        parl_ctx_s* c = g->ctx;
+        cudaStreamSynchronize(c->st);
+        delete g;
+        ctx_release(c);
+    }
+    return PARL_OK;
+}
+
+int parl_group_tokens(parl_group_t g) { return g->T; }
+int parl_group_scored(parl_group_t g) { return g->S; }
+
+parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_t* resp_flat, const int32_t* lens,
+                      int G, int max_seq) {
+    return guarded(g->ctx, [&] {
+        check_pack_inputs(g, P, lens, G, max_seq);
+        set_pack_meta(g, P, lens, G, max_seq);
+        cudaStream_t st = g->ctx->st;
+        int32_t* dp = g->in_prompt.as<int32_t>(g->max_T);
+        int32_t* dr = g->in_resp.as<int32_t>(g->max_T);
+        PARL_CUDA(cudaMemcpyAsync(dp, prompt, (size_t)P * 4, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaMemcpyAsync(dr, resp_flat, (size_t)g->S * 4, cudaMemcpyHostToDevice, st));
+        upload_meta(g);
+        ProfScope ps(g->ctx, PARL_KC_PACK, 24.0 * g->T + 24.0 * g->S);
+        launch_pack(dp, P, dr, group_cu(g), G, g->T, g->pk, st);
+        check_launch();
+    });
+}
+
+parl_status parl_pack_device(parl_group_t g, const int32_t* d_prompt, int P, const int32_t* d_resp,
+                             const int32_t* lens, int G, int max_seq) {
+    return guarded(g->ctx, [&] {
+        check_pack_inputs(g, P, lens, G, max_seq);
+        set_pack_meta(g, P, lens, G, max_seq);
+        upload_meta(g);
+        ProfScope ps(g->ctx, PARL_KC_PACK, 24.0 * g->T + 24.0 * g->S);
+        launch_pack(d_prompt, P, d_resp, group_cu(g), G, g->T, g->pk, g->ctx->st);
+        check_launch();
+    });
+}
+
+parl_status parl_set_sequence(parl_group_t g, const int32_t* tokens, const int32_t* positions, const int32_t* labels,
+                              int T, int prompt_len, const int32_t* resp_lens, int G, int vocab, int max_seq) {
+    return guarded(g->ctx, [&] {
+        // validate_forward_inputs (model.cpp:404-426), same order
+        PARL_REQUIRE(T > 0, PARL_E_SHAPE, "empty token sequence");
+        PARL_REQUIRE(T <= max_seq, PARL_E_SHAPE,
+                     "sequence length " + std::to_string(T) + " exceeds max_seq_len " + std::to_string(max_seq));
+        for (int t = 0; t < T; ++t)
+            PARL_REQUIRE(tokens[t] >= 0 && tokens[t] < vocab, PARL_E_VOCAB,
+                         "token id " + std::to_string(tokens[t]) + " outside vocab of size " + std::to_string(vocab));
+        for (int t = 0; t < T; ++t)
+            PARL_REQUIRE(positions[t] >= 0 && positions[t] < max_seq, PARL_E_SHAPE,
+                         "position id " + std::to_string(positions[t]) + " outside [0, max_seq_len)");
+        if (labels)
+            for (int t = 0; t < T; ++t)
+                PARL_REQUIRE(labels[t] == -1 || (labels[t] >= 0 && labels[t] < vocab), PARL_E_VOCAB,
+                             "label id " + std::to_string(labels[t]) + " outside vocab");
+        if (prompt_len > 0) {  // AttentionMaskSpec::validate (model.cpp:53-61)
+            PARL_REQUIRE(G >= 1, PARL_E_SHAPE, "shared_prompt mask needs >= 1 response");
+            long tot = prompt_len;
+            for (int k = 0; k < G; ++k) {
+                PARL_REQUIRE(resp_lens[k] >= 1, PARL_E_SHAPE, "shared_prompt mask response lengths must be >= 1");
+                tot += resp_lens[k];
+            }
+            PARL_REQUIRE(tot == T, PARL_E_SHAPE, "mask total length does not match sequence length");
+        }
+        PARL_REQUIRE(T <= g->max_T && G <= g->max_G, PARL_E_SHAPE, "sequence exceeds the group capacity");
+        const int Peff = prompt_len > 0 ? prompt_len : T;
+        std::vector<int32_t> seg(T, 0), pred(T), sp, sl, pp, so, rp(T + 1, 0), ri;
+        g->lens.clear();
+        g->span_start.clear();
+        if (prompt_len > 0) {
+            int t = prompt_len;
+            for (int k = 0; k < G; ++k) {
+                g->span_start.push_back(t);
+                g->lens.push_back(resp_lens[k]);
+                for (int i = 0; i < resp_lens[k]; ++i) seg[t++] = k + 1;
+            }
+        }
+        for (int t = 0; t < T; ++t)
+            pred[t] = (prompt_len > 0 && seg[t] != 0 && seg[t - 1] != seg[t]) ? prompt_len - 1 : t - 1;
+        std::vector<int> nsample(std::max(G, 1), 0);
+        if (labels)
+            for (int t = 0; t < T; ++t) {
+                if (labels[t] == -1) continue;
+                PARL_REQUIRE(pred[t] >= 0, PARL_E_SHAPE, "position 0 has no predecessor to score its label from");
+                sp.push_back(t);
+                sl.push_back(labels[t]);
+                pp.push_back(pred[t]);
+                const int k = seg[t] > 0 ? seg[t] - 1 : 0;
+                so.push_back(k);
+                nsample[k]++;
+            }
+        const int S = (int)sp.size();
+        // position -> gathered rows CSR (rows listed in scored order)
+        std::vector<std::vector<int>> owned(T);
+        for (int s = 0; s < S; ++s) owned[pp[s]].push_back(s);
+        for (int t = 0; t < T; ++t) {
+            rp[t + 1] = rp[t] + (int)owned[t].size();
+            for (int s : owned[t]) ri.push_back(s);
+        }
+        g->T = T;
+        g->P = prompt_len;
+        g->G = prompt_len > 0 ? G : 0;
+        g->pairs = 0.5 * Peff * (Peff + 1.0);
+        for (int k = 0; k < g->G; ++k) g->pairs += (double)resp_lens[k] * Peff + 0.5 * resp_lens[k] * (resp_lens[k] + 1.0);
+        g->S = S;
+        g->Peff = Peff;
+        g->n_samples = std::max(G, 1);
+        g->cu.assign(g->n_samples + 1, 0);
+        for (int k = 0; k < g->n_samples; ++k) g->cu[k + 1] = g->cu[k] + nsample[k];
+        g->max_seq = max_seq;
+        g->vocab = vocab;
+        g->epoch++;
+        cudaStream_t st = g->ctx->st;
+        auto up = [&](int32_t* dst, const void* src, size_t n) {
+            if (n) PARL_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, st));
+        };
+        up(g->pk.tokens, tokens, T);
+        up(g->pk.positions, positions, T);
+        if (labels) up(g->pk.labels, labels, T);
+        up(g->pk.seg, seg.data(), T);
+        up(g->pk.pred, pred.data(), T);
+        up(g->pk.scored_pos, sp.data(), S);
+        up(g->pk.scored_label, sl.data(), S);
+        up(g->pk.pred_pos, pp.data(), S);
+        up(g->pk.sample_of, so.data(), S);
+        up(g->pk.row_ptr, rp.data(), T + 1);
+        up(g->pk.row_idx, ri.data(), S);
+        upload_meta(g);
+        PARL_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    });
+}
+
+parl_status parl_group_download(parl_group_t g, int32_t* tokens, int32_t* labels, int32_t* positions, int32_t* seg,
+                                int32_t* pred, int32_t* span_start, int32_t* scored_pos) {
+    return guarded(g->ctx, [&] {
+        cudaStream_t st = g->ctx->st;
+        auto dn = [&](void* dst, const int32_t* src, size_t n) {
+            if (dst && n) PARL_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToHost, st));
+        };
+        dn(tokens, g->pk.tokens, g->T);
+        dn(labels, g->pk.labels, g->T);
+        dn(positions, g->pk.positions, g->T);
+        dn(seg, g->pk.seg, g->T);
+        dn(pred, g->pk.pred, g->T);
+        dn(scored_pos, g->pk.scored_pos, g->S);
+        PARL_CUDA(cudaStreamSynchronize(st));
+        if (span_start) std::copy(g->span_start.begin(), g->span_start.end(), span_start);
+    });
+}
+
+// ---- forward ------------------------------------------------------------------
+static void do_forward(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, parl_act_t* act_out) {
+    PARL_REQUIRE(slot >= 0 && slot < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
+    PARL_REQUIRE(g->T > 0, PARL_E_SHAPE, "group is empty (pack or set a sequence first)");
+    PARL_REQUIRE(g->T <= m->cfg.max_seq_len, PARL_E_SHAPE, "sequence length exceeds max_seq_len");
+    g->vocab = m->cfg.vocab_size;
+    parl_act_s* act = nullptr;
+    if (act_out) {
+        act = *act_out ? *act_out : new parl_act_s();
+        *act_out = act;
+    }
+    if (c->prec == PARL_PREC_BF16) forward_impl<bf16>(c, m, g, slot, act);
+    else forward_impl<float>(c, m, g, slot, act);
+    const uint64_t gen = ++m->forward_gen;  // bump_forward_generation, model.cpp:559
+    if (act) {
+        act->owner = m;
+        act->group = g;
+        act->version = m->version;
+        act->gen = gen;
+        act->epoch = g->epoch;
+        act->T = g->T;
+        act->S = g->S;
+    }
+}
+
+parl_status parl_forward(parl_ctx_t ctx, parl_model_t m, parl_group_t g, int slot, parl_act_t* act_out) {
+    return guarded(ctx, [&] { do_forward(ctx, m, g, slot, act_out); });
+}
+
+parl_status parl_trimodel_forward(parl_ctx_t ctx, parl_model_t pol, parl_model_t old, parl_model_t ref,
+                                  parl_group_t g, parl_act_t* act_out) {
+    return guarded(ctx, [&] {
+        do_forward(ctx, pol, g, 0, act_out);
+        if (old) do_forward(ctx, old, g, 1, nullptr);
+        do_forward(ctx, ref, g, 2, nullptr);
+    });
+}
+
+parl_status parl_group_logprobs(parl_group_t g, int slot, double* out) {
+    return guarded(g->ctx, [&] {
+        PARL_REQUIRE(slot >= 0 && slot < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
+        std::vector<float> h(g->S);
+        if (g->S)
+            PARL_CUDA(cudaMemcpyAsync(h.data(), static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T, g->S * 4,
+                                      cudaMemcpyDeviceToHost, g->ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
+        for (int s = 0; s < g->S; ++s) out[s] = h[s];
+    });
+}
+
+parl_status parl_group_set_logprobs(parl_group_t g, int slot, const double* in) {
+    return guarded(g->ctx, [&] {
+        std::vector<float> h(in, in + g->S);
+        if (g->S)
+            PARL_CUDA(cudaMemcpyAsync(static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T, h.data(), g->S * 4,
+                                      cudaMemcpyHostToDevice, g->ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
+    });
+}
+
+parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, double* rows) {
+    // forward_logprob_rows: every position is a head row.
+    return guarded(ctx, [&] {
+        const int T = g->T, V = m->cfg.vocab_size;
+        std::vector<int32_t> tok(T), pos(T);
+        PARL_CUDA(cudaMemcpyAsync(tok.data(), g->pk.tokens, T * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaMemcpyAsync(pos.data(), g->pk.positions, T * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
+        // rows: score label 0 at every position from the position itself
+        std::vector<int32_t> lens(g->lens.begin(), g->lens.end());
+        parl_group_s tmp;
+        tmp.ctx = ctx;
+        tmp.max_T = std::max(T, 1);
+        tmp.max_G = std::max(g->max_G, 1);
+        alloc_group_arrays(&tmp);
+        // a T+1 long sequence would change attention; instead gather every row as a predecessor
+        std::vector<int32_t> seg(T), pred(T), sp(T), sl(T, 0), pp(T), so(T, 0), rp(T + 1), ri(T);
+        PARL_CUDA(cudaMemcpyAsync(seg.data(), g->pk.seg, T * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
+        for (int t = 0; t < T; ++t) {
+            sp[t] = t; pp[t] = t; rp[t] = t; ri[t] = t;
+        }
+        rp[T] = T;
+        tmp.T = T; tmp.P = g->P; tmp.G = g->G; tmp.S = T; tmp.Peff = g->Peff; tmp.n_samples = 1;
+        tmp.lens = g->lens; tmp.span_start = g->span_start; tmp.cu = {0, T};
+        tmp.vocab = V; tmp.max_seq = m->cfg.max_seq_len;
+        auto up = [&](int32_t* dst, const void* src, size_t n) {
+            PARL_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, ctx->st));
+        };
+        up(tmp.pk.tokens, tok.data(), T);
+        up(tmp.pk.positions, pos.data(), T);
+        up(tmp.pk.seg, seg.data(), T);
+        up(tmp.pk.scored_pos, sp.data(), T);
+        up(tmp.pk.scored_label, sl.data(), T);
+        up(tmp.pk.pred_pos, pp.data(), T);
+        up(tmp.pk.row_ptr, rp.data(), T + 1);
+        up(tmp.pk.row_idx, ri.data(), T);
+        upload_meta(&tmp);
+        if (ctx->prec == PARL_PREC_BF16) forward_impl<bf16>(ctx, m, &tmp, 0, nullptr);
+        else forward_impl<float>(ctx, m, &tmp, 0, nullptr);
+        ++m->forward_gen;
+        std::vector<float> z((size_t)T * V), lse(T);
+        PARL_CUDA(cudaMemcpyAsync(z.data(), ctx->logits.p, z.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaMemcpyAsync(lse.data(), ctx->lse_head.p, T * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
+        for (int t = 0; t < T; ++t)
+            for (int v = 0; v < V; ++v) rows[(size_t)t * V + v] = (double)z[(size_t)t * V + v] - (double)lse[t];
+    });
+}
+
+parl_status parl_act_destroy(parl_act_t a) {
+    delete a;
+    return PARL_OK;
+}
+
+// ---- loss ---------------------------------------------------------------------
+parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards, const double* advantages,
+                           const parl_hyper* hp, parl_loss_stats* out) {
+    return guarded(ctx, [&] {
+        const int G = g->n_samples;
+        PARL_REQUIRE(hp->epsilon > 0.0 && hp->epsilon < 1.0, PARL_E_CONFIG, "epsilon must be in (0, 1)");
+        PARL_REQUIRE(hp->beta >= 0.0, PARL_E_CONFIG, "beta must be >= 0");
+        for (int k = 0; k < G; ++k)
+            PARL_REQUIRE(g->cu[k + 1] > g->cu[k], PARL_E_SHAPE, "sample has empty response");
+        cudaStream_t st = ctx->st;
+        double* adv = g->adv.as<double>(G);
+        if (rewards) {
+            PARL_REQUIRE(G >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
+            double* r = g->rewards.as<double>(G);
+            PARL_CUDA(cudaMemcpyAsync(r, rewards, G * sizeof(double), cudaMemcpyHostToDevice, st));
+            launch_advantages(r, G, hp->advantage_mean_only, adv, st);
+        } else {
+            for (int k = 0; k < G; ++k)
+                PARL_REQUIRE(std::isfinite(advantages[k]), PARL_E_NUMERIC, "advantage is not finite");
+            PARL_CUDA(cudaMemcpyAsync(adv, advantages, G * sizeof(double), cudaMemcpyHostToDevice, st));
+        }
+        const float* lp = static_cast<float*>(g->lp.p);
+        double* stats = ctx->stats.as<double>(8);
+        ProfScope ps(ctx, PARL_KC_LOSS, 20.0 * g->S + 16.0 * G);
+        launch_grpo(lp, lp + g->max_T, lp + 2 * (size_t)g->max_T, group_cu(g), G, adv, hp->epsilon, hp->beta,
+                    hp->granularity, static_cast<float*>(g->upstream.p), ctx->per_sample.as<double>(4 * (size_t)G),
+                    stats, st);
+        check_launch();
+        if (out) {
+            double h[5];
+            PARL_CUDA(cudaMemcpyAsync(h, stats, 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaStreamSynchronize(st));
+            out->objective_sum = h[0];
+            out->clip_sum = h[1];
+            out->kl_sum = h[2];
+            out->clipped_units = h[3];
+            out->total_units = h[4];
+        }
+    });
+}
+
+parl_status parl_group_upstream(parl_group_t g, double* out) {
+    return guarded(g->ctx, [&] {
+        std::vector<float> h(g->S);
+        if (g->S)
+            PARL_CUDA(cudaMemcpyAsync(h.data(), g->upstream.p, g->S * 4, cudaMemcpyDeviceToHost, g->ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
+        for (int s = 0; s < g->S; ++s) out[s] = h[s];
+    });
+}
+
+parl_status parl_group_set_upstream(parl_group_t g, const double* in) {
+    return guarded(g->ctx, [&] {
+        std::vector<float> h(in, in + g->S);
+        if (g->S)
+            PARL_CUDA(cudaMemcpyAsync(g->upstream.p, h.data(), g->S * 4, cudaMemcpyHostToDevice, g->ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
+    });
+}
+
+parl_status parl_stats_download(parl_ctx_t ctx, parl_loss_stats* out) {
+    return guarded(ctx, [&] {
+        double h[5];
+        PARL_CUDA(cudaMemcpyAsync(h, ctx->stats.as<double>(8), 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
+        out->objective_sum = h[0];
+        out->clip_sum = h[1];
+        out->kl_sum = h[2];
+        out->clipped_units = h[3];
+        out->total_units = h[4];
+    });
+}
+
+parl_status parl_stats_reset(parl_ctx_t ctx) {
+    return guarded(ctx, [&] { PARL_CUDA(cudaMemsetAsync(ctx->stats.as<double>(8), 0, 8 * sizeof(double), ctx->st)); });
+}
+
+// ---- backward -----------------------------------------------------------------
+parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out) {
+    return guarded(ctx, [&] {
+        auto gr = std::make_unique<parl_grad_s>();
+        gr->ctx = ctx;
+        ctx->refs++;
+        gr->cfg = like->cfg;
+        gr->L = like->L;
+        float* p = gr->g.as<float>(gr->L.total);
+        PARL_CUDA(cudaMemsetAsync(p, 0, gr->L.total * sizeof(float), ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
+        *out = gr.release();
+    });
+}
+
+parl_status parl_grad_destroy(parl_grad_t gr) {
+    if (gr) {
+        parl_ctx_s* c = gr->ctx;
+        cudaStreamSynchronize(c->st);
+        delete gr;
+        ctx_release(c);
+    }
+    return PARL_OK;
+}
+
+parl_status parl_grad_reset(parl_grad_t gr) {
+    return guarded(gr->ctx, [&] {
+        PARL_CUDA(cudaMemsetAsync(gr->g.p, 0, gr->L.total * sizeof(float), gr->ctx->st));
+        gr->micro_steps = 0;
+    });
+}
+
+int parl_grad_micro_steps(parl_grad_t gr) { return gr->micro_steps; }
+
+parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl_group_t g, parl_grad_t gr) {
+    return guarded(ctx, [&] {
+        // lifecycle checks, model.cpp:590-598
+        PARL_REQUIRE(act != nullptr && act->owner != nullptr, PARL_E_LIFECYCLE,
+                     "backward requires a cached forward result");
+        PARL_REQUIRE(act->owner == pol && act->version == pol->version && act->gen == pol->forward_gen &&
+                         act->group == g && act->epoch == g->epoch,
+                     PARL_E_LIFECYCLE, "stale activation handle: a newer forward or update invalidated this cache");
+        PARL_REQUIRE(same_cfg(gr->cfg, pol->cfg), PARL_E_SHAPE, "gradient buffers have incongruent layouts");
+        if (ctx->prec == PARL_PREC_BF16) backward_impl<bf16>(ctx, pol, act, g, gr);
+        else backward_impl<float>(ctx, pol, act, g, gr);
+    });
+}
+
+parl_status parl_grad_download(parl_grad_t gr, double* flat, size_t n) {
+    return guarded(gr->ctx, [&] {
+        PARL_REQUIRE(n == gr->L.total, PARL_E_SHAPE, "gradient array size does not match the layout");
+        cudaStream_t st = gr->ctx->st;
+        const size_t chunk = (size_t)64 << 20;
+        for (size_t o = 0; o < n; o += chunk) {
+            const size_t cnt = std::min(chunk, n - o);
+            double* stg = gr->ctx->staging.as<double>(cnt);
+            launch_f32_to_f64(static_cast<float*>(gr->g.p) + o, stg, (long)cnt, st);
+            PARL_CUDA(cudaMemcpyAsync(flat + o, stg, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaStreamSynchronize(st));
+        }
+    });
+}
+
+parl_status parl_train_microbatch(parl_ctx_t ctx, parl_model_t pol, parl_model_t old, parl_model_t ref,
+                                  parl_group_t g, const double* rewards, const double* advantages,
+                                  const parl_hyper* hp, parl_grad_t gr, parl_loss_stats* stats_out) {
+    // Pipeline::train_microbatch shared-prompt branch (pipeline.cpp:97-141)
+    parl_act_t act = nullptr;
+    parl_status s = parl_trimodel_forward(ctx, pol, old, ref, g, &act);
+    if (s == PARL_OK) s = parl_grpo_loss(ctx, g, rewards, advantages, hp, stats_out);
+    if (s == PARL_OK) s = parl_backward(ctx, pol, act, g, gr);
+    delete act;
+    return s;
+}
+
+parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr) {
+    // ModelParams::apply_update, model.cpp:202-219
+    return guarded(m->ctx, [&] {
+        PARL_REQUIRE(same_cfg(gr->cfg, m->cfg), PARL_E_SHAPE, "gradient layout not congruent with parameters");
+        PARL_REQUIRE(gr->micro_steps > 0, PARL_E_CONFIG, "apply_update requires micro_step_count > 0");
+        PARL_REQUIRE(lr >= 0.0 && std::isfinite(lr), PARL_E_CONFIG, "learning rate must be finite and >= 0");
+        PARL_REQUIRE(m->has_master, PARL_E_CONFIG, "apply_update needs the fp64 master copy");
+        cudaStream_t st = m->ctx->st;
+        int* flags = m->ctx->flags.as<int>(1);
+        PARL_CUDA(cudaMemsetAsync(flags, 0, 4, st));
+        const double scale = lr / gr->micro_steps;
+        launch_sgd(static_cast<float*>(gr->g.p), static_cast<double*>(m->master.p), (long)m->L.total, scale, flags, 0, st);
+        int h = 0;
+        PARL_CUDA(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, st));
+        PARL_CUDA(cudaStreamSynchronize(st));
+        PARL_REQUIRE(!(h & 1), PARL_E_NUMERIC, "refusing update: gradient contains NaN/Inf");
+        PARL_REQUIRE(!(h & 2), PARL_E_NUMERIC, "refusing update: result would be non-finite");
+        launch_sgd(static_cast<float*>(gr->g.p), static_cast<double*>(m->master.p), (long)m->L.total, scale, flags, 1, st);
+        convert_from_master(m);
+        PARL_CUDA(cudaStreamSynchronize(st));
+        ++m->version;
+    });
+}
+
+// ---- NCCL (loaded at run time; data-parallel gradient/stat allreduce) -------------
+static NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.h) {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (api.h) {
+            api.getUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
+            api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(api.h, "ncclAllReduce");
+            api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+            api.getErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+        }
+    }
+    if (!api.h || !api.getUniqueId) throw Error{PARL_E_NCCL, "libnccl.so.2 not loadable"};
+    return api;
+}
+
+struct NcclId {
+    char b[PARL_NCCL_ID_BYTES];
+};
+
+parl_status parl_comm_unique_id(char id[PARL_NCCL_ID_BYTES]) {
+    return guarded(nullptr, [&] {
+        int r = nccl().getUniqueId(id);
+        PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclGetUniqueId failed");
+    });
+}
+
+parl_status parl_comm_init(parl_ctx_t ctx, const char id[PARL_NCCL_ID_BYTES], int rank, int nranks) {
+    return guarded(ctx, [&] {
+        auto& api = nccl();
+        using InitFn = int (*)(void**, int, NcclId, int);
+        auto init = (InitFn)dlsym(api.h, "ncclCommInitRank");
+        PARL_REQUIRE(init != nullptr, PARL_E_NCCL, "ncclCommInitRank missing");
+        NcclId uid;
+        std::memcpy(uid.b, id, PARL_NCCL_ID_BYTES);
+        PARL_CUDA(cudaSetDevice(ctx->device));
+        int r = init(&ctx->comm, nranks, uid, rank);
+        PARL_REQUIRE(r == 0, PARL_E_NCCL, std::string("ncclCommInitRank: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+    });
+}
+
+parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
+    return guarded(ctx, [&] {
+        if (!ctx->comm || ctx->nranks == 1) return;
+        // ncclFloat32 = 7, ncclSum = 0
+        int r = nccl().allReduce(gr->g.p, gr->g.p, gr->L.total, 7, 0, ctx->comm, ctx->st);
+        PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce(grad) failed");
+    });
+}
+
+parl_status parl_stats_allreduce(parl_ctx_t ctx) {
+    return guarded(ctx, [&] {
+        if (!ctx->comm || ctx->nranks == 1) return;
+        // ncclFloat64 = 8
+        int r = nccl().allReduce(ctx->stats.p, ctx->stats.p, 5, 8, 0, ctx->comm, ctx->st);
+        PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce(stats) failed");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,659 @@
+// HBM-bound / integer kernels of the hot path:
+//   K1  packer                 pack_group + build_segments/predecessor (packing.cpp:7-45, model.cpp:230-253)
+//   K2  embedding gather       model.cpp:449-455
+//   K5  LayerNorm fwd / bwd    model.cpp:317-369
+//   K6b vocab LSE + gather     model.cpp:523-556 (FFMA mode; the tcgen05 head fuses this)
+//   K7  GRPO loss              grpo.cpp:24-151 + pipeline.cpp:127-139
+//   K8a softmax backward seed  model.cpp:637-650
+//   K11 embedding-grad reduce  model.cpp:825-834 (deterministic: stable sort + segmented sum)
+// plus column reductions (bias / LN parameter grads), weight conversion,
+// device init, SGD update.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace parl_gpu {
+
+// ---------------------------------------------------------------------------
+// K1: device packer.  One thread per packed position t.  cu[k] = scored offset
+// of response k (exclusive prefix of resp_lens), cu[G] = S.
+__global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t* __restrict__ resp_flat,
+                       const int32_t* __restrict__ cu, int G, PackedDev pk) {
+    const int T = P + cu[G];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+        if (t < P) {
+            pk.tokens[t] = prompt[t];
+            pk.labels[t] = -1;
+            pk.positions[t] = t;
+            pk.seg[t] = 0;
+            pk.pred[t] = t - 1;
+            pk.row_ptr[t] = 0;
+        } else {
+            const int s = t - P;
+            int lo = 0, hi = G - 1;  // response k with cu[k] <= s < cu[k+1]
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (cu[mid] <= s) lo = mid; else hi = mid - 1;
+            }
+            const int k = lo, i = s - cu[k];
+            const int tok = resp_flat[s];
+            pk.tokens[t] = tok;
+            pk.labels[t] = tok;  // self-aligned labels, packing.cpp:37
+            pk.positions[t] = P + i;
+            pk.seg[t] = k + 1;
+            const int pr = (i == 0) ? P - 1 : t - 1;  // model.cpp:251
+            pk.pred[t] = pr;
+            pk.scored_pos[s] = t;
+            pk.scored_label[s] = tok;
+            pk.pred_pos[s] = pr;
+            pk.sample_of[s] = k;
+            // position -> gathered head rows (CSR): P-1 owns the G response
+            // starts, every non-final response token owns row t+1-P.
+            pk.row_ptr[t] = G + s - k;
+            const bool last = (i == cu[k + 1] - cu[k] - 1);
+            if (!last) pk.row_idx[G + s - k] = s + 1;
+        }
+        if (t == P - 1)
+            for (int k = 0; k < G; ++k) pk.row_idx[k] = cu[k];
+        if (t == T - 1) pk.row_ptr[T] = cu[G];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: x[t] = tok_emb[tokens[t]] + pos_emb[positions[t]]  (fp32 residual stream)
+__global__ void k_embed(const float* __restrict__ tok_emb, const float* __restrict__ pos_emb,
+                        const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions, int T,
+                        int D, float* __restrict__ x) {
+    const long n = (long)T * D;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int t = (int)(e / D), i = (int)(e % D);
+        x[e] = tok_emb[(long)tokens[t] * D + i] + pos_emb[(long)positions[t] * D + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: LayerNorm forward, one warp per row; rows optionally gathered through
+// `rows` (final LN over the head's predecessor rows).  Two-pass mean/variance
+// (population), eps 1e-5 (model.cpp:132, 317-343).
+template <class T>
+__global__ void k_layernorm(const float* __restrict__ x, const int32_t* __restrict__ rows, int R, int D,
+                            const float* __restrict__ gamma, const float* __restrict__ beta,
+                            T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= R) return;
+    const int src = rows ? rows[warp] : warp;
+    const float* xr = x + (long)src * D;
+    float s = 0.f;
+    for (int i = lane; i < D; i += 32) s += xr[i];
+    const float mean = warp_sum(s) / D;
+    float v = 0.f;
+    for (int i = lane; i < D; i += 32) {
+        const float c = xr[i] - mean;
+        v += c * c;
+    }
+    const float rstd = rsqrtf(warp_sum(v) / D + 1e-5f);
+    T* yr = y + (long)warp * D;
+    for (int i = lane; i < D; i += 32) yr[i] = from_f<T>((xr[i] - mean) * rstd * gamma[i] + beta[i]);
+    if (lane == 0) {
+        mean_out[warp] = mean;
+        rstd_out[warp] = rstd;
+    }
+}
+
+// LayerNorm backward (input part), one warp per row:
+//   dx[r] = (res ? res[r] : 0) + rstd * (dxh - mean(dxh) - xhat * mean(dxh*xhat)),  dxh = dy*gamma
+// x rows gathered through `rows` when given (stats are per output row).
+__global__ void k_layernorm_bwd(const float* __restrict__ dy, const float* __restrict__ x,
+                                const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                const float* __restrict__ rstd, const float* __restrict__ gamma, int R, int D,
+                                const float* __restrict__ res, float* __restrict__ dx) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= R) return;
+    const float* xr = x + (long)(rows ? rows[warp] : warp) * D;
+    const float* dyr = dy + (long)warp * D;
+    const float mu = mean[warp], rs = rstd[warp];
+    float a = 0.f, b = 0.f;
+    for (int i = lane; i < D; i += 32) {
+        const float dxh = dyr[i] * gamma[i];
+        a += dxh;
+        b += dxh * (xr[i] - mu) * rs;
+    }
+    a = warp_sum(a) / D;
+    b = warp_sum(b) / D;
+    float* o = dx + (long)warp * D;
+    const float* rr = res ? res + (long)warp * D : nullptr;
+    for (int i = lane; i < D; i += 32) {
+        const float xh = (xr[i] - mu) * rs;
+        const float v = rs * (dyr[i] * gamma[i] - a - xh * b);
+        o[i] = rr ? rr[i] + v : v;
+    }
+}
+
+// Column reductions, deterministic (fixed per-thread row stripes, fixed smem tree).
+//   mode 0: out[c] += sum_r X[r][c]                          (bias grads)
+//   mode 1: out[c] += sum_r dy[r][c]*xhat[r][c], out2[c] += sum_r dy[r][c]  (LN gamma/beta)
+template <class T>
+__global__ void k_colsum(const T* __restrict__ X, long ldx, int R, int N, float* __restrict__ out,
+                         const float* __restrict__ xs, const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                         const float* __restrict__ rstd, float* __restrict__ out2, int mode) {
+    __shared__ float sa[8][33], sb[8][33];
+    const int c = blockIdx.x * 32 + threadIdx.x;
+    const int ty = threadIdx.y;  // 8 row stripes
+    float a = 0.f, b = 0.f;
+    if (c < N) {
+        for (int r = ty; r < R; r += 8) {
+            const float v = to_f<T>(X[(long)r * ldx + c]);
+            if (mode == 0) {
+                a += v;
+            } else {
+                const float xv = xs[(long)(rows ? rows[r] : r) * N + c];
+                a += v * (xv - mean[r]) * rstd[r];
+                b += v;
+            }
+        }
+    }
+    sa[ty][threadIdx.x] = a;
+    sb[ty][threadIdx.x] = b;
+    __syncthreads();
+    if (ty == 0 && c < N) {
+        float ta = 0.f, tb = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            ta += sa[i][threadIdx.x];
+            tb += sb[i][threadIdx.x];
+        }
+        out[c] += ta;
+        if (mode == 1) out2[c] += tb;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6b (FFMA mode): per head row s: lse = logsumexp(z[s,:]); lp[s] = z[s,label] - lse.
+__global__ void k_row_lse(const float* __restrict__ z, int V, const int32_t* __restrict__ labels,
+                          float* __restrict__ lse_out, float* __restrict__ lp_out) {
+    __shared__ float sm[32], ss[32];
+    const int s = blockIdx.x;
+    const float* row = z + (long)s * V;
+    float m = -INFINITY, sum = 0.f;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        const float x = row[v];
+        if (x > m) {
+            sum = sum * __expf(m - x) + 1.f;
+            m = x;
+        } else {
+            sum += __expf(x - m);
+        }
+    }
+    // warp then block combine of (m, sum)
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mm = fmaxf(m, m2);
+        sum = (m == -INFINITY ? 0.f : sum * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+        m = mm;
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sm[w] = m;
+        ss[w] = sum;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        m = lane < nw ? sm[lane] : -INFINITY;
+        sum = lane < nw ? ss[lane] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+            const float mm = fmaxf(m, m2);
+            sum = (m == -INFINITY ? 0.f : sum * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+            m = mm;
+        }
+        if (lane == 0) {
+            const float lse = m + logf(sum);
+            lse_out[s] = lse;
+            if (lp_out) lp_out[s] = row[labels[s]] - lse;
+        }
+    }
+}
+
+// Combine the tcgen05 head's per-tile (max, sumexp) partials: lse and lp.
+__global__ void k_lse_combine(const float* __restrict__ part, int n_parts, const float* __restrict__ target,
+                              int S, float* __restrict__ lse_out, float* __restrict__ lp_out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const float* p = part + (long)s * n_parts * 2;
+    float m = -INFINITY;
+    for (int i = 0; i < n_parts; ++i) m = fmaxf(m, p[2 * i]);
+    float sum = 0.f;
+    for (int i = 0; i < n_parts; ++i) sum += p[2 * i + 1] * __expf(p[2 * i] - m);
+    const float lse = m + logf(sum);
+    lse_out[s] = lse;
+    lp_out[s] = target[s] - lse;
+}
+
+// K8a: dZ[s, v] = u[s] * (onehot(label[s]) - exp(z[s, v] - lse[s]))   (model.cpp:637-650)
+template <class Tin, class Tout>
+__global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restrict__ dz, long lddz, int S, int V,
+                              const float* __restrict__ lse, const float* __restrict__ u,
+                              const int32_t* __restrict__ labels) {
+    const long n = (long)S * V;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int s = (int)(e / V), v = (int)(e % V);
+        const float us = u[s];
+        const float p = __expf(to_f<Tin>(z[(long)s * ldz + v]) - lse[s]);
+        dz[(long)s * lddz + v] = from_f<Tout>(us * ((v == labels[s] ? 1.f : 0.f) - p));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: GRPO.  Advantages (grpo.cpp:24-48), one warp.
+__global__ void k_advantages(const double* __restrict__ rewards, int G, int mean_only, double* __restrict__ adv) {
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    for (int i = lane; i < G; i += 32) s += rewards[i];
+    const double mean = warp_sum_d(s) / G;
+    double v = 0.0;
+    for (int i = lane; i < G; i += 32) v += (rewards[i] - mean) * (rewards[i] - mean);
+    const double sd = sqrt(warp_sum_d(v) / G);
+    for (int i = lane; i < G; i += 32)
+        adv[i] = mean_only ? rewards[i] - mean : (sd < 1e-8 ? 0.0 : (rewards[i] - mean) / sd);
+}
+
+__device__ __forceinline__ void clip_eval(double lp, double old, double A, double eps, double& val,
+                                          double& grad, int& clipped) {  // grpo.cpp:64-80
+    const double r = exp(lp - old), lo = 1.0 - eps, hi = 1.0 + eps;
+    const double cl = fmin(fmax(r, lo), hi);
+    const double un = r * A, cv = cl * A;
+    clipped = (r < lo || r > hi);
+    if (un <= cv) {
+        val = un;
+        grad = r * A;
+    } else {
+        val = cv;
+        grad = (r > lo && r < hi) ? r * A : 0.0;
+    }
+}
+
+// One block per response j (tokens [cu[j], cu[j+1])).  Writes the backward
+// seed upstream[t] = -d(L_j - beta KL_j)/d lp_t (pipeline.cpp:138) and the
+// per-sample {clip_term, kl, clipped, units} into per_sample[j][4].
+__global__ void k_grpo_terms(const float* __restrict__ lp, const float* __restrict__ old,
+                             const float* __restrict__ ref, const int32_t* __restrict__ cu,
+                             const double* __restrict__ adv, double eps, double beta, int granularity,
+                             float* __restrict__ upstream, double* __restrict__ per_sample) {
+    __shared__ double red[4][32];
+    const int j = blockIdx.x;
+    const int b = cu[j], e = cu[j + 1], n = e - b;
+    const double A = adv[j], inv = 1.0 / n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double a0 = 0, a1 = 0, a2 = 0;
+    if (granularity == 0) {
+        for (int t = b + threadIdx.x; t < e; t += blockDim.x) {
+            double cv, cg;
+            int c;
+            clip_eval(lp[t], old[t], A, eps, cv, cg, c);
+            const double d = (double)ref[t] - (double)lp[t];  // grpo.cpp:89-93
+            const double em = expm1(d);
+            a0 += cv;
+            a1 += em - d;
+            a2 += c;
+            upstream[t] = (float)(-inv * (cg + beta * em));
+        }
+    } else {
+        for (int t = b + threadIdx.x; t < e; t += blockDim.x) {
+            a0 += lp[t];
+            a1 += old[t];
+            a2 += ref[t];
+        }
+    }
+    a0 = warp_sum_d(a0);
+    a1 = warp_sum_d(a1);
+    a2 = warp_sum_d(a2);
+    if (lane == 0) {
+        red[0][w] = a0;
+        red[1][w] = a1;
+        red[2][w] = a2;
+    }
+    __syncthreads();
+    __shared__ double g_seq;
+    if (threadIdx.x == 0) {
+        double s0 = 0, s1 = 0, s2 = 0;
+        for (int i = 0; i < nw; ++i) {
+            s0 += red[0][i];
+            s1 += red[1][i];
+            s2 += red[2][i];
+        }
+        double* o = per_sample + 4 * j;
+        if (granularity == 0) {
+            o[0] = s0 * inv;
+            o[1] = s1 * inv;
+            o[2] = s2;
+            o[3] = n;
+        } else {  // grpo.cpp:134-149: one evaluation on the summed log-probs
+            double cv, cg;
+            int c;
+            clip_eval(s0, s1, A, eps, cv, cg, c);
+            const double d = s2 - s0, em = expm1(d);
+            o[0] = cv;
+            o[1] = em - d;
+            o[2] = c;
+            o[3] = 1;
+            g_seq = cg + beta * em;
+        }
+    }
+    __syncthreads();
+    if (granularity == 1)
+        for (int t = b + threadIdx.x; t < e; t += blockDim.x) upstream[t] = (float)(-g_seq);
+}
+
+// Sum per-sample terms in sample order into the running stats
+// (pipeline.cpp:133-137): objective, clip, kl, clipped, units.
+__global__ void k_grpo_stats(const double* __restrict__ per_sample, int G, double beta, double* __restrict__ stats) {
+    if (threadIdx.x != 0) return;
+    for (int j = 0; j < G; ++j) {
+        const double* o = per_sample + 4 * j;
+        stats[0] += o[0] - beta * o[1];
+        stats[1] += o[0];
+        stats[2] += o[1];
+        stats[3] += o[2];
+        stats[4] += o[3];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dx[t] = sum over gathered head rows r owned by position t of dxg[r]  (CSR;
+// rows of positions without scored successors are zero).
+__global__ void k_scatter_rows(const float* __restrict__ dxg, const int32_t* __restrict__ row_ptr,
+                               const int32_t* __restrict__ row_idx, int T, int D, float* __restrict__ dx) {
+    const long n = (long)T * D;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int t = (int)(e / D), i = (int)(e % D);
+        float acc = 0.f;
+        for (int r = row_ptr[t]; r < row_ptr[t + 1]; ++r) acc += dxg[(long)row_idx[r] * D + i];
+        dx[e] = acc;
+    }
+}
+
+// K11: segmented sum of dx rows over runs of equal keys (keys sorted stably,
+// so each run lists its rows in position order): grad[key] += sum dx[idx].
+__global__ void k_embed_grad(const int32_t* __restrict__ keys, const int32_t* __restrict__ idx, int T,
+                             const float* __restrict__ dx, int D, float* __restrict__ grad) {
+    const int i = blockIdx.x;
+    if (i >= T) return;
+    const int key = keys[i];
+    if (i > 0 && keys[i - 1] == key) return;  // not a run start
+    int end = i + 1;
+    while (end < T && keys[end] == key) ++end;
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float acc = 0.f;
+        for (int r = i; r < end; ++r) acc += dx[(long)idx[r] * D + c];
+        grad[(long)key * D + c] += acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// conversions
+template <class T>
+__global__ void k_f32_to_act(const float* __restrict__ x, T* __restrict__ y, long n) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+        y[e] = from_f<T>(x[e]);
+}
+
+// src fp64 [rows x cols] (row-major) -> dst [rows x cols] (transposed=0) or
+// [cols x rows] (transposed=1) in dtype T, with dst leading dimension ldd.
+template <class T>
+__global__ void k_convert_w(const double* __restrict__ src, int rows, int cols, T* __restrict__ dst, long ldd,
+                            int transposed) {
+    __shared__ float tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = (float)src[(long)r * cols + c];
+    }
+    __syncthreads();
+    if (!transposed) {
+        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+            const int r = r0 + i, c = c0 + threadIdx.x;
+            if (r < rows && c < cols) dst[(long)r * ldd + c] = from_f<T>(tile[i][threadIdx.x]);
+        }
+    } else {
+        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+            const int c = c0 + i, r = r0 + threadIdx.x;
+            if (r < rows && c < cols) dst[(long)c * ldd + r] = from_f<T>(tile[threadIdx.x][i]);
+        }
+    }
+}
+
+// reverse of the above into fp64 (model download)
+template <class T>
+__global__ void k_export_w(const T* __restrict__ src, long lds, int rows, int cols, int transposed,
+                           double* __restrict__ dst) {
+    const long n = (long)rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / cols), c = (int)(e % cols);
+        dst[e] = (double)to_f<T>(transposed ? src[(long)c * lds + r] : src[(long)r * lds + c]);
+    }
+}
+
+__global__ void k_f32_to_f64(const float* __restrict__ x, double* __restrict__ y, long n) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) y[e] = x[e];
+}
+
+// Philox-based N(0,1) * scale (+ base): device init of large configs.
+__device__ __forceinline__ uint2 philox(uint2 ctr, uint32_t key_lo, uint32_t key_hi, uint32_t c2) {
+    uint32_t c0 = ctr.x, c1 = ctr.y, k0 = key_lo, k1 = key_hi, cc2 = c2, c3 = 0;
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * cc2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        cc2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return make_uint2(c0, cc2);
+}
+
+__global__ void k_randn(double* __restrict__ out, long n, uint64_t seed, uint32_t stream, double scale,
+                        const double* __restrict__ base) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const uint2 r = philox(make_uint2((uint32_t)e, (uint32_t)(e >> 32)), (uint32_t)seed, (uint32_t)(seed >> 32),
+                               stream);
+        const double u1 = ((r.x >> 8) + 1.0) * (1.0 / 16777217.0), u2 = (r.y >> 8) * (1.0 / 16777216.0);
+        const double z = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+        out[e] = (base ? base[e] : 0.0) + scale * z;
+    }
+}
+
+__global__ void k_fill_f64(double* __restrict__ out, long n, double v) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) out[e] = v;
+}
+
+// apply_update (model.cpp:202-219): flag non-finite gradients / results.
+__global__ void k_sgd_check(const float* __restrict__ g, const double* __restrict__ w, long n, double scale,
+                            int* __restrict__ flags) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        if (!isfinite(g[e])) atomicOr(flags, 1);
+        else if (!isfinite(w[e] - scale * (double)g[e])) atomicOr(flags, 2);
+    }
+}
+__global__ void k_sgd_apply(const float* __restrict__ g, double* __restrict__ w, long n, double scale) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+        w[e] -= scale * (double)g[e];
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+static int grid_for(long n, int bs = 256) {
+    long g = (n + bs - 1) / bs;
+    return (int)(g < 148L * 16 ? (g < 1 ? 1 : g) : 148L * 16);
+}
+
+void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
+                 const PackedDev& pk, cudaStream_t st) {
+    k_pack<<<grid_for(T), 256, 0, st>>>(prompt, P, resp, cu, G, pk);
+    PARL_LAUNCHED();
+}
+
+void launch_embed(const float* tok, const float* pos, const int32_t* tokens, const int32_t* positions, int T, int D,
+                  float* x, cudaStream_t st) {
+    k_embed<<<grid_for((long)T * D), 256, 0, st>>>(tok, pos, tokens, positions, T, D, x);
+    PARL_LAUNCHED();
+}
+
+template <class T>
+void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
+                      float* mean, float* rstd, cudaStream_t st) {
+    if (R <= 0) return;
+    k_layernorm<T><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    PARL_LAUNCHED();
+}
+template void launch_layernorm<float>(const float*, const int32_t*, int, int, const float*, const float*, float*,
+                                      float*, float*, cudaStream_t);
+template void launch_layernorm<bf16>(const float*, const int32_t*, int, int, const float*, const float*, bf16*,
+                                     float*, float*, cudaStream_t);
+
+void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
+                          const float* gamma, int R, int D, const float* res, float* dx, float* dgamma, float* dbeta,
+                          cudaStream_t st) {
+    if (R <= 0) return;
+    k_layernorm_bwd<<<cdiv(R, 8), 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx);
+    PARL_LAUNCHED();
+    k_colsum<float><<<cdiv(D, 32), dim3(32, 8), 0, st>>>(dy, D, R, D, dgamma, x, rows, mean, rstd, dbeta, 1);
+    PARL_LAUNCHED();
+}
+
+template <class T>
+void launch_colsum(const T* X, long ldx, int R, int N, float* out, cudaStream_t st) {
+    if (R <= 0) return;
+    k_colsum<T><<<cdiv(N, 32), dim3(32, 8), 0, st>>>(X, ldx, R, N, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+    PARL_LAUNCHED();
+}
+template void launch_colsum<float>(const float*, long, int, int, float*, cudaStream_t);
+template void launch_colsum<bf16>(const bf16*, long, int, int, float*, cudaStream_t);
+
+void launch_row_lse(const float* z, int S, int V, const int32_t* labels, float* lse, float* lp, cudaStream_t st) {
+    if (S <= 0) return;
+    k_row_lse<<<S, 256, 0, st>>>(z, V, labels, lse, lp);
+    PARL_LAUNCHED();
+}
+
+void launch_lse_combine(const float* part, int n_parts, const float* target, int S, float* lse, float* lp,
+                        cudaStream_t st) {
+    if (S <= 0) return;
+    k_lse_combine<<<cdiv(S, 128), 128, 0, st>>>(part, n_parts, target, S, lse, lp);
+    PARL_LAUNCHED();
+}
+
+template <class Tin, class Tout>
+void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int V, const float* lse, const float* u,
+                        const int32_t* labels, cudaStream_t st) {
+    if (S <= 0) return;
+    k_softmax_bwd<Tin, Tout><<<grid_for((long)S * V), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
+    PARL_LAUNCHED();
+}
+template void launch_softmax_bwd<float, float>(const float*, long, float*, long, int, int, const float*,
+                                               const float*, const int32_t*, cudaStream_t);
+template void launch_softmax_bwd<float, bf16>(const float*, long, bf16*, long, int, int, const float*, const float*,
+                                              const int32_t*, cudaStream_t);
+template void launch_softmax_bwd<bf16, bf16>(const bf16*, long, bf16*, long, int, int, const float*, const float*,
+                                             const int32_t*, cudaStream_t);
+
+void launch_advantages(const double* rewards, int G, int mean_only, double* adv, cudaStream_t st) {
+    k_advantages<<<1, 32, 0, st>>>(rewards, G, mean_only, adv);
+    PARL_LAUNCHED();
+}
+
+void launch_grpo(const float* lp, const float* old, const float* ref, const int32_t* cu, int G, const double* adv,
+                 double eps, double beta, int gran, float* upstream, double* per_sample, double* stats,
+                 cudaStream_t st) {
+    k_grpo_terms<<<G, 256, 0, st>>>(lp, old, ref, cu, adv, eps, beta, gran, upstream, per_sample);
+    PARL_LAUNCHED();
+    k_grpo_stats<<<1, 32, 0, st>>>(per_sample, G, beta, stats);
+    PARL_LAUNCHED();
+}
+
+void launch_scatter_rows(const float* dxg, const int32_t* row_ptr, const int32_t* row_idx, int T, int D, float* dx,
+                         cudaStream_t st) {
+    k_scatter_rows<<<grid_for((long)T * D), 256, 0, st>>>(dxg, row_ptr, row_idx, T, D, dx);
+    PARL_LAUNCHED();
+}
+
+size_t sort_temp_bytes(int n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, n);
+    return bytes;
+}
+
+void launch_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
+                       const int32_t* vals_in, int32_t* vals_out, int n, int end_bit, cudaStream_t st) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, end_bit, st);
+    PARL_LAUNCHED();
+}
+
+__global__ void k_iota(int32_t* x, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = i;
+}
+void launch_iota(int32_t* x, int n, cudaStream_t st) {
+    k_iota<<<cdiv(n, 256), 256, 0, st>>>(x, n);
+    PARL_LAUNCHED();
+}
+
+void launch_embed_grad(const int32_t* keys, const int32_t* idx, int T, const float* dx, int D, float* grad,
+                       cudaStream_t st) {
+    if (T <= 0) return;
+    k_embed_grad<<<T, 128, 0, st>>>(keys, idx, T, dx, D, grad);
+    PARL_LAUNCHED();
+}
+
+template <class T>
+void launch_f32_to_act(const float* x, T* y, long n, cudaStream_t st) {
+    k_f32_to_act<T><<<grid_for(n), 256, 0, st>>>(x, y, n);
+    PARL_LAUNCHED();
+}
+template void launch_f32_to_act<float>(const float*, float*, long, cudaStream_t);
+template void launch_f32_to_act<bf16>(const float*, bf16*, long, cudaStream_t);
+
+template <class T>
+void launch_convert_w(const double* src, int rows, int cols, T* dst, long ldd, int transposed, cudaStream_t st) {
+    dim3 grid(cdiv(cols, 32), cdiv(rows, 32));
+    k_convert_w<T><<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst, ldd, transposed);
+    PARL_LAUNCHED();
+}
+template void launch_convert_w<float>(const double*, int, int, float*, long, int, cudaStream_t);
+template void launch_convert_w<bf16>(const double*, int, int, bf16*, long, int, cudaStream_t);
+
+template <class T>
+void launch_export_w(const T* src, long lds, int rows, int cols, int transposed, double* dst, cudaStream_t st) {
+    k_export_w<T><<<grid_for((long)rows * cols), 256, 0, st>>>(src, lds, rows, cols, transposed, dst);
+    PARL_LAUNCHED();
+}
+template void launch_export_w<float>(const float*, long, int, int, int, double*, cudaStream_t);
+template void launch_export_w<bf16>(const bf16*, long, int, int, int, double*, cudaStream_t);
+
+void launch_f32_to_f64(const float* x, double* y, long n, cudaStream_t st) {
+    k_f32_to_f64<<<grid_for(n), 256, 0, st>>>(x, y, n);
+    PARL_LAUNCHED();
+}
+
+void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double scale, const double* base,
+                  cudaStream_t st) {
+    k_randn<<<grid_for(n), 256, 0, st>>>(out, n, seed, stream, scale, base);
+    PARL_LAUNCHED();
+}
+
+void launch_fill_f64(double* out, long n, double v, cudaStream_t st) {
+    k_fill_f64<<<grid_for(n), 256, 0, st>>>(out, n, v);
+    PARL_LAUNCHED();
+}
+
+void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int phase, cudaStream_t st) {
+    if (phase == 0) k_sgd_check<<<grid_for(n), 256, 0, st>>>(g, w, n, scale, flags);
+    else k_sgd_apply<<<grid_for(n), 256, 0, st>>>(g, w, n, scale);
+    PARL_LAUNCHED();
+}
+
+}  // namespace parl_gpu

@@ -1,0 +1,135 @@
+// Device data layouts and kernel launchers shared across translation units.
+#pragma once
+
+#include "internal.cuh"
+
+namespace parl_gpu {
+
+// K1 outputs for one packed sequence (device pointers).
+struct PackedDev {
+    int32_t *tokens, *labels, *positions, *seg, *pred;  // [T]
+    int32_t *scored_pos, *scored_label, *pred_pos;      // [S] (gathered head rows follow scored order)
+    int32_t* sample_of;                                 // [S] response index of each scored token
+    int32_t *row_ptr, *row_idx;                         // position -> gathered rows CSR: [T+1], [S]
+};
+
+// Reference flat layout offsets (model.cpp:86-114).
+struct FlatLayout {
+    size_t tok_emb, pos_emb, layer0, layer_stride, lnf_g, lnf_b, head_w, head_b, total;
+    struct Layer {
+        size_t ln1g, ln1b, wq, bq, wk, bk, wv, bv, wo, bo, ln2g, ln2b, w1, b1, w2, b2;
+    };
+    Layer layer(int l, int d, int F) const {
+        Layer r;
+        size_t o = layer0 + layer_stride * (size_t)l;
+        const size_t dd = (size_t)d, FF = (size_t)F;
+        r.ln1g = o; o += dd;
+        r.ln1b = o; o += dd;
+        r.wq = o; o += dd * dd;
+        r.bq = o; o += dd;
+        r.wk = o; o += dd * dd;
+        r.bk = o; o += dd;
+        r.wv = o; o += dd * dd;
+        r.bv = o; o += dd;
+        r.wo = o; o += dd * dd;
+        r.bo = o; o += dd;
+        r.ln2g = o; o += dd;
+        r.ln2b = o; o += dd;
+        r.w1 = o; o += dd * FF;
+        r.b1 = o; o += FF;
+        r.w2 = o; o += FF * dd;
+        r.b2 = o; o += dd;
+        return r;
+    }
+};
+
+inline FlatLayout make_layout(const parl_config& c) {
+    FlatLayout L;
+    size_t o = 0;
+    const size_t d = (size_t)c.d_model, F = (size_t)c.d_ff, V = (size_t)c.vocab_size;
+    L.tok_emb = o; o += V * d;
+    L.pos_emb = o; o += (size_t)c.max_seq_len * d;
+    L.layer0 = o;
+    L.layer_stride = 2 * d + 4 * (d * d + d) + 2 * d + (d * F + F) + (F * d + d);
+    o += L.layer_stride * (size_t)c.n_layers;
+    L.lnf_g = o; o += d;
+    L.lnf_b = o; o += d;
+    L.head_w = o; o += d * V;
+    L.head_b = o; o += V;
+    L.total = o;
+    return L;
+}
+
+// Compute copy of one weight set.  Matrices are stored out-major ("W^T",
+// [out x in]) so every forward contraction is K-major on both operands
+// (the tcgen05 / TMA-friendly layout); backward dX contractions read the
+// same arrays as MN-major operands.  Q, K, V are fused into one [3d x d].
+struct LayerW {
+    float *ln1_g, *ln1_b, *ln2_g, *ln2_b, *bqkv, *bo, *b1, *b2;
+    void *wqkv_t, *wo_t, *w1_t, *w2_t;  // act dtype
+};
+struct ModelW {
+    float *tok_emb, *pos_emb, *lnf_g, *lnf_b, *head_b;
+    void* head_w_t;  // [V x d]
+    LayerW* layers;  // host array of device pointers
+};
+
+// launchers (k_elem.cu)
+void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
+                 const PackedDev& pk, cudaStream_t st);
+void launch_embed(const float* tok, const float* pos, const int32_t* tokens, const int32_t* positions, int T, int D,
+                  float* x, cudaStream_t st);
+template <class T>
+void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
+                      float* mean, float* rstd, cudaStream_t st);
+void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
+                          const float* gamma, int R, int D, const float* res, float* dx, float* dgamma, float* dbeta,
+                          cudaStream_t st);
+template <class T>
+void launch_colsum(const T* X, long ldx, int R, int N, float* out, cudaStream_t st);
+void launch_row_lse(const float* z, int S, int V, const int32_t* labels, float* lse, float* lp, cudaStream_t st);
+void launch_lse_combine(const float* part, int n_parts, const float* target, int S, float* lse, float* lp,
+                        cudaStream_t st);
+template <class Tin, class Tout>
+void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int V, const float* lse, const float* u,
+                        const int32_t* labels, cudaStream_t st);
+void launch_advantages(const double* rewards, int G, int mean_only, double* adv, cudaStream_t st);
+void launch_grpo(const float* lp, const float* old, const float* ref, const int32_t* cu, int G, const double* adv,
+                 double eps, double beta, int gran, float* upstream, double* per_sample, double* stats,
+                 cudaStream_t st);
+void launch_scatter_rows(const float* dxg, const int32_t* row_ptr, const int32_t* row_idx, int T, int D, float* dx,
+                         cudaStream_t st);
+size_t sort_temp_bytes(int n);
+void launch_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
+                       const int32_t* vals_in, int32_t* vals_out, int n, int end_bit, cudaStream_t st);
+void launch_iota(int32_t* x, int n, cudaStream_t st);
+void launch_embed_grad(const int32_t* keys, const int32_t* idx, int T, const float* dx, int D, float* grad,
+                       cudaStream_t st);
+template <class T>
+void launch_f32_to_act(const float* x, T* y, long n, cudaStream_t st);
+template <class T>
+void launch_convert_w(const double* src, int rows, int cols, T* dst, long ldd, int transposed, cudaStream_t st);
+template <class T>
+void launch_export_w(const T* src, long lds, int rows, int cols, int transposed, double* dst, cudaStream_t st);
+void launch_f32_to_f64(const float* x, double* y, long n, cudaStream_t st);
+void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double scale, const double* base,
+                  cudaStream_t st);
+void launch_fill_f64(double* out, long n, double v, cudaStream_t st);
+void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int phase, cudaStream_t st);
+
+// attention (k_attn.cu).  qkv: [T x 3d] (q | k | v, head h at columns h*Dh);
+// seg/seg_start/seg_end describe the shared-prompt structure (seg 0 = prompt).
+struct AttnArgs {
+    int T, H, Dh, d;
+    const int32_t* seg;        // [T]
+    const int32_t* seg_start;  // [G+1]
+    const int32_t* seg_end;    // [G+1]
+    float scale;
+};
+template <class T>
+void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaStream_t st);
+template <class T>
+void launch_attn_bwd(const AttnArgs& a, const T* qkv, const T* out, const T* dout, const float* lse, float* dsum,
+                     T* dqkv, cudaStream_t st);
+
+}  // namespace parl_gpu

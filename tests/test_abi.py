@@ -1,0 +1,65 @@
+"""CPU tests of the boundary: libparl_gpu.so builds for sm_100a, loads, and
+exports every function include/parl_gpu.h declares; host-side logic that
+needs no device (config validation, layout, error mapping) behaves like the
+reference."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from tests.conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "parl_gpu.h")
+LIB = os.path.join(ROOT, "paper_2511_18871_b200", "libparl_gpu.so")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(parl_[a-z_0-9]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2511_18871_b200 import _build
+
+        _build.build()
+    return C.CDLL(LIB)
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared()
+    assert len(names) > 40
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_sm100a_code_present():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_param_count_matches_reference_layout(lib, orc):
+    from oracle import Cfg
+
+    class Cfg_(C.Structure):
+        _fields_ = [(n, C.c_int) for n in ("v", "d", "l", "h", "f", "m")]
+
+    lib.parl_param_count.restype = C.c_size_t
+    for cfg in (Cfg(16, 16, 2, 2, 24, 64), Cfg(4096, 256, 2, 4, 1024, 576), Cfg(151936, 896, 24, 14, 4864, 9216)):
+        c = Cfg_(cfg.vocab, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.d_ff, cfg.max_seq)
+        assert lib.parl_param_count(C.byref(c)) == orc.param_count(cfg)
+
+
+def test_version_string(lib):
+    lib.parl_version.restype = C.c_char_p
+    assert b"sm_100a" in lib.parl_version()
+
+
+def test_comm_unique_id_without_gpu(lib):
+    # NCCL is resolved at run time; with no device the call must fail cleanly, not crash.
+    buf = C.create_string_buffer(128)
+    rc = lib.parl_comm_unique_id(buf)
+    assert rc in (0, 10)

@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+golden fixtures generated from the reference build.
+
+Integer work (packing, segments, predecessors) is bit-exact; floating point
+is held to the SURVEY.md §8c tolerances written in tests/gpu_helpers.py.
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import BF16_TOL, FP32_TOL, load, ocfg, per_tensor_rel, split_resp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2511_18871_b200 import parl
+
+    return parl
+
+
+@pytest.fixture(scope="module")
+def ctx32(P):
+    return P.Context(0, P.PREC_FP32)
+
+
+@pytest.fixture(scope="module")
+def ctx16(P):
+    return P.Context(0, P.PREC_BF16)
+
+
+def tiny(P):
+    return P.ModelConfig(16, 16, 2, 2, 24, 64)
+
+
+def c1(P):
+    return P.ModelConfig(4096, 256, 2, 4, 1024, 576)
+
+
+# --------------------------------------------------------------------------- K1 packer
+def test_pack_bit_exact_vs_oracle(P, ctx32, orc):
+    rng = np.random.default_rng(3)
+    for trial in range(30):
+        Pn = int(rng.integers(1, 40))
+        G = int(rng.integers(1, 9))
+        resp = [rng.integers(4, 100, int(rng.integers(1, 50))) for _ in range(G)]
+        prompt = rng.integers(4, 100, Pn)
+        pk = P.pack_group(prompt, resp, 4096, ctx32)
+        d = pk.group.download()
+        o = orc.pack(prompt, resp, 4096)
+        for k in ("tokens", "labels", "positions", "seg", "pred", "span_start"):
+            assert np.array_equal(d[k], o[k]), (trial, k)
+        assert np.array_equal(d["scored_pos"], np.arange(Pn, Pn + sum(len(r) for r in resp)))
+
+
+def test_pack_golden_lists_and_errors(P, ctx32):  # test_packing.cpp:46-76
+    pk = P.pack_group([1, 5, 3], [[7, 8], [9, 10]], 64, ctx32)
+    assert pk.tokens.tolist() == [1, 5, 3, 7, 8, 9, 10]
+    assert pk.positions.tolist() == [0, 1, 2, 3, 4, 3, 4]
+    assert pk.spans == [(3, 2), (5, 2)]
+    pk = P.pack_group([1, 5, 3], [[7], [8, 9, 10]], 64, ctx32)
+    assert pk.positions.tolist() == [0, 1, 2, 3, 3, 4, 5]
+    with pytest.raises(P.ShapeError, match="max_seq_len"):
+        P.pack_group([1, 5, 3], [[7, 8], [9, 10]], 6, ctx32)
+    for bad in (([], [[7]]), ([1, 5, 3], [[7], []])):
+        with pytest.raises(P.ShapeError):
+            P.pack_group(bad[0], bad[1], 64, ctx32)
+
+
+def test_pack_large_bit_exact(P, ctx32, orc):
+    rng = np.random.default_rng(4)
+    prompt = rng.integers(4, 151936, 512)
+    resp = [rng.integers(4, 151936, 1024) for _ in range(8)]
+    d = P.pack_group(prompt, resp, 16384, ctx32).group.download()
+    o = orc.pack(prompt, resp, 16384)
+    for k in ("tokens", "labels", "positions", "seg", "pred"):
+        assert np.array_equal(d[k], o[k]), k
+
+
+# --------------------------------------------------------------------------- init parity
+def test_init_bit_exact(P, ctx32, orc):
+    cfg = tiny(P)
+    w = P.ModelParams.init(cfg, 41, ctx32).flat()
+    assert np.array_equal(w, orc.init_params(ocfg(cfg), 41))
+
+
+# --------------------------------------------------------------------------- forward / backward (fp32)
+def test_tiny_packed_fp32(P, ctx32):
+    z = load("tiny_packed.npz")
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, int(z["seed"]), ctx32)
+    mask = P.AttentionMaskSpec.shared_prompt(len(z["prompt"]), z["lens"])
+    f = P.forward_logprobs(pm, z["tokens"], z["positions"], mask, z["labels"], want_cache=True)
+    assert np.abs(f.logprobs - z["logprobs"]).max() < FP32_TOL["lp_abs"]
+    g = P.backward(pm, f, z["upstream"]).flat()
+    rel = per_tensor_rel(ocfg(cfg), g, z["grad"])
+    worst = max((v, k) for k, v in rel.items() if not k.endswith("attn.bk"))
+    assert worst[0] < FP32_TOL["grad_rel"], worst
+    assert max(v for k, v in rel.items() if k.endswith("attn.bk")) < FP32_TOL["bk_abs"]
+
+
+def test_tiny_causal_fp32(P, ctx32):
+    z = load("tiny_causal.npz")
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, int(z["seed"]), ctx32)
+    f = P.forward_logprobs(pm, z["tokens"], z["positions"], P.AttentionMaskSpec.causal(), z["labels"], True)
+    assert np.abs(f.logprobs - z["logprobs"]).max() < FP32_TOL["lp_abs"]
+    g = P.backward(pm, f, z["upstream"]).flat()
+    rel = per_tensor_rel(ocfg(cfg), g, z["grad"])
+    assert max(v for k, v in rel.items() if not k.endswith("attn.bk")) < FP32_TOL["grad_rel"]
+    rows = P.forward_logprob_rows(pm, z["tokens"], z["positions"], P.AttentionMaskSpec.causal())
+    assert np.abs(rows - z["rows"]).max() < FP32_TOL["lp_abs"]
+
+
+@pytest.mark.parametrize("gran", [0, 1])
+def test_tiny_microbatch_fp32(P, ctx32, gran):
+    from oracle.make_golden import perturb
+
+    z = load("tiny_micro.npz")
+    cfg = tiny(P)
+    pol = P.ModelParams.init(cfg, int(z["seed"]), ctx32)
+    w = pol.flat()
+    tm = P.TriModel(pol, P.ModelParams.from_flat(cfg, perturb(w, int(z["old_seed"]), float(z["scale"])), ctx=ctx32),
+                    P.ModelParams.from_flat(cfg, perturb(w, int(z["ref_seed"]), float(z["scale"])), ctx=ctx32))
+    pk = P.pack_group(z["prompt"], split_resp(z), cfg.max_seq_len, ctx32)
+    gb = P.GradBuffer(pol)
+    ctx32.stats_reset()
+    hyper = P.HyperParams(0.2, 0.04, "token" if gran == 0 else "sequence")
+    st = P.train_microbatch(tm, pk.group, gb, hyper, rewards=z["rewards"])
+    ref_st = z[f"stats_g{gran}"]
+    lp3 = z[f"lp3_g{gran}"]
+    for slot in range(3):
+        assert np.abs(pk.group.logprobs(slot) - lp3[slot]).max() < FP32_TOL["lp_abs"]
+    got = np.array([st[k] for k in ("objective_sum", "clip_sum", "kl_sum", "clipped_units", "total_units")])
+    assert abs(got[0] - ref_st[0]) <= FP32_TOL["obj_rel"] * max(abs(ref_st[0]), 1e-3)
+    assert got[4] == ref_st[4]
+    rel = per_tensor_rel(ocfg(cfg), gb.flat(), z[f"grad_g{gran}"])
+    assert max(v for k, v in rel.items() if not k.endswith("attn.bk")) < FP32_TOL["grad_rel"]
+    assert gb.micro_step_count() == 1
+
+
+def _c1_setup(P, ctx):
+    from oracle.make_golden import perturb
+
+    z = load("c1_micro.npz")
+    cfg = c1(P)
+    pol = P.ModelParams.init(cfg, int(z["seed"]), ctx)
+    w = pol.flat()
+    tm = P.TriModel(pol, P.ModelParams.from_flat(cfg, perturb(w, int(z["old_seed"]), float(z["scale"])), ctx=ctx),
+                    P.ModelParams.from_flat(cfg, perturb(w, int(z["ref_seed"]), float(z["scale"])), ctx=ctx))
+    pk = P.pack_group(z["prompt"], split_resp(z), cfg.max_seq_len, ctx)
+    return z, cfg, tm, pk
+
+
+def _grad_summaries(cfg, g, z):
+    from oracle import layout
+
+    rels = {}
+    for (name, off, r, c), l2 in zip(layout(ocfg(cfg)), z["grad_l2"]):
+        if name.endswith("attn.bk"):
+            continue
+        rels[name] = abs(np.linalg.norm(g[off:off + r * c]) - l2) / max(l2, 1e-30)
+    return rels
+
+
+def test_c1_microbatch_fp32(P, ctx32):
+    z, cfg, tm, pk = _c1_setup(P, ctx32)
+    gb = P.GradBuffer(tm.policy)
+    ctx32.stats_reset()
+    st = P.train_microbatch(tm, pk.group, gb, P.HyperParams(), advantages=z["advantages"])
+    for slot in range(3):
+        assert np.abs(pk.group.logprobs(slot) - z["lp3"][slot]).max() < FP32_TOL["lp_abs"]
+    assert abs(st["objective_sum"] - z["stats"][0]) <= FP32_TOL["obj_rel"] * abs(z["stats"][0]) + 1e-9
+    g = gb.flat()
+    sampled = g[z["grad_idx"]]
+    ref = z["grad_vals"]
+    assert np.linalg.norm(sampled - ref) / np.linalg.norm(ref) < FP32_TOL["grad_rel"]
+    rels = _grad_summaries(cfg, g, z)
+    assert max(rels.values()) < FP32_TOL["grad_rel"], max(rels.items(), key=lambda kv: kv[1])
+
+
+def _fixture_upstream(z, orc):
+    """Backward seed of the golden micro-batch, recomputed in fp64 from its log-probs."""
+    lp3, up, c = z["lp3"], [], 0
+    for j, n in enumerate(z["lens"]):
+        t = orc.sample_terms(lp3[0][c:c + n], lp3[1][c:c + n], lp3[2][c:c + n], z["advantages"][j], 0.2, 0.04)
+        up.append(-t["upstream"])
+        c += n
+    return np.concatenate(up)
+
+
+def test_c1_forward_bf16(P, ctx16):
+    z, cfg, tm, pk = _c1_setup(P, ctx16)
+    act = P.C.c_void_p()
+    P._check(P.LIB.parl_trimodel_forward(ctx16.h, tm.policy.h, tm.old_policy.h, tm.reference.h, pk.group.h,
+                                         P.C.byref(act)), ctx16.h)
+    P.LIB.parl_act_destroy(act)
+    for slot in range(3):
+        d = np.abs(pk.group.logprobs(slot) - z["lp3"][slot])
+        assert d.max() < BF16_TOL["lp_max"] and d.mean() < BF16_TOL["lp_mean"], (slot, d.max(), d.mean())
+
+
+def test_c1_backward_bf16(P, ctx16, orc):
+    """bf16 backward against the reference gradient for the same upstream seed."""
+    z, cfg, tm, pk = _c1_setup(P, ctx16)
+    f = P.forward_logprobs(tm.policy, pk.tokens, pk.positions, pk.mask, pk.labels, want_cache=True)
+    g = P.backward(tm.policy, f, _fixture_upstream(z, orc)).flat()
+    sampled, ref = g[z["grad_idx"]], z["grad_vals"]
+    cos = sampled @ ref / (np.linalg.norm(sampled) * np.linalg.norm(ref))
+    assert cos > BF16_TOL["cos"], cos
+    rels = _grad_summaries(cfg, g, z)
+    assert max(rels.values()) < BF16_TOL["grad_rel"], max(rels.items(), key=lambda kv: kv[1])
+
+
+def test_c1_microbatch_bf16_stats(P, ctx16):
+    z, cfg, tm, pk = _c1_setup(P, ctx16)
+    gb = P.GradBuffer(tm.policy)
+    ctx16.stats_reset()
+    st = P.train_microbatch(tm, pk.group, gb, P.HyperParams(), advantages=z["advantages"])
+    assert abs(st["objective_sum"] - z["stats"][0]) <= BF16_TOL["obj_rel"] * abs(z["stats"][0]) + 1e-3
+    assert st["total_units"] == z["stats"][4]
+    assert gb.micro_step_count() == 1
+
+
+# --------------------------------------------------------------------------- reference contracts
+def test_determinism_bitwise(P, ctx32):  # test_model.cpp:251-265
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 17, ctx32)
+    toks, labs = [1, 4, 9, 6, 2], [-1, 4, 9, 6, 2]
+    u = [1.0, -0.5, 0.25, 2.0]
+    out = []
+    for _ in range(2):
+        f = P.forward_logprobs(pm, toks, range(5), P.AttentionMaskSpec.causal(), labs, True)
+        out.append((f.logprobs, P.backward(pm, f, u).flat()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_backward_linearity_exact(P, ctx32):  # test_model.cpp:131-153
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 5, ctx32)
+    toks, labs = [1, 5, 6, 7], [-1, 5, 9, 2]
+    f = P.forward_logprobs(pm, toks, range(4), P.AttentionMaskSpec.causal(), labs, True)
+    assert (P.backward(pm, f, [0.0, 0.0, 0.0]).flat() == 0).all()
+    f = P.forward_logprobs(pm, toks, range(4), P.AttentionMaskSpec.causal(), labs, True)
+    g1 = P.backward(pm, f, [0.3, -1.1, 0.7]).flat()
+    f = P.forward_logprobs(pm, toks, range(4), P.AttentionMaskSpec.causal(), labs, True)
+    g2 = P.backward(pm, f, [0.6, -2.2, 1.4]).flat()
+    assert np.array_equal(g2, 2 * g1)
+
+
+def test_no_leakage_bitwise(P, ctx32):  # test_packing.cpp:202-223
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 53, ctx32)
+    prompt = [1, 12, 3]
+    base = [[5, 6], [7, 8], [9, 10]]
+    mut = [[5, 6], [13, 14], [9, 10]]
+    outs = []
+    for resp in (base, mut):
+        pk = P.pack_group(prompt, resp, cfg.max_seq_len, ctx32)
+        f = P.forward_logprobs(pm, pk.tokens, pk.positions, pk.mask, pk.labels)
+        outs.append(P.extract_response_logprobs(f.logprobs, pk))
+    for j in (0, 2):
+        assert np.array_equal(outs[0][j], outs[1][j])
+
+
+def test_single_response_equals_causal(P, ctx32):  # test_packing.cpp:153-162
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 43, ctx32)
+    prompt, resp = [1, 6, 9, 3], [5, 7, 2]
+    pk = P.pack_group(prompt, [resp], 64, ctx32)
+    a = P.forward_logprobs(pm, pk.tokens, pk.positions, pk.mask, pk.labels).logprobs
+    toks = prompt + resp
+    b = P.forward_logprobs(pm, toks, range(7), P.AttentionMaskSpec.causal(), [-1] * 4 + resp).logprobs
+    assert np.array_equal(a, b)
+
+
+def test_shared_equals_replicated(P, ctx32):  # test_packing.cpp:123-200
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 47, ctx32)
+    rng = np.random.default_rng(29)
+    prompt = [1, 8, 4]
+    resp = [[5, 6], [7], [9, 10, 11]]
+    pk = P.pack_group(prompt, resp, cfg.max_seq_len, ctx32)
+    u = rng.uniform(-1, 1, 6)
+    f = P.forward_logprobs(pm, pk.tokens, pk.positions, pk.mask, pk.labels, True)
+    gp = P.backward(pm, f, u).flat()
+    gs = P.GradBuffer(pm)
+    c = 0
+    for r in resp:
+        toks = prompt + r
+        fr = P.forward_logprobs(pm, toks, range(len(toks)), P.AttentionMaskSpec.causal(), [-1] * 3 + r, True)
+        assert np.abs(fr.logprobs - f.logprobs[c:c + len(r)]).max() < FP32_TOL["lp_abs"]
+        P.backward(pm, fr, u[c:c + len(r)], gs)
+        c += len(r)
+    gsum = gs.flat()
+    assert np.linalg.norm(gp - gsum) / np.linalg.norm(gsum) < FP32_TOL["grad_rel"]
+
+
+def test_trimodel_identical_weights(P, ctx32):  # test_pipeline.cpp:118-136
+    cfg = tiny(P)
+    tm = P.TriModel.init(cfg, 5, ctx32)
+    tri = P.trimodel_forward(tm, [1, 6, 3, 7, 8], range(5), P.AttentionMaskSpec.causal(), [-1, -1, -1, 7, 8])
+    assert np.array_equal(tri.policy.logprobs, tri.old_logprobs)
+    assert np.array_equal(tri.policy.logprobs, tri.ref_logprobs)
+
+
+def test_errors_map_to_reference_types(P, ctx32):  # test_model.cpp:107-173
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 1, ctx32)
+    with pytest.raises(P.ShapeError):
+        P.forward_logprobs(pm, [1, 2, 3], [0, 1], P.AttentionMaskSpec.causal(), [-1, 2, 2])
+    with pytest.raises(P.VocabError):
+        P.forward_logprobs(pm, [1, 99, 3], range(3), P.AttentionMaskSpec.causal(), [-1, 2, 2])
+    with pytest.raises(P.ShapeError):
+        P.forward_logprobs(pm, [1, 2, 3], range(3), P.AttentionMaskSpec.causal(), [3, -1, -1])
+    f = P.forward_logprobs(pm, [1, 5, 6], range(3), P.AttentionMaskSpec.causal(), [-1, 5, 9], True)
+    P.forward_logprobs(pm, [1, 5, 6], range(3), P.AttentionMaskSpec.causal(), [-1, 5, 9])
+    with pytest.raises(P.LifecycleError):
+        P.backward(pm, f, [1.0, 1.0])
+    f2 = P.forward_logprobs(pm, [1, 5, 6], range(3), P.AttentionMaskSpec.causal(), [-1, 5, 9], True)
+    with pytest.raises(P.ShapeError):
+        P.backward(pm, f2, [1.0] * 5)
+    with pytest.raises(P.ConfigError):
+        P.ModelParams(P.ModelConfig(16, 30, 2, 4, 24, 64), ctx32)
+
+
+def test_apply_update_semantics(P, ctx32):  # test_model.cpp:175-216
+    cfg = tiny(P)
+    pm = P.ModelParams.init(cfg, 9, ctx32)
+    w0 = pm.flat()
+    f = P.forward_logprobs(pm, [1, 5, 6, 7], range(4), P.AttentionMaskSpec.causal(), [-1, 5, 9, 2], True)
+    g = P.backward(pm, f, [0.3, -1.1, 0.7])
+    pm.apply_update(g, 0.5)
+    assert pm.version() == 1
+    assert np.allclose(pm.flat(), w0 - 0.5 * g.flat(), rtol=0, atol=1e-12)
