@@ -1,0 +1,24 @@
+/*
+ * parl_gpu_debug.h — test hooks of libparl_gpu.so (not part of the drop-in
+ * boundary): direct access to the contraction kernel so the tensor-core
+ * layouts and fused epilogues can be unit-tested against torch.
+ */
+#ifndef PARL_GPU_DEBUG_H
+#define PARL_GPU_DEBUG_H
+#include "parl_gpu.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C[M x N] (epilogue `epi`, see csrc/internal.cuh Epi) = sum_k A(m,k) B(n,k),
+ * A(m,k) = A[m*sam + k*sak], B(n,k) = B[n*sbn + k*sbk]; bf16 device operands.
+ * path: 0 = tcgen05 (fails with PARL_E_CONFIG if the shape is not supported),
+ *       1 = FFMA tile kernel.  Synchronises the current device. */
+parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const void* A, long sam, long sak, const void* B,
+                                 long sbn, long sbk, int epi, const float* bias, float* Cf, long ldc,
+                                 const float* resid, void* Ca, long ldca, void* Caux, const void* aux_in,
+                                 const int32_t* labels, float* part, float* target, void* logits_act,
+                                 int n_parts);
+#ifdef __cplusplus
+}
+#endif
+#endif

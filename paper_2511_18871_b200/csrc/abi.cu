@@ -139,6 +139,7 @@ struct parl_act_s {
     int T = 0, S = 0;
     DevBuf xs, xmid, a, qkv, ctxo, bn, pre, actv, stats, lse_attn;  // per-layer stacks
     DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
+    bool logits_bf16 = false;  // logits stored bf16 by the fused tcgen05 head
 };
 
 struct parl_grad_s {
@@ -416,14 +417,36 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     float* lnf_mean = act ? act->lnf_mean.as<float>(S) : c->lnf_mean.as<float>(S);
     float* lnf_rstd = act ? act->lnf_rstd.as<float>(S) : c->lnf_rstd.as<float>(S);
     float* lse_head = act ? act->lse_head.as<float>(S) : c->lse_head.as<float>(S);
-    float* logits = act ? act->logits.as<float>((size_t)S * V) : c->logits.as<float>((size_t)S * V);
     float* lp = static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T;
     if (S > 0) {
         launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, lnf_mean, lnf_rstd, st);
-        GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
-        ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
-        gemm<T>(c, ga, PARL_KC_HEAD);
-        launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
+        bool fused = false;
+        if constexpr (std::is_same_v<T, bf16>) {
+            // tcgen05 head with the vocab log-sum-exp and target gather fused
+            // into the epilogue: logits reach HBM only for the policy (bf16,
+            // kept for the backward), never for old/ref.
+            const int n_parts = (V + 255) / 256;
+            GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
+            ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
+            ga.part = c->part.as<float>((size_t)S * n_parts * 2);
+            ga.target = c->target.as<float>(S);
+            ga.n_parts = n_parts; ga.part_cols = 256;
+            ga.logits_act = act ? act->logits.as<bf16>((size_t)S * V) : nullptr;
+            ga.ldca = V;
+            {
+                ProfScope ps(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
+                fused = gemm_tc(ga, st);
+                if (fused) launch_lse_combine(ga.part, n_parts, ga.target, S, lse_head, lp, st);
+            }
+        }
+        if (!fused) {
+            float* logits = act ? act->logits.as<float>((size_t)S * V) : c->logits.as<float>((size_t)S * V);
+            GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
+            ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
+            gemm_simt<T>(ga, st);
+            launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
+        }
+        if (act) act->logits_bf16 = fused;
     }
     check_launch();
 }
@@ -443,10 +466,13 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     float* dx = c->dx.as<float>(TD);
     if (S > 0) {
         // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
-        float* logits = static_cast<float*>(act->logits.p);
         T* dz = c->dz.as<T>((size_t)S * V);
-        launch_softmax_bwd<float, T>(logits, V, dz, V, S, V, static_cast<float*>(act->lse_head.p), u,
-                                     g->pk.scored_label, st);
+        if (act->logits_bf16)
+            launch_softmax_bwd<bf16, T>(static_cast<bf16*>(act->logits.p), V, dz, V, S, V,
+                                        static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
+        else
+            launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
+                                         static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
         launch_colsum<T>(dz, V, S, V, G + L.head_b, st);
         T* hf = static_cast<T*>(act->hf.p);
         float* dhf = c->dhf.as<float>((size_t)S * D);
@@ -1404,3 +1430,25 @@ parl_status parl_stats_allreduce(parl_ctx_t ctx) {
 }
 
 }  // extern "C"
+
+// ---- test hooks (include/parl_gpu_debug.h) -------------------------------------
+#include "parl_gpu_debug.h"
+extern "C" parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const void* A, long sam, long sak,
+                                            const void* B, long sbn, long sbk, int epi, const float* bias, float* Cf,
+                                            long ldc, const float* resid, void* Ca, long ldca, void* Caux,
+                                            const void* aux_in, const int32_t* labels, float* part, float* target,
+                                            void* logits_act, int n_parts) {
+    return guarded(nullptr, [&] {
+        GemmArgs g = mk(M, N, K, A, sam, sak, B, sbn, sbk);
+        g.epi = epi; g.bias = bias; g.Cf = Cf; g.ldc = ldc; g.resid = resid; g.Ca = Ca; g.ldca = ldca;
+        g.Caux = Caux; g.aux_in = aux_in; g.labels = labels; g.part = part; g.target = target;
+        g.logits_act = logits_act; g.n_parts = n_parts; g.part_cols = 256;
+        if (path == 0) {
+            PARL_REQUIRE(gemm_tc(g, 0), PARL_E_CONFIG, "shape/layout not supported by the tcgen05 kernel");
+        } else {
+            gemm_simt<bf16>(g, 0);
+        }
+        PARL_CUDA(cudaGetLastError());
+        PARL_CUDA(cudaDeviceSynchronize());
+    });
+}

@@ -559,6 +559,8 @@ template void launch_softmax_bwd<float, bf16>(const float*, long, bf16*, long, i
                                               const int32_t*, cudaStream_t);
 template void launch_softmax_bwd<bf16, bf16>(const bf16*, long, bf16*, long, int, int, const float*, const float*,
                                              const int32_t*, cudaStream_t);
+template void launch_softmax_bwd<bf16, float>(const bf16*, long, float*, long, int, int, const float*, const float*,
+                                              const int32_t*, cudaStream_t);
 
 void launch_advantages(const double* rewards, int G, int mean_only, double* adv, cudaStream_t st) {
     k_advantages<<<1, 32, 0, st>>>(rewards, G, mean_only, adv);
