@@ -18,6 +18,17 @@ parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const void* A, l
                                  const float* resid, void* Ca, long ldca, void* Caux, const void* aux_in,
                                  const int32_t* labels, float* part, float* target, void* logits_act,
                                  int n_parts);
+/* Shared-prompt attention forward over qkv [T x 3*H*Dh] (bf16, device):
+ * out [T x H*Dh] bf16, lse [H x T]; seg/seg_start/seg_end as produced by the
+ * packer.  path 0 = tcgen05, 1 = FFMA. */
+parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
+                                 const int32_t* seg_start, const int32_t* seg_end, const void* qkv, void* out,
+                                 float* lse);
+/* Attention backward: dqkv [T x 3*H*Dh] from dout [T x H*Dh], the forward's
+ * out and lse; dsum [H x T] is scratch.  path 0 = tcgen05, 1 = FFMA. */
+parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
+                                     const int32_t* seg_start, const int32_t* seg_end, const void* qkv,
+                                     const void* out, const void* dout, const float* lse, float* dsum, void* dqkv);
 #ifdef __cplusplus
 }
 #endif

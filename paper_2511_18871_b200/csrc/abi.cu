@@ -98,6 +98,8 @@ struct parl_ctx_s {
         }
         prof_pending.clear();
     }
+    // activation handle reused by parl_train_microbatch (no per-call allocation)
+    parl_act_s* act_cache = nullptr;
     // lifetime: objects created on this context keep it alive
     int refs = 0;
     bool closing = false;
@@ -153,6 +155,7 @@ struct parl_grad_s {
 static void ctx_release(parl_ctx_s* ctx) {
     if (--ctx->refs > 0 || !ctx->closing) return;
     cudaStreamSynchronize(ctx->st);
+    delete ctx->act_cache;
     cudaStreamDestroy(ctx->st);
     delete ctx;
 }
@@ -368,8 +371,12 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
     aa.seg_end = aa.seg_start + (g->max_G + 1);
     aa.scale = 1.0f / std::sqrt((float)Dh);
+    aa.Peff = g->Peff;
 
-    launch_embed(m->W.tok_emb, m->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(0), st);
+    {
+        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12);
+        launch_embed(m->W.tok_emb, m->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(0), st);
+    }
     for (int l = 0; l < NL; ++l) {
         const LayerW& w = m->layers[l];
         float* xin = xin_of(l);
@@ -384,7 +391,10 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
         float* st4 = stats + lay((size_t)4 * Tn, l);
         float* la = lse_attn + lay((size_t)H * Tn, l);
 
-        launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, st4, st4 + Tn, st);
+        {
+            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
+            launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, st4, st4 + Tn, st);
+        }
         {  // fused Q|K|V projection (model.cpp:464-466)
             GemmArgs ga = mk(Tn, 3 * D, D, al, D, 1, w.wqkv_t, D, 1);
             ga.epi = EPI_ACT; ga.bias = w.bqkv; ga.Ca = ql; ga.ldca = 3 * D;
@@ -392,14 +402,19 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
         }
         {
             ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D);
-            launch_attn_fwd<T>(aa, ql, cl, la, st);
+            bool done = false;
+            if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
+            if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
         }
         {  // O projection + residual (model.cpp:504-506)
             GemmArgs ga = mk(Tn, D, D, cl, D, 1, w.wo_t, D, 1);
             ga.epi = EPI_RESID; ga.bias = w.bo; ga.resid = xin; ga.Cf = xm; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, st4 + 2 * Tn, st4 + 3 * Tn, st);
+        {
+            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
+            launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, st4 + 2 * Tn, st4 + 3 * Tn, st);
+        }
         {  // W1 + bias + GELU (model.cpp:509-511)
             GemmArgs ga = mk(Tn, F, D, bl, D, 1, w.w1_t, D, 1);
             ga.epi = EPI_GELU; ga.bias = w.b1; ga.Ca = pl; ga.Caux = vl; ga.ldca = F;
@@ -473,7 +488,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         else
             launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
                                          static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
-        launch_colsum<T>(dz, V, S, V, G + L.head_b, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dz, V, S, V, G + L.head_b, st); }
         T* hf = static_cast<T*>(act->hf.p);
         float* dhf = c->dhf.as<float>((size_t)S * D);
         {  // dH = dZ W_head^T (model.cpp:654-666)
@@ -492,7 +507,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         launch_layernorm_bwd(dhf, xfin, g->pk.pred_pos, static_cast<float*>(act->lnf_mean.p),
                              static_cast<float*>(act->lnf_rstd.p), m->W.lnf_g, S, D, nullptr, dxg, G + L.lnf_g,
                              G + L.lnf_b, st);
-        launch_scatter_rows(dxg, g->pk.row_ptr, g->pk.row_idx, Tn, D, dx, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_scatter_rows(dxg, g->pk.row_ptr, g->pk.row_idx, Tn, D, dx, st); }
     } else {
         PARL_CUDA(cudaMemsetAsync(dx, 0, TD * sizeof(float), st));
     }
@@ -514,6 +529,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
     aa.seg_end = aa.seg_start + (g->max_G + 1);
     aa.scale = 1.0f / std::sqrt((float)Dh);
+    aa.Peff = g->Peff;
 
     for (int l = NL - 1; l >= 0; --l) {
         const LayerW& w = m->layers[l];
@@ -530,7 +546,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         float* la = static_cast<float*>(act->lse_attn.p) + (size_t)H * Tn * l;
 
         // FFN (model.cpp:688-727)
-        launch_f32_to_act<T>(dx, dx_act, TD, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_f32_to_act<T>(dx, dx_act, TD, st); }
         {
             GemmArgs ga = mk(Tn, F, D, dx_act, D, 1, w.w2_t, 1, F);
             ga.epi = EPI_GELU_BWD; ga.aux_in = pl; ga.Ca = dpre; ga.ldca = F;
@@ -541,7 +557,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w2; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        launch_colsum<float>(dx, D, Tn, D, G + o.b2, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<float>(dx, D, Tn, D, G + o.b2, st); }
         {
             GemmArgs ga = mk(Tn, D, F, dpre, F, 1, w.w1_t, 1, D);
             ga.epi = EPI_F32; ga.Cf = dbn; ga.ldc = D;
@@ -552,12 +568,12 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w1; ga.ldc = F;
             gemm<T>(c, ga);
         }
-        launch_colsum<T>(dpre, F, Tn, F, G + o.b1, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dpre, F, Tn, F, G + o.b1, st); }
         // LN2 (model.cpp:729-730)
         launch_layernorm_bwd(dbn, xm, nullptr, st4 + 2 * Tn, st4 + 3 * Tn, w.ln2_g, Tn, D, dx, dmid, G + o.ln2g,
                              G + o.ln2b, st);
         // O projection (model.cpp:733-749)
-        launch_f32_to_act<T>(dmid, dmid_act, TD, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_f32_to_act<T>(dmid, dmid_act, TD, st); }
         {
             GemmArgs ga = mk(Tn, D, D, dmid_act, D, 1, w.wo_t, 1, D);
             ga.epi = EPI_ACT; ga.Ca = dctx; ga.ldca = D;
@@ -568,11 +584,16 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.wo; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        launch_colsum<float>(dmid, D, Tn, D, G + o.bo, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<float>(dmid, D, Tn, D, G + o.bo, st); }
         // attention (model.cpp:752-786)
         {
             ProfScope ps(c, PARL_KC_ATTN_BWD, 10.0 * g->pairs * D);
-            launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
+            bool done = false;
+            if constexpr (std::is_same_v<T, bf16>) {
+                launch_attn_dsum<T>(aa, cl, dctx, dsum, st);
+                done = attn_bwd_tc(aa, ql, dctx, la, dsum, dqkv, st);
+            }
+            if (!done) launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
         }
         // Q/K/V projections (model.cpp:789-817)
         {
@@ -585,10 +606,10 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             GemmArgs ga = mk(D, D, Tn, al, 1, D, dqkv + (size_t)p * D, 1, 3 * D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + woff[p]; ga.ldc = D;
             gemm<T>(c, ga);
-            launch_colsum<T>(dqkv + (size_t)p * D, 3 * D, Tn, D, G + boff[p], st);
+            { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dqkv + (size_t)p * D, 3 * D, Tn, D, G + boff[p], st); }
         }
         // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da)
-        launch_layernorm_bwd(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, G + o.ln1g, G + o.ln1b, st);
+        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_layernorm_bwd(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, G + o.ln1g, G + o.ln1b, st); }
         std::swap(dx, dx2);
     }
     // embeddings (model.cpp:826-834), deterministic segmented sums
@@ -1333,12 +1354,13 @@ parl_status parl_grad_download(parl_grad_t gr, double* flat, size_t n) {
 parl_status parl_train_microbatch(parl_ctx_t ctx, parl_model_t pol, parl_model_t old, parl_model_t ref,
                                   parl_group_t g, const double* rewards, const double* advantages,
                                   const parl_hyper* hp, parl_grad_t gr, parl_loss_stats* stats_out) {
-    // Pipeline::train_microbatch shared-prompt branch (pipeline.cpp:97-141)
-    parl_act_t act = nullptr;
+    // Pipeline::train_microbatch shared-prompt branch (pipeline.cpp:97-141).
+    // The activation handle is context-owned and reused across micro-batches.
+    parl_act_t act = ctx->act_cache;
     parl_status s = parl_trimodel_forward(ctx, pol, old, ref, g, &act);
+    ctx->act_cache = act;
     if (s == PARL_OK) s = parl_grpo_loss(ctx, g, rewards, advantages, hp, stats_out);
     if (s == PARL_OK) s = parl_backward(ctx, pol, act, g, gr);
-    delete act;
     return s;
 }
 
@@ -1447,6 +1469,48 @@ extern "C" parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const
             PARL_REQUIRE(gemm_tc(g, 0), PARL_E_CONFIG, "shape/layout not supported by the tcgen05 kernel");
         } else {
             gemm_simt<bf16>(g, 0);
+        }
+        PARL_CUDA(cudaGetLastError());
+        PARL_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
+                                            const int32_t* seg_start, const int32_t* seg_end, const void* qkv,
+                                            void* out, float* lse) {
+    return guarded(nullptr, [&] {
+        AttnArgs aa;
+        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
+        aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
+        aa.scale = 1.0f / std::sqrt((float)Dh);
+        if (path == 0) {
+            PARL_REQUIRE(attn_fwd_tc(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0), PARL_E_CONFIG,
+                         "head dim not supported by the tcgen05 attention");
+        } else {
+            launch_attn_fwd<bf16>(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0);
+        }
+        PARL_CUDA(cudaGetLastError());
+        PARL_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
+                                                const int32_t* seg_start, const int32_t* seg_end, const void* qkv,
+                                                const void* out, const void* dout, const float* lse, float* dsum,
+                                                void* dqkv) {
+    return guarded(nullptr, [&] {
+        AttnArgs aa;
+        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
+        aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
+        aa.scale = 1.0f / std::sqrt((float)Dh);
+        const bf16* q = static_cast<const bf16*>(qkv);
+        if (path == 0) {
+            launch_attn_dsum<bf16>(aa, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), dsum, 0);
+            PARL_REQUIRE(attn_bwd_tc(aa, q, static_cast<const bf16*>(dout), lse, dsum, static_cast<bf16*>(dqkv), 0),
+                         PARL_E_CONFIG, "head dim not supported by the tcgen05 attention");
+        } else {
+            launch_attn_bwd<bf16>(aa, q, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), lse, dsum,
+                                  static_cast<bf16*>(dqkv), 0);
         }
         PARL_CUDA(cudaGetLastError());
         PARL_CUDA(cudaDeviceSynchronize());

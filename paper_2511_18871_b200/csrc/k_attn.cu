@@ -243,11 +243,19 @@ void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaSt
 }
 
 template <class T>
-void launch_attn_bwd(const AttnArgs& a, const T* qkv, const T* out, const T* dout, const float* lse, float* dsum,
-                     T* dqkv, cudaStream_t st) {
+void launch_attn_dsum(const AttnArgs& a, const T* out, const T* dout, float* dsum, cudaStream_t st) {
     const long warps = (long)a.T * a.H;
     k_attn_dsum<T><<<cdiv(warps * 32, 256), 256, 0, st>>>(a, out, dout, dsum);
     PARL_LAUNCHED();
+}
+template void launch_attn_dsum<float>(const AttnArgs&, const float*, const float*, float*, cudaStream_t);
+template void launch_attn_dsum<bf16>(const AttnArgs&, const bf16*, const bf16*, float*, cudaStream_t);
+
+template <class T>
+void launch_attn_bwd(const AttnArgs& a, const T* qkv, const T* out, const T* dout, const float* lse, float* dsum,
+                     T* dqkv, cudaStream_t st) {
+    const long warps = (long)a.T * a.H;
+    launch_attn_dsum<T>(a, out, dout, dsum, st);
     const size_t sm = WPB * 2 * a.Dh * sizeof(float);
     k_attn_bwd_dq<T><<<cdiv(warps, WPB), WPB * 32, sm, st>>>(a, qkv, dout, lse, dsum, dqkv);
     PARL_LAUNCHED();

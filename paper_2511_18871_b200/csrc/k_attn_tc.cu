@@ -1,0 +1,890 @@
+// tcgen05 varlen shared-prompt attention (bf16 in, fp32 accumulate).
+//
+// Forward: one CTA per (128-row query tile, head).  Replaces the attention
+// loops of run_forward (proj/src/model.cpp:468-501) under the shared-prompt
+// rule of model.cpp:242-245:
+//   warp 0      TMA: Q once, then K/V tiles into a 2-stage ring
+//   warp 1      MMA: S_j = Q K_j^T into a double-buffered TMEM S, then
+//               O += P_j V_j (P from smem, V as an MN-major operand)
+//   warps 2..5  softmax, thread = query row: S row from TMEM, online max in
+//               the log2 domain, P = exp2(S - m) to smem (SW128 K-major,
+//               the A operand of the PV MMA); O is rescaled in TMEM only when
+//               a row's max grows by more than 2^8 (exact: every P and O term
+//               uses the same stale max, normalised at the end)
+// Key tiles are visited only when some row of the query tile can see them;
+// response-to-response tiles of different responses are skipped, and only
+// tiles straddling a boundary apply the per-element mask.  The forward saves
+// only the row log-sum-exp.
+#include <cudaTypedefs.h>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "tc_util.cuh"
+
+namespace parl_gpu {
+
+namespace {
+
+constexpr int TQ = 128, TK = 128;
+constexpr int NTHR = 192;  // 6 warps
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct AttnTcArgs {
+    int T, H, Dh, d, Peff;
+    const int32_t* seg;
+    float scale_log2;  // scale * log2(e)
+    bf16* out;         // [T x d]
+    float* lse;        // [H x T] natural log
+};
+
+template <int DH>
+struct AttnSmem {
+    static constexpr int Q_BYTES = TQ * DH * 2;
+    static constexpr int KV_BYTES = TK * DH * 2;
+    static constexpr int P_BYTES = TQ * TK * 2;
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = OFF_Q + Q_BYTES;              // 2 stages
+    static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;         // 2 stages
+    static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
+    static constexpr int OFF_SEG = OFF_P + P_BYTES;            // 128 ints (key segments)
+    static constexpr int OFF_BAR = OFF_SEG + TK * 4;
+    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+// Does any row of query tile [i0,i1) see a key of tile [j0,j1)?  (superset test)
+__device__ __forceinline__ bool tile_visible(const AttnTcArgs& a, int i0, int i1, int j0, int j1) {
+    if (j0 > i1 - 1) return false;
+    if (j0 < a.Peff) return true;  // prompt keys: every response row, and prompt rows i >= j0
+    const int sq_lo = a.seg[i0], sq_hi = a.seg[i1 - 1];
+    const int sk_lo = a.seg[j0], sk_hi = a.seg[j1 - 1];
+    return sq_hi >= 1 && max(sq_lo, sk_lo) <= min(sq_hi, sk_hi);
+}
+
+// Are all (row, key) pairs of the tile allowed (no mask needed)?
+__device__ __forceinline__ bool tile_full(const AttnTcArgs& a, int i0, int i1, int j0) {
+    const int j1 = j0 + TK;
+    if (j1 > a.T || i1 - i0 < TQ) return false;
+    if (j1 <= a.Peff) return a.seg[i0] >= 1 || j1 - 1 <= i0;
+    const int s = a.seg[j0];
+    return s >= 1 && a.seg[j1 - 1] == s && a.seg[i0] == s && a.seg[i1 - 1] == s && j1 - 1 <= i0;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, AttnTcArgs a) {
+    using L = AttnSmem<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* kv_full = bar + 1;   // [2]
+    uint64_t* kv_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;    // [2]
+    uint64_t* p_full = bar + 7;
+    uint64_t* o_done = bar + 8;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 9);
+    int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x, h = blockIdx.y;
+    const int i0 = qt * TQ, i1 = min(a.T, i0 + TQ);
+    const int last_kt = (i1 - 1) / TK;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&kv_full[s], 1);
+            tc::mbar_init(&kv_empty[s], 1);
+            tc::mbar_init(&s_full[s], 1);
+        }
+        tc::mbar_init(p_full, 128);
+        tc::mbar_init(o_done, 1);
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tm_qkv);
+    }
+    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+    const uint32_t t_s0 = tbase, t_o = tbase + 256;  // S buffers at cols 0/128, O at 256
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA
+            tc::mbar_expect_tx(q_full, L::Q_BYTES);
+#pragma unroll
+            for (int r = 0; r < DH / 64; ++r)
+                tc::tma_load_2d(smem + L::OFF_Q + r * TQ * 128, &tm_qkv, q_full, h * DH + r * 64, i0);
+            int n = 0;
+            for (int kt = 0; kt <= last_kt; ++kt) {
+                const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
+                if (!tile_visible(a, i0, i1, j0, j1)) continue;
+                const int st = n & 1;
+                tc::mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
+                uint8_t* kb = smem + L::OFF_K + st * L::KV_BYTES;
+                uint8_t* vb = smem + L::OFF_V + st * L::KV_BYTES;
+#pragma unroll
+                for (int r = 0; r < DH / 64; ++r) {
+                    tc::tma_load_2d(kb + r * TK * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, j0);
+                    tc::tma_load_2d(vb + r * TK * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, j0);
+                }
+                ++n;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA
+            constexpr uint32_t id_s = tc::idesc_bf16(TQ, TK, 0, 0);
+            constexpr uint32_t id_o = tc::idesc_bf16(TQ, DH, 0, 1);
+            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q);
+            const uint32_t sp = tc::smem_u32(smem + L::OFF_P);
+            // collect the visible tiles (same rule as the producer)
+            int n_tiles = 0;
+            for (int kt = 0; kt <= last_kt; ++kt) {
+                const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
+                if (tile_visible(a, i0, i1, j0, j1)) ++n_tiles;
+            }
+            tc::mbar_wait(q_full, 0);
+            auto issue_s = [&](int n) {
+                const int st = n & 1;
+                tc::mbar_wait(&kv_full[st], (n >> 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::KV_BYTES);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_s0 + (n & 1) * TK, tc::sdesc(sq + off, 16, 1024),
+                                 tc::sdesc(sk + (ks >> 2) * (TK * 128) + (ks & 3) * 32, 16, 1024), id_s, ks > 0);
+                }
+                tc::mma_commit(&s_full[n & 1]);
+            };
+            if (n_tiles > 0) issue_s(0);
+            for (int n = 0; n < n_tiles; ++n) {
+                if (n + 1 < n_tiles) issue_s(n + 1);
+                tc::mbar_wait(p_full, n & 1);
+                tc::tc_fence_after();
+                const int st = n & 1;
+                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::KV_BYTES);
+#pragma unroll
+                for (int ks = 0; ks < TK / 16; ++ks) {
+                    const uint32_t pa = sp + (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_o, tc::sdesc(pa, 16, 1024), tc::sdesc(sv + ks * 2048, TK * 128, 1024), id_o,
+                                 (n > 0 || ks > 0) ? 1u : 0u);
+                }
+                tc::mma_commit(o_done);
+                tc::mma_commit(&kv_empty[st]);
+            }
+        }
+    } else {
+        // ---------------- softmax: warps 2..5 -> TMEM lane quarter (warp % 4)
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;  // tile row
+        const int i = i0 + r;
+        const bool row_ok = i < a.T;
+        const int seg_i = row_ok ? a.seg[i] : -1;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        float m_used = -INFINITY, l = 0.f;
+        int n = 0;
+        uint8_t* P = smem + L::OFF_P;
+        for (int kt = 0; kt <= last_kt; ++kt) {
+            const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
+            if (!tile_visible(a, i0, i1, j0, j1)) continue;
+            const bool full = tile_full(a, i0, i1, j0);
+            if (!full) {
+                // key segment ids of this tile (j >= T marked -2: never visible)
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int jj = j0 + (threadIdx.x - 64);
+                kseg[threadIdx.x - 64] = jj < a.T ? a.seg[jj] : -2;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+            tc::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
+            tc::tc_fence_after();
+            float s[TK];
+#pragma unroll
+            for (int c = 0; c < TK / 32; ++c) tc::tmem_ld32(t_s0 + (n & 1) * TK + c * 32 + lane_off, s + c * 32);
+            float mx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < TK; ++j) {
+                float v = s[j] * a.scale_log2;
+                if (!full) {
+                    const int sj = kseg[j], jg = j0 + j;
+                    const bool ok = sj >= 0 && row_ok &&
+                                    (sj == 0 ? (seg_i != 0 || jg <= i) : (sj == seg_i && jg <= i));
+                    v = ok ? v : -INFINITY;
+                }
+                s[j] = v;
+                mx = fmaxf(mx, v);
+            }
+            // conditional rescale (threshold 8 in log2 units)
+            const bool need = mx > m_used + 8.f;
+            const float m_new = need ? mx : m_used;
+            const float alpha = need ? exp2f(m_used - m_new) : 1.f;  // m_used = -inf -> 0
+            const float mb = m_new == -INFINITY ? 0.f : m_new;
+            float sum = 0.f;
+            uint32_t pk[TK / 2];
+#pragma unroll
+            for (int j = 0; j < TK; j += 2) {
+                const float p0 = exp2f(s[j] - mb), p1 = exp2f(s[j + 1] - mb);
+                sum += p0 + p1;
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                pk[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            // PV of the previous tile must be done: P smem is reused, O is rescaled
+            if (n > 0) {
+                tc::mbar_wait(o_done, (n - 1) & 1);
+                tc::tc_fence_after();
+                if (__any_sync(0xffffffffu, need) && n > 0) {
+#pragma unroll
+                    for (int c = 0; c < DH / 32; ++c) {
+                        float o[32];
+                        tc::tmem_ld32(t_o + c * 32 + lane_off, o);
+                        uint32_t w[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) w[q] = __float_as_uint(o[q] * alpha);
+                        tc::tmem_st16(t_o + c * 32 + lane_off, w);
+                        tc::tmem_st16(t_o + c * 32 + 16 + lane_off, w + 16);
+                    }
+                    tc::tmem_st_wait();
+                }
+            }
+            l = l * alpha + sum;
+            m_used = m_new;
+            // P row r -> SW128 K-major tile: 64-key atom columns of [128 rows x 128 B]
+#pragma unroll
+            for (int c = 0; c < TK / 8; ++c) {
+                const int atom = c >> 3, chunk = c & 7;
+                uint8_t* dst = P + atom * (TQ * 128) + r * 128 + ((chunk ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc::tc_fence_before();
+            tc::mbar_arrive(p_full);
+            ++n;
+        }
+        // epilogue: O / l -> out (bf16), lse
+        if (n > 0) {
+            tc::mbar_wait(o_done, (n - 1) & 1);
+            tc::tc_fence_after();
+        }
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+            float o[32];
+            tc::tmem_ld32(t_o + c * 32 + lane_off, o);
+            if (row_ok) {
+                bf16* dst = a.out + (long)i * a.d + h * DH + c * 32;
+#pragma unroll
+                for (int q = 0; q < 32; q += 8) {
+                    __align__(16) bf16 t[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(o[q + e] * inv);
+                    *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
+                }
+            }
+        }
+        if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tbase);
+    }
+}
+
+// ===========================================================================
+// Backward (model.cpp:751-786 recomputed flash-style; deterministic, no atomics)
+//   k_attn_dkv_tc : CTA per (key tile, head), loops over the query tiles that
+//                   see it:  S^T = K Q^T, dP^T = V dO^T (TMEM), thread = key row:
+//                   P^T = exp2(S^T*c - lse), dS^T = P^T (dP^T - D) -> smem,
+//                   dV += P^T dO, dK += dS^T Q (TMEM accumulators)
+//   k_attn_dq_tc  : CTA per (query tile, head), loops over visible key tiles:
+//                   S = Q K^T, dP = dO V^T, dS -> smem, dQ += dS K
+struct AttnBwdArgs {
+    int T, H, Dh, d, Peff, n_qt;
+    const int32_t* seg;
+    float scale, scale_log2;
+    const float* lse;   // [H x T] natural log
+    const float* dsum;  // [H x T]
+    bf16* dqkv;         // [T x 3d]
+};
+
+__device__ __forceinline__ void write_rowtile_sw128(uint8_t* base, int r, const uint32_t* pk /*64 words*/) {
+    // one 128-element bf16 row r of a [128 x 128] K-major SW128 tile (two 64-wide atom columns)
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        const int atom = c >> 3, chunk = c & 7;
+        uint8_t* dst = base + atom * (128 * 128) + r * 128 + ((chunk ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+    }
+}
+
+// 32 bf16 columns [c0, c0+32) of row r (16 packed words) into a K-major SW128 tile
+__device__ __forceinline__ void write_row32_sw128(uint8_t* base, int r, int c0, const uint32_t* pk) {
+    const int atom = c0 >> 6, chunk0 = (c0 & 63) >> 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint8_t* dst = base + atom * (128 * 128) + r * 128 + (((chunk0 + q) ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+}
+
+template <int DH>
+struct DkvSmem {
+    static constexpr int ST = DH == 128 ? 1 : 2;
+    static constexpr int TILE = 128 * DH * 2;
+    static constexpr int OFF_K = 0, OFF_V = TILE;
+    static constexpr int OFF_Q = 2 * TILE;                 // [ST]
+    static constexpr int OFF_DO = OFF_Q + ST * TILE;       // [ST]
+    static constexpr int OFF_P = OFF_DO + ST * TILE;       // P^T  [128 x 128] bf16
+    static constexpr int OFF_DS = OFF_P + 128 * 128 * 2;   // dS^T
+    static constexpr int OFF_VEC = OFF_DS + 128 * 128 * 2; // lse*log2e, D, seg of the query tile
+    static constexpr int OFF_BAR = OFF_VEC + 3 * 128 * 4;
+    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_attn_dkv_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                  AttnBwdArgs a) {
+    using L = DkvSmem<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* kv_full = bar + 0;
+    uint64_t* q_full = bar + 1;   // [2]
+    uint64_t* q_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* p_full = bar + 6;
+    uint64_t* g_done = bar + 7;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 8);
+    float* v_lse = reinterpret_cast<float*>(smem + L::OFF_VEC);
+    float* v_d = v_lse + 128;
+    int* v_seg = reinterpret_cast<int*>(v_d + 128);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kt = blockIdx.x, h = blockIdx.y;
+    const int j0 = kt * 128, j1 = min(a.T, j0 + 128);
+    AttnTcArgs va;  // visibility helpers reuse the forward's rules
+    va.T = a.T; va.Peff = a.Peff; va.seg = a.seg;
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(kv_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&q_full[s], 1);
+            tc::mbar_init(&q_empty[s], 1);
+        }
+        tc::mbar_init(s_full, 1);
+        tc::mbar_init(p_full, 128);
+        tc::mbar_init(g_done, 1);
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tm_qkv);
+        tc::tma_prefetch(&tm_do);
+    }
+    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+    const uint32_t t_s = tbase, t_dp = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + DH;
+
+    auto visible = [&](int qt) {
+        const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
+        return tile_visible(va, i0, i1, j0, j1);
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA
+            tc::mbar_expect_tx(kv_full, 2 * L::TILE);
+#pragma unroll
+            for (int r = 0; r < DH / 64; ++r) {
+                tc::tma_load_2d(smem + L::OFF_K + r * 128 * 128, &tm_qkv, kv_full, a.d + h * DH + r * 64, j0);
+                tc::tma_load_2d(smem + L::OFF_V + r * 128 * 128, &tm_qkv, kv_full, 2 * a.d + h * DH + r * 64, j0);
+            }
+            int n = 0;
+            for (int qt = kt; qt < a.n_qt; ++qt) {
+                if (!visible(qt)) continue;
+                const int st = n % L::ST;
+                tc::mbar_wait(&q_empty[st], ((n / L::ST) & 1) ^ 1);
+                tc::mbar_expect_tx(&q_full[st], 2 * L::TILE);
+                uint8_t* qb = smem + L::OFF_Q + st * L::TILE;
+                uint8_t* db = smem + L::OFF_DO + st * L::TILE;
+#pragma unroll
+                for (int r = 0; r < DH / 64; ++r) {
+                    tc::tma_load_2d(qb + r * 128 * 128, &tm_qkv, &q_full[st], h * DH + r * 64, qt * 128);
+                    tc::tma_load_2d(db + r * 128 * 128, &tm_do, &q_full[st], h * DH + r * 64, qt * 128);
+                }
+                ++n;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA
+            constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
+            constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);    // P^T dO, dS^T Q
+            const uint32_t sk = tc::smem_u32(smem + L::OFF_K), sv = tc::smem_u32(smem + L::OFF_V);
+            const uint32_t sp = tc::smem_u32(smem + L::OFF_P), sds = tc::smem_u32(smem + L::OFF_DS);
+            tc::mbar_wait(kv_full, 0);
+            // visible query tiles, in order
+            auto next_visible = [&](int qt) {
+                while (qt < a.n_qt && !visible(qt)) ++qt;
+                return qt;
+            };
+            auto issue_sdp = [&](int n) {
+                const int st = n % L::ST;
+                tc::mbar_wait(&q_full[st], (n / L::ST) & 1);
+                tc::tc_fence_after();
+                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + st * L::TILE);
+                const uint32_t sd = tc::smem_u32(smem + L::OFF_DO + st * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_s, tc::sdesc(sk + off, 16, 1024), tc::sdesc(sq + off, 16, 1024), id_s, ks > 0);
+                    tc::mma_bf16(t_dp, tc::sdesc(sv + off, 16, 1024), tc::sdesc(sd + off, 16, 1024), id_s, ks > 0);
+                }
+                tc::mma_commit(s_full);
+            };
+            auto issue_grad = [&](int n) {
+                const int st = n % L::ST;
+                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + st * L::TILE);
+                const uint32_t sd = tc::smem_u32(smem + L::OFF_DO + st * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t aoff = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_dv, tc::sdesc(sp + aoff, 16, 1024), tc::sdesc(sd + ks * 2048, 128 * 128, 1024),
+                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
+                    tc::mma_bf16(t_dk, tc::sdesc(sds + aoff, 16, 1024), tc::sdesc(sq + ks * 2048, 128 * 128, 1024),
+                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
+                }
+                tc::mma_commit(g_done);
+                tc::mma_commit(&q_empty[st]);
+            };
+            int n_tiles = 0;
+            for (int qt = next_visible(kt); qt < a.n_qt; qt = next_visible(qt + 1)) ++n_tiles;
+            if (n_tiles > 0) issue_sdp(0);
+            for (int n = 0; n < n_tiles; ++n) {
+                tc::mbar_wait(p_full, n & 1);
+                tc::tc_fence_after();
+                // with two Q/dO stages the next tile's S/dP overlaps this tile's dV/dK MMAs
+                if (L::ST == 2 && n + 1 < n_tiles) issue_sdp(n + 1);
+                issue_grad(n);
+                if (L::ST == 1 && n + 1 < n_tiles) issue_sdp(n + 1);
+            }
+        }
+    } else {
+        // element-wise: thread = key row
+        const int q4 = warp & 3, r = q4 * 32 + lane, j = j0 + r;
+        const int tid = threadIdx.x - 64;
+        const bool key_ok = j < a.T;
+        const int seg_j = key_ok ? a.seg[j] : -2;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        int n = 0;
+        for (int qt = kt; qt < a.n_qt; ++qt) {
+            if (!visible(qt)) continue;
+            const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
+            const bool full = tile_full(va, i0, i1, j0) && (j1 - j0 == 128);
+            // per-query vectors of this tile (loads overlap the S/dP MMAs)
+            const int iq = i0 + tid;
+            const float lq = iq < a.T ? a.lse[(long)h * a.T + iq] * LOG2E : 0.f;
+            const float dq = iq < a.T ? a.dsum[(long)h * a.T + iq] : 0.f;
+            const int sq = iq < a.T ? a.seg[iq] : -1;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done reading the vectors
+            v_lse[tid] = lq;
+            v_d[tid] = dq;
+            v_seg[tid] = sq;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            tc::mbar_wait(s_full, n & 1);
+            tc::tc_fence_after();
+            float sv[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tc::tmem_ld32(t_s + c * 32 + lane_off, sv + c * 32);
+            uint32_t pk[64];
+#pragma unroll
+            for (int c = 0; c < 128; c += 2) {
+                float p2[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int cc = c + e, i = i0 + cc;
+                    float p = exp2f(sv[cc] * a.scale_log2 - v_lse[cc]);
+                    if (!full) {
+                        const int si = v_seg[cc];
+                        const bool ok = key_ok && si >= 0 &&
+                                        (seg_j == 0 ? (si != 0 || j <= i) : (si == seg_j && j <= i));
+                        p = ok ? p : 0.f;
+                    }
+                    p2[e] = p;
+                    sv[cc] = p;
+                }
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+                pk[c / 2] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            // previous tile's dV/dK MMAs must be done before P^T/dS^T are overwritten
+            if (n > 0) tc::mbar_wait(g_done, (n - 1) & 1);
+            write_rowtile_sw128(smem + L::OFF_P, r, pk);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float dp[32];
+                tc::tmem_ld32(t_dp + c * 32 + lane_off, dp);
+                uint32_t w[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const int cc = c * 32 + e;
+                    __nv_bfloat162 b2 =
+                        __floats2bfloat162_rn(sv[cc] * (dp[e] - v_d[cc]), sv[cc + 1] * (dp[e + 1] - v_d[cc + 1]));
+                    w[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                write_row32_sw128(smem + L::OFF_DS, r, c * 32, w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc::tc_fence_before();
+            tc::mbar_arrive(p_full);
+            ++n;
+        }
+        if (n > 0) {
+            tc::mbar_wait(g_done, (n - 1) & 1);
+            tc::tc_fence_after();
+        }
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {  // 0: dV, 1: dK (scaled)
+            const uint32_t src = part ? t_dk : t_dv;
+            const float mul = part ? a.scale : 1.f;
+#pragma unroll
+            for (int c = 0; c < DH / 32; ++c) {
+                float o[32];
+                tc::tmem_ld32(src + c * 32 + lane_off, o);
+                if (key_ok) {
+                    bf16* dst = a.dqkv + (long)j * 3 * a.d + (part ? a.d : 2 * a.d) + h * DH + c * 32;
+#pragma unroll
+                    for (int q = 0; q < 32; q += 8) {
+                        __align__(16) bf16 t[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(n > 0 ? o[q + e] * mul : 0.f);
+                        *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
+                    }
+                }
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tbase);
+    }
+}
+
+template <int DH>
+struct DqSmem {
+    static constexpr int ST = DH == 128 ? 1 : 2;
+    static constexpr int TILE = 128 * DH * 2;
+    static constexpr int OFF_Q = 0, OFF_DO = TILE;
+    static constexpr int OFF_K = 2 * TILE;            // [ST]
+    static constexpr int OFF_V = OFF_K + ST * TILE;   // [ST]
+    static constexpr int OFF_DS = OFF_V + ST * TILE;  // dS [128 x 128] bf16
+    static constexpr int OFF_SEG = OFF_DS + 128 * 128 * 2;
+    static constexpr int OFF_BAR = OFF_SEG + 128 * 4;
+    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(NTHR, 1)
+    k_attn_dq_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                 AttnBwdArgs a) {
+    using L = DqSmem<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* kv_full = bar + 1;   // [2]
+    uint64_t* kv_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* p_full = bar + 6;
+    uint64_t* g_done = bar + 7;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 8);
+    int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x, h = blockIdx.y;
+    const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
+    const int last_kt = (i1 - 1) / 128;
+    AttnTcArgs va;
+    va.T = a.T; va.Peff = a.Peff; va.seg = a.seg;
+    auto visible = [&](int kt) {
+        const int j0 = kt * 128, j1 = min(a.T, j0 + 128);
+        return tile_visible(va, i0, i1, j0, j1);
+    };
+
+    if (threadIdx.x == 0) {
+        tc::mbar_init(q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&kv_full[s], 1);
+            tc::mbar_init(&kv_empty[s], 1);
+        }
+        tc::mbar_init(s_full, 1);
+        tc::mbar_init(p_full, 128);
+        tc::mbar_init(g_done, 1);
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tm_qkv);
+        tc::tma_prefetch(&tm_do);
+    }
+    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+    const uint32_t t_s = tbase, t_dp = tbase + 128, t_dq = tbase + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::mbar_expect_tx(q_full, 2 * L::TILE);
+#pragma unroll
+            for (int r = 0; r < DH / 64; ++r) {
+                tc::tma_load_2d(smem + L::OFF_Q + r * 128 * 128, &tm_qkv, q_full, h * DH + r * 64, i0);
+                tc::tma_load_2d(smem + L::OFF_DO + r * 128 * 128, &tm_do, q_full, h * DH + r * 64, i0);
+            }
+            int n = 0;
+            for (int kt = 0; kt <= last_kt; ++kt) {
+                if (!visible(kt)) continue;
+                const int st = n % L::ST;
+                tc::mbar_wait(&kv_empty[st], ((n / L::ST) & 1) ^ 1);
+                tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
+                uint8_t* kb = smem + L::OFF_K + st * L::TILE;
+                uint8_t* vb = smem + L::OFF_V + st * L::TILE;
+#pragma unroll
+                for (int r = 0; r < DH / 64; ++r) {
+                    tc::tma_load_2d(kb + r * 128 * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, kt * 128);
+                    tc::tma_load_2d(vb + r * 128 * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, kt * 128);
+                }
+                ++n;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);
+            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q), sd = tc::smem_u32(smem + L::OFF_DO);
+            const uint32_t sds = tc::smem_u32(smem + L::OFF_DS);
+            tc::mbar_wait(q_full, 0);
+            auto issue_sdp = [&](int n) {
+                const int st = n % L::ST;
+                tc::mbar_wait(&kv_full[st], (n / L::ST) & 1);
+                tc::tc_fence_after();
+                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
+                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_s, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s, ks > 0);
+                    tc::mma_bf16(t_dp, tc::sdesc(sd + off, 16, 1024), tc::sdesc(sv + off, 16, 1024), id_s, ks > 0);
+                }
+                tc::mma_commit(s_full);
+            };
+            auto issue_grad = [&](int n) {
+                const int st = n % L::ST;
+                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t aoff = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_dq, tc::sdesc(sds + aoff, 16, 1024), tc::sdesc(sk + ks * 2048, 128 * 128, 1024),
+                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
+                }
+                tc::mma_commit(g_done);
+                tc::mma_commit(&kv_empty[st]);
+            };
+            int n_tiles = 0;
+            for (int kt = 0; kt <= last_kt; ++kt) n_tiles += visible(kt) ? 1 : 0;
+            if (n_tiles > 0) issue_sdp(0);
+            for (int n = 0; n < n_tiles; ++n) {
+                tc::mbar_wait(p_full, n & 1);
+                tc::tc_fence_after();
+                if (L::ST == 2 && n + 1 < n_tiles) issue_sdp(n + 1);
+                issue_grad(n);
+                if (L::ST == 1 && n + 1 < n_tiles) issue_sdp(n + 1);
+            }
+        }
+    } else {
+        const int q4 = warp & 3, r = q4 * 32 + lane, i = i0 + r;
+        const bool row_ok = i < a.T;
+        const int seg_i = row_ok ? a.seg[i] : -1;
+        const float Lr = row_ok ? a.lse[(long)h * a.T + i] * LOG2E : 0.f;
+        const float Dr = row_ok ? a.dsum[(long)h * a.T + i] : 0.f;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        int n = 0;
+        for (int kt = 0; kt <= last_kt; ++kt) {
+            if (!visible(kt)) continue;
+            const int j0 = kt * 128;
+            const bool full = tile_full(va, i0, i1, j0);
+            if (!full) {
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int jj = j0 + (threadIdx.x - 64);
+                kseg[threadIdx.x - 64] = jj < a.T ? a.seg[jj] : -2;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+            tc::mbar_wait(s_full, n & 1);
+            tc::tc_fence_after();
+            float sv[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tc::tmem_ld32(t_s + c * 32 + lane_off, sv + c * 32);
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                float p = exp2f(sv[c] * a.scale_log2 - Lr);
+                if (!full) {
+                    const int sj = kseg[c], jg = j0 + c;
+                    const bool ok = sj >= 0 && row_ok && (sj == 0 ? (seg_i != 0 || jg <= i) : (sj == seg_i && jg <= i));
+                    p = ok ? p : 0.f;
+                }
+                sv[c] = p;
+            }
+            if (n > 0) tc::mbar_wait(g_done, (n - 1) & 1);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float dp[32];
+                tc::tmem_ld32(t_dp + c * 32 + lane_off, dp);
+                uint32_t w[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const int cc = c * 32 + e;
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(sv[cc] * (dp[e] - Dr), sv[cc + 1] * (dp[e + 1] - Dr));
+                    w[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                write_row32_sw128(smem + L::OFF_DS, r, c * 32, w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc::tc_fence_before();
+            tc::mbar_arrive(p_full);
+            ++n;
+        }
+        if (n > 0) {
+            tc::mbar_wait(g_done, (n - 1) & 1);
+            tc::tc_fence_after();
+        }
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) {
+            float o[32];
+            tc::tmem_ld32(t_dq + c * 32 + lane_off, o);
+            if (row_ok) {
+                bf16* dst = a.dqkv + (long)i * 3 * a.d + h * DH + c * 32;
+#pragma unroll
+                for (int q = 0; q < 32; q += 8) {
+                    __align__(16) bf16 t[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(n > 0 ? o[q + e] * a.scale : 0.f);
+                    *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
+                }
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tbase);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int DH>
+void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
+    using L = AttnSmem<DH>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_fwd_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    dim3 grid((a.T + TQ - 1) / TQ, a.H);
+    k_attn_fwd_tc<DH><<<grid, NTHR, L::TOTAL, st>>>(m, a);
+    PARL_LAUNCHED();
+}
+
+bool make_qkv_map(CUtensorMap* m, const bf16* base, long cols, long rows) {
+    auto fn = encode();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DH>
+void launch_bwd(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwdArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_dkv_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem<DH>::TOTAL);
+        cudaFuncSetAttribute(k_attn_dq_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem<DH>::TOTAL);
+        attr = true;
+    }
+    dim3 grid(a.n_qt, a.H);
+    k_attn_dkv_tc<DH><<<grid, NTHR, DkvSmem<DH>::TOTAL, st>>>(mq, md, a);
+    PARL_LAUNCHED();
+    k_attn_dq_tc<DH><<<grid, NTHR, DqSmem<DH>::TOTAL, st>>>(mq, md, a);
+    PARL_LAUNCHED();
+}
+
+}  // namespace
+
+// dqkv <- attention backward given dO = dout [T x d], the forward's lse and
+// D = rowsum(dO * O) (dsum).  false if unsupported.
+bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* dout, const float* lse, const float* dsum,
+                 bf16* dqkv, cudaStream_t st) {
+    if (!(aa.Dh == 64 || aa.Dh == 128)) return false;
+    if (((long)aa.d * 2) % 16 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15) ||
+        (reinterpret_cast<uintptr_t>(dqkv) & 15))
+        return false;
+    CUtensorMap mq, md;
+    if (!make_qkv_map(&mq, qkv, 3L * aa.d, aa.T) || !make_qkv_map(&md, dout, aa.d, aa.T)) return false;
+    AttnBwdArgs a;
+    a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d; a.Peff = aa.Peff;
+    a.n_qt = (aa.T + 127) / 128;
+    a.seg = aa.seg;
+    a.scale = aa.scale;
+    a.scale_log2 = aa.scale * LOG2E;
+    a.lse = lse;
+    a.dsum = dsum;
+    a.dqkv = dqkv;
+    if (aa.Dh == 64) launch_bwd<64>(mq, md, a, st);
+    else launch_bwd<128>(mq, md, a, st);
+    return true;
+}
+
+// qkv: [T x 3d] bf16; returns false when the head dim / alignment is unsupported.
+bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cudaStream_t st) {
+    if (!(aa.Dh == 64 || aa.Dh == 128)) return false;
+    if (((3L * aa.d * 2) % 16) || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+        return false;
+    auto fn = encode();
+    if (!fn) return false;
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)(3 * aa.d), (cuuint64_t)aa.T};
+    cuuint64_t strides[1] = {(cuuint64_t)(3 * aa.d) * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(qkv), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    AttnTcArgs a;
+    a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
+    a.Peff = aa.Peff;
+    a.seg = aa.seg;
+    a.scale_log2 = aa.scale * LOG2E;
+    a.out = out;
+    a.lse = lse;
+    if (aa.Dh == 64) launch_fwd<64>(m, a, st);
+    else launch_fwd<128>(m, a, st);
+    return true;
+}
+
+}  // namespace parl_gpu

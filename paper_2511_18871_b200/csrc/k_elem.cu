@@ -8,6 +8,7 @@
 //   K11 embedding-grad reduce  model.cpp:825-834 (deterministic: stable sort + segmented sum)
 // plus column reductions (bias / LN parameter grads), weight conversion,
 // device init, SGD update.
+#include <algorithm>
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -130,19 +131,23 @@ __global__ void k_layernorm_bwd(const float* __restrict__ dy, const float* __res
     }
 }
 
-// Column reductions, deterministic (fixed per-thread row stripes, fixed smem tree).
-//   mode 0: out[c] += sum_r X[r][c]                          (bias grads)
-//   mode 1: out[c] += sum_r dy[r][c]*xhat[r][c], out2[c] += sum_r dy[r][c]  (LN gamma/beta)
+// Column reductions, deterministic two-stage: block (col chunk, row split)
+// sums its rows in fixed stripe order into partial[split][col]; stage 2 adds
+// the splits in order.
+//   mode 0: out[c] += sum_r X[r][c]                                      (bias grads)
+//   mode 1: out[c] += sum_r dy[r][c]*xhat[r][c], out2[c] += sum_r dy[r][c] (LN gamma/beta)
 template <class T>
-__global__ void k_colsum(const T* __restrict__ X, long ldx, int R, int N, float* __restrict__ out,
-                         const float* __restrict__ xs, const int32_t* __restrict__ rows, const float* __restrict__ mean,
-                         const float* __restrict__ rstd, float* __restrict__ out2, int mode) {
+__global__ void k_colsum_part(const T* __restrict__ X, long ldx, int R, int N, int rows_per_split,
+                              const float* __restrict__ xs, const int32_t* __restrict__ rows,
+                              const float* __restrict__ mean, const float* __restrict__ rstd, int mode,
+                              float* __restrict__ part_a, float* __restrict__ part_b) {
     __shared__ float sa[8][33], sb[8][33];
     const int c = blockIdx.x * 32 + threadIdx.x;
-    const int ty = threadIdx.y;  // 8 row stripes
+    const int ty = threadIdx.y;
+    const int r0 = blockIdx.y * rows_per_split, r1 = min(R, r0 + rows_per_split);
     float a = 0.f, b = 0.f;
     if (c < N) {
-        for (int r = ty; r < R; r += 8) {
+        for (int r = r0 + ty; r < r1; r += 8) {
             const float v = to_f<T>(X[(long)r * ldx + c]);
             if (mode == 0) {
                 a += v;
@@ -163,9 +168,53 @@ __global__ void k_colsum(const T* __restrict__ X, long ldx, int R, int N, float*
             ta += sa[i][threadIdx.x];
             tb += sb[i][threadIdx.x];
         }
-        out[c] += ta;
-        if (mode == 1) out2[c] += tb;
+        part_a[(long)blockIdx.y * N + c] = ta;
+        if (mode == 1) part_b[(long)blockIdx.y * N + c] = tb;
     }
+}
+
+__global__ void k_colsum_final(const float* __restrict__ part_a, const float* __restrict__ part_b, int splits, int N,
+                               float* __restrict__ out, float* __restrict__ out2, int mode) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    float a = 0.f, b = 0.f;
+    for (int s = 0; s < splits; ++s) {
+        a += part_a[(long)s * N + c];
+        if (mode == 1) b += part_b[(long)s * N + c];
+    }
+    out[c] += a;
+    if (mode == 1) out2[c] += b;
+}
+
+namespace {
+struct Scratch {
+    float* p = nullptr;
+    size_t n = 0;
+    float* get(size_t need) {
+        if (need > n) {
+            if (p) cudaFree(p);
+            if (cudaMalloc(&p, need * sizeof(float)) != cudaSuccess) throw Error{PARL_E_CUDA, "scratch alloc"};
+            n = need;
+        }
+        return p;
+    }
+} g_colsum_scratch;
+}  // namespace
+
+template <class T>
+static void colsum_impl(const T* X, long ldx, int R, int N, float* out, const float* xs, const int32_t* rows,
+                        const float* mean, const float* rstd, float* out2, int mode, cudaStream_t st) {
+    const int col_blocks = cdiv(N, 32);
+    int splits = std::max(1, std::min(cdiv(R, 64), cdiv(4 * 148, col_blocks)));
+    const int rps = cdiv(R, splits);
+    splits = cdiv(R, rps);
+    float* pa = g_colsum_scratch.get((size_t)2 * splits * N);
+    float* pb = pa + (size_t)splits * N;
+    k_colsum_part<T><<<dim3(col_blocks, splits), dim3(32, 8), 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd, mode,
+                                                                      pa, pb);
+    PARL_LAUNCHED();
+    k_colsum_final<<<cdiv(N, 256), 256, 0, st>>>(pa, pb, splits, N, out, out2, mode);
+    PARL_LAUNCHED();
 }
 
 // ---------------------------------------------------------------------------
@@ -232,16 +281,22 @@ __global__ void k_lse_combine(const float* __restrict__ part, int n_parts, const
 }
 
 // K8a: dZ[s, v] = u[s] * (onehot(label[s]) - exp(z[s, v] - lse[s]))   (model.cpp:637-650)
+// grid: (column chunks, rows); 8 columns per thread.
 template <class Tin, class Tout>
 __global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restrict__ dz, long lddz, int S, int V,
                               const float* __restrict__ lse, const float* __restrict__ u,
                               const int32_t* __restrict__ labels) {
-    const long n = (long)S * V;
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
-        const int s = (int)(e / V), v = (int)(e % V);
-        const float us = u[s];
-        const float p = __expf(to_f<Tin>(z[(long)s * ldz + v]) - lse[s]);
-        dz[(long)s * lddz + v] = from_f<Tout>(us * ((v == labels[s] ? 1.f : 0.f) - p));
+    const int s = blockIdx.y;
+    const float us = u[s], L = lse[s];
+    const int lab = labels[s];
+    const Tin* zr = z + (long)s * ldz;
+    Tout* dr = dz + (long)s * lddz;
+    for (int v0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8; v0 < V; v0 += gridDim.x * blockDim.x * 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int v = v0 + q;
+            if (v < V) dr[v] = from_f<Tout>(us * ((v == lab ? 1.f : 0.f) - __expf(to_f<Tin>(zr[v]) - L)));
+        }
     }
 }
 
@@ -520,15 +575,13 @@ void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, 
     if (R <= 0) return;
     k_layernorm_bwd<<<cdiv(R, 8), 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx);
     PARL_LAUNCHED();
-    k_colsum<float><<<cdiv(D, 32), dim3(32, 8), 0, st>>>(dy, D, R, D, dgamma, x, rows, mean, rstd, dbeta, 1);
-    PARL_LAUNCHED();
+    colsum_impl<float>(dy, D, R, D, dgamma, x, rows, mean, rstd, dbeta, 1, st);
 }
 
 template <class T>
 void launch_colsum(const T* X, long ldx, int R, int N, float* out, cudaStream_t st) {
     if (R <= 0) return;
-    k_colsum<T><<<cdiv(N, 32), dim3(32, 8), 0, st>>>(X, ldx, R, N, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
-    PARL_LAUNCHED();
+    colsum_impl<T>(X, ldx, R, N, out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, st);
 }
 template void launch_colsum<float>(const float*, long, int, int, float*, cudaStream_t);
 template void launch_colsum<bf16>(const bf16*, long, int, int, float*, cudaStream_t);
@@ -550,7 +603,8 @@ template <class Tin, class Tout>
 void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int V, const float* lse, const float* u,
                         const int32_t* labels, cudaStream_t st) {
     if (S <= 0) return;
-    k_softmax_bwd<Tin, Tout><<<grid_for((long)S * V), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
+    const int cx = std::max(1, std::min(cdiv(V, 256 * 8), 8));
+    k_softmax_bwd<Tin, Tout><<<dim3(cx, S), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
     PARL_LAUNCHED();
 }
 template void launch_softmax_bwd<float, float>(const float*, long, float*, long, int, int, const float*,

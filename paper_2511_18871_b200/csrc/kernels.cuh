@@ -121,13 +121,21 @@ void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int
 // seg/seg_start/seg_end describe the shared-prompt structure (seg 0 = prompt).
 struct AttnArgs {
     int T, H, Dh, d;
+    int Peff;                  // end of segment 0 (prompt length, or T when causal)
     const int32_t* seg;        // [T]
     const int32_t* seg_start;  // [G+1]
     const int32_t* seg_end;    // [G+1]
     float scale;
 };
+// tcgen05 forward (k_attn_tc.cu); false if the head dim / alignment is unsupported
+bool attn_fwd_tc(const AttnArgs& a, const bf16* qkv, bf16* out, float* lse, cudaStream_t st);
 template <class T>
 void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaStream_t st);
+// tcgen05 backward (k_attn_tc.cu): dqkv from dO, lse and D = rowsum(dO*O)
+bool attn_bwd_tc(const AttnArgs& a, const bf16* qkv, const bf16* dout, const float* lse, const float* dsum,
+                 bf16* dqkv, cudaStream_t st);
+template <class T>
+void launch_attn_dsum(const AttnArgs& a, const T* out, const T* dout, float* dsum, cudaStream_t st);
 template <class T>
 void launch_attn_bwd(const AttnArgs& a, const T* qkv, const T* out, const T* dout, const float* lse, float* dsum,
                      T* dqkv, cudaStream_t st);

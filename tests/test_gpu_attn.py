@@ -1,0 +1,109 @@
+"""GPU tests of the tcgen05 shared-prompt attention against an fp32 torch
+reference (dense allowed-pair mask from model.cpp:242-245) on the same bf16
+Q/K/V, with segment boundaries deliberately not aligned to 128-row tiles."""
+import ctypes as C
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    from paper_2511_18871_b200 import parl as P
+
+    f = P.LIB.parl_debug_attn_bf16
+    f.restype = C.c_int
+    f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 5 + [C.c_void_p]
+    return torch, P, f
+
+
+def structure(torch, P_len, lens):
+    T = P_len + sum(lens)
+    seg = torch.zeros(T, dtype=torch.int32)
+    starts, ends = [0], [P_len if lens else T]
+    t = P_len
+    for k, n in enumerate(lens):
+        seg[t:t + n] = k + 1
+        starts.append(t)
+        ends.append(t + n)
+        t += n
+    i = torch.arange(T)
+    si, sj = seg[:, None], seg[None, :]
+    allowed = torch.where(si == 0, (sj == 0) & (i[None, :] <= i[:, None]),
+                          (sj == 0) | ((sj == si) & (i[None, :] <= i[:, None])))
+    return T, seg.cuda(), torch.tensor(starts, dtype=torch.int32).cuda(), torch.tensor(
+        ends, dtype=torch.int32).cuda(), allowed.cuda()
+
+
+def reference(torch, qkv, H, Dh, allowed):
+    T = qkv.shape[0]
+    d = H * Dh
+    q = qkv[:, :d].float().view(T, H, Dh).transpose(0, 1)
+    k = qkv[:, d:2 * d].float().view(T, H, Dh).transpose(0, 1)
+    v = qkv[:, 2 * d:].float().view(T, H, Dh).transpose(0, 1)
+    s = (q @ k.transpose(1, 2)) / math.sqrt(Dh)
+    s = s.masked_fill(~allowed[None], float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ v
+    return o.transpose(0, 1).reshape(T, d), lse
+
+
+CASES = [(300, [200, 250, 260], 2, 64), (64, [128, 128, 128, 128], 3, 64), (130, [5, 300, 1, 77], 2, 128),
+         (700, [], 2, 64), (512, [1024] * 2, 1, 128)]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_attention_fwd_tc_vs_torch(env, case):
+    torch, P, f = env
+    P_len, lens, H, Dh = case
+    T, seg, starts, ends, allowed = structure(torch, P_len, lens)
+    Peff = P_len if lens else T
+    g = torch.Generator(device="cuda").manual_seed(1)
+    qkv = (torch.randn(T, 3 * H * Dh, device="cuda", generator=g) * 1.5).bfloat16()
+    ref_o, ref_lse = reference(torch, qkv, H, Dh, allowed)
+    for path in (0, 1):
+        out = torch.zeros(T, H * Dh, device="cuda", dtype=torch.bfloat16)
+        lse = torch.zeros(H, T, device="cuda")
+        rc = f(path, T, H, Dh, Peff, seg.data_ptr(), starts.data_ptr(), ends.data_ptr(), qkv.data_ptr(),
+               out.data_ptr(), lse.data_ptr())
+        assert rc == 0, P.LIB.parl_last_error(None)
+        eo = (out.float() - ref_o).abs().max().item()
+        el = (lse - ref_lse).abs().max().item()
+        assert eo < 2e-2 and el < 1e-3, (path, eo, el)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_attention_bwd_tc_vs_torch(env, case):
+    torch, P, f = env
+    fb = P.LIB.parl_debug_attn_bwd_bf16
+    fb.restype = C.c_int
+    fb.argtypes = [C.c_int] * 5 + [C.c_void_p] * 9
+    P_len, lens, H, Dh = case
+    T, seg, starts, ends, allowed = structure(torch, P_len, lens)
+    Peff = P_len if lens else T
+    d = H * Dh
+    g = torch.Generator(device="cuda").manual_seed(2)
+    qkv = (torch.randn(T, 3 * d, device="cuda", generator=g) * 1.5).bfloat16()
+    dout = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    x = qkv.float().requires_grad_(True)
+    o, _ = reference(torch, x, H, Dh, allowed)
+    (o * dout.float()).sum().backward()
+    ref = x.grad
+    out = torch.zeros(T, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(H, T, device="cuda")
+    assert f(0, T, H, Dh, Peff, seg.data_ptr(), starts.data_ptr(), ends.data_ptr(), qkv.data_ptr(), out.data_ptr(),
+             lse.data_ptr()) == 0
+    scale = ref.abs().max().item()
+    for path in (0, 1):
+        dqkv = torch.zeros(T, 3 * d, device="cuda", dtype=torch.bfloat16)
+        dsum = torch.zeros(H, T, device="cuda")
+        rc = fb(path, T, H, Dh, Peff, seg.data_ptr(), starts.data_ptr(), ends.data_ptr(), qkv.data_ptr(),
+                out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(), dqkv.data_ptr())
+        assert rc == 0, P.LIB.parl_last_error(None)
+        for name, sl in (("dq", slice(0, d)), ("dk", slice(d, 2 * d)), ("dv", slice(2 * d, 3 * d))):
+            err = (dqkv[:, sl].float() - ref[:, sl]).abs().max().item() / scale
+            assert err < 3e-2, (path, name, err)
