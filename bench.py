@@ -217,12 +217,9 @@ def run_ours(args, c):
     prec = P.PREC_BF16 if c["prec"] == "bf16" else P.PREC_FP32
     ctx = P.Context(local, prec)
     if world > 1:
-        uid = P.Context.comm_unique_id() if rank == 0 else b""
-        import torch.distributed as dist
+        from paper_2511_18871_b200.dp import bootstrap_comm
 
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.comm_init(obj[0], rank, world)
+        bootstrap_comm(ctx, rank, world)
 
     cfg = P.ModelConfig(c["vocab"], c["d"], c["L"], c["H"], c["F"], c["max_seq"])
     pol = P.ModelParams.init_device(cfg, 7, ctx)

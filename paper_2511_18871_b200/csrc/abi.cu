@@ -128,7 +128,8 @@ struct parl_group_s {
     uint64_t epoch = 0;
     PackedDev pk{};
     DevBuf ints, seg_se, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
-    DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp;
+    DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf;
+    AttnSched sched;
     uint64_t sorted_epoch = ~0ull;
     std::vector<int> lens, span_start, cu;
     int max_seq = 0, vocab = 0;
@@ -372,6 +373,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     aa.seg_end = aa.seg_start + (g->max_G + 1);
     aa.scale = 1.0f / std::sqrt((float)Dh);
     aa.Peff = g->Peff;
+    aa.sched = g->sched;
 
     {
         ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12);
@@ -530,6 +532,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     aa.seg_end = aa.seg_start + (g->max_G + 1);
     aa.scale = 1.0f / std::sqrt((float)Dh);
     aa.Peff = g->Peff;
+    aa.sched = g->sched;
 
     for (int l = NL - 1; l >= 0; --l) {
         const LayerW& w = m->layers[l];
@@ -622,6 +625,69 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     gr->micro_steps += 1;
 }
 
+// Host-side attention tile schedule (see AttnSched in kernels.cuh): the same
+// visibility rule as the shared-prompt mask (model.cpp:242-245) at tile level.
+AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const std::vector<int>& lens, DevBuf& buf,
+                         cudaStream_t st) {
+    const int nt = (T + 127) / 128;
+    auto seg_at = [&](int i) -> int {
+        if (i < Peff) return 0;
+        int k = (int)(std::upper_bound(starts.begin(), starts.end(), i) - starts.begin()) - 1;
+        return k + 1;
+    };
+    auto visible = [&](int i0, int i1, int j0, int j1) {
+        if (j0 > i1 - 1) return false;
+        if (j0 < Peff) return true;
+        const int sq_lo = seg_at(i0), sq_hi = seg_at(i1 - 1), sk_lo = seg_at(j0), sk_hi = seg_at(j1 - 1);
+        return sq_hi >= 1 && std::max(sq_lo, sk_lo) <= std::min(sq_hi, sk_hi);
+    };
+    auto full = [&](int i0, int i1, int j0) {
+        const int j1 = j0 + 128;
+        if (j1 > T || i1 - i0 < 128) return false;
+        if (j1 <= Peff) return seg_at(i0) >= 1 || j1 - 1 <= i0;
+        const int s = seg_at(j0);
+        return s >= 1 && seg_at(j1 - 1) == s && seg_at(i0) == s && seg_at(i1 - 1) == s && j1 - 1 <= i0;
+    };
+    std::vector<int32_t> q_ptr(nt + 1, 0), q_list, k_ptr(nt + 1, 0), k_list;
+    std::vector<std::vector<int32_t>> per_k(nt);
+    for (int qt = 0; qt < nt; ++qt) {
+        const int i0 = qt * 128, i1 = std::min(T, i0 + 128);
+        for (int kt = 0; kt <= (i1 - 1) / 128; ++kt) {
+            const int j0 = kt * 128, j1 = std::min(T, j0 + 128);
+            if (!visible(i0, i1, j0, j1)) continue;
+            const int32_t e = (full(i0, i1, j0) ? (1 << 30) : 0);
+            q_list.push_back(kt | e);
+            per_k[kt].push_back(qt | e);
+        }
+        q_ptr[qt + 1] = (int32_t)q_list.size();
+    }
+    for (int kt = 0; kt < nt; ++kt) {
+        k_list.insert(k_list.end(), per_k[kt].begin(), per_k[kt].end());
+        k_ptr[kt + 1] = (int32_t)k_list.size();
+    }
+    std::vector<int32_t> q_order(nt), k_order(nt);
+    for (int t = 0; t < nt; ++t) q_order[t] = k_order[t] = t;
+    std::stable_sort(q_order.begin(), q_order.end(),
+                     [&](int x, int y) { return q_ptr[x + 1] - q_ptr[x] > q_ptr[y + 1] - q_ptr[y]; });
+    std::stable_sort(k_order.begin(), k_order.end(),
+                     [&](int x, int y) { return k_ptr[x + 1] - k_ptr[x] > k_ptr[y + 1] - k_ptr[y]; });
+    std::vector<int32_t> all;
+    all.reserve(4 * (nt + 1) + q_list.size() + k_list.size());
+    size_t o_qp = all.size(); all.insert(all.end(), q_ptr.begin(), q_ptr.end());
+    size_t o_ql = all.size(); all.insert(all.end(), q_list.begin(), q_list.end());
+    size_t o_qo = all.size(); all.insert(all.end(), q_order.begin(), q_order.end());
+    size_t o_kp = all.size(); all.insert(all.end(), k_ptr.begin(), k_ptr.end());
+    size_t o_kl = all.size(); all.insert(all.end(), k_list.begin(), k_list.end());
+    size_t o_ko = all.size(); all.insert(all.end(), k_order.begin(), k_order.end());
+    int32_t* d = buf.as<int32_t>(all.size());
+    PARL_CUDA(cudaMemcpyAsync(d, all.data(), all.size() * 4, cudaMemcpyHostToDevice, st));
+    PARL_CUDA(cudaStreamSynchronize(st));  // host vector goes out of scope
+    AttnSched s;
+    s.q_ptr = d + o_qp; s.q_list = d + o_ql; s.q_order = d + o_qo;
+    s.k_ptr = d + o_kp; s.k_list = d + o_kl; s.k_order = d + o_ko;
+    return s;
+}
+
 void alloc_group_arrays(parl_group_s* g) {
     const int T = g->max_T, G = g->max_G;
     // tokens labels positions seg pred [T] ; scored_pos scored_label pred_pos sample_of [T];
@@ -658,6 +724,7 @@ void upload_meta(parl_group_s* g) {
     }
     PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
+    g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->ctx->st);
 }
 
 void check_pack_inputs(parl_group_s* g, int P, const int32_t* lens, int G, int max_seq) {
@@ -1483,6 +1550,31 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
         aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
         aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
         aa.scale = 1.0f / std::sqrt((float)Dh);
+        static DevBuf dbg_sched;
+        {
+            int G = 0;
+            std::vector<int32_t> st_h, en_h;
+            if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
+                G = 0;
+                std::vector<int32_t> tmp(2 * (T + 1));
+                PARL_CUDA(cudaMemcpy(tmp.data(), seg_end, 4, cudaMemcpyDeviceToHost));
+                // count responses: walk ends until T
+                std::vector<int32_t> s1(T + 1), e1(T + 1);
+                int n = 1;
+                while (true) {
+                    PARL_CUDA(cudaMemcpy(e1.data() + n - 1, seg_end + n - 1, 4, cudaMemcpyDeviceToHost));
+                    if (e1[n - 1] >= T) break;
+                    ++n;
+                }
+                PARL_CUDA(cudaMemcpy(s1.data(), seg_start, 4 * n, cudaMemcpyDeviceToHost));
+                for (int k = 1; k < n; ++k) {
+                    st_h.push_back(s1[k]);
+                    en_h.push_back(e1[k] - s1[k]);
+                }
+            }
+            std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, 0);
+        }
         if (path == 0) {
             PARL_REQUIRE(attn_fwd_tc(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0), PARL_E_CONFIG,
                          "head dim not supported by the tcgen05 attention");
@@ -1503,6 +1595,31 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
         aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
         aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
         aa.scale = 1.0f / std::sqrt((float)Dh);
+        static DevBuf dbg_sched;
+        {
+            int G = 0;
+            std::vector<int32_t> st_h, en_h;
+            if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
+                G = 0;
+                std::vector<int32_t> tmp(2 * (T + 1));
+                PARL_CUDA(cudaMemcpy(tmp.data(), seg_end, 4, cudaMemcpyDeviceToHost));
+                // count responses: walk ends until T
+                std::vector<int32_t> s1(T + 1), e1(T + 1);
+                int n = 1;
+                while (true) {
+                    PARL_CUDA(cudaMemcpy(e1.data() + n - 1, seg_end + n - 1, 4, cudaMemcpyDeviceToHost));
+                    if (e1[n - 1] >= T) break;
+                    ++n;
+                }
+                PARL_CUDA(cudaMemcpy(s1.data(), seg_start, 4 * n, cudaMemcpyDeviceToHost));
+                for (int k = 1; k < n; ++k) {
+                    st_h.push_back(s1[k]);
+                    en_h.push_back(e1[k] - s1[k]);
+                }
+            }
+            std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, 0);
+        }
         const bf16* q = static_cast<const bf16*>(qkv);
         if (path == 0) {
             launch_attn_dsum<bf16>(aa, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), dsum, 0);

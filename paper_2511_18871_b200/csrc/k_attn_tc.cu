@@ -32,6 +32,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 struct AttnTcArgs {
     int T, H, Dh, d, Peff;
     const int32_t* seg;
+    const int32_t *q_ptr, *q_list, *q_order;  // tile schedule (see build_attn_schedule)
     float scale_log2;  // scale * log2(e)
     bf16* out;         // [T x d]
     float* lse;        // [H x T] natural log
@@ -51,24 +52,6 @@ struct AttnSmem {
     static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
-// Does any row of query tile [i0,i1) see a key of tile [j0,j1)?  (superset test)
-__device__ __forceinline__ bool tile_visible(const AttnTcArgs& a, int i0, int i1, int j0, int j1) {
-    if (j0 > i1 - 1) return false;
-    if (j0 < a.Peff) return true;  // prompt keys: every response row, and prompt rows i >= j0
-    const int sq_lo = a.seg[i0], sq_hi = a.seg[i1 - 1];
-    const int sk_lo = a.seg[j0], sk_hi = a.seg[j1 - 1];
-    return sq_hi >= 1 && max(sq_lo, sk_lo) <= min(sq_hi, sk_hi);
-}
-
-// Are all (row, key) pairs of the tile allowed (no mask needed)?
-__device__ __forceinline__ bool tile_full(const AttnTcArgs& a, int i0, int i1, int j0) {
-    const int j1 = j0 + TK;
-    if (j1 > a.T || i1 - i0 < TQ) return false;
-    if (j1 <= a.Peff) return a.seg[i0] >= 1 || j1 - 1 <= i0;
-    const int s = a.seg[j0];
-    return s >= 1 && a.seg[j1 - 1] == s && a.seg[i0] == s && a.seg[i1 - 1] == s && j1 - 1 <= i0;
-}
-
 template <int DH>
 __global__ void __launch_bounds__(NTHR, 1)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, AttnTcArgs a) {
@@ -86,9 +69,8 @@ __global__ void __launch_bounds__(NTHR, 1)
     int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x, h = blockIdx.y;
-    const int i0 = qt * TQ, i1 = min(a.T, i0 + TQ);
-    const int last_kt = (i1 - 1) / TK;
+    const int qt = a.q_order[blockIdx.x], h = blockIdx.y;
+    const int i0 = qt * TQ;
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, 1);
@@ -116,9 +98,8 @@ __global__ void __launch_bounds__(NTHR, 1)
             for (int r = 0; r < DH / 64; ++r)
                 tc::tma_load_2d(smem + L::OFF_Q + r * TQ * 128, &tm_qkv, q_full, h * DH + r * 64, i0);
             int n = 0;
-            for (int kt = 0; kt <= last_kt; ++kt) {
-                const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
-                if (!tile_visible(a, i0, i1, j0, j1)) continue;
+            for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e) {
+                const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
                 const int st = n & 1;
                 tc::mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
                 tc::mbar_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
@@ -138,12 +119,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             constexpr uint32_t id_o = tc::idesc_bf16(TQ, DH, 0, 1);
             const uint32_t sq = tc::smem_u32(smem + L::OFF_Q);
             const uint32_t sp = tc::smem_u32(smem + L::OFF_P);
-            // collect the visible tiles (same rule as the producer)
-            int n_tiles = 0;
-            for (int kt = 0; kt <= last_kt; ++kt) {
-                const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
-                if (tile_visible(a, i0, i1, j0, j1)) ++n_tiles;
-            }
+            const int n_tiles = a.q_ptr[qt + 1] - a.q_ptr[qt];
             tc::mbar_wait(q_full, 0);
             auto issue_s = [&](int n) {
                 const int st = n & 1;
@@ -186,10 +162,9 @@ __global__ void __launch_bounds__(NTHR, 1)
         float m_used = -INFINITY, l = 0.f;
         int n = 0;
         uint8_t* P = smem + L::OFF_P;
-        for (int kt = 0; kt <= last_kt; ++kt) {
-            const int j0 = kt * TK, j1 = min(a.T, j0 + TK);
-            if (!tile_visible(a, i0, i1, j0, j1)) continue;
-            const bool full = tile_full(a, i0, i1, j0);
+        for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e) {
+            const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
+            const bool full = (a.q_list[e] >> 30) & 1;
             if (!full) {
                 // key segment ids of this tile (j >= T marked -2: never visible)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -200,8 +175,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             tc::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
             tc::tc_fence_after();
             float s[TK];
-#pragma unroll
-            for (int c = 0; c < TK / 32; ++c) tc::tmem_ld32(t_s0 + (n & 1) * TK + c * 32 + lane_off, s + c * 32);
+            tc::tmem_ld128(t_s0 + (n & 1) * TK + lane_off, s);
             float mx = -INFINITY;
 #pragma unroll
             for (int j = 0; j < TK; ++j) {
@@ -250,11 +224,12 @@ __global__ void __launch_bounds__(NTHR, 1)
             l = l * alpha + sum;
             m_used = m_new;
             // P row r -> SW128 K-major tile: 64-key atom columns of [128 rows x 128 B]
+            const uint32_t pbase = tc::smem_u32(P) + r * 128;
 #pragma unroll
             for (int c = 0; c < TK / 8; ++c) {
                 const int atom = c >> 3, chunk = c & 7;
-                uint8_t* dst = P + atom * (TQ * 128) + r * 128 + ((chunk ^ (r & 7)) << 4);
-                *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                tc::sts128(pbase + atom * (TQ * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                           pk[4 * c + 3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc::tc_fence_before();
@@ -303,6 +278,8 @@ __global__ void __launch_bounds__(NTHR, 1)
 struct AttnBwdArgs {
     int T, H, Dh, d, Peff, n_qt;
     const int32_t* seg;
+    const int32_t *q_ptr, *q_list, *q_order;  // per query tile: visible key tiles
+    const int32_t *k_ptr, *k_list, *k_order;  // per key tile: query tiles that see it
     float scale, scale_log2;
     const float* lse;   // [H x T] natural log
     const float* dsum;  // [H x T]
@@ -311,22 +288,22 @@ struct AttnBwdArgs {
 
 __device__ __forceinline__ void write_rowtile_sw128(uint8_t* base, int r, const uint32_t* pk /*64 words*/) {
     // one 128-element bf16 row r of a [128 x 128] K-major SW128 tile (two 64-wide atom columns)
+    const uint32_t b = tc::smem_u32(base) + r * 128;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
         const int atom = c >> 3, chunk = c & 7;
-        uint8_t* dst = base + atom * (128 * 128) + r * 128 + ((chunk ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        tc::sts128(b + atom * (128 * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                   pk[4 * c + 3]);
     }
 }
 
 // 32 bf16 columns [c0, c0+32) of row r (16 packed words) into a K-major SW128 tile
 __device__ __forceinline__ void write_row32_sw128(uint8_t* base, int r, int c0, const uint32_t* pk) {
     const int atom = c0 >> 6, chunk0 = (c0 & 63) >> 3;
+    const uint32_t b = tc::smem_u32(base) + atom * (128 * 128) + r * 128;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint8_t* dst = base + atom * (128 * 128) + r * 128 + (((chunk0 + q) ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    }
+    for (int q = 0; q < 4; ++q)
+        tc::sts128(b + (((chunk0 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
 template <int DH>
@@ -363,10 +340,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     int* v_seg = reinterpret_cast<int*>(v_d + 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kt = blockIdx.x, h = blockIdx.y;
+    const int kt = a.k_order[blockIdx.x], h = blockIdx.y;
     const int j0 = kt * 128, j1 = min(a.T, j0 + 128);
-    AttnTcArgs va;  // visibility helpers reuse the forward's rules
-    va.T = a.T; va.Peff = a.Peff; va.seg = a.seg;
+    const int e0 = a.k_ptr[kt], e1 = a.k_ptr[kt + 1];
 
     if (threadIdx.x == 0) {
         tc::mbar_init(kv_full, 1);
@@ -388,11 +364,6 @@ __global__ void __launch_bounds__(NTHR, 1)
     const uint32_t tbase = *tbase_s;
     const uint32_t t_s = tbase, t_dp = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + DH;
 
-    auto visible = [&](int qt) {
-        const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
-        return tile_visible(va, i0, i1, j0, j1);
-    };
-
     if (warp == 0) {
         if (lane == 0) {  // TMA
             tc::mbar_expect_tx(kv_full, 2 * L::TILE);
@@ -402,8 +373,8 @@ __global__ void __launch_bounds__(NTHR, 1)
                 tc::tma_load_2d(smem + L::OFF_V + r * 128 * 128, &tm_qkv, kv_full, 2 * a.d + h * DH + r * 64, j0);
             }
             int n = 0;
-            for (int qt = kt; qt < a.n_qt; ++qt) {
-                if (!visible(qt)) continue;
+            for (int e = e0; e < e1; ++e) {
+                const int qt = a.k_list[e] & 0x3fffffff;
                 const int st = n % L::ST;
                 tc::mbar_wait(&q_empty[st], ((n / L::ST) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[st], 2 * L::TILE);
@@ -424,11 +395,6 @@ __global__ void __launch_bounds__(NTHR, 1)
             const uint32_t sk = tc::smem_u32(smem + L::OFF_K), sv = tc::smem_u32(smem + L::OFF_V);
             const uint32_t sp = tc::smem_u32(smem + L::OFF_P), sds = tc::smem_u32(smem + L::OFF_DS);
             tc::mbar_wait(kv_full, 0);
-            // visible query tiles, in order
-            auto next_visible = [&](int qt) {
-                while (qt < a.n_qt && !visible(qt)) ++qt;
-                return qt;
-            };
             auto issue_sdp = [&](int n) {
                 const int st = n % L::ST;
                 tc::mbar_wait(&q_full[st], (n / L::ST) & 1);
@@ -458,8 +424,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 tc::mma_commit(g_done);
                 tc::mma_commit(&q_empty[st]);
             };
-            int n_tiles = 0;
-            for (int qt = next_visible(kt); qt < a.n_qt; qt = next_visible(qt + 1)) ++n_tiles;
+            const int n_tiles = e1 - e0;
             if (n_tiles > 0) issue_sdp(0);
             for (int n = 0; n < n_tiles; ++n) {
                 tc::mbar_wait(p_full, n & 1);
@@ -478,10 +443,10 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int seg_j = key_ok ? a.seg[j] : -2;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         int n = 0;
-        for (int qt = kt; qt < a.n_qt; ++qt) {
-            if (!visible(qt)) continue;
-            const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
-            const bool full = tile_full(va, i0, i1, j0) && (j1 - j0 == 128);
+        for (int e = e0; e < e1; ++e) {
+            const int qt = a.k_list[e] & 0x3fffffff;
+            const int i0 = qt * 128;
+            const bool full = (a.k_list[e] >> 30) & 1;
             // per-query vectors of this tile (loads overlap the S/dP MMAs)
             const int iq = i0 + tid;
             const float lq = iq < a.T ? a.lse[(long)h * a.T + iq] * LOG2E : 0.f;
@@ -495,8 +460,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             tc::mbar_wait(s_full, n & 1);
             tc::tc_fence_after();
             float sv[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tc::tmem_ld32(t_s + c * 32 + lane_off, sv + c * 32);
+            tc::tmem_ld128(t_s + lane_off, sv);
             uint32_t pk[64];
 #pragma unroll
             for (int c = 0; c < 128; c += 2) {
@@ -603,15 +567,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x, h = blockIdx.y;
-    const int i0 = qt * 128, i1 = min(a.T, i0 + 128);
-    const int last_kt = (i1 - 1) / 128;
-    AttnTcArgs va;
-    va.T = a.T; va.Peff = a.Peff; va.seg = a.seg;
-    auto visible = [&](int kt) {
-        const int j0 = kt * 128, j1 = min(a.T, j0 + 128);
-        return tile_visible(va, i0, i1, j0, j1);
-    };
+    const int qt = a.q_order[blockIdx.x], h = blockIdx.y;
+    const int i0 = qt * 128;
+    const int e0 = a.q_ptr[qt], e1 = a.q_ptr[qt + 1];
 
     if (threadIdx.x == 0) {
         tc::mbar_init(q_full, 1);
@@ -642,8 +600,8 @@ __global__ void __launch_bounds__(NTHR, 1)
                 tc::tma_load_2d(smem + L::OFF_DO + r * 128 * 128, &tm_do, q_full, h * DH + r * 64, i0);
             }
             int n = 0;
-            for (int kt = 0; kt <= last_kt; ++kt) {
-                if (!visible(kt)) continue;
+            for (int e = e0; e < e1; ++e) {
+                const int kt = a.q_list[e] & 0x3fffffff;
                 const int st = n % L::ST;
                 tc::mbar_wait(&kv_empty[st], ((n / L::ST) & 1) ^ 1);
                 tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
@@ -690,8 +648,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 tc::mma_commit(g_done);
                 tc::mma_commit(&kv_empty[st]);
             };
-            int n_tiles = 0;
-            for (int kt = 0; kt <= last_kt; ++kt) n_tiles += visible(kt) ? 1 : 0;
+            const int n_tiles = e1 - e0;
             if (n_tiles > 0) issue_sdp(0);
             for (int n = 0; n < n_tiles; ++n) {
                 tc::mbar_wait(p_full, n & 1);
@@ -709,10 +666,9 @@ __global__ void __launch_bounds__(NTHR, 1)
         const float Dr = row_ok ? a.dsum[(long)h * a.T + i] : 0.f;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         int n = 0;
-        for (int kt = 0; kt <= last_kt; ++kt) {
-            if (!visible(kt)) continue;
-            const int j0 = kt * 128;
-            const bool full = tile_full(va, i0, i1, j0);
+        for (int e = e0; e < e1; ++e) {
+            const int j0 = (a.q_list[e] & 0x3fffffff) * 128;
+            const bool full = (a.q_list[e] >> 30) & 1;
             if (!full) {
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 const int jj = j0 + (threadIdx.x - 64);
@@ -722,8 +678,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             tc::mbar_wait(s_full, n & 1);
             tc::tc_fence_after();
             float sv[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tc::tmem_ld32(t_s + c * 32 + lane_off, sv + c * 32);
+            tc::tmem_ld128(t_s + lane_off, sv);
 #pragma unroll
             for (int c = 0; c < 128; ++c) {
                 float p = exp2f(sv[c] * a.scale_log2 - Lr);
@@ -849,6 +804,9 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* dout, const fl
     a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d; a.Peff = aa.Peff;
     a.n_qt = (aa.T + 127) / 128;
     a.seg = aa.seg;
+    a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
+    a.k_ptr = aa.sched.k_ptr; a.k_list = aa.sched.k_list; a.k_order = aa.sched.k_order;
+    if (!a.q_ptr || !a.k_ptr) return false;
     a.scale = aa.scale;
     a.scale_log2 = aa.scale * LOG2E;
     a.lse = lse;
@@ -879,6 +837,8 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
     a.Peff = aa.Peff;
     a.seg = aa.seg;
+    a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
+    if (!a.q_ptr) return false;
     a.scale_log2 = aa.scale * LOG2E;
     a.out = out;
     a.lse = lse;

@@ -119,7 +119,18 @@ void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int
 
 // attention (k_attn.cu).  qkv: [T x 3d] (q | k | v, head h at columns h*Dh);
 // seg/seg_start/seg_end describe the shared-prompt structure (seg 0 = prompt).
+// Attention tile schedule (128 x 128 tiles), built once per packed sequence on
+// the host: for every query tile the visible key tiles, for every key tile the
+// query tiles that see it; entries are tile | (full << 30), where full means
+// every (row, key) pair of the tile is allowed (no per-element mask).  Orders
+// list the tiles heaviest-first for load balance.
+struct AttnSched {
+    const int32_t *q_ptr = nullptr, *q_list = nullptr, *q_order = nullptr;
+    const int32_t *k_ptr = nullptr, *k_list = nullptr, *k_order = nullptr;
+};
+
 struct AttnArgs {
+    AttnSched sched;
     int T, H, Dh, d;
     int Peff;                  // end of segment 0 (prompt length, or T when causal)
     const int32_t* seg;        // [T]
