@@ -178,6 +178,8 @@ parl_status parl_grad_reset(parl_grad_t gr);
 parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl_group_t g,
                           parl_grad_t gr);
 parl_status parl_grad_download(parl_grad_t gr, double* flat, size_t n);
+/* GradBuffer::accumulate (model.cpp:189-194): dst += src, counts add. */
+parl_status parl_grad_accumulate(parl_grad_t dst, parl_grad_t src);
 int parl_grad_micro_steps(parl_grad_t gr);
 
 /* ---- whole micro-step: Pipeline::train_microbatch shared-prompt branch

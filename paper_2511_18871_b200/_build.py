@@ -60,5 +60,21 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_cpp_tests() -> str:
+    """C++ drop-in parity suite: header-only layer + libparl_gpu.so + the C oracle."""
+    build()
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    out = os.path.join(BUILD, "test_dropin")
+    deps = [src, os.path.join(ROOT, "include", "parl_gpu.hpp"), os.path.join(ROOT, "include", "parl_gpu.h"), LIB]
+    if _stale(out, deps):
+        oracle_o = os.path.join(BUILD, "parl_oracle.o")
+        subprocess.check_call(["gcc", "-std=c11", "-O2", "-c", os.path.join(ROOT, "oracle", "parl_oracle.c"),
+                               "-o", oracle_o])
+        subprocess.check_call(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                               "-I/usr/local/cuda/include", src, oracle_o, "-L" + PKG, "-lparl_gpu",
+                               "-Wl,-rpath," + PKG, "-lm", "-o", out])
+    return out
+
+
 if __name__ == "__main__":
     build(verbose=True)

@@ -1389,6 +1389,16 @@ parl_status parl_grad_reset(parl_grad_t gr) {
 
 int parl_grad_micro_steps(parl_grad_t gr) { return gr->micro_steps; }
 
+parl_status parl_grad_accumulate(parl_grad_t dst, parl_grad_t src) {
+    return guarded(dst->ctx, [&] {
+        PARL_REQUIRE(same_cfg(dst->cfg, src->cfg), PARL_E_SHAPE, "gradient buffers have incongruent layouts");
+        launch_axpy(static_cast<const float*>(src->g.p), static_cast<float*>(dst->g.p), (long)dst->L.total,
+                    dst->ctx->st);
+        check_launch();
+        dst->micro_steps += src->micro_steps;
+    });
+}
+
 parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl_group_t g, parl_grad_t gr) {
     return guarded(ctx, [&] {
         // lifecycle checks, model.cpp:590-598

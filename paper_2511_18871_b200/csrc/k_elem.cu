@@ -525,6 +525,10 @@ __global__ void k_fill_f64(double* __restrict__ out, long n, double v) {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) out[e] = v;
 }
 
+__global__ void k_axpy(const float* __restrict__ x, float* __restrict__ y, long n) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) y[e] += x[e];
+}
+
 // apply_update (model.cpp:202-219): flag non-finite gradients / results.
 __global__ void k_sgd_check(const float* __restrict__ g, const double* __restrict__ w, long n, double scale,
                             int* __restrict__ flags) {
@@ -703,6 +707,11 @@ void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double sc
 
 void launch_fill_f64(double* out, long n, double v, cudaStream_t st) {
     k_fill_f64<<<grid_for(n), 256, 0, st>>>(out, n, v);
+    PARL_LAUNCHED();
+}
+
+void launch_axpy(const float* x, float* y, long n, cudaStream_t st) {
+    k_axpy<<<grid_for(n), 256, 0, st>>>(x, y, n);
     PARL_LAUNCHED();
 }
 

@@ -115,6 +115,7 @@ void launch_f32_to_f64(const float* x, double* y, long n, cudaStream_t st);
 void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double scale, const double* base,
                   cudaStream_t st);
 void launch_fill_f64(double* out, long n, double v, cudaStream_t st);
+void launch_axpy(const float* x, float* y, long n, cudaStream_t st);  // y += x
 void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int phase, cudaStream_t st);
 
 // attention (k_attn.cu).  qkv: [T x 3d] (q | k | v, head h at columns h*Dh);

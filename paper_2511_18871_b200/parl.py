@@ -123,6 +123,7 @@ def _load():
         "parl_stats_download": [vp, C.POINTER(_Stats)], "parl_stats_reset": [vp],
         "parl_grad_create": [vp, vp, C.POINTER(vp)], "parl_grad_destroy": [vp], "parl_grad_reset": [vp],
         "parl_backward": [vp, vp, vp, vp, vp], "parl_grad_download": [vp, f64p, C.c_size_t],
+        "parl_grad_accumulate": [vp, vp],
         "parl_train_microbatch": [vp, vp, vp, vp, vp, f64p, f64p, C.POINTER(_Hyper), vp, C.POINTER(_Stats)],
         "parl_apply_update": [vp, vp, C.c_double],
         "parl_comm_unique_id": [C.c_char_p], "parl_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
@@ -348,6 +349,10 @@ class GradBuffer:
 
     def allreduce(self):
         _check(LIB.parl_grad_allreduce(self.ctx.h, self.h), self.ctx.h)
+
+    def accumulate(self, other: "GradBuffer"):
+        """GradBuffer::accumulate (model.cpp:189-194)."""
+        _check(LIB.parl_grad_accumulate(self.h, other.h), self.ctx.h)
 
     def __del__(self):
         try:
