@@ -442,12 +442,12 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
             // tcgen05 head with the vocab log-sum-exp and target gather fused
             // into the epilogue: logits reach HBM only for the policy (bf16,
             // kept for the backward), never for old/ref.
-            const int n_parts = (V + 255) / 256;
+            const int n_parts = (V + 127) / 128;
             GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
             ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
             ga.part = c->part.as<float>((size_t)S * n_parts * 2);
             ga.target = c->target.as<float>(S);
-            ga.n_parts = n_parts; ga.part_cols = 256;
+            ga.n_parts = n_parts; ga.part_cols = 128;
             ga.logits_act = act ? act->logits.as<bf16>((size_t)S * V) : nullptr;
             ga.ldca = V;
             {
@@ -1541,7 +1541,7 @@ extern "C" parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const
         GemmArgs g = mk(M, N, K, A, sam, sak, B, sbn, sbk);
         g.epi = epi; g.bias = bias; g.Cf = Cf; g.ldc = ldc; g.resid = resid; g.Ca = Ca; g.ldca = ldca;
         g.Caux = Caux; g.aux_in = aux_in; g.labels = labels; g.part = part; g.target = target;
-        g.logits_act = logits_act; g.n_parts = n_parts; g.part_cols = 256;
+        g.logits_act = logits_act; g.n_parts = n_parts; g.part_cols = 128;
         if (path == 0) {
             PARL_REQUIRE(gemm_tc(g, 0), PARL_E_CONFIG, "shape/layout not supported by the tcgen05 kernel");
         } else {

@@ -27,7 +27,9 @@ namespace parl_gpu {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, NTHREADS = 256;
+constexpr int BM = 128, BK = 64;
+constexpr int EPI_WARPS = 8;                      // two per TMEM lane quadrant, each half the columns
+constexpr int NTHREADS = 128 + 32 * EPI_WARPS;    // warps 0-3 producer/MMA/TMEM/spare, 4.. epilogue
 
 struct TcArgs {
     int M, N, K, nkb, tiles_m, tiles_n, splits, kbs, epi, vec_ok;
@@ -53,13 +55,29 @@ struct Cfg {
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int STAGES = BN == 256 ? 4 : 6;
-    static constexpr int EPI_OFF = STAGES * STAGE + 256;          // after the barriers
-    static constexpr int SMEM = EPI_OFF + 4 * 32 * 33 * 4 + 1024;  // + per-warp epilogue tiles + align
+    static constexpr int EPI_OFF = STAGES * STAGE + 256;                  // after the barriers
+    static constexpr int SMEM = EPI_OFF + EPI_WARPS * 32 * 33 * 4 + 1024;  // + per-warp epilogue tiles + align
 };
 
-__device__ __forceinline__ float gelu_dev(float x) { return 0.5f * x * erfcf(-x * 0.70710678118654752f); }
-__device__ __forceinline__ float gelu_grad_dev(float x) {
-    return 0.5f * erfcf(-x * 0.70710678118654752f) + x * 0.39894228040143267794f * __expf(-0.5f * x * x);
+// Phi(x) = 0.5 (1 + erf(x / sqrt 2)) with Abramowitz-Stegun 7.1.26 (|erf err| <= 1.5e-7,
+// far below the bf16 rounding of the outputs); returns exp(-x^2/2) for GELU' too.
+__device__ __forceinline__ float phi_fast(float x, float& e) {
+    const float z = fabsf(x) * 0.70710678118654752f;
+    const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+    e = __expf(-z * z);
+    const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
+                                0.254829592f);
+    const float erf_abs = 1.f - poly * e;
+    return 0.5f * (1.f + copysignf(erf_abs, x));
+}
+__device__ __forceinline__ float gelu_dev(float x) {  // x * Phi(x)  (model.cpp:255)
+    float e;
+    return x * phi_fast(x, e);
+}
+__device__ __forceinline__ float gelu_grad_dev(float x) {  // Phi(x) + x phi(x)  (model.cpp:257-260)
+    float e;
+    const float p = phi_fast(x, e);
+    return p + x * 0.39894228040143267794f * e;
 }
 
 // Epilogue of one 32-row x 32-column chunk.  v[] arrives in the TMEM layout
@@ -111,13 +129,17 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, int row0, int co
                 } else {
                     // batch the loads first: stores may alias, so the compiler
                     // would otherwise serialise every load behind a store
-                    float old[32];
 #pragma unroll
-                    for (int r = 0; r < 32; ++r)
-                        old[r] = r < rmax ? a.Cf[(long)(row0 + r) * a.ldc + col] : 0.f;
+                    for (int h = 0; h < 32; h += 16) {
+                        float old[16];
 #pragma unroll
-                    for (int r = 0; r < 32; ++r)
-                        if (r < rmax) a.Cf[(long)(row0 + r) * a.ldc + col] = old[r] + sm[r * 33 + lane];
+                        for (int r = 0; r < 16; ++r)
+                            old[r] = h + r < rmax ? a.Cf[(long)(row0 + h + r) * a.ldc + col] : 0.f;
+#pragma unroll
+                        for (int r = 0; r < 16; ++r)
+                            if (h + r < rmax)
+                                a.Cf[(long)(row0 + h + r) * a.ldc + col] = old[r] + sm[(h + r) * 33 + lane];
+                    }
                 }
                 break;
             case EPI_ACT:
@@ -125,12 +147,16 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, int row0, int co
                     a.Ca[(long)(row0 + r) * a.ldca + col] = __float2bfloat16_rn(sm[r * 33 + lane] + b);
                 break;
             case EPI_RESID: {
-                float rv[32];
 #pragma unroll
-                for (int r = 0; r < 32; ++r) rv[r] = r < rmax ? a.resid[(long)(row0 + r) * a.ldc + col] : 0.f;
+                for (int h = 0; h < 32; h += 16) {
+                    float rv[16];
 #pragma unroll
-                for (int r = 0; r < 32; ++r)
-                    if (r < rmax) a.Cf[(long)(row0 + r) * a.ldc + col] = rv[r] + (sm[r * 33 + lane] + b);
+                    for (int r = 0; r < 16; ++r)
+                        rv[r] = h + r < rmax ? a.resid[(long)(row0 + h + r) * a.ldc + col] : 0.f;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r)
+                        if (h + r < rmax) a.Cf[(long)(row0 + h + r) * a.ldc + col] = rv[r] + (sm[(h + r) * 33 + lane] + b);
+                }
                 break;
             }
             case EPI_GELU:
@@ -142,15 +168,18 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, int row0, int co
                 }
                 break;
             case EPI_GELU_BWD: {
-                bf16 uv[32];
 #pragma unroll
-                for (int r = 0; r < 32; ++r)
-                    uv[r] = r < rmax ? a.aux_in[(long)(row0 + r) * a.ldca + col] : __float2bfloat16_rn(0.f);
+                for (int h = 0; h < 32; h += 16) {
+                    bf16 uv[16];
 #pragma unroll
-                for (int r = 0; r < 32; ++r)
-                    if (r < rmax)
-                        a.Ca[(long)(row0 + r) * a.ldca + col] =
-                            __float2bfloat16_rn(sm[r * 33 + lane] * gelu_grad_dev(__bfloat162float(uv[r])));
+                    for (int r = 0; r < 16; ++r)
+                        uv[r] = h + r < rmax ? a.aux_in[(long)(row0 + h + r) * a.ldca + col] : __float2bfloat16_rn(0.f);
+#pragma unroll
+                    for (int r = 0; r < 16; ++r)
+                        if (h + r < rmax)
+                            a.Ca[(long)(row0 + h + r) * a.ldca + col] =
+                                __float2bfloat16_rn(sm[(h + r) * 33 + lane] * gelu_grad_dev(__bfloat162float(uv[r])));
+                }
                 break;
             }
             case EPI_LSE:
@@ -186,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             tc::mbar_init(&tfull[s], 1);
-            tc::mbar_init(&tempty[s], 128);
+            tc::mbar_init(&tempty[s], 32 * EPI_WARPS);
         }
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
@@ -257,8 +286,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue
-        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
-        float* esm = reinterpret_cast<float*>(smem + C::EPI_OFF) + ew * 32 * 33;
+        const int ew = warp & 3;           // TMEM lane quadrant (a warp may only touch lanes 32*(warp%4)..)
+        const int half = (warp - 4) >> 2;  // which half of the tile's columns
+        float* esm = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - 4) * 32 * 33;
         uint32_t local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             const int mt = item % a.tiles_m, rest = item / a.tiles_m;
@@ -269,14 +299,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int row0 = mt * BM + ew * 32, row = row0 + lane;
             const int label = (a.epi == EPI_LSE && row < a.M) ? a.labels[row] : -1;
             float lm = -INFINITY, ls = 0.f;
+            constexpr int HALF = BN / 2;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < HALF / 32; ++c) {
                 float v[32];
-                tc::tmem_ld32(tbase + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), v);
-                epilogue_chunk(a, row0, nt * BN + c * 32, v, sp, esm, lm, ls, label);
+                const int col = half * HALF + c * 32;
+                tc::tmem_ld32(tbase + acc * BN + col + ((uint32_t)(ew * 32) << 16), v);
+                epilogue_chunk(a, row0, nt * BN + col, v, sp, esm, lm, ls, label);
             }
-            if (a.epi == EPI_LSE && row < a.M) {
-                float* p = a.part + ((long)row * a.n_parts + nt) * 2;
+            if (a.epi == EPI_LSE && row < a.M) {  // partials per 128 columns
+                float* p = a.part + ((long)row * a.n_parts + (nt * BN + half * HALF) / 128) * 2;
                 p[0] = lm;
                 p[1] = ls;
             }
@@ -387,7 +419,7 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     if (!encode_fn()) return false;
 
     // tile width: 128 when N is a multiple of 128 but not of 256, or N is small
-    // (the LSE epilogue always uses 256-column partials: n_parts = ceil(N / 256))
+    // (the LSE epilogue writes one (max, sumexp) partial per 128 columns: n_parts = ceil(N / 128))
     const int BN = g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256);
     CUtensorMap ma, mb;
     bool ok;

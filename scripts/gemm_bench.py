@@ -36,7 +36,7 @@ for name, M, N, K, amn, bmn, epi in cases:
     aux = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if epi in ("GELU", "GELU_BWD") else None
     bias = torch.zeros(N, device="cuda")
     labels = torch.randint(0, N, (M,), device="cuda", dtype=torch.int32) if epi == "LSE" else None
-    n_parts = (N + 255) // 256
+    n_parts = (N + 127) // 128
     part = torch.empty(M, n_parts, 2, device="cuda") if epi == "LSE" else None
     target = torch.empty(M, device="cuda") if epi == "LSE" else None
     p = lambda t: None if t is None else t.data_ptr()

@@ -122,7 +122,7 @@ def test_lse_epilogue(env):
     bias = torch.randn(N, device="cuda") * 0.1
     z = ref + bias
     labels = torch.randint(0, N, (M,), device="cuda", dtype=torch.int32)
-    n_parts = (N + 255) // 256
+    n_parts = (N + 127) // 128
     part = torch.zeros(M, n_parts, 2, device="cuda")
     target = torch.zeros(M, device="cuda")
     logits = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
