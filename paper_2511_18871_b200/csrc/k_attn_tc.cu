@@ -32,6 +32,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 struct AttnTcArgs {
     int T, H, Dh, d, Peff;
     const int32_t* seg;
+    const int32_t *seg_start, *seg_end;      // [G+1]: segment k spans [seg_start[k], seg_end[k])
     const int32_t *q_ptr, *q_list, *q_order;  // tile schedule (see build_attn_schedule)
     float scale_log2;  // scale * log2(e)
     bf16* out;         // [T x d]
@@ -43,8 +44,8 @@ struct AttnSmem {
     static constexpr int Q_BYTES = TQ * DH * 2;
     static constexpr int KV_BYTES = TK * DH * 2;
     static constexpr int P_BYTES = TQ * TK * 2;
-    static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + Q_BYTES;              // 2 stages
+    static constexpr int OFF_Q = 0;                            // 2 buffers (double-buffered across items)
+    static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;          // 2 stages
     static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;         // 2 stages
     static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
     static constexpr int OFF_SEG = OFF_P + P_BYTES;            // 128 ints (key segments)
@@ -52,32 +53,39 @@ struct AttnSmem {
     static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
+// Persistent forward: CTA b processes work items b, b+grid, ... of the
+// heavy-first list item -> (q_order[item / H], item % H).  All tiles of all of
+// the CTA's items form one continuous stream (global tile counter n), so the
+// next item's Q load and first QK^T overlap the current item's epilogue.
 template <int DH>
 __global__ void __launch_bounds__(NTHR, 1)
-    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, AttnTcArgs a) {
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, AttnTcArgs a, int n_items) {
     using L = AttnSmem<DH>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-    uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;   // [2]
-    uint64_t* kv_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;    // [2]
-    uint64_t* p_full = bar + 7;
-    uint64_t* o_done = bar + 8;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 9);
-    int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
+    uint64_t* q_full = bar + 0;    // [2]
+    uint64_t* q_empty = bar + 2;   // [2]
+    uint64_t* kv_full = bar + 4;   // [2]
+    uint64_t* kv_empty = bar + 6;  // [2]
+    uint64_t* s_full = bar + 8;    // [2]
+    uint64_t* p_full = bar + 10;
+    uint64_t* o_done = bar + 11;
+    uint64_t* o_free = bar + 12;   // [2]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 14);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = a.q_order[blockIdx.x], h = blockIdx.y;
-    const int i0 = qt * TQ;
+    auto item_qt = [&](int it) { return a.q_order[it / a.H]; };
+    auto item_h = [&](int it) { return it % a.H; };
 
     if (threadIdx.x == 0) {
-        tc::mbar_init(q_full, 1);
         for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&q_full[s], 1);
+            tc::mbar_init(&q_empty[s], 1);
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 1);
             tc::mbar_init(&s_full[s], 1);
+            tc::mbar_init(&o_free[s], 128);
         }
         tc::mbar_init(p_full, 128);
         tc::mbar_init(o_done, 1);
@@ -89,175 +97,202 @@ __global__ void __launch_bounds__(NTHR, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
-    const uint32_t t_s0 = tbase, t_o = tbase + 256;  // S buffers at cols 0/128, O at 256
+    const uint32_t t_s0 = tbase, t_o0 = tbase + 256;  // S buffers at cols 0/128, O buffers at 256 / 256+DH
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA
-            tc::mbar_expect_tx(q_full, L::Q_BYTES);
+            int n = 0, li = 0;
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+                const int qt = item_qt(it), h = item_h(it), qb = li & 1;
+                tc::mbar_wait(&q_empty[qb], ((li >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&q_full[qb], L::Q_BYTES);
 #pragma unroll
-            for (int r = 0; r < DH / 64; ++r)
-                tc::tma_load_2d(smem + L::OFF_Q + r * TQ * 128, &tm_qkv, q_full, h * DH + r * 64, i0);
-            int n = 0;
-            for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e) {
-                const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
-                const int st = n & 1;
-                tc::mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
-                uint8_t* kb = smem + L::OFF_K + st * L::KV_BYTES;
-                uint8_t* vb = smem + L::OFF_V + st * L::KV_BYTES;
+                for (int r = 0; r < DH / 64; ++r)
+                    tc::tma_load_2d(smem + L::OFF_Q + qb * L::Q_BYTES + r * TQ * 128, &tm_qkv, &q_full[qb],
+                                    h * DH + r * 64, qt * TQ);
+                for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e, ++n) {
+                    const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
+                    const int st = n & 1;
+                    tc::mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
+                    tc::mbar_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
+                    uint8_t* kb = smem + L::OFF_K + st * L::KV_BYTES;
+                    uint8_t* vb = smem + L::OFF_V + st * L::KV_BYTES;
 #pragma unroll
-                for (int r = 0; r < DH / 64; ++r) {
-                    tc::tma_load_2d(kb + r * TK * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, j0);
-                    tc::tma_load_2d(vb + r * TK * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, j0);
+                    for (int r = 0; r < DH / 64; ++r) {
+                        tc::tma_load_2d(kb + r * TK * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, j0);
+                        tc::tma_load_2d(vb + r * TK * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, j0);
+                    }
                 }
-                ++n;
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA
             constexpr uint32_t id_s = tc::idesc_bf16(TQ, TK, 0, 0);
             constexpr uint32_t id_o = tc::idesc_bf16(TQ, DH, 0, 1);
-            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q);
             const uint32_t sp = tc::smem_u32(smem + L::OFF_P);
-            const int n_tiles = a.q_ptr[qt + 1] - a.q_ptr[qt];
-            tc::mbar_wait(q_full, 0);
-            auto issue_s = [&](int n) {
-                const int st = n & 1;
-                tc::mbar_wait(&kv_full[st], (n >> 1) & 1);
+            // S-iterator (runs one tile ahead of the PV iterator)
+            int s_it = blockIdx.x, s_li = 0, s_e = 0, s_end = 0, s_n = 0;
+            auto s_begin_item = [&]() {
+                if (s_it < n_items) {
+                    const int qt = item_qt(s_it);
+                    s_e = a.q_ptr[qt];
+                    s_end = a.q_ptr[qt + 1];
+                }
+            };
+            s_begin_item();
+            auto issue_s = [&]() -> bool {  // returns false when the stream is exhausted
+                while (s_it < n_items && s_e >= s_end) {
+                    s_it += gridDim.x;
+                    ++s_li;
+                    s_begin_item();
+                }
+                if (s_it >= n_items) return false;
+                const int qb = s_li & 1;
+                if (s_e == a.q_ptr[item_qt(s_it)]) tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
+                const int st = s_n & 1;
+                tc::mbar_wait(&kv_full[st], (s_n >> 1) & 1);
                 tc::tc_fence_after();
+                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + qb * L::Q_BYTES);
                 const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::KV_BYTES);
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     const uint32_t off = (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_s0 + (n & 1) * TK, tc::sdesc(sq + off, 16, 1024),
+                    tc::mma_bf16(t_s0 + st * TK, tc::sdesc(sq + off, 16, 1024),
                                  tc::sdesc(sk + (ks >> 2) * (TK * 128) + (ks & 3) * 32, 16, 1024), id_s, ks > 0);
                 }
-                tc::mma_commit(&s_full[n & 1]);
+                tc::mma_commit(&s_full[st]);
+                ++s_e;
+                ++s_n;
+                return true;
             };
-            if (n_tiles > 0) issue_s(0);
-            for (int n = 0; n < n_tiles; ++n) {
-                if (n + 1 < n_tiles) issue_s(n + 1);
-                tc::mbar_wait(p_full, n & 1);
-                tc::tc_fence_after();
-                const int st = n & 1;
-                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::KV_BYTES);
+            bool more = issue_s();
+            int n = 0, li = 0;
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+                const int qt = item_qt(it), qb = li & 1, ob = li & 1;
+                const int nt = a.q_ptr[qt + 1] - a.q_ptr[qt];
+                for (int t = 0; t < nt; ++t, ++n) {
+                    if (more) more = issue_s();  // S of the next tile (possibly the next item)
+                    tc::mbar_wait(p_full, n & 1);
+                    if (t == 0) tc::mbar_wait(&o_free[ob], ((li >> 1) & 1) ^ 1);
+                    tc::tc_fence_after();
+                    const int st = n & 1;
+                    const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::KV_BYTES);
 #pragma unroll
-                for (int ks = 0; ks < TK / 16; ++ks) {
-                    const uint32_t pa = sp + (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_o, tc::sdesc(pa, 16, 1024), tc::sdesc(sv + ks * 2048, TK * 128, 1024), id_o,
-                                 (n > 0 || ks > 0) ? 1u : 0u);
+                    for (int ks = 0; ks < TK / 16; ++ks) {
+                        const uint32_t pa = sp + (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
+                        tc::mma_bf16(t_o0 + ob * DH, tc::sdesc(pa, 16, 1024),
+                                     tc::sdesc(sv + ks * 2048, TK * 128, 1024), id_o, (t > 0 || ks > 0) ? 1u : 0u);
+                    }
+                    tc::mma_commit(o_done);
+                    tc::mma_commit(&kv_empty[st]);
+                    if (t == nt - 1) tc::mma_commit(&q_empty[qb]);
                 }
-                tc::mma_commit(o_done);
-                tc::mma_commit(&kv_empty[st]);
             }
         }
     } else {
         // ---------------- softmax: warps 2..5 -> TMEM lane quarter (warp % 4)
         const int q4 = warp & 3;
         const int r = q4 * 32 + lane;  // tile row
-        const int i = i0 + r;
-        const bool row_ok = i < a.T;
-        const int seg_i = row_ok ? a.seg[i] : -1;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        float m_used = -INFINITY, l = 0.f;
-        int n = 0;
         uint8_t* P = smem + L::OFF_P;
-        for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e) {
-            const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
-            const bool full = (a.q_list[e] >> 30) & 1;
-            if (!full) {
-                // key segment ids of this tile (j >= T marked -2: never visible)
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                const int jj = j0 + (threadIdx.x - 64);
-                kseg[threadIdx.x - 64] = jj < a.T ? a.seg[jj] : -2;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
-            tc::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
-            tc::tc_fence_after();
-            float s[TK];
-            tc::tmem_ld128(t_s0 + (n & 1) * TK + lane_off, s);
-            float mx = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < TK; ++j) {
-                float v = s[j] * a.scale_log2;
-                if (!full) {
-                    const int sj = kseg[j], jg = j0 + j;
-                    const bool ok = sj >= 0 && row_ok &&
-                                    (sj == 0 ? (seg_i != 0 || jg <= i) : (sj == seg_i && jg <= i));
-                    v = ok ? v : -INFINITY;
-                }
-                s[j] = v;
-                mx = fmaxf(mx, v);
-            }
-            // conditional rescale (threshold 8 in log2 units)
-            const bool need = mx > m_used + 8.f;
-            const float m_new = need ? mx : m_used;
-            const float alpha = need ? exp2f(m_used - m_new) : 1.f;  // m_used = -inf -> 0
-            const float mb = m_new == -INFINITY ? 0.f : m_new;
-            float sum = 0.f;
-            uint32_t pk[TK / 2];
-#pragma unroll
-            for (int j = 0; j < TK; j += 2) {
-                const float p0 = exp2f(s[j] - mb), p1 = exp2f(s[j + 1] - mb);
-                sum += p0 + p1;
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                pk[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            // PV of the previous tile must be done: P smem is reused, O is rescaled
-            if (n > 0) {
-                tc::mbar_wait(o_done, (n - 1) & 1);
+        int n = 0, li = 0;
+        for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+            const int qt = item_qt(it), h = item_h(it), ob = li & 1;
+            const int i0 = qt * TQ, i = i0 + r;
+            const bool row_ok = i < a.T;
+            const int seg_i = row_ok ? a.seg[i] : -1;
+            // allowed keys of row i: [0, e0) and [b1, i] (model.cpp:242-245)
+            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
+            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
+            float m_used = -INFINITY, l = 0.f;
+            const int ea = a.q_ptr[qt], eb = a.q_ptr[qt + 1];
+            for (int e = ea; e < eb; ++e, ++n) {
+                const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
+                // the row's allowed keys in this tile as local ranges [0, h0) u [l1, h1)
+                const int h0 = min(max(e0 - j0, 0), TK);
+                const int l1 = min(max(b1 - j0, 0), TK), h1 = min(max(e1 - j0, 0), TK);
+                tc::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
                 tc::tc_fence_after();
-                if (__any_sync(0xffffffffu, need) && n > 0) {
+                float s[TK];
+                tc::tmem_ld128(t_s0 + (n & 1) * TK + lane_off, s);
+                float mx = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < TK; ++j) {
+                    const bool ok = (j < h0) | ((j >= l1) & (j < h1));
+                    const float v = ok ? s[j] * a.scale_log2 : -INFINITY;
+                    s[j] = v;
+                    mx = fmaxf(mx, v);
+                }
+                // conditional rescale (threshold 8 in log2 units)
+                const bool need = mx > m_used + 8.f;
+                const float m_new = need ? mx : m_used;
+                const float alpha = need ? exp2f(m_used - m_new) : 1.f;  // m_used = -inf -> 0
+                const float mb = m_new == -INFINITY ? 0.f : m_new;
+                float sum = 0.f;
+                uint32_t pk[TK / 2];
+#pragma unroll
+                for (int j = 0; j < TK; j += 2) {
+                    const float p0 = exp2f(s[j] - mb), p1 = exp2f(s[j + 1] - mb);
+                    sum += p0 + p1;
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                    pk[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                // the previous PV (this item's or the previous item's) must be done:
+                // P smem is reused and O is rescaled
+                if (n > 0) {
+                    tc::mbar_wait(o_done, (n - 1) & 1);
+                    tc::tc_fence_after();
+                }
+                if (e > ea && __any_sync(0xffffffffu, need)) {
 #pragma unroll
                     for (int c = 0; c < DH / 32; ++c) {
                         float o[32];
-                        tc::tmem_ld32(t_o + c * 32 + lane_off, o);
+                        tc::tmem_ld32(t_o0 + ob * DH + c * 32 + lane_off, o);
                         uint32_t w[32];
 #pragma unroll
                         for (int q = 0; q < 32; ++q) w[q] = __float_as_uint(o[q] * alpha);
-                        tc::tmem_st16(t_o + c * 32 + lane_off, w);
-                        tc::tmem_st16(t_o + c * 32 + 16 + lane_off, w + 16);
+                        tc::tmem_st16(t_o0 + ob * DH + c * 32 + lane_off, w);
+                        tc::tmem_st16(t_o0 + ob * DH + c * 32 + 16 + lane_off, w + 16);
                     }
                     tc::tmem_st_wait();
                 }
-            }
-            l = l * alpha + sum;
-            m_used = m_new;
-            // P row r -> SW128 K-major tile: 64-key atom columns of [128 rows x 128 B]
-            const uint32_t pbase = tc::smem_u32(P) + r * 128;
+                l = l * alpha + sum;
+                m_used = m_new;
+                // P row r -> SW128 K-major tile: 64-key atom columns of [128 rows x 128 B]
+                const uint32_t pbase = tc::smem_u32(P) + r * 128;
 #pragma unroll
-            for (int c = 0; c < TK / 8; ++c) {
-                const int atom = c >> 3, chunk = c & 7;
-                tc::sts128(pbase + atom * (TQ * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                           pk[4 * c + 3]);
+                for (int c = 0; c < TK / 8; ++c) {
+                    const int atom = c >> 3, chunk = c & 7;
+                    tc::sts128(pbase + atom * (TQ * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1],
+                               pk[4 * c + 2], pk[4 * c + 3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tc::tc_fence_before();
+                tc::mbar_arrive(p_full);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tc::tc_fence_before();
-            tc::mbar_arrive(p_full);
-            ++n;
-        }
-        // epilogue: O / l -> out (bf16), lse
-        if (n > 0) {
+            // item epilogue: O / l -> out (bf16), lse; then release the O buffer
             tc::mbar_wait(o_done, (n - 1) & 1);
             tc::tc_fence_after();
-        }
-        const float inv = l > 0.f ? 1.f / l : 0.f;
+            const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
-            float o[32];
-            tc::tmem_ld32(t_o + c * 32 + lane_off, o);
-            if (row_ok) {
-                bf16* dst = a.out + (long)i * a.d + h * DH + c * 32;
+            for (int c = 0; c < DH / 32; ++c) {
+                float o[32];
+                tc::tmem_ld32(t_o0 + ob * DH + c * 32 + lane_off, o);
+                if (row_ok) {
+                    bf16* dst = a.out + (long)i * a.d + h * DH + c * 32;
 #pragma unroll
-                for (int q = 0; q < 32; q += 8) {
-                    __align__(16) bf16 t[8];
+                    for (int q = 0; q < 32; q += 8) {
+                        __align__(16) bf16 t[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(o[q + e] * inv);
-                    *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
+                        for (int e2 = 0; e2 < 8; ++e2) t[e2] = __float2bfloat16_rn(o[q + e2] * inv);
+                        *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
+                    }
                 }
             }
+            if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+            tc::tc_fence_before();
+            tc::mbar_arrive(&o_free[ob]);
         }
-        if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -266,6 +301,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         tc::tmem_dealloc<512>(tbase);
     }
 }
+
 
 // ===========================================================================
 // Backward (model.cpp:751-786 recomputed flash-style; deterministic, no atomics)
@@ -278,6 +314,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 struct AttnBwdArgs {
     int T, H, Dh, d, Peff, n_qt;
     const int32_t* seg;
+    const int32_t *seg_start, *seg_end;
     const int32_t *q_ptr, *q_list, *q_order;  // per query tile: visible key tiles
     const int32_t *k_ptr, *k_list, *k_order;  // per key tile: query tiles that see it
     float scale, scale_log2;
@@ -337,7 +374,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 8);
     float* v_lse = reinterpret_cast<float*>(smem + L::OFF_VEC);
     float* v_d = v_lse + 128;
-    int* v_seg = reinterpret_cast<int*>(v_d + 128);
+
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kt = a.k_order[blockIdx.x], h = blockIdx.y;
@@ -441,21 +478,21 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int tid = threadIdx.x - 64;
         const bool key_ok = j < a.T;
         const int seg_j = key_ok ? a.seg[j] : -2;
+        // queries that see key j: [j, T) for a prompt key, [j, end_k) for a key of response k
+        const int qhi = !key_ok ? 0 : (seg_j == 0 ? a.T : a.seg_end[seg_j]);
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         int n = 0;
         for (int e = e0; e < e1; ++e) {
             const int qt = a.k_list[e] & 0x3fffffff;
             const int i0 = qt * 128;
-            const bool full = (a.k_list[e] >> 30) & 1;
+            const int lo = min(max(j - i0, 0), 128), hi = min(max(qhi - i0, 0), 128);
             // per-query vectors of this tile (loads overlap the S/dP MMAs)
             const int iq = i0 + tid;
             const float lq = iq < a.T ? a.lse[(long)h * a.T + iq] * LOG2E : 0.f;
             const float dq = iq < a.T ? a.dsum[(long)h * a.T + iq] : 0.f;
-            const int sq = iq < a.T ? a.seg[iq] : -1;
             asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done reading the vectors
             v_lse[tid] = lq;
             v_d[tid] = dq;
-            v_seg[tid] = sq;
             asm volatile("bar.sync 1, 128;" ::: "memory");
             tc::mbar_wait(s_full, n & 1);
             tc::tc_fence_after();
@@ -466,17 +503,11 @@ __global__ void __launch_bounds__(NTHR, 1)
             for (int c = 0; c < 128; c += 2) {
                 float p2[2];
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int cc = c + e, i = i0 + cc;
-                    float p = exp2f(sv[cc] * a.scale_log2 - v_lse[cc]);
-                    if (!full) {
-                        const int si = v_seg[cc];
-                        const bool ok = key_ok && si >= 0 &&
-                                        (seg_j == 0 ? (si != 0 || j <= i) : (si == seg_j && j <= i));
-                        p = ok ? p : 0.f;
-                    }
-                    p2[e] = p;
-                    sv[cc] = p;
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const int cc = c + e2;
+                    const float p = exp2f(sv[cc] * a.scale_log2 - v_lse[cc]);
+                    p2[e2] = (cc >= lo) & (cc < hi) ? p : 0.f;
+                    sv[cc] = p2[e2];
                 }
                 __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
                 pk[c / 2] = *reinterpret_cast<uint32_t*>(&b2);
@@ -662,32 +693,25 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int q4 = warp & 3, r = q4 * 32 + lane, i = i0 + r;
         const bool row_ok = i < a.T;
         const int seg_i = row_ok ? a.seg[i] : -1;
+        const int ea0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
+        const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, ea1 = seg_i > 0 ? i + 1 : 0;
         const float Lr = row_ok ? a.lse[(long)h * a.T + i] * LOG2E : 0.f;
         const float Dr = row_ok ? a.dsum[(long)h * a.T + i] : 0.f;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         int n = 0;
         for (int e = e0; e < e1; ++e) {
             const int j0 = (a.q_list[e] & 0x3fffffff) * 128;
-            const bool full = (a.q_list[e] >> 30) & 1;
-            if (!full) {
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                const int jj = j0 + (threadIdx.x - 64);
-                kseg[threadIdx.x - 64] = jj < a.T ? a.seg[jj] : -2;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
+            const int h0 = min(max(ea0 - j0, 0), 128);
+            const int l1 = min(max(b1 - j0, 0), 128), h1 = min(max(ea1 - j0, 0), 128);
             tc::mbar_wait(s_full, n & 1);
             tc::tc_fence_after();
             float sv[128];
             tc::tmem_ld128(t_s + lane_off, sv);
 #pragma unroll
             for (int c = 0; c < 128; ++c) {
-                float p = exp2f(sv[c] * a.scale_log2 - Lr);
-                if (!full) {
-                    const int sj = kseg[c], jg = j0 + c;
-                    const bool ok = sj >= 0 && row_ok && (sj == 0 ? (seg_i != 0 || jg <= i) : (sj == seg_i && jg <= i));
-                    p = ok ? p : 0.f;
-                }
-                sv[c] = p;
+                const bool ok = (c < h0) | ((c >= l1) & (c < h1));
+                const float p = exp2f(sv[c] * a.scale_log2 - Lr);
+                sv[c] = ok ? p : 0.f;
             }
             if (n > 0) tc::mbar_wait(g_done, (n - 1) & 1);
 #pragma unroll
@@ -756,8 +780,14 @@ void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(k_attn_fwd_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         attr = true;
     }
-    dim3 grid((a.T + TQ - 1) / TQ, a.H);
-    k_attn_fwd_tc<DH><<<grid, NTHR, L::TOTAL, st>>>(m, a);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int n_items = ((a.T + TQ - 1) / TQ) * a.H;
+    k_attn_fwd_tc<DH><<<std::min(n_items, sms), NTHR, L::TOTAL, st>>>(m, a, n_items);
     PARL_LAUNCHED();
 }
 
@@ -804,6 +834,8 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* dout, const fl
     a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d; a.Peff = aa.Peff;
     a.n_qt = (aa.T + 127) / 128;
     a.seg = aa.seg;
+    a.seg_start = aa.seg_start;
+    a.seg_end = aa.seg_end;
     a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
     a.k_ptr = aa.sched.k_ptr; a.k_list = aa.sched.k_list; a.k_order = aa.sched.k_order;
     if (!a.q_ptr || !a.k_ptr) return false;
@@ -837,6 +869,8 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
     a.Peff = aa.Peff;
     a.seg = aa.seg;
+    a.seg_start = aa.seg_start;
+    a.seg_end = aa.seg_end;
     a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
     if (!a.q_ptr) return false;
     a.scale_log2 = aa.scale * LOG2E;
