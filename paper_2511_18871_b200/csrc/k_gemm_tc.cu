@@ -323,6 +323,161 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a 256 x 256 output tile per SM pair.  Each
+// CTA loads its 128 rows of A and its 128 columns of B; the leader CTA issues
+// tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs' shared memory and
+// writes each CTA's 128 accumulator rows into its own TMEM.  Per SM this halves
+// the operand bytes per MMA cycle relative to the 1-CTA 128 x 256 tile, so the
+// 6-stage ring covers the TMA latency.
+constexpr int BN2 = 256;
+struct Cfg2 {
+    static constexpr int A_BYTES = BM * BK * 2;          // 128 rows of A
+    static constexpr int B_BYTES = (BN2 / 2) * BK * 2;   // 128 columns of B
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = 6;
+    static constexpr int EPI_OFF = STAGES * STAGE + 256;
+    static constexpr int SMEM = EPI_OFF + EPI_WARPS * 32 * 33 * 4 + 1024;
+};
+
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    using C = Cfg2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int tiles_m2 = (a.M + 2 * BM - 1) / (2 * BM);
+    const int n_items = tiles_m2 * a.tiles_n * a.splits;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&tfull[s], 1);
+            tc::mbar_init(&tempty[s], 2 * 32 * EPI_WARPS);  // both CTAs' epilogue threads
+        }
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tmA);
+        tc::tma_prefetch(&tmB);
+    }
+    if (warp == 2) tc::tmem_alloc_pair<2 * BN2>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer (both CTAs, completing on the leader's barrier)
+        uint32_t cnt = 0;
+        for (int item = cid; item < n_items; item += ncl) {
+            const int mt = item % tiles_m2, rest = item / tiles_m2;
+            const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
+            const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
+            const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * BN2 + (int)rank * (BN2 / 2);
+            for (int kb = kb0; kb < kb1; ++kb, ++cnt) {
+                const int s = cnt % C::STAGES;
+                const uint32_t ph = (cnt / C::STAGES) & 1;
+                tc::mbar_wait(&empty[s], ph ^ 1);
+                const uint32_t fb = tc::mapa(&full[s], 0);
+                if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * C::STAGE);
+                uint8_t* sa = smem + s * C::STAGE;
+                uint8_t* sb = sa + C::A_BYTES;
+                if (!A_MN) {
+                    tc::tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
+                } else {
+                    tc::tma_load_2d_pair(sa, &tmA, fb, m0, kb * BK);
+                    tc::tma_load_2d_pair(sa + 8192, &tmA, fb, m0 + 64, kb * BK);
+                }
+                if (!B_MN) {
+                    tc::tma_load_2d_pair(sb, &tmB, fb, kb * BK, n0);
+                } else {
+                    tc::tma_load_2d_pair(sb, &tmB, fb, n0, kb * BK);
+                    tc::tma_load_2d_pair(sb + 8192, &tmB, fb, n0 + 64, kb * BK);
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA only)
+        constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, A_MN, B_MN);
+        uint32_t cnt = 0, local = 0;
+        for (int item = cid; item < n_items; item += ncl, ++local) {
+            const int rest = item / tiles_m2;
+            const int sp = rest / a.tiles_n;
+            const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
+            const uint32_t acc = local & 1, use = local >> 1;
+            tc::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+            tc::tc_fence_after();
+            const uint32_t dcol = tbase + acc * BN2;
+            for (int kb = kb0; kb < kb1; ++kb, ++cnt) {
+                const int s = cnt % C::STAGES;
+                const uint32_t ph = (cnt / C::STAGES) & 1;
+                tc::mbar_wait(&full[s], ph);
+                tc::tc_fence_after();
+                const uint32_t sa = tc::smem_u32(smem + s * C::STAGE);
+                const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                for (int ks = 0; ks < BK / 16; ++ks) {
+                    const uint64_t ad = A_MN ? tc::sdesc(sa + ks * 2048, 8192, 1024) : tc::sdesc(sa + ks * 32, 16, 1024);
+                    const uint64_t bd = B_MN ? tc::sdesc(sb + ks * 2048, 8192, 1024) : tc::sdesc(sb + ks * 32, 16, 1024);
+                    tc::mma_bf16_pair(dcol, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                }
+                tc::mma_commit_pair(&empty[s], 0x3);
+            }
+            tc::mma_commit_pair(&tfull[acc], 0x3);
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue (both CTAs: this CTA's 128 rows x all 256 columns)
+        const int ew = warp & 3;
+        const int half = (warp - 4) >> 2;
+        float* esm = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - 4) * 32 * 33;
+        uint32_t local = 0;
+        for (int item = cid; item < n_items; item += ncl, ++local) {
+            const int mt = item % tiles_m2, rest = item / tiles_m2;
+            const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
+            const uint32_t acc = local & 1, use = local >> 1;
+            tc::mbar_wait(&tfull[acc], use & 1);
+            tc::tc_fence_after();
+            const int row0 = mt * 2 * BM + (int)rank * BM + ew * 32, row = row0 + lane;
+            const int label = (a.epi == EPI_LSE && row < a.M) ? a.labels[row] : -1;
+            float lm = -INFINITY, ls = 0.f;
+            constexpr int HALF = BN2 / 2;
+#pragma unroll 1
+            for (int c = 0; c < HALF / 32; ++c) {
+                float v[32];
+                const int col = half * HALF + c * 32;
+                tc::tmem_ld32(tbase + acc * BN2 + col + ((uint32_t)(ew * 32) << 16), v);
+                epilogue_chunk(a, row0, nt * BN2 + col, v, sp, esm, lm, ls, label);
+            }
+            if (a.epi == EPI_LSE && row < a.M) {
+                float* p = a.part + ((long)row * a.n_parts + (nt * BN2 + half * HALF) / 128) * 2;
+                p[0] = lm;
+                p[1] = ls;
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive_cluster(tc::mapa(&tempty[acc], 0));
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::cluster_sync();
+    if (warp == 2) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_pair<2 * BN2>(tbase);
+    }
+}
+
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C, long ldc) {
     const long n = (long)M * N;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
@@ -404,7 +559,29 @@ void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, int g
     PARL_LAUNCHED();
 }
 
+template <int A_MN, int B_MN>
+void launch2(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, int grid, cudaStream_t st) {
+    auto k = k_gemm_tc2<A_MN, B_MN>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+        attr = true;
+    }
+    k<<<grid, NTHREADS, Cfg2::SMEM, st>>>(ma, mb, a);
+    PARL_LAUNCHED();
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// PARL_GEMM_PAIR=0 disables the CTA-pair kernel (diagnostics)
+bool pair_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PARL_GEMM_PAIR");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
 
 }  // namespace
 
@@ -420,13 +597,19 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
 
     // tile width: 128 when N is a multiple of 128 but not of 256, or N is small
     // (the LSE epilogue writes one (max, sumexp) partial per 128 columns: n_parts = ceil(N / 128))
-    const int BN = g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256);
+    // CTA pair (256 x 256 tiles) when the problem has enough of them; N must be a
+    // multiple of 128 so each CTA's half-tile of B is full-width aligned.
+    const int sms0 = num_sms();
+    const bool pair = pair_enabled() && g.M > 128 && g.N >= 256 && (g.N % 128) == 0 &&
+                      (long)((g.M + 255) / 256) * ((g.N + 255) / 256) >= sms0 / 4 && (a_k || b_mn);
+    const int BN = pair ? 256 : (g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256));
     CUtensorMap ma, mb;
     bool ok;
     if (a_k) ok = make_map(&ma, g.A, g.K, g.M, lda, BK, BM);
     else ok = make_map(&ma, g.A, g.M, g.K, lda, 64, BK);
     if (!ok) return false;
-    if (b_k) ok = make_map(&mb, g.B, g.K, g.N, ldb, BK, BN);
+    const int bbox = pair ? BN / 2 : BN;  // rows of B per CTA
+    if (b_k) ok = make_map(&mb, g.B, g.K, g.N, ldb, BK, bbox);
     else ok = make_map(&mb, g.B, g.N, g.K, ldb, 64, BK);
     if (!ok) return false;
 
@@ -443,11 +626,12 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     a.logits_act = static_cast<bf16*>(g.logits_act);
     a.n_parts = g.n_parts;
     const int sms = num_sms();
-    const int tiles = a.tiles_m * a.tiles_n;
+    const int tiles = pair ? ((g.M + 255) / 256) * a.tiles_n : a.tiles_m * a.tiles_n;
     a.splits = 1;
     a.kbs = a.nkb;
-    if (g.epi == EPI_F32_ACC && tiles < sms && a.nkb >= 4) {
-        int want = std::min((sms + tiles - 1) / tiles, a.nkb / 2);
+    const int slots = pair ? sms / 2 : sms;  // concurrently running tiles
+    if (g.epi == EPI_F32_ACC && tiles < slots && a.nkb >= 4) {
+        int want = std::min((slots + tiles - 1) / tiles, a.nkb / 2);
         want = std::max(want, 1);
         a.kbs = (a.nkb + want - 1) / want;
         a.splits = (a.nkb + a.kbs - 1) / a.kbs;
@@ -466,12 +650,18 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     if (a.splits > 1 && (g.N % 4) != 0) a.vec_ok = 0;
 
     const int items = tiles * a.splits;
-    const int grid = std::min(items, sms);
-    if (BN == 256) {
+    if (pair) {
+        const int grid = 2 * std::min(items, sms / 2);
+        if (a_k && b_k) launch2<0, 0>(ma, mb, a, grid, st);
+        else if (a_k && b_mn) launch2<0, 1>(ma, mb, a, grid, st);
+        else launch2<1, 1>(ma, mb, a, grid, st);
+    } else if (BN == 256) {
+        const int grid = std::min(items, sms);
         if (a_k && b_k) launch<256, 0, 0>(ma, mb, a, grid, st);
         else if (a_k && b_mn) launch<256, 0, 1>(ma, mb, a, grid, st);
         else launch<256, 1, 1>(ma, mb, a, grid, st);
     } else {
+        const int grid = std::min(items, sms);
         if (a_k && b_k) launch<128, 0, 0>(ma, mb, a, grid, st);
         else if (a_k && b_mn) launch<128, 0, 1>(ma, mb, a, grid, st);
         else launch<128, 1, 1>(ma, mb, a, grid, st);

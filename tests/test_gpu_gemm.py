@@ -54,7 +54,9 @@ def operands(torch, M, N, K, a_mn, b_mn, seed=0):
 
 
 LAYOUTS = [(0, 0), (0, 1), (1, 1)]
-SHAPES = [(128, 256, 64), (256, 512, 192), (296, 200, 104), (128, 896, 896), (1000, 384, 520), (64, 40, 24)]
+SHAPES = [(128, 256, 64), (256, 512, 192), (296, 200, 104), (128, 896, 896), (1000, 384, 520), (64, 40, 24),
+          # large enough for the CTA-pair (cta_group::2) kernel, with M/K tails
+          (4096, 1024, 512), (4000, 1152, 520), (8704, 896, 896)]
 
 
 @pytest.mark.parametrize("lay", LAYOUTS)
@@ -68,6 +70,16 @@ def test_layouts_f32(env, lay, shape):
     run(env, 0, A, sam, sak, B, sbn, sbk, M, N, K, EPI["F32"], bias=bias, Cf=out, ldc=N)
     err = (out - (ref + bias)).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+def test_split_k_accumulate_pair(env):
+    torch = env[0]
+    M, N, K = 896, 4864, 8704  # dW shape: pair kernel + split-K
+    A, sam, sak, B, sbn, sbk, ref = operands(torch, M, N, K, 1, 1, seed=9)
+    out = torch.zeros(M, N, device="cuda")
+    run(env, 0, A, sam, sak, B, sbn, sbk, M, N, K, EPI["F32_ACC"], Cf=out, ldc=N)
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 3e-5, err  # fp32 accumulation over K = 8704 in a different order than torch
 
 
 def test_split_k_accumulate(env):
