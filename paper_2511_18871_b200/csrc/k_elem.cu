@@ -77,25 +77,52 @@ __global__ void k_embed(const float* __restrict__ tok_emb, const float* __restri
 // K5: LayerNorm forward, one warp per row; rows optionally gathered through
 // `rows` (final LN over the head's predecessor rows).  Two-pass mean/variance
 // (population), eps 1e-5 (model.cpp:132, 317-343).
-template <class T>
+template <class T, int PER>
 __global__ void k_layernorm(const float* __restrict__ x, const int32_t* __restrict__ rows, int R, int D,
                             const float* __restrict__ gamma, const float* __restrict__ beta,
                             T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    // PER > 0: the row stays in registers (PER floats per lane, D <= 32 * PER); 0: strided passes
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= R) return;
     const int src = rows ? rows[warp] : warp;
     const float* xr = x + (long)src * D;
-    float s = 0.f;
-    for (int i = lane; i < D; i += 32) s += xr[i];
-    const float mean = warp_sum(s) / D;
-    float v = 0.f;
-    for (int i = lane; i < D; i += 32) {
-        const float c = xr[i] - mean;
-        v += c * c;
-    }
-    const float rstd = rsqrtf(warp_sum(v) / D + 1e-5f);
     T* yr = y + (long)warp * D;
-    for (int i = lane; i < D; i += 32) yr[i] = from_f<T>((xr[i] - mean) * rstd * gamma[i] + beta[i]);
+    float mean, rstd;
+    if constexpr (PER > 0) {
+        float v[PER];
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = lane + 32 * q;
+            v[q] = i < D ? xr[i] : 0.f;
+            s += v[q];
+        }
+        mean = warp_sum(s) / D;
+        float var = 0.f;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = lane + 32 * q;
+            const float c = i < D ? v[q] - mean : 0.f;
+            var += c * c;
+        }
+        rstd = rsqrtf(warp_sum(var) / D + 1e-5f);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = lane + 32 * q;
+            if (i < D) yr[i] = from_f<T>((v[q] - mean) * rstd * gamma[i] + beta[i]);
+        }
+    } else {
+        float s = 0.f;
+        for (int i = lane; i < D; i += 32) s += xr[i];
+        mean = warp_sum(s) / D;
+        float v = 0.f;
+        for (int i = lane; i < D; i += 32) {
+            const float c = xr[i] - mean;
+            v += c * c;
+        }
+        rstd = rsqrtf(warp_sum(v) / D + 1e-5f);
+        for (int i = lane; i < D; i += 32) yr[i] = from_f<T>((xr[i] - mean) * rstd * gamma[i] + beta[i]);
+    }
     if (lane == 0) {
         mean_out[warp] = mean;
         rstd_out[warp] = rstd;
@@ -137,10 +164,99 @@ __global__ void k_layernorm_bwd(const float* __restrict__ dy, const float* __res
 //   mode 0: out[c] += sum_r X[r][c]                                      (bias grads)
 //   mode 1: out[c] += sum_r dy[r][c]*xhat[r][c], out2[c] += sum_r dy[r][c] (LN gamma/beta)
 template <class T>
-__global__ void k_colsum_part(const T* __restrict__ X, long ldx, int R, int N, int rows_per_split,
-                              const float* __restrict__ xs, const int32_t* __restrict__ rows,
-                              const float* __restrict__ mean, const float* __restrict__ rstd, int mode,
-                              float* __restrict__ part_a, float* __restrict__ part_b) {
+struct Pair2;
+template <>
+struct Pair2<float> {
+    using V = float2;
+    static __device__ __forceinline__ float2 f(V v) { return v; }
+};
+template <>
+struct Pair2<bf16> {
+    using V = __nv_bfloat162;
+    static __device__ __forceinline__ float2 f(V v) { return __bfloat1622float2(v); }
+};
+
+// Block = 8 warps over 64 columns (2 per lane, one contiguous segment per row
+// per warp); warps stripe the block's row range with 4-row ILP.  Requires even
+// N and ldx (else the scalar kernel below is used).
+template <class T>
+__global__ void __launch_bounds__(256) k_colsum_part(const T* __restrict__ X, long ldx, int R, int N,
+                                                     int rows_per_split, const float* __restrict__ xs,
+                                                     const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, int mode,
+                                                     float* __restrict__ part_a, float* __restrict__ part_b) {
+    __shared__ float2 sa[8][32], sb[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = blockIdx.x * 64 + 2 * lane;
+    const int r0 = blockIdx.y * rows_per_split, r1 = min(R, r0 + rows_per_split);
+    float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+    if (c < N) {
+        int r = r0 + w;
+        for (; r + 24 < r1; r += 32) {
+            float2 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                v[q] = Pair2<T>::f(*reinterpret_cast<const typename Pair2<T>::V*>(X + (long)(r + 8 * q) * ldx + c));
+            if (mode == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a.x += v[q].x;
+                    a.y += v[q].y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int rr = r + 8 * q;
+                    const float2 xv = *reinterpret_cast<const float2*>(xs + (long)(rows ? rows[rr] : rr) * N + c);
+                    const float mu = mean[rr], rs = rstd[rr];
+                    a.x += v[q].x * (xv.x - mu) * rs;
+                    a.y += v[q].y * (xv.y - mu) * rs;
+                    b.x += v[q].x;
+                    b.y += v[q].y;
+                }
+            }
+        }
+        for (; r < r1; r += 8) {
+            const float2 v = Pair2<T>::f(*reinterpret_cast<const typename Pair2<T>::V*>(X + (long)r * ldx + c));
+            if (mode == 0) {
+                a.x += v.x;
+                a.y += v.y;
+            } else {
+                const float2 xv = *reinterpret_cast<const float2*>(xs + (long)(rows ? rows[r] : r) * N + c);
+                a.x += v.x * (xv.x - mean[r]) * rstd[r];
+                a.y += v.y * (xv.y - mean[r]) * rstd[r];
+                b.x += v.x;
+                b.y += v.y;
+            }
+        }
+    }
+    sa[w][lane] = a;
+    sb[w][lane] = b;
+    __syncthreads();
+    if (w == 0 && c < N) {
+        float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            ta.x += sa[i][lane].x;
+            ta.y += sa[i][lane].y;
+            tb.x += sb[i][lane].x;
+            tb.y += sb[i][lane].y;
+        }
+        part_a[(long)blockIdx.y * N + c] = ta.x;
+        part_a[(long)blockIdx.y * N + c + 1] = ta.y;
+        if (mode == 1) {
+            part_b[(long)blockIdx.y * N + c] = tb.x;
+            part_b[(long)blockIdx.y * N + c + 1] = tb.y;
+        }
+    }
+}
+
+// scalar variant (odd N / ldx)
+template <class T>
+__global__ void k_colsum_part1(const T* __restrict__ X, long ldx, int R, int N, int rows_per_split,
+                               const float* __restrict__ xs, const int32_t* __restrict__ rows,
+                               const float* __restrict__ mean, const float* __restrict__ rstd, int mode,
+                               float* __restrict__ part_a, float* __restrict__ part_b) {
     __shared__ float sa[8][33], sb[8][33];
     const int c = blockIdx.x * 32 + threadIdx.x;
     const int ty = threadIdx.y;
@@ -204,14 +320,20 @@ struct Scratch {
 template <class T>
 static void colsum_impl(const T* X, long ldx, int R, int N, float* out, const float* xs, const int32_t* rows,
                         const float* mean, const float* rstd, float* out2, int mode, cudaStream_t st) {
-    const int col_blocks = cdiv(N, 32);
-    int splits = std::max(1, std::min(cdiv(R, 64), cdiv(4 * 148, col_blocks)));
+    const bool vec = (N % 2 == 0) && (ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 7) == 0);
+    const int cw = vec ? 64 : 32;
+    const int col_blocks = cdiv(N, cw);
+    int splits = std::max(1, std::min(cdiv(R, 128), cdiv(4 * 148, col_blocks)));
     const int rps = cdiv(R, splits);
     splits = cdiv(R, rps);
     float* pa = g_colsum_scratch.get((size_t)2 * splits * N);
     float* pb = pa + (size_t)splits * N;
-    k_colsum_part<T><<<dim3(col_blocks, splits), dim3(32, 8), 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd, mode,
-                                                                      pa, pb);
+    if (vec)
+        k_colsum_part<T><<<dim3(col_blocks, splits), 256, 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd, mode, pa,
+                                                                   pb);
+    else
+        k_colsum_part1<T><<<dim3(col_blocks, splits), dim3(32, 8), 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd,
+                                                                           mode, pa, pb);
     PARL_LAUNCHED();
     k_colsum_final<<<cdiv(N, 256), 256, 0, st>>>(pa, pb, splits, N, out, out2, mode);
     PARL_LAUNCHED();
@@ -565,7 +687,10 @@ template <class T>
 void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
                       float* mean, float* rstd, cudaStream_t st) {
     if (R <= 0) return;
-    k_layernorm<T><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    if (D <= 256) k_layernorm<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    else if (D <= 1024) k_layernorm<T, 32><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    else if (D <= 2048) k_layernorm<T, 64><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    else k_layernorm<T, 0><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
     PARL_LAUNCHED();
 }
 template void launch_layernorm<float>(const float*, const int32_t*, int, int, const float*, const float*, float*,
