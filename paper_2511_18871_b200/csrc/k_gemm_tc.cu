@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 p[1] = ls;
             }
             tc::tc_fence_before();
-            tc::mbar_arrive(&tempty[acc]);
+            tc::mbar_arrive_relaxed(&tempty[acc]);
         }
     }
     __syncthreads();
@@ -466,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 p[1] = ls;
             }
             tc::tc_fence_before();
-            tc::mbar_arrive_cluster(tc::mapa(&tempty[acc], 0));
+            tc::mbar_arrive_cluster_relaxed(tc::mapa(&tempty[acc], 0));
         }
     }
     tc::tc_fence_before();

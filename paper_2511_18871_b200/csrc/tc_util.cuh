@@ -162,6 +162,14 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed arrives: signal-only (no ordering of this thread's prior memory
+// operations), for barriers that only track TMEM reads fenced by tcgen05.fence.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // 2D tile load into this CTA's smem, completing bytes on the leader CTA's barrier
 __device__ __forceinline__ void tma_load_2d_pair(void* smem, const CUtensorMap* map, uint32_t leader_bar, int c0,
                                                  int c1) {
