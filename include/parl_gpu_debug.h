@@ -11,7 +11,8 @@ extern "C" {
 #endif
 /* C[M x N] (epilogue `epi`, see csrc/internal.cuh Epi) = sum_k A(m,k) B(n,k),
  * A(m,k) = A[m*sam + k*sak], B(n,k) = B[n*sbn + k*sbk]; bf16 device operands.
- * path: 0 = tcgen05 (fails with PARL_E_CONFIG if the shape is not supported),
+ * path: 0 = tcgen05 (fails with PARL_E_CONFIG if the shape is not supported), 2 = the same without the
+ *       trailing device synchronisation (timing loops),
  *       1 = FFMA tile kernel.  Synchronises the current device. */
 parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const void* A, long sam, long sak, const void* B,
                                  long sbn, long sbk, int epi, const float* bias, float* Cf, long ldc,

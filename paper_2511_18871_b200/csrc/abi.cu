@@ -1542,13 +1542,13 @@ extern "C" parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const
         g.epi = epi; g.bias = bias; g.Cf = Cf; g.ldc = ldc; g.resid = resid; g.Ca = Ca; g.ldca = ldca;
         g.Caux = Caux; g.aux_in = aux_in; g.labels = labels; g.part = part; g.target = target;
         g.logits_act = logits_act; g.n_parts = n_parts; g.part_cols = 128;
-        if (path == 0) {
+        if (path == 0 || path == 2) {  // 2: tcgen05, no device sync (timing loops)
             PARL_REQUIRE(gemm_tc(g, 0), PARL_E_CONFIG, "shape/layout not supported by the tcgen05 kernel");
         } else {
             gemm_simt<bf16>(g, 0);
         }
         PARL_CUDA(cudaGetLastError());
-        PARL_CUDA(cudaDeviceSynchronize());
+        if (path != 2) PARL_CUDA(cudaDeviceSynchronize());
     });
 }
 

@@ -18,6 +18,7 @@
 // dX/dW loops of `backward` (model.cpp:652-817).
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "internal.cuh"
@@ -30,23 +31,20 @@ namespace {
 constexpr int BM = 128, BK = 64;
 constexpr int EPI_WARPS = 8;                      // two per TMEM lane quadrant, each half the columns
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;    // warps 0-3 producer/MMA/TMEM/spare, 4.. epilogue
+constexpr int STG_BYTES = 4096;                   // epilogue staging buffer: 32 rows x 128 B
+constexpr int EPI_SMEM = EPI_WARPS * 2 * STG_BYTES;  // double-buffered per epilogue warp
 
 struct TcArgs {
-    int M, N, K, nkb, tiles_m, tiles_n, splits, kbs, epi, vec_ok;
+    int M, N, K, nkb, tiles_m, tiles_n, splits, kbs, epi;
     const float* bias;
-    float* Cf;
-    long ldc;
-    const float* resid;
-    bf16* Ca;
-    long ldca;
-    bf16* Caux;
-    const bf16* aux_in;
+    int bias_vec;          // bias is 16-byte aligned
     const int32_t* labels;
     float* part;
     float* target;
-    bf16* logits_act;
     int n_parts;
-    float* ws;  // split-K partials [splits x M x N]
+    int store_logits;      // EPI_LSE: also store bf16 logits (policy, for the backward) by TMA
+    bf16* logits_direct;   // EPI_LSE: ... or by plain stores when the row stride is not 16-byte aligned
+    long ldl;
 };
 
 template <int BN>
@@ -54,17 +52,18 @@ struct Cfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
-    static constexpr int EPI_OFF = STAGES * STAGE + 256;                  // after the barriers
-    static constexpr int SMEM = EPI_OFF + EPI_WARPS * 32 * 33 * 4 + 1024;  // + per-warp epilogue tiles + align
+    static constexpr int STAGES = BN == 256 ? 3 : 4;
+    static constexpr int STG_OFF = STAGES * STAGE;  // 1024-aligned
+    static constexpr int BAR_OFF = STG_OFF + EPI_SMEM;
+    static constexpr int SMEM = BAR_OFF + 512 + 1024;
 };
 
 // Phi(x) = 0.5 (1 + erf(x / sqrt 2)) with Abramowitz-Stegun 7.1.26 (|erf err| <= 1.5e-7,
 // far below the bf16 rounding of the outputs); returns exp(-x^2/2) for GELU' too.
 __device__ __forceinline__ float phi_fast(float x, float& e) {
     const float z = fabsf(x) * 0.70710678118654752f;
-    const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
-    e = __expf(-z * z);
+    const float t = tc::rcp_approx(fmaf(0.3275911f, z, 1.f));
+    e = tc::ex2_approx(-z * z * 1.4426950408889634f);
     const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
                                 0.254829592f);
     const float erf_abs = 1.f - poly * e;
@@ -80,130 +79,243 @@ __device__ __forceinline__ float gelu_grad_dev(float x) {  // Phi(x) + x phi(x) 
     return p + x * 0.39894228040143267794f * e;
 }
 
-// Epilogue of one 32-row x 32-column chunk.  v[] arrives in the TMEM layout
-// (lane = tile row).  Element-wise epilogues are transposed through a padded
-// per-warp smem tile so that lane = column and every global access is a
-// coalesced row segment; the LSE epilogue reduces along its own row first.
-__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, int row0, int col0, float* v, int split,
-                                               float* sm /* [32][33] */, float& lse_m, float& lse_s, int label) {
-    const int lane = threadIdx.x & 31;
-    const int row = row0 + lane;
-    if (a.epi == EPI_LSE) {
-        const int ncol = min(32, a.N - col0);
-        if (row < a.M && ncol > 0) {
-            float cm = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                v[j] += (j < ncol && a.bias) ? a.bias[col0 + j] : 0.f;
-                if (j < ncol) cm = fmaxf(cm, v[j]);
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// byte offset of 16-byte chunk j of row r in a [32 x 128 B] SWIZZLE_128B / [32 x 64 B] SWIZZLE_64B tile
+__device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+__device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
+
+// The CTA's sequence of output tiles (both kernels share the epilogue).
+struct EpiSeq {
+    int first, stride, n_items, tiles_me;  // items first, first+stride, ...; m-tiles per n column
+    int mrows;                             // rows per m-tile (128, or 256 for a CTA pair)
+    int rank;                              // CTA rank within the pair
+};
+
+// Epilogue warps (4..11).  Thread = accumulator row (TMEM lane); warp w owns
+// lane quadrant w%4 and half of the tile's columns, in 32-column chunks:
+//   tcgen05.ld 32 columns -> registers -> fused math (bias, residual, GELU,
+//   GELU', log-sum-exp) -> swizzled smem staging -> one TMA bulk store per
+//   chunk (reduce-add for in-place gradient accumulation).
+// Inputs of the epilogue (fp32 residual, bf16 GELU pre-activation) arrive by
+// TMA into the same staging buffer one chunk ahead.  Two staging buffers per
+// warp let the store of chunk k drain while chunk k+1 is computed.
+template <int BNT, class Release>
+__device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMap* mo, const CUtensorMap* mo2,
+                                               const CUtensorMap* mi, uint8_t* stg_all, uint64_t* inbar_all,
+                                               uint64_t* tfull, uint32_t tbase, const EpiSeq& e, Release release) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ew = warp & 3, half = (warp - 4) >> 2, wi = warp - 4;
+    constexpr int HALF = BNT / 2, NCH = HALF / 32;
+    uint8_t* stg = stg_all + wi * 2 * STG_BYTES;
+    const uint32_t stg_s = tc::smem_u32(stg);
+    uint64_t* inbar = inbar_all + wi * 2;
+    const int epi = a.epi;
+    const bool has_in = epi == EPI_RESID || epi == EPI_GELU_BWD;
+    const uint32_t in_bytes = epi == EPI_RESID ? 4096u : 2048u;
+    const bool do_store = epi != EPI_LSE || a.store_logits;
+
+    auto coords = [&](int item, int& row, int& col, int& sp) {
+        const int mt = item % e.tiles_me, rest = item / e.tiles_me;
+        const int nt = rest % a.tiles_n;
+        sp = rest / a.tiles_n;
+        row = mt * e.mrows + e.rank * BM + ew * 32;
+        col = nt * BNT + half * HALF;
+    };
+    auto issue_in = [&](int item, int c, int b) {
+        int row, col, sp;
+        coords(item, row, col, sp);
+        tc::mbar_expect_tx(&inbar[b], in_bytes);
+        tc::tma_load_2d(stg + b * STG_BYTES, mi, &inbar[b], col + c * 32, row);
+    };
+
+    uint32_t k = 0, local = 0;
+    if (has_in && lane == 0 && e.first < e.n_items) issue_in(e.first, 0, 0);
+    for (int item = e.first; item < e.n_items; item += e.stride, ++local) {
+        const uint32_t acc = local & 1, use = local >> 1;
+        tc::mbar_wait(&tfull[acc], use & 1);
+        tc::tc_fence_after();
+        int row0, colh, sp;
+        coords(item, row0, colh, sp);
+        const int row = row0 + lane;
+        const int label = (epi == EPI_LSE && row < a.M) ? a.labels[row] : -1;
+        float lm = -INFINITY, ls = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c, ++k) {
+            const int col = colh + c * 32;
+            const uint32_t b = k & 1;
+            const uint32_t sb = stg_s + b * STG_BYTES;
+            float v[32];
+            tc::tmem_ld32(tbase + acc * BNT + half * HALF + c * 32 + ((uint32_t)(ew * 32) << 16), v);
+            if (c == NCH - 1) {  // accumulator fully read: hand it back to the MMA warp
+                tc::tc_fence_before();
+                release(acc);
             }
-            const float nm = fmaxf(lse_m, cm);
-            float s = lse_s * __expf(lse_m - nm);
+            if (a.bias) {
+                if (a.bias_vec && col + 32 <= a.N) {
+                    const float4* bp = reinterpret_cast<const float4*>(a.bias + col);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j < ncol) s += __expf(v[j] - nm);
-            lse_m = nm;
-            lse_s = s;
-            const int lj = label - col0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (j == lj) a.target[row] = v[j];
-        }
-        if (!a.logits_act) return;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) sm[lane * 33 + j] = v[j];
-    __syncwarp();
-    const int col = col0 + lane;
-    if (col < a.N) {
-        const float b = (a.bias && a.epi != EPI_LSE) ? a.bias[col] : 0.f;
-        const int rmax = min(32, a.M - row0);
-        switch (a.epi) {
-            case EPI_F32:
-                for (int r = 0; r < rmax; ++r) a.Cf[(long)(row0 + r) * a.ldc + col] = sm[r * 33 + lane] + b;
-                break;
-            case EPI_F32_ACC:
-                if (a.splits > 1) {
-                    for (int r = 0; r < rmax; ++r)
-                        a.ws[((long)split * a.M + row0 + r) * a.N + col] = sm[r * 33 + lane];
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 t = __ldg(bp + j);
+                        v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+                    }
                 } else {
-                    // batch the loads first: stores may alias, so the compiler
-                    // would otherwise serialise every load behind a store
 #pragma unroll
-                    for (int h = 0; h < 32; h += 16) {
-                        float old[16];
+                    for (int j = 0; j < 32; ++j)
+                        if (col + j < a.N) v[j] += __ldg(a.bias + col + j);
+                }
+            }
+            if (has_in) {
+                tc::mbar_wait(&inbar[b], (k >> 1) & 1);
+            } else if (do_store) {  // the store issued from this buffer two chunks ago has read it
+                if (lane == 0) tc::bulk_wait_read<1>();
+                __syncwarp();
+            }
+            switch (epi) {
+                case EPI_F32:
+                case EPI_F32_ACC:
 #pragma unroll
-                        for (int r = 0; r < 16; ++r)
-                            old[r] = h + r < rmax ? a.Cf[(long)(row0 + h + r) * a.ldc + col] : 0.f;
+                    for (int j = 0; j < 8; ++j)
+                        tc::sts128(sb + sw128(lane, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                   __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+                    break;
+                case EPI_RESID:
 #pragma unroll
-                        for (int r = 0; r < 16; ++r)
-                            if (h + r < rmax)
-                                a.Cf[(long)(row0 + h + r) * a.ldc + col] = old[r] + sm[(h + r) * 33 + lane];
+                    for (int j = 0; j < 8; ++j) {
+                        uint32_t r0, r1, r2, r3;
+                        const uint32_t ad = sb + sw128(lane, j);
+                        tc::lds128(ad, r0, r1, r2, r3);
+                        tc::sts128(ad, __float_as_uint(__uint_as_float(r0) + v[4 * j]),
+                                   __float_as_uint(__uint_as_float(r1) + v[4 * j + 1]),
+                                   __float_as_uint(__uint_as_float(r2) + v[4 * j + 2]),
+                                   __float_as_uint(__uint_as_float(r3) + v[4 * j + 3]));
+                    }
+                    break;
+                case EPI_ACT:
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        tc::sts128(sb + sw64(lane, j), pack_bf16(v[8 * j], v[8 * j + 1]),
+                                   pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                   pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                    break;
+                case EPI_GELU:
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t u[4], g[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            u[q] = pack_bf16(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
+                            g[q] = pack_bf16(gelu_dev(bf_lo(u[q])), gelu_dev(bf_hi(u[q])));
+                        }
+                        tc::sts128(sb + sw64(lane, j), u[0], u[1], u[2], u[3]);
+                        tc::sts128(sb + 2048 + sw64(lane, j), g[0], g[1], g[2], g[3]);
+                    }
+                    break;
+                case EPI_GELU_BWD:
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t x[4];
+                        const uint32_t ad = sb + sw64(lane, j);
+                        tc::lds128(ad, x[0], x[1], x[2], x[3]);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            x[q] = pack_bf16(v[8 * j + 2 * q] * gelu_grad_dev(bf_lo(x[q])),
+                                             v[8 * j + 2 * q + 1] * gelu_grad_dev(bf_hi(x[q])));
+                        tc::sts128(ad, x[0], x[1], x[2], x[3]);
+                    }
+                    break;
+                case EPI_LSE: {
+                    const int ncol = min(32, a.N - col);
+                    float cm = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < ncol) cm = fmaxf(cm, v[j]);
+                    const float nm = fmaxf(lm, cm);
+                    const float nml = nm * 1.4426950408889634f;
+                    float s = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < ncol) s += tc::ex2_approx(fmaf(v[j], 1.4426950408889634f, -nml));
+                    ls = ls * tc::ex2_approx((lm - nm) * 1.4426950408889634f) + s;
+                    lm = nm;
+                    const int lj = label - col;
+                    if ((unsigned)lj < 32u) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (j == lj) a.target[row] = v[j];
+                    }
+                    if (a.logits_direct && row < a.M) {
+                        bf16* dst = a.logits_direct + (long)row * a.ldl + col;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (j < ncol) dst[j] = __float2bfloat16_rn(v[j]);
+                    }
+                    if (a.store_logits) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            tc::sts128(sb + sw64(lane, j), pack_bf16(v[8 * j], v[8 * j + 1]),
+                                       pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                       pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+                    }
+                    break;
+                }
+                default:
+                    break;
+            }
+            if (do_store) {
+                tc::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (epi == EPI_F32_ACC) {
+                        if (a.splits > 1) tc::tma_store_3d(mo, sb, col, row0, sp);
+                        else tc::tma_reduce_add_2d(mo, sb, col, row0);
+                    } else {
+                        tc::tma_store_2d(mo, sb, col, row0);
+                        if (epi == EPI_GELU) tc::tma_store_2d(mo2, sb + 2048, col, row0);
+                    }
+                    tc::bulk_commit();
+                    if (has_in) {  // prefetch the next chunk's input into the other buffer
+                        int ni = item, nc = c + 1;
+                        if (nc == NCH) {
+                            ni = item + e.stride;
+                            nc = 0;
+                        }
+                        if (ni < e.n_items) {
+                            tc::bulk_wait_read<1>();  // the store that last used it has read it
+                            issue_in(ni, nc, b ^ 1);
+                        }
                     }
                 }
-                break;
-            case EPI_ACT:
-                for (int r = 0; r < rmax; ++r)
-                    a.Ca[(long)(row0 + r) * a.ldca + col] = __float2bfloat16_rn(sm[r * 33 + lane] + b);
-                break;
-            case EPI_RESID: {
-#pragma unroll
-                for (int h = 0; h < 32; h += 16) {
-                    float rv[16];
-#pragma unroll
-                    for (int r = 0; r < 16; ++r)
-                        rv[r] = h + r < rmax ? a.resid[(long)(row0 + h + r) * a.ldc + col] : 0.f;
-#pragma unroll
-                    for (int r = 0; r < 16; ++r)
-                        if (h + r < rmax) a.Cf[(long)(row0 + h + r) * a.ldc + col] = rv[r] + (sm[(h + r) * 33 + lane] + b);
-                }
-                break;
             }
-            case EPI_GELU:
-                for (int r = 0; r < rmax; ++r) {
-                    const long o = (long)(row0 + r) * a.ldca + col;
-                    const bf16 u = __float2bfloat16_rn(sm[r * 33 + lane] + b);
-                    a.Ca[o] = u;
-                    a.Caux[o] = __float2bfloat16_rn(gelu_dev(__bfloat162float(u)));
-                }
-                break;
-            case EPI_GELU_BWD: {
-#pragma unroll
-                for (int h = 0; h < 32; h += 16) {
-                    bf16 uv[16];
-#pragma unroll
-                    for (int r = 0; r < 16; ++r)
-                        uv[r] = h + r < rmax ? a.aux_in[(long)(row0 + h + r) * a.ldca + col] : __float2bfloat16_rn(0.f);
-#pragma unroll
-                    for (int r = 0; r < 16; ++r)
-                        if (h + r < rmax)
-                            a.Ca[(long)(row0 + h + r) * a.ldca + col] =
-                                __float2bfloat16_rn(sm[(h + r) * 33 + lane] * gelu_grad_dev(__bfloat162float(uv[r])));
-                }
-                break;
-            }
-            case EPI_LSE:
-                for (int r = 0; r < rmax; ++r)
-                    a.logits_act[(long)(row0 + r) * a.ldca + col] = __float2bfloat16_rn(sm[r * 33 + lane]);
-                break;
-            default:
-                break;
+        }
+        if (epi == EPI_LSE && row < a.M) {  // one (max, sumexp) partial per 128 columns
+            float* p = a.part + ((long)row * a.n_parts + colh / 128) * 2;
+            p[0] = lm;
+            p[1] = ls;
         }
     }
+    if (lane == 0) tc::bulk_wait<0>();
     __syncwarp();
 }
 
 template <int BN, int A_MN, int B_MN>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
+              const __grid_constant__ CUtensorMap tmI, TcArgs a) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x 2]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + 2 * EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_items = a.tiles_m * a.tiles_n * a.splits;
@@ -217,6 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], 32 * EPI_WARPS);
         }
+        for (int s = 0; s < 2 * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
@@ -285,36 +398,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::mma_commit(&tfull[acc]);
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue
-        const int ew = warp & 3;           // TMEM lane quadrant (a warp may only touch lanes 32*(warp%4)..)
-        const int half = (warp - 4) >> 2;  // which half of the tile's columns
-        float* esm = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - 4) * 32 * 33;
-        uint32_t local = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-            const int mt = item % a.tiles_m, rest = item / a.tiles_m;
-            const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
-            const uint32_t acc = local & 1, use = local >> 1;
-            tc::mbar_wait(&tfull[acc], use & 1);
-            tc::tc_fence_after();
-            const int row0 = mt * BM + ew * 32, row = row0 + lane;
-            const int label = (a.epi == EPI_LSE && row < a.M) ? a.labels[row] : -1;
-            float lm = -INFINITY, ls = 0.f;
-            constexpr int HALF = BN / 2;
-#pragma unroll 1
-            for (int c = 0; c < HALF / 32; ++c) {
-                float v[32];
-                const int col = half * HALF + c * 32;
-                tc::tmem_ld32(tbase + acc * BN + col + ((uint32_t)(ew * 32) << 16), v);
-                epilogue_chunk(a, row0, nt * BN + col, v, sp, esm, lm, ls, label);
-            }
-            if (a.epi == EPI_LSE && row < a.M) {  // partials per 128 columns
-                float* p = a.part + ((long)row * a.n_parts + (nt * BN + half * HALF) / 128) * 2;
-                p[0] = lm;
-                p[1] = ls;
-            }
-            tc::tc_fence_before();
-            tc::mbar_arrive_relaxed(&tempty[acc]);
-        }
+        const EpiSeq e{(int)blockIdx.x, (int)gridDim.x, n_items, a.tiles_m, BM, 0};
+        epilogue_warps<BN>(a, &tmO, &tmO2, &tmI, smem + C::STG_OFF, inbar, tfull, tbase, e,
+                           [&](uint32_t acc) { tc::mbar_arrive_relaxed(&tempty[acc]); });
     }
     __syncthreads();
     if (warp == 2) {
@@ -328,29 +414,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // CTA loads its 128 rows of A and its 128 columns of B; the leader CTA issues
 // tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs' shared memory and
 // writes each CTA's 128 accumulator rows into its own TMEM.  Per SM this halves
-// the operand bytes per MMA cycle relative to the 1-CTA 128 x 256 tile, so the
-// 6-stage ring covers the TMA latency.
+// the operand bytes per MMA cycle relative to the 1-CTA 128 x 256 tile.
 constexpr int BN2 = 256;
 struct Cfg2 {
     static constexpr int A_BYTES = BM * BK * 2;          // 128 rows of A
     static constexpr int B_BYTES = (BN2 / 2) * BK * 2;   // 128 columns of B
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = 6;
-    static constexpr int EPI_OFF = STAGES * STAGE + 256;
-    static constexpr int SMEM = EPI_OFF + EPI_WARPS * 32 * 33 * 4 + 1024;
+    static constexpr int STAGES = 4;
+    static constexpr int STG_OFF = STAGES * STAGE;
+    static constexpr int BAR_OFF = STG_OFF + EPI_SMEM;
+    static constexpr int SMEM = BAR_OFF + 512 + 1024;
 };
 
 template <int A_MN, int B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
+               const __grid_constant__ CUtensorMap tmI, TcArgs a) {
     using C = Cfg2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x 2]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + 2 * EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_ctarank();
@@ -367,6 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], 2 * 32 * EPI_WARPS);  // both CTAs' epilogue threads
         }
+        for (int s = 0; s < 2 * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
@@ -439,35 +529,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs: this CTA's 128 rows x all 256 columns)
-        const int ew = warp & 3;
-        const int half = (warp - 4) >> 2;
-        float* esm = reinterpret_cast<float*>(smem + C::EPI_OFF) + (warp - 4) * 32 * 33;
-        uint32_t local = 0;
-        for (int item = cid; item < n_items; item += ncl, ++local) {
-            const int mt = item % tiles_m2, rest = item / tiles_m2;
-            const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
-            const uint32_t acc = local & 1, use = local >> 1;
-            tc::mbar_wait(&tfull[acc], use & 1);
-            tc::tc_fence_after();
-            const int row0 = mt * 2 * BM + (int)rank * BM + ew * 32, row = row0 + lane;
-            const int label = (a.epi == EPI_LSE && row < a.M) ? a.labels[row] : -1;
-            float lm = -INFINITY, ls = 0.f;
-            constexpr int HALF = BN2 / 2;
-#pragma unroll 1
-            for (int c = 0; c < HALF / 32; ++c) {
-                float v[32];
-                const int col = half * HALF + c * 32;
-                tc::tmem_ld32(tbase + acc * BN2 + col + ((uint32_t)(ew * 32) << 16), v);
-                epilogue_chunk(a, row0, nt * BN2 + col, v, sp, esm, lm, ls, label);
-            }
-            if (a.epi == EPI_LSE && row < a.M) {
-                float* p = a.part + ((long)row * a.n_parts + (nt * BN2 + half * HALF) / 128) * 2;
-                p[0] = lm;
-                p[1] = ls;
-            }
-            tc::tc_fence_before();
-            tc::mbar_arrive_cluster_relaxed(tc::mapa(&tempty[acc], 0));
-        }
+        const EpiSeq e{cid, ncl, n_items, tiles_m2, 2 * BM, (int)rank};
+        const uint32_t leader_tempty0 = tc::mapa(&tempty[0], 0);
+        epilogue_warps<BN2>(a, &tmO, &tmO2, &tmI, smem + C::STG_OFF, inbar, tfull, tbase, e, [&](uint32_t acc) {
+            tc::mbar_arrive_cluster_relaxed(leader_tempty0 + acc * 8);
+        });
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -502,7 +568,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// bf16 2D map: inner (contiguous) extent, outer extent, outer stride (elements), box.
+// bf16 2D operand map: inner (contiguous) extent, outer extent, outer stride (elements), box.
 bool make_map(CUtensorMap* m, const void* base, long inner, long outer, long stride_elems, int box_inner,
               int box_outer) {
     auto fn = encode_fn();
@@ -513,6 +579,27 @@ bool make_map(CUtensorMap* m, const void* base, long inner, long outer, long str
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Epilogue tile map: [rows x cols] (optionally x `planes`) row-major with row
+// stride ld (elements); 32 x 32 boxes; fp32 rows use SWIZZLE_128B, bf16 rows
+// SWIZZLE_64B (matching sw128 / sw64 in the epilogue).
+bool make_epi_map(CUtensorMap* m, const void* base, bool f32, long cols, long rows, long ld, int planes = 1) {
+    auto fn = encode_fn();
+    if (!fn || !base || !aligned16(base)) return false;
+    const int es = f32 ? 4 : 2;
+    if ((ld * es) % 16) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * es, (cuuint64_t)ld * es * rows};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t el[3] = {1, 1, 1};
+    CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, planes > 1 ? 3 : 2,
+                    const_cast<void*>(base), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -547,31 +634,33 @@ struct Workspace {
 };
 Workspace g_ws;
 
+struct Maps {
+    CUtensorMap a, b, o, o2, i;
+};
+
 template <int BN, int A_MN, int B_MN>
-void launch(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, int grid, cudaStream_t st) {
+void launch(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
     auto k = k_gemm_tc<BN, A_MN, B_MN>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
         attr = true;
     }
-    k<<<grid, NTHREADS, Cfg<BN>::SMEM, st>>>(ma, mb, a);
+    k<<<grid, NTHREADS, Cfg<BN>::SMEM, st>>>(m.a, m.b, m.o, m.o2, m.i, a);
     PARL_LAUNCHED();
 }
 
 template <int A_MN, int B_MN>
-void launch2(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, int grid, cudaStream_t st) {
+void launch2(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
     auto k = k_gemm_tc2<A_MN, B_MN>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
         attr = true;
     }
-    k<<<grid, NTHREADS, Cfg2::SMEM, st>>>(ma, mb, a);
+    k<<<grid, NTHREADS, Cfg2::SMEM, st>>>(m.a, m.b, m.o, m.o2, m.i, a);
     PARL_LAUNCHED();
 }
-
-inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // PARL_GEMM_PAIR=0 disables the CTA-pair kernel (diagnostics)
 bool pair_enabled() {
@@ -599,18 +688,19 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     // (the LSE epilogue writes one (max, sumexp) partial per 128 columns: n_parts = ceil(N / 128))
     // CTA pair (256 x 256 tiles) when the problem has enough of them; N must be a
     // multiple of 128 so each CTA's half-tile of B is full-width aligned.
-    const int sms0 = num_sms();
+    const int sms = num_sms();
     const bool pair = pair_enabled() && g.M > 128 && g.N >= 256 && (g.N % 128) == 0 &&
-                      (long)((g.M + 255) / 256) * ((g.N + 255) / 256) >= sms0 / 4 && (a_k || b_mn);
+                      (long)((g.M + 255) / 256) * ((g.N + 255) / 256) >= sms / 4 && (a_k || b_mn);
     const int BN = pair ? 256 : (g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256));
-    CUtensorMap ma, mb;
+    Maps mp;
+    std::memset(&mp, 0, sizeof(mp));
     bool ok;
-    if (a_k) ok = make_map(&ma, g.A, g.K, g.M, lda, BK, BM);
-    else ok = make_map(&ma, g.A, g.M, g.K, lda, 64, BK);
+    if (a_k) ok = make_map(&mp.a, g.A, g.K, g.M, lda, BK, BM);
+    else ok = make_map(&mp.a, g.A, g.M, g.K, lda, 64, BK);
     if (!ok) return false;
     const int bbox = pair ? BN / 2 : BN;  // rows of B per CTA
-    if (b_k) ok = make_map(&mb, g.B, g.K, g.N, ldb, BK, bbox);
-    else ok = make_map(&mb, g.B, g.N, g.K, ldb, 64, BK);
+    if (b_k) ok = make_map(&mp.b, g.B, g.K, g.N, ldb, BK, bbox);
+    else ok = make_map(&mp.b, g.B, g.N, g.K, ldb, 64, BK);
     if (!ok) return false;
 
     TcArgs a{};
@@ -619,13 +709,11 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     a.tiles_m = (g.M + BM - 1) / BM;
     a.tiles_n = (g.N + BN - 1) / BN;
     a.epi = g.epi;
-    a.bias = g.bias; a.Cf = g.Cf; a.ldc = g.ldc; a.resid = g.resid;
-    a.Ca = static_cast<bf16*>(g.Ca); a.ldca = g.ldca; a.Caux = static_cast<bf16*>(g.Caux);
-    a.aux_in = static_cast<const bf16*>(g.aux_in);
+    a.bias = g.bias;
+    a.bias_vec = g.bias && aligned16(g.bias);
     a.labels = g.labels; a.part = g.part; a.target = g.target;
-    a.logits_act = static_cast<bf16*>(g.logits_act);
     a.n_parts = g.n_parts;
-    const int sms = num_sms();
+    a.store_logits = g.logits_act != nullptr;
     const int tiles = pair ? ((g.M + 255) / 256) * a.tiles_n : a.tiles_m * a.tiles_n;
     a.splits = 1;
     a.kbs = a.nkb;
@@ -635,41 +723,68 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
         want = std::max(want, 1);
         a.kbs = (a.nkb + want - 1) / want;
         a.splits = (a.nkb + a.kbs - 1) / a.kbs;
-        if (a.splits > 1) {
-            a.ws = g_ws.get((size_t)a.splits * g.M * g.N * sizeof(float));
-            if (!a.ws) return false;
-        }
     }
-    a.vec_ok = ((g.ldc % 4) == 0 && (g.ldca % 8) == 0 && (g.N % 4) == 0) ? 1 : 0;
-    if (g.Cf && !aligned16(g.Cf)) a.vec_ok = 0;
-    if (g.Ca && !aligned16(g.Ca)) a.vec_ok = 0;
-    if (g.Caux && !aligned16(g.Caux)) a.vec_ok = 0;
-    if (g.aux_in && !aligned16(g.aux_in)) a.vec_ok = 0;
-    if (g.resid && !aligned16(g.resid)) a.vec_ok = 0;
-    if (g.logits_act && !aligned16(g.logits_act)) a.vec_ok = 0;
-    if (a.splits > 1 && (g.N % 4) != 0) a.vec_ok = 0;
+    float* ws = nullptr;
+    if (a.splits > 1) {
+        ws = g_ws.get((size_t)a.splits * g.M * g.N * sizeof(float));
+        if (!ws) return false;
+    }
+    // epilogue maps
+    switch (g.epi) {
+        case EPI_F32:
+            ok = make_epi_map(&mp.o, g.Cf, true, g.N, g.M, g.ldc);
+            break;
+        case EPI_F32_ACC:
+            ok = a.splits > 1 ? make_epi_map(&mp.o, ws, true, g.N, g.M, g.N, a.splits)
+                              : make_epi_map(&mp.o, g.Cf, true, g.N, g.M, g.ldc);
+            break;
+        case EPI_RESID:
+            ok = make_epi_map(&mp.o, g.Cf, true, g.N, g.M, g.ldc) && make_epi_map(&mp.i, g.resid, true, g.N, g.M, g.ldc);
+            break;
+        case EPI_ACT:
+            ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca);
+            break;
+        case EPI_GELU:
+            ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca) && make_epi_map(&mp.o2, g.Caux, false, g.N, g.M, g.ldca);
+            break;
+        case EPI_GELU_BWD:
+            ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca) &&
+                 make_epi_map(&mp.i, g.aux_in, false, g.N, g.M, g.ldca);
+            break;
+        case EPI_LSE:
+            ok = true;
+            if (g.logits_act && !make_epi_map(&mp.o, g.logits_act, false, g.N, g.M, g.ldca)) {
+                a.store_logits = 0;
+                a.logits_direct = static_cast<bf16*>(g.logits_act);
+                a.ldl = g.ldca;
+            }
+            break;
+        default:
+            ok = false;
+    }
+    if (!ok) return false;
 
     const int items = tiles * a.splits;
     if (pair) {
         const int grid = 2 * std::min(items, sms / 2);
-        if (a_k && b_k) launch2<0, 0>(ma, mb, a, grid, st);
-        else if (a_k && b_mn) launch2<0, 1>(ma, mb, a, grid, st);
-        else launch2<1, 1>(ma, mb, a, grid, st);
+        if (a_k && b_k) launch2<0, 0>(mp, a, grid, st);
+        else if (a_k && b_mn) launch2<0, 1>(mp, a, grid, st);
+        else launch2<1, 1>(mp, a, grid, st);
     } else if (BN == 256) {
         const int grid = std::min(items, sms);
-        if (a_k && b_k) launch<256, 0, 0>(ma, mb, a, grid, st);
-        else if (a_k && b_mn) launch<256, 0, 1>(ma, mb, a, grid, st);
-        else launch<256, 1, 1>(ma, mb, a, grid, st);
+        if (a_k && b_k) launch<256, 0, 0>(mp, a, grid, st);
+        else if (a_k && b_mn) launch<256, 0, 1>(mp, a, grid, st);
+        else launch<256, 1, 1>(mp, a, grid, st);
     } else {
         const int grid = std::min(items, sms);
-        if (a_k && b_k) launch<128, 0, 0>(ma, mb, a, grid, st);
-        else if (a_k && b_mn) launch<128, 0, 1>(ma, mb, a, grid, st);
-        else launch<128, 1, 1>(ma, mb, a, grid, st);
+        if (a_k && b_k) launch<128, 0, 0>(mp, a, grid, st);
+        else if (a_k && b_mn) launch<128, 0, 1>(mp, a, grid, st);
+        else launch<128, 1, 1>(mp, a, grid, st);
     }
     if (a.splits > 1) {
         const long n = (long)g.M * g.N;
         const int blocks = (int)std::min<long>((n + 255) / 256, 148L * 8);
-        k_splitk_reduce<<<blocks, 256, 0, st>>>(a.ws, a.splits, g.M, g.N, g.Cf, g.ldc);
+        k_splitk_reduce<<<blocks, 256, 0, st>>>(ws, a.splits, g.M, g.N, g.Cf, g.ldc);
         PARL_LAUNCHED();
     }
     return true;
