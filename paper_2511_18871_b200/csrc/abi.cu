@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <queue>
 #include <random>
 #include <type_traits>
 #include <vector>
@@ -43,6 +44,34 @@ struct DevBuf {
         bytes = 0;
     }
     ~DevBuf() { release(); }
+};
+
+// pinned host staging for small async uploads: the buffer is reused only once the
+// previous copy out of it has completed (event), so no stream synchronisation
+struct HostStage {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+    void upload(void* dst, const void* src, size_t n, cudaStream_t st) {
+        if (pending) PARL_CUDA(cudaEventSynchronize(ev));
+        if (n > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            PARL_CUDA(cudaMallocHost(&p, n));
+            bytes = n;
+        }
+        if (!ev) PARL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        std::memcpy(p, src, n);
+        PARL_CUDA(cudaMemcpyAsync(dst, p, n, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaEventRecord(ev, st));
+        pending = true;
+    }
+    ~HostStage() {
+        if (pending) cudaEventSynchronize(ev);
+        if (ev) cudaEventDestroy(ev);
+        if (p) cudaFreeHost(p);
+    }
 };
 
 struct NcclApi {
@@ -128,8 +157,12 @@ struct parl_group_s {
     uint64_t epoch = 0;
     PackedDev pk{};
     DevBuf ints, seg_se, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
-    DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf;
+    DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf, work_buf;
+    HostStage sched_stage, work_stage;
     AttnSched sched;
+    std::vector<int32_t> pair_ptr_h;  // host copy of sched.p_ptr (forward work lists)
+    int work_H = -1;
+    uint64_t work_epoch = ~0ull;
     uint64_t sorted_epoch = ~0ull;
     std::vector<int> lens, span_start, cu;
     int max_seq = 0, vocab = 0;
@@ -326,6 +359,8 @@ void ensure_sorted(parl_group_s* g) {
     g->sorted_epoch = g->epoch;
 }
 
+void ensure_fwd_work(parl_group_s* g, int H);
+
 // ---------------------------------------------------------------------------
 // forward (forward_logprobs, model.cpp:534-567; run_forward 430-521)
 template <class T>
@@ -366,6 +401,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     auto lay = [&](size_t per, int l) { return act ? per * (size_t)l : 0; };
     auto xin_of = [&](int l) { return xs + (act ? TD * l : TD * (l & 1)); };
 
+    if constexpr (std::is_same_v<T, bf16>) ensure_fwd_work(g, H);
     AttnArgs aa;
     aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
     aa.seg = g->pk.seg;
@@ -628,7 +664,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
 // Host-side attention tile schedule (see AttnSched in kernels.cuh): the same
 // visibility rule as the shared-prompt mask (model.cpp:242-245) at tile level.
 AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const std::vector<int>& lens, DevBuf& buf,
-                         cudaStream_t st) {
+                         HostStage& stage, cudaStream_t st, std::vector<int32_t>* pair_ptr_out = nullptr) {
     const int nt = (T + 127) / 128;
     auto seg_at = [&](int i) -> int {
         if (i < Peff) return 0;
@@ -671,21 +707,97 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
                      [&](int x, int y) { return q_ptr[x + 1] - q_ptr[x] > q_ptr[y + 1] - q_ptr[y]; });
     std::stable_sort(k_order.begin(), k_order.end(),
                      [&](int x, int y) { return k_ptr[x + 1] - k_ptr[x] > k_ptr[y + 1] - k_ptr[y]; });
+    // query-tile pairs: merged key lists with per-tile visibility / fullness flags
+    const int np = (nt + 1) / 2;
+    std::vector<int32_t> p_ptr(np + 1, 0), p_list, p_order(np);
+    for (int p = 0; p < np; ++p) {
+        int a0 = q_ptr[2 * p], a1 = q_ptr[2 * p + 1];
+        int b0 = 2 * p + 1 < nt ? q_ptr[2 * p + 1] : 0, b1 = 2 * p + 1 < nt ? q_ptr[2 * p + 2] : 0;
+        while (a0 < a1 || b0 < b1) {
+            const int ka = a0 < a1 ? (q_list[a0] & 0x3fffffff) : INT32_MAX;
+            const int kb = b0 < b1 ? (q_list[b0] & 0x3fffffff) : INT32_MAX;
+            const int kt = std::min(ka, kb);
+            int32_t e = kt;
+            if (ka == kt) {
+                e |= (1 << 24) | ((q_list[a0] >> 30) & 1) << 25;
+                ++a0;
+            }
+            if (kb == kt) {
+                e |= (1 << 26) | ((q_list[b0] >> 30) & 1) << 27;
+                ++b0;
+            }
+            p_list.push_back(e);
+        }
+        p_ptr[p + 1] = (int32_t)p_list.size();
+        p_order[p] = p;
+    }
+    std::stable_sort(p_order.begin(), p_order.end(),
+                     [&](int x, int y) { return p_ptr[x + 1] - p_ptr[x] > p_ptr[y + 1] - p_ptr[y]; });
     std::vector<int32_t> all;
-    all.reserve(4 * (nt + 1) + q_list.size() + k_list.size());
+    all.reserve(4 * (nt + 1) + q_list.size() + k_list.size() + 2 * (np + 1) + p_list.size());
     size_t o_qp = all.size(); all.insert(all.end(), q_ptr.begin(), q_ptr.end());
     size_t o_ql = all.size(); all.insert(all.end(), q_list.begin(), q_list.end());
     size_t o_qo = all.size(); all.insert(all.end(), q_order.begin(), q_order.end());
     size_t o_kp = all.size(); all.insert(all.end(), k_ptr.begin(), k_ptr.end());
     size_t o_kl = all.size(); all.insert(all.end(), k_list.begin(), k_list.end());
     size_t o_ko = all.size(); all.insert(all.end(), k_order.begin(), k_order.end());
+    size_t o_pp = all.size(); all.insert(all.end(), p_ptr.begin(), p_ptr.end());
+    size_t o_pl = all.size(); all.insert(all.end(), p_list.begin(), p_list.end());
+    size_t o_po = all.size(); all.insert(all.end(), p_order.begin(), p_order.end());
     int32_t* d = buf.as<int32_t>(all.size());
-    PARL_CUDA(cudaMemcpyAsync(d, all.data(), all.size() * 4, cudaMemcpyHostToDevice, st));
-    PARL_CUDA(cudaStreamSynchronize(st));  // host vector goes out of scope
+    stage.upload(d, all.data(), all.size() * 4, st);
+    if (pair_ptr_out) *pair_ptr_out = p_ptr;
     AttnSched s;
     s.q_ptr = d + o_qp; s.q_list = d + o_ql; s.q_order = d + o_qo;
     s.k_ptr = d + o_kp; s.k_list = d + o_kl; s.k_order = d + o_ko;
+    s.p_ptr = d + o_pp; s.p_list = d + o_pl; s.p_order = d + o_po;
+    s.n_pairs = np;
     return s;
+}
+
+// Longest-processing-time assignment of the forward's (query-tile pair, head)
+// items to one persistent CTA per SM; cost = key tiles + 1 (per-item overhead).
+void build_fwd_work(AttnSched& s, const std::vector<int32_t>& p_ptr, int H, DevBuf& buf, HostStage& stage,
+                    cudaStream_t st) {
+    const int np = (int)p_ptr.size() - 1;
+    const int n = np * H;
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = std::max(1, std::min(n, sms));
+    std::vector<int32_t> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    auto cost = [&](int it) { return p_ptr[it / H + 1] - p_ptr[it / H] + 1; };
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    std::vector<std::vector<int32_t>> per(grid);
+    using L = std::pair<long, int>;
+    std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
+    for (int b = 0; b < grid; ++b) heap.push({0, b});
+    for (int it : order) {
+        auto [load, b] = heap.top();
+        heap.pop();
+        per[b].push_back(it);
+        heap.push({load + cost(it), b});
+    }
+    std::vector<int32_t> all;
+    all.reserve(grid + 1 + n);
+    all.push_back(0);
+    for (int b = 0; b < grid; ++b) all.push_back(all.back() + (int32_t)per[b].size());
+    for (int b = 0; b < grid; ++b) all.insert(all.end(), per[b].begin(), per[b].end());
+    int32_t* d = buf.as<int32_t>(all.size());
+    stage.upload(d, all.data(), all.size() * 4, st);
+    s.w_ptr = d;
+    s.w_items = d + grid + 1;
+    s.w_grid = grid;
+}
+
+void ensure_fwd_work(parl_group_s* g, int H) {
+    if (g->work_H == H) return;
+    build_fwd_work(g->sched, g->pair_ptr_h, H, g->work_buf, g->work_stage, g->ctx->st);
+    g->work_H = H;
 }
 
 void alloc_group_arrays(parl_group_s* g) {
@@ -724,7 +836,9 @@ void upload_meta(parl_group_s* g) {
     }
     PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
-    g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->ctx->st);
+    g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->sched_stage, g->ctx->st,
+                              &g->pair_ptr_h);
+    g->work_H = -1;
 }
 
 void check_pack_inputs(parl_group_s* g, int P, const int32_t* lens, int G, int max_seq) {
@@ -1561,7 +1675,13 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
         aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
         aa.scale = 1.0f / std::sqrt((float)Dh);
         static DevBuf dbg_sched;
-        {
+        static HostStage dbg_stage;
+        static AttnSched cached;
+        static long key[4] = {-1, -1, -1, -1};
+        const long k4[4] = {T, Peff, (long)(uintptr_t)seg_start, (long)(uintptr_t)seg_end};
+        if (path == 2 && std::memcmp(key, k4, sizeof(k4)) == 0) {  // timing loops reuse the schedule
+            aa.sched = cached;
+        } else {
             int G = 0;
             std::vector<int32_t> st_h, en_h;
             if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
@@ -1583,16 +1703,22 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
                 }
             }
             std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, 0);
+            std::vector<int32_t> pp;
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &pp);
+            static DevBuf dbg_work;
+            static HostStage dbg_wstage;
+            build_fwd_work(aa.sched, pp, H, dbg_work, dbg_wstage, 0);
+            cached = aa.sched;
+            std::memcpy(key, k4, sizeof(k4));
         }
-        if (path == 0) {
+        if (path == 0 || path == 2) {  // 2: no device sync (timing loops)
             PARL_REQUIRE(attn_fwd_tc(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0), PARL_E_CONFIG,
                          "head dim not supported by the tcgen05 attention");
         } else {
             launch_attn_fwd<bf16>(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0);
         }
         PARL_CUDA(cudaGetLastError());
-        PARL_CUDA(cudaDeviceSynchronize());
+        if (path != 2) PARL_CUDA(cudaDeviceSynchronize());
     });
 }
 
@@ -1606,6 +1732,7 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
         aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
         aa.scale = 1.0f / std::sqrt((float)Dh);
         static DevBuf dbg_sched;
+        static HostStage dbg_stage;
         {
             int G = 0;
             std::vector<int32_t> st_h, en_h;
@@ -1628,7 +1755,7 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
                 }
             }
             std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, 0);
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0);
         }
         const bf16* q = static_cast<const bf16*>(qkv);
         if (path == 0) {

@@ -303,6 +303,346 @@ __global__ void __launch_bounds__(NTHR, 1)
 }
 
 
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// ===========================================================================
+// Forward, two query tiles per CTA (Dh = 64).  Work item = (pair of adjacent
+// 128-row query tiles, head); the pair's key tiles are the union of both
+// tiles' visible lists, flagged per tile (visible / full).  Roles:
+//   warps 0-3  softmax of query tile 0, warps 4-7 softmax of query tile 1
+//              (thread = query row; two warps per SM sub-partition so the
+//              exp/max/pack stream of one tile overlaps the other's)
+//   warp 8     TMA: Q pair (double-buffered across items), K/V 3-stage ring
+//   warps 9,10 MMA, one issuer per query tile: S_w = Q_w K^T (TMEM, one buffer per tile, re-issued as soon
+//              as the softmax has pulled the previous S into registers), then
+//              O_w += P_w V with P_w read from TMEM (tcgen05 "TS" form)
+//   setmaxnreg moves registers from the TMA/MMA group to the softmax groups so
+//   a whole 128-key score row stays in registers.
+// TMEM: S0 | S1 | O0 | O1 | P0 | P1  (128 | 128 | 64 | 64 | 64 | 64 columns).
+struct AttnPairArgs {
+    int T, H, d, Peff, grid;
+    const int32_t* seg;
+    const int32_t* seg_start;
+    const int32_t *p_ptr, *p_list;
+    const int32_t *w_ptr, *w_items;  // per-CTA item lists (item = pair * H + head)
+    float scale_log2;
+    bf16* out;
+    float* lse;
+};
+
+constexpr int PAIR_NTHR = 384;  // 3 warp groups: softmax 0, softmax 1, TMA/MMA
+constexpr int KV_STAGES = 3;
+constexpr uint32_t VIS0 = 1u << 24, FULL0 = 1u << 25, VIS1 = 1u << 26, FULL1 = 1u << 27;
+
+template <int DH>
+struct PairSmem {
+    static constexpr int TILE = 128 * DH * 2;
+    static constexpr int OFF_Q = 0;                          // [2 buffers][2 tiles]
+    static constexpr int OFF_K = OFF_Q + 4 * TILE;           // [KV_STAGES]
+    static constexpr int OFF_V = OFF_K + KV_STAGES * TILE;   // [KV_STAGES]
+    static constexpr int OFF_BAR = OFF_V + KV_STAGES * TILE;
+    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+
+template <int DH>
+__global__ void __launch_bounds__(PAIR_NTHR, 1)
+    k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, AttnPairArgs a) {
+    static_assert(DH == 64, "TMEM budget: 2 x (S 128 + O DH + P 64) <= 512");
+    using L = PairSmem<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* q_full = bar + 0;                   // [2]
+    uint64_t* q_empty = bar + 2;                  // [2]
+    uint64_t* kv_full = bar + 4;                  // [3]
+    uint64_t* kv_empty = bar + 7;                 // [3]
+    uint64_t* s_full = bar + 10;                  // [2] per query tile
+    uint64_t* s_free = bar + 12;                  // [2]
+    uint64_t* p_full = bar + 14;                  // [2]
+    uint64_t* o_done = bar + 16;                  // [2]
+    uint64_t* o_free = bar + 18;                  // [2]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 20);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = a.H;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&q_full[s], 1);
+            tc::mbar_init(&q_empty[s], 2);  // one release per MMA issuer
+            tc::mbar_init(&s_full[s], 1);
+            tc::mbar_init(&s_free[s], 4);
+            tc::mbar_init(&p_full[s], 4);
+            tc::mbar_init(&o_done[s], 1);
+            tc::mbar_init(&o_free[s], 4);
+        }
+        for (int s = 0; s < KV_STAGES; ++s) {
+            tc::mbar_init(&kv_full[s], 1);
+            tc::mbar_init(&kv_empty[s], 2);
+        }
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tm_qkv);
+    }
+    if (warp == 9) tc::tmem_alloc<512>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+    const uint32_t t_s = tbase, t_o = tbase + 256, t_p = tbase + 256 + 2 * DH;
+
+    if (warp >= 8) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+      if (warp == 8) {
+        if (lane == 0) {  // ---------------- TMA
+            int g = 0, li = 0;
+            for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k, ++li) {
+                const int it = a.w_items[k];
+                const int p = it / H, h = it % H, qb = li & 1;
+                tc::mbar_wait(&q_empty[qb], ((li >> 1) & 1) ^ 1);
+                tc::mbar_expect_tx(&q_full[qb], 2 * L::TILE);
+#pragma unroll
+                for (int w = 0; w < 2; ++w)
+#pragma unroll
+                    for (int r = 0; r < DH / 64; ++r)
+                        tc::tma_load_2d(smem + L::OFF_Q + (qb * 2 + w) * L::TILE + r * 128 * 128, &tm_qkv, &q_full[qb],
+                                        h * DH + r * 64, (2 * p + w) * 128);
+                for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e, ++g) {
+                    const int j0 = (a.p_list[e] & 0xffffff) * 128;
+                    const int st = g % KV_STAGES;
+                    tc::mbar_wait(&kv_empty[st], ((g / KV_STAGES) & 1) ^ 1);
+                    tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
+#pragma unroll
+                    for (int r = 0; r < DH / 64; ++r) {
+                        tc::tma_load_2d(smem + L::OFF_K + st * L::TILE + r * 128 * 128, &tm_qkv, &kv_full[st],
+                                        a.d + h * DH + r * 64, j0);
+                        tc::tma_load_2d(smem + L::OFF_V + st * L::TILE + r * 128 * 128, &tm_qkv, &kv_full[st],
+                                        2 * a.d + h * DH + r * 64, j0);
+                    }
+                }
+            }
+        }
+    } else if ((warp == 9 || warp == 10) && lane == 0) {
+        // ---------------- MMA issuers: warp 9 serves query tile 0, warp 10 tile 1,
+        // so neither softmax group waits on the other's progress.  K/V stages and
+        // the Q pair are released when both issuers are done with them.
+        const int w = warp - 9;
+        const uint32_t VIS = w ? VIS1 : VIS0;
+        constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
+        constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);
+        int cS = 0, cP = 0, nI = 0;
+        // S look-ahead iterator over the entries visible to this tile
+        const int k_end = a.w_ptr[blockIdx.x + 1];
+        int s_k = a.w_ptr[blockIdx.x], s_li = 0, s_e = 0, s_end = 0, gS = 0;
+        auto s_load_item = [&]() {
+            if (s_k < k_end) {
+                const int p = a.w_items[s_k] / H;
+                s_e = a.p_ptr[p];
+                s_end = a.p_ptr[p + 1];
+            }
+        };
+        s_load_item();
+        auto issue_next_s = [&]() {
+            while (s_k < k_end) {
+                if (s_e >= s_end) {
+                    ++s_k;
+                    ++s_li;
+                    s_load_item();
+                    continue;
+                }
+                const uint32_t f = (uint32_t)a.p_list[s_e];
+                const int g = gS;
+                ++s_e;
+                ++gS;
+                if (!(f & VIS)) continue;
+                const int st = g % KV_STAGES, qb = s_li & 1;
+                tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
+                tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
+                if (cS > 0) tc::mbar_wait(&s_free[w], (cS - 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
+                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + (qb * 2 + w) * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                    tc::mma_bf16(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
+                                 ks > 0);
+                }
+                tc::mma_commit(&s_full[w]);
+                ++cS;
+                return;
+            }
+        };
+        issue_next_s();
+        int g = 0, li = 0;
+        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
+            const int p = a.w_items[k] / H, qb = li & 1;
+            const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
+            bool started = false;
+            for (int e = ea; e < eb; ++e, ++g) {
+                const uint32_t f = (uint32_t)a.p_list[e];
+                const int st = g % KV_STAGES;
+                if (!(f & VIS)) {  // not ours: release the stage once it holds this entry
+                    tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
+                    tc::mbar_arrive(&kv_empty[st]);
+                    continue;
+                }
+                issue_next_s();  // S of the next visible key tile (possibly in the next item)
+                tc::mbar_wait(&p_full[w], cP & 1);
+                if (!started && nI > 0) tc::mbar_wait(&o_free[w], (nI - 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma_bf16_ts(t_o + w * DH, t_p + w * 64 + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
+                                    id_o, (started || ks > 0) ? 1u : 0u);
+                tc::mma_commit(&o_done[w]);
+                tc::mma_commit(&kv_empty[st]);
+                ++cP;
+                if (!started) {
+                    started = true;
+                    ++nI;
+                }
+            }
+            if (started) {
+                tc::mma_commit(&q_empty[qb]);
+            } else {
+                tc::mbar_wait(&q_full[qb], (li >> 1) & 1);
+                tc::mbar_arrive(&q_empty[qb]);
+            }
+        }
+      }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+        // ---------------- softmax: warp group w = query tile w of the pair
+        const int w = warp >> 2, q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        const uint32_t VIS = w ? VIS1 : VIS0, FULL = w ? FULL1 : FULL0;
+        const float c2 = a.scale_log2;
+        int cS = 0;
+        for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k) {
+            const int it = a.w_items[k];
+            const int p = it / H, h = it % H;
+            const int i = (2 * p + w) * 128 + r;
+            const bool row_ok = i < a.T;
+            const int seg_i = row_ok ? a.seg[i] : -1;
+            // allowed keys of row i: [0, e0) and [b1, e1) (model.cpp:242-245)
+            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
+            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
+            float m_used = -INFINITY, l = 0.f;
+            bool first = true;
+            for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e) {
+                const uint32_t f = (uint32_t)a.p_list[e];
+                if (!(f & VIS)) continue;
+                tc::mbar_wait(&s_full[w], cS & 1);
+                tc::tc_fence_after();
+                float sv[128];
+                tc::tmem_ld128(t_s + w * 128 + lane_off, sv);
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&s_free[w]);  // the next S of this tile may be issued
+                if (!(f & FULL)) {
+                    const int j0 = (int)(f & 0xffffff) * 128;
+                    const int h0 = min(max(e0 - j0, 0), 128);
+                    const int l1 = min(max(b1 - j0, 0), 128), h1 = min(max(e1 - j0, 0), 128);
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) {
+                        const bool ok = (j < h0) | ((j >= l1) & (j < h1));
+                        sv[j] = ok ? sv[j] : -INFINITY;
+                    }
+                }
+                float mx = fmax3(sv[0], sv[1], sv[2]);
+#pragma unroll
+                for (int j = 3; j < 127; j += 2) mx = fmax3(mx, sv[j], sv[j + 1]);
+                mx = fmaxf(mx, sv[127]);
+                const float mxl = mx * c2;
+                const bool need = mxl > m_used + 8.f;
+                const float m_new = need ? mxl : m_used;
+                const float alpha = need ? tc::ex2_approx(m_used - m_new) : 1.f;
+                const float mb = m_new == -INFINITY ? 0.f : m_new;
+                // P = exp2(S * c - m) -> bf16 (registers)
+                float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
+                uint32_t pk[64];
+#pragma unroll
+                for (int j = 0; j < 128; j += 4) {
+                    const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
+                    const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
+                    const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
+                    const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
+                    sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
+                    pk[j / 2] = pack2(p0, p1);
+                    pk[j / 2 + 1] = pack2(p2, p3);
+                }
+                // the previous PV of this tile has finished reading P and writing O
+                if (cS > 0) {
+                    tc::mbar_wait(&o_done[w], (cS - 1) & 1);
+                    tc::tc_fence_after();
+                }
+                if (!first && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+                    for (int c = 0; c < DH / 32; ++c) {
+                        float o[32];
+                        tc::tmem_ld32(t_o + w * DH + c * 32 + lane_off, o);
+                        uint32_t wv[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) wv[q] = __float_as_uint(o[q] * alpha);
+                        tc::tmem_st16(t_o + w * DH + c * 32 + lane_off, wv);
+                        tc::tmem_st16(t_o + w * DH + c * 32 + 16 + lane_off, wv + 16);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tc::tmem_st16(t_p + w * 64 + c * 16 + lane_off, pk + 16 * c);
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&p_full[w]);
+                l = l * alpha + ((sm0 + sm1) + (sm2 + sm3));
+                m_used = m_new;
+                first = false;
+                ++cS;
+            }
+            if (first) continue;  // no key tile for this query tile (past the end)
+            // item epilogue: O / l -> out (bf16), lse; then release O to the next item
+            tc::mbar_wait(&o_done[w], (cS - 1) & 1);
+            tc::tc_fence_after();
+            float o[DH];
+#pragma unroll
+            for (int c = 0; c < DH / 32; ++c) tc::tmem_ld32_nowait(t_o + w * DH + c * 32 + lane_off,
+                                                                   reinterpret_cast<uint32_t*>(o) + 32 * c);
+            tc::tmem_ld_wait();
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&o_free[w]);
+            if (row_ok) {
+                const float inv = l > 0.f ? 1.f / l : 0.f;
+                bf16* dst = a.out + (long)i * a.d + h * DH;
+#pragma unroll
+                for (int q = 0; q < DH; q += 8) {
+                    uint4 v4;
+                    v4.x = pack2(o[q] * inv, o[q + 1] * inv);
+                    v4.y = pack2(o[q + 2] * inv, o[q + 3] * inv);
+                    v4.z = pack2(o[q + 4] * inv, o[q + 5] * inv);
+                    v4.w = pack2(o[q + 6] * inv, o[q + 7] * inv);
+                    *reinterpret_cast<uint4*>(dst + q) = v4;
+                }
+                a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tbase);
+    }
+}
+
 // ===========================================================================
 // Backward (model.cpp:751-786 recomputed flash-style; deterministic, no atomics)
 //   k_attn_dkv_tc : CTA per (key tile, head), loops over the query tiles that
@@ -791,6 +1131,33 @@ void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
+void launch_fwd_pair(const CUtensorMap& m, const AttnPairArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_fwd_pair<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem<64>::TOTAL);
+        attr = true;
+    }
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    (void)sms;
+    k_attn_fwd_pair<64><<<a.grid, PAIR_NTHR, PairSmem<64>::TOTAL, st>>>(m, a);
+    PARL_LAUNCHED();
+}
+
+// PARL_ATTN_PAIR=0 selects the one-query-tile forward (diagnostics)
+bool attn_pair_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PARL_ATTN_PAIR");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 bool make_qkv_map(CUtensorMap* m, const bf16* base, long cols, long rows) {
     auto fn = encode();
     if (!fn) return false;
@@ -876,6 +1243,18 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     a.scale_log2 = aa.scale * LOG2E;
     a.out = out;
     a.lse = lse;
+    if (aa.Dh == 64 && aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
+        AttnPairArgs pa;
+        pa.T = aa.T; pa.H = aa.H; pa.d = aa.d; pa.Peff = aa.Peff;
+        pa.grid = aa.sched.w_grid;
+        pa.seg = aa.seg; pa.seg_start = aa.seg_start;
+        pa.p_ptr = aa.sched.p_ptr; pa.p_list = aa.sched.p_list;
+        pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
+        pa.scale_log2 = aa.scale * LOG2E;
+        pa.out = out; pa.lse = lse;
+        launch_fwd_pair(m, pa, st);
+        return true;
+    }
     if (aa.Dh == 64) launch_fwd<64>(m, a, st);
     else launch_fwd<128>(m, a, st);
     return true;

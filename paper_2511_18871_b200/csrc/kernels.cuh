@@ -128,6 +128,14 @@ void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int
 struct AttnSched {
     const int32_t *q_ptr = nullptr, *q_list = nullptr, *q_order = nullptr;
     const int32_t *k_ptr = nullptr, *k_list = nullptr, *k_order = nullptr;
+    // pairs of adjacent query tiles (2p, 2p+1): union of their key tiles, each
+    // entry kt | VIS0 << 24 | FULL0 << 25 | VIS1 << 26 | FULL1 << 27
+    const int32_t *p_ptr = nullptr, *p_list = nullptr, *p_order = nullptr;
+    int n_pairs = 0;
+    // forward work lists: CTA b processes items w_items[w_ptr[b] .. w_ptr[b+1]),
+    // item = pair * H + head, balanced over w_grid CTAs (LPT on key-tile counts)
+    const int32_t *w_ptr = nullptr, *w_items = nullptr;
+    int w_grid = 0;
 };
 
 struct AttnArgs {
