@@ -274,6 +274,12 @@ def run_ours(args, c):
     for _ in range(args.warmup):
         step_device()
     ctx.sync()
+    if args.launch_list:  # one step inside an NVTX range for `ncu --nvtx --nvtx-include step/`
+        torch.cuda.nvtx.range_push("step")
+        step_device()
+        ctx.sync()
+        torch.cuda.nvtx.range_pop()
+        return
 
     # ---- device-resident timed region (CUDA events on the library's stream)
     l0 = ctx.launches
@@ -368,6 +374,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--groups", type=int, default=0, help="prompt groups per rank per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="run one step inside an NVTX range 'step' (for ncu launch lists) and exit")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     if args.impl == "reference":

@@ -455,7 +455,12 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
         }
         {  // W1 + bias + GELU (model.cpp:509-511)
             GemmArgs ga = mk(Tn, F, D, bl, D, 1, w.w1_t, D, 1);
-            ga.epi = EPI_GELU; ga.bias = w.b1; ga.Ca = pl; ga.Caux = vl; ga.ldca = F;
+            ga.bias = w.b1; ga.ldca = F;
+            if (act) {  // the backward needs the pre-activation u (GELU') and the activation
+                ga.epi = EPI_GELU; ga.Ca = pl; ga.Caux = vl;
+            } else {
+                ga.epi = EPI_GELU_ACT; ga.Ca = vl;
+            }
             gemm<T>(c, ga);
         }
         {  // W2 + bias + residual (model.cpp:513-515)

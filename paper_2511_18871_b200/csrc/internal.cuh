@@ -87,6 +87,7 @@ enum Epi : int {
     EPI_GELU = 4,         // Ca  = u = acc + bias; Caux = gelu(u)
     EPI_GELU_BWD = 5,     // Ca  = acc * gelu'(aux_in)
     EPI_LSE = 6,          // logits (+bias) -> per-row (max, sumexp) partials + label gather
+    EPI_GELU_ACT = 7,     // Ca  = gelu(acc + bias)         (forward without an activation cache)
 };
 
 struct GemmArgs {

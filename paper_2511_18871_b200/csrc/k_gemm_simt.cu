@@ -105,6 +105,11 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmArgs g) {
                     static_cast<T*>(g.Caux)[(long)m * g.ldca + n] = from_f<T>(gelu_f(to_f<T>(u)));
                     break;
                 }
+                case EPI_GELU_ACT: {
+                    if (g.bias) v += g.bias[n];
+                    static_cast<T*>(g.Ca)[(long)m * g.ldca + n] = from_f<T>(gelu_f(to_f<T>(from_f<T>(v))));
+                    break;
+                }
                 case EPI_GELU_BWD: {
                     const float u = to_f<T>(static_cast<const T*>(g.aux_in)[(long)m * g.ldca + n]);
                     static_cast<T*>(g.Ca)[(long)m * g.ldca + n] = from_f<T>(v * gelu_grad_f(u));

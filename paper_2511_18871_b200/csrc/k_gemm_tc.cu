@@ -32,7 +32,8 @@ constexpr int BM = 128, BK = 64;
 constexpr int EPI_WARPS = 8;                      // two per TMEM lane quadrant, each half the columns
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;    // warps 0-3 producer/MMA/TMEM/spare, 4.. epilogue
 constexpr int STG_BYTES = 4096;                   // epilogue staging buffer: 32 rows x 128 B
-constexpr int EPI_SMEM = EPI_WARPS * 2 * STG_BYTES;  // double-buffered per epilogue warp
+constexpr int NBUF = 3;                           // staging buffers per epilogue warp
+constexpr int EPI_SMEM = EPI_WARPS * NBUF * STG_BYTES;
 
 struct TcArgs {
     int M, N, K, nkb, tiles_m, tiles_n, splits, kbs, epi;
@@ -52,31 +53,34 @@ struct Cfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 3 : 4;
+    static constexpr int STAGES = BN == 256 ? 2 : 4;
     static constexpr int STG_OFF = STAGES * STAGE;  // 1024-aligned
     static constexpr int BAR_OFF = STG_OFF + EPI_SMEM;
     static constexpr int SMEM = BAR_OFF + 512 + 1024;
 };
 
-// Phi(x) = 0.5 (1 + erf(x / sqrt 2)) with Abramowitz-Stegun 7.1.26 (|erf err| <= 1.5e-7,
-// far below the bf16 rounding of the outputs); returns exp(-x^2/2) for GELU' too.
-__device__ __forceinline__ float phi_fast(float x, float& e) {
-    const float z = fabsf(x) * 0.70710678118654752f;
-    const float t = tc::rcp_approx(fmaf(0.3275911f, z, 1.f));
-    e = tc::ex2_approx(-z * z * 1.4426950408889634f);
-    const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
-                                0.254829592f);
-    const float erf_abs = 1.f - poly * e;
-    return 0.5f * (1.f + copysignf(erf_abs, x));
+// Phi(x) = 0.5 (1 + erf(x / sqrt 2)) with erf(z) ~= tanh(z (a0 + a1 z^2 + a2 z^4))
+// (minimax fit on [0, 6]: |erf err| <= 3.7e-5, plus the hardware tanh.approx's
+// ~2^-11 relative error, both far below the bf16 rounding of the outputs).
+// One MUFU op per GELU, two per GELU'.
+__device__ __forceinline__ float tanh_approx(float x) {
+    float r;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float erf_arg(float x, float x2) {  // y with erf(x / sqrt 2) ~= tanh(y)
+    x2 = fminf(x2, 72.f);  // the fit's range |x| <= 6 sqrt 2; beyond it tanh(y) saturates at +-1
+    return x * fmaf(x2, fmaf(x2, -0.000315806263f, 0.0367982576f), 0.797717834f);
 }
 __device__ __forceinline__ float gelu_dev(float x) {  // x * Phi(x)  (model.cpp:255)
-    float e;
-    return x * phi_fast(x, e);
+    const float h = 0.5f * x;
+    return fmaf(h, tanh_approx(erf_arg(x, x * x)), h);
 }
 __device__ __forceinline__ float gelu_grad_dev(float x) {  // Phi(x) + x phi(x)  (model.cpp:257-260)
-    float e;
-    const float p = phi_fast(x, e);
-    return p + x * 0.39894228040143267794f * e;
+    const float x2 = x * x;
+    const float phi = fmaf(0.5f, tanh_approx(erf_arg(x, x2)), 0.5f);
+    const float e = tc::ex2_approx(x2 * -0.72134752044448170368f);  // exp(-x^2 / 2)
+    return fmaf(x * 0.39894228040143267794f, e, phi);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -102,8 +106,8 @@ struct EpiSeq {
 //   GELU', log-sum-exp) -> swizzled smem staging -> one TMA bulk store per
 //   chunk (reduce-add for in-place gradient accumulation).
 // Inputs of the epilogue (fp32 residual, bf16 GELU pre-activation) arrive by
-// TMA into the same staging buffer one chunk ahead.  Two staging buffers per
-// warp let the store of chunk k drain while chunk k+1 is computed.
+// TMA into the same staging buffer two chunks ahead.  Three staging buffers per
+// warp let the stores of chunks k-1, k-2 drain while chunk k is computed.
 template <int BNT, class Release>
 __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMap* mo, const CUtensorMap* mo2,
                                                const CUtensorMap* mi, uint8_t* stg_all, uint64_t* inbar_all,
@@ -111,9 +115,9 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ew = warp & 3, half = (warp - 4) >> 2, wi = warp - 4;
     constexpr int HALF = BNT / 2, NCH = HALF / 32;
-    uint8_t* stg = stg_all + wi * 2 * STG_BYTES;
+    uint8_t* stg = stg_all + wi * NBUF * STG_BYTES;
     const uint32_t stg_s = tc::smem_u32(stg);
-    uint64_t* inbar = inbar_all + wi * 2;
+    uint64_t* inbar = inbar_all + wi * NBUF;
     const int epi = a.epi;
     const bool has_in = epi == EPI_RESID || epi == EPI_GELU_BWD;
     const uint32_t in_bytes = epi == EPI_RESID ? 4096u : 2048u;
@@ -126,15 +130,49 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
         row = mt * e.mrows + e.rank * BM + ew * 32;
         col = nt * BNT + half * HALF;
     };
+    // chunk stream: (item, c) -> the next chunk; item >= n_items when exhausted
+    auto next = [&](int& item, int& c) {
+        if (++c == NCH) {
+            c = 0;
+            item += e.stride;
+        }
+    };
     auto issue_in = [&](int item, int c, int b) {
         int row, col, sp;
         coords(item, row, col, sp);
         tc::mbar_expect_tx(&inbar[b], in_bytes);
         tc::tma_load_2d(stg + b * STG_BYTES, mi, &inbar[b], col + c * 32, row);
     };
+    // bias of a chunk, loaded one chunk ahead (broadcast loads: every lane reads the same columns)
+    float bn[32];
+    auto load_bias = [&](int item, int c) {
+        if (!a.bias || item >= e.n_items) return;
+        int row, col, sp;
+        coords(item, row, col, sp);
+        col += c * 32;
+        if (a.bias_vec && col + 32 <= a.N) {
+            const float4* bp = reinterpret_cast<const float4*>(a.bias + col);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 t = __ldg(bp + j);
+                bn[4 * j] = t.x; bn[4 * j + 1] = t.y; bn[4 * j + 2] = t.z; bn[4 * j + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) bn[j] = col + j < a.N ? __ldg(a.bias + col + j) : 0.f;
+        }
+    };
 
     uint32_t k = 0, local = 0;
-    if (has_in && lane == 0 && e.first < e.n_items) issue_in(e.first, 0, 0);
+    // input prefetch runs two chunks ahead (NBUF = 3 staging buffers)
+    int pf_item = e.first, pf_c = 0;
+    if (has_in && lane == 0) {
+        for (int q = 0; q < 2 && pf_item < e.n_items; ++q) {
+            issue_in(pf_item, pf_c, q);
+            next(pf_item, pf_c);
+        }
+    }
+    load_bias(e.first, 0);
     for (int item = e.first; item < e.n_items; item += e.stride, ++local) {
         const uint32_t acc = local & 1, use = local >> 1;
         tc::mbar_wait(&tfull[acc], use & 1);
@@ -147,7 +185,7 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c, ++k) {
             const int col = colh + c * 32;
-            const uint32_t b = k & 1;
+            const uint32_t b = k % NBUF;
             const uint32_t sb = stg_s + b * STG_BYTES;
             float v[32];
             tc::tmem_ld32(tbase + acc * BNT + half * HALF + c * 32 + ((uint32_t)(ew * 32) << 16), v);
@@ -156,23 +194,16 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
                 release(acc);
             }
             if (a.bias) {
-                if (a.bias_vec && col + 32 <= a.N) {
-                    const float4* bp = reinterpret_cast<const float4*>(a.bias + col);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 t = __ldg(bp + j);
-                        v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col + j < a.N) v[j] += __ldg(a.bias + col + j);
-                }
+                for (int j = 0; j < 32; ++j) v[j] += bn[j];
+                int ni = item, nc = c;
+                next(ni, nc);
+                load_bias(ni, nc);
             }
             if (has_in) {
-                tc::mbar_wait(&inbar[b], (k >> 1) & 1);
-            } else if (do_store) {  // the store issued from this buffer two chunks ago has read it
-                if (lane == 0) tc::bulk_wait_read<1>();
+                tc::mbar_wait(&inbar[b], (k / NBUF) & 1);
+            } else if (do_store) {  // the store issued from this buffer NBUF chunks ago has read it
+                if (lane == 0) tc::bulk_wait_read<NBUF - 1>();
                 __syncwarp();
             }
             switch (epi) {
@@ -213,6 +244,18 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
                         }
                         tc::sts128(sb + sw64(lane, j), u[0], u[1], u[2], u[3]);
                         tc::sts128(sb + 2048 + sw64(lane, j), g[0], g[1], g[2], g[3]);
+                    }
+                    break;
+                case EPI_GELU_ACT:  // activation only (no backward will need the pre-activation)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t g[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t u = pack_bf16(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
+                            g[q] = pack_bf16(gelu_dev(bf_lo(u)), gelu_dev(bf_hi(u)));
+                        }
+                        tc::sts128(sb + sw64(lane, j), g[0], g[1], g[2], g[3]);
                     }
                     break;
                 case EPI_GELU_BWD:
@@ -278,16 +321,11 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
                         if (epi == EPI_GELU) tc::tma_store_2d(mo2, sb + 2048, col, row0);
                     }
                     tc::bulk_commit();
-                    if (has_in) {  // prefetch the next chunk's input into the other buffer
-                        int ni = item, nc = c + 1;
-                        if (nc == NCH) {
-                            ni = item + e.stride;
-                            nc = 0;
-                        }
-                        if (ni < e.n_items) {
-                            tc::bulk_wait_read<1>();  // the store that last used it has read it
-                            issue_in(ni, nc, b ^ 1);
-                        }
+                    if (has_in && pf_item < e.n_items) {
+                        // chunk k+2 goes into the buffer chunk k-1 used: its store has read it
+                        tc::bulk_wait_read<1>();
+                        issue_in(pf_item, pf_c, (k + 2) % NBUF);
+                        next(pf_item, pf_c);
                     }
                 }
             }
@@ -314,8 +352,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x 2]
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + 2 * EPI_WARPS);
+    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x NBUF]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + NBUF * EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_items = a.tiles_m * a.tiles_n * a.splits;
@@ -329,7 +367,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], 32 * EPI_WARPS);
         }
-        for (int s = 0; s < 2 * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
+        for (int s = 0; s < NBUF * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
@@ -438,8 +476,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x 2]
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + 2 * EPI_WARPS);
+    uint64_t* inbar = tempty + 2;  // [EPI_WARPS x NBUF]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(inbar + NBUF * EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_ctarank();
@@ -456,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tc::mbar_init(&tfull[s], 1);
             tc::mbar_init(&tempty[s], 2 * 32 * EPI_WARPS);  // both CTAs' epilogue threads
         }
-        for (int s = 0; s < 2 * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
+        for (int s = 0; s < NBUF * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
         tc::fence_barrier_init();
         tc::tma_prefetch(&tmA);
         tc::tma_prefetch(&tmB);
@@ -746,6 +784,9 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
             break;
         case EPI_GELU:
             ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca) && make_epi_map(&mp.o2, g.Caux, false, g.N, g.M, g.ldca);
+            break;
+        case EPI_GELU_ACT:
+            ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca);
             break;
         case EPI_GELU_BWD:
             ok = make_epi_map(&mp.o, g.Ca, false, g.N, g.M, g.ldca) &&

@@ -7,10 +7,10 @@ import io
 import subprocess
 import sys
 
-UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 
 
-def launches(path):
+def launches(path, by_grid=False):
     rows = list(csv.reader(open(path)))
     hdr = next(r for r in rows if "Kernel Name" in r)
     data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
@@ -20,6 +20,8 @@ def launches(path):
             continue
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("parl_gpu::", "")
         name = name.replace("(anonymous namespace)::", "").replace("unnamed>::", "")
+        if by_grid:
+            name += " " + d.get("Grid Size", "")
         us = float(d["Metric Value"].replace(",", "")) * UNIT.get(d["Metric Unit"], 1.0)
         agg[name][0] += 1
         agg[name][1] += us
@@ -56,4 +58,7 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], by_grid="--by-grid" in sys.argv)
+    else:
+        report(sys.argv[2])

@@ -9,7 +9,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-EPI = dict(F32=0, F32_ACC=1, ACT=2, RESID=3, GELU=4, GELU_BWD=5, LSE=6)
+EPI = dict(F32=0, F32_ACC=1, ACT=2, RESID=3, GELU=4, GELU_BWD=5, LSE=6, GELU_ACT=7)
 
 
 @pytest.fixture(scope="module")
@@ -96,9 +96,10 @@ def test_split_k_accumulate(env):
     assert torch.equal(out, out2)  # deterministic split order
 
 
-def test_epilogues(env):
+@pytest.mark.parametrize("shape", [(384, 512, 256), (4096, 1024, 512), (2000, 896, 200)])
+def test_epilogues(env, shape):
     torch = env[0]
-    M, N, K = 384, 512, 256
+    M, N, K = shape
     A, sam, sak, B, sbn, sbk, ref = operands(torch, M, N, K, 0, 0, seed=3)
     bias = torch.randn(N, device="cuda")
     # ACT
@@ -118,6 +119,10 @@ def test_epilogues(env):
     assert torch.allclose(u.float(), uref.float(), rtol=1e-2, atol=1e-2)
     gref = torch.nn.functional.gelu(u.float()).bfloat16()
     assert torch.allclose(act.float(), gref.float(), rtol=1e-2, atol=1e-2)
+    # GELU_ACT (activation only)
+    act2 = torch.empty_like(u)
+    run(env, 0, A, sam, sak, B, sbn, sbk, M, N, K, EPI["GELU_ACT"], bias=bias, Ca=act2, ldca=N)
+    assert torch.equal(act2, act)
     # GELU_BWD
     aux = torch.randn(M, N, device="cuda").bfloat16()
     d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
