@@ -74,6 +74,10 @@ struct HostStage {
     }
 };
 
+struct SchedHost {
+    std::vector<int32_t> q_ptr, k_ptr, p_ptr;
+};
+
 struct NcclApi {
     void* h = nullptr;
     int (*getUniqueId)(void*) = nullptr;
@@ -160,7 +164,7 @@ struct parl_group_s {
     DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf, work_buf;
     HostStage sched_stage, work_stage;
     AttnSched sched;
-    std::vector<int32_t> pair_ptr_h;  // host copy of sched.p_ptr (forward work lists)
+    SchedHost sched_h;  // host copies of the schedule's tile pointers (work lists)
     int work_H = -1;
     uint64_t work_epoch = ~0ull;
     uint64_t sorted_epoch = ~0ull;
@@ -359,7 +363,7 @@ void ensure_sorted(parl_group_s* g) {
     g->sorted_epoch = g->epoch;
 }
 
-void ensure_fwd_work(parl_group_s* g, int H);
+void ensure_attn_work(parl_group_s* g, int H);
 
 // ---------------------------------------------------------------------------
 // forward (forward_logprobs, model.cpp:534-567; run_forward 430-521)
@@ -401,7 +405,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     auto lay = [&](size_t per, int l) { return act ? per * (size_t)l : 0; };
     auto xin_of = [&](int l) { return xs + (act ? TD * l : TD * (l & 1)); };
 
-    if constexpr (std::is_same_v<T, bf16>) ensure_fwd_work(g, H);
+    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
     AttnArgs aa;
     aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
     aa.seg = g->pk.seg;
@@ -566,6 +570,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     float* dsum = c->dsum.as<float>((size_t)H * Tn);
     float* dx2 = c->dx2.as<float>(TD);
 
+    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
     AttnArgs aa;
     aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
     aa.seg = g->pk.seg;
@@ -634,8 +639,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ProfScope ps(c, PARL_KC_ATTN_BWD, 10.0 * g->pairs * D);
             bool done = false;
             if constexpr (std::is_same_v<T, bf16>) {
-                launch_attn_dsum<T>(aa, cl, dctx, dsum, st);
-                done = attn_bwd_tc(aa, ql, dctx, la, dsum, dqkv, st);
+                done = attn_bwd_tc(aa, ql, cl, dctx, la, dsum, dqkv, st);  // computes D = rowsum(dO O) itself
             }
             if (!done) launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
         }
@@ -669,7 +673,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
 // Host-side attention tile schedule (see AttnSched in kernels.cuh): the same
 // visibility rule as the shared-prompt mask (model.cpp:242-245) at tile level.
 AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const std::vector<int>& lens, DevBuf& buf,
-                         HostStage& stage, cudaStream_t st, std::vector<int32_t>* pair_ptr_out = nullptr) {
+                         HostStage& stage, cudaStream_t st, SchedHost* host_out = nullptr) {
     const int nt = (T + 127) / 128;
     auto seg_at = [&](int i) -> int {
         if (i < Peff) return 0;
@@ -751,7 +755,11 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
     size_t o_po = all.size(); all.insert(all.end(), p_order.begin(), p_order.end());
     int32_t* d = buf.as<int32_t>(all.size());
     stage.upload(d, all.data(), all.size() * 4, st);
-    if (pair_ptr_out) *pair_ptr_out = p_ptr;
+    if (host_out) {
+        host_out->q_ptr = q_ptr;
+        host_out->k_ptr = k_ptr;
+        host_out->p_ptr = p_ptr;
+    }
     AttnSched s;
     s.q_ptr = d + o_qp; s.q_list = d + o_ql; s.q_order = d + o_qo;
     s.k_ptr = d + o_kp; s.k_list = d + o_kl; s.k_order = d + o_ko;
@@ -760,12 +768,12 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
     return s;
 }
 
-// Longest-processing-time assignment of the forward's (query-tile pair, head)
-// items to one persistent CTA per SM; cost = key tiles + 1 (per-item overhead).
-void build_fwd_work(AttnSched& s, const std::vector<int32_t>& p_ptr, int H, DevBuf& buf, HostStage& stage,
-                    cudaStream_t st) {
-    const int np = (int)p_ptr.size() - 1;
-    const int n = np * H;
+// Longest-processing-time assignment of attention work items (tile * H + head)
+// to one persistent CTA per SM; cost = partner tiles + 1 (per-item overhead).
+// Appends [ptr (grid + 1) | items] to `all`; returns the grid.
+int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all) {
+    const int nt = (int)ptr.size() - 1;
+    const int n = nt * H;
     int sms = 148;
     {
         int dev = 0;
@@ -775,7 +783,7 @@ void build_fwd_work(AttnSched& s, const std::vector<int32_t>& p_ptr, int H, DevB
     const int grid = std::max(1, std::min(n, sms));
     std::vector<int32_t> order(n);
     for (int i = 0; i < n; ++i) order[i] = i;
-    auto cost = [&](int it) { return p_ptr[it / H + 1] - p_ptr[it / H] + 1; };
+    auto cost = [&](int it) { return ptr[it / H + 1] - ptr[it / H] + 1; };
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
     std::vector<std::vector<int32_t>> per(grid);
     using L = std::pair<long, int>;
@@ -787,21 +795,32 @@ void build_fwd_work(AttnSched& s, const std::vector<int32_t>& p_ptr, int H, DevB
         per[b].push_back(it);
         heap.push({load + cost(it), b});
     }
-    std::vector<int32_t> all;
-    all.reserve(grid + 1 + n);
+    int32_t acc = 0;
     all.push_back(0);
-    for (int b = 0; b < grid; ++b) all.push_back(all.back() + (int32_t)per[b].size());
+    for (int b = 0; b < grid; ++b) all.push_back(acc += (int32_t)per[b].size());
     for (int b = 0; b < grid; ++b) all.insert(all.end(), per[b].begin(), per[b].end());
-    int32_t* d = buf.as<int32_t>(all.size());
-    stage.upload(d, all.data(), all.size() * 4, st);
-    s.w_ptr = d;
-    s.w_items = d + grid + 1;
-    s.w_grid = grid;
+    return grid;
 }
 
-void ensure_fwd_work(parl_group_s* g, int H) {
+// forward (query-tile pairs), dK/dV (key tiles) and dQ (query tiles) work lists
+void build_attn_work(AttnSched& s, const SchedHost& hs, int H, DevBuf& buf, HostStage& stage, cudaStream_t st) {
+    std::vector<int32_t> all;
+    const size_t o_f = all.size();
+    const int gf = lpt_lists(hs.p_ptr, H, all);
+    const size_t o_k = all.size();
+    const int gk = lpt_lists(hs.k_ptr, H, all);
+    const size_t o_q = all.size();
+    const int gq = lpt_lists(hs.q_ptr, H, all);
+    int32_t* d = buf.as<int32_t>(all.size());
+    stage.upload(d, all.data(), all.size() * 4, st);
+    s.w_ptr = d + o_f; s.w_items = d + o_f + gf + 1; s.w_grid = gf;
+    s.bk_ptr = d + o_k; s.bk_items = d + o_k + gk + 1; s.bk_grid = gk;
+    s.bq_ptr = d + o_q; s.bq_items = d + o_q + gq + 1; s.bq_grid = gq;
+}
+
+void ensure_attn_work(parl_group_s* g, int H) {
     if (g->work_H == H) return;
-    build_fwd_work(g->sched, g->pair_ptr_h, H, g->work_buf, g->work_stage, g->ctx->st);
+    build_attn_work(g->sched, g->sched_h, H, g->work_buf, g->work_stage, g->ctx->st);
     g->work_H = H;
 }
 
@@ -842,7 +861,7 @@ void upload_meta(parl_group_s* g) {
     PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->sched_stage, g->ctx->st,
-                              &g->pair_ptr_h);
+                              &g->sched_h);
     g->work_H = -1;
 }
 
@@ -1708,11 +1727,11 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
                 }
             }
             std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            std::vector<int32_t> pp;
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &pp);
+            SchedHost hs;
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
             static DevBuf dbg_work;
             static HostStage dbg_wstage;
-            build_fwd_work(aa.sched, pp, H, dbg_work, dbg_wstage, 0);
+            build_attn_work(aa.sched, hs, H, dbg_work, dbg_wstage, 0);
             cached = aa.sched;
             std::memcpy(key, k4, sizeof(k4));
         }
@@ -1738,7 +1757,12 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
         aa.scale = 1.0f / std::sqrt((float)Dh);
         static DevBuf dbg_sched;
         static HostStage dbg_stage;
-        {
+        static AttnSched cached;
+        static long key[4] = {-1, -1, -1, -1};
+        const long k4[4] = {T, Peff, (long)(uintptr_t)seg_start, (long)(uintptr_t)seg_end};
+        if (path == 2 && std::memcmp(key, k4, sizeof(k4)) == 0) {  // timing loops reuse the schedule
+            aa.sched = cached;
+        } else {
             int G = 0;
             std::vector<int32_t> st_h, en_h;
             if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
@@ -1760,18 +1784,24 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
                 }
             }
             std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0);
+            SchedHost hs;
+            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
+            static DevBuf dbg_work;
+            static HostStage dbg_wstage;
+            build_attn_work(aa.sched, hs, H, dbg_work, dbg_wstage, 0);
+            cached = aa.sched;
+            std::memcpy(key, k4, sizeof(k4));
         }
         const bf16* q = static_cast<const bf16*>(qkv);
-        if (path == 0) {
-            launch_attn_dsum<bf16>(aa, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), dsum, 0);
-            PARL_REQUIRE(attn_bwd_tc(aa, q, static_cast<const bf16*>(dout), lse, dsum, static_cast<bf16*>(dqkv), 0),
+        if (path == 0 || path == 2) {  // 2: no device sync (timing loops)
+            PARL_REQUIRE(attn_bwd_tc(aa, q, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), lse, dsum,
+                                     static_cast<bf16*>(dqkv), 0),
                          PARL_E_CONFIG, "head dim not supported by the tcgen05 attention");
         } else {
             launch_attn_bwd<bf16>(aa, q, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), lse, dsum,
                                   static_cast<bf16*>(dqkv), 0);
         }
         PARL_CUDA(cudaGetLastError());
-        PARL_CUDA(cudaDeviceSynchronize());
+        if (path != 2) PARL_CUDA(cudaDeviceSynchronize());
     });
 }

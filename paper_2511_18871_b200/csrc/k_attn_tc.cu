@@ -643,6 +643,432 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     }
 }
 
+
+// Backward prologue for the v2 kernels: D = rowsum(dO * O) per (head, row),
+// lse in log2 units, and per-row visibility bounds {qhi, b1} (b1 = -1 for
+// prompt rows): key j is seen by queries [j, qhi_j); query i sees keys
+// [0, e0) u [b1, i] with e0 = i + 1 (prompt row) or Peff (response row).
+__global__ void k_attn_prep(int T, int H, int d, int Peff, const int32_t* __restrict__ seg,
+                            const int32_t* __restrict__ seg_start, const int32_t* __restrict__ seg_end,
+                            const bf16* __restrict__ out, const bf16* __restrict__ dout,
+                            const float* __restrict__ lse, float* __restrict__ dsum, float* __restrict__ lse2,
+                            int2* __restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (long)T * H) return;
+    const int h = (int)(gw / T), i = (int)(gw % T);
+    const long off = (long)i * d + h * 64 + 2 * lane;
+    const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(out + off);
+    const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(dout + off);
+    float acc = __bfloat162float(o2.x) * __bfloat162float(g2.x) + __bfloat162float(o2.y) * __bfloat162float(g2.y);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        dsum[(long)h * T + i] = acc;
+        lse2[(long)h * T + i] = lse[(long)h * T + i] * LOG2E;
+    }
+    if (h == 0 && lane == 1) {
+        const int sg = seg[i];
+        meta[i] = make_int2(sg == 0 ? T : seg_end[sg], sg == 0 ? -1 : seg_start[sg]);
+    }
+    (void)Peff;
+}
+
+struct BwdWs {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            if (cudaMalloc(&p, need) != cudaSuccess) {
+                p = nullptr;
+                bytes = 0;
+                return nullptr;
+            }
+            bytes = need;
+        }
+        return p;
+    }
+};
+BwdWs g_bwd_ws;
+
+// ===========================================================================
+// Backward v2 (Dh = 64): persistent CTAs over LPT-balanced work lists.
+//   MODE_DKV: item = (key tile, head); streams the query tiles that see it:
+//             S^T = K Q^T, dP^T = V dO^T, P^T = exp2(S^T c - lse), dS^T = P^T (dP^T - D),
+//             dV += P^T dO, dK += dS^T Q           (thread = key row)
+//   MODE_DQ:  item = (query tile, head); streams its visible key tiles:
+//             S = Q K^T, dP = dO V^T, dS = P (dP - D), dQ += dS K   (thread = query row)
+// Roles (12 warps): 0-7 element-wise (warp w: TMEM lane quadrant w%4, 64 of the
+// tile's 128 columns), 8 TMA (+ the per-query lse / D vectors for MODE_DKV),
+// 9 MMA issuer.  P and dS go to TMEM and feed the gradient MMAs as the A
+// operand (TS form).  S/dP of the next streamed tile (possibly of the next
+// item) are issued as soon as the element-wise warps have read the current
+// ones.  No atomics: every output row is written by exactly one CTA.
+// TMEM: S | dP | acc1 | acc2 | P | dS = 128 | 128 | 64 | 64 | 64 | 64 columns.
+enum { MODE_DKV = 0, MODE_DQ = 1 };
+
+struct AttnBwd2Args {
+    int T, H, d, Peff;
+    const int32_t* seg;
+    const int32_t *seg_start, *seg_end;
+    const int32_t *lst_ptr, *lst;    // per item tile: partner tiles (k_ptr/k_list or q_ptr/q_list)
+    const int32_t *w_ptr, *w_items;  // per-CTA items (tile * H + head)
+    float scale, scale_log2;
+    const float* lse2;  // [H x T] log-sum-exp in log2 units
+    const float* dsum;  // [H x T]
+    const int2* meta;   // [T] {qhi, b1} (k_attn_prep)
+    bf16* dqkv;         // [T x 3d]
+};
+
+constexpr int BWD_NTHR = 384;
+constexpr int BWD_ST = 3;
+
+template <int DH>
+struct Bwd2Smem {
+    static constexpr int TILE = 128 * DH * 2;
+    static constexpr int OFF_A = 0;                          // item operands [2 buffers][2 tiles]
+    static constexpr int OFF_B = OFF_A + 4 * TILE;           // streamed operands [BWD_ST][2 tiles]
+    static constexpr int OFF_VEC = OFF_B + 2 * BWD_ST * TILE;  // [BWD_ST][lse*log2e | D][128] (MODE_DKV)
+    static constexpr int OFF_BAR = OFF_VEC + BWD_ST * 2 * 128 * 4;
+    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+};
+
+template <int DH, int MODE>
+__global__ void __launch_bounds__(BWD_NTHR, 1)
+    k_attn_bwd2(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                AttnBwd2Args a) {
+    static_assert(DH == 64, "TMEM budget");
+    using L = Bwd2Smem<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* a_full = bar + 0;    // [2]
+    uint64_t* a_empty = bar + 2;   // [2]
+    uint64_t* b_full = bar + 4;    // [BWD_ST]
+    uint64_t* b_empty = bar + 7;   // [BWD_ST]
+    uint64_t* s_full = bar + 10;
+    uint64_t* s_free = bar + 11;
+    uint64_t* p_full = bar + 12;
+    uint64_t* g_done = bar + 13;
+    uint64_t* acc_full = bar + 14;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 16);
+    float* vec = reinterpret_cast<float*>(smem + L::OFF_VEC);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = a.H;
+    const int k_begin = a.w_ptr[blockIdx.x], k_end = a.w_ptr[blockIdx.x + 1];
+    // item operand columns in qkv/dout: MODE_DKV fixes K, V and streams Q, dO; MODE_DQ the reverse
+    const int fix_col0 = MODE == MODE_DKV ? a.d : 0, fix_col1 = MODE == MODE_DKV ? 2 * a.d : 0;
+    const int str_col0 = MODE == MODE_DKV ? 0 : a.d, str_col1 = MODE == MODE_DKV ? 0 : 2 * a.d;
+    const CUtensorMap* fix_map1 = MODE == MODE_DKV ? &tm_qkv : &tm_do;  // V | dO
+    const CUtensorMap* str_map1 = MODE == MODE_DKV ? &tm_do : &tm_qkv;  // dO | V
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&a_full[s], 1);
+            tc::mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < BWD_ST; ++s) {
+            tc::mbar_init(&b_full[s], 1 + 32);  // TMA bytes + one cp.async completion per lane of warp 8
+            tc::mbar_init(&b_empty[s], 1);
+        }
+        tc::mbar_init(s_full, 1);
+        tc::mbar_init(s_free, 8);
+        tc::mbar_init(p_full, 8);
+        tc::mbar_init(g_done, 1);
+        tc::mbar_init(acc_full, 1);
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tm_qkv);
+        tc::tma_prefetch(&tm_do);
+    }
+    if (warp == 9) tc::tmem_alloc<512>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+    const uint32_t t_s = tbase, t_dp = tbase + 128, t_acc1 = tbase + 256, t_acc2 = tbase + 320;
+    const uint32_t t_p = tbase + 384, t_ds = tbase + 448;
+
+    if (warp >= 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+        if (warp == 8) {  // ---------------- TMA (whole warp: lane 0 issues, all lanes write vectors)
+            int g = 0, li = 0;
+            for (int k = k_begin; k < k_end; ++k, ++li) {
+                const int it = a.w_items[k], t = it / H, h = it % H, ab = li & 1;
+                tc::mbar_wait(&a_empty[ab], ((li >> 1) & 1) ^ 1);
+                if (lane == 0) {
+                    tc::mbar_expect_tx(&a_full[ab], 2 * L::TILE);
+                    uint8_t* A0 = smem + L::OFF_A + (ab * 2) * L::TILE;
+                    tc::tma_load_2d(A0, &tm_qkv, &a_full[ab], fix_col0 + h * DH, t * 128);
+                    tc::tma_load_2d(A0 + L::TILE, fix_map1, &a_full[ab], fix_col1 + h * DH, t * 128);
+                }
+                for (int e = a.lst_ptr[t]; e < a.lst_ptr[t + 1]; ++e, ++g) {
+                    const int u = a.lst[e] & 0x3fffffff;
+                    const int st = g % BWD_ST;
+                    tc::mbar_wait(&b_empty[st], ((g / BWD_ST) & 1) ^ 1);
+                    if (lane == 0) {
+                        tc::mbar_expect_tx(&b_full[st], 2 * L::TILE);
+                        uint8_t* B0 = smem + L::OFF_B + (st * 2) * L::TILE;
+                        tc::tma_load_2d(B0, &tm_qkv, &b_full[st], str_col0 + h * DH, u * 128);
+                        tc::tma_load_2d(B0 + L::TILE, str_map1, &b_full[st], str_col1 + h * DH, u * 128);
+                    }
+                    if (MODE == MODE_DKV) {  // lse2 and D of the streamed query tile (zero-filled past T)
+                        const uint32_t vl = tc::smem_u32(vec + st * 256);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = u * 128 + q * 32 + lane;
+                            const uint32_t n = i < a.T ? 4u : 0u;
+                            const long gi = (long)h * a.T + min(i, a.T - 1);
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(vl + (q * 32 + lane) * 4),
+                                         "l"(a.lse2 + gi), "r"(n) : "memory");
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(vl + (128 + q * 32 + lane) * 4),
+                                         "l"(a.dsum + gi), "r"(n) : "memory");
+                        }
+                    }
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&b_full[st]))
+                                 : "memory");
+                }
+            }
+        } else if (warp == 9 && lane == 0) {  // ---------------- MMA
+            constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);
+            int cS = 0, cP = 0;
+            // S/dP look-ahead iterator over (item, streamed tile)
+            int s_k = k_begin, s_li = 0, s_e = 0, s_end = 0, s_first = 0, gS = 0;
+            auto s_load = [&]() {
+                while (s_k < k_end) {
+                    const int t = a.w_items[s_k] / H;
+                    s_e = s_first = a.lst_ptr[t];
+                    s_end = a.lst_ptr[t + 1];
+                    if (s_e < s_end) return;
+                    ++s_k;
+                    ++s_li;
+                }
+            };
+            s_load();
+            auto issue_sd = [&]() {
+                if (s_k >= k_end) return;
+                const int st = gS % BWD_ST, ab = s_li & 1;
+                if (s_e == s_first) tc::mbar_wait(&a_full[ab], (s_li >> 1) & 1);
+                tc::mbar_wait(&b_full[st], (gS / BWD_ST) & 1);
+                if (cS > 0) tc::mbar_wait(s_free, (cS - 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t f0 = tc::smem_u32(smem + L::OFF_A + (ab * 2) * L::TILE);
+                const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks & 3) * 32;
+                    tc::mma_bf16(t_s, tc::sdesc(f0 + off, 16, 1024), tc::sdesc(s0 + off, 16, 1024), id_s, ks > 0);
+                    tc::mma_bf16(t_dp, tc::sdesc(f0 + L::TILE + off, 16, 1024),
+                                 tc::sdesc(s0 + L::TILE + off, 16, 1024), id_s, ks > 0);
+                }
+                tc::mma_commit(s_full);
+                ++cS;
+                ++gS;
+                if (++s_e == s_end) {
+                    ++s_k;
+                    ++s_li;
+                    s_load();
+                }
+            };
+            issue_sd();
+            int g = 0, li = 0;
+            for (int k = k_begin; k < k_end; ++k, ++li) {
+                const int t = a.w_items[k] / H, ab = li & 1;
+                const int ea = a.lst_ptr[t], eb = a.lst_ptr[t + 1];
+                if (ea == eb) {  // nothing streams into this item: release its operands
+                    tc::mbar_wait(&a_full[ab], (li >> 1) & 1);
+                    tc::mbar_arrive(&a_empty[ab]);
+                    continue;
+                }
+                for (int e = ea; e < eb; ++e, ++g) {
+                    const int st = g % BWD_ST;
+                    issue_sd();
+                    tc::mbar_wait(p_full, cP & 1);
+                    tc::tc_fence_after();
+                    const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
+                    const uint32_t acc = (e > ea) ? 1u : 0u;
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint64_t b0 = tc::sdesc(s0 + ks * 2048, 128 * 128, 1024);
+                        const uint64_t b1 = tc::sdesc(s0 + L::TILE + ks * 2048, 128 * 128, 1024);
+                        if (MODE == MODE_DKV) {
+                            tc::mma_bf16_ts(t_acc1, t_p + ks * 8, b1, id_g, (acc || ks > 0) ? 1u : 0u);   // dV += P^T dO
+                            tc::mma_bf16_ts(t_acc2, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dK += dS^T Q
+                        } else {
+                            tc::mma_bf16_ts(t_acc1, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dQ += dS K
+                        }
+                    }
+                    tc::mma_commit(g_done);
+                    tc::mma_commit(&b_empty[st]);
+                    ++cP;
+                }
+                tc::mma_commit(acc_full);
+                tc::mma_commit(&a_empty[ab]);
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+        // ---------------- element-wise: row = TMEM lane, 64 of the 128 streamed columns
+        const int q4 = warp & 3, half = warp >> 2;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        const float c2 = a.scale_log2;
+        int cS = 0, na = 0, g = 0;
+        // per-row data of an item (prefetched one item ahead)
+        int2 nmeta = make_int2(0, -1);
+        float nlr = 0.f, ndr = 0.f;
+        auto fetch = [&](int k) {
+            if (k >= k_end) return;
+            const int it = a.w_items[k], x = (it / H) * 128 + r, h = it % H;
+            if (x < a.T) {
+                nmeta = a.meta[x];
+                if (MODE == MODE_DQ) {
+                    nlr = a.lse2[(long)h * a.T + x];
+                    ndr = a.dsum[(long)h * a.T + x];
+                }
+            }
+        };
+        fetch(k_begin);
+        for (int k = k_begin; k < k_end; ++k) {
+            const int it = a.w_items[k], t = it / H, h = it % H;
+            const int x = t * 128 + r;  // this thread's row: key j (DKV) or query i (DQ)
+            const bool row_ok = x < a.T;
+            const int2 meta = nmeta;
+            const float lr = nlr, dr = ndr;
+            fetch(k + 1);
+            // DKV: queries that see key j are [j, qhi); DQ: keys seen by query i are [0, e0) u [b1, e1)
+            const int qhi = row_ok ? meta.x : 0;
+            const int e0 = !row_ok ? 0 : (meta.y < 0 ? x + 1 : a.Peff);
+            const int b1 = meta.y < 0 ? 0 : meta.y, e1 = (row_ok && meta.y >= 0) ? x + 1 : 0;
+            const int ea = a.lst_ptr[t], eb = a.lst_ptr[t + 1];
+            for (int e = ea; e < eb; ++e, ++g) {
+                const uint32_t fl = (uint32_t)a.lst[e];
+                const int u0 = (int)(fl & 0x3fffffff) * 128;  // first row of the streamed tile
+                const bool full = (fl >> 30) & 1;
+                const uint32_t vl = tc::smem_u32(vec + (g % BWD_ST) * 256);
+                tc::mbar_wait(s_full, cS & 1);
+                tc::tc_fence_after();
+                uint32_t pp[32], pd[32];  // packed bf16 P / dS of this thread's 64 columns
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int cb = half * 64 + c * 32;  // first tile column of the chunk
+                    float sv[32], dp[32];
+                    tc::tmem_ld32_nowait(t_s + cb + lane_off, reinterpret_cast<uint32_t*>(sv));
+                    tc::tmem_ld32_nowait(t_dp + cb + lane_off, reinterpret_cast<uint32_t*>(dp));
+                    tc::tmem_ld_wait();
+                    if (c == 1) {  // S and dP read: the next tile's S/dP may be issued
+                        tc::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(s_free);
+                    }
+                    // exponent argument (log2 units); -inf where the pair is masked
+                    float arg[32], dd[32];
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float l4[4], d4[4];
+                        if (MODE == MODE_DKV) {
+                            uint32_t w0, w1, w2, w3;
+                            tc::lds128(vl + (cb + j) * 4, w0, w1, w2, w3);
+                            l4[0] = __uint_as_float(w0); l4[1] = __uint_as_float(w1);
+                            l4[2] = __uint_as_float(w2); l4[3] = __uint_as_float(w3);
+                            tc::lds128(vl + (128 + cb + j) * 4, w0, w1, w2, w3);
+                            d4[0] = __uint_as_float(w0); d4[1] = __uint_as_float(w1);
+                            d4[2] = __uint_as_float(w2); d4[3] = __uint_as_float(w3);
+                        } else {
+                            l4[0] = l4[1] = l4[2] = l4[3] = lr;
+                            d4[0] = d4[1] = d4[2] = d4[3] = dr;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            arg[j + q] = fmaf(sv[j + q], c2, -l4[q]);
+                            dd[j + q] = dp[j + q] - d4[q];
+                        }
+                    }
+                    if (!full) {
+                        const int cu = u0 + cb;
+                        int lo, hi, l2, h2;
+                        if (MODE == MODE_DKV) {
+                            lo = min(max(x - cu, 0), 32);
+                            hi = min(max(qhi - cu, 0), 32);
+                            l2 = h2 = 32;
+                        } else {
+                            lo = 0;
+                            hi = min(max(e0 - cu, 0), 32);
+                            l2 = min(max(b1 - cu, 0), 32);
+                            h2 = min(max(e1 - cu, 0), 32);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = ((j >= lo) & (j < hi)) | ((j >= l2) & (j < h2));
+                            arg[j] = ok ? arg[j] : -INFINITY;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const float p0 = tc::ex2_approx(arg[j]), p1 = tc::ex2_approx(arg[j + 1]);
+                        pp[c * 16 + j / 2] = pack2(p0, p1);
+                        pd[c * 16 + j / 2] = pack2(p0 * dd[j], p1 * dd[j + 1]);
+                    }
+                }
+                // the previous tile's gradient MMAs have read P / dS
+                if (cS > 0) {
+                    tc::mbar_wait(g_done, (cS - 1) & 1);
+                    tc::tc_fence_after();
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    if (MODE == MODE_DKV) tc::tmem_st16(t_p + half * 32 + c * 16 + lane_off, pp + 16 * c);
+                    tc::tmem_st16(t_ds + half * 32 + c * 16 + lane_off, pd + 16 * c);
+                }
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(p_full);
+                ++cS;
+            }
+            // item epilogue: accumulators -> bf16 rows of dqkv (MODE_DKV: half 0 dV -> 2d + h DH,
+            // half 1 dK * scale -> d + h DH; MODE_DQ: dQ * scale, half h -> columns [32 h, 32 h + 32))
+            constexpr int NC = MODE == MODE_DKV ? 64 : 32;
+            bf16* dst = a.dqkv + (long)x * 3 * a.d + h * DH +
+                        (MODE == MODE_DKV ? (half ? a.d : 2 * a.d) : half * 32);
+            if (eb > ea) {
+                tc::mbar_wait(acc_full, na & 1);
+                tc::tc_fence_after();
+                ++na;
+                float o[NC];
+                const uint32_t src = MODE == MODE_DKV ? (half ? t_acc2 : t_acc1) : t_acc1 + half * 32;
+#pragma unroll
+                for (int c = 0; c < NC / 32; ++c)
+                    tc::tmem_ld32_nowait(src + c * 32 + lane_off, reinterpret_cast<uint32_t*>(o) + 32 * c);
+                tc::tmem_ld_wait();
+                const float mul = (MODE == MODE_DQ || half) ? a.scale : 1.f;
+                if (row_ok) {
+#pragma unroll
+                    for (int q = 0; q < NC; q += 8) {
+                        uint4 v4;
+                        v4.x = pack2(o[q] * mul, o[q + 1] * mul);
+                        v4.y = pack2(o[q + 2] * mul, o[q + 3] * mul);
+                        v4.z = pack2(o[q + 4] * mul, o[q + 5] * mul);
+                        v4.w = pack2(o[q + 6] * mul, o[q + 7] * mul);
+                        *reinterpret_cast<uint4*>(dst + q) = v4;
+                    }
+                }
+            } else if (row_ok) {
+#pragma unroll
+                for (int q = 0; q < NC; q += 8) *reinterpret_cast<uint4*>(dst + q) = make_uint4(0, 0, 0, 0);
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tbase);
+    }
+}
+
 // ===========================================================================
 // Backward (model.cpp:751-786 recomputed flash-style; deterministic, no atomics)
 //   k_attn_dkv_tc : CTA per (key tile, head), loops over the query tiles that
@@ -1187,10 +1613,21 @@ void launch_bwd(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwdArgs&
 
 }  // namespace
 
+template <int MODE>
+void launch_bwd2(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwd2Args& a, int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_bwd2<64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Smem<64>::TOTAL);
+        attr = true;
+    }
+    k_attn_bwd2<64, MODE><<<grid, BWD_NTHR, Bwd2Smem<64>::TOTAL, st>>>(mq, md, a);
+    PARL_LAUNCHED();
+}
+
 // dqkv <- attention backward given dO = dout [T x d], the forward's lse and
 // D = rowsum(dO * O) (dsum).  false if unsupported.
-bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* dout, const float* lse, const float* dsum,
-                 bf16* dqkv, cudaStream_t st) {
+bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf16* dout, const float* lse,
+                 float* dsum, bf16* dqkv, cudaStream_t st) {
     if (!(aa.Dh == 64 || aa.Dh == 128)) return false;
     if (((long)aa.d * 2) % 16 || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15) ||
         (reinterpret_cast<uintptr_t>(dqkv) & 15))
@@ -1211,6 +1648,29 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* dout, const fl
     a.lse = lse;
     a.dsum = dsum;
     a.dqkv = dqkv;
+    if (aa.Dh == 64 && aa.sched.bk_ptr && aa.sched.bq_ptr && attn_pair_enabled() && out) {
+        const size_t ht = (size_t)aa.H * aa.T;
+        float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 8 + 16));
+        if (!lse2) return false;
+        int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
+        const long warps = (long)aa.T * aa.H;
+        k_attn_prep<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(aa.T, aa.H, aa.d, aa.Peff, aa.seg, aa.seg_start,
+                                                                      aa.seg_end, out, dout, lse, dsum, lse2, meta);
+        PARL_LAUNCHED();
+        AttnBwd2Args b;
+        b.T = aa.T; b.H = aa.H; b.d = aa.d; b.Peff = aa.Peff;
+        b.seg = aa.seg; b.seg_start = aa.seg_start; b.seg_end = aa.seg_end;
+        b.scale = aa.scale; b.scale_log2 = aa.scale * LOG2E;
+        b.lse2 = lse2; b.dsum = dsum; b.meta = meta; b.dqkv = dqkv;
+        b.lst_ptr = aa.sched.k_ptr; b.lst = aa.sched.k_list;
+        b.w_ptr = aa.sched.bk_ptr; b.w_items = aa.sched.bk_items;
+        launch_bwd2<MODE_DKV>(mq, md, b, aa.sched.bk_grid, st);
+        b.lst_ptr = aa.sched.q_ptr; b.lst = aa.sched.q_list;
+        b.w_ptr = aa.sched.bq_ptr; b.w_items = aa.sched.bq_items;
+        launch_bwd2<MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
+        return true;
+    }
+    if (out) launch_attn_dsum<bf16>(aa, out, dout, dsum, st);
     if (aa.Dh == 64) launch_bwd<64>(mq, md, a, st);
     else launch_bwd<128>(mq, md, a, st);
     return true;

@@ -136,6 +136,9 @@ struct AttnSched {
     // item = pair * H + head, balanced over w_grid CTAs (LPT on key-tile counts)
     const int32_t *w_ptr = nullptr, *w_items = nullptr;
     int w_grid = 0;
+    // backward work lists: dK/dV items = key tile * H + head, dQ items = query tile * H + head
+    const int32_t *bk_ptr = nullptr, *bk_items = nullptr, *bq_ptr = nullptr, *bq_items = nullptr;
+    int bk_grid = 0, bq_grid = 0;
 };
 
 struct AttnArgs {
@@ -152,7 +155,7 @@ bool attn_fwd_tc(const AttnArgs& a, const bf16* qkv, bf16* out, float* lse, cuda
 template <class T>
 void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaStream_t st);
 // tcgen05 backward (k_attn_tc.cu): dqkv from dO, lse and D = rowsum(dO*O)
-bool attn_bwd_tc(const AttnArgs& a, const bf16* qkv, const bf16* dout, const float* lse, const float* dsum,
+bool attn_bwd_tc(const AttnArgs& a, const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dsum,
                  bf16* dqkv, cudaStream_t st);
 template <class T>
 void launch_attn_dsum(const AttnArgs& a, const T* out, const T* dout, float* dsum, cudaStream_t st);

@@ -59,9 +59,10 @@ for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
         assert fb(*args) == 0, P.LIB.parl_last_error(None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = 5 if path == 0 else 1
+        args2 = ((2,) + args[1:]) if path == 0 else args
         e0.record()
         for _ in range(n):
-            fb(*args)
+            fb(*args2)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / n
         print(f"attn bwd {'tc' if path == 0 else 'ffma'} T={T} H={H} Dh={Dh}: {ms:.3f} ms  {flops/ms/1e9:.1f} TFLOP/s", flush=True)
