@@ -7,6 +7,7 @@ Cases
 -----
 tiny_*   : the reference tests' small config (V=16, d=16, L=2, H=2, F=24; test_packing.cpp:14-23)
 c1_*     : BASELINE configs[0] (d=256, H=4, L=2, F=1024, V=4096; P=64, G=4, R=128; T=576)
+c2w_*    : C2's layer width (d=896, H=14, F=4864) at L=1, V=4096; P=64, G=3, R=[96, 80, 131]
 
 Weights come from ModelParams::init (model.cpp:142-164) and, for old/ref, from
 `perturb(w, seed, scale)` below, which is reproducible with numpy alone so the GPU
@@ -24,6 +25,9 @@ GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))
 
 TINY = Cfg(vocab=16, d_model=16, n_layers=2, n_heads=2, d_ff=24, max_seq=64)
 C1 = Cfg(vocab=4096, d_model=256, n_layers=2, n_heads=4, d_ff=1024, max_seq=576)
+# C2 width (Qwen2.5-0.5B: d=896, H=14, F=4864) at L=1, a 4096-token vocab and a small
+# ragged group whose response boundaries are not tile aligned
+C2W = Cfg(vocab=4096, d_model=896, n_layers=1, n_heads=14, d_ff=4864, max_seq=512)
 
 
 def perturb(w: np.ndarray, seed: int, scale: float) -> np.ndarray:
@@ -50,9 +54,11 @@ def grad_summary(cfg: Cfg, g: np.ndarray, n_samples: int = 4096, seed: int = 5):
     return np.array(names), np.array(sums), np.array(l2), idx, g[idx]
 
 
-def main():
+def main(only=None):
     os.makedirs(GOLDEN, exist_ok=True)
     ref = Oracle("ref")
+    if only == "c2w":
+        return _c2w(ref)
 
     # ---- tiny: packed forward/backward with an arbitrary upstream -------------
     w = ref.init_params(TINY, 41)
@@ -100,8 +106,27 @@ def main():
                         prompt=prompt, resp_flat=np.concatenate(responses), lens=np.array([128] * 4, np.int32),
                         rewards=rewards, advantages=adv, stats=st, lp3=lp3, grad_names=names, grad_sums=sums,
                         grad_l2=l2, grad_idx=idx, grad_vals=vals, param_sum=w1.sum(), param_head=w1[:64])
+    _c2w(ref)
+
+
+def _c2w(ref):
+    if True:  # ---- C2-width micro-batch
+        lens = [96, 80, 131]
+        w2 = ref.init_params(C2W, 7)
+        prompt, responses, rewards = group_inputs(321, C2W.vocab, 64, lens)
+        w2_old = perturb(w2, 31, 0.01)
+        w2_ref = perturb(w2, 32, 0.01)
+        adv = ref.group_advantages(rewards)
+        g, st, lp3 = ref.train_microbatch(C2W, w2, w2_old, w2_ref, prompt, responses, adv, 0.2, 0.04, 0)
+        names, sums, l2, idx, vals = grad_summary(C2W, g)
+        np.savez_compressed(os.path.join(GOLDEN, "c2w_micro.npz"), seed=7, old_seed=31, ref_seed=32, scale=0.01,
+                            prompt=prompt, resp_flat=np.concatenate(responses), lens=np.array(lens, np.int32),
+                            rewards=rewards, advantages=adv, stats=st, lp3=lp3, grad_names=names, grad_sums=sums,
+                            grad_l2=l2, grad_idx=idx, grad_vals=vals, param_sum=w2.sum(), param_head=w2[:64])
     print("wrote", sorted(os.listdir(GOLDEN)))
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

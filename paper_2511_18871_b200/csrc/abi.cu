@@ -180,6 +180,7 @@ struct parl_act_s {
     DevBuf xs, xmid, a, qkv, ctxo, bn, pre, actv, stats, lse_attn;  // per-layer stacks
     DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
     bool logits_bf16 = false;  // logits stored bf16 by the fused tcgen05 head
+    uintptr_t pad_sig[7] = {};  // buffers / sizes the bias columns were filled for
 };
 
 struct parl_grad_s {
@@ -373,7 +374,12 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     const auto& cf = m->cfg;
     const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
     const int NL = cf.n_layers;
-    const size_t TD = (size_t)Tn * D, TF = (size_t)Tn * F;
+    const size_t TD = (size_t)Tn * D;
+    // GEMM-operand activations carry PAD extra columns: column D (F) is 1.0 so the
+    // weight-gradient GEMM of the backward also produces the bias gradient
+    // (the bias row follows the weight in the flat layout, model.cpp:86-114)
+    const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
+    const size_t TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
 
     float* xs;   // residual stream stack: layer inputs x_0..x_L
     float* xmid; // per-layer x_mid
@@ -382,23 +388,23 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     if (act) {
         xs = act->xs.as<float>(TD * (NL + 1));
         xmid = act->xmid.as<float>(TD * NL);
-        a = act->a.as<T>(TD * NL);
+        a = act->a.as<T>(TDp * NL);
         qkv = act->qkv.as<T>(3 * TD * NL);
-        ctxo = act->ctxo.as<T>(TD * NL);
-        bn = act->bn.as<T>(TD * NL);
-        pre = act->pre.as<T>(TF * NL);
-        actv = act->actv.as<T>(TF * NL);
+        ctxo = act->ctxo.as<T>(TDp * NL);
+        bn = act->bn.as<T>(TDp * NL);
+        pre = act->pre.as<T>(TFp * NL);
+        actv = act->actv.as<T>(TFp * NL);
         stats = act->stats.as<float>((size_t)4 * Tn * NL);
         lse_attn = act->lse_attn.as<float>((size_t)H * Tn * NL);
     } else {
         xs = c->x0.as<float>(TD * 2);
         xmid = c->xmid.as<float>(TD);
-        a = c->a.as<T>(TD);
+        a = c->a.as<T>(TDp);
         qkv = c->qkv.as<T>(3 * TD);
-        ctxo = c->ctxo.as<T>(TD);
-        bn = c->bn.as<T>(TD);
-        pre = c->pre.as<T>(TF);
-        actv = c->actv.as<T>(TF);
+        ctxo = c->ctxo.as<T>(TDp);
+        bn = c->bn.as<T>(TDp);
+        pre = c->pre.as<T>(TFp);
+        actv = c->actv.as<T>(TFp);
         stats = c->mean1.as<float>((size_t)4 * Tn);
         lse_attn = c->lse_attn.as<float>((size_t)H * Tn);
     }
@@ -414,6 +420,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     aa.scale = 1.0f / std::sqrt((float)Dh);
     aa.Peff = g->Peff;
     aa.sched = g->sched;
+    aa.ldo = Dp;
 
     {
         ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12);
@@ -424,21 +431,21 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
         float* xin = xin_of(l);
         float* xout = xin_of(l + 1);
         float* xm = xmid + lay(TD, l);
-        T* al = a + lay(TD, l);
+        T* al = a + lay(TDp, l);
         T* ql = qkv + lay(3 * TD, l);
-        T* cl = ctxo + lay(TD, l);
-        T* bl = bn + lay(TD, l);
-        T* pl = pre + lay(TF, l);
-        T* vl = actv + lay(TF, l);
+        T* cl = ctxo + lay(TDp, l);
+        T* bl = bn + lay(TDp, l);
+        T* pl = pre + lay(TFp, l);
+        T* vl = actv + lay(TFp, l);
         float* st4 = stats + lay((size_t)4 * Tn, l);
         float* la = lse_attn + lay((size_t)H * Tn, l);
 
         {
             ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
-            launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, st4, st4 + Tn, st);
+            launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, Dp, st4, st4 + Tn, st);
         }
         {  // fused Q|K|V projection (model.cpp:464-466)
-            GemmArgs ga = mk(Tn, 3 * D, D, al, D, 1, w.wqkv_t, D, 1);
+            GemmArgs ga = mk(Tn, 3 * D, D, al, Dp, 1, w.wqkv_t, D, 1);
             ga.epi = EPI_ACT; ga.bias = w.bqkv; ga.Ca = ql; ga.ldca = 3 * D;
             gemm<T>(c, ga);
         }
@@ -449,17 +456,17 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
             if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
         }
         {  // O projection + residual (model.cpp:504-506)
-            GemmArgs ga = mk(Tn, D, D, cl, D, 1, w.wo_t, D, 1);
+            GemmArgs ga = mk(Tn, D, D, cl, Dp, 1, w.wo_t, D, 1);
             ga.epi = EPI_RESID; ga.bias = w.bo; ga.resid = xin; ga.Cf = xm; ga.ldc = D;
             gemm<T>(c, ga);
         }
         {
             ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
-            launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, st4 + 2 * Tn, st4 + 3 * Tn, st);
+            launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
         }
         {  // W1 + bias + GELU (model.cpp:509-511)
-            GemmArgs ga = mk(Tn, F, D, bl, D, 1, w.w1_t, D, 1);
-            ga.bias = w.b1; ga.ldca = F;
+            GemmArgs ga = mk(Tn, F, D, bl, Dp, 1, w.w1_t, D, 1);
+            ga.bias = w.b1; ga.ldca = Fp;
             if (act) {  // the backward needs the pre-activation u (GELU') and the activation
                 ga.epi = EPI_GELU; ga.Ca = pl; ga.Caux = vl;
             } else {
@@ -468,27 +475,39 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
             gemm<T>(c, ga);
         }
         {  // W2 + bias + residual (model.cpp:513-515)
-            GemmArgs ga = mk(Tn, D, F, vl, F, 1, w.w2_t, F, 1);
+            GemmArgs ga = mk(Tn, D, F, vl, Fp, 1, w.w2_t, F, 1);
             ga.epi = EPI_RESID; ga.bias = w.b2; ga.resid = xm; ga.Cf = xout; ga.ldc = D;
             gemm<T>(c, ga);
         }
     }
     float* xfin = xin_of(NL);
     // final LN + head only on the scored tokens' predecessor rows (model.cpp:518-556)
-    T* hf = act ? act->hf.as<T>((size_t)S * D) : c->hf.as<T>((size_t)S * D);
+    T* hf = act ? act->hf.as<T>((size_t)S * Dp) : c->hf.as<T>((size_t)S * Dp);
+    if (act) {  // bias columns of the weight-gradient operands (refilled when the buffers move)
+        const uintptr_t sig[7] = {(uintptr_t)a, (uintptr_t)ctxo, (uintptr_t)bn, (uintptr_t)actv, (uintptr_t)hf,
+                                  (uintptr_t)Tn, (uintptr_t)S};
+        if (std::memcmp(sig, act->pad_sig, sizeof(sig)) != 0) {
+            launch_fill_pad<T>(a, (long)Tn * NL, D, Dp, st);
+            launch_fill_pad<T>(ctxo, (long)Tn * NL, D, Dp, st);
+            launch_fill_pad<T>(bn, (long)Tn * NL, D, Dp, st);
+            launch_fill_pad<T>(actv, (long)Tn * NL, F, Fp, st);
+            launch_fill_pad<T>(hf, (long)S, D, Dp, st);
+            std::memcpy(act->pad_sig, sig, sizeof(sig));
+        }
+    }
     float* lnf_mean = act ? act->lnf_mean.as<float>(S) : c->lnf_mean.as<float>(S);
     float* lnf_rstd = act ? act->lnf_rstd.as<float>(S) : c->lnf_rstd.as<float>(S);
     float* lse_head = act ? act->lse_head.as<float>(S) : c->lse_head.as<float>(S);
     float* lp = static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T;
     if (S > 0) {
-        launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, lnf_mean, lnf_rstd, st);
+        launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, Dp, lnf_mean, lnf_rstd, st);
         bool fused = false;
         if constexpr (std::is_same_v<T, bf16>) {
             // tcgen05 head with the vocab log-sum-exp and target gather fused
             // into the epilogue: logits reach HBM only for the policy (bf16,
             // kept for the backward), never for old/ref.
             const int n_parts = (V + 127) / 128;
-            GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
+            GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
             ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
             ga.part = c->part.as<float>((size_t)S * n_parts * 2);
             ga.target = c->target.as<float>(S);
@@ -503,7 +522,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
         }
         if (!fused) {
             float* logits = act ? act->logits.as<float>((size_t)S * V) : c->logits.as<float>((size_t)S * V);
-            GemmArgs ga = mk(S, V, D, hf, D, 1, m->W.head_w_t, D, 1);
+            GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
             ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
             gemm_simt<T>(ga, st);
             launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
@@ -520,12 +539,14 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     const auto& cf = m->cfg;
     const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
     const int NL = cf.n_layers;
-    const size_t TD = (size_t)Tn * D, TF = (size_t)Tn * F;
+    const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
+    const size_t TD = (size_t)Tn * D, TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
     float* G = static_cast<float*>(gr->g.p);
     const FlatLayout& L = gr->L;
     const float* u = static_cast<const float*>(g->upstream.p);
 
     float* dx = c->dx.as<float>(TD);
+    T* dx_act = c->dx_act.as<T>(TD);
     if (S > 0) {
         // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
         T* dz = c->dz.as<T>((size_t)S * V);
@@ -535,7 +556,6 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         else
             launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
                                          static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dz, V, S, V, G + L.head_b, st); }
         T* hf = static_cast<T*>(act->hf.p);
         float* dhf = c->dhf.as<float>((size_t)S * D);
         {  // dH = dZ W_head^T (model.cpp:654-666)
@@ -543,24 +563,28 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ga.epi = EPI_F32; ga.Cf = dhf; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        {  // dW_head += H^T dZ
-            GemmArgs ga = mk(D, V, S, hf, 1, D, dz, 1, V);
+        {  // [dW_head; db_head] += [H 1]^T dZ  (hf's column D is 1)
+            GemmArgs ga = mk(D + 1, V, S, hf, 1, Dp, dz, 1, V);
             ga.epi = EPI_F32_ACC; ga.Cf = G + L.head_w; ga.ldc = V;
             gemm<T>(c, ga);
         }
         // final LN backward on the gathered rows, then scatter to positions
         float* dxg = c->dxg.as<float>((size_t)S * D);
         float* xfin = static_cast<float*>(act->xs.p) + TD * NL;
-        launch_layernorm_bwd(dhf, xfin, g->pk.pred_pos, static_cast<float*>(act->lnf_mean.p),
-                             static_cast<float*>(act->lnf_rstd.p), m->W.lnf_g, S, D, nullptr, dxg, G + L.lnf_g,
-                             G + L.lnf_b, st);
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_scatter_rows(dxg, g->pk.row_ptr, g->pk.row_idx, Tn, D, dx, st); }
+        {
+            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+            launch_layernorm_bwd<T>(dhf, xfin, g->pk.pred_pos, static_cast<float*>(act->lnf_mean.p),
+                                    static_cast<float*>(act->lnf_rstd.p), m->W.lnf_g, S, D, nullptr, dxg,
+                                    static_cast<T*>(nullptr), G + L.lnf_g, G + L.lnf_b, st);
+            launch_scatter_rows(dxg, g->pk.row_ptr, g->pk.row_idx, Tn, D, dx, st);
+            launch_f32_to_act<T>(dx, dx_act, TD, st);
+        }
     } else {
         PARL_CUDA(cudaMemsetAsync(dx, 0, TD * sizeof(float), st));
+        PARL_CUDA(cudaMemsetAsync(dx_act, 0, TD * sizeof(T), st));
     }
 
-    T* dx_act = c->dx_act.as<T>(TD);
-    T* dpre = c->dpre.as<T>(TF);
+    T* dpre = c->dpre.as<T>(TFp);
     float* dbn = c->dbn.as<float>(TD);
     float* dmid = c->dmid.as<float>(TD);
     T* dmid_act = c->dmid_act.as<T>(TD);
@@ -579,61 +603,60 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     aa.scale = 1.0f / std::sqrt((float)Dh);
     aa.Peff = g->Peff;
     aa.sched = g->sched;
+    aa.ldo = Dp;
 
     for (int l = NL - 1; l >= 0; --l) {
         const LayerW& w = m->layers[l];
         const auto o = L.layer(l, D, F);
         float* xin = static_cast<float*>(act->xs.p) + TD * l;
         float* xm = static_cast<float*>(act->xmid.p) + TD * l;
-        T* al = static_cast<T*>(act->a.p) + TD * l;
+        T* al = static_cast<T*>(act->a.p) + TDp * l;
         T* ql = static_cast<T*>(act->qkv.p) + 3 * TD * l;
-        T* cl = static_cast<T*>(act->ctxo.p) + TD * l;
-        T* bl = static_cast<T*>(act->bn.p) + TD * l;
-        T* pl = static_cast<T*>(act->pre.p) + TF * l;
-        T* vl = static_cast<T*>(act->actv.p) + TF * l;
+        T* cl = static_cast<T*>(act->ctxo.p) + TDp * l;
+        T* bl = static_cast<T*>(act->bn.p) + TDp * l;
+        T* pl = static_cast<T*>(act->pre.p) + TFp * l;
+        T* vl = static_cast<T*>(act->actv.p) + TFp * l;
         float* st4 = static_cast<float*>(act->stats.p) + (size_t)4 * Tn * l;
         float* la = static_cast<float*>(act->lse_attn.p) + (size_t)H * Tn * l;
 
-        // FFN (model.cpp:688-727)
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_f32_to_act<T>(dx, dx_act, TD, st); }
+        // FFN (model.cpp:688-727); dx_act holds the compute-dtype copy of dx
         {
             GemmArgs ga = mk(Tn, F, D, dx_act, D, 1, w.w2_t, 1, F);
-            ga.epi = EPI_GELU_BWD; ga.aux_in = pl; ga.Ca = dpre; ga.ldca = F;
+            ga.epi = EPI_GELU_BWD; ga.aux_in = pl; ga.Ca = dpre; ga.ldca = Fp;
             gemm<T>(c, ga);
         }
-        {
-            GemmArgs ga = mk(F, D, Tn, vl, 1, F, dx_act, 1, D);
+        {  // [dW2; db2] += [act 1]^T dx
+            GemmArgs ga = mk(F + 1, D, Tn, vl, 1, Fp, dx_act, 1, D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w2; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<float>(dx, D, Tn, D, G + o.b2, st); }
         {
-            GemmArgs ga = mk(Tn, D, F, dpre, F, 1, w.w1_t, 1, D);
+            GemmArgs ga = mk(Tn, D, F, dpre, Fp, 1, w.w1_t, 1, D);
             ga.epi = EPI_F32; ga.Cf = dbn; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        {
-            GemmArgs ga = mk(D, F, Tn, bl, 1, D, dpre, 1, F);
+        {  // [dW1; db1] += [LN2 1]^T dpre
+            GemmArgs ga = mk(D + 1, F, Tn, bl, 1, Dp, dpre, 1, Fp);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w1; ga.ldc = F;
             gemm<T>(c, ga);
         }
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dpre, F, Tn, F, G + o.b1, st); }
-        // LN2 (model.cpp:729-730)
-        launch_layernorm_bwd(dbn, xm, nullptr, st4 + 2 * Tn, st4 + 3 * Tn, w.ln2_g, Tn, D, dx, dmid, G + o.ln2g,
-                             G + o.ln2b, st);
+        // LN2 (model.cpp:729-730): dmid = dx + LN2^T(dbn), plus its compute-dtype copy
+        {
+            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+            launch_layernorm_bwd<T>(dbn, xm, nullptr, st4 + 2 * Tn, st4 + 3 * Tn, w.ln2_g, Tn, D, dx, dmid, dmid_act,
+                                    G + o.ln2g, G + o.ln2b, st);
+        }
         // O projection (model.cpp:733-749)
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_f32_to_act<T>(dmid, dmid_act, TD, st); }
         {
             GemmArgs ga = mk(Tn, D, D, dmid_act, D, 1, w.wo_t, 1, D);
             ga.epi = EPI_ACT; ga.Ca = dctx; ga.ldca = D;
             gemm<T>(c, ga);
         }
-        {
-            GemmArgs ga = mk(D, D, Tn, cl, 1, D, dmid_act, 1, D);
+        {  // [dWo; dbo] += [ctx 1]^T dmid
+            GemmArgs ga = mk(D + 1, D, Tn, cl, 1, Dp, dmid_act, 1, D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.wo; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<float>(dmid, D, Tn, D, G + o.bo, st); }
         // attention (model.cpp:752-786)
         {
             ProfScope ps(c, PARL_KC_ATTN_BWD, 10.0 * g->pairs * D);
@@ -649,15 +672,18 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ga.epi = EPI_F32; ga.Cf = da; ga.ldc = D;
             gemm<T>(c, ga);
         }
-        const size_t woff[3] = {o.wq, o.wk, o.wv}, boff[3] = {o.bq, o.bk, o.bv};
-        for (int p = 0; p < 3; ++p) {
-            GemmArgs ga = mk(D, D, Tn, al, 1, D, dqkv + (size_t)p * D, 1, 3 * D);
+        const size_t woff[3] = {o.wq, o.wk, o.wv};
+        for (int p = 0; p < 3; ++p) {  // [dWp; dbp] += [LN1 1]^T dqkv_p
+            GemmArgs ga = mk(D + 1, D, Tn, al, 1, Dp, dqkv + (size_t)p * D, 1, 3 * D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + woff[p]; ga.ldc = D;
             gemm<T>(c, ga);
-            { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_colsum<T>(dqkv + (size_t)p * D, 3 * D, Tn, D, G + boff[p], st); }
         }
-        // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da)
-        { ProfScope ps_(c, PARL_KC_NORM, 0.0); launch_layernorm_bwd(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, G + o.ln1g, G + o.ln1b, st); }
+        // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da), plus the next layer's compute-dtype copy
+        {
+            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+            launch_layernorm_bwd<T>(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, dx_act, G + o.ln1g,
+                                    G + o.ln1b, st);
+        }
         std::swap(dx, dx2);
     }
     // embeddings (model.cpp:826-834), deterministic segmented sums

@@ -32,9 +32,18 @@ struct Error {
         if (!(cond)) throw ::parl_gpu::Error{code, msg};    \
     } while (0)
 
-// counts kernel launches per process (bench evidence: "gpu_launches")
+// counts kernel launches per process (bench evidence: "gpu_launches") and fails
+// loudly on a launch error right at its launch site (a later library call such as
+// a CUB sort would otherwise consume the error and skip its own work)
 extern uint64_t g_launches;
-#define PARL_LAUNCHED() (++::parl_gpu::g_launches)
+#define PARL_LAUNCHED()                                                                                  \
+    do {                                                                                                 \
+        ++::parl_gpu::g_launches;                                                                        \
+        cudaError_t e_ = cudaPeekAtLastError();                                                          \
+        if (e_ != cudaSuccess)                                                                           \
+            throw ::parl_gpu::Error{PARL_E_CUDA, std::string("kernel launch at ") + __FILE__ + ":" +      \
+                                                     std::to_string(__LINE__) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // small device helpers

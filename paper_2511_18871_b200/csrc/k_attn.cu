@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(WPB * 32) k_attn_fwd(AttnArgs a, const T* __re
         }
     }
     const float inv = 1.f / l;
-    T* orow = out + (long)i * a.d + h * Dh;
+    T* orow = out + (long)i * (a.ldo ? a.ldo : a.d) + h * Dh;
 #pragma unroll
     for (int q = 0; q < MAXE; ++q) {
         const int e = lane + 32 * q;
@@ -108,7 +108,7 @@ __global__ void k_attn_dsum(AttnArgs a, const T* __restrict__ out, const T* __re
     float acc = 0.f;
     for (int e = lane; e < a.Dh; e += 32) {
         const long off = (long)i * a.d + h * a.Dh + e;
-        acc += to_f<T>(out[off]) * to_f<T>(dout[off]);
+        acc += to_f<T>(out[(long)i * (a.ldo ? a.ldo : a.d) + h * a.Dh + e]) * to_f<T>(dout[off]);
     }
     acc = warp_sum(acc);
     if (lane == 0) dsum[(long)h * a.T + i] = acc;

@@ -35,7 +35,8 @@ struct AttnTcArgs {
     const int32_t *seg_start, *seg_end;      // [G+1]: segment k spans [seg_start[k], seg_end[k])
     const int32_t *q_ptr, *q_list, *q_order;  // tile schedule (see build_attn_schedule)
     float scale_log2;  // scale * log2(e)
-    bf16* out;         // [T x d]
+    bf16* out;         // [T x ldo]
+    long ldo;
     float* lse;        // [H x T] natural log
 };
 
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 float o[32];
                 tc::tmem_ld32(t_o0 + ob * DH + c * 32 + lane_off, o);
                 if (row_ok) {
-                    bf16* dst = a.out + (long)i * a.d + h * DH + c * 32;
+                    bf16* dst = a.out + (long)i * a.ldo + h * DH + c * 32;
 #pragma unroll
                     for (int q = 0; q < 32; q += 8) {
                         __align__(16) bf16 t[8];
@@ -331,6 +332,7 @@ struct AttnPairArgs {
     const int32_t *w_ptr, *w_items;  // per-CTA item lists (item = pair * H + head)
     float scale_log2;
     bf16* out;
+    long ldo;
     float* lse;
 };
 
@@ -621,7 +623,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             if (lane == 0) tc::mbar_arrive(&o_free[w]);
             if (row_ok) {
                 const float inv = l > 0.f ? 1.f / l : 0.f;
-                bf16* dst = a.out + (long)i * a.d + h * DH;
+                bf16* dst = a.out + (long)i * a.ldo + h * DH;
 #pragma unroll
                 for (int q = 0; q < DH; q += 8) {
                     uint4 v4;
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
 // lse in log2 units, and per-row visibility bounds {qhi, b1} (b1 = -1 for
 // prompt rows): key j is seen by queries [j, qhi_j); query i sees keys
 // [0, e0) u [b1, i] with e0 = i + 1 (prompt row) or Peff (response row).
-__global__ void k_attn_prep(int T, int H, int d, int Peff, const int32_t* __restrict__ seg,
+__global__ void k_attn_prep(int T, int H, int d, long ldo, const int32_t* __restrict__ seg,
                             const int32_t* __restrict__ seg_start, const int32_t* __restrict__ seg_end,
                             const bf16* __restrict__ out, const bf16* __restrict__ dout,
                             const float* __restrict__ lse, float* __restrict__ dsum, float* __restrict__ lse2,
@@ -658,7 +660,7 @@ __global__ void k_attn_prep(int T, int H, int d, int Peff, const int32_t* __rest
     if (gw >= (long)T * H) return;
     const int h = (int)(gw / T), i = (int)(gw % T);
     const long off = (long)i * d + h * 64 + 2 * lane;
-    const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(out + off);
+    const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(out + (long)i * ldo + h * 64 + 2 * lane);
     const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(dout + off);
     float acc = __bfloat162float(o2.x) * __bfloat162float(g2.x) + __bfloat162float(o2.y) * __bfloat162float(g2.y);
     acc = warp_sum(acc);
@@ -670,7 +672,6 @@ __global__ void k_attn_prep(int T, int H, int d, int Peff, const int32_t* __rest
         const int sg = seg[i];
         meta[i] = make_int2(sg == 0 ? T : seg_end[sg], sg == 0 ? -1 : seg_start[sg]);
     }
-    (void)Peff;
 }
 
 struct BwdWs {
@@ -1654,7 +1655,7 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         if (!lse2) return false;
         int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
         const long warps = (long)aa.T * aa.H;
-        k_attn_prep<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(aa.T, aa.H, aa.d, aa.Peff, aa.seg, aa.seg_start,
+        k_attn_prep<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(aa.T, aa.H, aa.d, aa.ldo ? aa.ldo : aa.d, aa.seg, aa.seg_start,
                                                                       aa.seg_end, out, dout, lse, dsum, lse2, meta);
         PARL_LAUNCHED();
         AttnBwd2Args b;
@@ -1679,7 +1680,8 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
 // qkv: [T x 3d] bf16; returns false when the head dim / alignment is unsupported.
 bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cudaStream_t st) {
     if (!(aa.Dh == 64 || aa.Dh == 128)) return false;
-    if (((3L * aa.d * 2) % 16) || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    if (((3L * aa.d * 2) % 16) || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+        (((aa.ldo ? aa.ldo : aa.d) * 2) % 16))
         return false;
     auto fn = encode();
     if (!fn) return false;
@@ -1702,6 +1704,7 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     if (!a.q_ptr) return false;
     a.scale_log2 = aa.scale * LOG2E;
     a.out = out;
+    a.ldo = aa.ldo ? aa.ldo : aa.d;
     a.lse = lse;
     if (aa.Dh == 64 && aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
         AttnPairArgs pa;
@@ -1711,7 +1714,7 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
         pa.p_ptr = aa.sched.p_ptr; pa.p_list = aa.sched.p_list;
         pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
         pa.scale_log2 = aa.scale * LOG2E;
-        pa.out = out; pa.lse = lse;
+        pa.out = out; pa.ldo = aa.ldo ? aa.ldo : aa.d; pa.lse = lse;
         launch_fwd_pair(m, pa, st);
         return true;
     }

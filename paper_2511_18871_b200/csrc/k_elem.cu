@@ -80,13 +80,13 @@ __global__ void k_embed(const float* __restrict__ tok_emb, const float* __restri
 template <class T, int PER>
 __global__ void k_layernorm(const float* __restrict__ x, const int32_t* __restrict__ rows, int R, int D,
                             const float* __restrict__ gamma, const float* __restrict__ beta,
-                            T* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+                            T* __restrict__ y, long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
     // PER > 0: the row stays in registers (PER floats per lane, D <= 32 * PER); 0: strided passes
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= R) return;
     const int src = rows ? rows[warp] : warp;
     const float* xr = x + (long)src * D;
-    T* yr = y + (long)warp * D;
+    T* yr = y + (long)warp * ldy;
     float mean, rstd;
     if constexpr (PER > 0) {
         float v[PER];
@@ -683,29 +683,236 @@ void launch_embed(const float* tok, const float* pos, const int32_t* tokens, con
     PARL_LAUNCHED();
 }
 
+// float4 variant (D % 4 == 0): every load of the row is issued before any use
+template <class T>
+__device__ __forceinline__ void store4(T* p, float4 v);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+template <>
+__device__ __forceinline__ void store4<bf16>(bf16* p, float4 v) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(p) = u;
+}
+
+// float4 variant of the forward (D % 4 == 0, 16-byte aligned rows)
+template <class T, int P4>
+__global__ void __launch_bounds__(256) k_layernorm4(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                                                    int R, int D, const float* __restrict__ gamma,
+                                                    const float* __restrict__ beta, T* __restrict__ y, long ldy,
+                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const int D4 = D >> 2;
+    const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
+    float4 v[P4];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        v[k] = c < D4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+    }
+    const float mean = warp_sum(s) / D;
+    float var = 0.f;
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        if (c < D4) {
+            const float a = v[k].x - mean, b = v[k].y - mean, cc = v[k].z - mean, d = v[k].w - mean;
+            var += (a * a + b * b) + (cc * cc + d * d);
+        }
+    }
+    const float rstd = rsqrtf(warp_sum(var) / D + 1e-5f);
+    T* yr = y + (long)r * ldy;
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        if (c < D4) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+            const float4 b = __ldg(reinterpret_cast<const float4*>(beta) + c);
+            float4 o;
+            o.x = (v[k].x - mean) * rstd * g.x + b.x;
+            o.y = (v[k].y - mean) * rstd * g.y + b.y;
+            o.z = (v[k].z - mean) * rstd * g.z + b.z;
+            o.w = (v[k].w - mean) * rstd * g.w + b.w;
+            store4<T>(yr + 4 * c, o);
+        }
+    }
+    if (lane == 0) {
+        mean_out[r] = mean;
+        rstd_out[r] = rstd;
+    }
+}
+
 template <class T>
 void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
-                      float* mean, float* rstd, cudaStream_t st) {
+                      long ldy, float* mean, float* rstd, cudaStream_t st) {
     if (R <= 0) return;
-    if (D <= 256) k_layernorm<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
-    else if (D <= 1024) k_layernorm<T, 32><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
-    else if (D <= 2048) k_layernorm<T, 64><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
-    else k_layernorm<T, 0><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, mean, rstd);
+    const bool v4 = D % 4 == 0 && (ldy * (long)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+    if (v4 && D <= 512) k_layernorm4<T, 4><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 896) k_layernorm4<T, 7><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 1024) k_layernorm4<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (D <= 256) k_layernorm<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (D <= 1024) k_layernorm<T, 32><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (D <= 2048) k_layernorm<T, 64><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else k_layernorm<T, 0><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
     PARL_LAUNCHED();
 }
 template void launch_layernorm<float>(const float*, const int32_t*, int, int, const float*, const float*, float*,
-                                      float*, float*, cudaStream_t);
+                                      long, float*, float*, cudaStream_t);
 template void launch_layernorm<bf16>(const float*, const int32_t*, int, int, const float*, const float*, bf16*,
-                                     float*, float*, cudaStream_t);
+                                     long, float*, float*, cudaStream_t);
 
+// LayerNorm backward (model.cpp:319-343 reversed), input part: one warp per row
+// with the row held in registers: dx = (res) + rstd (dxh - mean(dxh) - xhat mean(dxh xhat)),
+// dxh = dy gamma, plus an optional compute-dtype copy of dx (the next GEMM's
+// operand).  The gamma / beta gradients are column sums done by colsum_impl
+// (mode 1) in a fixed order.
+template <class T, int PER>
+__global__ void __launch_bounds__(256) k_ln_bwd_rows(const float* __restrict__ dy, const float* __restrict__ x,
+                                                     const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                                     int R, int D, const float* __restrict__ res,
+                                                     float* __restrict__ dx, T* __restrict__ dx_act) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const float* xr = x + (long)(rows ? rows[r] : r) * D;
+    const float* dyr = dy + (long)r * D;
+    const float mu = mean[r], rs = rstd[r];
+    float vy[PER], xh[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int i = lane + 32 * q;
+        vy[q] = i < D ? dyr[i] * __ldg(gamma + i) : 0.f;
+        xh[q] = i < D ? (xr[i] - mu) * rs : 0.f;
+    }
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        sa += vy[q];
+        sb += vy[q] * xh[q];
+    }
+    sa = warp_sum(sa) / D;
+    sb = warp_sum(sb) / D;
+    float* o = dx + (long)r * D;
+    const float* rr = res ? res + (long)r * D : nullptr;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int i = lane + 32 * q;
+        if (i < D) {
+            float v = rs * (vy[q] - sa - xh[q] * sb);
+            if (rr) v += rr[i];
+            o[i] = v;
+            if (dx_act) dx_act[(long)r * D + i] = from_f<T>(v);
+        }
+    }
+}
+
+template <class T, int P4>
+__global__ void __launch_bounds__(256) k_ln_bwd_rows4(const float* __restrict__ dy, const float* __restrict__ x,
+                                                      const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                                      const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                                      int R, int D, const float* __restrict__ res,
+                                                      float* __restrict__ dx, T* __restrict__ dx_act) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const int D4 = D >> 2;
+    const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
+    const float4* dyr = reinterpret_cast<const float4*>(dy + (long)r * D);
+    const float4* rr = res ? reinterpret_cast<const float4*>(res + (long)r * D) : nullptr;
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    float4 vy[P4], vx[P4], vr[P4];
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        const bool ok = c < D4;
+        vy[k] = ok ? dyr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        vx[k] = ok ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        vr[k] = (ok && rr) ? rr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float mu = mean[r], rs = rstd[r];
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        const float4 g = c < D4 ? __ldg(g4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        vy[k].x *= g.x; vy[k].y *= g.y; vy[k].z *= g.z; vy[k].w *= g.w;  // dxh
+        vx[k].x = (vx[k].x - mu) * rs; vx[k].y = (vx[k].y - mu) * rs;     // xhat
+        vx[k].z = (vx[k].z - mu) * rs; vx[k].w = (vx[k].w - mu) * rs;
+        sa += (vy[k].x + vy[k].y) + (vy[k].z + vy[k].w);
+        sb += (vy[k].x * vx[k].x + vy[k].y * vx[k].y) + (vy[k].z * vx[k].z + vy[k].w * vx[k].w);
+    }
+    sa = warp_sum(sa) / D;
+    sb = warp_sum(sb) / D;
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+        const int c = lane + 32 * k;
+        if (c < D4) {
+            float4 v;
+            v.x = rs * (vy[k].x - sa - vx[k].x * sb) + vr[k].x;
+            v.y = rs * (vy[k].y - sa - vx[k].y * sb) + vr[k].y;
+            v.z = rs * (vy[k].z - sa - vx[k].z * sb) + vr[k].z;
+            v.w = rs * (vy[k].w - sa - vx[k].w * sb) + vr[k].w;
+            reinterpret_cast<float4*>(dx + (long)r * D)[c] = v;
+            if (dx_act) store4<T>(dx_act + (long)r * D + 4 * c, v);
+        }
+    }
+}
+
+template <class T>
 void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
-                          const float* gamma, int R, int D, const float* res, float* dx, float* dgamma, float* dbeta,
-                          cudaStream_t st) {
+                          const float* gamma, int R, int D, const float* res, float* dx, T* dx_act, float* dgamma,
+                          float* dbeta, cudaStream_t st) {
     if (R <= 0) return;
-    k_layernorm_bwd<<<cdiv(R, 8), 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx);
+    const int blocks = cdiv(R, 8);
+    if (D % 4 == 0 && D <= 1024) {
+        if (D <= 512) k_ln_bwd_rows4<T, 4><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+        else if (D <= 896) k_ln_bwd_rows4<T, 7><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+        else k_ln_bwd_rows4<T, 8><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    } else if (D <= 256) k_ln_bwd_rows<T, 8><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    else if (D <= 512) k_ln_bwd_rows<T, 16><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    else if (D <= 768) k_ln_bwd_rows<T, 24><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    else if (D <= 896) k_ln_bwd_rows<T, 28><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    else if (D <= 1024) k_ln_bwd_rows<T, 32><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    else {
+        k_layernorm_bwd<<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx);
+        PARL_LAUNCHED();
+        if (dx_act) launch_f32_to_act<T>(dx, dx_act, (size_t)R * D, st);
+        colsum_impl<float>(dy, D, R, D, dgamma, x, rows, mean, rstd, dbeta, 1, st);
+        return;
+    }
     PARL_LAUNCHED();
     colsum_impl<float>(dy, D, R, D, dgamma, x, rows, mean, rstd, dbeta, 1, st);
 }
+template void launch_layernorm_bwd<float>(const float*, const float*, const int32_t*, const float*, const float*,
+                                          const float*, int, int, const float*, float*, float*, float*, float*,
+                                          cudaStream_t);
+template void launch_layernorm_bwd<bf16>(const float*, const float*, const int32_t*, const float*, const float*,
+                                         const float*, int, int, const float*, float*, bf16*, float*, float*,
+                                         cudaStream_t);
+
+// pad columns [D, ld) of every row: 1 at column D (bias row of a weight-gradient
+// GEMM), 0 after it
+template <class T>
+__global__ void k_fill_pad(T* __restrict__ y, long rows, int D, long ld) {
+    const long n = rows * (ld - D);
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const long r = e / (ld - D);
+        const int c = (int)(e % (ld - D));
+        y[r * ld + D + c] = from_f<T>(c == 0 ? 1.f : 0.f);
+    }
+}
+template <class T>
+void launch_fill_pad(T* y, long rows, int D, long ld, cudaStream_t st) {
+    if (rows <= 0 || ld <= D) return;
+    k_fill_pad<T><<<grid_for(rows * (ld - D)), 256, 0, st>>>(y, rows, D, ld);
+    PARL_LAUNCHED();
+}
+template void launch_fill_pad<float>(float*, long, int, long, cudaStream_t);
+template void launch_fill_pad<bf16>(bf16*, long, int, long, cudaStream_t);
 
 template <class T>
 void launch_colsum(const T* X, long ldx, int R, int N, float* out, cudaStream_t st) {
@@ -774,7 +981,9 @@ size_t sort_temp_bytes(int n) {
 
 void launch_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
                        const int32_t* vals_in, int32_t* vals_out, int n, int end_bit, cudaStream_t st) {
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n, 0, end_bit, st);
+    const cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, n,
+                                                          0, end_bit, st);
+    if (e != cudaSuccess) throw Error{PARL_E_CUDA, std::string("radix sort: ") + cudaGetErrorString(e)};
     PARL_LAUNCHED();
 }
 

@@ -14,6 +14,10 @@ struct PackedDev {
 };
 
 // Reference flat layout offsets (model.cpp:86-114).
+// Activations that feed weight-gradient GEMMs carry PAD_COLS extra columns
+// (1, 0, ..., 0): the GEMM over in+1 rows then yields the bias gradient too.
+constexpr int PAD_COLS = 64;  // keeps padded rows 128-byte aligned (bf16) for TMA
+
 struct FlatLayout {
     size_t tok_emb, pos_emb, layer0, layer_stride, lnf_g, lnf_b, head_w, head_b, total;
     struct Layer {
@@ -81,10 +85,13 @@ void launch_embed(const float* tok, const float* pos, const int32_t* tokens, con
                   float* x, cudaStream_t st);
 template <class T>
 void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
-                      float* mean, float* rstd, cudaStream_t st);
+                      long ldy, float* mean, float* rstd, cudaStream_t st);
+template <class T>
 void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
-                          const float* gamma, int R, int D, const float* res, float* dx, float* dgamma, float* dbeta,
-                          cudaStream_t st);
+                          const float* gamma, int R, int D, const float* res, float* dx, T* dx_act, float* dgamma,
+                          float* dbeta, cudaStream_t st);
+template <class T>
+void launch_fill_pad(T* y, long rows, int D, long ld, cudaStream_t st);
 template <class T>
 void launch_colsum(const T* X, long ldx, int R, int N, float* out, cudaStream_t st);
 void launch_row_lse(const float* z, int S, int V, const int32_t* labels, float* lse, float* lp, cudaStream_t st);
@@ -144,6 +151,7 @@ struct AttnSched {
 struct AttnArgs {
     AttnSched sched;
     int T, H, Dh, d;
+    long ldo = 0;              // row stride of the attention output O (0: d)
     int Peff;                  // end of segment 0 (prompt length, or T when causal)
     const int32_t* seg;        // [T]
     const int32_t* seg_start;  // [G+1]

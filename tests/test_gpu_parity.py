@@ -139,11 +139,15 @@ def test_tiny_microbatch_fp32(P, ctx32, gran):
     assert gb.micro_step_count() == 1
 
 
-def _c1_setup(P, ctx):
+def c2w(P):
+    return P.ModelConfig(4096, 896, 1, 14, 4864, 512)
+
+
+def _c1_setup(P, ctx, name="c1_micro.npz", cfg_of=c1):
     from oracle.make_golden import perturb
 
-    z = load("c1_micro.npz")
-    cfg = c1(P)
+    z = load(name)
+    cfg = cfg_of(P)
     pol = P.ModelParams.init(cfg, int(z["seed"]), ctx)
     w = pol.flat()
     tm = P.TriModel(pol, P.ModelParams.from_flat(cfg, perturb(w, int(z["old_seed"]), float(z["scale"])), ctx=ctx),
@@ -220,6 +224,33 @@ def test_c1_microbatch_bf16_stats(P, ctx16):
     assert abs(st["objective_sum"] - z["stats"][0]) <= BF16_TOL["obj_rel"] * abs(z["stats"][0]) + 1e-3
     assert st["total_units"] == z["stats"][4]
     assert gb.micro_step_count() == 1
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_c2_width_microbatch(P, ctx32, ctx16, prec):
+    """C2's layer width (d=896, H=14, F=4864) on a ragged group: the kernels' wide-row
+    paths (LayerNorm backward, padded activations, head) against the reference."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    tol = FP32_TOL if prec == "fp32" else BF16_TOL
+    z, cfg, tm, pk = _c1_setup(P, ctx, "c2w_micro.npz", c2w)
+    gb = P.GradBuffer(tm.policy)
+    ctx.stats_reset()
+    st = P.train_microbatch(tm, pk.group, gb, P.HyperParams(), advantages=z["advantages"])
+    for slot in range(3):
+        d = np.abs(pk.group.logprobs(slot) - z["lp3"][slot])
+        if prec == "fp32":  # fp32 rounding grows with the contraction widths: 2x C1's bound at d=896, F=4864
+            assert d.max() < 2 * tol["lp_abs"], (slot, d.max())
+        else:
+            assert d.max() < tol["lp_max"] and d.mean() < tol["lp_mean"], (slot, d.max(), d.mean())
+    assert abs(st["objective_sum"] - z["stats"][0]) <= tol["obj_rel"] * abs(z["stats"][0]) + 1e-3
+    g = gb.flat()
+    sampled, ref = g[z["grad_idx"]], z["grad_vals"]
+    if prec == "fp32":
+        assert np.linalg.norm(sampled - ref) / np.linalg.norm(ref) < tol["grad_rel"]
+    else:
+        assert sampled @ ref / (np.linalg.norm(sampled) * np.linalg.norm(ref)) > tol["cos"]
+    rels = _grad_summaries(cfg, g, z)
+    assert max(rels.values()) < tol["grad_rel"], max(rels.items(), key=lambda kv: kv[1])
 
 
 # --------------------------------------------------------------------------- reference contracts
