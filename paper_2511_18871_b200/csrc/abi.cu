@@ -605,6 +605,26 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     aa.sched = g->sched;
     aa.ldo = Dp;
 
+    // weight-gradient GEMMs of a layer are collected and run as one grouped launch
+    // (bf16); the fp32 path runs them as they come
+    std::vector<GemmArgs> dw;
+    auto add_dw = [&](const GemmArgs& ga) {
+        if constexpr (std::is_same_v<T, bf16>) dw.push_back(ga);
+        else gemm<T>(c, ga);
+    };
+    auto flush_dw = [&]() {
+        if (dw.empty()) return;
+        bool done = false;
+        if constexpr (std::is_same_v<T, bf16>) {
+            double fl = 0;
+            for (const auto& ga : dw) fl += 2.0 * ga.M * (double)ga.N * ga.K;
+            ProfScope ps(c, PARL_KC_GEMM, fl);
+            done = gemm_tc_group_dw(dw.data(), (int)dw.size(), st);
+        }
+        if (!done)
+            for (const auto& ga : dw) gemm<T>(c, ga);
+        dw.clear();
+    };
     for (int l = NL - 1; l >= 0; --l) {
         const LayerW& w = m->layers[l];
         const auto o = L.layer(l, D, F);
@@ -628,7 +648,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         {  // [dW2; db2] += [act 1]^T dx
             GemmArgs ga = mk(F + 1, D, Tn, vl, 1, Fp, dx_act, 1, D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w2; ga.ldc = D;
-            gemm<T>(c, ga);
+            add_dw(ga);
         }
         {
             GemmArgs ga = mk(Tn, D, F, dpre, Fp, 1, w.w1_t, 1, D);
@@ -638,7 +658,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         {  // [dW1; db1] += [LN2 1]^T dpre
             GemmArgs ga = mk(D + 1, F, Tn, bl, 1, Dp, dpre, 1, Fp);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.w1; ga.ldc = F;
-            gemm<T>(c, ga);
+            add_dw(ga);
         }
         // LN2 (model.cpp:729-730): dmid = dx + LN2^T(dbn), plus its compute-dtype copy
         {
@@ -655,7 +675,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         {  // [dWo; dbo] += [ctx 1]^T dmid
             GemmArgs ga = mk(D + 1, D, Tn, cl, 1, Dp, dmid_act, 1, D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + o.wo; ga.ldc = D;
-            gemm<T>(c, ga);
+            add_dw(ga);
         }
         // attention (model.cpp:752-786)
         {
@@ -676,8 +696,9 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         for (int p = 0; p < 3; ++p) {  // [dWp; dbp] += [LN1 1]^T dqkv_p
             GemmArgs ga = mk(D + 1, D, Tn, al, 1, Dp, dqkv + (size_t)p * D, 1, 3 * D);
             ga.epi = EPI_F32_ACC; ga.Cf = G + woff[p]; ga.ldc = D;
-            gemm<T>(c, ga);
+            add_dw(ga);
         }
+        flush_dw();  // dx_act is overwritten next
         // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da), plus the next layer's compute-dtype copy
         {
             ProfScope ps_(c, PARL_KC_NORM, 0.0);

@@ -127,5 +127,7 @@ template <class T>
 void gemm_simt(const GemmArgs& g, cudaStream_t st);
 // tcgen05 path (bf16 only).  Returns false if the shape/layout is not supported.
 bool gemm_tc(const GemmArgs& g, cudaStream_t st);
+// all weight-gradient GEMMs of a layer in one launch (MN-major A and B, shared K, fp32 accumulate)
+bool gemm_tc_group_dw(const GemmArgs* gs, int n, cudaStream_t st);
 
 }  // namespace parl_gpu

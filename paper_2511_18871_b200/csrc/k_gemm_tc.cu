@@ -582,6 +582,160 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Grouped weight-gradient GEMM (CTA pair, A and B MN-major, K shared):
+//   for each problem p:  C_p[M_p x N_p] += A_p^T B_p   (fp32, TMA reduce-add)
+// One persistent launch covers all dW / db GEMMs of a layer, so the tile count
+// fills the machine without split-K (every output element has exactly one
+// writer: deterministic) and one problem's last wave overlaps the next's.
+constexpr int GROUP_MAX = 8;
+struct GroupMaps {
+    CUtensorMap a[GROUP_MAX], b[GROUP_MAX], o[GROUP_MAX];
+};
+struct GroupArgs {
+    int n_prob, nkb;
+    int M[GROUP_MAX], tiles_m2[GROUP_MAX], tiles_n[GROUP_MAX], start[GROUP_MAX + 1];  // start: first pair-tile of p
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_gemm_group2(const __grid_constant__ GroupMaps mp, const __grid_constant__ GroupArgs g) {
+    using C = Cfg2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int n_items = g.start[g.n_prob];
+    // item -> (problem, m pair-tile, n tile)
+    auto decode = [&](int item, int& p, int& mt, int& nt) {
+        p = 0;
+        while (p + 1 < g.n_prob && item >= g.start[p + 1]) ++p;
+        const int t = item - g.start[p];
+        mt = t % g.tiles_m2[p];
+        nt = t / g.tiles_m2[p];
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&tfull[s], 1);
+            tc::mbar_init(&tempty[s], 2 * 32 * EPI_WARPS);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 2) tc::tmem_alloc_pair<2 * BN2>(tbase_s);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tbase = *tbase_s;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer
+        uint32_t cnt = 0;
+        for (int item = cid; item < n_items; item += ncl) {
+            int p, mt, nt;
+            decode(item, p, mt, nt);
+            const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * BN2 + (int)rank * (BN2 / 2);
+            for (int kb = 0; kb < g.nkb; ++kb, ++cnt) {
+                const int s = cnt % C::STAGES;
+                const uint32_t ph = (cnt / C::STAGES) & 1;
+                tc::mbar_wait(&empty[s], ph ^ 1);
+                const uint32_t fb = tc::mapa(&full[s], 0);
+                if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * C::STAGE);
+                uint8_t* sa = smem + s * C::STAGE;
+                uint8_t* sb = sa + C::A_BYTES;
+                tc::tma_load_2d_pair(sa, &mp.a[p], fb, m0, kb * BK);
+                tc::tma_load_2d_pair(sa + 8192, &mp.a[p], fb, m0 + 64, kb * BK);
+                tc::tma_load_2d_pair(sb, &mp.b[p], fb, n0, kb * BK);
+                tc::tma_load_2d_pair(sb + 8192, &mp.b[p], fb, n0 + 64, kb * BK);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA)
+        constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, 1, 1);
+        uint32_t cnt = 0, local = 0;
+        for (int item = cid; item < n_items; item += ncl, ++local) {
+            const uint32_t acc = local & 1, use = local >> 1;
+            tc::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+            tc::tc_fence_after();
+            const uint32_t dcol = tbase + acc * BN2;
+            for (int kb = 0; kb < g.nkb; ++kb, ++cnt) {
+                const int s = cnt % C::STAGES;
+                const uint32_t ph = (cnt / C::STAGES) & 1;
+                tc::mbar_wait(&full[s], ph);
+                tc::tc_fence_after();
+                const uint32_t sa = tc::smem_u32(smem + s * C::STAGE);
+                const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                for (int ks = 0; ks < BK / 16; ++ks)
+                    tc::mma_bf16_pair(dcol, tc::sdesc(sa + ks * 2048, 8192, 1024), tc::sdesc(sb + ks * 2048, 8192, 1024),
+                                      idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                tc::mma_commit_pair(&empty[s], 0x3);
+            }
+            tc::mma_commit_pair(&tfull[acc], 0x3);
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: fp32 accumulator -> swizzled staging -> TMA reduce-add
+        const int ew = warp & 3, half = (warp - 4) >> 2, wi = warp - 4;
+        const uint32_t stg = tc::smem_u32(smem + C::STG_OFF + wi * NBUF * STG_BYTES);
+        const uint32_t leader_tempty0 = tc::mapa(&tempty[0], 0);
+        uint32_t k = 0, local = 0;
+        for (int item = cid; item < n_items; item += ncl, ++local) {
+            int p, mt, nt;
+            decode(item, p, mt, nt);
+            const uint32_t acc = local & 1, use = local >> 1;
+            tc::mbar_wait(&tfull[acc], use & 1);
+            tc::tc_fence_after();
+            const int row0 = mt * 2 * BM + (int)rank * BM + ew * 32;
+            const bool rows_live = row0 < g.M[p];
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c, ++k) {
+                const int col = nt * BN2 + half * 128 + c * 32;
+                const uint32_t sb = stg + (k % NBUF) * STG_BYTES;
+                float v[32];
+                tc::tmem_ld32(tbase + acc * BN2 + half * 128 + c * 32 + ((uint32_t)(ew * 32) << 16), v);
+                if (c == 3) {
+                    tc::tc_fence_before();
+                    tc::mbar_arrive_cluster_relaxed(leader_tempty0 + acc * 8);
+                }
+                if (!rows_live) continue;  // the whole 32-row slab is past M (e.g. beyond a bias row)
+                if (lane == 0) tc::bulk_wait_read<NBUF - 1>();
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    tc::sts128(sb + sw128(lane, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                               __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+                tc::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::tma_reduce_add_2d(&mp.o[p], sb, col, row0);
+                    tc::bulk_commit();
+                }
+            }
+        }
+        if (lane == 0) tc::bulk_wait<0>();
+        __syncwarp();
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::cluster_sync();
+    if (warp == 2) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_pair<2 * BN2>(tbase);
+    }
+}
+
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C, long ldc) {
     const long n = (long)M * N;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
@@ -711,6 +865,43 @@ bool pair_enabled() {
 }
 
 }  // namespace
+
+// C_p += A_p^T B_p for every problem (A_p: [K x M_p], B_p: [K x N_p] bf16 row-major,
+// i.e. MN-major operands; C_p fp32 [M_p x N_p] with row stride ldc_p).  All
+// problems share K.  Returns false when a problem is unsupported (the caller
+// then runs them one by one).
+bool gemm_tc_group_dw(const GemmArgs* gs, int n, cudaStream_t st) {
+    if (n <= 0 || n > GROUP_MAX || !pair_enabled() || !encode_fn()) return false;
+    static GroupMaps maps;  // host staging of the kernel parameter (copied at launch)
+    GroupArgs ga{};
+    ga.n_prob = n;
+    const int K = gs[0].K;
+    ga.nkb = (K + BK - 1) / BK;
+    int tiles = 0;
+    for (int p = 0; p < n; ++p) {
+        const GemmArgs& g = gs[p];
+        if (g.K != K || g.sam != 1 || g.sbn != 1 || g.epi != EPI_F32_ACC || g.N % 128 != 0) return false;
+        if ((g.sak * 2) % 16 || (g.sbk * 2) % 16 || !aligned16(g.A) || !aligned16(g.B)) return false;
+        if (!make_map(&maps.a[p], g.A, g.M, g.K, g.sak, 64, BK)) return false;
+        if (!make_map(&maps.b[p], g.B, g.N, g.K, g.sbk, 64, BK)) return false;
+        if (!make_epi_map(&maps.o[p], g.Cf, true, g.N, g.M, g.ldc)) return false;
+        ga.M[p] = g.M;
+        ga.tiles_m2[p] = (g.M + 2 * BM - 1) / (2 * BM);
+        ga.tiles_n[p] = (g.N + BN2 - 1) / BN2;
+        ga.start[p] = tiles;
+        tiles += ga.tiles_m2[p] * ga.tiles_n[p];
+    }
+    ga.start[n] = tiles;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_group2, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+        attr = true;
+    }
+    const int grid = 2 * std::min(tiles, num_sms() / 2);
+    k_gemm_group2<<<grid, NTHREADS, Cfg2::SMEM, st>>>(maps, ga);
+    PARL_LAUNCHED();
+    return true;
+}
 
 bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return true;
