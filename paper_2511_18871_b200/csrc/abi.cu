@@ -550,12 +550,15 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     if (S > 0) {
         // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
         T* dz = c->dz.as<T>((size_t)S * V);
-        if (act->logits_bf16)
-            launch_softmax_bwd<bf16, T>(static_cast<bf16*>(act->logits.p), V, dz, V, S, V,
-                                        static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
-        else
-            launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
-                                         static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
+        {
+            ProfScope ps_sm(c, PARL_KC_HEAD, 4.0 * S * (double)V);
+            if (act->logits_bf16)
+                launch_softmax_bwd<bf16, T>(static_cast<bf16*>(act->logits.p), V, dz, V, S, V,
+                                            static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
+            else
+                launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
+                                             static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
+        }
         T* hf = static_cast<T*>(act->hf.p);
         float* dhf = c->dhf.as<float>((size_t)S * D);
         {  // dH = dZ W_head^T (model.cpp:654-666)

@@ -8,6 +8,7 @@
 //   K11 embedding-grad reduce  model.cpp:825-834 (deterministic: stable sort + segmented sum)
 // plus column reductions (bias / LN parameter grads), weight conversion,
 // device init, SGD update.
+#include <type_traits>
 #include <algorithm>
 #include <cub/cub.cuh>
 
@@ -419,6 +420,35 @@ __global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restr
             const int v = v0 + q;
             if (v < V) dr[v] = from_f<Tout>(us * ((v == lab ? 1.f : 0.f) - __expf(to_f<Tin>(zr[v]) - L)));
         }
+    }
+}
+
+// bf16 -> bf16 variant with 16-byte loads / stores (ldz, lddz, V multiples of 8)
+__global__ void k_softmax_bwd_v8(const bf16* __restrict__ z, long ldz, bf16* __restrict__ dz, long lddz, int S, int V,
+                                 const float* __restrict__ lse, const float* __restrict__ u,
+                                 const int32_t* __restrict__ labels) {
+    const int s = blockIdx.y;
+    const float us = u[s], L2 = lse[s] * 1.4426950408889634f;
+    const int lab = labels[s];
+    const uint4* zr = reinterpret_cast<const uint4*>(z + (long)s * ldz);
+    uint4* dr = reinterpret_cast<uint4*>(dz + (long)s * lddz);
+    const int n8 = V >> 3;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n8; c += gridDim.x * blockDim.x) {
+        const uint4 in = zr[c];
+        const uint32_t w[4] = {in.x, in.y, in.z, in.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int v = 8 * c + 2 * q;
+            const float z0 = __uint_as_float(w[q] << 16), z1 = __uint_as_float(w[q] & 0xffff0000u);
+            float d0 = -us * exp2f(fmaf(z0, 1.4426950408889634f, -L2));
+            float d1 = -us * exp2f(fmaf(z1, 1.4426950408889634f, -L2));
+            if (v == lab) d0 += us;
+            if (v + 1 == lab) d1 += us;
+            __nv_bfloat162 b = __floats2bfloat162_rn(d0, d1);
+            o[q] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        dr[c] = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
 
@@ -940,6 +970,14 @@ void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int 
                         const int32_t* labels, cudaStream_t st) {
     if (S <= 0) return;
     const int cx = std::max(1, std::min(cdiv(V, 256 * 8), 8));
+    if constexpr (std::is_same_v<Tin, bf16> && std::is_same_v<Tout, bf16>) {
+        if (V % 8 == 0 && ldz % 8 == 0 && lddz % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
+            (reinterpret_cast<uintptr_t>(dz) & 15) == 0) {
+            k_softmax_bwd_v8<<<dim3(cx, S), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
+            PARL_LAUNCHED();
+            return;
+        }
+    }
     k_softmax_bwd<Tin, Tout><<<dim3(cx, S), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
     PARL_LAUNCHED();
 }
