@@ -53,6 +53,22 @@ def flops_per_group(c, P, lens, reference_head=False):
     return 3 * (gemm + attn + head) + 2 * gemm + 2.5 * attn + 2 * head
 
 
+def measured_traffic(cls):
+    """DRAM bytes per launch of a kernel class from the newest committed ncu traffic
+    summary (profiles/rNN_traffic.json, scripts/traffic.py), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        return d["classes"][cls]["dram_bytes_per_launch"], os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -329,6 +345,7 @@ def run_ours(args, c):
     dp = prof[dom]
     achieved = dp["work"] / (dp["ms"] / 1000.0) / 1e12 if dp["ms"] > 0 else 0.0
     step_ms = ms_max / args.steps
+    traffic, traffic_src = measured_traffic(dom)
     share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
     c["name"] = args.config
     cpu = reference_sample(c) if (rank == 0 and world == 1 and not args.no_cpu) else None
@@ -348,7 +365,8 @@ def run_ours(args, c):
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": achieved / bf16_sus, "peak_kind": f"{src} bf16 sustained",
-                     "traffic": None, "share_of_step": share},
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, read + write)",
+                     "traffic_source": traffic_src, "share_of_step": share},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                                "achieved": (v["work"] / (v["ms"] / 1e3) / (1e12 if k in tc else 1e9))
                                if v["ms"] > 0 else None,
