@@ -559,10 +559,15 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                         sv[j] = ok ? sv[j] : -INFINITY;
                     }
                 }
-                float mx = fmax3(sv[0], sv[1], sv[2]);
+                float mq[4];  // four independent max chains
 #pragma unroll
-                for (int j = 3; j < 127; j += 2) mx = fmax3(mx, sv[j], sv[j + 1]);
-                mx = fmaxf(mx, sv[127]);
+                for (int q = 0; q < 4; ++q) mq[q] = fmaxf(sv[q], sv[q + 4]);
+#pragma unroll
+                for (int j = 8; j < 128; j += 8) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mq[q] = fmax3(mq[q], sv[j + 2 * q], sv[j + 2 * q + 1]);
+                }
+                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
                 const float mxl = mx * c2;
                 const bool need = mxl > m_used + 8.f;
                 const float m_new = need ? mxl : m_used;

@@ -26,7 +26,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libparl_gpu.so")
+LIB_PATH = os.environ.get("PARL_LIB", os.path.join(_HERE, "libparl_gpu.so"))  # PARL_LIB: A/B runs of another build
 
 kIgnoreLabel = -1
 

@@ -24,7 +24,7 @@ for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
         args = (path, T, H, Dh, Pl, seg.data_ptr(), st.data_ptr(), en.data_ptr(), qkv.data_ptr(), out.data_ptr(), lse.data_ptr())
         assert f(*args) == 0, P.LIB.parl_last_error(None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 5 if path == 0 else 1
+        n = 30 if path == 0 else 1
         args2 = ((2,) + args[1:]) if path == 0 else args
         e0.record()
         for _ in range(n):
@@ -58,7 +58,7 @@ for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
                 dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(), dqkv.data_ptr())
         assert fb(*args) == 0, P.LIB.parl_last_error(None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 5 if path == 0 else 1
+        n = 30 if path == 0 else 1
         args2 = ((2,) + args[1:]) if path == 0 else args
         e0.record()
         for _ in range(n):
