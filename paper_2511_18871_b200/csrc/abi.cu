@@ -18,6 +18,14 @@
 
 namespace parl_gpu {
 uint64_t g_launches = 0;
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PARL_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
 }
 
 using namespace parl_gpu;

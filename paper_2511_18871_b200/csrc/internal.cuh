@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "parl_gpu.h"
 
@@ -44,6 +45,32 @@ extern uint64_t g_launches;
             throw ::parl_gpu::Error{PARL_E_CUDA, std::string("kernel launch at ") + __FILE__ + ":" +      \
                                                      std::to_string(__LINE__) + ": " + cudaGetErrorString(e_)}; \
     } while (0)
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: kernels launched with launch_pdl() may start
+// while the previous kernel of the stream is still draining; they run their
+// input-independent prologue, then pdl_wait() for the predecessor's completion
+// (and memory) before touching its outputs.  pdl_trigger() lets the successor
+// launch before this grid has fully exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // PARL_PDL=0 disables (diagnostics)
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // small device helpers

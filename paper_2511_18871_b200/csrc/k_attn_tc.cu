@@ -397,6 +397,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
     const uint32_t t_s = tbase, t_o = tbase + 256, t_p = tbase + 256 + 2 * DH;
+    pdl_wait();
+    pdl_trigger();
 
     if (warp >= 8) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
@@ -660,6 +662,7 @@ __global__ void k_attn_prep(int T, int H, int d, long ldo, const int32_t* __rest
                             const bf16* __restrict__ out, const bf16* __restrict__ dout,
                             const float* __restrict__ lse, float* __restrict__ dsum, float* __restrict__ lse2,
                             int2* __restrict__ meta) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long)T * H) return;
@@ -794,6 +797,8 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
     const uint32_t t_s = tbase, t_dp = tbase + 128, t_acc1 = tbase + 256, t_acc2 = tbase + 320;
+    pdl_wait();
+    pdl_trigger();
     const uint32_t t_p = tbase + 384, t_ds = tbase + 448;
 
     if (warp >= 8) {
@@ -1576,7 +1581,7 @@ void launch_fwd_pair(const CUtensorMap& m, const AttnPairArgs& a, cudaStream_t s
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     (void)sms;
-    k_attn_fwd_pair<64><<<a.grid, PAIR_NTHR, PairSmem<64>::TOTAL, st>>>(m, a);
+    launch_pdl(k_attn_fwd_pair<64>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<64>::TOTAL, st, m, a);
     PARL_LAUNCHED();
 }
 
@@ -1626,7 +1631,7 @@ void launch_bwd2(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwd2Arg
         cudaFuncSetAttribute(k_attn_bwd2<64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Smem<64>::TOTAL);
         attr = true;
     }
-    k_attn_bwd2<64, MODE><<<grid, BWD_NTHR, Bwd2Smem<64>::TOTAL, st>>>(mq, md, a);
+    launch_pdl(k_attn_bwd2<64, MODE>, dim3(grid), dim3(BWD_NTHR), Bwd2Smem<64>::TOTAL, st, mq, md, a);
     PARL_LAUNCHED();
 }
 
@@ -1660,8 +1665,8 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         if (!lse2) return false;
         int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
         const long warps = (long)aa.T * aa.H;
-        k_attn_prep<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(aa.T, aa.H, aa.d, aa.ldo ? aa.ldo : aa.d, aa.seg, aa.seg_start,
-                                                                      aa.seg_end, out, dout, lse, dsum, lse2, meta);
+        launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d,
+                   (long)(aa.ldo ? aa.ldo : aa.d), aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
         PARL_LAUNCHED();
         AttnBwd2Args b;
         b.T = aa.T; b.H = aa.H; b.d = aa.d; b.Peff = aa.Peff;

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(256) k_colsum_part(const T* __restrict__ X, lo
                                                      const int32_t* __restrict__ rows, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, int mode,
                                                      float* __restrict__ part_a, float* __restrict__ part_b) {
+    pdl_wait();
     __shared__ float2 sa[8][32], sb[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x * 64 + 2 * lane;
@@ -292,6 +293,7 @@ __global__ void k_colsum_part1(const T* __restrict__ X, long ldx, int R, int N, 
 
 __global__ void k_colsum_final(const float* __restrict__ part_a, const float* __restrict__ part_b, int splits, int N,
                                float* __restrict__ out, float* __restrict__ out2, int mode) {
+    pdl_wait();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     float a = 0.f, b = 0.f;
@@ -330,13 +332,14 @@ static void colsum_impl(const T* X, long ldx, int R, int N, float* out, const fl
     float* pa = g_colsum_scratch.get((size_t)2 * splits * N);
     float* pb = pa + (size_t)splits * N;
     if (vec)
-        k_colsum_part<T><<<dim3(col_blocks, splits), 256, 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd, mode, pa,
-                                                                   pb);
+        launch_pdl(k_colsum_part<T>, dim3(col_blocks, splits), dim3(256), 0, st, X, ldx, R, N, rps, xs, rows, mean, rstd,
+                   mode, pa, pb);
     else
         k_colsum_part1<T><<<dim3(col_blocks, splits), dim3(32, 8), 0, st>>>(X, ldx, R, N, rps, xs, rows, mean, rstd,
                                                                            mode, pa, pb);
     PARL_LAUNCHED();
-    k_colsum_final<<<cdiv(N, 256), 256, 0, st>>>(pa, pb, splits, N, out, out2, mode);
+    launch_pdl(k_colsum_final, dim3(cdiv(N, 256)), dim3(256), 0, st, (const float*)pa, (const float*)pb, splits, N, out,
+               out2, mode);
     PARL_LAUNCHED();
 }
 
@@ -427,6 +430,7 @@ __global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restr
 __global__ void k_softmax_bwd_v8(const bf16* __restrict__ z, long ldz, bf16* __restrict__ dz, long lddz, int S, int V,
                                  const float* __restrict__ lse, const float* __restrict__ u,
                                  const int32_t* __restrict__ labels) {
+    pdl_wait();
     const int s = blockIdx.y;
     const float us = u[s], L2 = lse[s] * 1.4426950408889634f;
     const int lab = labels[s];
@@ -733,6 +737,7 @@ __global__ void __launch_bounds__(256) k_layernorm4(const float* __restrict__ x,
                                                     int R, int D, const float* __restrict__ gamma,
                                                     const float* __restrict__ beta, T* __restrict__ y, long ldy,
                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    pdl_wait();
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (r >= R) return;
     const int D4 = D >> 2;
@@ -782,9 +787,9 @@ void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const f
                       long ldy, float* mean, float* rstd, cudaStream_t st) {
     if (R <= 0) return;
     const bool v4 = D % 4 == 0 && (ldy * (long)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
-    if (v4 && D <= 512) k_layernorm4<T, 4><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
-    else if (v4 && D <= 896) k_layernorm4<T, 7><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
-    else if (v4 && D <= 1024) k_layernorm4<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
+    if (v4 && D <= 512) launch_pdl(k_layernorm4<T, 4>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 896) launch_pdl(k_layernorm4<T, 7>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 1024) launch_pdl(k_layernorm4<T, 8>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 256) k_layernorm<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 1024) k_layernorm<T, 32><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 2048) k_layernorm<T, 64><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
@@ -847,6 +852,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd_rows4(const float* __restrict__ 
                                                       const float* __restrict__ rstd, const float* __restrict__ gamma,
                                                       int R, int D, const float* __restrict__ res,
                                                       float* __restrict__ dx, T* __restrict__ dx_act) {
+    pdl_wait();
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (r >= R) return;
     const int D4 = D >> 2;
@@ -899,9 +905,9 @@ void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, 
     if (R <= 0) return;
     const int blocks = cdiv(R, 8);
     if (D % 4 == 0 && D <= 1024) {
-        if (D <= 512) k_ln_bwd_rows4<T, 4><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
-        else if (D <= 896) k_ln_bwd_rows4<T, 7><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
-        else k_ln_bwd_rows4<T, 8><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+        if (D <= 512) launch_pdl(k_ln_bwd_rows4<T, 4>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+        else if (D <= 896) launch_pdl(k_ln_bwd_rows4<T, 7>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+        else launch_pdl(k_ln_bwd_rows4<T, 8>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
     } else if (D <= 256) k_ln_bwd_rows<T, 8><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
     else if (D <= 512) k_ln_bwd_rows<T, 16><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
     else if (D <= 768) k_ln_bwd_rows<T, 24><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
@@ -973,7 +979,7 @@ void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int 
     if constexpr (std::is_same_v<Tin, bf16> && std::is_same_v<Tout, bf16>) {
         if (V % 8 == 0 && ldz % 8 == 0 && lddz % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
             (reinterpret_cast<uintptr_t>(dz) & 15) == 0) {
-            k_softmax_bwd_v8<<<dim3(cx, S), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
+            launch_pdl(k_softmax_bwd_v8, dim3(cx, S), dim3(256), 0, st, z, ldz, dz, lddz, S, V, lse, u, labels);
             PARL_LAUNCHED();
             return;
         }

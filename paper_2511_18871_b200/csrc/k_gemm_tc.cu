@@ -377,6 +377,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
+    pdl_wait();  // operands come from the previous kernel
+    pdl_trigger();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
@@ -505,6 +507,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tc::cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer (both CTAs, completing on the leader's barrier)
@@ -639,6 +643,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tc::cluster_sync();
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
@@ -838,7 +844,7 @@ void launch(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
         attr = true;
     }
-    k<<<grid, NTHREADS, Cfg<BN>::SMEM, st>>>(m.a, m.b, m.o, m.o2, m.i, a);
+    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg<BN>::SMEM, st, m.a, m.b, m.o, m.o2, m.i, a);
     PARL_LAUNCHED();
 }
 
@@ -850,7 +856,7 @@ void launch2(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
         attr = true;
     }
-    k<<<grid, NTHREADS, Cfg2::SMEM, st>>>(m.a, m.b, m.o, m.o2, m.i, a);
+    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg2::SMEM, st, m.a, m.b, m.o, m.o2, m.i, a);
     PARL_LAUNCHED();
 }
 
@@ -898,7 +904,7 @@ bool gemm_tc_group_dw(const GemmArgs* gs, int n, cudaStream_t st) {
         attr = true;
     }
     const int grid = 2 * std::min(tiles, num_sms() / 2);
-    k_gemm_group2<<<grid, NTHREADS, Cfg2::SMEM, st>>>(maps, ga);
+    launch_pdl(k_gemm_group2, dim3(grid), dim3(NTHREADS), Cfg2::SMEM, st, maps, ga);
     PARL_LAUNCHED();
     return true;
 }
