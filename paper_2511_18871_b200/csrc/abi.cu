@@ -99,9 +99,13 @@ struct parl_ctx_s {
     parl_precision prec = PARL_PREC_FP32;
     cudaStream_t st = nullptr;
     std::string err;
-    // forward/backward workspaces
-    DevBuf x0, x1, xmid, a, qkv, ctxo, bn, pre, actv, mean1, rstd1, mean2, rstd2, lse_attn;
-    DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head, part, target;
+    // forward workspaces of cache-less forwards, one set per role slot (models of a
+    // layer-interleaved tri-model forward are live at the same time)
+    struct FwdScratch {
+        DevBuf x, xmid, a, qkv, ctxo, bn, actv, stats, lse_attn, hf, lnf_mean, lnf_rstd, lse_head, logits;
+    } scr[3];
+    DevBuf part, target;
+    // backward workspaces
     DevBuf dx, dx2, dx_act, dpre, dbn, dmid, dmid_act, dctx, dqkv, da, dsum, dhf, dxg, dz;
     DevBuf stats, per_sample, staging, flags;
     // kernel-class profiler (parl_ctx_profile)
@@ -376,10 +380,35 @@ void ensure_attn_work(parl_group_s* g, int H);
 
 // ---------------------------------------------------------------------------
 // forward (forward_logprobs, model.cpp:534-567; run_forward 430-521)
+//
+// Several models over the same packed group (trimodel_forward, pipeline.cpp:22-30)
+// run layer-interleaved: the three models' copies of each layer GEMM go out as one
+// grouped launch (3x the tiles: full waves, one prologue), with per-model kernels
+// for LayerNorm, attention and the head.  Every model runs the same kernels, so
+// identical weights still give bit-identical outputs (test_pipeline.cpp:126-127).
+// Model 0 may keep its activations (`act`, the policy); the others use per-slot
+// scratch that holds one layer at a time.
 template <class T>
-void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, parl_act_s* act) {
+void gemm_multi(parl_ctx_s* c, const GemmArgs* gs, int n) {
+    double fl = 0;
+    for (int q = 0; q < n; ++q) fl += 2.0 * gs[q].M * (double)gs[q].N * gs[q].K;
+    ProfScope ps(c, PARL_KC_GEMM, fl);
+    if constexpr (std::is_same_v<T, bf16>) {
+        if (gemm_tc_multi(gs, n, c->st)) return;
+    }
+    for (int q = 0; q < n; ++q) {
+        if constexpr (std::is_same_v<T, bf16>) {
+            if (gemm_tc(gs[q], c->st)) continue;
+        }
+        gemm_simt<T>(gs[q], c->st);
+    }
+}
+
+template <class T>
+void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int nm, parl_group_s* g,
+                  parl_act_s* act, bool full_logits = false) {
     cudaStream_t st = c->st;
-    const auto& cf = m->cfg;
+    const auto& cf = ms[0]->cfg;
     const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
     const int NL = cf.n_layers;
     const size_t TD = (size_t)Tn * D;
@@ -389,35 +418,44 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
     const size_t TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
 
-    float* xs;   // residual stream stack: layer inputs x_0..x_L
-    float* xmid; // per-layer x_mid
-    T *a, *qkv, *ctxo, *bn, *pre, *actv;
-    float *stats, *lse_attn;
-    if (act) {
-        xs = act->xs.as<float>(TD * (NL + 1));
-        xmid = act->xmid.as<float>(TD * NL);
-        a = act->a.as<T>(TDp * NL);
-        qkv = act->qkv.as<T>(3 * TD * NL);
-        ctxo = act->ctxo.as<T>(TDp * NL);
-        bn = act->bn.as<T>(TDp * NL);
-        pre = act->pre.as<T>(TFp * NL);
-        actv = act->actv.as<T>(TFp * NL);
-        stats = act->stats.as<float>((size_t)4 * Tn * NL);
-        lse_attn = act->lse_attn.as<float>((size_t)H * Tn * NL);
-    } else {
-        xs = c->x0.as<float>(TD * 2);
-        xmid = c->xmid.as<float>(TD);
-        a = c->a.as<T>(TDp);
-        qkv = c->qkv.as<T>(3 * TD);
-        ctxo = c->ctxo.as<T>(TDp);
-        bn = c->bn.as<T>(TDp);
-        pre = c->pre.as<T>(TFp);
-        actv = c->actv.as<T>(TFp);
-        stats = c->mean1.as<float>((size_t)4 * Tn);
-        lse_attn = c->lse_attn.as<float>((size_t)H * Tn);
+    struct Bufs {
+        bool keep;     // per-layer stacks kept for the backward
+        float* xs;     // residual stream: layer inputs x_0..x_L (stack) or ping-pong
+        float* xmid;   // per-layer x_mid
+        T *a, *qkv, *ctxo, *bn, *pre, *actv;
+        float *stats, *lse_attn;
+        size_t lay(size_t per, int l) const { return keep ? per * (size_t)l : 0; }
+    };
+    Bufs B[3];
+    for (int k = 0; k < nm; ++k) {
+        Bufs& b = B[k];
+        b.keep = k == 0 && act;
+        if (b.keep) {
+            b.xs = act->xs.as<float>(TD * (NL + 1));
+            b.xmid = act->xmid.as<float>(TD * NL);
+            b.a = act->a.as<T>(TDp * NL);
+            b.qkv = act->qkv.as<T>(3 * TD * NL);
+            b.ctxo = act->ctxo.as<T>(TDp * NL);
+            b.bn = act->bn.as<T>(TDp * NL);
+            b.pre = act->pre.as<T>(TFp * NL);
+            b.actv = act->actv.as<T>(TFp * NL);
+            b.stats = act->stats.as<float>((size_t)4 * Tn * NL);
+            b.lse_attn = act->lse_attn.as<float>((size_t)H * Tn * NL);
+        } else {
+            auto& r = c->scr[slots[k]];
+            b.xs = r.x.as<float>(TD * 2);
+            b.xmid = r.xmid.as<float>(TD);
+            b.a = r.a.as<T>(TDp);
+            b.qkv = r.qkv.as<T>(3 * TD);
+            b.ctxo = r.ctxo.as<T>(TDp);
+            b.bn = r.bn.as<T>(TDp);
+            b.pre = nullptr;
+            b.actv = r.actv.as<T>(TFp);
+            b.stats = r.stats.as<float>((size_t)4 * Tn);
+            b.lse_attn = r.lse_attn.as<float>((size_t)H * Tn);
+        }
     }
-    auto lay = [&](size_t per, int l) { return act ? per * (size_t)l : 0; };
-    auto xin_of = [&](int l) { return xs + (act ? TD * l : TD * (l & 1)); };
+    auto xin_of = [&](const Bufs& b, int l) { return b.xs + (b.keep ? TD * l : TD * (l & 1)); };
 
     if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
     AttnArgs aa;
@@ -431,111 +469,133 @@ void forward_impl(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, par
     aa.ldo = Dp;
 
     {
-        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12);
-        launch_embed(m->W.tok_emb, m->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(0), st);
+        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12 * nm);
+        for (int k = 0; k < nm; ++k)
+            launch_embed(ms[k]->W.tok_emb, ms[k]->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(B[k], 0),
+                         st);
     }
+    GemmArgs gs[3];
     for (int l = 0; l < NL; ++l) {
-        const LayerW& w = m->layers[l];
-        float* xin = xin_of(l);
-        float* xout = xin_of(l + 1);
-        float* xm = xmid + lay(TD, l);
-        T* al = a + lay(TDp, l);
-        T* ql = qkv + lay(3 * TD, l);
-        T* cl = ctxo + lay(TDp, l);
-        T* bl = bn + lay(TDp, l);
-        T* pl = pre + lay(TFp, l);
-        T* vl = actv + lay(TFp, l);
-        float* st4 = stats + lay((size_t)4 * Tn, l);
-        float* la = lse_attn + lay((size_t)H * Tn, l);
-
         {
-            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
-            launch_layernorm<T>(xin, nullptr, Tn, D, w.ln1_g, w.ln1_b, al, Dp, st4, st4 + Tn, st);
+            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+            for (int k = 0; k < nm; ++k) {
+                const Bufs& b = B[k];
+                float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
+                launch_layernorm<T>(xin_of(b, l), nullptr, Tn, D, ms[k]->layers[l].ln1_g, ms[k]->layers[l].ln1_b,
+                                    b.a + b.lay(TDp, l), Dp, st4, st4 + Tn, st);
+            }
         }
-        {  // fused Q|K|V projection (model.cpp:464-466)
-            GemmArgs ga = mk(Tn, 3 * D, D, al, Dp, 1, w.wqkv_t, D, 1);
-            ga.epi = EPI_ACT; ga.bias = w.bqkv; ga.Ca = ql; ga.ldca = 3 * D;
-            gemm<T>(c, ga);
+        for (int k = 0; k < nm; ++k) {  // fused Q|K|V projection (model.cpp:464-466)
+            const Bufs& b = B[k];
+            const LayerW& w = ms[k]->layers[l];
+            gs[k] = mk(Tn, 3 * D, D, b.a + b.lay(TDp, l), Dp, 1, w.wqkv_t, D, 1);
+            gs[k].epi = EPI_ACT; gs[k].bias = w.bqkv; gs[k].Ca = b.qkv + b.lay(3 * TD, l); gs[k].ldca = 3 * D;
         }
+        gemm_multi<T>(c, gs, nm);
         {
-            ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D);
-            bool done = false;
-            if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
-            if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
+            ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D * nm);
+            for (int k = 0; k < nm; ++k) {
+                const Bufs& b = B[k];
+                T* ql = b.qkv + b.lay(3 * TD, l);
+                T* cl = b.ctxo + b.lay(TDp, l);
+                float* la = b.lse_attn + b.lay((size_t)H * Tn, l);
+                bool done = false;
+                if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
+                if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
+            }
         }
-        {  // O projection + residual (model.cpp:504-506)
-            GemmArgs ga = mk(Tn, D, D, cl, Dp, 1, w.wo_t, D, 1);
-            ga.epi = EPI_RESID; ga.bias = w.bo; ga.resid = xin; ga.Cf = xm; ga.ldc = D;
-            gemm<T>(c, ga);
+        for (int k = 0; k < nm; ++k) {  // O projection + residual (model.cpp:504-506)
+            const Bufs& b = B[k];
+            const LayerW& w = ms[k]->layers[l];
+            gs[k] = mk(Tn, D, D, b.ctxo + b.lay(TDp, l), Dp, 1, w.wo_t, D, 1);
+            gs[k].epi = EPI_RESID; gs[k].bias = w.bo; gs[k].resid = xin_of(b, l);
+            gs[k].Cf = b.xmid + b.lay(TD, l); gs[k].ldc = D;
         }
+        gemm_multi<T>(c, gs, nm);
         {
-            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)));
-            launch_layernorm<T>(xm, nullptr, Tn, D, w.ln2_g, w.ln2_b, bl, Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
+            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+            for (int k = 0; k < nm; ++k) {
+                const Bufs& b = B[k];
+                float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
+                launch_layernorm<T>(b.xmid + b.lay(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln2_g,
+                                    ms[k]->layers[l].ln2_b, b.bn + b.lay(TDp, l), Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
+            }
         }
-        {  // W1 + bias + GELU (model.cpp:509-511)
-            GemmArgs ga = mk(Tn, F, D, bl, Dp, 1, w.w1_t, D, 1);
-            ga.bias = w.b1; ga.ldca = Fp;
-            if (act) {  // the backward needs the pre-activation u (GELU') and the activation
-                ga.epi = EPI_GELU; ga.Ca = pl; ga.Caux = vl;
+        for (int k = 0; k < nm; ++k) {  // W1 + bias + GELU (model.cpp:509-511)
+            const Bufs& b = B[k];
+            const LayerW& w = ms[k]->layers[l];
+            gs[k] = mk(Tn, F, D, b.bn + b.lay(TDp, l), Dp, 1, w.w1_t, D, 1);
+            gs[k].bias = w.b1; gs[k].ldca = Fp;
+            if (b.keep) {  // the backward needs the pre-activation u (GELU') and the activation
+                gs[k].epi = EPI_GELU; gs[k].Ca = b.pre + b.lay(TFp, l); gs[k].Caux = b.actv + b.lay(TFp, l);
             } else {
-                ga.epi = EPI_GELU_ACT; ga.Ca = vl;
+                gs[k].epi = EPI_GELU_ACT; gs[k].Ca = b.actv;
             }
-            gemm<T>(c, ga);
         }
-        {  // W2 + bias + residual (model.cpp:513-515)
-            GemmArgs ga = mk(Tn, D, F, vl, Fp, 1, w.w2_t, F, 1);
-            ga.epi = EPI_RESID; ga.bias = w.b2; ga.resid = xm; ga.Cf = xout; ga.ldc = D;
-            gemm<T>(c, ga);
+        gemm_multi<T>(c, gs, nm);
+        for (int k = 0; k < nm; ++k) {  // W2 + bias + residual (model.cpp:513-515)
+            const Bufs& b = B[k];
+            const LayerW& w = ms[k]->layers[l];
+            gs[k] = mk(Tn, D, F, b.actv + b.lay(TFp, l), Fp, 1, w.w2_t, F, 1);
+            gs[k].epi = EPI_RESID; gs[k].bias = w.b2; gs[k].resid = b.xmid + b.lay(TD, l);
+            gs[k].Cf = xin_of(b, l + 1); gs[k].ldc = D;
         }
+        gemm_multi<T>(c, gs, nm);
     }
-    float* xfin = xin_of(NL);
     // final LN + head only on the scored tokens' predecessor rows (model.cpp:518-556)
-    T* hf = act ? act->hf.as<T>((size_t)S * Dp) : c->hf.as<T>((size_t)S * Dp);
-    if (act) {  // bias columns of the weight-gradient operands (refilled when the buffers move)
-        const uintptr_t sig[7] = {(uintptr_t)a, (uintptr_t)ctxo, (uintptr_t)bn, (uintptr_t)actv, (uintptr_t)hf,
-                                  (uintptr_t)Tn, (uintptr_t)S};
-        if (std::memcmp(sig, act->pad_sig, sizeof(sig)) != 0) {
-            launch_fill_pad<T>(a, (long)Tn * NL, D, Dp, st);
-            launch_fill_pad<T>(ctxo, (long)Tn * NL, D, Dp, st);
-            launch_fill_pad<T>(bn, (long)Tn * NL, D, Dp, st);
-            launch_fill_pad<T>(actv, (long)Tn * NL, F, Fp, st);
-            launch_fill_pad<T>(hf, (long)S, D, Dp, st);
-            std::memcpy(act->pad_sig, sig, sizeof(sig));
-        }
-    }
-    float* lnf_mean = act ? act->lnf_mean.as<float>(S) : c->lnf_mean.as<float>(S);
-    float* lnf_rstd = act ? act->lnf_rstd.as<float>(S) : c->lnf_rstd.as<float>(S);
-    float* lse_head = act ? act->lse_head.as<float>(S) : c->lse_head.as<float>(S);
-    float* lp = static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T;
-    if (S > 0) {
-        launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, Dp, lnf_mean, lnf_rstd, st);
-        bool fused = false;
-        if constexpr (std::is_same_v<T, bf16>) {
-            // tcgen05 head with the vocab log-sum-exp and target gather fused
-            // into the epilogue: logits reach HBM only for the policy (bf16,
-            // kept for the backward), never for old/ref.
-            const int n_parts = (V + 127) / 128;
-            GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
-            ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
-            ga.part = c->part.as<float>((size_t)S * n_parts * 2);
-            ga.target = c->target.as<float>(S);
-            ga.n_parts = n_parts; ga.part_cols = 128;
-            ga.logits_act = act ? act->logits.as<bf16>((size_t)S * V) : nullptr;
-            ga.ldca = V;
-            {
-                ProfScope ps(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
-                fused = gemm_tc(ga, st);
-                if (fused) launch_lse_combine(ga.part, n_parts, ga.target, S, lse_head, lp, st);
+    for (int k = 0; k < nm; ++k) {
+        const Bufs& b = B[k];
+        parl_model_s* m = ms[k];
+        parl_act_s* ak = b.keep ? act : nullptr;
+        auto& r = c->scr[slots[k]];
+        float* xfin = xin_of(b, NL);
+        T* hf = ak ? ak->hf.as<T>((size_t)S * Dp) : r.hf.as<T>((size_t)S * Dp);
+        if (ak) {  // bias columns of the weight-gradient operands (refilled when the buffers move)
+            const uintptr_t sig[7] = {(uintptr_t)b.a, (uintptr_t)b.ctxo, (uintptr_t)b.bn, (uintptr_t)b.actv,
+                                      (uintptr_t)hf, (uintptr_t)Tn, (uintptr_t)S};
+            if (std::memcmp(sig, ak->pad_sig, sizeof(sig)) != 0) {
+                launch_fill_pad<T>(b.a, (long)Tn * NL, D, Dp, st);
+                launch_fill_pad<T>(b.ctxo, (long)Tn * NL, D, Dp, st);
+                launch_fill_pad<T>(b.bn, (long)Tn * NL, D, Dp, st);
+                launch_fill_pad<T>(b.actv, (long)Tn * NL, F, Fp, st);
+                launch_fill_pad<T>(hf, (long)S, D, Dp, st);
+                std::memcpy(ak->pad_sig, sig, sizeof(sig));
             }
         }
-        if (!fused) {
-            float* logits = act ? act->logits.as<float>((size_t)S * V) : c->logits.as<float>((size_t)S * V);
-            GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
-            ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
-            gemm_simt<T>(ga, st);
-            launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
+        float* lnf_mean = ak ? ak->lnf_mean.as<float>(S) : r.lnf_mean.as<float>(S);
+        float* lnf_rstd = ak ? ak->lnf_rstd.as<float>(S) : r.lnf_rstd.as<float>(S);
+        float* lse_head = ak ? ak->lse_head.as<float>(S) : r.lse_head.as<float>(S);
+        float* lp = static_cast<float*>(g->lp.p) + (size_t)slots[k] * g->max_T;
+        if (S > 0) {
+            launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, Dp, lnf_mean, lnf_rstd, st);
+            bool fused = false;
+            if (std::is_same_v<T, bf16> && !full_logits) {
+                // tcgen05 head with the vocab log-sum-exp and target gather fused
+                // into the epilogue: logits reach HBM only for the policy (bf16,
+                // kept for the backward), never for old/ref.
+                const int n_parts = (V + 127) / 128;
+                GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
+                ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
+                ga.part = c->part.as<float>((size_t)S * n_parts * 2);
+                ga.target = c->target.as<float>(S);
+                ga.n_parts = n_parts; ga.part_cols = 128;
+                ga.logits_act = ak ? ak->logits.as<bf16>((size_t)S * V) : nullptr;
+                ga.ldca = V;
+                {
+                    ProfScope ps(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
+                    fused = gemm_tc(ga, st);
+                    if (fused) launch_lse_combine(ga.part, n_parts, ga.target, S, lse_head, lp, st);
+                }
+            }
+            if (!fused) {
+                float* logits = ak ? ak->logits.as<float>((size_t)S * V) : r.logits.as<float>((size_t)S * V);
+                GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
+                ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
+                gemm_simt<T>(ga, st);
+                launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
+            }
+            if (ak) ak->logits_bf16 = fused;
         }
-        if (act) act->logits_bf16 = fused;
     }
     check_launch();
 }
@@ -1360,28 +1420,40 @@ parl_status parl_group_download(parl_group_t g, int32_t* tokens, int32_t* labels
 }
 
 // ---- forward ------------------------------------------------------------------
-static void do_forward(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, parl_act_t* act_out) {
-    PARL_REQUIRE(slot >= 0 && slot < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
+// forwards of nm models over one group (model k -> log-prob slot slots[k]); the
+// first model's activations go to *act_out when given
+static void do_forward_n(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int nm, parl_group_s* g,
+                         parl_act_t* act_out) {
     PARL_REQUIRE(g->T > 0, PARL_E_SHAPE, "group is empty (pack or set a sequence first)");
-    PARL_REQUIRE(g->T <= m->cfg.max_seq_len, PARL_E_SHAPE, "sequence length exceeds max_seq_len");
-    g->vocab = m->cfg.vocab_size;
+    for (int k = 0; k < nm; ++k) {
+        PARL_REQUIRE(slots[k] >= 0 && slots[k] < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
+        PARL_REQUIRE(g->T <= ms[k]->cfg.max_seq_len, PARL_E_SHAPE, "sequence length exceeds max_seq_len");
+        PARL_REQUIRE(same_cfg(ms[k]->cfg, ms[0]->cfg), PARL_E_CONFIG, "models of one forward must share a config");
+    }
+    g->vocab = ms[0]->cfg.vocab_size;
     parl_act_s* act = nullptr;
     if (act_out) {
         act = *act_out ? *act_out : new parl_act_s();
         *act_out = act;
     }
-    if (c->prec == PARL_PREC_BF16) forward_impl<bf16>(c, m, g, slot, act);
-    else forward_impl<float>(c, m, g, slot, act);
-    const uint64_t gen = ++m->forward_gen;  // bump_forward_generation, model.cpp:559
-    if (act) {
-        act->owner = m;
-        act->group = g;
-        act->version = m->version;
-        act->gen = gen;
-        act->epoch = g->epoch;
-        act->T = g->T;
-        act->S = g->S;
+    if (c->prec == PARL_PREC_BF16) forward_impl<bf16>(c, ms, slots, nm, g, act);
+    else forward_impl<float>(c, ms, slots, nm, g, act);
+    for (int k = 0; k < nm; ++k) {
+        const uint64_t gen = ++ms[k]->forward_gen;  // bump_forward_generation, model.cpp:559
+        if (k == 0 && act) {
+            act->owner = ms[0];
+            act->group = g;
+            act->version = ms[0]->version;
+            act->gen = gen;
+            act->epoch = g->epoch;
+            act->T = g->T;
+            act->S = g->S;
+        }
     }
+}
+
+static void do_forward(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, int slot, parl_act_t* act_out) {
+    do_forward_n(c, &m, &slot, 1, g, act_out);
 }
 
 parl_status parl_forward(parl_ctx_t ctx, parl_model_t m, parl_group_t g, int slot, parl_act_t* act_out) {
@@ -1391,9 +1463,9 @@ parl_status parl_forward(parl_ctx_t ctx, parl_model_t m, parl_group_t g, int slo
 parl_status parl_trimodel_forward(parl_ctx_t ctx, parl_model_t pol, parl_model_t old, parl_model_t ref,
                                   parl_group_t g, parl_act_t* act_out) {
     return guarded(ctx, [&] {
-        do_forward(ctx, pol, g, 0, act_out);
-        if (old) do_forward(ctx, old, g, 1, nullptr);
-        do_forward(ctx, ref, g, 2, nullptr);
+        parl_model_s* ms[3] = {pol, old ? old : ref, ref};
+        int slots[3] = {0, old ? 1 : 2, 2};
+        do_forward_n(ctx, ms, slots, old ? 3 : 2, g, act_out);
     });
 }
 
@@ -1457,12 +1529,14 @@ parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, do
         up(tmp.pk.row_ptr, rp.data(), T + 1);
         up(tmp.pk.row_idx, ri.data(), T);
         upload_meta(&tmp);
-        if (ctx->prec == PARL_PREC_BF16) forward_impl<bf16>(ctx, m, &tmp, 0, nullptr);
-        else forward_impl<float>(ctx, m, &tmp, 0, nullptr);
+        int slot0 = 0;
+        // every row's full distribution: the unfused head (fp32 logits + row log-sum-exp)
+        if (ctx->prec == PARL_PREC_BF16) forward_impl<bf16>(ctx, &m, &slot0, 1, &tmp, nullptr, true);
+        else forward_impl<float>(ctx, &m, &slot0, 1, &tmp, nullptr, true);
         ++m->forward_gen;
         std::vector<float> z((size_t)T * V), lse(T);
-        PARL_CUDA(cudaMemcpyAsync(z.data(), ctx->logits.p, z.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
-        PARL_CUDA(cudaMemcpyAsync(lse.data(), ctx->lse_head.p, T * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaMemcpyAsync(z.data(), ctx->scr[0].logits.p, z.size() * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaMemcpyAsync(lse.data(), ctx->scr[0].lse_head.p, T * 4, cudaMemcpyDeviceToHost, ctx->st));
         PARL_CUDA(cudaStreamSynchronize(ctx->st));
         for (int t = 0; t < T; ++t)
             for (int v = 0; v < V; ++v) rows[(size_t)t * V + v] = (double)z[(size_t)t * V + v] - (double)lse[t];
@@ -1862,4 +1936,12 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
         PARL_CUDA(cudaGetLastError());
         if (path != 2) PARL_CUDA(cudaDeviceSynchronize());
     });
+}
+
+namespace parl_gpu {
+bool attn_trace_read(unsigned long long* out);
+}
+// phase timestamps of the attention forward's CTA 0 (builds with -DPARL_ATTN_TRACE only)
+extern "C" parl_status parl_debug_attn_trace(unsigned long long* out) {
+    return parl_gpu::attn_trace_read(out) ? PARL_OK : PARL_E_CONFIG;
 }

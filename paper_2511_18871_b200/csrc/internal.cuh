@@ -154,6 +154,8 @@ template <class T>
 void gemm_simt(const GemmArgs& g, cudaStream_t st);
 // tcgen05 path (bf16 only).  Returns false if the shape/layout is not supported.
 bool gemm_tc(const GemmArgs& g, cudaStream_t st);
+// n equal-shape GEMMs; one grouped CTA-pair launch when n is 2 or 3 and they qualify
+bool gemm_tc_multi(const GemmArgs* gs, int n, cudaStream_t st);
 // all weight-gradient GEMMs of a layer in one launch (MN-major A and B, shared K, fp32 accumulate)
 bool gemm_tc_group_dw(const GemmArgs* gs, int n, cudaStream_t st);
 

@@ -17,6 +17,8 @@
 // only the row log-sum-exp.
 #include <cudaTypedefs.h>
 
+#include <cuda_fp16.h>
+
 #include "internal.cuh"
 #include "kernels.cuh"
 #include "tc_util.cuh"
@@ -352,6 +354,19 @@ struct PairSmem {
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 
+#ifdef PARL_ATTN_TRACE
+// phase timestamps of CTA 0 (build with -DPARL_ATTN_TRACE; read by parl_debug_attn_trace)
+__device__ unsigned long long g_attn_trace[4][64][8];
+#define ATTN_TRACE(role, n, k)                                                                  \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (n) < 64) g_attn_trace[role][n][k] = clock64(); \
+    } while (0)
+#else
+#define ATTN_TRACE(role, n, k) \
+    do {                       \
+    } while (0)
+#endif
+
 template <int DH>
 __global__ void __launch_bounds__(PAIR_NTHR, 1)
     k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, AttnPairArgs a) {
@@ -478,6 +493,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                                  ks > 0);
                 }
                 tc::mma_commit(&s_full[w]);
+                ATTN_TRACE(2 + w, cS, 0);
                 ++cS;
                 return;
             }
@@ -497,9 +513,11 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     continue;
                 }
                 issue_next_s();  // S of the next visible key tile (possibly in the next item)
+                ATTN_TRACE(2 + w, cP, 1);
                 tc::mbar_wait(&p_full[w], cP & 1);
                 if (!started && nI > 0) tc::mbar_wait(&o_free[w], (nI - 1) & 1);
                 tc::tc_fence_after();
+                ATTN_TRACE(2 + w, cP, 2);
                 const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
@@ -544,13 +562,16 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e) {
                 const uint32_t f = (uint32_t)a.p_list[e];
                 if (!(f & VIS)) continue;
+                if (q4 == 0) ATTN_TRACE(w, cS, 0);
                 tc::mbar_wait(&s_full[w], cS & 1);
                 tc::tc_fence_after();
+                if (q4 == 0) ATTN_TRACE(w, cS, 1);
                 float sv[128];
                 tc::tmem_ld128(t_s + w * 128 + lane_off, sv);
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&s_free[w]);  // the next S of this tile may be issued
+                if (q4 == 0) ATTN_TRACE(w, cS, 2);
                 if (!(f & FULL)) {
                     const int j0 = (int)(f & 0xffffff) * 128;
                     const int h0 = min(max(e0 - j0, 0), 128);
@@ -588,11 +609,13 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     pk[j / 2] = pack2(p0, p1);
                     pk[j / 2 + 1] = pack2(p2, p3);
                 }
+                if (q4 == 0) ATTN_TRACE(w, cS, 3);
                 // the previous PV of this tile has finished reading P and writing O
                 if (cS > 0) {
                     tc::mbar_wait(&o_done[w], (cS - 1) & 1);
                     tc::tc_fence_after();
                 }
+                if (q4 == 0) ATTN_TRACE(w, cS, 4);
                 if (!first && __any_sync(0xffffffffu, need)) {
 #pragma unroll
                     for (int c = 0; c < DH / 32; ++c) {
@@ -611,6 +634,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&p_full[w]);
+                if (q4 == 0) ATTN_TRACE(w, cS, 5);
                 l = l * alpha + ((sm0 + sm1) + (sm2 + sm3));
                 m_used = m_new;
                 first = false;
@@ -1732,5 +1756,13 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     else launch_fwd<128>(m, a, st);
     return true;
 }
+
+#ifdef PARL_ATTN_TRACE
+bool attn_trace_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess;
+}
+#else
+bool attn_trace_read(unsigned long long*) { return false; }
+#endif
 
 }  // namespace parl_gpu

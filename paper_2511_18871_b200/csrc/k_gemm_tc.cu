@@ -98,6 +98,7 @@ struct EpiSeq {
     int first, stride, n_items, tiles_me;  // items first, first+stride, ...; m-tiles per n column
     int mrows;                             // rows per m-tile (128, or 256 for a CTA pair)
     int rank;                              // CTA rank within the pair
+    int tpp;                               // items per problem (grouped launches of equal-shape problems)
 };
 
 // Epilogue warps (4..11).  Thread = accumulator row (TMEM lane); warp w owns
@@ -108,8 +109,11 @@ struct EpiSeq {
 // Inputs of the epilogue (fp32 residual, bf16 GELU pre-activation) arrive by
 // TMA into the same staging buffer two chunks ahead.  Three staging buffers per
 // warp let the stores of chunks k-1, k-2 drain while chunk k is computed.
+// Grouped launches (NP > 1 equal-shape problems, e.g. the three models' copies
+// of one layer GEMM): item = problem * tpp + tile; av / mo / mo2 / mi are per
+// problem.  The epilogue class (input, number of outputs) is the same for all.
 template <int BNT, class Release>
-__device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMap* mo, const CUtensorMap* mo2,
+__device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorMap* mo, const CUtensorMap* mo2,
                                                const CUtensorMap* mi, uint8_t* stg_all, uint64_t* inbar_all,
                                                uint64_t* tfull, uint32_t tbase, const EpiSeq& e, Release release) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,15 +122,16 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
     uint8_t* stg = stg_all + wi * NBUF * STG_BYTES;
     const uint32_t stg_s = tc::smem_u32(stg);
     uint64_t* inbar = inbar_all + wi * NBUF;
-    const int epi = a.epi;
-    const bool has_in = epi == EPI_RESID || epi == EPI_GELU_BWD;
-    const uint32_t in_bytes = epi == EPI_RESID ? 4096u : 2048u;
-    const bool do_store = epi != EPI_LSE || a.store_logits;
+    const TcArgs& a0 = av[0];
+    const bool has_in = a0.epi == EPI_RESID || a0.epi == EPI_GELU_BWD;
+    const uint32_t in_bytes = a0.epi == EPI_RESID ? 4096u : 2048u;
+    const bool do_store = a0.epi != EPI_LSE || a0.store_logits;
 
     auto coords = [&](int item, int& row, int& col, int& sp) {
-        const int mt = item % e.tiles_me, rest = item / e.tiles_me;
-        const int nt = rest % a.tiles_n;
-        sp = rest / a.tiles_n;
+        const int t = item % e.tpp;
+        const int mt = t % e.tiles_me, rest = t / e.tiles_me;
+        const int nt = rest % a0.tiles_n;
+        sp = rest / a0.tiles_n;
         row = mt * e.mrows + e.rank * BM + ew * 32;
         col = nt * BNT + half * HALF;
     };
@@ -141,12 +146,14 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
         int row, col, sp;
         coords(item, row, col, sp);
         tc::mbar_expect_tx(&inbar[b], in_bytes);
-        tc::tma_load_2d(stg + b * STG_BYTES, mi, &inbar[b], col + c * 32, row);
+        tc::tma_load_2d(stg + b * STG_BYTES, mi + item / e.tpp, &inbar[b], col + c * 32, row);
     };
     // bias of a chunk, loaded one chunk ahead (broadcast loads: every lane reads the same columns)
     float bn[32];
     auto load_bias = [&](int item, int c) {
-        if (!a.bias || item >= e.n_items) return;
+        if (item >= e.n_items) return;
+        const TcArgs& a = av[item / e.tpp];
+        if (!a.bias) return;
         int row, col, sp;
         coords(item, row, col, sp);
         col += c * 32;
@@ -175,6 +182,9 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
     load_bias(e.first, 0);
     for (int item = e.first; item < e.n_items; item += e.stride, ++local) {
         const uint32_t acc = local & 1, use = local >> 1;
+        const int prob = item / e.tpp;
+        const TcArgs& a = av[prob];
+        const int epi = a.epi;
         tc::mbar_wait(&tfull[acc], use & 1);
         tc::tc_fence_after();
         int row0, colh, sp;
@@ -314,11 +324,11 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs& a, const CUtensorMa
                 __syncwarp();
                 if (lane == 0) {
                     if (epi == EPI_F32_ACC) {
-                        if (a.splits > 1) tc::tma_store_3d(mo, sb, col, row0, sp);
-                        else tc::tma_reduce_add_2d(mo, sb, col, row0);
+                        if (a.splits > 1) tc::tma_store_3d(mo + prob, sb, col, row0, sp);
+                        else tc::tma_reduce_add_2d(mo + prob, sb, col, row0);
                     } else {
-                        tc::tma_store_2d(mo, sb, col, row0);
-                        if (epi == EPI_GELU) tc::tma_store_2d(mo2, sb + 2048, col, row0);
+                        tc::tma_store_2d(mo + prob, sb, col, row0);
+                        if (epi == EPI_GELU) tc::tma_store_2d(mo2 + prob, sb + 2048, col, row0);
                     }
                     tc::bulk_commit();
                     if (has_in && pf_item < e.n_items) {
@@ -438,8 +448,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::mma_commit(&tfull[acc]);
         }
     } else if (warp >= 4) {
-        const EpiSeq e{(int)blockIdx.x, (int)gridDim.x, n_items, a.tiles_m, BM, 0};
-        epilogue_warps<BN>(a, &tmO, &tmO2, &tmI, smem + C::STG_OFF, inbar, tfull, tbase, e,
+        const EpiSeq e{(int)blockIdx.x, (int)gridDim.x, n_items, a.tiles_m, BM, 0, n_items};
+        epilogue_warps<BN>(&a, &tmO, &tmO2, &tmI, smem + C::STG_OFF, inbar, tfull, tbase, e,
                            [&](uint32_t acc) { tc::mbar_arrive_relaxed(&tempty[acc]); });
     }
     __syncthreads();
@@ -466,11 +476,20 @@ struct Cfg2 {
     static constexpr int SMEM = BAR_OFF + 512 + 1024;
 };
 
-template <int A_MN, int B_MN>
+template <int NP>
+struct PairMaps {
+    CUtensorMap a[NP], b[NP], o[NP], o2[NP], i[NP];
+};
+template <int NP>
+struct PairArgs {
+    TcArgs a[NP];
+};
+
+// NP equal-shape problems per launch (item = problem * tiles-per-problem + tile)
+template <int A_MN, int B_MN, int NP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
-               const __grid_constant__ CUtensorMap tmI, TcArgs a) {
+    k_gemm_tc2(const __grid_constant__ PairMaps<NP> mp, const __grid_constant__ PairArgs<NP> pa) {
+    const TcArgs& a = pa.a[0];  // shape / K-split fields are common to the problems
     using C = Cfg2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -485,7 +504,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t rank = tc::cluster_ctarank();
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int tiles_m2 = (a.M + 2 * BM - 1) / (2 * BM);
-    const int n_items = tiles_m2 * a.tiles_n * a.splits;
+    const int tpp = tiles_m2 * a.tiles_n * a.splits;
+    const int n_items = tpp * NP;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -498,8 +518,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
         for (int s = 0; s < NBUF * EPI_WARPS; ++s) tc::mbar_init(&inbar[s], 1);
         tc::fence_barrier_init();
-        tc::tma_prefetch(&tmA);
-        tc::tma_prefetch(&tmB);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            tc::tma_prefetch(&mp.a[q]);
+            tc::tma_prefetch(&mp.b[q]);
+        }
     }
     if (warp == 2) tc::tmem_alloc_pair<2 * BN2>(tbase_s);
     tc::tc_fence_before();
@@ -514,7 +537,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // ---------------- TMA producer (both CTAs, completing on the leader's barrier)
         uint32_t cnt = 0;
         for (int item = cid; item < n_items; item += ncl) {
-            const int mt = item % tiles_m2, rest = item / tiles_m2;
+            const int prob = item / tpp, t = item % tpp;
+            const CUtensorMap* tA = &mp.a[prob];
+            const CUtensorMap* tB = &mp.b[prob];
+            const int mt = t % tiles_m2, rest = t / tiles_m2;
             const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
             const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
             const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * BN2 + (int)rank * (BN2 / 2);
@@ -527,16 +553,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 uint8_t* sa = smem + s * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
                 if (!A_MN) {
-                    tc::tma_load_2d_pair(sa, &tmA, fb, kb * BK, m0);
+                    tc::tma_load_2d_pair(sa, tA, fb, kb * BK, m0);
                 } else {
-                    tc::tma_load_2d_pair(sa, &tmA, fb, m0, kb * BK);
-                    tc::tma_load_2d_pair(sa + 8192, &tmA, fb, m0 + 64, kb * BK);
+                    tc::tma_load_2d_pair(sa, tA, fb, m0, kb * BK);
+                    tc::tma_load_2d_pair(sa + 8192, tA, fb, m0 + 64, kb * BK);
                 }
                 if (!B_MN) {
-                    tc::tma_load_2d_pair(sb, &tmB, fb, kb * BK, n0);
+                    tc::tma_load_2d_pair(sb, tB, fb, kb * BK, n0);
                 } else {
-                    tc::tma_load_2d_pair(sb, &tmB, fb, n0, kb * BK);
-                    tc::tma_load_2d_pair(sb + 8192, &tmB, fb, n0 + 64, kb * BK);
+                    tc::tma_load_2d_pair(sb, tB, fb, n0, kb * BK);
+                    tc::tma_load_2d_pair(sb + 8192, tB, fb, n0 + 64, kb * BK);
                 }
             }
         }
@@ -545,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, A_MN, B_MN);
         uint32_t cnt = 0, local = 0;
         for (int item = cid; item < n_items; item += ncl, ++local) {
-            const int rest = item / tiles_m2;
+            const int rest = (item % tpp) / tiles_m2;
             const int sp = rest / a.tiles_n;
             const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
             const uint32_t acc = local & 1, use = local >> 1;
@@ -571,9 +597,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs: this CTA's 128 rows x all 256 columns)
-        const EpiSeq e{cid, ncl, n_items, tiles_m2, 2 * BM, (int)rank};
+        const EpiSeq e{cid, ncl, n_items, tiles_m2, 2 * BM, (int)rank, tpp};
         const uint32_t leader_tempty0 = tc::mapa(&tempty[0], 0);
-        epilogue_warps<BN2>(a, &tmO, &tmO2, &tmI, smem + C::STG_OFF, inbar, tfull, tbase, e, [&](uint32_t acc) {
+        epilogue_warps<BN2>(pa.a, mp.o, mp.o2, mp.i, smem + C::STG_OFF, inbar, tfull, tbase, e, [&](uint32_t acc) {
             tc::mbar_arrive_cluster_relaxed(leader_tempty0 + acc * 8);
         });
     }
@@ -848,16 +874,21 @@ void launch(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
-template <int A_MN, int B_MN>
-void launch2(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
-    auto k = k_gemm_tc2<A_MN, B_MN>;
+template <int A_MN, int B_MN, int NP>
+void launch2(const Maps* m, const TcArgs* a, int grid, cudaStream_t st) {
+    auto k = k_gemm_tc2<A_MN, B_MN, NP>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
         attr = true;
     }
-    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg2::SMEM, st, m.a, m.b, m.o, m.o2, m.i, a);
-    PARL_LAUNCHED();
+    PairMaps<NP> pm;
+    PairArgs<NP> pa;
+    for (int q = 0; q < NP; ++q) {
+        pm.a[q] = m[q].a; pm.b[q] = m[q].b; pm.o[q] = m[q].o; pm.o2[q] = m[q].o2; pm.i[q] = m[q].i;
+        pa.a[q] = a[q];
+    }
+    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg2::SMEM, st, pm, pa);
 }
 
 // PARL_GEMM_PAIR=0 disables the CTA-pair kernel (diagnostics)
@@ -909,8 +940,18 @@ bool gemm_tc_group_dw(const GemmArgs* gs, int n, cudaStream_t st) {
     return true;
 }
 
-bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
-    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return true;
+namespace {
+// Launch plan of one GEMM: kernel variant, tiling, tensor maps, device args.
+struct Plan {
+    bool pair = false;
+    int BN = 256, variant = 0, items = 0;  // variant: 0 K/K, 1 K/MN, 2 MN/MN
+    Maps mp;
+    TcArgs a{};
+    float* ws = nullptr;
+};
+
+// false if the shape / layout is not supported by the tcgen05 kernels
+bool plan_gemm(const GemmArgs& g, Plan& P) {
     const bool a_k = g.sak == 1, a_mn = g.sam == 1 && !a_k;
     const bool b_k = g.sbk == 1, b_mn = g.sbn == 1 && !b_k;
     if (!(a_k || a_mn) || !(b_k || b_mn)) return false;
@@ -918,6 +959,7 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     if ((lda * 2) % 16 || (ldb * 2) % 16 || !aligned16(g.A) || !aligned16(g.B)) return false;
     if (a_mn && !b_mn) return false;  // combination not instantiated
     if (!encode_fn()) return false;
+    P.variant = a_k && b_k ? 0 : (a_k ? 1 : 2);
 
     // tile width: 128 when N is a multiple of 128 but not of 256, or N is small
     // (the LSE epilogue writes one (max, sumexp) partial per 128 columns: n_parts = ceil(N / 128))
@@ -927,7 +969,9 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     const bool pair = pair_enabled() && g.M > 128 && g.N >= 256 && (g.N % 128) == 0 &&
                       (long)((g.M + 255) / 256) * ((g.N + 255) / 256) >= sms / 4 && (a_k || b_mn);
     const int BN = pair ? 256 : (g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256));
-    Maps mp;
+    P.pair = pair;
+    P.BN = BN;
+    Maps& mp = P.mp;
     std::memset(&mp, 0, sizeof(mp));
     bool ok;
     if (a_k) ok = make_map(&mp.a, g.A, g.K, g.M, lda, BK, BM);
@@ -938,7 +982,8 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
     else ok = make_map(&mp.b, g.B, g.N, g.K, ldb, 64, BK);
     if (!ok) return false;
 
-    TcArgs a{};
+    TcArgs& a = P.a;
+    a = TcArgs{};
     a.M = g.M; a.N = g.N; a.K = g.K;
     a.nkb = (g.K + BK - 1) / BK;
     a.tiles_m = (g.M + BM - 1) / BM;
@@ -959,10 +1004,10 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
         a.kbs = (a.nkb + want - 1) / want;
         a.splits = (a.nkb + a.kbs - 1) / a.kbs;
     }
-    float* ws = nullptr;
+    P.ws = nullptr;
     if (a.splits > 1) {
-        ws = g_ws.get((size_t)a.splits * g.M * g.N * sizeof(float));
-        if (!ws) return false;
+        P.ws = g_ws.get((size_t)a.splits * g.M * g.N * sizeof(float));
+        if (!P.ws) return false;
     }
     // epilogue maps
     switch (g.epi) {
@@ -970,7 +1015,7 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
             ok = make_epi_map(&mp.o, g.Cf, true, g.N, g.M, g.ldc);
             break;
         case EPI_F32_ACC:
-            ok = a.splits > 1 ? make_epi_map(&mp.o, ws, true, g.N, g.M, g.N, a.splits)
+            ok = a.splits > 1 ? make_epi_map(&mp.o, P.ws, true, g.N, g.M, g.N, a.splits)
                               : make_epi_map(&mp.o, g.Cf, true, g.N, g.M, g.ldc);
             break;
         case EPI_RESID:
@@ -1001,29 +1046,83 @@ bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
             ok = false;
     }
     if (!ok) return false;
+    P.items = tiles * a.splits;
+    return true;
+}
 
-    const int items = tiles * a.splits;
-    if (pair) {
-        const int grid = 2 * std::min(items, sms / 2);
-        if (a_k && b_k) launch2<0, 0>(mp, a, grid, st);
-        else if (a_k && b_mn) launch2<0, 1>(mp, a, grid, st);
-        else launch2<1, 1>(mp, a, grid, st);
-    } else if (BN == 256) {
-        const int grid = std::min(items, sms);
-        if (a_k && b_k) launch<256, 0, 0>(mp, a, grid, st);
-        else if (a_k && b_mn) launch<256, 0, 1>(mp, a, grid, st);
-        else launch<256, 1, 1>(mp, a, grid, st);
+void run_plan(const Plan& P, const GemmArgs& g, cudaStream_t st) {
+    const int sms = num_sms();
+    const int v = P.variant;
+    if (P.pair) {
+        const int grid = 2 * std::min(P.items, sms / 2);
+        if (v == 0) launch2<0, 0, 1>(&P.mp, &P.a, grid, st);
+        else if (v == 1) launch2<0, 1, 1>(&P.mp, &P.a, grid, st);
+        else launch2<1, 1, 1>(&P.mp, &P.a, grid, st);
+    } else if (P.BN == 256) {
+        const int grid = std::min(P.items, sms);
+        if (v == 0) launch<256, 0, 0>(P.mp, P.a, grid, st);
+        else if (v == 1) launch<256, 0, 1>(P.mp, P.a, grid, st);
+        else launch<256, 1, 1>(P.mp, P.a, grid, st);
     } else {
-        const int grid = std::min(items, sms);
-        if (a_k && b_k) launch<128, 0, 0>(mp, a, grid, st);
-        else if (a_k && b_mn) launch<128, 0, 1>(mp, a, grid, st);
-        else launch<128, 1, 1>(mp, a, grid, st);
+        const int grid = std::min(P.items, sms);
+        if (v == 0) launch<128, 0, 0>(P.mp, P.a, grid, st);
+        else if (v == 1) launch<128, 0, 1>(P.mp, P.a, grid, st);
+        else launch<128, 1, 1>(P.mp, P.a, grid, st);
     }
-    if (a.splits > 1) {
+    if (P.a.splits > 1) {
         const long n = (long)g.M * g.N;
         const int blocks = (int)std::min<long>((n + 255) / 256, 148L * 8);
-        k_splitk_reduce<<<blocks, 256, 0, st>>>(ws, a.splits, g.M, g.N, g.Cf, g.ldc);
+        k_splitk_reduce<<<blocks, 256, 0, st>>>(P.ws, P.a.splits, g.M, g.N, g.Cf, g.ldc);
         PARL_LAUNCHED();
+    }
+}
+}  // namespace
+
+bool gemm_tc(const GemmArgs& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return true;
+    Plan P;
+    if (!plan_gemm(g, P)) return false;
+    run_plan(P, g, st);
+    return true;
+}
+
+// Equal-shape GEMMs (the three models' copies of one layer GEMM) in one CTA-pair
+// launch; falls back to one launch per problem when they cannot be grouped.
+bool gemm_tc_multi(const GemmArgs* gs, int n, cudaStream_t st) {
+    if (n <= 0) return true;
+    static Plan P[3];
+    bool group = (n == 2 || n == 3) && pair_enabled();
+    for (int q = 0; q < n; ++q) {
+        if (gs[q].M <= 0 || gs[q].N <= 0 || gs[q].K <= 0) return n == 1;
+        if (!plan_gemm(gs[q], P[q < 3 ? q : 0])) return false;
+        if (q >= 3) group = false;
+    }
+    if (group) {
+        for (int q = 0; q < n; ++q)
+            group = group && P[q].pair && P[q].a.splits == 1 && P[q].variant == P[0].variant &&
+                    P[q].a.M == P[0].a.M && P[q].a.N == P[0].a.N && P[q].a.K == P[0].a.K &&
+                    P[q].a.store_logits == P[0].a.store_logits && P[q].a.logits_direct == nullptr &&
+                    ((P[q].a.epi == EPI_RESID || P[q].a.epi == EPI_GELU_BWD) ==
+                     (P[0].a.epi == EPI_RESID || P[0].a.epi == EPI_GELU_BWD));
+    }
+    if (!group) {
+        for (int q = 0; q < n; ++q) {
+            if (q >= 3 && !plan_gemm(gs[q], P[0])) return false;
+            run_plan(P[q < 3 ? q : 0], gs[q], st);
+        }
+        return true;
+    }
+    Maps m3[3] = {P[0].mp, P[1].mp, P[2].mp};
+    TcArgs a3[3] = {P[0].a, P[1].a, P[2].a};
+    const int grid = 2 * std::min(n * P[0].items, num_sms() / 2);
+    if (n == 3) {
+        if (P[0].variant == 0) launch2<0, 0, 3>(m3, a3, grid, st);
+        else if (P[0].variant == 1) launch2<0, 1, 3>(m3, a3, grid, st);
+        else launch2<1, 1, 3>(m3, a3, grid, st);
+    } else {
+        if (P[0].variant == 0) launch2<0, 0, 2>(m3, a3, grid, st);
+        else if (P[0].variant == 1) launch2<0, 1, 2>(m3, a3, grid, st);
+        else launch2<1, 1, 2>(m3, a3, grid, st);
     }
     return true;
 }

@@ -1,0 +1,55 @@
+"""Phase timeline of the attention forward's CTA 0 (needs a -DPARL_ATTN_TRACE build,
+loaded through PARL_LIB).  Prints per-tile cycle offsets for the two softmax groups
+(wait S, S ready, S loaded, exps done, PV(prev) done, P handed over) and the two
+MMA issuers (S issued, PV wait begin, PV issued)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2511_18871_b200 import parl as P
+
+f = P.LIB.parl_debug_attn_bf16
+f.restype = C.c_int
+f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 6
+Pl, G, R, H, Dh = 512, 8, 1024, 14, 64
+T = Pl + G * R
+seg = torch.zeros(T, dtype=torch.int32)
+st, en = [0], [Pl]
+t = Pl
+for k in range(G):
+    seg[t:t + R] = k + 1
+    st.append(t)
+    en.append(t + R)
+    t += R
+seg, st, en = seg.cuda(), torch.tensor(st, dtype=torch.int32).cuda(), torch.tensor(en, dtype=torch.int32).cuda()
+qkv = torch.randn(T, 3 * H * Dh, device="cuda").bfloat16()
+out = torch.zeros(T, H * Dh, device="cuda", dtype=torch.bfloat16)
+lse = torch.zeros(H, T, device="cuda")
+args = (2, T, H, Dh, Pl, seg.data_ptr(), st.data_ptr(), en.data_ptr(), qkv.data_ptr(), out.data_ptr(), lse.data_ptr())
+for _ in range(3):
+    f(*args)
+torch.cuda.synchronize()
+buf = np.zeros((4, 64, 8), dtype=np.uint64)
+assert P.LIB.parl_debug_attn_trace(buf.ctypes.data_as(C.c_void_p)) == 0
+b = buf.astype(np.int64)
+t0 = b[b > 0].min()
+np.set_printoptions(linewidth=200)
+for w in range(2):
+    print(f"softmax group {w}: [wait S, S ready, S loaded, exps done, PV(prev) done, P handed] - t0")
+    for n in range(40):
+        if b[w, n, 0] == 0:
+            break
+        r = b[w, n, :6] - t0
+        print(n, r, "dur", r[5] - r[0], "waitS", r[1] - r[0], "load", r[2] - r[1], "exp", r[3] - r[2],
+              "waitPV", r[4] - r[3], "store", r[5] - r[4])
+for w in range(2):
+    print(f"mma {w}: [S issued, PV wait begin, PV issued] - t0")
+    for n in range(40):
+        if b[2 + w, n, 0] == 0 and b[2 + w, n, 1] == 0:
+            break
+        print(n, b[2 + w, n, :3] - t0)
