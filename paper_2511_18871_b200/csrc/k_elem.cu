@@ -296,10 +296,25 @@ __global__ void k_colsum_final(const float* __restrict__ part_a, const float* __
     pdl_wait();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
+    // loads issued 8 at a time, added in split order (deterministic)
     float a = 0.f, b = 0.f;
-    for (int s = 0; s < splits; ++s) {
-        a += part_a[(long)s * N + c];
-        if (mode == 1) b += part_b[(long)s * N + c];
+    int s0 = 0;
+    for (; s0 + 8 <= splits; s0 += 8) {
+        float va[8], vb[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            va[q] = part_a[(long)(s0 + q) * N + c];
+            vb[q] = mode == 1 ? part_b[(long)(s0 + q) * N + c] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            a += va[q];
+            b += vb[q];
+        }
+    }
+    for (; s0 < splits; ++s0) {
+        a += part_a[(long)s0 * N + c];
+        if (mode == 1) b += part_b[(long)s0 * N + c];
     }
     out[c] += a;
     if (mode == 1) out2[c] += b;
@@ -392,18 +407,34 @@ __global__ void k_row_lse(const float* __restrict__ z, int V, const int32_t* __r
 }
 
 // Combine the tcgen05 head's per-tile (max, sumexp) partials: lse and lp.
+// one warp per head row: lanes stride over the row's (max, sumexp) partials with
+// 8-byte coalesced loads, keep an online (max, sum), then combine in a fixed
+// shuffle tree (deterministic)
 __global__ void k_lse_combine(const float* __restrict__ part, int n_parts, const float* __restrict__ target,
                               int S, float* __restrict__ lse_out, float* __restrict__ lp_out) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (s >= S) return;
-    const float* p = part + (long)s * n_parts * 2;
-    float m = -INFINITY;
-    for (int i = 0; i < n_parts; ++i) m = fmaxf(m, p[2 * i]);
-    float sum = 0.f;
-    for (int i = 0; i < n_parts; ++i) sum += p[2 * i + 1] * __expf(p[2 * i] - m);
-    const float lse = m + logf(sum);
-    lse_out[s] = lse;
-    lp_out[s] = target[s] - lse;
+    const float2* p = reinterpret_cast<const float2*>(part + (long)s * n_parts * 2);
+    float m = -INFINITY, sum = 0.f;
+    for (int i = lane; i < n_parts; i += 32) {
+        const float2 v = p[i];
+        const float nm = fmaxf(m, v.x);
+        if (nm > -INFINITY) sum = sum * __expf(m - nm) + v.y * __expf(v.x - nm);
+        m = nm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float nm = fmaxf(m, om);
+        sum = nm > -INFINITY ? sum * __expf(m - nm) + os * __expf(om - nm) : 0.f;
+        m = nm;
+    }
+    if (lane == 0) {
+        const float lse = m + logf(sum);
+        lse_out[s] = lse;
+        lp_out[s] = target[s] - lse;
+    }
 }
 
 // K8a: dZ[s, v] = u[s] * (onehot(label[s]) - exp(z[s, v] - lse[s]))   (model.cpp:637-650)
@@ -967,7 +998,7 @@ void launch_row_lse(const float* z, int S, int V, const int32_t* labels, float* 
 void launch_lse_combine(const float* part, int n_parts, const float* target, int S, float* lse, float* lp,
                         cudaStream_t st) {
     if (S <= 0) return;
-    k_lse_combine<<<cdiv(S, 128), 128, 0, st>>>(part, n_parts, target, S, lse, lp);
+    launch_pdl(k_lse_combine, dim3(cdiv(S, 8)), dim3(256), 0, st, (const float*)part, n_parts, target, S, lse, lp);
     PARL_LAUNCHED();
 }
 
