@@ -356,7 +356,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf
 
 #ifdef PARL_ATTN_TRACE
 // phase timestamps of CTA 0 (build with -DPARL_ATTN_TRACE; read by parl_debug_attn_trace)
-__device__ unsigned long long g_attn_trace[4][64][8];
+__device__ unsigned long long g_attn_trace[16][64][8];
 #define ATTN_TRACE(role, n, k)                                                                  \
     do {                                                                                        \
         if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (n) < 64) g_attn_trace[role][n][k] = clock64(); \
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 }
             }
         }
-    } else if ((warp == 9 || warp == 10) && lane == 0) {
+    } else if (warp == 9 || warp == 10) {  // whole warp; one elected lane issues
         // ---------------- MMA issuers: warp 9 serves query tile 0, warp 10 tile 1,
         // so neither softmax group waits on the other's progress.  K/V stages and
         // the Q pair are released when both issuers are done with them.
@@ -489,10 +489,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
+                    tc::mma_bf16_e(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
                                  ks > 0);
                 }
-                tc::mma_commit(&s_full[w]);
+                tc::mma_commit_e(&s_full[w]);
                 ATTN_TRACE(2 + w, cS, 0);
                 ++cS;
                 return;
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const int st = g % KV_STAGES;
                 if (!(f & VIS)) {  // not ours: release the stage once it holds this entry
                     tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
-                    tc::mbar_arrive(&kv_empty[st]);
+                    if (lane == 0) tc::mbar_arrive(&kv_empty[st]);
                     continue;
                 }
                 issue_next_s();  // S of the next visible key tile (possibly in the next item)
@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
-                    tc::mma_bf16_ts(t_o + w * DH, t_p + w * 64 + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
+                    tc::mma_bf16_ts_e(t_o + w * DH, t_p + w * 64 + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
                                     id_o, (started || ks > 0) ? 1u : 0u);
-                tc::mma_commit(&o_done[w]);
-                tc::mma_commit(&kv_empty[st]);
+                tc::mma_commit_e(&o_done[w]);
+                tc::mma_commit_e(&kv_empty[st]);
                 ++cP;
                 if (!started) {
                     started = true;
@@ -532,10 +532,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 }
             }
             if (started) {
-                tc::mma_commit(&q_empty[qb]);
+                tc::mma_commit_e(&q_empty[qb]);
             } else {
                 tc::mbar_wait(&q_full[qb], (li >> 1) & 1);
-                tc::mbar_arrive(&q_empty[qb]);
+                if (lane == 0) tc::mbar_arrive(&q_empty[qb]);
             }
         }
       }
@@ -755,7 +755,7 @@ struct AttnBwd2Args {
 };
 
 constexpr int BWD_NTHR = 384;
-constexpr int BWD_ST = 3;
+constexpr int BWD_ST = 4;
 
 template <int DH>
 struct Bwd2Smem {
@@ -778,14 +778,14 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     uint64_t* a_full = bar + 0;    // [2]
     uint64_t* a_empty = bar + 2;   // [2]
-    uint64_t* b_full = bar + 4;    // [BWD_ST]
-    uint64_t* b_empty = bar + 7;   // [BWD_ST]
-    uint64_t* s_full = bar + 10;
-    uint64_t* s_free = bar + 11;
-    uint64_t* p_full = bar + 12;
-    uint64_t* g_done = bar + 13;
-    uint64_t* acc_full = bar + 14;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 16);
+    uint64_t* b_full = bar + 4;              // [BWD_ST]
+    uint64_t* b_empty = b_full + BWD_ST;     // [BWD_ST]
+    uint64_t* s_full = b_empty + BWD_ST;
+    uint64_t* s_free = s_full + 1;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* g_done = s_full + 3;
+    uint64_t* acc_full = s_full + 4;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(s_full + 6);
     float* vec = reinterpret_cast<float*>(smem + L::OFF_VEC);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                                  : "memory");
                 }
             }
-        } else if (warp == 9 && lane == 0) {  // ---------------- MMA
+        } else if (warp == 9) {  // ---------------- MMA (whole warp; one elected lane issues)
             constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);
             int cS = 0, cP = 0;
@@ -885,20 +885,25 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             auto issue_sd = [&]() {
                 if (s_k >= k_end) return;
                 const int st = gS % BWD_ST, ab = s_li & 1;
+                if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 0);
                 if (s_e == s_first) tc::mbar_wait(&a_full[ab], (s_li >> 1) & 1);
+                if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 1);
                 tc::mbar_wait(&b_full[st], (gS / BWD_ST) & 1);
+                if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 2);
                 if (cS > 0) tc::mbar_wait(s_free, (cS - 1) & 1);
+                if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 3);
                 tc::tc_fence_after();
                 const uint32_t f0 = tc::smem_u32(smem + L::OFF_A + (ab * 2) * L::TILE);
                 const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     const uint32_t off = (ks & 3) * 32;
-                    tc::mma_bf16(t_s, tc::sdesc(f0 + off, 16, 1024), tc::sdesc(s0 + off, 16, 1024), id_s, ks > 0);
-                    tc::mma_bf16(t_dp, tc::sdesc(f0 + L::TILE + off, 16, 1024),
+                    tc::mma_bf16_e(t_s, tc::sdesc(f0 + off, 16, 1024), tc::sdesc(s0 + off, 16, 1024), id_s, ks > 0);
+                    tc::mma_bf16_e(t_dp, tc::sdesc(f0 + L::TILE + off, 16, 1024),
                                  tc::sdesc(s0 + L::TILE + off, 16, 1024), id_s, ks > 0);
                 }
-                tc::mma_commit(s_full);
+                tc::mma_commit_e(s_full);
+                if (MODE == MODE_DKV) ATTN_TRACE(2, cS, 0);
                 ++cS;
                 ++gS;
                 if (++s_e == s_end) {
@@ -914,14 +919,16 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 const int ea = a.lst_ptr[t], eb = a.lst_ptr[t + 1];
                 if (ea == eb) {  // nothing streams into this item: release its operands
                     tc::mbar_wait(&a_full[ab], (li >> 1) & 1);
-                    tc::mbar_arrive(&a_empty[ab]);
+                    if (lane == 0) tc::mbar_arrive(&a_empty[ab]);
                     continue;
                 }
                 for (int e = ea; e < eb; ++e, ++g) {
                     const int st = g % BWD_ST;
                     issue_sd();
+                    if (MODE == MODE_DKV) ATTN_TRACE(2, cP, 1);
                     tc::mbar_wait(p_full, cP & 1);
                     tc::tc_fence_after();
+                    if (MODE == MODE_DKV) ATTN_TRACE(2, cP, 2);
                     const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
                     const uint32_t acc = (e > ea) ? 1u : 0u;
 #pragma unroll
@@ -929,18 +936,18 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                         const uint64_t b0 = tc::sdesc(s0 + ks * 2048, 128 * 128, 1024);
                         const uint64_t b1 = tc::sdesc(s0 + L::TILE + ks * 2048, 128 * 128, 1024);
                         if (MODE == MODE_DKV) {
-                            tc::mma_bf16_ts(t_acc1, t_p + ks * 8, b1, id_g, (acc || ks > 0) ? 1u : 0u);   // dV += P^T dO
-                            tc::mma_bf16_ts(t_acc2, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dK += dS^T Q
+                            tc::mma_bf16_ts_e(t_acc1, t_p + ks * 8, b1, id_g, (acc || ks > 0) ? 1u : 0u);   // dV += P^T dO
+                            tc::mma_bf16_ts_e(t_acc2, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dK += dS^T Q
                         } else {
-                            tc::mma_bf16_ts(t_acc1, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dQ += dS K
+                            tc::mma_bf16_ts_e(t_acc1, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dQ += dS K
                         }
                     }
-                    tc::mma_commit(g_done);
-                    tc::mma_commit(&b_empty[st]);
+                    tc::mma_commit_e(g_done);
+                    tc::mma_commit_e(&b_empty[st]);
                     ++cP;
                 }
-                tc::mma_commit(acc_full);
-                tc::mma_commit(&a_empty[ab]);
+                tc::mma_commit_e(acc_full);
+                tc::mma_commit_e(&a_empty[ab]);
             }
         }
     } else {
@@ -983,21 +990,28 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 const int u0 = (int)(fl & 0x3fffffff) * 128;  // first row of the streamed tile
                 const bool full = (fl >> 30) & 1;
                 const uint32_t vl = tc::smem_u32(vec + (g % BWD_ST) * 256);
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 0);
                 tc::mbar_wait(s_full, cS & 1);
                 tc::tc_fence_after();
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 1);
                 uint32_t pp[32], pd[32];  // packed bf16 P / dS of this thread's 64 columns
+                // all four TMEM loads (S and dP, both 32-column chunks) in flight at once, then
+                // S/dP are released so the next tile's S/dP MMAs overlap this tile's math
+                float sall[64], dall[64];
+                tc::tmem_ld32_nowait(t_s + half * 64 + lane_off, reinterpret_cast<uint32_t*>(sall));
+                tc::tmem_ld32_nowait(t_dp + half * 64 + lane_off, reinterpret_cast<uint32_t*>(dall));
+                tc::tmem_ld32_nowait(t_s + half * 64 + 32 + lane_off, reinterpret_cast<uint32_t*>(sall) + 32);
+                tc::tmem_ld32_nowait(t_dp + half * 64 + 32 + lane_off, reinterpret_cast<uint32_t*>(dall) + 32);
+                tc::tmem_ld_wait();
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(s_free);
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 2);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int cb = half * 64 + c * 32;  // first tile column of the chunk
-                    float sv[32], dp[32];
-                    tc::tmem_ld32_nowait(t_s + cb + lane_off, reinterpret_cast<uint32_t*>(sv));
-                    tc::tmem_ld32_nowait(t_dp + cb + lane_off, reinterpret_cast<uint32_t*>(dp));
-                    tc::tmem_ld_wait();
-                    if (c == 1) {  // S and dP read: the next tile's S/dP may be issued
-                        tc::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) tc::mbar_arrive(s_free);
-                    }
+                    const float* sv = sall + 32 * c;
+                    const float* dp = dall + 32 * c;
                     // exponent argument (log2 units); -inf where the pair is masked
                     float arg[32], dd[32];
 #pragma unroll
@@ -1047,11 +1061,13 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                         pd[c * 16 + j / 2] = pack2(p0 * dd[j], p1 * dd[j + 1]);
                     }
                 }
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 3);
                 // the previous tile's gradient MMAs have read P / dS
                 if (cS > 0) {
                     tc::mbar_wait(g_done, (cS - 1) & 1);
                     tc::tc_fence_after();
                 }
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 4);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     if (MODE == MODE_DKV) tc::tmem_st16(t_p + half * 32 + c * 16 + lane_off, pp + 16 * c);
@@ -1061,6 +1077,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(p_full);
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 5);
                 ++cS;
             }
             // item epilogue: accumulators -> bf16 rows of dqkv (MODE_DKV: half 0 dV -> 2d + h DH,

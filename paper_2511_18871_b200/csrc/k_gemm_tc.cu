@@ -418,8 +418,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (whole warp; one elected lane issues)
         constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN, B_MN);
         uint32_t cnt = 0, local = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
@@ -441,11 +441,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int ks = 0; ks < BK / 16; ++ks) {
                     const uint64_t ad = A_MN ? tc::sdesc(sa + ks * 2048, 8192, 1024) : tc::sdesc(sa + ks * 32, 16, 1024);
                     const uint64_t bd = B_MN ? tc::sdesc(sb + ks * 2048, 8192, 1024) : tc::sdesc(sb + ks * 32, 16, 1024);
-                    tc::mma_bf16(dcol, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                    tc::mma_bf16_e(dcol, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                 }
-                tc::mma_commit(&empty[s]);
+                tc::mma_commit_e(&empty[s]);
             }
-            tc::mma_commit(&tfull[acc]);
+            tc::mma_commit_e(&tfull[acc]);
         }
     } else if (warp >= 4) {
         const EpiSeq e{(int)blockIdx.x, (int)gridDim.x, n_items, a.tiles_m, BM, 0, n_items};
@@ -566,8 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
-        // ---------------- MMA issuer (leader CTA only)
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA only; whole warp, one elected lane issues)
         constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, A_MN, B_MN);
         uint32_t cnt = 0, local = 0;
         for (int item = cid; item < n_items; item += ncl, ++local) {
@@ -589,11 +589,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 for (int ks = 0; ks < BK / 16; ++ks) {
                     const uint64_t ad = A_MN ? tc::sdesc(sa + ks * 2048, 8192, 1024) : tc::sdesc(sa + ks * 32, 16, 1024);
                     const uint64_t bd = B_MN ? tc::sdesc(sb + ks * 2048, 8192, 1024) : tc::sdesc(sb + ks * 32, 16, 1024);
-                    tc::mma_bf16_pair(dcol, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                    tc::mma_bf16_pair_e(dcol, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                 }
-                tc::mma_commit_pair(&empty[s], 0x3);
+                tc::mma_commit_pair_e(&empty[s], 0x3);
             }
-            tc::mma_commit_pair(&tfull[acc], 0x3);
+            tc::mma_commit_pair_e(&tfull[acc], 0x3);
         }
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs: this CTA's 128 rows x all 256 columns)
@@ -693,8 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 tc::tma_load_2d_pair(sb + 8192, &mp.b[p], fb, n0 + 64, kb * BK);
             }
         }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
-        // ---------------- MMA issuer (leader CTA)
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA; whole warp, one elected lane issues)
         constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, 1, 1);
         uint32_t cnt = 0, local = 0;
         for (int item = cid; item < n_items; item += ncl, ++local) {
@@ -711,11 +711,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
                 for (int ks = 0; ks < BK / 16; ++ks)
-                    tc::mma_bf16_pair(dcol, tc::sdesc(sa + ks * 2048, 8192, 1024), tc::sdesc(sb + ks * 2048, 8192, 1024),
+                    tc::mma_bf16_pair_e(dcol, tc::sdesc(sa + ks * 2048, 8192, 1024), tc::sdesc(sb + ks * 2048, 8192, 1024),
                                       idesc, (kb > 0 || ks > 0) ? 1u : 0u);
-                tc::mma_commit_pair(&empty[s], 0x3);
+                tc::mma_commit_pair_e(&empty[s], 0x3);
             }
-            tc::mma_commit_pair(&tfull[acc], 0x3);
+            tc::mma_commit_pair_e(&tfull[acc], 0x3);
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: fp32 accumulator -> swizzled staging -> TMA reduce-add

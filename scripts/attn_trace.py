@@ -34,20 +34,40 @@ args = (2, T, H, Dh, Pl, seg.data_ptr(), st.data_ptr(), en.data_ptr(), qkv.data_
 for _ in range(3):
     f(*args)
 torch.cuda.synchronize()
-buf = np.zeros((4, 64, 8), dtype=np.uint64)
+if len(sys.argv) > 1 and sys.argv[1] == "bwd":  # trace the dK/dV kernel instead
+    fb = P.LIB.parl_debug_attn_bwd_bf16
+    fb.restype = C.c_int
+    fb.argtypes = [C.c_int] * 5 + [C.c_void_p] * 9
+    dout = torch.randn(T, H * Dh, device="cuda").bfloat16()
+    dsum = torch.zeros(H, T, device="cuda")
+    dqkv = torch.zeros(T, 3 * H * Dh, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        fb(2, T, H, Dh, Pl, seg.data_ptr(), st.data_ptr(), en.data_ptr(), qkv.data_ptr(), out.data_ptr(),
+           dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(), dqkv.data_ptr())
+    torch.cuda.synchronize()
+buf = np.zeros((16, 64, 8), dtype=np.uint64)
 assert P.LIB.parl_debug_attn_trace(buf.ctypes.data_as(C.c_void_p)) == 0
 b = buf.astype(np.int64)
 t0 = b[b > 0].min()
 np.set_printoptions(linewidth=200)
+if len(sys.argv) > 1 and sys.argv[1] == "bwd":
+    t0 = b[4:12][b[4:12] > 0].min()
+    print("per element-wise warp: P handed (k=5) and S loaded (k=2) of tiles 2..8, minus t0")
+    for wp in range(8):
+        print(wp, "S loaded", b[4 + wp, 2:9, 2] - t0, "P handed", b[4 + wp, 2:9, 5] - t0)
+    print("mma: S issued", b[2, 2:10, 0] - t0, "PV wait", b[2, 2:10, 1] - t0, "PV issued", b[2, 2:10, 2] - t0)
+    print("issue_sd: enter", b[3, 2:10, 0] - t0, "a_full ok", b[3, 2:10, 1] - t0, "b_full ok", b[3, 2:10, 2] - t0,
+          "s_free ok", b[3, 2:10, 3] - t0)
+    sys.exit(0)
 for w in range(2):
-    print(f"softmax group {w}: [wait S, S ready, S loaded, exps done, PV(prev) done, P handed] - t0")
+    print(f"element-wise group {w}: [wait S, S ready, S loaded, exps done, MMA(prev) done, P handed] - t0")
     for n in range(40):
         if b[w, n, 0] == 0:
             break
         r = b[w, n, :6] - t0
         print(n, r, "dur", r[5] - r[0], "waitS", r[1] - r[0], "load", r[2] - r[1], "exp", r[3] - r[2],
               "waitPV", r[4] - r[3], "store", r[5] - r[4])
-for w in range(2):
+for w in range(2 if not (len(sys.argv) > 1 and sys.argv[1] == "bwd") else 1):
     print(f"mma {w}: [S issued, PV wait begin, PV issued] - t0")
     for n in range(40):
         if b[2 + w, n, 0] == 0 and b[2 + w, n, 1] == 0:
