@@ -118,7 +118,11 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
                                                uint64_t* tfull, uint32_t tbase, const EpiSeq& e, Release release) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ew = warp & 3, half = (warp - 4) >> 2, wi = warp - 4;
-    constexpr int HALF = BNT / 2, NCH = HALF / 32;
+    // the two warp halves own columns [0, H0) and [H0, BNT) of the tile (224-wide pair
+    // tiles split 128 + 96 so every chunk is a full 32 columns)
+    constexpr int H0 = BNT == 224 ? 128 : BNT / 2;
+    const int hcol = half ? H0 : 0;
+    const int NCH = (half ? BNT - H0 : H0) / 32;
     uint8_t* stg = stg_all + wi * NBUF * STG_BYTES;
     const uint32_t stg_s = tc::smem_u32(stg);
     uint64_t* inbar = inbar_all + wi * NBUF;
@@ -133,7 +137,7 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
         const int nt = rest % a0.tiles_n;
         sp = rest / a0.tiles_n;
         row = mt * e.mrows + e.rank * BM + ew * 32;
-        col = nt * BNT + half * HALF;
+        col = nt * BNT + hcol;
     };
     // chunk stream: (item, c) -> the next chunk; item >= n_items when exhausted
     auto next = [&](int& item, int& c) {
@@ -198,7 +202,7 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
             const uint32_t b = k % NBUF;
             const uint32_t sb = stg_s + b * STG_BYTES;
             float v[32];
-            tc::tmem_ld32(tbase + acc * BNT + half * HALF + c * 32 + ((uint32_t)(ew * 32) << 16), v);
+            tc::tmem_ld32(tbase + acc * BNT + hcol + c * 32 + ((uint32_t)(ew * 32) << 16), v);
             if (c == NCH - 1) {  // accumulator fully read: hand it back to the MMA warp
                 tc::tc_fence_before();
                 release(acc);
@@ -466,15 +470,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // writes each CTA's 128 accumulator rows into its own TMEM.  Per SM this halves
 // the operand bytes per MMA cycle relative to the 1-CTA 128 x 256 tile.
 constexpr int BN2 = 256;
-struct Cfg2 {
+// NB = tile width of the pair (256, or 224 for N = 896 / 2688-like problems so no
+// half-empty tile column is computed); each CTA holds NB / 2 columns of B.
+template <int NB>
+struct Cfg2T {
     static constexpr int A_BYTES = BM * BK * 2;          // 128 rows of A
-    static constexpr int B_BYTES = (BN2 / 2) * BK * 2;   // 128 columns of B
+    static constexpr int B_BYTES = 128 * BK * 2;         // NB / 2 <= 128 columns of B (MN-major loads two 64-wide boxes)
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int STAGES = 4;
     static constexpr int STG_OFF = STAGES * STAGE;
     static constexpr int BAR_OFF = STG_OFF + EPI_SMEM;
     static constexpr int SMEM = BAR_OFF + 512 + 1024;
 };
+using Cfg2 = Cfg2T<256>;
 
 template <int NP>
 struct PairMaps {
@@ -486,11 +494,13 @@ struct PairArgs {
 };
 
 // NP equal-shape problems per launch (item = problem * tiles-per-problem + tile)
-template <int A_MN, int B_MN, int NP>
+template <int A_MN, int B_MN, int NP, int NB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_gemm_tc2(const __grid_constant__ PairMaps<NP> mp, const __grid_constant__ PairArgs<NP> pa) {
     const TcArgs& a = pa.a[0];  // shape / K-split fields are common to the problems
-    using C = Cfg2;
+    using C = Cfg2T<NB>;
+    // expected bytes per stage and CTA: A + the B half actually transferred
+    constexpr uint32_t STAGE_TX = C::A_BYTES + (B_MN ? 128 : NB / 2) * BK * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -524,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tc::tma_prefetch(&mp.b[q]);
         }
     }
-    if (warp == 2) tc::tmem_alloc_pair<2 * BN2>(tbase_s);
+    if (warp == 2) tc::tmem_alloc_pair<512>(tbase_s);
     tc::tc_fence_before();
     __syncthreads();
     tc::cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
@@ -543,13 +553,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const int mt = t % tiles_m2, rest = t / tiles_m2;
             const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
             const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
-            const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * BN2 + (int)rank * (BN2 / 2);
+            const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * NB + (int)rank * (NB / 2);
             for (int kb = kb0; kb < kb1; ++kb, ++cnt) {
                 const int s = cnt % C::STAGES;
                 const uint32_t ph = (cnt / C::STAGES) & 1;
                 tc::mbar_wait(&empty[s], ph ^ 1);
                 const uint32_t fb = tc::mapa(&full[s], 0);
-                if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * C::STAGE);
+                if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * STAGE_TX);
                 uint8_t* sa = smem + s * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
                 if (!A_MN) {
@@ -568,7 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == 1 && rank == 0) {
         // ---------------- MMA issuer (leader CTA only; whole warp, one elected lane issues)
-        constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN2, A_MN, B_MN);
+        constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, NB, A_MN, B_MN);
         uint32_t cnt = 0, local = 0;
         for (int item = cid; item < n_items; item += ncl, ++local) {
             const int rest = (item % tpp) / tiles_m2;
@@ -577,7 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const uint32_t acc = local & 1, use = local >> 1;
             tc::mbar_wait(&tempty[acc], (use & 1) ^ 1);
             tc::tc_fence_after();
-            const uint32_t dcol = tbase + acc * BN2;
+            const uint32_t dcol = tbase + acc * NB;
             for (int kb = kb0; kb < kb1; ++kb, ++cnt) {
                 const int s = cnt % C::STAGES;
                 const uint32_t ph = (cnt / C::STAGES) & 1;
@@ -599,7 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // ---------------- epilogue (both CTAs: this CTA's 128 rows x all 256 columns)
         const EpiSeq e{cid, ncl, n_items, tiles_m2, 2 * BM, (int)rank, tpp};
         const uint32_t leader_tempty0 = tc::mapa(&tempty[0], 0);
-        epilogue_warps<BN2>(pa.a, mp.o, mp.o2, mp.i, smem + C::STG_OFF, inbar, tfull, tbase, e, [&](uint32_t acc) {
+        epilogue_warps<NB>(pa.a, mp.o, mp.o2, mp.i, smem + C::STG_OFF, inbar, tfull, tbase, e, [&](uint32_t acc) {
             tc::mbar_arrive_cluster_relaxed(leader_tempty0 + acc * 8);
         });
     }
@@ -608,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tc::cluster_sync();
     if (warp == 2) {
         tc::tc_fence_after();
-        tc::tmem_dealloc_pair<2 * BN2>(tbase);
+        tc::tmem_dealloc_pair<512>(tbase);
     }
 }
 
@@ -874,12 +884,12 @@ void launch(const Maps& m, const TcArgs& a, int grid, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
-template <int A_MN, int B_MN, int NP>
+template <int A_MN, int B_MN, int NP, int NB = 256>
 void launch2(const Maps* m, const TcArgs* a, int grid, cudaStream_t st) {
-    auto k = k_gemm_tc2<A_MN, B_MN, NP>;
+    auto k = k_gemm_tc2<A_MN, B_MN, NP, NB>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2T<NB>::SMEM);
         attr = true;
     }
     PairMaps<NP> pm;
@@ -888,7 +898,7 @@ void launch2(const Maps* m, const TcArgs* a, int grid, cudaStream_t st) {
         pm.a[q] = m[q].a; pm.b[q] = m[q].b; pm.o[q] = m[q].o; pm.o2[q] = m[q].o2; pm.i[q] = m[q].i;
         pa.a[q] = a[q];
     }
-    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg2::SMEM, st, pm, pa);
+    launch_pdl(k, dim3(grid), dim3(NTHREADS), Cfg2T<NB>::SMEM, st, pm, pa);
 }
 
 // PARL_GEMM_PAIR=0 disables the CTA-pair kernel (diagnostics)
@@ -944,7 +954,7 @@ namespace {
 // Launch plan of one GEMM: kernel variant, tiling, tensor maps, device args.
 struct Plan {
     bool pair = false;
-    int BN = 256, variant = 0, items = 0;  // variant: 0 K/K, 1 K/MN, 2 MN/MN
+    int BN = 256, variant = 0, items = 0;  // variant: 0 K/K, 1 K/MN, 2 MN/MN; BN: tile width (pair: 256 or 224)
     Maps mp;
     TcArgs a{};
     float* ws = nullptr;
@@ -968,7 +978,9 @@ bool plan_gemm(const GemmArgs& g, Plan& P) {
     const int sms = num_sms();
     const bool pair = pair_enabled() && g.M > 128 && g.N >= 256 && (g.N % 128) == 0 &&
                       (long)((g.M + 255) / 256) * ((g.N + 255) / 256) >= sms / 4 && (a_k || b_mn);
-    const int BN = pair ? 256 : (g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256));
+    // pair tiles are 224 wide when that covers N exactly and 256 does not (N = 896, 2688, ...)
+    const int NB = (g.N % 256 != 0 && g.N % 224 == 0 && g.epi != EPI_LSE) ? 224 : 256;
+    const int BN = pair ? NB : (g.epi == EPI_LSE ? 256 : ((g.N % 256 != 0 && g.N % 128 == 0) || g.N <= 128 ? 128 : 256));
     P.pair = pair;
     P.BN = BN;
     Maps& mp = P.mp;
@@ -1055,9 +1067,15 @@ void run_plan(const Plan& P, const GemmArgs& g, cudaStream_t st) {
     const int v = P.variant;
     if (P.pair) {
         const int grid = 2 * std::min(P.items, sms / 2);
-        if (v == 0) launch2<0, 0, 1>(&P.mp, &P.a, grid, st);
-        else if (v == 1) launch2<0, 1, 1>(&P.mp, &P.a, grid, st);
-        else launch2<1, 1, 1>(&P.mp, &P.a, grid, st);
+        if (P.BN == 224) {
+            if (v == 0) launch2<0, 0, 1, 224>(&P.mp, &P.a, grid, st);
+            else if (v == 1) launch2<0, 1, 1, 224>(&P.mp, &P.a, grid, st);
+            else launch2<1, 1, 1, 224>(&P.mp, &P.a, grid, st);
+        } else {
+            if (v == 0) launch2<0, 0, 1>(&P.mp, &P.a, grid, st);
+            else if (v == 1) launch2<0, 1, 1>(&P.mp, &P.a, grid, st);
+            else launch2<1, 1, 1>(&P.mp, &P.a, grid, st);
+        }
     } else if (P.BN == 256) {
         const int grid = std::min(P.items, sms);
         if (v == 0) launch<256, 0, 0>(P.mp, P.a, grid, st);
@@ -1099,7 +1117,7 @@ bool gemm_tc_multi(const GemmArgs* gs, int n, cudaStream_t st) {
     }
     if (group) {
         for (int q = 0; q < n; ++q)
-            group = group && P[q].pair && P[q].a.splits == 1 && P[q].variant == P[0].variant &&
+            group = group && P[q].pair && P[q].a.splits == 1 && P[q].variant == P[0].variant && P[q].BN == P[0].BN &&
                     P[q].a.M == P[0].a.M && P[q].a.N == P[0].a.N && P[q].a.K == P[0].a.K &&
                     P[q].a.store_logits == P[0].a.store_logits && P[q].a.logits_direct == nullptr &&
                     ((P[q].a.epi == EPI_RESID || P[q].a.epi == EPI_GELU_BWD) ==
@@ -1115,13 +1133,22 @@ bool gemm_tc_multi(const GemmArgs* gs, int n, cudaStream_t st) {
     Maps m3[3] = {P[0].mp, P[1].mp, P[2].mp};
     TcArgs a3[3] = {P[0].a, P[1].a, P[2].a};
     const int grid = 2 * std::min(n * P[0].items, num_sms() / 2);
-    if (n == 3) {
-        if (P[0].variant == 0) launch2<0, 0, 3>(m3, a3, grid, st);
-        else if (P[0].variant == 1) launch2<0, 1, 3>(m3, a3, grid, st);
+    const int v = P[0].variant;
+    if (n == 3 && P[0].BN == 224) {
+        if (v == 0) launch2<0, 0, 3, 224>(m3, a3, grid, st);
+        else if (v == 1) launch2<0, 1, 3, 224>(m3, a3, grid, st);
+        else launch2<1, 1, 3, 224>(m3, a3, grid, st);
+    } else if (n == 3) {
+        if (v == 0) launch2<0, 0, 3>(m3, a3, grid, st);
+        else if (v == 1) launch2<0, 1, 3>(m3, a3, grid, st);
         else launch2<1, 1, 3>(m3, a3, grid, st);
+    } else if (P[0].BN == 224) {
+        if (v == 0) launch2<0, 0, 2, 224>(m3, a3, grid, st);
+        else if (v == 1) launch2<0, 1, 2, 224>(m3, a3, grid, st);
+        else launch2<1, 1, 2, 224>(m3, a3, grid, st);
     } else {
-        if (P[0].variant == 0) launch2<0, 0, 2>(m3, a3, grid, st);
-        else if (P[0].variant == 1) launch2<0, 1, 2>(m3, a3, grid, st);
+        if (v == 0) launch2<0, 0, 2>(m3, a3, grid, st);
+        else if (v == 1) launch2<0, 1, 2>(m3, a3, grid, st);
         else launch2<1, 1, 2>(m3, a3, grid, st);
     }
     return true;

@@ -56,7 +56,7 @@ def operands(torch, M, N, K, a_mn, b_mn, seed=0):
 LAYOUTS = [(0, 0), (0, 1), (1, 1)]
 SHAPES = [(128, 256, 64), (256, 512, 192), (296, 200, 104), (128, 896, 896), (1000, 384, 520), (64, 40, 24),
           # large enough for the CTA-pair (cta_group::2) kernel, with M/K tails
-          (4096, 1024, 512), (4000, 1152, 520), (8704, 896, 896)]
+          (4096, 1024, 512), (4000, 1152, 520), (8704, 896, 896), (4096, 2688, 200)]
 
 
 @pytest.mark.parametrize("lay", LAYOUTS)
@@ -96,7 +96,9 @@ def test_split_k_accumulate(env):
     assert torch.equal(out, out2)  # deterministic split order
 
 
-@pytest.mark.parametrize("shape", [(384, 512, 256), (4096, 1024, 512), (2000, 896, 200)])
+@pytest.mark.parametrize("shape", [(384, 512, 256), (4096, 1024, 512), (2000, 896, 200),
+                                   # 224-wide CTA-pair tiles (N = 896, 2688)
+                                   (4096, 896, 512), (3000, 2688, 256)])
 def test_epilogues(env, shape):
     torch = env[0]
     M, N, K = shape
