@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
         constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);
         int cS = 0, cP = 0, nI = 0;
-        // S look-ahead iterator over the entries visible to this tile
+        // S look-ahead over the entries visible to this tile.  A look-ahead S may only
+        // wait for a K/V stage that cannot depend on this thread's own later releases:
+        // its entry must lie within KV_STAGES - 1 of the entry being processed (a tile
+        // whose pair partner sees many more key tiles skips long runs of entries).
         const int k_end = a.w_ptr[blockIdx.x + 1];
         int s_k = a.w_ptr[blockIdx.x], s_li = 0, s_e = 0, s_end = 0, gS = 0;
         auto s_load_item = [&]() {
@@ -465,8 +468,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 s_end = a.p_ptr[p + 1];
             }
         };
-        s_load_item();
-        auto issue_next_s = [&]() {
+        // move the iterator to the next entry visible to this tile (global index gS); false at the end
+        auto s_seek = [&]() -> bool {
             while (s_k < k_end) {
                 if (s_e >= s_end) {
                     ++s_k;
@@ -474,31 +477,37 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     s_load_item();
                     continue;
                 }
-                const uint32_t f = (uint32_t)a.p_list[s_e];
-                const int g = gS;
+                if ((uint32_t)a.p_list[s_e] & VIS) return true;
                 ++s_e;
                 ++gS;
-                if (!(f & VIS)) continue;
-                const int st = g % KV_STAGES, qb = s_li & 1;
-                tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
-                tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
-                if (cS > 0) tc::mbar_wait(&s_free[w], (cS - 1) & 1);
-                tc::tc_fence_after();
-                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
-                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + (qb * 2 + w) * L::TILE);
-#pragma unroll
-                for (int ks = 0; ks < DH / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16_e(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
-                                 ks > 0);
-                }
-                tc::mma_commit_e(&s_full[w]);
-                ATTN_TRACE(2 + w, cS, 0);
-                ++cS;
-                return;
             }
+            return false;
         };
-        issue_next_s();
+        s_load_item();
+        auto issue_s = [&]() {  // S for the iterator's entry (visible, gS)
+            const int g = gS, st = g % KV_STAGES, qb = s_li & 1;
+            tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
+            tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
+            if (cS > 0) tc::mbar_wait(&s_free[w], (cS - 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
+            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + (qb * 2 + w) * L::TILE);
+#pragma unroll
+            for (int ks = 0; ks < DH / 16; ++ks) {
+                const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                tc::mma_bf16_e(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
+                               ks > 0);
+            }
+            tc::mma_commit_e(&s_full[w]);
+            ATTN_TRACE(2 + w, cS, 0);
+            ++cS;
+            ++s_e;
+            ++gS;
+        };
+        // issue pending S (at most one beyond the tile being processed) within the stage window
+        auto advance_s = [&](int g_now) {
+            while (cS < cP + 2 && s_seek() && gS <= g_now + KV_STAGES - 1) issue_s();
+        };
         int g = 0, li = 0;
         for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
             const int p = a.w_items[k] / H, qb = li & 1;
@@ -507,12 +516,12 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             for (int e = ea; e < eb; ++e, ++g) {
                 const uint32_t f = (uint32_t)a.p_list[e];
                 const int st = g % KV_STAGES;
+                advance_s(g);  // S of this entry (if not yet issued) and of the next visible one
                 if (!(f & VIS)) {  // not ours: release the stage once it holds this entry
                     tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
                     if (lane == 0) tc::mbar_arrive(&kv_empty[st]);
                     continue;
                 }
-                issue_next_s();  // S of the next visible key tile (possibly in the next item)
                 ATTN_TRACE(2 + w, cP, 1);
                 tc::mbar_wait(&p_full[w], cP & 1);
                 if (!started && nI > 0) tc::mbar_wait(&o_free[w], (nI - 1) & 1);
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
                     tc::mma_bf16_ts_e(t_o + w * DH, t_p + w * 64 + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
-                                    id_o, (started || ks > 0) ? 1u : 0u);
+                                      id_o, (started || ks > 0) ? 1u : 0u);
                 tc::mma_commit_e(&o_done[w]);
                 tc::mma_commit_e(&kv_empty[st]);
                 ++cP;
@@ -530,6 +539,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     started = true;
                     ++nI;
                 }
+                advance_s(g);  // look ahead right after handing this PV off
             }
             if (started) {
                 tc::mma_commit_e(&q_empty[qb]);

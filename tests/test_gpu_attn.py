@@ -53,7 +53,10 @@ def reference(torch, qkv, H, Dh, allowed):
 
 
 CASES = [(300, [200, 250, 260], 2, 64), (64, [128, 128, 128, 128], 3, 64), (130, [5, 300, 1, 77], 2, 128),
-         (700, [], 2, 64), (512, [1024] * 2, 1, 128)]
+         (700, [], 2, 64), (512, [1024] * 2, 1, 128),
+         # long responses ending mid-pair: one tile of a pair skips a whole response's key
+         # tiles (more than the K/V ring holds) while its partner consumes them
+         (1638, [3000, 2700], 2, 64), (200, [1500, 900, 700], 2, 64)]
 
 
 @pytest.mark.parametrize("case", CASES)
