@@ -35,7 +35,19 @@ CONFIGS = {
     "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=4),
     # BASELINE.json configs[1]: Qwen2.5-0.5B-shaped random-init tri-model, G=8, 512+1k, bf16, single B200
     "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=2),
+    # configs[2]: Qwen2.5-7B-shaped tri-model, G=16, 1k prompt + 4k responses (T=66,560 per group),
+    # one group per rank (prompt groups sharded over the GPUs); runs with activation recomputation
+    "c3": dict(vocab=152064, d=3584, L=28, H=28, F=18944, max_seq=66560, P=1024, G=16, R=4096, prec="bf16",
+               groups=1),
+    # configs[3]: long-CoT ragged batch, Qwen2.5-1.5B shape, 2k prompt + 8 responses of 1k-16k tokens
+    # (SURVEY.md 8d seed: random.Random(20251118).randint(1024, 16384), group 0; T=87,893)
+    "c4": dict(vocab=151936, d=1536, L=28, H=12, F=8960, max_seq=90112, P=2048, G=8, R=None, prec="bf16", groups=1,
+               lens=[15781, 14233, 10574, 3139, 3977, 14992, 13452, 9697]),
 }
+
+
+def group_lens(c):
+    return list(c["lens"]) if c.get("lens") else [c["R"]] * c["G"]
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -154,14 +166,36 @@ def barrier(pg):
         pg.barrier()
 
 
-def cpu_threads(per_thread_bytes: float) -> int:
-    cores = os.cpu_count() or 1
+def host_mem_available() -> int:
     try:
         with open("/proc/meminfo") as f:
-            avail = next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable"))
+            return next(int(l.split()[1]) * 1024 for l in f if l.startswith("MemAvailable"))
     except Exception:
-        avail = 16 << 30
-    return max(1, min(cores, int(0.6 * avail / per_thread_bytes)))
+        return 16 << 30
+
+
+def cpu_threads(per_thread_bytes: float) -> int:
+    cores = os.cpu_count() or 1
+    return max(1, min(cores, int(0.6 * host_mem_available() / per_thread_bytes)))
+
+
+def _sample_cfg(c):
+    from oracle import Cfg
+
+    # the workload's model dims with a tiny packed group: P=2, G=2, R=1 per worker (T=4)
+    sP, sG, sR = (2, 2, 1) if c["vocab"] > 10000 else (c["P"], c["G"], c["R"])
+    return Cfg(c["vocab"], c["d"], c["L"], c["H"], c["F"], max(sP + sG * sR, 8)), sP, sG, sR
+
+
+def reference_fits(c):
+    """Whether one reference worker (fp64 params + grads + clones) fits host memory."""
+    from oracle import Oracle
+
+    try:
+        ref = Oracle("ref")
+    except FileNotFoundError:
+        return False
+    return 6.0 * 8 * ref.param_count(_sample_cfg(c)[0]) <= 0.6 * host_mem_available()
 
 
 def reference_sample(c, reps=1, threads=None):
@@ -173,16 +207,16 @@ def reference_sample(c, reps=1, threads=None):
         ref = Oracle("ref")
     except FileNotFoundError:
         return None
-    # C2 dims with a tiny packed group: P=2, G=2, R=1 per worker (T=4)
-    sP, sG, sR = (2, 2, 1) if c["vocab"] > 10000 else (c["P"], c["G"], c["R"])
-    cfg = Cfg(c["vocab"], c["d"], c["L"], c["H"], c["F"], max(sP + sG * sR, 8))
+    cfg, sP, sG, sR = _sample_cfg(c)
     n_params = ref.param_count(cfg)
+    if 6.0 * 8 * n_params > 0.6 * host_mem_available():  # fp64 params + grads + clones per thread
+        return None
     thr = threads or cpu_threads(6.0 * 8 * n_params)
     secs = ref.bench_microbatch(cfg, 7, sP, sG, sR, reps, thr)
     T_s = sP + sG * sR
     fl_s = flops_per_group(c, sP, [sR] * sG, reference_head=True)
-    fl_w = flops_per_group(c, c["P"], [c["R"]] * c["G"], reference_head=True)
-    T_w = c["P"] + c["G"] * c["R"]
+    fl_w = flops_per_group(c, c["P"], group_lens(c), reference_head=True)
+    T_w = c["P"] + sum(group_lens(c))
     tok_s_sample = thr * reps * T_s / secs
     scaled = tok_s_sample * (fl_s / T_s) / (fl_w / T_w)
     info = {"cores": thr, "sample": f"reference train_microbatch (shared-prompt) at {c['name']} model dims, "
@@ -198,13 +232,17 @@ def run_reference(args, c):
     if rank != 0:
         return
     c["name"] = args.config
-    T_w = c["P"] + c["G"] * c["R"]
+    T_w = c["P"] + sum(group_lens(c))
     from oracle import Oracle
 
     try:
         Oracle("ref")
     except FileNotFoundError:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparl_ref.so not built"}))
+        return
+    if not reference_fits(c):
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference's fp64 model at {args.config} dims does "
+                                                              f"not fit this host's memory"}))
         return
     for _ in range(args.warmup):
         reference_sample(c)
@@ -219,7 +257,7 @@ def run_reference(args, c):
            "ms_per_step": 1000.0 * T_w / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
-                                  f"P={c['P']} G={c['G']} R={c['R']} (T={T_w}) per group"},
+                                  f"P={c['P']} G={c['G']} R={group_lens(c)} (T={T_w}) per group"},
            "cpu_baseline": {"value": value, "unit": "packed tokens/s", "cores": infos[0]["cores"],
                             "kind": "reference", "sample": infos[0]["sample"]},
            "e2e": {"value": value, "unit": "packed tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -245,13 +283,14 @@ def run_ours(args, c):
     grads = P.GradBuffer(pol)
     hyper = P.HyperParams(0.2, 0.04, "token")
 
-    Pn, G, R, ng = c["P"], c["G"], c["R"], args.groups or c["groups"]
-    T = Pn + G * R
+    Pn, G, ng = c["P"], c["G"], args.groups or c["groups"]
+    lens = np.array(group_lens(c), np.int32)
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    T = Pn + int(lens.sum())
     rng = np.random.default_rng(123 + rank)
     prompts = [rng.integers(4, c["vocab"], Pn).astype(np.int32) for _ in range(ng)]
-    resps = [rng.integers(4, c["vocab"], G * R).astype(np.int32) for _ in range(ng)]
+    resps = [rng.integers(4, c["vocab"], T - Pn).astype(np.int32) for _ in range(ng)]
     rewards = [rng.random(G) for _ in range(ng)]
-    lens = np.full(G, R, np.int32)
     group = P.Group(T, G, ctx)
 
     import torch
@@ -279,7 +318,7 @@ def run_ours(args, c):
         grads.reset()
         st = None
         for i in range(ng):
-            group.pack(h_prompts[i], [h_resps[i][k * R:(k + 1) * R] for k in range(G)], c["max_seq"])
+            group.pack(h_prompts[i], [h_resps[i][offs[k]:offs[k + 1]] for k in range(G)], c["max_seq"])
             st = P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=True)
         if world > 1:
             grads.allreduce()
@@ -355,7 +394,7 @@ def run_ours(args, c):
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": c["prec"], "data": "synthetic (random-init weights, uniform tokens in [4,V), U[0,1) rewards)",
         "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
-                               f"P={Pn} G={G} R={R} (T={T}) x {ng} groups per rank per step",
+                               f"P={Pn} G={G} R={c['R'] or lens.tolist()} (T={T}) x {ng} groups per rank per step",
                    "groups_per_rank": ng, "packed_tokens_per_group": T,
                    "l2": "working set (weights+activations, GBs) exceeds the 126 MB L2; no explicit flush",
                    "roofline_timing": "per-launch CUDA events over a second identical K-step region",
@@ -372,8 +411,8 @@ def run_ours(args, c):
                                if v["ms"] > 0 else None,
                                "unit": "TFLOP/s" if k in ("gemm", "head", "attn_fwd", "attn_bwd") else "GB/s"}
                            for k, v in prof.items()},
-        "flops_per_group": flops_per_group(c, Pn, [R] * G),
-        "model_tflops": flops_per_group(c, Pn, [R] * G) * ng * world / (step_ms / 1e3) / 1e12,
+        "flops_per_group": flops_per_group(c, Pn, lens.tolist()),
+        "model_tflops": flops_per_group(c, Pn, lens.tolist()) * ng * world / (step_ms / 1e3) / 1e12,
         "clocks": clk.summary(),
     }
     if cpu is not None:

@@ -95,6 +95,15 @@ parl_status parl_ctx_profile(parl_ctx_t ctx, int enable);
  * classes), launches = count; then resets the class. */
 parl_status parl_ctx_profile_read(parl_ctx_t ctx, int kernel_class, double* ms, double* work, long* launches);
 
+/* Activation recomputation of the policy forward (B200 memory policy, no
+ * reference counterpart): 0 = auto (keep every layer's activations when they
+ * fit in HBM next to the backward's workspaces, else keep only the residual
+ * stream and rebuild each layer in the backward), 1 = always, 2 = never.
+ * Results are bit-identical in all modes.  Default 0, or $PARL_RECOMPUTE. */
+parl_status parl_ctx_set_recompute(parl_ctx_t ctx, int mode);
+/* 1 if the activation handle was produced in recompute mode, else 0 */
+int parl_act_recompute(parl_act_t act);
+
 /* ---- models: ModelParams (model.hpp:64-106) ---------------------------- */
 parl_status parl_model_create(parl_ctx_t ctx, const parl_config* cfg, parl_model_t* out);
 parl_status parl_model_destroy(parl_model_t m);

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <queue>
@@ -143,6 +144,8 @@ struct parl_ctx_s {
         }
         prof_pending.clear();
     }
+    // activation recomputation: 0 auto (when the stacks do not fit), 1 always, 2 never
+    int recompute = 0;
     // activation handle reused by parl_train_microbatch (no per-call allocation)
     parl_act_s* act_cache = nullptr;
     // lifetime: objects created on this context keep it alive
@@ -192,7 +195,8 @@ struct parl_act_s {
     DevBuf xs, xmid, a, qkv, ctxo, bn, pre, actv, stats, lse_attn;  // per-layer stacks
     DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
     bool logits_bf16 = false;  // logits stored bf16 by the fused tcgen05 head
-    uintptr_t pad_sig[7] = {};  // buffers / sizes the bias columns were filled for
+    bool recompute = false;    // only x_0..x_L kept; layers (and bf16 logits) rebuilt in the backward
+    uintptr_t pad_sig[8] = {};  // buffers / sizes the bias columns were filled for
 };
 
 struct parl_grad_s {
@@ -332,6 +336,14 @@ void convert_tensor(parl_model_s* m, const TensorMap& t, const double* dsrc) {
     }
 }
 
+// compute copy of one tensor -> fp64 (flat reference layout)
+void export_tensor(parl_model_s* m, const TensorMap& t, double* stg, cudaStream_t st) {
+    if (!t.matrix) launch_export_w<float>(static_cast<float*>(t.dst), t.cols, t.rows, t.cols, 0, stg, st);
+    else if (m->ctx->prec == PARL_PREC_BF16)
+        launch_export_w<bf16>(static_cast<bf16*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
+    else launch_export_w<float>(static_cast<float*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
+}
+
 // Rebuild the compute copy from the device fp64 master.
 void convert_from_master(parl_model_s* m) {
     const double* base = static_cast<const double*>(m->master.p);
@@ -404,12 +416,167 @@ void gemm_multi(parl_ctx_s* c, const GemmArgs* gs, int n) {
     }
 }
 
+// Per-layer activation buffers of one model in a forward.  With `stack_layers`
+// every layer's tensors are kept for the backward; without it one layer's set is
+// reused (cache-less forwards, and the policy under activation recomputation,
+// where only the residual stream x_0..x_L is kept: `stack_x`).
+template <class T>
+struct FwdBufs {
+    bool stack_x = false, stack_layers = false;
+    float* xs = nullptr;    // residual stream: layer inputs x_0..x_L (stack) or ping-pong
+    float* xmid = nullptr;  // x_mid
+    T *a = nullptr, *qkv = nullptr, *ctxo = nullptr, *bn = nullptr, *pre = nullptr, *actv = nullptr;
+    float *stats = nullptr, *lse_attn = nullptr;
+    size_t lay(size_t per, int l) const { return stack_layers ? per * (size_t)l : 0; }
+    float* xin(size_t TD, int l) const { return xs + (stack_x ? TD * l : TD * (l & 1)); }
+};
+
+AttnArgs attn_args(parl_group_s* g, const parl_config& cf) {
+    AttnArgs aa;
+    aa.T = g->T; aa.H = cf.n_heads; aa.Dh = cf.d_model / cf.n_heads; aa.d = cf.d_model;
+    aa.seg = g->pk.seg;
+    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
+    aa.seg_end = aa.seg_start + (g->max_G + 1);
+    aa.scale = 1.0f / std::sqrt((float)aa.Dh);
+    aa.Peff = g->Peff;
+    aa.sched = g->sched;
+    aa.ldo = cf.d_model + PAD_COLS;
+    return aa;
+}
+
+// One decoder layer (model.cpp:458-516) for nm models at once (grouped GEMMs).
+// `recompute`: rebuild the layer's activations for the backward; the W2 GEMM
+// (whose output x_{l+1} is already kept) is skipped.
+template <class T>
+void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs<T>* B, int l, parl_group_s* g,
+                   const AttnArgs& aa, bool recompute) {
+    cudaStream_t st = c->st;
+    const auto& cf = ms[0]->cfg;
+    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, F = cf.d_ff;
+    const size_t TD = (size_t)Tn * D;
+    const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
+    const size_t TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
+    GemmArgs gs[3];
+    {
+        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+        for (int k = 0; k < nm; ++k) {
+            const FwdBufs<T>& b = B[k];
+            float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
+            launch_layernorm<T>(b.xin(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln1_g, ms[k]->layers[l].ln1_b,
+                                b.a + b.lay(TDp, l), Dp, st4, st4 + Tn, st);
+        }
+    }
+    for (int k = 0; k < nm; ++k) {  // fused Q|K|V projection (model.cpp:464-466)
+        const FwdBufs<T>& b = B[k];
+        const LayerW& w = ms[k]->layers[l];
+        gs[k] = mk(Tn, 3 * D, D, b.a + b.lay(TDp, l), Dp, 1, w.wqkv_t, D, 1);
+        gs[k].epi = EPI_ACT; gs[k].bias = w.bqkv; gs[k].Ca = b.qkv + b.lay(3 * TD, l); gs[k].ldca = 3 * D;
+    }
+    gemm_multi<T>(c, gs, nm);
+    {
+        ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D * nm);
+        for (int k = 0; k < nm; ++k) {
+            const FwdBufs<T>& b = B[k];
+            T* ql = b.qkv + b.lay(3 * TD, l);
+            T* cl = b.ctxo + b.lay(TDp, l);
+            float* la = b.lse_attn + b.lay((size_t)H * Tn, l);
+            bool done = false;
+            if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
+            if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
+        }
+    }
+    for (int k = 0; k < nm; ++k) {  // O projection + residual (model.cpp:504-506)
+        const FwdBufs<T>& b = B[k];
+        const LayerW& w = ms[k]->layers[l];
+        gs[k] = mk(Tn, D, D, b.ctxo + b.lay(TDp, l), Dp, 1, w.wo_t, D, 1);
+        gs[k].epi = EPI_RESID; gs[k].bias = w.bo; gs[k].resid = b.xin(TD, l);
+        gs[k].Cf = b.xmid + b.lay(TD, l); gs[k].ldc = D;
+    }
+    gemm_multi<T>(c, gs, nm);
+    {
+        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+        for (int k = 0; k < nm; ++k) {
+            const FwdBufs<T>& b = B[k];
+            float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
+            launch_layernorm<T>(b.xmid + b.lay(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln2_g, ms[k]->layers[l].ln2_b,
+                                b.bn + b.lay(TDp, l), Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
+        }
+    }
+    for (int k = 0; k < nm; ++k) {  // W1 + bias + GELU (model.cpp:509-511)
+        const FwdBufs<T>& b = B[k];
+        const LayerW& w = ms[k]->layers[l];
+        gs[k] = mk(Tn, F, D, b.bn + b.lay(TDp, l), Dp, 1, w.w1_t, D, 1);
+        gs[k].bias = w.b1; gs[k].ldca = Fp;
+        if (b.pre) {  // the backward needs the pre-activation u (GELU') and the activation
+            gs[k].epi = EPI_GELU; gs[k].Ca = b.pre + b.lay(TFp, l); gs[k].Caux = b.actv + b.lay(TFp, l);
+        } else {
+            gs[k].epi = EPI_GELU_ACT; gs[k].Ca = b.actv;
+        }
+    }
+    gemm_multi<T>(c, gs, nm);
+    if (recompute) return;
+    for (int k = 0; k < nm; ++k) {  // W2 + bias + residual (model.cpp:513-515)
+        const FwdBufs<T>& b = B[k];
+        const LayerW& w = ms[k]->layers[l];
+        gs[k] = mk(Tn, D, F, b.actv + b.lay(TFp, l), Fp, 1, w.w2_t, F, 1);
+        gs[k].epi = EPI_RESID; gs[k].bias = w.b2; gs[k].resid = b.xmid + b.lay(TD, l);
+        gs[k].Cf = b.xin(TD, l + 1); gs[k].ldc = D;
+    }
+    gemm_multi<T>(c, gs, nm);
+}
+
+// Bytes of the per-layer activation stacks (all layers) and of the backward's
+// workspaces, for the recompute decision.
+size_t layer_act_bytes(const parl_config& cf, int Tn, size_t es) {
+    const size_t D = cf.d_model, F = cf.d_ff, H = cf.n_heads, Dp = D + PAD_COLS, Fp = F + PAD_COLS;
+    return (size_t)Tn * (4 * D + es * (3 * Dp + 3 * D + 2 * Fp) + 16 + 4 * H);
+}
+
+// Activation recomputation (c->recompute: 0 auto, 1 always, 2 never).  Auto keeps
+// every layer's activations when they fit next to the backward's workspaces;
+// otherwise only the residual stream is kept and each layer is rebuilt in the
+// backward (C3 / C4 sizes: 150-280 GB of stacks).
+template <class T>
+bool want_recompute(parl_ctx_s* c, parl_act_s* act, const parl_config& cf, int Tn, int S) {
+    if (c->recompute == 1) return true;
+    if (c->recompute == 2) return false;
+    const size_t es = sizeof(T), D = cf.d_model, F = cf.d_ff, V = cf.vocab_size, H = cf.n_heads;
+    const size_t stacks = layer_act_bytes(cf, Tn, es) * cf.n_layers + (size_t)S * V * es;
+    const size_t held = act->xmid.bytes + act->a.bytes + act->qkv.bytes + act->ctxo.bytes + act->bn.bytes +
+                        act->pre.bytes + act->actv.bytes + act->stats.bytes + act->lse_attn.bytes + act->logits.bytes;
+    const size_t TD = (size_t)Tn * D;
+    const size_t ws = (size_t)S * V * es + (size_t)Tn * (F + PAD_COLS) * es + 5 * TD * 4 + 6 * TD * es +
+                      H * Tn * 4 + 2 * (size_t)S * D * 4;
+    const size_t ws_held = c->dz.bytes + c->dpre.bytes + c->dx.bytes + c->dx2.bytes + c->dbn.bytes + c->dmid.bytes +
+                           c->da.bytes + c->dx_act.bytes + c->dmid_act.bytes + c->dctx.bytes + c->dqkv.bytes +
+                           c->dsum.bytes + c->dhf.bytes + c->dxg.bytes;
+    size_t free_b = 0, total_b = 0;
+    PARL_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t avail = free_b + held, need = stacks + (ws > ws_held ? ws - ws_held : 0) + ((size_t)3 << 30);
+    return need > avail;
+}
+
+// LM head with the fused vocab log-sum-exp / target gather epilogue (bf16 path);
+// `logits`: where the bf16 logits go (the policy's backward), or null
+GemmArgs head_lse_args(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, const bf16* hf, bf16* logits) {
+    const int S = g->S, V = m->cfg.vocab_size, D = m->cfg.d_model;
+    const int n_parts = (V + 127) / 128;
+    GemmArgs ga = mk(S, V, D, hf, D + PAD_COLS, 1, m->W.head_w_t, D, 1);
+    ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
+    ga.part = c->part.as<float>((size_t)S * n_parts * 2);
+    ga.target = c->target.as<float>(S);
+    ga.n_parts = n_parts; ga.part_cols = 128;
+    ga.logits_act = logits;
+    ga.ldca = V;
+    return ga;
+}
+
 template <class T>
 void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int nm, parl_group_s* g,
                   parl_act_s* act, bool full_logits = false) {
     cudaStream_t st = c->st;
     const auto& cf = ms[0]->cfg;
-    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
+    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, F = cf.d_ff, V = cf.vocab_size, S = g->S;
     const int NL = cf.n_layers;
     const size_t TD = (size_t)Tn * D;
     // GEMM-operand activations carry PAD extra columns: column D (F) is 1.0 so the
@@ -418,29 +585,25 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
     const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
     const size_t TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
 
-    struct Bufs {
-        bool keep;     // per-layer stacks kept for the backward
-        float* xs;     // residual stream: layer inputs x_0..x_L (stack) or ping-pong
-        float* xmid;   // per-layer x_mid
-        T *a, *qkv, *ctxo, *bn, *pre, *actv;
-        float *stats, *lse_attn;
-        size_t lay(size_t per, int l) const { return keep ? per * (size_t)l : 0; }
-    };
-    Bufs B[3];
-    for (int k = 0; k < nm; ++k) {
-        Bufs& b = B[k];
-        b.keep = k == 0 && act;
-        if (b.keep) {
+    FwdBufs<T> B[3];
+    for (int k = nm - 1; k >= 0; --k) {  // the policy's (k = 0) last: its recompute decision sees the rest
+        FwdBufs<T>& b = B[k];
+        if (k == 0 && act) {
+            const bool rc = want_recompute<T>(c, act, cf, Tn, S);
+            const int nl = rc ? 1 : NL;
+            act->recompute = rc;
+            b.stack_x = true;
+            b.stack_layers = !rc;
             b.xs = act->xs.as<float>(TD * (NL + 1));
-            b.xmid = act->xmid.as<float>(TD * NL);
-            b.a = act->a.as<T>(TDp * NL);
-            b.qkv = act->qkv.as<T>(3 * TD * NL);
-            b.ctxo = act->ctxo.as<T>(TDp * NL);
-            b.bn = act->bn.as<T>(TDp * NL);
-            b.pre = act->pre.as<T>(TFp * NL);
-            b.actv = act->actv.as<T>(TFp * NL);
-            b.stats = act->stats.as<float>((size_t)4 * Tn * NL);
-            b.lse_attn = act->lse_attn.as<float>((size_t)H * Tn * NL);
+            b.xmid = act->xmid.as<float>(TD * nl);
+            b.a = act->a.as<T>(TDp * nl);
+            b.qkv = act->qkv.as<T>(3 * TD * nl);
+            b.ctxo = act->ctxo.as<T>(TDp * nl);
+            b.bn = act->bn.as<T>(TDp * nl);
+            b.pre = rc ? nullptr : act->pre.as<T>(TFp * nl);
+            b.actv = act->actv.as<T>(TFp * nl);
+            b.stats = act->stats.as<float>((size_t)4 * Tn * nl);
+            b.lse_attn = act->lse_attn.as<float>((size_t)H * Tn * nl);
         } else {
             auto& r = c->scr[slots[k]];
             b.xs = r.x.as<float>(TD * 2);
@@ -455,109 +618,33 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
             b.lse_attn = r.lse_attn.as<float>((size_t)H * Tn);
         }
     }
-    auto xin_of = [&](const Bufs& b, int l) { return b.xs + (b.keep ? TD * l : TD * (l & 1)); };
 
     if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
-    AttnArgs aa;
-    aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
-    aa.seg = g->pk.seg;
-    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
-    aa.seg_end = aa.seg_start + (g->max_G + 1);
-    aa.scale = 1.0f / std::sqrt((float)Dh);
-    aa.Peff = g->Peff;
-    aa.sched = g->sched;
-    aa.ldo = Dp;
-
+    const AttnArgs aa = attn_args(g, cf);
     {
         ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12 * nm);
         for (int k = 0; k < nm; ++k)
-            launch_embed(ms[k]->W.tok_emb, ms[k]->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, xin_of(B[k], 0),
+            launch_embed(ms[k]->W.tok_emb, ms[k]->W.pos_emb, g->pk.tokens, g->pk.positions, Tn, D, B[k].xin(TD, 0),
                          st);
     }
-    GemmArgs gs[3];
-    for (int l = 0; l < NL; ++l) {
-        {
-            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
-            for (int k = 0; k < nm; ++k) {
-                const Bufs& b = B[k];
-                float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
-                launch_layernorm<T>(xin_of(b, l), nullptr, Tn, D, ms[k]->layers[l].ln1_g, ms[k]->layers[l].ln1_b,
-                                    b.a + b.lay(TDp, l), Dp, st4, st4 + Tn, st);
-            }
-        }
-        for (int k = 0; k < nm; ++k) {  // fused Q|K|V projection (model.cpp:464-466)
-            const Bufs& b = B[k];
-            const LayerW& w = ms[k]->layers[l];
-            gs[k] = mk(Tn, 3 * D, D, b.a + b.lay(TDp, l), Dp, 1, w.wqkv_t, D, 1);
-            gs[k].epi = EPI_ACT; gs[k].bias = w.bqkv; gs[k].Ca = b.qkv + b.lay(3 * TD, l); gs[k].ldca = 3 * D;
-        }
-        gemm_multi<T>(c, gs, nm);
-        {
-            ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D * nm);
-            for (int k = 0; k < nm; ++k) {
-                const Bufs& b = B[k];
-                T* ql = b.qkv + b.lay(3 * TD, l);
-                T* cl = b.ctxo + b.lay(TDp, l);
-                float* la = b.lse_attn + b.lay((size_t)H * Tn, l);
-                bool done = false;
-                if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
-                if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
-            }
-        }
-        for (int k = 0; k < nm; ++k) {  // O projection + residual (model.cpp:504-506)
-            const Bufs& b = B[k];
-            const LayerW& w = ms[k]->layers[l];
-            gs[k] = mk(Tn, D, D, b.ctxo + b.lay(TDp, l), Dp, 1, w.wo_t, D, 1);
-            gs[k].epi = EPI_RESID; gs[k].bias = w.bo; gs[k].resid = xin_of(b, l);
-            gs[k].Cf = b.xmid + b.lay(TD, l); gs[k].ldc = D;
-        }
-        gemm_multi<T>(c, gs, nm);
-        {
-            ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
-            for (int k = 0; k < nm; ++k) {
-                const Bufs& b = B[k];
-                float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
-                launch_layernorm<T>(b.xmid + b.lay(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln2_g,
-                                    ms[k]->layers[l].ln2_b, b.bn + b.lay(TDp, l), Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
-            }
-        }
-        for (int k = 0; k < nm; ++k) {  // W1 + bias + GELU (model.cpp:509-511)
-            const Bufs& b = B[k];
-            const LayerW& w = ms[k]->layers[l];
-            gs[k] = mk(Tn, F, D, b.bn + b.lay(TDp, l), Dp, 1, w.w1_t, D, 1);
-            gs[k].bias = w.b1; gs[k].ldca = Fp;
-            if (b.keep) {  // the backward needs the pre-activation u (GELU') and the activation
-                gs[k].epi = EPI_GELU; gs[k].Ca = b.pre + b.lay(TFp, l); gs[k].Caux = b.actv + b.lay(TFp, l);
-            } else {
-                gs[k].epi = EPI_GELU_ACT; gs[k].Ca = b.actv;
-            }
-        }
-        gemm_multi<T>(c, gs, nm);
-        for (int k = 0; k < nm; ++k) {  // W2 + bias + residual (model.cpp:513-515)
-            const Bufs& b = B[k];
-            const LayerW& w = ms[k]->layers[l];
-            gs[k] = mk(Tn, D, F, b.actv + b.lay(TFp, l), Fp, 1, w.w2_t, F, 1);
-            gs[k].epi = EPI_RESID; gs[k].bias = w.b2; gs[k].resid = b.xmid + b.lay(TD, l);
-            gs[k].Cf = xin_of(b, l + 1); gs[k].ldc = D;
-        }
-        gemm_multi<T>(c, gs, nm);
-    }
+    for (int l = 0; l < NL; ++l) layer_forward<T>(c, ms, nm, B, l, g, aa, false);
     // final LN + head only on the scored tokens' predecessor rows (model.cpp:518-556)
     for (int k = 0; k < nm; ++k) {
-        const Bufs& b = B[k];
+        const FwdBufs<T>& b = B[k];
         parl_model_s* m = ms[k];
-        parl_act_s* ak = b.keep ? act : nullptr;
+        parl_act_s* ak = (k == 0) ? act : nullptr;
         auto& r = c->scr[slots[k]];
-        float* xfin = xin_of(b, NL);
+        float* xfin = b.xin(TD, NL);
         T* hf = ak ? ak->hf.as<T>((size_t)S * Dp) : r.hf.as<T>((size_t)S * Dp);
         if (ak) {  // bias columns of the weight-gradient operands (refilled when the buffers move)
-            const uintptr_t sig[7] = {(uintptr_t)b.a, (uintptr_t)b.ctxo, (uintptr_t)b.bn, (uintptr_t)b.actv,
-                                      (uintptr_t)hf, (uintptr_t)Tn, (uintptr_t)S};
+            const long rows = (long)Tn * (b.stack_layers ? NL : 1);
+            const uintptr_t sig[8] = {(uintptr_t)b.a, (uintptr_t)b.ctxo, (uintptr_t)b.bn, (uintptr_t)b.actv,
+                                      (uintptr_t)hf, (uintptr_t)Tn, (uintptr_t)S, (uintptr_t)rows};
             if (std::memcmp(sig, ak->pad_sig, sizeof(sig)) != 0) {
-                launch_fill_pad<T>(b.a, (long)Tn * NL, D, Dp, st);
-                launch_fill_pad<T>(b.ctxo, (long)Tn * NL, D, Dp, st);
-                launch_fill_pad<T>(b.bn, (long)Tn * NL, D, Dp, st);
-                launch_fill_pad<T>(b.actv, (long)Tn * NL, F, Fp, st);
+                launch_fill_pad<T>(b.a, rows, D, Dp, st);
+                launch_fill_pad<T>(b.ctxo, rows, D, Dp, st);
+                launch_fill_pad<T>(b.bn, rows, D, Dp, st);
+                launch_fill_pad<T>(b.actv, rows, F, Fp, st);
                 launch_fill_pad<T>(hf, (long)S, D, Dp, st);
                 std::memcpy(ak->pad_sig, sig, sizeof(sig));
             }
@@ -569,22 +656,16 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
         if (S > 0) {
             launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, Dp, lnf_mean, lnf_rstd, st);
             bool fused = false;
-            if (std::is_same_v<T, bf16> && !full_logits) {
+            if constexpr (std::is_same_v<T, bf16>) if (!full_logits) {
                 // tcgen05 head with the vocab log-sum-exp and target gather fused
                 // into the epilogue: logits reach HBM only for the policy (bf16,
-                // kept for the backward), never for old/ref.
-                const int n_parts = (V + 127) / 128;
-                GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
-                ga.epi = EPI_LSE; ga.bias = m->W.head_b; ga.labels = g->pk.scored_label;
-                ga.part = c->part.as<float>((size_t)S * n_parts * 2);
-                ga.target = c->target.as<float>(S);
-                ga.n_parts = n_parts; ga.part_cols = 128;
-                ga.logits_act = ak ? ak->logits.as<bf16>((size_t)S * V) : nullptr;
-                ga.ldca = V;
+                // kept for the backward unless it recomputes them), never for old/ref.
+                bf16* keep = (ak && !ak->recompute) ? ak->logits.as<bf16>((size_t)S * V) : nullptr;
+                GemmArgs ga = head_lse_args(c, m, g, hf, keep);
                 {
                     ProfScope ps(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
                     fused = gemm_tc(ga, st);
-                    if (fused) launch_lse_combine(ga.part, n_parts, ga.target, S, lse_head, lp, st);
+                    if (fused) launch_lse_combine(ga.part, ga.n_parts, ga.target, S, lse_head, lp, st);
                 }
             }
             if (!fused) {
@@ -605,7 +686,7 @@ template <class T>
 void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s* g, parl_grad_s* gr) {
     cudaStream_t st = c->st;
     const auto& cf = m->cfg;
-    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, Dh = D / H, F = cf.d_ff, V = cf.vocab_size, S = g->S;
+    const int Tn = g->T, D = cf.d_model, H = cf.n_heads, F = cf.d_ff, V = cf.vocab_size, S = g->S;
     const int NL = cf.n_layers;
     const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
     const size_t TD = (size_t)Tn * D, TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
@@ -620,7 +701,16 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         T* dz = c->dz.as<T>((size_t)S * V);
         {
             ProfScope ps_sm(c, PARL_KC_HEAD, 4.0 * S * (double)V);
-            if (act->logits_bf16)
+            if (act->logits_bf16 && act->recompute) {
+                if constexpr (std::is_same_v<T, bf16>) {
+                    // logits were not kept: the same head GEMM rebuilds them (bit-identical)
+                    // into dZ, which the softmax backward then overwrites in place
+                    GemmArgs ga = head_lse_args(c, m, g, static_cast<const bf16*>(act->hf.p), dz);
+                    PARL_REQUIRE(gemm_tc(ga, st), PARL_E_CUDA, "head recompute: tcgen05 GEMM unavailable");
+                    launch_softmax_bwd<bf16, T>(dz, V, dz, V, S, V, static_cast<float*>(act->lse_head.p), u,
+                                                g->pk.scored_label, st);
+                }
+            } else if (act->logits_bf16)
                 launch_softmax_bwd<bf16, T>(static_cast<bf16*>(act->logits.p), V, dz, V, S, V,
                                             static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
             else
@@ -666,15 +756,22 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     float* dx2 = c->dx2.as<float>(TD);
 
     if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
-    AttnArgs aa;
-    aa.T = Tn; aa.H = H; aa.Dh = Dh; aa.d = D;
-    aa.seg = g->pk.seg;
-    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
-    aa.seg_end = aa.seg_start + (g->max_G + 1);
-    aa.scale = 1.0f / std::sqrt((float)Dh);
-    aa.Peff = g->Peff;
-    aa.sched = g->sched;
-    aa.ldo = Dp;
+    const AttnArgs aa = attn_args(g, cf);
+    // recompute mode: one layer's activation set, rebuilt from x_l before its backward
+    const bool rc = act->recompute;
+    FwdBufs<T> RB;
+    RB.stack_x = true;
+    RB.xs = static_cast<float*>(act->xs.p);
+    RB.xmid = static_cast<float*>(act->xmid.p);
+    RB.a = static_cast<T*>(act->a.p);
+    RB.qkv = static_cast<T*>(act->qkv.p);
+    RB.ctxo = static_cast<T*>(act->ctxo.p);
+    RB.bn = static_cast<T*>(act->bn.p);
+    RB.pre = rc ? act->pre.as<T>(TFp) : static_cast<T*>(act->pre.p);
+    RB.actv = static_cast<T*>(act->actv.p);
+    RB.stats = static_cast<float*>(act->stats.p);
+    RB.lse_attn = static_cast<float*>(act->lse_attn.p);
+    const int ll = rc ? 0 : 1;  // layer stride multiplier of the stacks
 
     // weight-gradient GEMMs of a layer are collected and run as one grouped launch
     // (bf16); the fp32 path runs them as they come
@@ -699,16 +796,18 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     for (int l = NL - 1; l >= 0; --l) {
         const LayerW& w = m->layers[l];
         const auto o = L.layer(l, D, F);
-        float* xin = static_cast<float*>(act->xs.p) + TD * l;
-        float* xm = static_cast<float*>(act->xmid.p) + TD * l;
-        T* al = static_cast<T*>(act->a.p) + TDp * l;
-        T* ql = static_cast<T*>(act->qkv.p) + 3 * TD * l;
-        T* cl = static_cast<T*>(act->ctxo.p) + TDp * l;
-        T* bl = static_cast<T*>(act->bn.p) + TDp * l;
-        T* pl = static_cast<T*>(act->pre.p) + TFp * l;
-        T* vl = static_cast<T*>(act->actv.p) + TFp * l;
-        float* st4 = static_cast<float*>(act->stats.p) + (size_t)4 * Tn * l;
-        float* la = static_cast<float*>(act->lse_attn.p) + (size_t)H * Tn * l;
+        if (rc) layer_forward<T>(c, &m, 1, &RB, l, g, aa, true);
+        const int li = l * ll;
+        float* xin = RB.xs + TD * l;
+        float* xm = RB.xmid + TD * li;
+        T* al = RB.a + TDp * li;
+        T* ql = RB.qkv + 3 * TD * li;
+        T* cl = RB.ctxo + TDp * li;
+        T* bl = RB.bn + TDp * li;
+        T* pl = RB.pre + TFp * li;
+        T* vl = RB.actv + TFp * li;
+        float* st4 = RB.stats + (size_t)4 * Tn * li;
+        float* la = RB.lse_attn + (size_t)H * Tn * li;
 
         // FFN (model.cpp:688-727); dx_act holds the compute-dtype copy of dx
         {
@@ -1038,6 +1137,8 @@ parl_status parl_ctx_create(int device, parl_precision prec, parl_ctx_t* out) {
         PARL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
         double* s = c->stats.as<double>(8);
         PARL_CUDA(cudaMemsetAsync(s, 0, 8 * sizeof(double), c->st));
+        if (const char* e = std::getenv("PARL_RECOMPUTE")) c->recompute = std::atoi(e);
+        PARL_REQUIRE(c->recompute >= 0 && c->recompute <= 2, PARL_E_CONFIG, "PARL_RECOMPUTE must be 0, 1 or 2");
         *out = c.release();
     });
 }
@@ -1219,8 +1320,21 @@ parl_status parl_model_copy(parl_model_t dst, parl_model_t src, uint64_t seed, d
                 PARL_CUDA(cudaMemcpyAsync(dst->master.p, src->master.p, dst->L.total * sizeof(double),
                                           cudaMemcpyDeviceToDevice, st));
             convert_from_master(dst);
+        } else if (scale != 0.0) {
+            // no fp64 master (large models): perturb tensor by tensor through the fp64 staging
+            // buffer, from the source's compute copy
+            const auto ts = tensor_maps(src), td = tensor_maps(dst);
+            uint32_t stream = 0xC0FFEEu;
+            for (size_t i = 0; i < ts.size(); ++i) {
+                const auto& t = ts[i];
+                const size_t cnt = (size_t)t.rows * t.cols;
+                double* stg = dst->ctx->staging.as<double>(cnt);
+                export_tensor(src, t, stg, st);
+                launch_randn(stg, (long)cnt, seed, stream++, scale, stg, st);
+                convert_tensor(dst, td[i], stg);
+            }
+            check_launch();
         } else {
-            PARL_REQUIRE(scale == 0.0, PARL_E_CONFIG, "perturbed copy needs an fp64 master copy");
             PARL_CUDA(cudaMemcpyAsync(dst->f32.p, src->f32.p, src->f32.bytes, cudaMemcpyDeviceToDevice, st));
             PARL_CUDA(cudaMemcpyAsync(dst->act.p, src->act.p, src->act.bytes, cudaMemcpyDeviceToDevice, st));
         }
@@ -1239,10 +1353,7 @@ parl_status parl_model_download(parl_model_t m, double* flat, size_t n) {
             for (const auto& t : tensor_maps(m)) {
                 const size_t cnt = (size_t)t.rows * t.cols;
                 double* stg = m->ctx->staging.as<double>(cnt);
-                if (!t.matrix) launch_export_w<float>(static_cast<float*>(t.dst), t.cols, t.rows, t.cols, 0, stg, st);
-                else if (m->ctx->prec == PARL_PREC_BF16)
-                    launch_export_w<bf16>(static_cast<bf16*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
-                else launch_export_w<float>(static_cast<float*>(t.dst), t.ldd, t.rows, t.cols, 1, stg, st);
+                export_tensor(m, t, stg, st);
                 PARL_CUDA(cudaMemcpyAsync(flat + t.src_off, stg, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
                 PARL_CUDA(cudaStreamSynchronize(st));
             }
@@ -1542,6 +1653,15 @@ parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, do
             for (int v = 0; v < V; ++v) rows[(size_t)t * V + v] = (double)z[(size_t)t * V + v] - (double)lse[t];
     });
 }
+
+parl_status parl_ctx_set_recompute(parl_ctx_t ctx, int mode) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(mode >= 0 && mode <= 2, PARL_E_CONFIG, "recompute mode must be 0, 1 or 2");
+        ctx->recompute = mode;
+    });
+}
+
+int parl_act_recompute(parl_act_t a) { return a && a->recompute ? 1 : 0; }
 
 parl_status parl_act_destroy(parl_act_t a) {
     delete a;

@@ -313,19 +313,20 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // ===========================================================================
-// Forward, two query tiles per CTA (Dh = 64).  Work item = (pair of adjacent
+// Forward, two query tiles per CTA (Dh = 64 / 128).  Work item = (pair of adjacent
 // 128-row query tiles, head); the pair's key tiles are the union of both
 // tiles' visible lists, flagged per tile (visible / full).  Roles:
 //   warps 0-3  softmax of query tile 0, warps 4-7 softmax of query tile 1
 //              (thread = query row; two warps per SM sub-partition so the
 //              exp/max/pack stream of one tile overlaps the other's)
-//   warp 8     TMA: Q pair (double-buffered across items), K/V 3-stage ring
+//   warp 8     TMA: Q pair (double-buffered across items at Dh = 64), K/V ring (3 / 2 stages)
 //   warps 9,10 MMA, one issuer per query tile: S_w = Q_w K^T (TMEM, one buffer per tile, re-issued as soon
 //              as the softmax has pulled the previous S into registers), then
 //              O_w += P_w V with P_w read from TMEM (tcgen05 "TS" form)
 //   setmaxnreg moves registers from the TMA/MMA group to the softmax groups so
 //   a whole 128-key score row stays in registers.
-// TMEM: S0 | S1 | O0 | O1 | P0 | P1  (128 | 128 | 64 | 64 | 64 | 64 columns).
+// TMEM: S0 | S1 | O0 | O1 | P0 | P1  (128 | 128 | 64 | 64 | 64 | 64 columns) at Dh = 64;
+// S0 | S1 | O0 | O1 (128 each, P_w over S_w) at Dh = 128.
 struct AttnPairArgs {
     int T, H, d, Peff, grid;
     const int32_t* seg;
@@ -345,10 +346,12 @@ constexpr uint32_t VIS0 = 1u << 24, FULL0 = 1u << 25, VIS1 = 1u << 26, FULL1 = 1
 template <int DH>
 struct PairSmem {
     static constexpr int TILE = 128 * DH * 2;
-    static constexpr int OFF_Q = 0;                          // [2 buffers][2 tiles]
-    static constexpr int OFF_K = OFF_Q + 4 * TILE;           // [KV_STAGES]
-    static constexpr int OFF_V = OFF_K + KV_STAGES * TILE;   // [KV_STAGES]
-    static constexpr int OFF_BAR = OFF_V + KV_STAGES * TILE;
+    static constexpr int QB = DH == 128 ? 1 : 2;             // Q pair buffers (across items)
+    static constexpr int KVS = DH == 128 ? 2 : KV_STAGES;    // K/V ring stages
+    static constexpr int OFF_Q = 0;                          // [QB buffers][2 tiles]
+    static constexpr int OFF_K = OFF_Q + 2 * QB * TILE;      // [KVS]
+    static constexpr int OFF_V = OFF_K + KVS * TILE;         // [KVS]
+    static constexpr int OFF_BAR = OFF_V + KVS * TILE;
     static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
@@ -370,8 +373,13 @@ __device__ unsigned long long g_attn_trace[16][64][8];
 template <int DH>
 __global__ void __launch_bounds__(PAIR_NTHR, 1)
     k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, AttnPairArgs a) {
-    static_assert(DH == 64, "TMEM budget: 2 x (S 128 + O DH + P 64) <= 512");
+    static_assert(DH == 64 || DH == 128, "head dim");
     using L = PairSmem<DH>;
+    // TMEM: Dh = 64: S0 | S1 | O0 | O1 | P0 | P1; Dh = 128: S0 | S1 | O0 | O1 with P_w written
+    // over S_w (the S of a tile's next key tile is then issued only behind its PV, which the
+    // tensor pipe executes in issue order)
+    constexpr bool P_IN_S = DH == 128;
+    constexpr int KVS = L::KVS, QB = L::QB, PCOL = P_IN_S ? 128 : 64;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
@@ -399,7 +407,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             tc::mbar_init(&o_done[s], 1);
             tc::mbar_init(&o_free[s], 4);
         }
-        for (int s = 0; s < KV_STAGES; ++s) {
+        for (int s = 0; s < KVS; ++s) {
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 2);
         }
@@ -411,7 +419,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
-    const uint32_t t_s = tbase, t_o = tbase + 256, t_p = tbase + 256 + 2 * DH;
+    const uint32_t t_s = tbase, t_o = tbase + 256, t_p = P_IN_S ? tbase : tbase + 256 + 2 * DH;
     pdl_wait();
     pdl_trigger();
 
@@ -422,8 +430,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             int g = 0, li = 0;
             for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k, ++li) {
                 const int it = a.w_items[k];
-                const int p = it / H, h = it % H, qb = li & 1;
-                tc::mbar_wait(&q_empty[qb], ((li >> 1) & 1) ^ 1);
+                const int p = it / H, h = it % H, qb = li % QB;
+                tc::mbar_wait(&q_empty[qb], ((li / QB) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[qb], 2 * L::TILE);
 #pragma unroll
                 for (int w = 0; w < 2; ++w)
@@ -433,8 +441,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                                         h * DH + r * 64, (2 * p + w) * 128);
                 for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e, ++g) {
                     const int j0 = (a.p_list[e] & 0xffffff) * 128;
-                    const int st = g % KV_STAGES;
-                    tc::mbar_wait(&kv_empty[st], ((g / KV_STAGES) & 1) ^ 1);
+                    const int st = g % KVS;
+                    tc::mbar_wait(&kv_empty[st], ((g / KVS) & 1) ^ 1);
                     tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
 #pragma unroll
                     for (int r = 0; r < DH / 64; ++r) {
@@ -485,9 +493,9 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         };
         s_load_item();
         auto issue_s = [&]() {  // S for the iterator's entry (visible, gS)
-            const int g = gS, st = g % KV_STAGES, qb = s_li & 1;
-            tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
-            tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
+            const int g = gS, st = g % KVS, qb = s_li % QB;
+            tc::mbar_wait(&q_full[qb], (s_li / QB) & 1);
+            tc::mbar_wait(&kv_full[st], (g / KVS) & 1);
             if (cS > 0) tc::mbar_wait(&s_free[w], (cS - 1) & 1);
             tc::tc_fence_after();
             const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
@@ -505,20 +513,23 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             ++gS;
         };
         // issue pending S (at most one beyond the tile being processed) within the stage window
-        auto advance_s = [&](int g_now) {
-            while (cS < cP + 2 && s_seek() && gS <= g_now + KV_STAGES - 1) issue_s();
+        // (and at most QB - 1 items ahead: the Q buffer of a later item is freed by this
+        // issuer's own end-of-item release)
+        auto advance_s = [&](int g_now, int li_now) {
+            while (cS < cP + (P_IN_S ? 1 : 2) && s_seek() && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1)
+                issue_s();
         };
         int g = 0, li = 0;
         for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
-            const int p = a.w_items[k] / H, qb = li & 1;
+            const int p = a.w_items[k] / H, qb = li % QB;
             const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
             bool started = false;
             for (int e = ea; e < eb; ++e, ++g) {
                 const uint32_t f = (uint32_t)a.p_list[e];
-                const int st = g % KV_STAGES;
-                advance_s(g);  // S of this entry (if not yet issued) and of the next visible one
+                const int st = g % KVS;
+                advance_s(g, li);  // S of this entry (if not yet issued) and of the next visible one
                 if (!(f & VIS)) {  // not ours: release the stage once it holds this entry
-                    tc::mbar_wait(&kv_full[st], (g / KV_STAGES) & 1);
+                    tc::mbar_wait(&kv_full[st], (g / KVS) & 1);
                     if (lane == 0) tc::mbar_arrive(&kv_empty[st]);
                     continue;
                 }
@@ -530,7 +541,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks)
-                    tc::mma_bf16_ts_e(t_o + w * DH, t_p + w * 64 + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
+                    tc::mma_bf16_ts_e(t_o + w * DH, t_p + w * PCOL + ks * 8, tc::sdesc(sv + ks * 2048, 128 * 128, 1024),
                                       id_o, (started || ks > 0) ? 1u : 0u);
                 tc::mma_commit_e(&o_done[w]);
                 tc::mma_commit_e(&kv_empty[st]);
@@ -539,12 +550,12 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     started = true;
                     ++nI;
                 }
-                advance_s(g);  // look ahead right after handing this PV off
+                advance_s(g, li);  // look ahead right after handing this PV off
             }
             if (started) {
                 tc::mma_commit_e(&q_empty[qb]);
             } else {
-                tc::mbar_wait(&q_full[qb], (li >> 1) & 1);
+                tc::mbar_wait(&q_full[qb], (li / QB) & 1);
                 if (lane == 0) tc::mbar_arrive(&q_empty[qb]);
             }
         }
@@ -639,7 +650,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tc::tmem_st16(t_p + w * 64 + c * 16 + lane_off, pk + 16 * c);
+                for (int c = 0; c < 4; ++c) tc::tmem_st16(t_p + w * PCOL + c * 16 + lane_off, pk + 16 * c);
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
                 __syncwarp();
@@ -654,28 +665,34 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             // item epilogue: O / l -> out (bf16), lse; then release O to the next item
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
-            float o[DH];
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            bf16* dst = a.out + (long)i * a.ldo + h * DH;
 #pragma unroll
-            for (int c = 0; c < DH / 32; ++c) tc::tmem_ld32_nowait(t_o + w * DH + c * 32 + lane_off,
-                                                                   reinterpret_cast<uint32_t*>(o) + 32 * c);
-            tc::tmem_ld_wait();
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&o_free[w]);
-            if (row_ok) {
-                const float inv = l > 0.f ? 1.f / l : 0.f;
-                bf16* dst = a.out + (long)i * a.ldo + h * DH;
+            for (int hc = 0; hc < DH / 64; ++hc) {  // 64 columns at a time (register pressure)
+                float o[64];
 #pragma unroll
-                for (int q = 0; q < DH; q += 8) {
-                    uint4 v4;
-                    v4.x = pack2(o[q] * inv, o[q + 1] * inv);
-                    v4.y = pack2(o[q + 2] * inv, o[q + 3] * inv);
-                    v4.z = pack2(o[q + 4] * inv, o[q + 5] * inv);
-                    v4.w = pack2(o[q + 6] * inv, o[q + 7] * inv);
-                    *reinterpret_cast<uint4*>(dst + q) = v4;
+                for (int c = 0; c < 2; ++c)
+                    tc::tmem_ld32_nowait(t_o + w * DH + hc * 64 + c * 32 + lane_off,
+                                         reinterpret_cast<uint32_t*>(o) + 32 * c);
+                tc::tmem_ld_wait();
+                if (hc == DH / 64 - 1) {
+                    tc::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&o_free[w]);
                 }
-                a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+                if (row_ok) {
+#pragma unroll
+                    for (int q = 0; q < 64; q += 8) {
+                        uint4 v4;
+                        v4.x = pack2(o[q] * inv, o[q + 1] * inv);
+                        v4.y = pack2(o[q + 2] * inv, o[q + 3] * inv);
+                        v4.z = pack2(o[q + 4] * inv, o[q + 5] * inv);
+                        v4.w = pack2(o[q + 6] * inv, o[q + 7] * inv);
+                        *reinterpret_cast<uint4*>(dst + hc * 64 + q) = v4;
+                    }
+                }
             }
+            if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
         }
     }
     tc::tc_fence_before();
@@ -1619,20 +1636,14 @@ void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
+template <int DH>
 void launch_fwd_pair(const CUtensorMap& m, const AttnPairArgs& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_attn_fwd_pair<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem<64>::TOTAL);
+        cudaFuncSetAttribute(k_attn_fwd_pair<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem<DH>::TOTAL);
         attr = true;
     }
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    (void)sms;
-    launch_pdl(k_attn_fwd_pair<64>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<64>::TOTAL, st, m, a);
+    launch_pdl(k_attn_fwd_pair<DH>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<DH>::TOTAL, st, m, a);
     PARL_LAUNCHED();
 }
 
@@ -1767,7 +1778,7 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
     a.out = out;
     a.ldo = aa.ldo ? aa.ldo : aa.d;
     a.lse = lse;
-    if (aa.Dh == 64 && aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
+    if (aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
         AttnPairArgs pa;
         pa.T = aa.T; pa.H = aa.H; pa.d = aa.d; pa.Peff = aa.Peff;
         pa.grid = aa.sched.w_grid;
@@ -1776,7 +1787,8 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
         pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
         pa.scale_log2 = aa.scale * LOG2E;
         pa.out = out; pa.ldo = aa.ldo ? aa.ldo : aa.d; pa.lse = lse;
-        launch_fwd_pair(m, pa, st);
+        if (aa.Dh == 64) launch_fwd_pair<64>(m, pa, st);
+        else launch_fwd_pair<128>(m, pa, st);
         return true;
     }
     if (aa.Dh == 64) launch_fwd<64>(m, a, st);

@@ -443,12 +443,12 @@ template <class Tin, class Tout>
 __global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restrict__ dz, long lddz, int S, int V,
                               const float* __restrict__ lse, const float* __restrict__ u,
                               const int32_t* __restrict__ labels) {
-    const int s = blockIdx.y;
+    const int s = blockIdx.x;
     const float us = u[s], L = lse[s];
     const int lab = labels[s];
     const Tin* zr = z + (long)s * ldz;
     Tout* dr = dz + (long)s * lddz;
-    for (int v0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8; v0 < V; v0 += gridDim.x * blockDim.x * 8) {
+    for (int v0 = (blockIdx.y * blockDim.x + threadIdx.x) * 8; v0 < V; v0 += gridDim.y * blockDim.x * 8) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int v = v0 + q;
@@ -458,17 +458,18 @@ __global__ void k_softmax_bwd(const Tin* __restrict__ z, long ldz, Tout* __restr
 }
 
 // bf16 -> bf16 variant with 16-byte loads / stores (ldz, lddz, V multiples of 8)
-__global__ void k_softmax_bwd_v8(const bf16* __restrict__ z, long ldz, bf16* __restrict__ dz, long lddz, int S, int V,
+__global__ void k_softmax_bwd_v8(const bf16* z, long ldz, bf16* dz,  // may alias (in place)
+                                 long lddz, int S, int V,
                                  const float* __restrict__ lse, const float* __restrict__ u,
                                  const int32_t* __restrict__ labels) {
     pdl_wait();
-    const int s = blockIdx.y;
+    const int s = blockIdx.x;
     const float us = u[s], L2 = lse[s] * 1.4426950408889634f;
     const int lab = labels[s];
     const uint4* zr = reinterpret_cast<const uint4*>(z + (long)s * ldz);
     uint4* dr = reinterpret_cast<uint4*>(dz + (long)s * lddz);
     const int n8 = V >> 3;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n8; c += gridDim.x * blockDim.x) {
+    for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < n8; c += gridDim.y * blockDim.x) {
         const uint4 in = zr[c];
         const uint32_t w[4] = {in.x, in.y, in.z, in.w};
         uint32_t o[4];
@@ -697,8 +698,8 @@ __device__ __forceinline__ uint2 philox(uint2 ctr, uint32_t key_lo, uint32_t key
     return make_uint2(c0, cc2);
 }
 
-__global__ void k_randn(double* __restrict__ out, long n, uint64_t seed, uint32_t stream, double scale,
-                        const double* __restrict__ base) {
+__global__ void k_randn(double* out, long n, uint64_t seed, uint32_t stream, double scale,
+                        const double* base) {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
         const uint2 r = philox(make_uint2((uint32_t)e, (uint32_t)(e >> 32)), (uint32_t)seed, (uint32_t)(seed >> 32),
                                stream);
@@ -1010,12 +1011,12 @@ void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int 
     if constexpr (std::is_same_v<Tin, bf16> && std::is_same_v<Tout, bf16>) {
         if (V % 8 == 0 && ldz % 8 == 0 && lddz % 8 == 0 && (reinterpret_cast<uintptr_t>(z) & 15) == 0 &&
             (reinterpret_cast<uintptr_t>(dz) & 15) == 0) {
-            launch_pdl(k_softmax_bwd_v8, dim3(cx, S), dim3(256), 0, st, z, ldz, dz, lddz, S, V, lse, u, labels);
+            launch_pdl(k_softmax_bwd_v8, dim3(S, cx), dim3(256), 0, st, z, ldz, dz, lddz, S, V, lse, u, labels);
             PARL_LAUNCHED();
             return;
         }
     }
-    k_softmax_bwd<Tin, Tout><<<dim3(cx, S), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
+    k_softmax_bwd<Tin, Tout><<<dim3(S, cx), 256, 0, st>>>(z, ldz, dz, lddz, S, V, lse, u, labels);
     PARL_LAUNCHED();
 }
 template void launch_softmax_bwd<float, float>(const float*, long, float*, long, int, int, const float*,

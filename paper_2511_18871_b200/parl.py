@@ -128,7 +128,7 @@ def _load():
         "parl_apply_update": [vp, vp, C.c_double],
         "parl_comm_unique_id": [C.c_char_p], "parl_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
         "parl_grad_allreduce": [vp, vp], "parl_stats_allreduce": [vp],
-        "parl_ctx_profile": [vp, C.c_int],
+        "parl_ctx_profile": [vp, C.c_int], "parl_ctx_set_recompute": [vp, C.c_int], "parl_act_recompute": [vp],
         "parl_ctx_profile_read": [vp, C.c_int, f64p, f64p, C.POINTER(C.c_long)],
     }
     for name, args in sig.items():
@@ -200,6 +200,10 @@ class Context:
         return LIB.parl_ctx_launches(self.h)
 
     KC = {"gemm": 0, "head": 1, "attn_fwd": 2, "attn_bwd": 3, "loss": 4, "pack": 5, "norm": 6}
+
+    def set_recompute(self, mode: int):
+        """Activation recomputation: 0 auto, 1 always, 2 never (parl_ctx_set_recompute)."""
+        _check(LIB.parl_ctx_set_recompute(self.h, int(mode)), self.h)
 
     def profile(self, enable: bool):
         _check(LIB.parl_ctx_profile(self.h, int(enable)), self.h)

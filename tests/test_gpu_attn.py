@@ -56,7 +56,9 @@ CASES = [(300, [200, 250, 260], 2, 64), (64, [128, 128, 128, 128], 3, 64), (130,
          (700, [], 2, 64), (512, [1024] * 2, 1, 128),
          # long responses ending mid-pair: one tile of a pair skips a whole response's key
          # tiles (more than the K/V ring holds) while its partner consumes them
-         (1638, [3000, 2700], 2, 64), (200, [1500, 900, 700], 2, 64)]
+         (1638, [3000, 2700], 2, 64), (200, [1500, 900, 700], 2, 64),
+         # many heads: several work items per persistent CTA (Q buffer / K/V ring reuse across items)
+         (1000, [2000, 1300, 700], 40, 128), (1000, [2000, 1300, 700], 40, 64)]
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -76,7 +78,10 @@ def test_attention_fwd_tc_vs_torch(env, case):
         assert rc == 0, P.LIB.parl_last_error(None)
         eo = (out.float() - ref_o).abs().max().item()
         el = (lse - ref_lse).abs().max().item()
-        assert eo < 2e-2 and el < 1e-3, (path, eo, el)
+        # O is rounded to bf16 (and P enters PV in bf16): the bound scales with |O|max
+        # (both kernels measure max 0.026 at |O|max 6.7, 40 heads; bf16 rounding alone 0.016)
+        tol = 2e-2 * max(1.0, ref_o.abs().max().item() / 4)
+        assert eo < tol and el < 1e-3, (path, eo, el, tol)
 
 
 @pytest.mark.parametrize("case", CASES)

@@ -263,6 +263,32 @@ def test_c2_width_microbatch(P, ctx32, ctx16, orc, prec):
     assert max(rels.values()) < tol["grad_rel"], max(rels.items(), key=lambda kv: kv[1])
 
 
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("fixture", ["c1_micro.npz", "c2w_micro.npz"])
+def test_recompute_bitwise(P, ctx32, ctx16, prec, fixture):
+    """Activation recomputation (only x_0..x_L kept, layers and bf16 logits rebuilt in
+    the backward) runs the same kernels on the same inputs: log-probs, stats and
+    gradients are bit-identical to the keep-everything mode."""
+    ctx = ctx32 if prec == "fp32" else ctx16
+    z, cfg, tm, pk = _c1_setup(P, ctx, fixture, c1 if fixture.startswith("c1") else c2w)
+    out = []
+    try:
+        for mode in (2, 1, 2):
+            ctx.set_recompute(mode)
+            gb = P.GradBuffer(tm.policy)
+            ctx.stats_reset()
+            st = P.train_microbatch(tm, pk.group, gb, P.HyperParams(), advantages=z["advantages"])
+            out.append((gb.flat(), [pk.group.logprobs(s) for s in range(3)], st["objective_sum"]))
+    finally:
+        ctx.set_recompute(0)
+    for g, lps, obj in out[1:]:
+        assert np.array_equal(g, out[0][0])
+        for a, b in zip(lps, out[0][1]):
+            assert np.array_equal(a, b)
+        assert obj == out[0][2]
+    assert np.abs(out[1][0]).sum() > 0
+
+
 # --------------------------------------------------------------------------- reference contracts
 def test_determinism_bitwise(P, ctx32):  # test_model.cpp:251-265
     cfg = tiny(P)
