@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
 // lse in log2 units, and per-row visibility bounds {qhi, b1} (b1 = -1 for
 // prompt rows): key j is seen by queries [j, qhi_j); query i sees keys
 // [0, e0) u [b1, i] with e0 = i + 1 (prompt row) or Peff (response row).
-__global__ void k_attn_prep(int T, int H, int d, long ldo, const int32_t* __restrict__ seg,
+__global__ void k_attn_prep(int T, int H, int d, int Dh, long ldo, const int32_t* __restrict__ seg,
                             const int32_t* __restrict__ seg_start, const int32_t* __restrict__ seg_end,
                             const bf16* __restrict__ out, const bf16* __restrict__ dout,
                             const float* __restrict__ lse, float* __restrict__ dsum, float* __restrict__ lse2,
@@ -718,10 +718,12 @@ __global__ void k_attn_prep(int T, int H, int d, long ldo, const int32_t* __rest
     const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long)T * H) return;
     const int h = (int)(gw / T), i = (int)(gw % T);
-    const long off = (long)i * d + h * 64 + 2 * lane;
-    const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(out + (long)i * ldo + h * 64 + 2 * lane);
-    const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(dout + off);
-    float acc = __bfloat162float(o2.x) * __bfloat162float(g2.x) + __bfloat162float(o2.y) * __bfloat162float(g2.y);
+    float acc = 0.f;
+    for (int c = 2 * lane; c < Dh; c += 64) {
+        const __nv_bfloat162 o2 = *reinterpret_cast<const __nv_bfloat162*>(out + (long)i * ldo + h * Dh + c);
+        const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(dout + (long)i * d + h * Dh + c);
+        acc += __bfloat162float(o2.x) * __bfloat162float(g2.x) + __bfloat162float(o2.y) * __bfloat162float(g2.y);
+    }
     acc = warp_sum(acc);
     if (lane == 0) {
         dsum[(long)h * T + i] = acc;
@@ -787,10 +789,12 @@ constexpr int BWD_ST = 4;
 template <int DH>
 struct Bwd2Smem {
     static constexpr int TILE = 128 * DH * 2;
-    static constexpr int OFF_A = 0;                          // item operands [2 buffers][2 tiles]
-    static constexpr int OFF_B = OFF_A + 4 * TILE;           // streamed operands [BWD_ST][2 tiles]
-    static constexpr int OFF_VEC = OFF_B + 2 * BWD_ST * TILE;  // [BWD_ST][lse*log2e | D][128] (MODE_DKV)
-    static constexpr int OFF_BAR = OFF_VEC + BWD_ST * 2 * 128 * 4;
+    static constexpr int AB = DH == 128 ? 1 : 2;             // item operand buffers
+    static constexpr int BST = DH == 128 ? 2 : BWD_ST;       // streamed operand stages
+    static constexpr int OFF_A = 0;                          // item operands [AB][2 tiles]
+    static constexpr int OFF_B = OFF_A + 2 * AB * TILE;      // streamed operands [BST][2 tiles]
+    static constexpr int OFF_VEC = OFF_B + 2 * BST * TILE;   // [BST][lse*log2e | D][128] (MODE_DKV)
+    static constexpr int OFF_BAR = OFF_VEC + BST * 2 * 128 * 4;
     static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
@@ -798,16 +802,24 @@ template <int DH, int MODE>
 __global__ void __launch_bounds__(BWD_NTHR, 1)
     k_attn_bwd2(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                 AttnBwd2Args a) {
-    static_assert(DH == 64, "TMEM budget");
+    static_assert(DH == 64 || DH == 128, "head dim");
     using L = Bwd2Smem<DH>;
+    constexpr int AB = L::AB, BST = L::BST;
+    // TMEM (512 columns): S | dP | acc1 | acc2 | P | dS at Dh = 64 (128|128|64|64|64|64).
+    // Dh = 128, MODE_DKV: S | dP | dV | dK, with P written over S and dS over dP (each half
+    // of the element-wise warps packs its 64 columns into the first 32 of its own half), so
+    // the next tile's S / dP MMAs are issued behind this tile's gradient MMAs (in-order pipe).
+    // Dh = 128, MODE_DQ: S | dP | dQ | dS.
+    constexpr bool ALIAS = DH == 128 && MODE == MODE_DKV;
+    constexpr int HSTR = ALIAS ? 64 : 32;  // TMEM column stride between the halves' packed P / dS
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     uint64_t* a_full = bar + 0;    // [2]
     uint64_t* a_empty = bar + 2;   // [2]
     uint64_t* b_full = bar + 4;              // [BWD_ST]
-    uint64_t* b_empty = b_full + BWD_ST;     // [BWD_ST]
-    uint64_t* s_full = b_empty + BWD_ST;
+    uint64_t* b_empty = b_full + BST;        // [BST]
+    uint64_t* s_full = b_empty + BST;
     uint64_t* s_free = s_full + 1;
     uint64_t* p_full = s_full + 2;
     uint64_t* g_done = s_full + 3;
@@ -829,7 +841,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             tc::mbar_init(&a_full[s], 1);
             tc::mbar_init(&a_empty[s], 1);
         }
-        for (int s = 0; s < BWD_ST; ++s) {
+        for (int s = 0; s < BST; ++s) {
             tc::mbar_init(&b_full[s], 1 + 32);  // TMA bytes + one cp.async completion per lane of warp 8
             tc::mbar_init(&b_empty[s], 1);
         }
@@ -847,33 +859,42 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tbase = *tbase_s;
-    const uint32_t t_s = tbase, t_dp = tbase + 128, t_acc1 = tbase + 256, t_acc2 = tbase + 320;
+    const uint32_t t_s = tbase, t_dp = tbase + 128, t_acc1 = tbase + 256, t_acc2 = tbase + 256 + DH;
     pdl_wait();
     pdl_trigger();
-    const uint32_t t_p = tbase + 384, t_ds = tbase + 448;
+    const uint32_t t_p = ALIAS ? t_s : tbase + 384;
+    const uint32_t t_ds = ALIAS ? t_dp : (DH == 128 ? tbase + 384 : tbase + 448);
 
     if (warp >= 8) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
         if (warp == 8) {  // ---------------- TMA (whole warp: lane 0 issues, all lanes write vectors)
             int g = 0, li = 0;
             for (int k = k_begin; k < k_end; ++k, ++li) {
-                const int it = a.w_items[k], t = it / H, h = it % H, ab = li & 1;
-                tc::mbar_wait(&a_empty[ab], ((li >> 1) & 1) ^ 1);
+                const int it = a.w_items[k], t = it / H, h = it % H, ab = li % AB;
+                tc::mbar_wait(&a_empty[ab], ((li / AB) & 1) ^ 1);
                 if (lane == 0) {
                     tc::mbar_expect_tx(&a_full[ab], 2 * L::TILE);
                     uint8_t* A0 = smem + L::OFF_A + (ab * 2) * L::TILE;
-                    tc::tma_load_2d(A0, &tm_qkv, &a_full[ab], fix_col0 + h * DH, t * 128);
-                    tc::tma_load_2d(A0 + L::TILE, fix_map1, &a_full[ab], fix_col1 + h * DH, t * 128);
+#pragma unroll
+                    for (int r = 0; r < DH / 64; ++r) {
+                        tc::tma_load_2d(A0 + r * 128 * 128, &tm_qkv, &a_full[ab], fix_col0 + h * DH + r * 64, t * 128);
+                        tc::tma_load_2d(A0 + L::TILE + r * 128 * 128, fix_map1, &a_full[ab], fix_col1 + h * DH + r * 64,
+                                        t * 128);
+                    }
                 }
                 for (int e = a.lst_ptr[t]; e < a.lst_ptr[t + 1]; ++e, ++g) {
                     const int u = a.lst[e] & 0x3fffffff;
-                    const int st = g % BWD_ST;
-                    tc::mbar_wait(&b_empty[st], ((g / BWD_ST) & 1) ^ 1);
+                    const int st = g % BST;
+                    tc::mbar_wait(&b_empty[st], ((g / BST) & 1) ^ 1);
                     if (lane == 0) {
                         tc::mbar_expect_tx(&b_full[st], 2 * L::TILE);
                         uint8_t* B0 = smem + L::OFF_B + (st * 2) * L::TILE;
-                        tc::tma_load_2d(B0, &tm_qkv, &b_full[st], str_col0 + h * DH, u * 128);
-                        tc::tma_load_2d(B0 + L::TILE, str_map1, &b_full[st], str_col1 + h * DH, u * 128);
+#pragma unroll
+                        for (int r = 0; r < DH / 64; ++r) {
+                            tc::tma_load_2d(B0 + r * 128 * 128, &tm_qkv, &b_full[st], str_col0 + h * DH + r * 64, u * 128);
+                            tc::tma_load_2d(B0 + L::TILE + r * 128 * 128, str_map1, &b_full[st],
+                                            str_col1 + h * DH + r * 64, u * 128);
+                        }
                     }
                     if (MODE == MODE_DKV) {  // lse2 and D of the streamed query tile (zero-filled past T)
                         const uint32_t vl = tc::smem_u32(vec + st * 256);
@@ -911,11 +932,11 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             s_load();
             auto issue_sd = [&]() {
                 if (s_k >= k_end) return;
-                const int st = gS % BWD_ST, ab = s_li & 1;
+                const int st = gS % BST, ab = s_li % AB;
                 if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 0);
-                if (s_e == s_first) tc::mbar_wait(&a_full[ab], (s_li >> 1) & 1);
+                if (s_e == s_first) tc::mbar_wait(&a_full[ab], (s_li / AB) & 1);
                 if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 1);
-                tc::mbar_wait(&b_full[st], (gS / BWD_ST) & 1);
+                tc::mbar_wait(&b_full[st], (gS / BST) & 1);
                 if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 2);
                 if (cS > 0) tc::mbar_wait(s_free, (cS - 1) & 1);
                 if (MODE == MODE_DKV) ATTN_TRACE(3, cS, 3);
@@ -924,7 +945,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
-                    const uint32_t off = (ks & 3) * 32;
+                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
                     tc::mma_bf16_e(t_s, tc::sdesc(f0 + off, 16, 1024), tc::sdesc(s0 + off, 16, 1024), id_s, ks > 0);
                     tc::mma_bf16_e(t_dp, tc::sdesc(f0 + L::TILE + off, 16, 1024),
                                  tc::sdesc(s0 + L::TILE + off, 16, 1024), id_s, ks > 0);
@@ -939,19 +960,24 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                     s_load();
                 }
             };
-            issue_sd();
+            // S / dP issue window: one tile ahead of the gradient MMAs (none when P / dS live
+            // in S / dP's columns), and never into an item whose operand buffer this warp
+            // has not released yet
+            auto advance_sd = [&](int li_now) {
+                while (s_k < k_end && cS < cP + (ALIAS ? 1 : 2) && s_li <= li_now + AB - 1) issue_sd();
+            };
             int g = 0, li = 0;
             for (int k = k_begin; k < k_end; ++k, ++li) {
-                const int t = a.w_items[k] / H, ab = li & 1;
+                const int t = a.w_items[k] / H, ab = li % AB;
                 const int ea = a.lst_ptr[t], eb = a.lst_ptr[t + 1];
                 if (ea == eb) {  // nothing streams into this item: release its operands
-                    tc::mbar_wait(&a_full[ab], (li >> 1) & 1);
+                    tc::mbar_wait(&a_full[ab], (li / AB) & 1);
                     if (lane == 0) tc::mbar_arrive(&a_empty[ab]);
                     continue;
                 }
                 for (int e = ea; e < eb; ++e, ++g) {
-                    const int st = g % BWD_ST;
-                    issue_sd();
+                    const int st = g % BST;
+                    advance_sd(li);
                     if (MODE == MODE_DKV) ATTN_TRACE(2, cP, 1);
                     tc::mbar_wait(p_full, cP & 1);
                     tc::tc_fence_after();
@@ -962,19 +988,28 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                     for (int ks = 0; ks < 8; ++ks) {
                         const uint64_t b0 = tc::sdesc(s0 + ks * 2048, 128 * 128, 1024);
                         const uint64_t b1 = tc::sdesc(s0 + L::TILE + ks * 2048, 128 * 128, 1024);
+                        const uint32_t pc = (ks >> 2) * HSTR + (ks & 3) * 8;  // packed P / dS columns of this K step
                         if (MODE == MODE_DKV) {
-                            tc::mma_bf16_ts_e(t_acc1, t_p + ks * 8, b1, id_g, (acc || ks > 0) ? 1u : 0u);   // dV += P^T dO
-                            tc::mma_bf16_ts_e(t_acc2, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dK += dS^T Q
+                            tc::mma_bf16_ts_e(t_acc1, t_p + pc, b1, id_g, (acc || ks > 0) ? 1u : 0u);   // dV += P^T dO
+                            tc::mma_bf16_ts_e(t_acc2, t_ds + pc, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dK += dS^T Q
                         } else {
-                            tc::mma_bf16_ts_e(t_acc1, t_ds + ks * 8, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dQ += dS K
+                            tc::mma_bf16_ts_e(t_acc1, t_ds + pc, b0, id_g, (acc || ks > 0) ? 1u : 0u);  // dQ += dS K
                         }
                     }
                     tc::mma_commit_e(g_done);
                     tc::mma_commit_e(&b_empty[st]);
                     ++cP;
+                    if (e == eb - 1) {
+                        // item done: release the accumulators to the epilogue and the item operands
+                        // before looking ahead (the element-wise warps reach the next item's S only
+                        // after their epilogue)
+                        tc::mma_commit_e(acc_full);
+                        tc::mma_commit_e(&a_empty[ab]);
+                        advance_sd(li + 1);
+                    } else {
+                        advance_sd(li);
+                    }
                 }
-                tc::mma_commit_e(acc_full);
-                tc::mma_commit_e(&a_empty[ab]);
             }
         }
     } else {
@@ -1016,7 +1051,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 const uint32_t fl = (uint32_t)a.lst[e];
                 const int u0 = (int)(fl & 0x3fffffff) * 128;  // first row of the streamed tile
                 const bool full = (fl >> 30) & 1;
-                const uint32_t vl = tc::smem_u32(vec + (g % BWD_ST) * 256);
+                const uint32_t vl = tc::smem_u32(vec + (g % BST) * 256);
                 if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 0);
                 tc::mbar_wait(s_full, cS & 1);
                 tc::tc_fence_after();
@@ -1097,8 +1132,8 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 4);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    if (MODE == MODE_DKV) tc::tmem_st16(t_p + half * 32 + c * 16 + lane_off, pp + 16 * c);
-                    tc::tmem_st16(t_ds + half * 32 + c * 16 + lane_off, pd + 16 * c);
+                    if (MODE == MODE_DKV) tc::tmem_st16(t_p + half * HSTR + c * 16 + lane_off, pp + 16 * c);
+                    tc::tmem_st16(t_ds + half * HSTR + c * 16 + lane_off, pd + 16 * c);
                 }
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
@@ -1109,29 +1144,33 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             }
             // item epilogue: accumulators -> bf16 rows of dqkv (MODE_DKV: half 0 dV -> 2d + h DH,
             // half 1 dK * scale -> d + h DH; MODE_DQ: dQ * scale, half h -> columns [32 h, 32 h + 32))
-            constexpr int NC = MODE == MODE_DKV ? 64 : 32;
+            constexpr int NC = MODE == MODE_DKV ? DH : DH / 2;
+            constexpr int CH = NC < 64 ? NC : 64;  // columns per TMEM load batch
             bf16* dst = a.dqkv + (long)x * 3 * a.d + h * DH +
-                        (MODE == MODE_DKV ? (half ? a.d : 2 * a.d) : half * 32);
+                        (MODE == MODE_DKV ? (half ? a.d : 2 * a.d) : half * (DH / 2));
             if (eb > ea) {
                 tc::mbar_wait(acc_full, na & 1);
                 tc::tc_fence_after();
                 ++na;
-                float o[NC];
-                const uint32_t src = MODE == MODE_DKV ? (half ? t_acc2 : t_acc1) : t_acc1 + half * 32;
-#pragma unroll
-                for (int c = 0; c < NC / 32; ++c)
-                    tc::tmem_ld32_nowait(src + c * 32 + lane_off, reinterpret_cast<uint32_t*>(o) + 32 * c);
-                tc::tmem_ld_wait();
+                const uint32_t src = MODE == MODE_DKV ? (half ? t_acc2 : t_acc1) : t_acc1 + half * (DH / 2);
                 const float mul = (MODE == MODE_DQ || half) ? a.scale : 1.f;
-                if (row_ok) {
 #pragma unroll
-                    for (int q = 0; q < NC; q += 8) {
-                        uint4 v4;
-                        v4.x = pack2(o[q] * mul, o[q + 1] * mul);
-                        v4.y = pack2(o[q + 2] * mul, o[q + 3] * mul);
-                        v4.z = pack2(o[q + 4] * mul, o[q + 5] * mul);
-                        v4.w = pack2(o[q + 6] * mul, o[q + 7] * mul);
-                        *reinterpret_cast<uint4*>(dst + q) = v4;
+                for (int cb = 0; cb < NC; cb += CH) {
+                    float o[CH];
+#pragma unroll
+                    for (int c = 0; c < CH / 32; ++c)
+                        tc::tmem_ld32_nowait(src + cb + c * 32 + lane_off, reinterpret_cast<uint32_t*>(o) + 32 * c);
+                    tc::tmem_ld_wait();
+                    if (row_ok) {
+#pragma unroll
+                        for (int q = 0; q < CH; q += 8) {
+                            uint4 v4;
+                            v4.x = pack2(o[q] * mul, o[q + 1] * mul);
+                            v4.y = pack2(o[q + 2] * mul, o[q + 3] * mul);
+                            v4.z = pack2(o[q + 4] * mul, o[q + 5] * mul);
+                            v4.w = pack2(o[q + 6] * mul, o[q + 7] * mul);
+                            *reinterpret_cast<uint4*>(dst + cb + q) = v4;
+                        }
                     }
                 }
             } else if (row_ok) {
@@ -1686,14 +1725,14 @@ void launch_bwd(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwdArgs&
 
 }  // namespace
 
-template <int MODE>
+template <int DH, int MODE>
 void launch_bwd2(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwd2Args& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_attn_bwd2<64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Smem<64>::TOTAL);
+        cudaFuncSetAttribute(k_attn_bwd2<DH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Smem<DH>::TOTAL);
         attr = true;
     }
-    launch_pdl(k_attn_bwd2<64, MODE>, dim3(grid), dim3(BWD_NTHR), Bwd2Smem<64>::TOTAL, st, mq, md, a);
+    launch_pdl(k_attn_bwd2<DH, MODE>, dim3(grid), dim3(BWD_NTHR), Bwd2Smem<DH>::TOTAL, st, mq, md, a);
     PARL_LAUNCHED();
 }
 
@@ -1721,13 +1760,13 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
     a.lse = lse;
     a.dsum = dsum;
     a.dqkv = dqkv;
-    if (aa.Dh == 64 && aa.sched.bk_ptr && aa.sched.bq_ptr && attn_pair_enabled() && out) {
+    if (aa.sched.bk_ptr && aa.sched.bq_ptr && attn_pair_enabled() && out) {
         const size_t ht = (size_t)aa.H * aa.T;
         float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 8 + 16));
         if (!lse2) return false;
         int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
         const long warps = (long)aa.T * aa.H;
-        launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d,
+        launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, aa.Dh,
                    (long)(aa.ldo ? aa.ldo : aa.d), aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
         PARL_LAUNCHED();
         AttnBwd2Args b;
@@ -1737,10 +1776,12 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         b.lse2 = lse2; b.dsum = dsum; b.meta = meta; b.dqkv = dqkv;
         b.lst_ptr = aa.sched.k_ptr; b.lst = aa.sched.k_list;
         b.w_ptr = aa.sched.bk_ptr; b.w_items = aa.sched.bk_items;
-        launch_bwd2<MODE_DKV>(mq, md, b, aa.sched.bk_grid, st);
+        if (aa.Dh == 64) launch_bwd2<64, MODE_DKV>(mq, md, b, aa.sched.bk_grid, st);
+        else launch_bwd2<128, MODE_DKV>(mq, md, b, aa.sched.bk_grid, st);
         b.lst_ptr = aa.sched.q_ptr; b.lst = aa.sched.q_list;
         b.w_ptr = aa.sched.bq_ptr; b.w_items = aa.sched.bq_items;
-        launch_bwd2<MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
+        if (aa.Dh == 64) launch_bwd2<64, MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
+        else launch_bwd2<128, MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
         return true;
     }
     if (out) launch_attn_dsum<bf16>(aa, out, dout, dsum, st);
