@@ -123,6 +123,14 @@ parl_status parl_model_download(parl_model_t m, double* flat, size_t n);
 size_t parl_param_count(const parl_config* cfg);
 uint64_t parl_model_version(parl_model_t m);
 
+/* Checkpoints in the reference's PARLCKP1 format (docs/formats.md): save_checkpoint /
+ * load_checkpoint (model.cpp:924-987).  IoError on open / magic / truncation / layout
+ * mismatch, NumericError on non-finite weights, ConfigError on an invalid header config.
+ * load creates a new model on ctx holding the stored weights and version. */
+parl_status parl_checkpoint_save(parl_model_t m, const char* path);
+parl_status parl_model_config(parl_model_t m, parl_config* out);
+parl_status parl_checkpoint_load(parl_ctx_t ctx, const char* path, parl_model_t* out);
+
 /* ---- packing: pack_group (packing.cpp:7-45) + segments/predecessors
  *      (model.cpp:230-253), K1 on the device ------------------------------ */
 parl_status parl_group_create(parl_ctx_t ctx, int max_tokens, int max_responses, parl_group_t* out);

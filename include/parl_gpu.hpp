@@ -145,7 +145,20 @@ public:
     parl_model_t handle() const { return h_.get(); }
     Device& device() const { return *dev_; }
 
+    // save_checkpoint / load_checkpoint (model.cpp:924-987), PARLCKP1 format
+    void save(const std::string& path) const { check(parl_checkpoint_save(h_.get(), path.c_str()), dev_->ctx()); }
+    static ModelParams load(const std::string& path, Device& dev = Device::get()) {
+        parl_model_t m = nullptr;
+        check(parl_checkpoint_load(dev.ctx(), path.c_str(), &m), dev.ctx());
+        parl_config c{};
+        parl_model_config(m, &c);
+        return ModelParams(ModelConfig{c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len}, dev, m);
+    }
+
 private:
+    ModelParams(const ModelConfig& cfg, Device& dev, parl_model_t m) : cfg_(cfg), dev_(&dev) {
+        h_ = std::shared_ptr<parl_model_s>(m, [](parl_model_t x) { parl_model_destroy(x); });
+    }
     ModelParams(const ModelConfig& cfg, Device& dev) : cfg_(cfg), dev_(&dev) {
         parl_config c = cfg.c();
         parl_model_t m = nullptr;
@@ -180,6 +193,11 @@ private:
     std::size_t n_;
     std::shared_ptr<parl_grad_s> h_;
 };
+
+inline void save_checkpoint(const std::string& path, const ModelParams& params) { params.save(path); }
+inline ModelParams load_checkpoint(const std::string& path, Device& dev = Device::get()) {
+    return ModelParams::load(path, dev);
+}
 
 inline void ModelParams::apply_update(const GradBuffer& grads, double lr) {
     check(parl_apply_update(h_.get(), grads.handle(), lr), dev_->ctx());

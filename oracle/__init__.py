@@ -82,6 +82,9 @@ class Oracle:
             f.restype = C.c_double
             f.argtypes = [C.c_double] * (4 if name == "clipped_term" else 2)
         if kind == "ref":
+            self.lib.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_void_p, C.c_ulonglong, C.c_char_p]
+            self.lib.ref_load_checkpoint.restype = C.c_long
+            self.lib.ref_load_checkpoint.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             self.lib.ref_bench_microbatch.restype = C.c_double
             self.lib.ref_bench_microbatch.argtypes = [C.c_void_p, C.c_ulonglong] + [C.c_int] * 5
             self.lib.ref_param_count.restype = C.c_long
@@ -97,6 +100,23 @@ class Oracle:
         if rc < 0:
             raise OracleError(-rc, what)
         return rc
+
+    def save_checkpoint(self, cfg: Cfg, w, seed: int, path: str):
+        """The reference's save_checkpoint (model.cpp:924-946) of weights w (version 0)."""
+        assert self.kind == "ref"
+        c = cfg.c()
+        self._chk(self.lib.ref_save_checkpoint(C.byref(c), _p(_f64(w)), C.c_ulonglong(seed), os.fsencode(path)),
+                  "save_checkpoint")
+
+    def load_checkpoint(self, path: str):
+        """The reference's load_checkpoint (model.cpp:948-987): (Cfg, version, seed, flat)."""
+        assert self.kind == "ref"
+        c, ver, seed = (C.c_int * 6)(), C.c_ulonglong(), C.c_ulonglong()
+        n = self._chk(self.lib.ref_load_checkpoint(os.fsencode(path), C.byref(c), None, C.byref(ver),
+                                                   C.byref(seed)), "load_checkpoint")
+        w = np.zeros(n, dtype=np.float64)
+        self.lib.ref_load_checkpoint(os.fsencode(path), C.byref(c), _p(w), C.byref(ver), C.byref(seed))
+        return Cfg(*list(c)), ver.value, seed.value, w
 
     def param_count(self, cfg: Cfg) -> int:
         c = cfg.c()
@@ -215,6 +235,34 @@ class Oracle:
         assert self.kind == "ref"
         c = cfg.c()
         return float(self.lib.ref_bench_microbatch(C.byref(c), C.c_ulonglong(seed), P, G, R, reps, threads))
+
+
+def read_parlckp1(path: str):
+    """PARLCKP1 reader (save_checkpoint, model.cpp:924-946; docs/formats.md): header, then
+    per tensor u32 name length, name, u32 rows, u32 cols, rows * cols f64.  Returns
+    (Cfg, version, init_seed, [(name, rows, cols)], flat fp64)."""
+    import struct
+
+    with open(path, "rb") as f:
+        b = f.read()
+    if b[:8] != b"PARLCKP1":
+        raise ValueError("bad checkpoint magic")
+    V, d, L, H, F, S = struct.unpack_from("<6I", b, 8)
+    version, seed = struct.unpack_from("<2Q", b, 32)
+    (n,) = struct.unpack_from("<I", b, 48)
+    o, names, parts = 52, [], []
+    for _ in range(n):
+        (nl,) = struct.unpack_from("<I", b, o)
+        name = b[o + 4:o + 4 + nl].decode()
+        o += 4 + nl
+        r, c = struct.unpack_from("<2I", b, o)
+        o += 8
+        parts.append(np.frombuffer(b, dtype="<f8", count=r * c, offset=o))
+        o += 8 * r * c
+        names.append((name, r, c))
+    if o != len(b):
+        raise ValueError("trailing bytes in checkpoint")
+    return Cfg(V, d, L, H, F, S), version, seed, names, np.concatenate(parts)
 
 
 def layout(cfg: Cfg):

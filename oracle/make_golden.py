@@ -59,6 +59,8 @@ def main(only=None):
     ref = Oracle("ref")
     if only == "c2w":
         return _c2w(ref)
+    if only == "ckpt":
+        return _ckpt(ref)
 
     # ---- tiny: packed forward/backward with an arbitrary upstream -------------
     w = ref.init_params(TINY, 41)
@@ -107,6 +109,13 @@ def main(only=None):
                         rewards=rewards, advantages=adv, stats=st, lp3=lp3, grad_names=names, grad_sums=sums,
                         grad_l2=l2, grad_idx=idx, grad_vals=vals, param_sum=w1.sum(), param_head=w1[:64])
     _c2w(ref)
+
+
+def _ckpt(ref):
+    """PARLCKP1 file written by the reference's own save_checkpoint (model.cpp:924-946) for
+    the tiny config, init seed 41 (version 0)."""
+    ref.save_checkpoint(TINY, ref.init_params(TINY, 41), 41, os.path.join(GOLDEN, "tiny_seed41.parlckp1"))
+    print("wrote tiny_seed41.parlckp1")
 
 
 def _c2w(ref):

@@ -241,6 +241,37 @@ int ref_train_microbatch(const CCfg* c, const double* w_pol, const double* w_old
     });
 }
 
+// save_checkpoint / load_checkpoint (model.cpp:924-987) of the reference itself:
+// golden PARLCKP1 files and the check that the reference reads the GPU path's files.
+int ref_save_checkpoint(const CCfg* c, const double* w, unsigned long long seed, const char* path) {
+    return guarded([&] {
+        ModelParams p = ModelParams::init(to_cfg(c), seed);
+        if (w) std::memcpy(p.flat_mut().data(), w, p.flat().size() * sizeof(double));
+        save_checkpoint(path, p);
+        return 0;
+    });
+}
+
+// Returns the parameter count; fills cfg, version, seed and (if w) the weights.
+long ref_load_checkpoint(const char* path, CCfg* c, double* w, unsigned long long* version,
+                         unsigned long long* seed) {
+    try {
+        ModelParams p = load_checkpoint(path);
+        const auto& m = p.config();
+        *c = CCfg{m.vocab_size, m.d_model, m.n_layers, m.n_heads, m.d_ff, m.max_seq_len};
+        *version = p.version();
+        *seed = p.init_seed();
+        if (w) std::memcpy(w, p.flat().data(), p.flat().size() * sizeof(double));
+        return (long)p.flat().size();
+    } catch (const IoError&) {
+        return -8;
+    } catch (const NumericError&) {
+        return -5;
+    } catch (...) {
+        return -99;
+    }
+}
+
 // CPU baseline: `threads` independent workers, each with its own TriModel
 // (SPEC.md:113 allows distinct instances concurrently), each running `reps`
 // shared-prompt micro-batches of P + G x R tokens with random tokens in

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <string>
 #include <memory>
 #include <queue>
 #include <random>
@@ -165,6 +167,7 @@ struct parl_model_s {
     DevBuf f32, act, master;
     bool has_master = false;
     uint64_t version = 0, forward_gen = 0;
+    uint64_t init_seed = 0;  // ModelParams::init_seed (checkpoint header)
 };
 
 struct parl_group_s {
@@ -1286,6 +1289,7 @@ parl_status parl_model_init(parl_model_t m, uint64_t seed) {
     });
     if (s != PARL_OK) return s;
     // tensor_maps lists tensors in layout order, so draws follow model.cpp:153-162
+    m->init_seed = seed;
     return parl_model_upload(m, w.data(), w.size(), 0);
 }
 
@@ -1305,6 +1309,7 @@ parl_status parl_model_init_device(parl_model_t m, uint64_t seed, double scale) 
         check_launch();
         PARL_CUDA(cudaStreamSynchronize(st));
         m->version = 0;
+        m->init_seed = seed;
     });
 }
 
@@ -1360,6 +1365,142 @@ parl_status parl_model_download(parl_model_t m, double* flat, size_t n) {
         }
         PARL_CUDA(cudaStreamSynchronize(st));
     });
+}
+
+// ---- checkpoints: PARLCKP1 (save_checkpoint / load_checkpoint, model.cpp:907-987) --------
+// magic "PARLCKP1"; u32 vocab, d_model, n_layers, n_heads, d_ff, max_seq_len; u64 version,
+// init_seed; u32 n_tensors; per tensor in layout order: u32 name length, name bytes,
+// u32 rows, u32 cols, rows * cols f64 (the reference flat layout, model.cpp:86-114).
+extern "C++" {
+namespace {
+constexpr char kCkptMagic[8] = {'P', 'A', 'R', 'L', 'C', 'K', 'P', '1'};
+
+std::vector<std::string> tensor_names(const parl_config& c) {  // build_layout, model.cpp:86-114
+    std::vector<std::string> v = {"tok_emb", "pos_emb"};
+    static const char* per_layer[] = {"ln1.gamma", "ln1.beta", "attn.wq", "attn.bq", "attn.wk", "attn.bk",
+                                      "attn.wv",   "attn.bv",  "attn.wo", "attn.bo", "ln2.gamma", "ln2.beta",
+                                      "ffn.w1",    "ffn.b1",   "ffn.w2",  "ffn.b2"};
+    for (int l = 0; l < c.n_layers; ++l)
+        for (const char* n : per_layer) v.push_back("layers." + std::to_string(l) + "." + n);
+    for (const char* n : {"ln_f.gamma", "ln_f.beta", "head.w", "head.b"}) v.push_back(n);
+    return v;
+}
+
+template <class T>
+void put(std::ostream& os, T v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+template <class T>
+T get(std::istream& is) {
+    T v{};
+    is.read(reinterpret_cast<char*>(&v), sizeof(T));
+    PARL_REQUIRE(bool(is), PARL_E_IO, "checkpoint truncated");
+    return v;
+}
+}  // namespace
+}  // extern "C++"
+
+parl_status parl_model_config(parl_model_t m, parl_config* out) {
+    if (!m || !out) return PARL_E_CONFIG;
+    *out = m->cfg;
+    return PARL_OK;
+}
+
+parl_status parl_checkpoint_save(parl_model_t m, const char* path) {
+    return guarded(m->ctx, [&] {
+        std::ofstream os(path, std::ios::binary | std::ios::trunc);
+        PARL_REQUIRE(bool(os), PARL_E_IO, std::string("cannot open checkpoint for writing: ") + path);
+        os.write(kCkptMagic, sizeof(kCkptMagic));
+        const auto& c = m->cfg;
+        for (int v : {c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len}) put<uint32_t>(os, v);
+        put<uint64_t>(os, m->version);
+        put<uint64_t>(os, m->init_seed);
+        const auto maps = tensor_maps(m);
+        const auto names = tensor_names(c);
+        put<uint32_t>(os, (uint32_t)maps.size());
+        cudaStream_t st = m->ctx->st;
+        std::vector<double> h;
+        for (size_t i = 0; i < maps.size(); ++i) {
+            const auto& t = maps[i];
+            const size_t cnt = (size_t)t.rows * t.cols;
+            h.resize(cnt);
+            const double* src = m->has_master ? static_cast<const double*>(m->master.p) + t.src_off : nullptr;
+            if (!src) {
+                double* stg = m->ctx->staging.as<double>(cnt);
+                export_tensor(m, t, stg, st);
+                src = stg;
+            }
+            PARL_CUDA(cudaMemcpyAsync(h.data(), src, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaStreamSynchronize(st));
+            put<uint32_t>(os, (uint32_t)names[i].size());
+            os.write(names[i].data(), (std::streamsize)names[i].size());
+            put<uint32_t>(os, (uint32_t)t.rows);
+            put<uint32_t>(os, (uint32_t)t.cols);
+            os.write(reinterpret_cast<const char*>(h.data()), (std::streamsize)(cnt * sizeof(double)));
+        }
+        PARL_REQUIRE(bool(os), PARL_E_IO, std::string("write failed: ") + path);
+    });
+}
+
+parl_status parl_checkpoint_load(parl_ctx_t ctx, const char* path, parl_model_t* out) {
+    parl_model_t m = nullptr;
+    const parl_status s = guarded(ctx, [&] {
+        std::ifstream is(path, std::ios::binary);
+        PARL_REQUIRE(bool(is), PARL_E_IO, std::string("cannot open checkpoint: ") + path);
+        char magic[8];
+        is.read(magic, sizeof(magic));
+        PARL_REQUIRE(is && std::memcmp(magic, kCkptMagic, sizeof(magic)) == 0, PARL_E_IO,
+                     std::string("bad checkpoint magic in ") + path);
+        parl_config c{};
+        c.vocab_size = (int)get<uint32_t>(is);
+        c.d_model = (int)get<uint32_t>(is);
+        c.n_layers = (int)get<uint32_t>(is);
+        c.n_heads = (int)get<uint32_t>(is);
+        c.d_ff = (int)get<uint32_t>(is);
+        c.max_seq_len = (int)get<uint32_t>(is);
+        const uint64_t version = get<uint64_t>(is), seed = get<uint64_t>(is);
+        const uint32_t n_tensors = get<uint32_t>(is);
+        const parl_status cs = parl_model_create(ctx, &c, &m);  // ConfigError on a bad header
+        if (cs != PARL_OK) throw Error{cs, ctx->err};
+        const auto maps = tensor_maps(m);
+        const auto names = tensor_names(c);
+        PARL_REQUIRE(n_tensors == maps.size(), PARL_E_IO, std::string("checkpoint tensor count mismatch in ") + path);
+        cudaStream_t st = ctx->st;
+        std::vector<double> h;
+        for (size_t i = 0; i < maps.size(); ++i) {
+            const auto& t = maps[i];
+            const uint32_t nl = get<uint32_t>(is);
+            std::string name(nl, '\0');
+            is.read(name.data(), nl);
+            const uint32_t rows = get<uint32_t>(is), cols = get<uint32_t>(is);
+            PARL_REQUIRE(is && name == names[i] && rows == (uint32_t)t.rows && cols == (uint32_t)t.cols, PARL_E_IO,
+                         "checkpoint tensor '" + name + "' does not match expected layout");
+            const size_t cnt = (size_t)rows * cols;
+            h.resize(cnt);
+            is.read(reinterpret_cast<char*>(h.data()), (std::streamsize)(cnt * sizeof(double)));
+            PARL_REQUIRE(bool(is), PARL_E_IO, "checkpoint truncated in tensor " + name);
+            for (double v : h)
+                PARL_REQUIRE(std::isfinite(v), PARL_E_NUMERIC,
+                             std::string("checkpoint contains non-finite values: ") + path);
+            double* dst = m->has_master ? static_cast<double*>(m->master.p) + t.src_off
+                                        : ctx->staging.as<double>(cnt);
+            PARL_CUDA(cudaMemcpyAsync(dst, h.data(), cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+            if (!m->has_master) convert_tensor(m, t, dst);
+            PARL_CUDA(cudaStreamSynchronize(st));  // h is reused
+        }
+        if (m->has_master) convert_from_master(m);
+        check_launch();
+        PARL_CUDA(cudaStreamSynchronize(st));
+        m->version = version;
+        m->init_seed = seed;
+    });
+    if (s != PARL_OK) {
+        if (m) parl_model_destroy(m);
+        return s;
+    }
+    *out = m;
+    return PARL_OK;
 }
 
 // ---- groups -----------------------------------------------------------------

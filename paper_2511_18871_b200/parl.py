@@ -128,6 +128,8 @@ def _load():
         "parl_apply_update": [vp, vp, C.c_double],
         "parl_comm_unique_id": [C.c_char_p], "parl_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
         "parl_grad_allreduce": [vp, vp], "parl_stats_allreduce": [vp],
+        "parl_checkpoint_save": [vp, C.c_char_p], "parl_checkpoint_load": [vp, C.c_char_p, C.POINTER(vp)],
+        "parl_model_config": [vp, C.POINTER(_Config)],
         "parl_ctx_profile": [vp, C.c_int], "parl_ctx_set_recompute": [vp, C.c_int], "parl_act_recompute": [vp],
         "parl_ctx_profile_read": [vp, C.c_int, f64p, f64p, C.POINTER(C.c_long)],
     }
@@ -273,9 +275,12 @@ class ModelConfig:
 class ModelParams:
     """Device-resident weight set (replaces ModelParams, model.hpp:64-106)."""
 
-    def __init__(self, config: ModelConfig, ctx: Optional[Context] = None):
+    def __init__(self, config: ModelConfig, ctx: Optional[Context] = None, _handle=None):
         self.ctx = ctx or default_context()
         self.config = config
+        if _handle is not None:
+            self.h = _handle
+            return
         h = C.c_void_p()
         c = config.c()
         _check(LIB.parl_model_create(self.ctx.h, C.byref(c), C.byref(h)), self.ctx.h)
@@ -322,6 +327,21 @@ class ModelParams:
 
     def apply_update(self, grads: "GradBuffer", lr: float):
         _check(LIB.parl_apply_update(self.h, grads.h, lr), self.ctx.h)
+
+    def save(self, path: str):
+        """save_checkpoint (model.cpp:924-946): PARLCKP1 file of the fp64 weights."""
+        _check(LIB.parl_checkpoint_save(self.h, os.fsencode(path)), self.ctx.h)
+
+    @classmethod
+    def load(cls, path: str, ctx: Optional[Context] = None) -> "ModelParams":
+        """load_checkpoint (model.cpp:948-987)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(LIB.parl_checkpoint_load(ctx.h, os.fsencode(path), C.byref(h)), ctx.h)
+        c = _Config()
+        _check(LIB.parl_model_config(h, C.byref(c)), ctx.h)
+        cfg = ModelConfig(c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.d_ff, c.max_seq_len)
+        return cls(cfg, ctx, _handle=h)
 
     def __del__(self):
         try:

@@ -232,3 +232,29 @@ def test_oracle_matches_reference_live(orc, ref_orc):
         b = ref_orc.train_microbatch(cfg, w, wo, wr, prompt, resp, adv, 0.2, 0.04, gran)
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+# --------------------------------------------------------------------------- PARLCKP1 (model.cpp:907-987)
+TINY_CKPT = Cfg(vocab=16, d_model=16, n_layers=2, n_heads=2, d_ff=24, max_seq=64)
+
+
+def test_parlckp1_golden_layout_and_values(orc):
+    """The reference-written golden checkpoint: header, tensor names / shapes in
+    build_layout order (model.cpp:86-114), and the init(seed 41) weights bit-exact."""
+    from oracle import read_parlckp1
+
+    cfg, version, seed, names, flat = read_parlckp1(os.path.join(GOLDEN, "tiny_seed41.parlckp1"))
+    assert cfg == TINY_CKPT and version == 0 and seed == 41
+    assert [(n, r, c) for n, _, r, c in layout(cfg)] == names
+    assert np.array_equal(flat, orc.init_params(cfg, 41))
+
+
+def test_parlckp1_reference_round_trip(ref_orc, tmp_path):
+    from oracle import read_parlckp1
+
+    w = ref_orc.init_params(TINY_CKPT, 5) * 1.5
+    path = str(tmp_path / "w.parlckp1")
+    ref_orc.save_checkpoint(TINY_CKPT, w, 5, path)
+    cfg, version, seed, w2 = ref_orc.load_checkpoint(path)
+    assert cfg == TINY_CKPT and version == 0 and seed == 5 and np.array_equal(w, w2)
+    assert np.array_equal(read_parlckp1(path)[4], w)
