@@ -183,7 +183,7 @@ struct parl_group_s {
     HostStage sched_stage, work_stage;
     AttnSched sched;
     SchedHost sched_h;  // host copies of the schedule's tile pointers (work lists)
-    int work_H = -1;
+    int work_H = -1, work_d = -1;
     uint64_t work_epoch = ~0ull;
     uint64_t sorted_epoch = ~0ull;
     std::vector<int> lens, span_start, cu;
@@ -391,7 +391,7 @@ void ensure_sorted(parl_group_s* g) {
     g->sorted_epoch = g->epoch;
 }
 
-void ensure_attn_work(parl_group_s* g, int H);
+void ensure_attn_work(parl_group_s* g, int H, int d);
 
 // ---------------------------------------------------------------------------
 // forward (forward_logprobs, model.cpp:534-567; run_forward 430-521)
@@ -622,7 +622,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
         }
     }
 
-    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
+    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H, D);
     const AttnArgs aa = attn_args(g, cf);
     {
         ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * 12 * nm);
@@ -758,7 +758,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     float* dsum = c->dsum.as<float>((size_t)H * Tn);
     float* dx2 = c->dx2.as<float>(TD);
 
-    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H);
+    if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H, D);
     const AttnArgs aa = attn_args(g, cf);
     // recompute mode: one layer's activation set, rebuilt from x_l before its backward
     const bool rc = act->recompute;
@@ -991,7 +991,17 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
 // Longest-processing-time assignment of attention work items (tile * H + head)
 // to one persistent CTA per SM; cost = partner tiles + 1 (per-item overhead).
 // Appends [ptr (grid + 1) | items] to `all`; returns the grid.
-int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all) {
+// PARL_ATTN_ORDER=lpt: longest-first order (diagnostics); default head-major
+bool attn_order_lpt() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("PARL_ATTN_ORDER");
+        v = (e && std::strcmp(e, "lpt") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all, bool locality) {
     const int nt = (int)ptr.size() - 1;
     const int n = nt * H;
     int sms = 148;
@@ -1002,9 +1012,28 @@ int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all)
     }
     const int grid = std::max(1, std::min(n, sms));
     std::vector<int32_t> order(n);
-    for (int i = 0; i < n; ++i) order[i] = i;
     auto cost = [&](int it) { return ptr[it / H + 1] - ptr[it / H] + 1; };
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    if (!locality || attn_order_lpt()) {
+        for (int i = 0; i < n; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    } else {
+        // head-major, tiles ascending: the items in flight at any time belong to one or two
+        // heads, whose K/V (or Q/dO) tiles then stay in L2 (C3: 34 MB per head) instead of
+        // being re-read from HBM by every tile of every head.  Items far above the mean
+        // cost (prompt key tiles of the dK/dV pass, seen by every query tile) go first,
+        // longest first, so the greedy least-loaded assignment below stays balanced.
+        long tot = 0;
+        for (int t = 0; t < nt; ++t) tot += (long)(ptr[t + 1] - ptr[t] + 1) * H;
+        const double big = 2.0 * (double)tot / std::max(n, 1);
+        int k = 0;
+        for (int i = 0; i < n; ++i)
+            if (cost(i) > big) order[k++] = i;
+        std::stable_sort(order.begin(), order.begin() + k, [&](int x, int y) { return cost(x) > cost(y); });
+        for (int i = 0; i < n; ++i) {
+            const int it = (i % nt) * H + i / nt;
+            if (cost(it) <= big) order[k++] = it;
+        }
+    }
     std::vector<std::vector<int32_t>> per(grid);
     using L = std::pair<long, int>;
     std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
@@ -1023,14 +1052,19 @@ int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all)
 }
 
 // forward (query-tile pairs), dK/dV (key tiles) and dQ (query tiles) work lists
-void build_attn_work(AttnSched& s, const SchedHost& hs, int H, DevBuf& buf, HostStage& stage, cudaStream_t st) {
+// (forward: head-major order only when the K/V of all heads overflow about half the L2;
+// below that, longest-first balances better; the backward streams two operands per tile
+// and gains from head-major order at every size measured)
+void build_attn_work(AttnSched& s, const SchedHost& hs, int H, int dm, DevBuf& buf, HostStage& stage,
+                     cudaStream_t st) {
     std::vector<int32_t> all;
+    const double kv_bytes = 128.0 * ((double)hs.q_ptr.size() - 1) * dm * 4;
     const size_t o_f = all.size();
-    const int gf = lpt_lists(hs.p_ptr, H, all);
+    const int gf = lpt_lists(hs.p_ptr, H, all, kv_bytes > 64e6);
     const size_t o_k = all.size();
-    const int gk = lpt_lists(hs.k_ptr, H, all);
+    const int gk = lpt_lists(hs.k_ptr, H, all, true);
     const size_t o_q = all.size();
-    const int gq = lpt_lists(hs.q_ptr, H, all);
+    const int gq = lpt_lists(hs.q_ptr, H, all, true);
     int32_t* d = buf.as<int32_t>(all.size());
     stage.upload(d, all.data(), all.size() * 4, st);
     s.w_ptr = d + o_f; s.w_items = d + o_f + gf + 1; s.w_grid = gf;
@@ -1038,10 +1072,11 @@ void build_attn_work(AttnSched& s, const SchedHost& hs, int H, DevBuf& buf, Host
     s.bq_ptr = d + o_q; s.bq_items = d + o_q + gq + 1; s.bq_grid = gq;
 }
 
-void ensure_attn_work(parl_group_s* g, int H) {
-    if (g->work_H == H) return;
-    build_attn_work(g->sched, g->sched_h, H, g->work_buf, g->work_stage, g->ctx->st);
+void ensure_attn_work(parl_group_s* g, int H, int d) {
+    if (g->work_H == H && g->work_d == d) return;
+    build_attn_work(g->sched, g->sched_h, H, d, g->work_buf, g->work_stage, g->ctx->st);
     g->work_H = H;
+    g->work_d = d;
 }
 
 void alloc_group_arrays(parl_group_s* g) {
@@ -2124,7 +2159,7 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
             aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
             static DevBuf dbg_work;
             static HostStage dbg_wstage;
-            build_attn_work(aa.sched, hs, H, dbg_work, dbg_wstage, 0);
+            build_attn_work(aa.sched, hs, H, H * Dh, dbg_work, dbg_wstage, 0);
             cached = aa.sched;
             std::memcpy(key, k4, sizeof(k4));
         }
@@ -2181,7 +2216,7 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
             aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
             static DevBuf dbg_work;
             static HostStage dbg_wstage;
-            build_attn_work(aa.sched, hs, H, dbg_work, dbg_wstage, 0);
+            build_attn_work(aa.sched, hs, H, H * Dh, dbg_work, dbg_wstage, 0);
             cached = aa.sched;
             std::memcpy(key, k4, sizeof(k4));
         }

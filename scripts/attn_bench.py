@@ -1,4 +1,5 @@
-"""tcgen05 vs FFMA attention forward at C2 / C4-like shapes (CUDA events)."""
+"""tcgen05 vs FFMA attention forward / backward at C2 / C3-like shapes (CUDA events).
+   python scripts/attn_bench.py [c2|c3]   (default: both; the FFMA reference only where T < 20k)"""
 import ctypes as C, os, sys, math
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -6,7 +7,9 @@ from paper_2511_18871_b200 import parl as P
 f = P.LIB.parl_debug_attn_bf16
 f.restype = C.c_int
 f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 6
-for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
+SHAPES = {"c2": (512, 8, 1024, 14, 64), "c3": (1024, 16, 4096, 28, 128)}
+SEL = [SHAPES[a] for a in sys.argv[1:]] or list(SHAPES.values())
+for (Pl, G, R, H, Dh) in SEL:
     lens = [R] * G
     T = Pl + G * R
     seg = torch.zeros(T, dtype=torch.int32)
@@ -35,7 +38,9 @@ for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
 fb = P.LIB.parl_debug_attn_bwd_bf16
 fb.restype = C.c_int
 fb.argtypes = [C.c_int] * 5 + [C.c_void_p] * 9
-for (Pl, G, R, H, Dh) in [(512, 8, 1024, 14, 64), (1024, 16, 4096, 28, 128)]:
+SHAPES = {"c2": (512, 8, 1024, 14, 64), "c3": (1024, 16, 4096, 28, 128)}
+SEL = [SHAPES[a] for a in sys.argv[1:]] or list(SHAPES.values())
+for (Pl, G, R, H, Dh) in SEL:
     lens = [R] * G
     T = Pl + G * R
     seg = torch.zeros(T, dtype=torch.int32)
