@@ -351,7 +351,8 @@ struct PairSmem {
     static constexpr int OFF_Q = 0;                          // [QB buffers][2 tiles]
     static constexpr int OFF_K = OFF_Q + 2 * QB * TILE;      // [KVS]
     static constexpr int OFF_V = OFF_K + KVS * TILE;         // [KVS]
-    static constexpr int OFF_BAR = OFF_V + KVS * TILE;
+    static constexpr int OFF_OST = OFF_V + KVS * TILE;       // [8 softmax warps][32 rows x 128 B] output staging
+    static constexpr int OFF_BAR = OFF_OST + 8 * 4096;
     static constexpr int TOTAL = OFF_BAR + 256 + 1024;
 };
 
@@ -372,7 +373,8 @@ __device__ unsigned long long g_attn_trace[16][64][8];
 
 template <int DH>
 __global__ void __launch_bounds__(PAIR_NTHR, 1)
-    k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, AttnPairArgs a) {
+    k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_out,
+                    AttnPairArgs a) {
     static_assert(DH == 64 || DH == 128, "head dim");
     using L = PairSmem<DH>;
     // TMEM: Dh = 64: S0 | S1 | O0 | O1 | P0 | P1; Dh = 128: S0 | S1 | O0 | O1 with P_w written
@@ -387,12 +389,12 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     uint64_t* q_empty = bar + 2;                  // [2]
     uint64_t* kv_full = bar + 4;                  // [3]
     uint64_t* kv_empty = bar + 7;                 // [3]
-    uint64_t* s_full = bar + 10;                  // [2] per query tile
-    uint64_t* s_free = bar + 12;                  // [2]
-    uint64_t* p_full = bar + 14;                  // [2]
-    uint64_t* o_done = bar + 16;                  // [2]
-    uint64_t* o_free = bar + 18;                  // [2]
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 20);
+    uint64_t* s_full = bar + 10;                  // [2 tiles][2 S buffers] (Dh = 64: buffer 0 only)
+    uint64_t* s_free = bar + 14;                  // [2]
+    uint64_t* p_full = bar + 16;                  // [2]
+    uint64_t* o_done = bar + 18;                  // [2]
+    uint64_t* o_free = bar + 20;                  // [2]
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 22);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H;
@@ -401,7 +403,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int s = 0; s < 2; ++s) {
             tc::mbar_init(&q_full[s], 1);
             tc::mbar_init(&q_empty[s], 2);  // one release per MMA issuer
-            tc::mbar_init(&s_full[s], 1);
+            tc::mbar_init(&s_full[2 * s], 1);
+            tc::mbar_init(&s_full[2 * s + 1], 1);
             tc::mbar_init(&s_free[s], 4);
             tc::mbar_init(&p_full[s], 4);
             tc::mbar_init(&o_done[s], 1);
@@ -422,6 +425,267 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     const uint32_t t_s = tbase, t_o = tbase + 256, t_p = P_IN_S ? tbase : tbase + 256 + 2 * DH;
     pdl_wait();
     pdl_trigger();
+
+    // Item epilogue of a softmax warp: O / l (fp32, TMEM) -> bf16 rows of `out`, staged per
+    // warp through a 128B-swizzled 32 x 64 smem slab and written by TMA (coalesced; the
+    // rows past T are clipped by the tensor map), then lse.  Releases O after the last load.
+    auto store_out = [&](uint32_t t_ow, int w, int q4, int p, int h, int i, bool row_ok, float l, float m_used) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const uint32_t slab = tc::smem_u32(smem + L::OFF_OST + warp * 4096);
+#pragma unroll
+        for (int hc = 0; hc < DH / 64; ++hc) {
+            float o[64];
+            tc::tmem_ld32_nowait(t_ow + hc * 64, reinterpret_cast<uint32_t*>(o));
+            tc::tmem_ld32_nowait(t_ow + hc * 64 + 32, reinterpret_cast<uint32_t*>(o) + 32);
+            tc::tmem_ld_wait();
+            if (hc == DH / 64 - 1) {
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&o_free[w]);
+            }
+            if (lane == 0) tc::bulk_wait_read<0>();  // the slab's previous store has been read
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                tc::sts128(slab + lane * 128 + ((c ^ (lane & 7)) << 4), pack2(o[8 * c] * inv, o[8 * c + 1] * inv),
+                           pack2(o[8 * c + 2] * inv, o[8 * c + 3] * inv), pack2(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
+                           pack2(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+            tc::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tc::tma_store_2d(&tm_out, slab, h * DH + hc * 64, (2 * p + w) * 128 + q4 * 32);
+                tc::bulk_commit();
+            }
+        }
+        if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+    };
+
+    // ---- Dh = 128: key tiles are processed as two 64-key chunks so that each query tile
+    // has two S buffers (64 TMEM columns each) next to its 128-column O: the S MMA of the
+    // next chunk runs while the softmax works on the current one.  P (bf16, 32 columns)
+    // is written over its chunk's S buffer, which the S MMA two chunks later reuses only
+    // behind this chunk's PV (in-order tensor pipe).  s_full has one barrier per buffer.
+    auto mma_issuer_dh128 = [&]() {
+      if constexpr (DH == 128) {
+        const int w = warp - 9;
+        const uint32_t VIS = w ? VIS1 : VIS0;
+        constexpr uint32_t id_s = tc::idesc_bf16(128, 64, 0, 0);
+        constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);
+        const uint32_t t_sw = t_s + w * 128, t_ow = t_o + w * DH;
+        int cS = 0, cP = 0, nI = 0;  // chunk counters
+        const int k_end = a.w_ptr[blockIdx.x + 1];
+        int s_k = a.w_ptr[blockIdx.x], s_li = 0, s_e = 0, s_end = 0, gS = 0, s_h = 0;
+        auto s_load_item = [&]() {
+            if (s_k < k_end) {
+                const int p = a.w_items[s_k] / H;
+                s_e = a.p_ptr[p];
+                s_end = a.p_ptr[p + 1];
+            }
+        };
+        auto s_seek = [&]() -> bool {  // next visible (entry, chunk) of this tile
+            while (s_k < k_end) {
+                if (s_e >= s_end) {
+                    ++s_k;
+                    ++s_li;
+                    s_load_item();
+                    continue;
+                }
+                if ((uint32_t)a.p_list[s_e] & VIS) return true;
+                ++s_e;
+                ++gS;
+            }
+            return false;
+        };
+        s_load_item();
+        auto issue_s = [&]() {
+            const int st = gS % KVS, qb = s_li % QB;
+            tc::mbar_wait(&q_full[qb], (s_li / QB) & 1);
+            tc::mbar_wait(&kv_full[st], (gS / KVS) & 1);
+            tc::tc_fence_after();
+            const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE) + s_h * (64 * 128);
+            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + (qb * 2 + w) * L::TILE);
+#pragma unroll
+            for (int ks = 0; ks < DH / 16; ++ks) {
+                const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
+                tc::mma_bf16_e(t_sw + (cS & 1) * 64, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024),
+                               id_s, ks > 0);
+            }
+            tc::mma_commit_e(&s_full[2 * w + (cS & 1)]);
+            ATTN_TRACE(2 + w, cS, 0);
+            ++cS;
+            if (++s_h == 2) {
+                s_h = 0;
+                ++s_e;
+                ++gS;
+                // last S of this tile in the item: Q is no longer read (PV does not use it), so
+                // its buffer goes back to the TMA producer now, not after the item's last PV
+                bool more = false;
+                for (int e2 = s_e; e2 < s_end && !more; ++e2) more = ((uint32_t)a.p_list[e2] & VIS) != 0;
+                if (!more) tc::mma_commit_e(&q_empty[qb]);
+            }
+        };
+        // S of chunk n reuses the buffer of chunk n - 2: issued after PV(n - 2) (cS < cP + 2);
+        // within the K/V ring window and the Q buffers this issuer has released
+        auto advance_s = [&](int g_now, int li_now) {
+            while (cS < cP + 2 && s_seek() && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1) issue_s();
+        };
+        int g = 0, li = 0;
+        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
+            const int p = a.w_items[k] / H, qb = li % QB;
+            const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
+            bool started = false;
+            for (int e = ea; e < eb; ++e, ++g) {
+                const uint32_t f = (uint32_t)a.p_list[e];
+                const int st = g % KVS;
+                advance_s(g, li);
+                if (!(f & VIS)) {
+                    tc::mbar_wait(&kv_full[st], (g / KVS) & 1);
+                    if (lane == 0) tc::mbar_arrive(&kv_empty[st]);
+                    continue;
+                }
+                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    advance_s(g, li);
+                    ATTN_TRACE(2 + w, cP, 1);
+                    tc::mbar_wait(&p_full[w], cP & 1);
+                    if (!started && nI > 0) tc::mbar_wait(&o_free[w], (nI - 1) & 1);
+                    tc::tc_fence_after();
+                    ATTN_TRACE(2 + w, cP, 2);
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16_ts_e(t_ow, t_sw + (cP & 1) * 64 + ks * 8,
+                                          tc::sdesc(sv + h * (64 * 128) + ks * 2048, 128 * 128, 1024), id_o,
+                                          (started || ks > 0) ? 1u : 0u);
+                    tc::mma_commit_e(&o_done[w]);
+                    if (h == 1) tc::mma_commit_e(&kv_empty[st]);
+                    ++cP;
+                    if (!started) {
+                        started = true;
+                        ++nI;
+                    }
+                }
+                advance_s(g, li);
+            }
+            if (!started) {  // (released after the last S otherwise)
+                tc::mbar_wait(&q_full[qb], (li / QB) & 1);
+                if (lane == 0) tc::mbar_arrive(&q_empty[qb]);
+            }
+        }
+      }
+    };
+    auto softmax_dh128 = [&]() {
+      if constexpr (DH == 128) {
+        const int w = warp >> 2, q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        const uint32_t VIS = w ? VIS1 : VIS0, FULL = w ? FULL1 : FULL0;
+        const uint32_t t_sw = t_s + w * 128 + lane_off, t_ow = t_o + w * DH + lane_off;
+        const float c2 = a.scale_log2;
+        int cS = 0;
+        for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k) {
+            const int it = a.w_items[k];
+            const int p = it / H, h = it % H;
+            const int i = (2 * p + w) * 128 + r;
+            const bool row_ok = i < a.T;
+            const int seg_i = row_ok ? a.seg[i] : -1;
+            // allowed keys of row i: [0, e0) and [b1, e1) (model.cpp:242-245)
+            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
+            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
+            float m_used = -INFINITY, l = 0.f;
+            bool first = true;
+            for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e) {
+                const uint32_t f = (uint32_t)a.p_list[e];
+                if (!(f & VIS)) continue;
+#pragma unroll 1
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int buf = cS & 1;
+                    if (q4 == 0) ATTN_TRACE(w, cS, 0);
+                    tc::mbar_wait(&s_full[2 * w + buf], (cS >> 1) & 1);
+                    tc::tc_fence_after();
+                    if (q4 == 0) ATTN_TRACE(w, cS, 1);
+                    float sv[64];
+                    tc::tmem_ld32_nowait(t_sw + buf * 64, reinterpret_cast<uint32_t*>(sv));
+                    tc::tmem_ld32_nowait(t_sw + buf * 64 + 32, reinterpret_cast<uint32_t*>(sv) + 32);
+                    tc::tmem_ld_wait();
+                    if (q4 == 0) ATTN_TRACE(w, cS, 2);
+                    if (!(f & FULL)) {
+                        const int j0 = (int)(f & 0xffffff) * 128 + hc * 64;
+                        const int h0 = min(max(e0 - j0, 0), 64);
+                        const int l1 = min(max(b1 - j0, 0), 64), h1 = min(max(e1 - j0, 0), 64);
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) {
+                            const bool ok = (j < h0) | ((j >= l1) & (j < h1));
+                            sv[j] = ok ? sv[j] : -INFINITY;
+                        }
+                    }
+                    float mq[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mq[q] = fmaxf(sv[q], sv[q + 4]);
+#pragma unroll
+                    for (int j = 8; j < 64; j += 8) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) mq[q] = fmax3(mq[q], sv[j + 2 * q], sv[j + 2 * q + 1]);
+                    }
+                    const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                    const float mxl = mx * c2;
+                    const bool need = mxl > m_used + 8.f;
+                    const float m_new = need ? mxl : m_used;
+                    const float alpha = need ? tc::ex2_approx(m_used - m_new) : 1.f;
+                    const float mb = m_new == -INFINITY ? 0.f : m_new;
+                    float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int j = 0; j < 64; j += 4) {
+                        const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
+                        const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
+                        const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
+                        const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
+                        sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
+                        pk[j / 2] = pack2(p0, p1);
+                        pk[j / 2 + 1] = pack2(p2, p3);
+                    }
+                    if (q4 == 0) ATTN_TRACE(w, cS, 3);
+                    // the previous chunk's PV has finished writing O
+                    if (cS > 0) {
+                        tc::mbar_wait(&o_done[w], (cS - 1) & 1);
+                        tc::tc_fence_after();
+                    }
+                    if (q4 == 0) ATTN_TRACE(w, cS, 4);
+                    if (!first && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+                        for (int c = 0; c < DH / 32; ++c) {
+                            float o[32];
+                            tc::tmem_ld32(t_ow + c * 32, o);
+                            uint32_t wv[32];
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) wv[q] = __float_as_uint(o[q] * alpha);
+                            tc::tmem_st16(t_ow + c * 32, wv);
+                            tc::tmem_st16(t_ow + c * 32 + 16, wv + 16);
+                        }
+                    }
+                    tc::tmem_st16(t_sw + buf * 64, pk);
+                    tc::tmem_st16(t_sw + buf * 64 + 16, pk + 16);
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&p_full[w]);
+                    if (q4 == 0) ATTN_TRACE(w, cS, 5);
+                    l = l * alpha + ((sm0 + sm1) + (sm2 + sm3));
+                    m_used = m_new;
+                    first = false;
+                    ++cS;
+                }
+            }
+            if (first) continue;  // no key tile for this query tile (past the end)
+            tc::mbar_wait(&o_done[w], (cS - 1) & 1);
+            tc::tc_fence_after();
+            if (q4 == 0) ATTN_TRACE(w, cS - 1, 6);
+            store_out(t_ow, w, q4, p, h, i, row_ok, l, m_used);
+            if (q4 == 0) ATTN_TRACE(w, cS - 1, 7);
+        }
+      }
+    };
 
     if (warp >= 8) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
@@ -454,6 +718,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 }
             }
         }
+    } else if ((warp == 9 || warp == 10) && DH == 128) {
+        mma_issuer_dh128();
     } else if (warp == 9 || warp == 10) {  // whole warp; one elected lane issues
         // ---------------- MMA issuers: warp 9 serves query tile 0, warp 10 tile 1,
         // so neither softmax group waits on the other's progress.  K/V stages and
@@ -506,7 +772,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 tc::mma_bf16_e(t_s + w * 128, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s,
                                ks > 0);
             }
-            tc::mma_commit_e(&s_full[w]);
+            tc::mma_commit_e(&s_full[2 * w]);
             ATTN_TRACE(2 + w, cS, 0);
             ++cS;
             ++s_e;
@@ -560,6 +826,9 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             }
         }
       }
+    } else if (DH == 128) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+        softmax_dh128();
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
         // ---------------- softmax: warp group w = query tile w of the pair
@@ -584,7 +853,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const uint32_t f = (uint32_t)a.p_list[e];
                 if (!(f & VIS)) continue;
                 if (q4 == 0) ATTN_TRACE(w, cS, 0);
-                tc::mbar_wait(&s_full[w], cS & 1);
+                tc::mbar_wait(&s_full[2 * w], cS & 1);
                 tc::tc_fence_after();
                 if (q4 == 0) ATTN_TRACE(w, cS, 1);
                 float sv[128];
@@ -665,36 +934,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             // item epilogue: O / l -> out (bf16), lse; then release O to the next item
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16* dst = a.out + (long)i * a.ldo + h * DH;
-#pragma unroll
-            for (int hc = 0; hc < DH / 64; ++hc) {  // 64 columns at a time (register pressure)
-                float o[64];
-#pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    tc::tmem_ld32_nowait(t_o + w * DH + hc * 64 + c * 32 + lane_off,
-                                         reinterpret_cast<uint32_t*>(o) + 32 * c);
-                tc::tmem_ld_wait();
-                if (hc == DH / 64 - 1) {
-                    tc::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&o_free[w]);
-                }
-                if (row_ok) {
-#pragma unroll
-                    for (int q = 0; q < 64; q += 8) {
-                        uint4 v4;
-                        v4.x = pack2(o[q] * inv, o[q + 1] * inv);
-                        v4.y = pack2(o[q + 2] * inv, o[q + 3] * inv);
-                        v4.z = pack2(o[q + 4] * inv, o[q + 5] * inv);
-                        v4.w = pack2(o[q + 6] * inv, o[q + 7] * inv);
-                        *reinterpret_cast<uint4*>(dst + hc * 64 + q) = v4;
-                    }
-                }
-            }
-            if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+            store_out(t_o + w * DH + lane_off, w, q4, p, h, i, row_ok, l, m_used);
         }
     }
+    if (warp < 8 && lane == 0) tc::bulk_wait<0>();  // output stores complete before the CTA exits
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 9) {
@@ -1676,13 +1919,13 @@ void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
 }
 
 template <int DH>
-void launch_fwd_pair(const CUtensorMap& m, const AttnPairArgs& a, cudaStream_t st) {
+void launch_fwd_pair(const CUtensorMap& m, const CUtensorMap& mo, const AttnPairArgs& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_attn_fwd_pair<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem<DH>::TOTAL);
         attr = true;
     }
-    launch_pdl(k_attn_fwd_pair<DH>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<DH>::TOTAL, st, m, a);
+    launch_pdl(k_attn_fwd_pair<DH>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<DH>::TOTAL, st, m, mo, a);
     PARL_LAUNCHED();
 }
 
@@ -1828,8 +2071,17 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
         pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
         pa.scale_log2 = aa.scale * LOG2E;
         pa.out = out; pa.ldo = aa.ldo ? aa.ldo : aa.d; pa.lse = lse;
-        if (aa.Dh == 64) launch_fwd_pair<64>(m, pa, st);
-        else launch_fwd_pair<128>(m, pa, st);
+        // output tensor map: [T x d] bf16 with row stride ldo, 32 x 64 boxes, 128B swizzle
+        CUtensorMap mo;
+        cuuint64_t odims[2] = {(cuuint64_t)aa.d, (cuuint64_t)aa.T};
+        cuuint64_t ostr[1] = {(cuuint64_t)pa.ldo * 2};
+        cuuint32_t obox[2] = {64, 32};
+        if (fn(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, odims, ostr, obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return false;
+        if (aa.Dh == 64) launch_fwd_pair<64>(m, mo, pa, st);
+        else launch_fwd_pair<128>(m, mo, pa, st);
         return true;
     }
     if (aa.Dh == 64) launch_fwd<64>(m, a, st);

@@ -16,7 +16,8 @@ from paper_2511_18871_b200 import parl as P
 f = P.LIB.parl_debug_attn_bf16
 f.restype = C.c_int
 f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 6
-Pl, G, R, H, Dh = 512, 8, 1024, 14, 64
+# ATTN_SHAPE=c3: the C3 shape (Dh = 128)
+Pl, G, R, H, Dh = (1024, 16, 4096, 28, 128) if os.environ.get("ATTN_SHAPE") == "c3" else (512, 8, 1024, 14, 64)
 T = Pl + G * R
 seg = torch.zeros(T, dtype=torch.int32)
 st, en = [0], [Pl]
@@ -66,7 +67,8 @@ for w in range(2):
             break
         r = b[w, n, :6] - t0
         print(n, r, "dur", r[5] - r[0], "waitS", r[1] - r[0], "load", r[2] - r[1], "exp", r[3] - r[2],
-              "waitPV", r[4] - r[3], "store", r[5] - r[4])
+              "waitPV", r[4] - r[3], "store", r[5] - r[4],
+              ("item end: O ready %d, out written %d" % (b[w, n, 6] - t0, b[w, n, 7] - t0)) if b[w, n, 6] else "")
 for w in range(2 if not (len(sys.argv) > 1 and sys.argv[1] == "bwd") else 1):
     print(f"mma {w}: [S issued, PV wait begin, PV issued] - t0")
     for n in range(40):
