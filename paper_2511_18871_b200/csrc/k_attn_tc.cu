@@ -426,6 +426,31 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     pdl_wait();
     pdl_trigger();
 
+    // Per-row metadata of a softmax item (prefetched one item ahead): pair p, head h, row i,
+    // the row's allowed key ranges [0, e0) u [b1, e1) (model.cpp:242-245), the pair's entry
+    // range and its first entry
+    struct ItemMeta {
+        int p, h, i, e0, b1, e1, ea, eb;
+        uint32_t f0;
+    };
+    auto fetch_item = [&](int k, int k_end, int w, int r) -> ItemMeta {
+        ItemMeta m{0, 0, a.T, 0, 0, 0, 0, 0, 0u};
+        if (k >= k_end) return m;
+        const int it = a.w_items[k];
+        m.p = it / H;
+        m.h = it % H;
+        m.i = (2 * m.p + w) * 128 + r;
+        const bool row_ok = m.i < a.T;
+        const int seg_i = row_ok ? a.seg[m.i] : -1;
+        m.e0 = !row_ok ? 0 : (seg_i == 0 ? m.i + 1 : a.Peff);
+        m.b1 = seg_i > 0 ? a.seg_start[seg_i] : 0;
+        m.e1 = seg_i > 0 ? m.i + 1 : 0;
+        m.ea = a.p_ptr[m.p];
+        m.eb = a.p_ptr[m.p + 1];
+        m.f0 = m.ea < m.eb ? (uint32_t)a.p_list[m.ea] : 0u;
+        return m;
+    };
+
     // Item epilogue of a softmax warp: O / l (fp32, TMEM) -> bf16 rows of `out`, staged per
     // warp through a 128B-swizzled 32 x 64 smem slab and written by TMA (coalesced; the
     // rows past T are clipped by the tensor map), then lse.  Releases O after the last load.
@@ -583,19 +608,17 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const uint32_t t_sw = t_s + w * 128 + lane_off, t_ow = t_o + w * DH + lane_off;
         const float c2 = a.scale_log2;
         int cS = 0;
-        for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k) {
-            const int it = a.w_items[k];
-            const int p = it / H, h = it % H;
-            const int i = (2 * p + w) * 128 + r;
+        const int k_end = a.w_ptr[blockIdx.x + 1];
+        ItemMeta nx = fetch_item(a.w_ptr[blockIdx.x], k_end, w, r);
+        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k) {
+            const ItemMeta cur = nx;
+            nx = fetch_item(k + 1, k_end, w, r);  // the next item's chain of dependent loads, off the critical path
+            const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
-            const int seg_i = row_ok ? a.seg[i] : -1;
-            // allowed keys of row i: [0, e0) and [b1, e1) (model.cpp:242-245)
-            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
-            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
             float m_used = -INFINITY, l = 0.f;
             bool first = true;
-            for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e) {
-                const uint32_t f = (uint32_t)a.p_list[e];
+            for (int e = cur.ea; e < cur.eb; ++e) {
+                const uint32_t f = e == cur.ea ? cur.f0 : (uint32_t)a.p_list[e];
                 if (!(f & VIS)) continue;
 #pragma unroll 1
                 for (int hc = 0; hc < 2; ++hc) {
@@ -838,19 +861,17 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const uint32_t VIS = w ? VIS1 : VIS0, FULL = w ? FULL1 : FULL0;
         const float c2 = a.scale_log2;
         int cS = 0;
-        for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k) {
-            const int it = a.w_items[k];
-            const int p = it / H, h = it % H;
-            const int i = (2 * p + w) * 128 + r;
+        const int k_end = a.w_ptr[blockIdx.x + 1];
+        ItemMeta nx = fetch_item(a.w_ptr[blockIdx.x], k_end, w, r);
+        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k) {
+            const ItemMeta cur = nx;
+            nx = fetch_item(k + 1, k_end, w, r);  // the next item's chain of dependent loads, off the critical path
+            const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
-            const int seg_i = row_ok ? a.seg[i] : -1;
-            // allowed keys of row i: [0, e0) and [b1, e1) (model.cpp:242-245)
-            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
-            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
             float m_used = -INFINITY, l = 0.f;
             bool first = true;
-            for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e) {
-                const uint32_t f = (uint32_t)a.p_list[e];
+            for (int e = cur.ea; e < cur.eb; ++e) {
+                const uint32_t f = e == cur.ea ? cur.f0 : (uint32_t)a.p_list[e];
                 if (!(f & VIS)) continue;
                 if (q4 == 0) ATTN_TRACE(w, cS, 0);
                 tc::mbar_wait(&s_full[2 * w], cS & 1);
