@@ -333,6 +333,17 @@ struct Scratch {
         return p;
     }
 } g_colsum_scratch;
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 }  // namespace
 
 template <class T>
@@ -822,6 +833,10 @@ void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const f
     if (v4 && D <= 512) launch_pdl(k_layernorm4<T, 4>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (v4 && D <= 896) launch_pdl(k_layernorm4<T, 7>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (v4 && D <= 1024) launch_pdl(k_layernorm4<T, 8>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 1536) launch_pdl(k_layernorm4<T, 12>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 2048) launch_pdl(k_layernorm4<T, 16>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 3584) launch_pdl(k_layernorm4<T, 28>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
+    else if (v4 && D <= 4096) launch_pdl(k_layernorm4<T, 32>, dim3(cdiv(R, 8)), dim3(256), 0, st, x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 256) k_layernorm<T, 8><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 1024) k_layernorm<T, 32><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
     else if (D <= 2048) k_layernorm<T, 64><<<cdiv(R, 8), 256, 0, st>>>(x, rows, R, D, g, b, y, ldy, mean, rstd);
@@ -930,6 +945,187 @@ __global__ void __launch_bounds__(256) k_ln_bwd_rows4(const float* __restrict__ 
     }
 }
 
+// LayerNorm backward with the gamma / beta gradients fused (d <= 1024): persistent warps
+// over rows accumulate dgamma = sum dy * xhat and dbeta = sum dy for their lane's columns
+// in registers; each block then reduces its 8 warps in shared memory and writes one
+// partial row (k_colsum_final adds the partials in block order: deterministic).
+template <class T, int P4>
+__global__ void __launch_bounds__(256) k_ln_bwd_rows4_cs(const float* __restrict__ dy, const float* __restrict__ x,
+                                                       const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                                       const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                                       int R, int D, const float* __restrict__ res,
+                                                       float* __restrict__ dx, T* __restrict__ dx_act,
+                                                       float* __restrict__ part_a, float* __restrict__ part_b) {
+    // per-warp column partials in shared memory: [2][8 warps][D / 4] float4 (each element owned by one lane)
+    extern __shared__ float4 red[];
+    pdl_wait();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int D4 = D >> 2;
+    float4* sga = red + wib * D4;
+    float4* sgb = red + (8 + wib) * D4;
+    for (int c = lane; c < D4; c += 32) sga[c] = sgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    for (int r = blockIdx.x * 8 + wib; r < R; r += gridDim.x * 8) {
+        const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
+        const float4* dyr = reinterpret_cast<const float4*>(dy + (long)r * D);
+        float4 vy[P4], vx[P4];
+#pragma unroll
+        for (int k = 0; k < P4; ++k) {
+            const int c = lane + 32 * k;
+            const bool ok = c < D4;
+            vy[k] = ok ? dyr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            vx[k] = ok ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const float mu = mean[r], rs = rstd[r];
+        float sa = 0.f, sb = 0.f;
+#pragma unroll
+        for (int k = 0; k < P4; ++k) {
+            const int c = lane + 32 * k;
+            vx[k].x = (vx[k].x - mu) * rs; vx[k].y = (vx[k].y - mu) * rs;     // xhat
+            vx[k].z = (vx[k].z - mu) * rs; vx[k].w = (vx[k].w - mu) * rs;
+            if (c < D4) {
+                const float4 g = __ldg(g4 + c);
+                float4 a = sga[c], b = sgb[c];
+                a.x += vy[k].x * vx[k].x; a.y += vy[k].y * vx[k].y;           // dgamma
+                a.z += vy[k].z * vx[k].z; a.w += vy[k].w * vx[k].w;
+                b.x += vy[k].x; b.y += vy[k].y; b.z += vy[k].z; b.w += vy[k].w;  // dbeta
+                sga[c] = a;
+                sgb[c] = b;
+                vy[k].x *= g.x; vy[k].y *= g.y; vy[k].z *= g.z; vy[k].w *= g.w;  // dxh
+            }
+            sa += (vy[k].x + vy[k].y) + (vy[k].z + vy[k].w);
+            sb += (vy[k].x * vx[k].x + vy[k].y * vx[k].y) + (vy[k].z * vx[k].z + vy[k].w * vx[k].w);
+        }
+        sa = warp_sum(sa) / D;
+        sb = warp_sum(sb) / D;
+        const float4* rr = res ? reinterpret_cast<const float4*>(res + (long)r * D) : nullptr;
+#pragma unroll
+        for (int k = 0; k < P4; ++k) {
+            const int c = lane + 32 * k;
+            if (c < D4) {
+                const float4 rv = rr ? rr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 v;
+                v.x = rs * (vy[k].x - sa - vx[k].x * sb) + rv.x;
+                v.y = rs * (vy[k].y - sa - vx[k].y * sb) + rv.y;
+                v.z = rs * (vy[k].z - sa - vx[k].z * sb) + rv.z;
+                v.w = rs * (vy[k].w - sa - vx[k].w * sb) + rv.w;
+                reinterpret_cast<float4*>(dx + (long)r * D)[c] = v;
+                if (dx_act) store4<T>(dx_act + (long)r * D + 4 * c, v);
+            }
+        }
+    }
+    __syncthreads();
+    // block reduction over the 8 warps, in warp order
+    for (int c = threadIdx.x; c < 2 * D4; c += 256) {
+        const int pass = c >= D4, cc = c - pass * D4;
+        const float4* src = red + pass * 8 * D4 + cc;
+        float4 t = src[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) {
+            const float4 u = src[q * D4];
+            t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+        }
+        reinterpret_cast<float4*>((pass ? part_b : part_a) + (long)blockIdx.x * D)[cc] = t;
+    }
+}
+
+// resident blocks per SM of the fused kernel (registers / shared memory bound)
+template <class T, int P4>
+int ln_bwd_cs_occupancy(int D) {
+    static int occ[2] = {0, 0};
+    static int last_d = -1;
+    if (last_d != D) {
+        cudaFuncSetAttribute(k_ln_bwd_rows4_cs<T, P4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8 * 256 * 16);
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ln_bwd_rows4_cs<T, P4>, 256, (size_t)2 * 8 * (D / 4) * 16);
+        occ[0] = n > 0 ? n : 1;
+        last_d = D;
+    }
+    return occ[0];
+}
+
+// out[c] += sum_s part_a[s][c] (out2 likewise) for many partial rows: 32 columns x 8 row
+// groups per block, the groups combined in a fixed order (deterministic)
+__global__ void __launch_bounds__(256) k_colsum_final8(const float* __restrict__ part_a, const float* __restrict__ part_b,
+                                                      int splits, int N, float* __restrict__ out, float* __restrict__ out2) {
+    __shared__ float sa[8][33], sb[8][33];
+    pdl_wait();
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + tx;
+    float a = 0.f, b = 0.f;
+    if (c < N) {
+#pragma unroll 4
+        for (int s0 = ty; s0 < splits; s0 += 8) {
+            a += part_a[(long)s0 * N + c];
+            b += part_b[(long)s0 * N + c];
+        }
+    }
+    sa[ty][tx] = a;
+    sb[ty][tx] = b;
+    __syncthreads();
+    if (ty == 0 && c < N) {
+        float ta = 0.f, tb = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            ta += sa[q][tx];
+            tb += sb[q][tx];
+        }
+        out[c] += ta;
+        out2[c] += tb;
+    }
+}
+
+template <class T, int P4>
+void launch_ln_bwd_cs(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
+                      const float* gamma, int R, int D, const float* res, float* dx, T* dx_act, float* pa, float* pb,
+                      int grid, cudaStream_t st) {
+    const size_t smem = (size_t)2 * 8 * (D / 4) * 16;
+    launch_pdl(k_ln_bwd_rows4_cs<T, P4>, dim3(grid), dim3(256), smem, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx,
+               dx_act, pa, pb);
+    PARL_LAUNCHED();
+}
+
+// Wide rows (d > 1024: C3 / C4): the same math in two passes over the row (sums, then
+// outputs), so nothing is held in registers; the second pass re-reads dy / x from L2.
+template <class T>
+__global__ void __launch_bounds__(256) k_ln_bwd_rows4_2p(const float* __restrict__ dy, const float* __restrict__ x,
+                                                         const int32_t* __restrict__ rows, const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, const float* __restrict__ gamma,
+                                                         int R, int D, const float* __restrict__ res,
+                                                         float* __restrict__ dx, T* __restrict__ dx_act) {
+    pdl_wait();
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const int D4 = D >> 2;
+    const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
+    const float4* dyr = reinterpret_cast<const float4*>(dy + (long)r * D);
+    const float4* rr = res ? reinterpret_cast<const float4*>(res + (long)r * D) : nullptr;
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    const float mu = mean[r], rs = rstd[r];
+    float sa = 0.f, sb = 0.f;
+#pragma unroll 4
+    for (int c = lane; c < D4; c += 32) {
+        const float4 g = __ldg(g4 + c), yv = dyr[c], xv = xr[c];
+        const float a0 = yv.x * g.x, a1 = yv.y * g.y, a2 = yv.z * g.z, a3 = yv.w * g.w;
+        sa += (a0 + a1) + (a2 + a3);
+        sb += (a0 * (xv.x - mu) + a1 * (xv.y - mu)) + (a2 * (xv.z - mu) + a3 * (xv.w - mu));
+    }
+    sa = warp_sum(sa) / D;
+    sb = warp_sum(sb) * rs / D;
+#pragma unroll 4
+    for (int c = lane; c < D4; c += 32) {
+        const float4 g = __ldg(g4 + c), yv = dyr[c], xv = xr[c];
+        const float4 rv = rr ? rr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 v;
+        v.x = rs * (yv.x * g.x - sa - (xv.x - mu) * rs * sb) + rv.x;
+        v.y = rs * (yv.y * g.y - sa - (xv.y - mu) * rs * sb) + rv.y;
+        v.z = rs * (yv.z * g.z - sa - (xv.z - mu) * rs * sb) + rv.z;
+        v.w = rs * (yv.w * g.w - sa - (xv.w - mu) * rs * sb) + rv.w;
+        reinterpret_cast<float4*>(dx + (long)r * D)[c] = v;
+        if (dx_act) store4<T>(dx_act + (long)r * D + 4 * c, v);
+    }
+}
+
 template <class T>
 void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
                           const float* gamma, int R, int D, const float* res, float* dx, T* dx_act, float* dgamma,
@@ -937,9 +1133,27 @@ void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, 
     if (R <= 0) return;
     const int blocks = cdiv(R, 8);
     if (D % 4 == 0 && D <= 1024) {
+        // fused dgamma / dbeta: persistent blocks (all resident at once), one partial row per block
+        const int occ = D <= 512 ? ln_bwd_cs_occupancy<T, 4>(D) : D <= 896 ? ln_bwd_cs_occupancy<T, 7>(D)
+                                                                            : ln_bwd_cs_occupancy<T, 8>(D);
+        const int grid = std::min(blocks, occ * num_sms());
+        float* pa = g_colsum_scratch.get((size_t)2 * grid * D);
+        float* pb = pa + (size_t)grid * D;
+        if (D <= 512) launch_ln_bwd_cs<T, 4>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
+        else if (D <= 896) launch_ln_bwd_cs<T, 7>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
+        else launch_ln_bwd_cs<T, 8>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
+        launch_pdl(k_colsum_final8, dim3(cdiv(D, 32)), dim3(256), 0, st, (const float*)pa, (const float*)pb, grid, D,
+                   dgamma, dbeta);
+        PARL_LAUNCHED();
+        return;
+    }
+    if (D % 4 == 0 && D <= 1024) {
         if (D <= 512) launch_pdl(k_ln_bwd_rows4<T, 4>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
         else if (D <= 896) launch_pdl(k_ln_bwd_rows4<T, 7>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
         else launch_pdl(k_ln_bwd_rows4<T, 8>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
+    } else if (D % 4 == 0) {
+        launch_pdl(k_ln_bwd_rows4_2p<T>, dim3(blocks), dim3(256), 0, st, dy, x, rows, mean, rstd, gamma, R, D, res, dx,
+                   dx_act);
     } else if (D <= 256) k_ln_bwd_rows<T, 8><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
     else if (D <= 512) k_ln_bwd_rows<T, 16><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
     else if (D <= 768) k_ln_bwd_rows<T, 24><<<blocks, 256, 0, st>>>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act);
