@@ -127,6 +127,12 @@ uint64_t parl_model_version(parl_model_t m);
  * load_checkpoint (model.cpp:924-987).  IoError on open / magic / truncation / layout
  * mismatch, NumericError on non-finite weights, ConfigError on an invalid header config.
  * load creates a new model on ctx holding the stored weights and version. */
+/* sample_tokens (model.cpp:843-900): up to max_new_tokens sampled after `prompt` (greedy at
+ * temperature 0, else softmax(logits / temperature) with the reference RNG stream), stopping
+ * after kEosToken; out[max_new_tokens], *n_out = tokens written.  Same errors as the
+ * reference (ShapeError / ConfigError / VocabError). */
+parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int prompt_len,
+                               int max_new_tokens, double temperature, uint64_t rng_seed, int32_t* out, int* n_out);
 parl_status parl_checkpoint_save(parl_model_t m, const char* path);
 parl_status parl_model_config(parl_model_t m, parl_config* out);
 parl_status parl_checkpoint_load(parl_ctx_t ctx, const char* path, parl_model_t* out);

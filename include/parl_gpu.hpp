@@ -194,6 +194,18 @@ private:
     std::shared_ptr<parl_grad_s> h_;
 };
 
+// sample_tokens (model.cpp:843-900)
+inline std::vector<TokenId> sample_tokens(const ModelParams& params, std::span<const TokenId> prompt,
+                                          int max_new_tokens, double temperature, std::uint64_t rng_seed) {
+    std::vector<TokenId> out(std::max(max_new_tokens, 1));
+    int n = 0;
+    check(parl_sample_tokens(params.device().ctx(), params.handle(), prompt.data(), (int)prompt.size(),
+                             max_new_tokens, temperature, rng_seed, out.data(), &n),
+          params.device().ctx());
+    out.resize(n);
+    return out;
+}
+
 inline void save_checkpoint(const std::string& path, const ModelParams& params) { params.save(path); }
 inline ModelParams load_checkpoint(const std::string& path, Device& dev = Device::get()) {
     return ModelParams::load(path, dev);

@@ -108,6 +108,18 @@ class Oracle:
         self._chk(self.lib.ref_save_checkpoint(C.byref(c), _p(_f64(w)), C.c_ulonglong(seed), os.fsencode(path)),
                   "save_checkpoint")
 
+    def sample_tokens(self, cfg: Cfg, w, prompt, max_new: int, temperature: float, seed: int):
+        """The reference's sample_tokens (model.cpp:843-900)."""
+        assert self.kind == "ref"
+        c = cfg.c()
+        out = np.zeros(max(max_new, 1), dtype=np.int32)
+        pr = _i32(prompt)
+        self.lib.ref_sample_tokens.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double,
+                                               C.c_ulonglong, C.c_void_p]
+        n = self._chk(self.lib.ref_sample_tokens(C.byref(c), _p(_f64(w)), _p(pr), len(pr), max_new, temperature,
+                                                 C.c_ulonglong(seed), _p(out)), "sample_tokens")
+        return out[:n]
+
     def load_checkpoint(self, path: str):
         """The reference's load_checkpoint (model.cpp:948-987): (Cfg, version, seed, flat)."""
         assert self.kind == "ref"

@@ -61,6 +61,8 @@ def main(only=None):
         return _c2w(ref)
     if only == "ckpt":
         return _ckpt(ref)
+    if only == "sample":
+        return _sample(ref)
 
     # ---- tiny: packed forward/backward with an arbitrary upstream -------------
     w = ref.init_params(TINY, 41)
@@ -109,6 +111,24 @@ def main(only=None):
                         rewards=rewards, advantages=adv, stats=st, lp3=lp3, grad_names=names, grad_sums=sums,
                         grad_l2=l2, grad_idx=idx, grad_vals=vals, param_sum=w1.sum(), param_head=w1[:64])
     _c2w(ref)
+
+
+def _sample(ref):
+    """sample_tokens (model.cpp:843-900) of the reference: tiny model (init seed 41) and C1
+    width (seed 7), greedy and temperature runs."""
+    runs = []
+    for name, cfg, wseed in (("tiny", TINY, 41), ("c1", C1, 7)):
+        w = ref.init_params(cfg, wseed)
+        prompt = np.random.default_rng(5).integers(4, cfg.vocab, 6).astype(np.int32)
+        for temp, seed in ((0.0, 0), (0.8, 11), (1.5, 12)):
+            toks = ref.sample_tokens(cfg, w, prompt, 24, temp, seed)
+            runs.append((name, wseed, temp, seed, prompt, toks))
+    np.savez_compressed(os.path.join(GOLDEN, "sample_tokens.npz"),
+                        names=np.array([r[0] for r in runs]), wseeds=np.array([r[1] for r in runs]),
+                        temps=np.array([r[2] for r in runs]), seeds=np.array([r[3] for r in runs]),
+                        prompts=np.stack([r[4] for r in runs]),
+                        tokens=np.array([np.pad(r[5], (0, 24 - len(r[5])), constant_values=-1) for r in runs]))
+    print("wrote sample_tokens.npz", [len(r[5]) for r in runs])
 
 
 def _ckpt(ref):

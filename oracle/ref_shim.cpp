@@ -272,6 +272,17 @@ long ref_load_checkpoint(const char* path, CCfg* c, double* w, unsigned long lon
     }
 }
 
+// sample_tokens (model.cpp:843-900).  Returns the number of tokens written to out.
+int ref_sample_tokens(const CCfg* c, const double* w, const int* prompt, int P, int max_new, double temperature,
+                      unsigned long long seed, int* out) {
+    return guarded([&] {
+        ModelParams p = params_from(c, w);
+        auto toks = sample_tokens(p, std::span<const TokenId>(prompt, P), max_new, temperature, seed);
+        std::copy(toks.begin(), toks.end(), out);
+        return (int)toks.size();
+    });
+}
+
 // CPU baseline: `threads` independent workers, each with its own TriModel
 // (SPEC.md:113 allows distinct instances concurrently), each running `reps`
 // shared-prompt micro-batches of P + G x R tokens with random tokens in

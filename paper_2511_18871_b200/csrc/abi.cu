@@ -1839,6 +1839,97 @@ parl_status parl_ctx_set_recompute(parl_ctx_t ctx, int mode) {
 
 int parl_act_recompute(parl_act_t a) { return a && a->recompute ? 1 : 0; }
 
+// sample_tokens (model.cpp:843-900): autoregressive sampling from the model.  Each step
+// runs the causal forward over the sequence so far (as the reference does) with the LM
+// head on the last row only (fp32 logits of the compute path), and chooses the token on
+// the host with the reference's own fp64 arithmetic and RNG stream: greedy argmax (lowest
+// id on ties) at temperature 0, else inverse-CDF sampling of softmax(logits / temperature)
+// with Rng(mix_seed(seed, "sample")).uniform() (rng.hpp).  Stops after kEosToken.
+parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int P, int max_new_tokens,
+                               double temperature, uint64_t rng_seed, int32_t* out, int* n_out) {
+    return guarded(ctx, [&] {
+        const auto& c = m->cfg;
+        PARL_REQUIRE(P > 0, PARL_E_SHAPE, "empty prompt");
+        PARL_REQUIRE(max_new_tokens >= 0, PARL_E_CONFIG, "max_new_tokens must be >= 0");
+        PARL_REQUIRE(temperature >= 0.0, PARL_E_CONFIG, "temperature must be >= 0");
+        PARL_REQUIRE(P + max_new_tokens <= c.max_seq_len, PARL_E_SHAPE, "prompt + max_new_tokens exceeds max_seq_len");
+        for (int t = 0; t < P; ++t)
+            PARL_REQUIRE(prompt[t] >= 0 && prompt[t] < c.vocab_size, PARL_E_VOCAB, "token id out of vocabulary");
+        *n_out = 0;
+        if (max_new_tokens == 0) return;
+        auto sm64 = [](uint64_t x) {
+            x += 0x9e3779b97f4a7c15ull;
+            x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+            x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+            return x ^ (x >> 31);
+        };
+        std::mt19937_64 eng(sm64(sm64(sm64(rng_seed) ^ (0x9e3779b97f4a7c15ull + 0x73616d706c65ull))));
+        const int V = c.vocab_size, maxT = P + max_new_tokens;
+        parl_group_s g;
+        g.ctx = ctx;
+        g.max_T = maxT;
+        g.max_G = 1;
+        alloc_group_arrays(&g);
+        std::vector<int32_t> seq(prompt, prompt + P);
+        std::vector<int32_t> pos(maxT), zeros(maxT, 0);
+        for (int t = 0; t < maxT; ++t) pos[t] = t;
+        cudaStream_t st = ctx->st;
+        PARL_CUDA(cudaMemcpyAsync(g.pk.positions, pos.data(), maxT * 4, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaMemcpyAsync(g.pk.seg, zeros.data(), maxT * 4, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaMemcpyAsync(g.pk.scored_label, zeros.data(), 4, cudaMemcpyHostToDevice, st));
+        std::vector<float> row(V);
+        std::vector<double> w(V);
+        for (int step = 0; step < max_new_tokens; ++step) {
+            const int T = (int)seq.size();
+            const int32_t last = T - 1;
+            PARL_CUDA(cudaMemcpyAsync(g.pk.tokens, seq.data(), T * 4, cudaMemcpyHostToDevice, st));
+            PARL_CUDA(cudaMemcpyAsync(g.pk.pred_pos, &last, 4, cudaMemcpyHostToDevice, st));
+            g.T = T; g.P = T; g.G = 0; g.S = 1; g.Peff = T; g.n_samples = 1;
+            g.pairs = (double)T * (T + 1) / 2;
+            g.lens.clear(); g.span_start.clear(); g.cu = {0, 1};
+            g.vocab = V; g.max_seq = c.max_seq_len;
+            ++g.epoch;
+            upload_meta(&g);
+            int slot = 0;
+            if (ctx->prec == PARL_PREC_BF16) forward_impl<bf16>(ctx, &m, &slot, 1, &g, nullptr, true);
+            else forward_impl<float>(ctx, &m, &slot, 1, &g, nullptr, true);
+            ++m->forward_gen;  // bump_forward_generation (model.cpp:865)
+            PARL_CUDA(cudaMemcpyAsync(row.data(), ctx->scr[0].logits.p, (size_t)V * 4, cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaStreamSynchronize(st));
+            int32_t chosen = 0;
+            if (temperature == 0.0) {
+                double best = row[0];
+                for (int v = 1; v < V; ++v)
+                    if ((double)row[v] > best) {  // strict: lowest id wins ties
+                        best = row[v];
+                        chosen = v;
+                    }
+            } else {
+                double maxv = row[0];
+                for (int v = 1; v < V; ++v) maxv = std::max(maxv, (double)row[v]);
+                double z = 0.0;
+                for (int v = 0; v < V; ++v) {
+                    w[v] = std::exp(((double)row[v] - maxv) / temperature);
+                    z += w[v];
+                }
+                const double target = (double)(eng() >> 11) * 0x1.0p-53 * z;
+                double acc = 0.0;
+                chosen = V - 1;
+                for (int v = 0; v < V; ++v) {
+                    acc += w[v];
+                    if (target < acc) {
+                        chosen = v;
+                        break;
+                    }
+                }
+            }
+            out[(*n_out)++] = chosen;
+            seq.push_back(chosen);
+            if (chosen == 2) break;  // kEosToken (model.hpp:18)
+        }
+    });
+}
+
 parl_status parl_act_destroy(parl_act_t a) {
     delete a;
     return PARL_OK;

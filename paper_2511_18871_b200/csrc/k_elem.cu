@@ -8,6 +8,7 @@
 //   K11 embedding-grad reduce  model.cpp:825-834 (deterministic: stable sort + segmented sum)
 // plus column reductions (bias / LN parameter grads), weight conversion,
 // device init, SGD update.
+#include <cstdlib>
 #include <type_traits>
 #include <algorithm>
 #include <cub/cub.cuh>
@@ -1132,7 +1133,11 @@ void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, 
                           float* dbeta, cudaStream_t st) {
     if (R <= 0) return;
     const int blocks = cdiv(R, 8);
-    if (D % 4 == 0 && D <= 1024) {
+    static const bool fused = [] {
+        const char* e = std::getenv("PARL_LN_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (fused && D % 4 == 0 && D <= 1024) {
         // fused dgamma / dbeta: persistent blocks (all resident at once), one partial row per block
         const int occ = D <= 512 ? ln_bwd_cs_occupancy<T, 4>(D) : D <= 896 ? ln_bwd_cs_occupancy<T, 7>(D)
                                                                             : ln_bwd_cs_occupancy<T, 8>(D);

@@ -130,6 +130,7 @@ def _load():
         "parl_grad_allreduce": [vp, vp], "parl_stats_allreduce": [vp],
         "parl_checkpoint_save": [vp, C.c_char_p], "parl_checkpoint_load": [vp, C.c_char_p, C.POINTER(vp)],
         "parl_model_config": [vp, C.POINTER(_Config)],
+        "parl_sample_tokens": [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_uint64, vp, C.POINTER(C.c_int)],
         "parl_ctx_profile": [vp, C.c_int], "parl_ctx_set_recompute": [vp, C.c_int], "parl_act_recompute": [vp],
         "parl_ctx_profile_read": [vp, C.c_int, f64p, f64p, C.POINTER(C.c_long)],
     }
@@ -519,6 +520,19 @@ def pack_group(prompt, responses, max_seq_len: int, ctx: Optional[Context] = Non
                        AttentionMaskSpec.shared_prompt(len(prompt), group.response_lens), spans, group)
 
 
+def sample_tokens(params: "ModelParams", prompt, max_new_tokens: int, temperature: float = 0.0,
+                  rng_seed: int = 0) -> np.ndarray:
+    """sample_tokens (model.cpp:843-900) on the device forward; token choice on the host with the
+    reference's fp64 arithmetic and RNG stream."""
+    pr = np.ascontiguousarray(np.asarray(prompt, dtype=np.int32))
+    out = np.zeros(max(int(max_new_tokens), 1), dtype=np.int32)
+    n = C.c_int(0)
+    _check(LIB.parl_sample_tokens(params.ctx.h, params.h, pr.ctypes.data_as(C.c_void_p), len(pr), int(max_new_tokens),
+                                  float(temperature), int(rng_seed), out.ctypes.data_as(C.c_void_p), C.byref(n)),
+           params.ctx.h)
+    return out[:n.value]
+
+
 def extract_response_logprobs(logprobs, packed: PackedGroup):
     """packing.cpp:74-89."""
     expected = sum(n for _, n in packed.spans)
@@ -570,6 +584,18 @@ def forward_logprobs(params: ModelParams, tokens, positions, mask: AttentionMask
     _check(LIB.parl_forward(params.ctx.h, params.h, g.h, slot, C.byref(act) if want_cache else None), params.ctx.h)
     d = g.download()
     return ForwardResult(g.logprobs(slot), d["scored_pos"], Activations(act) if want_cache else None, g)
+
+
+def score_logprobs(params: ModelParams, prompt, response) -> np.ndarray:
+    """RolloutService::score_logprobs (rollout.cpp:52-66): log-probs of the response tokens
+    under a causal forward over prompt || response (the rollout-side old log-probs)."""
+    if len(response) == 0:
+        return np.zeros(0)
+    toks = np.concatenate([np.asarray(prompt, np.int32), np.asarray(response, np.int32)])
+    labels = np.full(len(toks), -1, np.int32)
+    labels[len(prompt):] = np.asarray(response, np.int32)
+    return forward_logprobs(params, toks, np.arange(len(toks), dtype=np.int32), AttentionMaskSpec.causal(),
+                            labels).logprobs
 
 
 def forward_logprob_rows(params: ModelParams, tokens, positions, mask: AttentionMaskSpec) -> np.ndarray:
