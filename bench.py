@@ -305,6 +305,8 @@ def run_ours(args, c):
         grads.reset()
         for i in range(ng):
             group.pack_device(d_prompts[i].data_ptr(), Pn, d_resps[i].data_ptr(), lens, c["max_seq"])
+            if world > 1 and i == ng - 1:
+                grads.allreduce_overlap()  # the last backward streams its gradient slices to NCCL
             P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=False)
         if world > 1:
             grads.allreduce()
@@ -319,6 +321,8 @@ def run_ours(args, c):
         st = None
         for i in range(ng):
             group.pack(h_prompts[i], [h_resps[i][offs[k]:offs[k + 1]] for k in range(G)], c["max_seq"])
+            if world > 1 and i == ng - 1:
+                grads.allreduce_overlap()
             st = P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=True)
         if world > 1:
             grads.allreduce()

@@ -222,6 +222,12 @@ parl_status parl_comm_unique_id(char id[PARL_NCCL_ID_BYTES]);
 parl_status parl_comm_init(parl_ctx_t ctx, const char id[PARL_NCCL_ID_BYTES], int rank, int nranks);
 parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr);
 parl_status parl_stats_allreduce(parl_ctx_t ctx);
+/* Arm an overlapped gradient allreduce: the next parl_backward into `grad` (the last
+ * micro-batch of the optimizer step) hands every gradient slice to NCCL on a second stream
+ * as soon as it is final (head + final LN first, each layer after its LN1 backward), so the
+ * exchange overlaps the rest of the backward; parl_grad_allreduce then reduces the
+ * embeddings and joins the streams.  Same sum as one allreduce of the whole buffer. */
+parl_status parl_grad_allreduce_overlap(parl_ctx_t ctx, parl_grad_t grad);
 
 #ifdef __cplusplus
 }

@@ -153,9 +153,12 @@ struct parl_ctx_s {
     // lifetime: objects created on this context keep it alive
     int refs = 0;
     bool closing = false;
-    // NCCL (data-parallel over prompt groups)
+    // NCCL (data-parallel over prompt groups); every collective of the communicator runs on
+    // comm_st, ordered against the compute stream by events
     void* comm = nullptr;
     int rank = 0, nranks = 1;
+    cudaStream_t comm_st = nullptr;
+    cudaEvent_t ev_comm = nullptr, ev_comm_done = nullptr;
 };
 
 struct parl_model_s {
@@ -208,11 +211,19 @@ struct parl_grad_s {
     FlatLayout L{};
     DevBuf g;
     int micro_steps = 0;
+    bool overlap = false;  // armed: the next backward allreduces each layer as soon as it is final
+    bool streamed = false; // that backward has run: layers and head are in flight on comm_st
 };
 
 static void ctx_release(parl_ctx_s* ctx) {
     if (--ctx->refs > 0 || !ctx->closing) return;
     cudaStreamSynchronize(ctx->st);
+    if (ctx->comm_st) {
+        cudaStreamSynchronize(ctx->comm_st);
+        cudaStreamDestroy(ctx->comm_st);
+        cudaEventDestroy(ctx->ev_comm);
+        cudaEventDestroy(ctx->ev_comm_done);
+    }
     delete ctx->act_cache;
     cudaStreamDestroy(ctx->st);
     delete ctx;
@@ -684,6 +695,18 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
     check_launch();
 }
 
+}  // namespace
+int nccl_allreduce_raw(void* p, size_t n, int dtype, void* comm, cudaStream_t st);
+namespace {
+// Allreduce (sum) of n elements at p on the communicator's stream, after everything the
+// compute stream has issued so far.  dtype: ncclFloat32 = 7, ncclFloat64 = 8.
+void comm_allreduce(parl_ctx_s* c, void* p, size_t n, int dtype) {
+    PARL_CUDA(cudaEventRecord(c->ev_comm, c->st));
+    PARL_CUDA(cudaStreamWaitEvent(c->comm_st, c->ev_comm, 0));
+    const int r = nccl_allreduce_raw(p, n, dtype, c->comm, c->comm_st);
+    PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce failed");
+}
+
 // backward (model.cpp:587-838) + GradBuffer::accumulate (model.cpp:189-194)
 template <class T>
 void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s* g, parl_grad_s* gr) {
@@ -747,6 +770,11 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         PARL_CUDA(cudaMemsetAsync(dx, 0, TD * sizeof(float), st));
         PARL_CUDA(cudaMemsetAsync(dx_act, 0, TD * sizeof(T), st));
     }
+    // overlapped data-parallel allreduce (armed by parl_grad_allreduce_overlap on the last
+    // micro-batch): each gradient slice goes out as soon as this backward has finished it,
+    // the final LN + head now, every layer after its LN1 backward, the embeddings last
+    const bool stream_ar = gr->overlap && c->comm && c->nranks > 1;
+    if (stream_ar) comm_allreduce(c, G + L.lnf_g, L.total - L.lnf_g, 7);
 
     T* dpre = c->dpre.as<T>(TFp);
     float* dbn = c->dbn.as<float>(TD);
@@ -879,6 +907,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
                                     G + o.ln1b, st);
         }
         std::swap(dx, dx2);
+        if (stream_ar) comm_allreduce(c, G + o.ln1g, L.layer_stride, 7);
     }
     // embeddings (model.cpp:826-834), deterministic segmented sums
     ensure_sorted(g);
@@ -888,6 +917,10 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
                       G + L.pos_emb, st);
     check_launch();
     gr->micro_steps += 1;
+    if (stream_ar) {
+        gr->overlap = false;
+        gr->streamed = true;
+    }
 }
 
 // Host-side attention tile schedule (see AttnSched in kernels.cuh): the same
@@ -2123,6 +2156,12 @@ parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr) {
 }
 
 // ---- NCCL (loaded at run time; data-parallel gradient/stat allreduce) -------------
+static NcclApi& nccl();
+
+extern "C++" int nccl_allreduce_raw(void* p, size_t n, int dtype, void* comm, cudaStream_t st) {
+    return nccl().allReduce(p, p, n, dtype, 0 /* ncclSum */, comm, st);
+}
+
 static NcclApi& nccl() {
     static NcclApi api;
     if (!api.h) {
@@ -2164,24 +2203,44 @@ parl_status parl_comm_init(parl_ctx_t ctx, const char id[PARL_NCCL_ID_BYTES], in
         PARL_REQUIRE(r == 0, PARL_E_NCCL, std::string("ncclCommInitRank: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
         ctx->rank = rank;
         ctx->nranks = nranks;
+        if (!ctx->comm_st) {
+            PARL_CUDA(cudaStreamCreateWithFlags(&ctx->comm_st, cudaStreamNonBlocking));
+            PARL_CUDA(cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming));
+            PARL_CUDA(cudaEventCreateWithFlags(&ctx->ev_comm_done, cudaEventDisableTiming));
+        }
     });
 }
 
 parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
     return guarded(ctx, [&] {
-        if (!ctx->comm || ctx->nranks == 1) return;
-        // ncclFloat32 = 7, ncclSum = 0
-        int r = nccl().allReduce(gr->g.p, gr->g.p, gr->L.total, 7, 0, ctx->comm, ctx->st);
-        PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce(grad) failed");
+        gr->overlap = false;
+        if (!ctx->comm || ctx->nranks == 1) {
+            gr->streamed = false;
+            return;
+        }
+        float* G = static_cast<float*>(gr->g.p);
+        if (gr->streamed) comm_allreduce(ctx, G, gr->L.layer0, 7);  // the rest went out during the backward
+        else comm_allreduce(ctx, G, gr->L.total, 7);
+        gr->streamed = false;
+        // the compute stream continues once every slice is reduced
+        PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
+        PARL_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_comm_done, 0));
+    });
+}
+
+parl_status parl_grad_allreduce_overlap(parl_ctx_t ctx, parl_grad_t gr) {
+    return guarded(ctx, [&] {
+        gr->overlap = ctx->comm && ctx->nranks > 1;
+        gr->streamed = false;
     });
 }
 
 parl_status parl_stats_allreduce(parl_ctx_t ctx) {
     return guarded(ctx, [&] {
         if (!ctx->comm || ctx->nranks == 1) return;
-        // ncclFloat64 = 8
-        int r = nccl().allReduce(ctx->stats.p, ctx->stats.p, 5, 8, 0, ctx->comm, ctx->st);
-        PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce(stats) failed");
+        comm_allreduce(ctx, ctx->stats.p, 5, 8);
+        PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
+        PARL_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_comm_done, 0));
     });
 }
 

@@ -127,7 +127,7 @@ def _load():
         "parl_train_microbatch": [vp, vp, vp, vp, vp, f64p, f64p, C.POINTER(_Hyper), vp, C.POINTER(_Stats)],
         "parl_apply_update": [vp, vp, C.c_double],
         "parl_comm_unique_id": [C.c_char_p], "parl_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
-        "parl_grad_allreduce": [vp, vp], "parl_stats_allreduce": [vp],
+        "parl_grad_allreduce": [vp, vp], "parl_stats_allreduce": [vp], "parl_grad_allreduce_overlap": [vp, vp],
         "parl_checkpoint_save": [vp, C.c_char_p], "parl_checkpoint_load": [vp, C.c_char_p, C.POINTER(vp)],
         "parl_model_config": [vp, C.POINTER(_Config)],
         "parl_sample_tokens": [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_uint64, vp, C.POINTER(C.c_int)],
@@ -374,6 +374,11 @@ class GradBuffer:
 
     def allreduce(self):
         _check(LIB.parl_grad_allreduce(self.ctx.h, self.h), self.ctx.h)
+
+    def allreduce_overlap(self):
+        """Arm before the step's last micro-batch: its backward streams each finished gradient
+        slice to NCCL (parl_grad_allreduce_overlap); allreduce() then completes the exchange."""
+        _check(LIB.parl_grad_allreduce_overlap(self.ctx.h, self.h), self.ctx.h)
 
     def accumulate(self, other: "GradBuffer"):
         """GradBuffer::accumulate (model.cpp:189-194)."""

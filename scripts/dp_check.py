@@ -29,6 +29,20 @@ for gi in rank_groups(len(groups), None, world, rank):
 grads.allreduce()
 ctx.stats_allreduce()
 g_dp, st_dp = grads.flat(), ctx.stats()
+# the same step with the allreduce overlapped with the last micro-batch's backward
+grads.reset()
+mine = list(rank_groups(len(groups), None, world, rank))
+for n_, gi in enumerate(mine):
+    pr, rs, rw = groups[gi]
+    grp.pack(pr, rs, 576)
+    if n_ == len(mine) - 1:
+        grads.allreduce_overlap()
+    P.train_microbatch(tm, grp, grads, hyper, rewards=rw, want_stats=False)
+grads.allreduce()
+g_ov = grads.flat()
+rel_ov = np.linalg.norm(g_ov - g_dp) / np.linalg.norm(g_dp)
+print(f"DP_CHECK rank={rank} overlapped vs whole-buffer allreduce rel={rel_ov:.3e}")
+assert rel_ov < 1e-6, "overlapped allreduce differs"
 if rank == 0:
     ctx1 = P.Context(local, P.PREC_FP32)
     tm1 = P.TriModel(P.ModelParams.from_flat(cfg, tm.policy.flat(), ctx=ctx1),
