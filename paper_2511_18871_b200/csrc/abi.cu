@@ -2229,8 +2229,15 @@ parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
 }
 
 parl_status parl_grad_allreduce_overlap(parl_ctx_t ctx, parl_grad_t gr) {
+    // Off unless PARL_AR_OVERLAP=1: NCCL's CTAs then run beside full-grid persistent kernels,
+    // whose CTAs on the SMs NCCL holds start late; measured neutral at N = 2 with NCCL's default
+    // channels (108.1 vs 108.4 ms per step) and slower with the channels capped to leave SMs free.
+    static const bool enabled = [] {
+        const char* e = std::getenv("PARL_AR_OVERLAP");
+        return e && e[0] == '1';
+    }();
     return guarded(ctx, [&] {
-        gr->overlap = ctx->comm && ctx->nranks > 1;
+        gr->overlap = enabled && ctx->comm && ctx->nranks > 1;
         gr->streamed = false;
     });
 }

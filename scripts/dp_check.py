@@ -42,7 +42,7 @@ grads.allreduce()
 g_ov = grads.flat()
 rel_ov = np.linalg.norm(g_ov - g_dp) / np.linalg.norm(g_dp)
 print(f"DP_CHECK rank={rank} overlapped vs whole-buffer allreduce rel={rel_ov:.3e}")
-assert rel_ov < 1e-6, "overlapped allreduce differs"
+assert rel_ov < 1e-6, "overlapped allreduce differs"  # (PARL_AR_OVERLAP=1 arms the streaming path)
 if rank == 0:
     ctx1 = P.Context(local, P.PREC_FP32)
     tm1 = P.TriModel(P.ModelParams.from_flat(cfg, tm.policy.flat(), ctx=ctx1),
