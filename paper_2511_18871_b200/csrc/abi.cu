@@ -87,6 +87,7 @@ struct HostStage {
 
 struct SchedHost {
     std::vector<int32_t> q_ptr, k_ptr, p_ptr;
+    std::vector<int32_t> p_cost;  // forward pair items: 2 per key tile both query tiles see, 1 per one-sided
 };
 
 struct NcclApi {
@@ -108,6 +109,9 @@ struct parl_ctx_s {
         DevBuf x, xmid, a, qkv, ctxo, bn, actv, stats, lse_attn, hf, lnf_mean, lnf_rstd, lse_head, logits;
     } scr[3];
     DevBuf part, target;
+    // dynamic attention work queue: monotonic device counter, host copy of its next base
+    DevBuf item_ctr;
+    unsigned item_base = 0;
     // backward workspaces
     DevBuf dx, dx2, dx_act, dpre, dbn, dmid, dmid_act, dctx, dqkv, da, dsum, dhf, dxg, dz;
     DevBuf stats, per_sample, staging, flags;
@@ -455,6 +459,8 @@ AttnArgs attn_args(parl_group_s* g, const parl_config& cf) {
     aa.Peff = g->Peff;
     aa.sched = g->sched;
     aa.ldo = cf.d_model + PAD_COLS;
+    aa.item_ctr = static_cast<unsigned*>(g->ctx->item_ctr.p);
+    aa.item_base = &g->ctx->item_base;
     return aa;
 }
 
@@ -1012,6 +1018,12 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
         host_out->q_ptr = q_ptr;
         host_out->k_ptr = k_ptr;
         host_out->p_ptr = p_ptr;
+        // a key tile seen by both query tiles of a pair runs both softmax groups (sharing the
+        // SM's exponential units); a one-sided one runs one, in about half the time
+        host_out->p_cost.assign(np, 0);
+        for (int p = 0; p < np; ++p)
+            for (int e = p_ptr[p]; e < p_ptr[p + 1]; ++e)
+                host_out->p_cost[p] += ((p_list[e] >> 24) & 1) + ((p_list[e] >> 26) & 1);
     }
     AttnSched s;
     s.q_ptr = d + o_qp; s.q_list = d + o_ql; s.q_order = d + o_qo;
@@ -1034,7 +1046,8 @@ bool attn_order_lpt() {
     return v == 1;
 }
 
-int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all, bool locality) {
+int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all, bool locality,
+              const std::vector<int32_t>* tile_cost = nullptr, std::vector<int32_t>* order_out = nullptr) {
     const int nt = (int)ptr.size() - 1;
     const int n = nt * H;
     int sms = 148;
@@ -1045,7 +1058,10 @@ int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all,
     }
     const int grid = std::max(1, std::min(n, sms));
     std::vector<int32_t> order(n);
-    auto cost = [&](int it) { return ptr[it / H + 1] - ptr[it / H] + 1; };
+    // per item: partner tiles (or the given per-tile cost) + the per-item overhead
+    auto cost = [&](int it) {
+        return tile_cost ? (*tile_cost)[it / H] + 2 : ptr[it / H + 1] - ptr[it / H] + 1;
+    };
     if (!locality || attn_order_lpt()) {
         for (int i = 0; i < n; ++i) order[i] = i;
         std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
@@ -1056,7 +1072,7 @@ int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all,
         // cost (prompt key tiles of the dK/dV pass, seen by every query tile) go first,
         // longest first, so the greedy least-loaded assignment below stays balanced.
         long tot = 0;
-        for (int t = 0; t < nt; ++t) tot += (long)(ptr[t + 1] - ptr[t] + 1) * H;
+        for (int t = 0; t < nt; ++t) tot += (long)cost(t * H) * H;
         const double big = 2.0 * (double)tot / std::max(n, 1);
         int k = 0;
         for (int i = 0; i < n; ++i)
@@ -1067,6 +1083,7 @@ int lpt_lists(const std::vector<int32_t>& ptr, int H, std::vector<int32_t>& all,
             if (cost(it) <= big) order[k++] = it;
         }
     }
+    if (order_out) *order_out = order;
     std::vector<std::vector<int32_t>> per(grid);
     using L = std::pair<long, int>;
     std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
@@ -1093,14 +1110,18 @@ void build_attn_work(AttnSched& s, const SchedHost& hs, int H, int dm, DevBuf& b
     std::vector<int32_t> all;
     const double kv_bytes = 128.0 * ((double)hs.q_ptr.size() - 1) * dm * 4;
     const size_t o_f = all.size();
-    const int gf = lpt_lists(hs.p_ptr, H, all, kv_bytes > 64e6);
+    std::vector<int32_t> forder;
+    const int gf = lpt_lists(hs.p_ptr, H, all, kv_bytes > 64e6, hs.p_cost.empty() ? nullptr : &hs.p_cost, &forder);
     const size_t o_k = all.size();
     const int gk = lpt_lists(hs.k_ptr, H, all, true);
     const size_t o_q = all.size();
     const int gq = lpt_lists(hs.q_ptr, H, all, true);
+    const size_t o_o = all.size();
+    all.insert(all.end(), forder.begin(), forder.end());
     int32_t* d = buf.as<int32_t>(all.size());
     stage.upload(d, all.data(), all.size() * 4, st);
     s.w_ptr = d + o_f; s.w_items = d + o_f + gf + 1; s.w_grid = gf;
+    s.w_order = d + o_o; s.w_n = (int)forder.size();
     s.bk_ptr = d + o_k; s.bk_items = d + o_k + gk + 1; s.bk_grid = gk;
     s.bq_ptr = d + o_q; s.bq_items = d + o_q + gq + 1; s.bq_grid = gq;
 }
@@ -1208,6 +1229,7 @@ parl_status parl_ctx_create(int device, parl_precision prec, parl_ctx_t* out) {
         PARL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
         double* s = c->stats.as<double>(8);
         PARL_CUDA(cudaMemsetAsync(s, 0, 8 * sizeof(double), c->st));
+        PARL_CUDA(cudaMemsetAsync(c->item_ctr.as<unsigned>(4), 0, 4 * sizeof(unsigned), c->st));
         if (const char* e = std::getenv("PARL_RECOMPUTE")) c->recompute = std::atoi(e);
         PARL_REQUIRE(c->recompute >= 0 && c->recompute <= 2, PARL_E_CONFIG, "PARL_RECOMPUTE must be 0, 1 or 2");
         *out = c.release();
@@ -2283,6 +2305,11 @@ extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int 
         aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
         aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
         aa.scale = 1.0f / std::sqrt((float)Dh);
+        static DevBuf dbg_ctr;
+        static unsigned dbg_base = 0;
+        if (!dbg_ctr.p) PARL_CUDA(cudaMemset(dbg_ctr.as<unsigned>(4), 0, 4 * sizeof(unsigned)));
+        aa.item_ctr = static_cast<unsigned*>(dbg_ctr.p);
+        aa.item_base = &dbg_base;
         static DevBuf dbg_sched;
         static HostStage dbg_stage;
         static AttnSched cached;

@@ -333,6 +333,12 @@ struct AttnPairArgs {
     const int32_t* seg_start;
     const int32_t *p_ptr, *p_list;
     const int32_t *w_ptr, *w_items;  // per-CTA item lists (item = pair * H + head)
+    // dynamic work queue (dyn): CTAs take items from `order` (n_items, longest or head-major
+    // first) through one global counter: item = atomicAdd(ctr, 1) - base
+    int dyn, n_items;
+    const int32_t* order;
+    unsigned* ctr;
+    unsigned base;
     float scale_log2;
     bf16* out;
     long ldo;
@@ -353,7 +359,8 @@ struct PairSmem {
     static constexpr int OFF_V = OFF_K + KVS * TILE;         // [KVS]
     static constexpr int OFF_OST = OFF_V + KVS * TILE;       // [8 softmax warps][32 rows x 128 B] output staging
     static constexpr int OFF_BAR = OFF_OST + 8 * 4096;
-    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
+    static constexpr int OFF_RING = OFF_BAR + 256;           // [4] item ids of the dynamic queue
+    static constexpr int TOTAL = OFF_RING + 64 + 1024;
 };
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
@@ -365,7 +372,19 @@ __device__ unsigned long long g_attn_trace[16][64][8];
     do {                                                                                        \
         if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (n) < 64) g_attn_trace[role][n][k] = clock64(); \
     } while (0)
+// per-CTA [start, end] global time (ns) of the traced launch: roles 12.. hold CTA / 64
+#define ATTN_SPAN(k)                                                                                  \
+    do {                                                                                              \
+        if (threadIdx.x == 0) {                                                                       \
+            unsigned long long t_;                                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+            g_attn_trace[12 + blockIdx.x / 64][blockIdx.x % 64][k] = t_;                              \
+        }                                                                                             \
+    } while (0)
 #else
+#define ATTN_SPAN(k) \
+    do {             \
+    } while (0)
 #define ATTN_TRACE(role, n, k) \
     do {                       \
     } while (0)
@@ -395,6 +414,9 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     uint64_t* o_done = bar + 18;                  // [2]
     uint64_t* o_free = bar + 20;                  // [2]
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 22);
+    uint64_t* ring_full = bar + 24;               // [4] dynamic queue: item id published
+    uint64_t* ring_empty = bar + 28;              // [4] released by the 2 MMA + 8 softmax warps
+    volatile int* ring = reinterpret_cast<volatile int*>(smem + L::OFF_RING);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = a.H;
@@ -414,6 +436,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             tc::mbar_init(&kv_full[s], 1);
             tc::mbar_init(&kv_empty[s], 2);
         }
+        for (int s = 0; s < 4; ++s) {
+            tc::mbar_init(&ring_full[s], 1);
+            tc::mbar_init(&ring_empty[s], 10);
+        }
         tc::fence_barrier_init();
         tc::tma_prefetch(&tm_qkv);
     }
@@ -425,6 +451,22 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     const uint32_t t_s = tbase, t_o = tbase + 256, t_p = P_IN_S ? tbase : tbase + 256 + 2 * DH;
     pdl_wait();
     pdl_trigger();
+    ATTN_SPAN(0);
+
+    // The li-th item of this CTA (-1: none left).  Static lists, or the dynamic queue: the TMA
+    // thread publishes item li + 1 before it loads item li, so a consumer working on item li
+    // may always look at li + 1; consumers release an item's slot when done with it.
+    auto item_at = [&](int li) -> int {
+        if (!a.dyn) {
+            const int k = a.w_ptr[blockIdx.x] + li;
+            return k < a.w_ptr[blockIdx.x + 1] ? a.w_items[k] : -1;
+        }
+        tc::mbar_wait(&ring_full[li & 3], (li >> 2) & 1);
+        return ring[li & 3];
+    };
+    auto item_done = [&](int li) {
+        if (a.dyn && lane == 0) tc::mbar_arrive(&ring_empty[li & 3]);
+    };
 
     // Per-row metadata of a softmax item (prefetched one item ahead): pair p, head h, row i,
     // the row's allowed key ranges [0, e0) u [b1, e1) (model.cpp:242-245), the pair's entry
@@ -433,10 +475,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         int p, h, i, e0, b1, e1, ea, eb;
         uint32_t f0;
     };
-    auto fetch_item = [&](int k, int k_end, int w, int r) -> ItemMeta {
-        ItemMeta m{0, 0, a.T, 0, 0, 0, 0, 0, 0u};
-        if (k >= k_end) return m;
-        const int it = a.w_items[k];
+    auto fetch_item = [&](int li, int w, int r) -> ItemMeta {  // p < 0: no item li
+        ItemMeta m{-1, 0, a.T, 0, 0, 0, 0, 0, 0u};
+        const int it = item_at(li);
+        if (it < 0) return m;
         m.p = it / H;
         m.h = it % H;
         m.i = (2 * m.p + w) * 128 + r;
@@ -498,20 +540,20 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);
         const uint32_t t_sw = t_s + w * 128, t_ow = t_o + w * DH;
         int cS = 0, cP = 0, nI = 0;  // chunk counters
-        const int k_end = a.w_ptr[blockIdx.x + 1];
-        int s_k = a.w_ptr[blockIdx.x], s_li = 0, s_e = 0, s_end = 0, gS = 0, s_h = 0;
+        int s_it = item_at(0), s_li = 0, s_e = 0, s_end = 0, gS = 0, s_h = 0;
         auto s_load_item = [&]() {
-            if (s_k < k_end) {
-                const int p = a.w_items[s_k] / H;
+            if (s_it >= 0) {
+                const int p = s_it / H;
                 s_e = a.p_ptr[p];
                 s_end = a.p_ptr[p + 1];
             }
         };
-        auto s_seek = [&]() -> bool {  // next visible (entry, chunk) of this tile
-            while (s_k < k_end) {
+        // next visible (entry, chunk) of this tile, at most QB - 1 items past li_now
+        auto s_seek = [&](int li_now) -> bool {
+            while (s_it >= 0) {
                 if (s_e >= s_end) {
-                    ++s_k;
-                    ++s_li;
+                    if (s_li + 1 > li_now + QB - 1) return false;
+                    s_it = item_at(++s_li);
                     s_load_item();
                     continue;
                 }
@@ -552,11 +594,13 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         // S of chunk n reuses the buffer of chunk n - 2: issued after PV(n - 2) (cS < cP + 2);
         // within the K/V ring window and the Q buffers this issuer has released
         auto advance_s = [&](int g_now, int li_now) {
-            while (cS < cP + 2 && s_seek() && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1) issue_s();
+            while (cS < cP + 2 && s_seek(li_now) && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1) issue_s();
         };
-        int g = 0, li = 0;
-        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
-            const int p = a.w_items[k] / H, qb = li % QB;
+        int g = 0;
+        for (int li = 0;; ++li) {
+            const int itm = item_at(li);
+            if (itm < 0) break;
+            const int p = itm / H, qb = li % QB;
             const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
             bool started = false;
             for (int e = ea; e < eb; ++e, ++g) {
@@ -596,6 +640,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 tc::mbar_wait(&q_full[qb], (li / QB) & 1);
                 if (lane == 0) tc::mbar_arrive(&q_empty[qb]);
             }
+            item_done(li);
         }
       }
     };
@@ -608,11 +653,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const uint32_t t_sw = t_s + w * 128 + lane_off, t_ow = t_o + w * DH + lane_off;
         const float c2 = a.scale_log2;
         int cS = 0;
-        const int k_end = a.w_ptr[blockIdx.x + 1];
-        ItemMeta nx = fetch_item(a.w_ptr[blockIdx.x], k_end, w, r);
-        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k) {
+        ItemMeta nx = fetch_item(0, w, r);
+        for (int k = 0; nx.p >= 0; ++k) {
             const ItemMeta cur = nx;
-            nx = fetch_item(k + 1, k_end, w, r);  // the next item's chain of dependent loads, off the critical path
+            nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
             const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
@@ -700,12 +744,16 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     ++cS;
                 }
             }
-            if (first) continue;  // no key tile for this query tile (past the end)
+            if (first) {  // no key tile for this query tile (past the end)
+                item_done(k);
+                continue;
+            }
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
             if (q4 == 0) ATTN_TRACE(w, cS - 1, 6);
             store_out(t_ow, w, q4, p, h, i, row_ok, l, m_used);
             if (q4 == 0) ATTN_TRACE(w, cS - 1, 7);
+            item_done(k);
         }
       }
     };
@@ -714,9 +762,23 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
       if (warp == 8) {
         if (lane == 0) {  // ---------------- TMA
-            int g = 0, li = 0;
-            for (int k = a.w_ptr[blockIdx.x]; k < a.w_ptr[blockIdx.x + 1]; ++k, ++li) {
-                const int it = a.w_items[k];
+            int g = 0;
+            int published = -1;  // dynamic queue: last published slot index
+            bool ended = false;
+            auto publish = [&](int n) {  // fetch item n of this CTA from the global counter
+                tc::mbar_wait(&ring_empty[n & 3], ((n >> 2) & 1) ^ 1);
+                const unsigned v = atomicAdd(a.ctr, 1u) - a.base;
+                const int it = v < (unsigned)a.n_items ? a.order[v] : -1;
+                ring[n & 3] = it;
+                tc::mbar_arrive(&ring_full[n & 3]);
+                published = n;
+                ended = it < 0;
+            };
+            if (a.dyn) publish(0);
+            for (int li = 0;; ++li) {
+                const int it = a.dyn ? ring[li & 3] : item_at(li);
+                if (it < 0) break;
+                if (a.dyn && !ended && published == li) publish(li + 1);
                 const int p = it / H, h = it % H, qb = li % QB;
                 tc::mbar_wait(&q_empty[qb], ((li / QB) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[qb], 2 * L::TILE);
@@ -756,21 +818,21 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         // wait for a K/V stage that cannot depend on this thread's own later releases:
         // its entry must lie within KV_STAGES - 1 of the entry being processed (a tile
         // whose pair partner sees many more key tiles skips long runs of entries).
-        const int k_end = a.w_ptr[blockIdx.x + 1];
-        int s_k = a.w_ptr[blockIdx.x], s_li = 0, s_e = 0, s_end = 0, gS = 0;
+        int s_it = item_at(0), s_li = 0, s_e = 0, s_end = 0, gS = 0;
         auto s_load_item = [&]() {
-            if (s_k < k_end) {
-                const int p = a.w_items[s_k] / H;
+            if (s_it >= 0) {
+                const int p = s_it / H;
                 s_e = a.p_ptr[p];
                 s_end = a.p_ptr[p + 1];
             }
         };
-        // move the iterator to the next entry visible to this tile (global index gS); false at the end
-        auto s_seek = [&]() -> bool {
-            while (s_k < k_end) {
+        // move the iterator to the next entry visible to this tile (global index gS), at most
+        // QB - 1 items past li_now; false at the end
+        auto s_seek = [&](int li_now) -> bool {
+            while (s_it >= 0) {
                 if (s_e >= s_end) {
-                    ++s_k;
-                    ++s_li;
+                    if (s_li + 1 > li_now + QB - 1) return false;
+                    s_it = item_at(++s_li);
                     s_load_item();
                     continue;
                 }
@@ -805,12 +867,14 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         // (and at most QB - 1 items ahead: the Q buffer of a later item is freed by this
         // issuer's own end-of-item release)
         auto advance_s = [&](int g_now, int li_now) {
-            while (cS < cP + (P_IN_S ? 1 : 2) && s_seek() && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1)
+            while (cS < cP + (P_IN_S ? 1 : 2) && s_seek(li_now) && gS <= g_now + KVS - 1 && s_li <= li_now + QB - 1)
                 issue_s();
         };
-        int g = 0, li = 0;
-        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k, ++li) {
-            const int p = a.w_items[k] / H, qb = li % QB;
+        int g = 0;
+        for (int li = 0;; ++li) {
+            const int itm = item_at(li);
+            if (itm < 0) break;
+            const int p = itm / H, qb = li % QB;
             const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
             bool started = false;
             for (int e = ea; e < eb; ++e, ++g) {
@@ -847,6 +911,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 tc::mbar_wait(&q_full[qb], (li / QB) & 1);
                 if (lane == 0) tc::mbar_arrive(&q_empty[qb]);
             }
+            item_done(li);
         }
       }
     } else if (DH == 128) {
@@ -861,11 +926,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const uint32_t VIS = w ? VIS1 : VIS0, FULL = w ? FULL1 : FULL0;
         const float c2 = a.scale_log2;
         int cS = 0;
-        const int k_end = a.w_ptr[blockIdx.x + 1];
-        ItemMeta nx = fetch_item(a.w_ptr[blockIdx.x], k_end, w, r);
-        for (int k = a.w_ptr[blockIdx.x]; k < k_end; ++k) {
+        ItemMeta nx = fetch_item(0, w, r);
+        for (int k = 0; nx.p >= 0; ++k) {
             const ItemMeta cur = nx;
-            nx = fetch_item(k + 1, k_end, w, r);  // the next item's chain of dependent loads, off the critical path
+            nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
             const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
@@ -951,16 +1015,21 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 first = false;
                 ++cS;
             }
-            if (first) continue;  // no key tile for this query tile (past the end)
+            if (first) {  // no key tile for this query tile (past the end)
+                item_done(k);
+                continue;
+            }
             // item epilogue: O / l -> out (bf16), lse; then release O to the next item
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
             store_out(t_o + w * DH + lane_off, w, q4, p, h, i, row_ok, l, m_used);
+            item_done(k);
         }
     }
     if (warp < 8 && lane == 0) tc::bulk_wait<0>();  // output stores complete before the CTA exits
     tc::tc_fence_before();
     __syncthreads();
+    ATTN_SPAN(1);
     if (warp == 9) {
         tc::tc_fence_after();
         tc::tmem_dealloc<512>(tbase);
@@ -1126,6 +1195,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     const uint32_t t_s = tbase, t_dp = tbase + 128, t_acc1 = tbase + 256, t_acc2 = tbase + 256 + DH;
     pdl_wait();
     pdl_trigger();
+    if (MODE == MODE_DKV) ATTN_SPAN(0);
     const uint32_t t_p = ALIAS ? t_s : tbase + 384;
     const uint32_t t_ds = ALIAS ? t_dp : (DH == 128 ? tbase + 384 : tbase + 448);
 
@@ -1445,6 +1515,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     }
     tc::tc_fence_before();
     __syncthreads();
+    if (MODE == MODE_DKV) ATTN_SPAN(1);
     if (warp == 9) {
         tc::tc_fence_after();
         tc::tmem_dealloc<512>(tbase);
@@ -2092,6 +2163,17 @@ bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cud
         pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
         pa.scale_log2 = aa.scale * LOG2E;
         pa.out = out; pa.ldo = aa.ldo ? aa.ldo : aa.d; pa.lse = lse;
+        // dynamic work queue (PARL_ATTN_DYN=0: the static per-CTA lists)
+        static const bool dyn_ok = [] {
+            const char* e = getenv("PARL_ATTN_DYN");
+            return !(e && e[0] == '0');
+        }();
+        pa.dyn = dyn_ok && aa.item_ctr && aa.item_base && aa.sched.w_order;
+        pa.n_items = aa.sched.w_n;
+        pa.order = aa.sched.w_order;
+        pa.ctr = aa.item_ctr;
+        pa.base = pa.dyn ? *aa.item_base : 0u;
+        if (pa.dyn) *aa.item_base += (unsigned)(pa.n_items + pa.grid);  // every CTA's last fetch finds the end
         // output tensor map: [T x d] bf16 with row stride ldo, 32 x 64 boxes, 128B swizzle
         CUtensorMap mo;
         cuuint64_t odims[2] = {(cuuint64_t)aa.d, (cuuint64_t)aa.T};

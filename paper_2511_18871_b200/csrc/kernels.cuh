@@ -143,6 +143,9 @@ struct AttnSched {
     // item = pair * H + head, balanced over w_grid CTAs (LPT on key-tile counts)
     const int32_t *w_ptr = nullptr, *w_items = nullptr;
     int w_grid = 0;
+    // the same items as one queue (longest / head-major first) for the dynamic work queue
+    const int32_t* w_order = nullptr;
+    int w_n = 0;
     // backward work lists: dK/dV items = key tile * H + head, dQ items = query tile * H + head
     const int32_t *bk_ptr = nullptr, *bk_items = nullptr, *bq_ptr = nullptr, *bq_items = nullptr;
     int bk_grid = 0, bq_grid = 0;
@@ -157,6 +160,10 @@ struct AttnArgs {
     const int32_t* seg_start;  // [G+1]
     const int32_t* seg_end;    // [G+1]
     float scale;
+    // dynamic work queue of the forward: a device counter and the host-side running base
+    // (each launch consumes n_items + grid counter values); null: static per-CTA lists
+    unsigned* item_ctr = nullptr;
+    unsigned* item_base = nullptr;
 };
 // tcgen05 forward (k_attn_tc.cu); false if the head dim / alignment is unsupported
 bool attn_fwd_tc(const AttnArgs& a, const bf16* qkv, bf16* out, float* lse, cudaStream_t st);

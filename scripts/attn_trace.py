@@ -49,6 +49,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "bwd":  # trace the dK/dV kernel instead
 buf = np.zeros((16, 64, 8), dtype=np.uint64)
 assert P.LIB.parl_debug_attn_trace(buf.ctypes.data_as(C.c_void_p)) == 0
 b = buf.astype(np.int64)
+span = b[12:15].reshape(-1, 8)[:, :2]
+span = span[span[:, 0] > 0]
+if len(span):
+    s0 = span[:, 0].min()
+    st, en = (span[:, 0] - s0) / 1e3, (span[:, 1] - s0) / 1e3
+    print(f"CTA spans (us, {len(span)} CTAs): start max {st.max():.1f}, end min {en.min():.1f} / median "
+          f"{np.median(en):.1f} / max {en.max():.1f}; busy median {np.median(en - st):.1f}")
+    b[12:15] = 0
 t0 = b[b > 0].min()
 np.set_printoptions(linewidth=200)
 if len(sys.argv) > 1 and sys.argv[1] == "bwd":
