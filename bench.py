@@ -317,18 +317,19 @@ def run_ours(args, c):
     h_resps = [torch.from_numpy(r).pin_memory().numpy() for r in resps]
 
     def step_e2e():
+        # host inputs in, the step's loss statistics out (one device -> host read per step,
+        # after the last micro-batch; the statistics accumulate on the device)
         grads.reset()
-        st = None
+        ctx.stats_reset()
         for i in range(ng):
             group.pack(h_prompts[i], [h_resps[i][offs[k]:offs[k + 1]] for k in range(G)], c["max_seq"])
             if world > 1 and i == ng - 1:
                 grads.allreduce_overlap()
-            st = P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=True)
+            P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=False)
         if world > 1:
             grads.allreduce()
             ctx.stats_allreduce()
-        ctx.sync()
-        return st
+        return ctx.stats()
 
     for _ in range(args.warmup):
         step_device()
@@ -404,7 +405,7 @@ def run_ours(args, c):
                    "roofline_timing": "per-launch CUDA events over a second identical K-step region",
                    "parallelism": f"dp{world} over prompt groups"},
         "e2e": {"value": e2e_val, "unit": "packed tokens/s", "h2d_bytes_per_step": ng * (T * 4 + G * 8),
-                "d2h_bytes_per_step": ng * 40},
+                "d2h_bytes_per_step": 40},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": achieved / bf16_sus, "peak_kind": f"{src} bf16 sustained",

@@ -194,6 +194,7 @@ struct parl_group_s {
     uint64_t work_epoch = ~0ull;
     uint64_t sorted_epoch = ~0ull;
     std::vector<int> lens, span_start, cu;
+    std::vector<int> sched_key;  // segment structure the schedule was built for
     int max_seq = 0, vocab = 0;
 };
 
@@ -1169,8 +1170,15 @@ void upload_meta(parl_group_s* g) {
     }
     PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
+    // the tile schedule and the attention work lists depend only on the segment structure:
+    // a group re-packed with the same lengths (every step of a fixed-shape run) keeps them
+    std::vector<int> key = {g->T, g->Peff, g->G};
+    key.insert(key.end(), g->lens.begin(), g->lens.end());
+    key.insert(key.end(), g->span_start.begin(), g->span_start.end());
+    if (key == g->sched_key && g->sched.q_ptr) return;
     g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->sched_stage, g->ctx->st,
                               &g->sched_h);
+    g->sched_key = std::move(key);
     g->work_H = -1;
 }
 
