@@ -496,15 +496,19 @@ void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs
     gemm_multi<T>(c, gs, nm);
     {
         ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D * nm);
+        T* ql[3];
+        T* cl[3];
+        float* la[3];
         for (int k = 0; k < nm; ++k) {
             const FwdBufs<T>& b = B[k];
-            T* ql = b.qkv + b.lay(3 * TD, l);
-            T* cl = b.ctxo + b.lay(TDp, l);
-            float* la = b.lse_attn + b.lay((size_t)H * Tn, l);
-            bool done = false;
-            if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc(aa, ql, cl, la, st);
-            if (!done) launch_attn_fwd<T>(aa, ql, cl, la, st);
+            ql[k] = b.qkv + b.lay(3 * TD, l);
+            cl[k] = b.ctxo + b.lay(TDp, l);
+            la[k] = b.lse_attn + b.lay((size_t)H * Tn, l);
         }
+        bool done = false;  // the models' attention as one launch (tcgen05 path)
+        if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc_multi(aa, ql, cl, la, nm, st);
+        if (!done)
+            for (int k = 0; k < nm; ++k) launch_attn_fwd<T>(aa, ql[k], cl[k], la[k], st);
     }
     for (int k = 0; k < nm; ++k) {  // O projection + residual (model.cpp:504-506)
         const FwdBufs<T>& b = B[k];

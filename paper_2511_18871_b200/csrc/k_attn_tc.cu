@@ -339,10 +339,16 @@ struct AttnPairArgs {
     const int32_t* order;
     unsigned* ctr;
     unsigned base;
+    // grouped launch over nm models (same schedule, the tri-model forward): item =
+    // model * n_base + pair * H + head, n_base = n_pairs * H; tensor maps per model
+    int nm, n_base;
+    float* lse[3];
     float scale_log2;
-    bf16* out;
     long ldo;
-    float* lse;
+};
+
+struct AttnPairMaps {
+    CUtensorMap qkv[3], out[3];
 };
 
 constexpr int PAIR_NTHR = 384;  // 3 warp groups: softmax 0, softmax 1, TMA/MMA
@@ -392,8 +398,7 @@ __device__ unsigned long long g_attn_trace[16][64][8];
 
 template <int DH>
 __global__ void __launch_bounds__(PAIR_NTHR, 1)
-    k_attn_fwd_pair(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_out,
-                    AttnPairArgs a) {
+    k_attn_fwd_pair(const __grid_constant__ AttnPairMaps maps, AttnPairArgs a) {
     static_assert(DH == 64 || DH == 128, "head dim");
     using L = PairSmem<DH>;
     // TMEM: Dh = 64: S0 | S1 | O0 | O1 | P0 | P1; Dh = 128: S0 | S1 | O0 | O1 with P_w written
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             tc::mbar_init(&ring_empty[s], 10);
         }
         tc::fence_barrier_init();
-        tc::tma_prefetch(&tm_qkv);
+        for (int m = 0; m < a.nm; ++m) tc::tma_prefetch(&maps.qkv[m]);
     }
     if (warp == 9) tc::tmem_alloc<512>(tbase_s);
     tc::tc_fence_before();
@@ -474,12 +479,14 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     struct ItemMeta {
         int p, h, i, e0, b1, e1, ea, eb;
         uint32_t f0;
+        int mdl;
     };
     auto fetch_item = [&](int li, int w, int r) -> ItemMeta {  // p < 0: no item li
-        ItemMeta m{-1, 0, a.T, 0, 0, 0, 0, 0, 0u};
+        ItemMeta m{-1, 0, a.T, 0, 0, 0, 0, 0, 0u, 0};
         const int it = item_at(li);
         if (it < 0) return m;
-        m.p = it / H;
+        m.mdl = it / a.n_base;
+        m.p = (it % a.n_base) / H;
         m.h = it % H;
         m.i = (2 * m.p + w) * 128 + r;
         const bool row_ok = m.i < a.T;
@@ -496,7 +503,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     // Item epilogue of a softmax warp: O / l (fp32, TMEM) -> bf16 rows of `out`, staged per
     // warp through a 128B-swizzled 32 x 64 smem slab and written by TMA (coalesced; the
     // rows past T are clipped by the tensor map), then lse.  Releases O after the last load.
-    auto store_out = [&](uint32_t t_ow, int w, int q4, int p, int h, int i, bool row_ok, float l, float m_used) {
+    auto store_out = [&](uint32_t t_ow, int w, int q4, int mdl, int p, int h, int i, bool row_ok, float l,
+                         float m_used) {
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const uint32_t slab = tc::smem_u32(smem + L::OFF_OST + warp * 4096);
 #pragma unroll
@@ -520,11 +528,11 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             tc::fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tc::tma_store_2d(&tm_out, slab, h * DH + hc * 64, (2 * p + w) * 128 + q4 * 32);
+                tc::tma_store_2d(&maps.out[mdl], slab, h * DH + hc * 64, (2 * p + w) * 128 + q4 * 32);
                 tc::bulk_commit();
             }
         }
-        if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
+        if (row_ok) a.lse[mdl][(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
     };
 
     // ---- Dh = 128: key tiles are processed as two 64-key chunks so that each query tile
@@ -543,7 +551,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         int s_it = item_at(0), s_li = 0, s_e = 0, s_end = 0, gS = 0, s_h = 0;
         auto s_load_item = [&]() {
             if (s_it >= 0) {
-                const int p = s_it / H;
+                const int p = (s_it % a.n_base) / H;
                 s_e = a.p_ptr[p];
                 s_end = a.p_ptr[p + 1];
             }
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int li = 0;; ++li) {
             const int itm = item_at(li);
             if (itm < 0) break;
-            const int p = itm / H, qb = li % QB;
+            const int p = (itm % a.n_base) / H, qb = li % QB;
             const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
             bool started = false;
             for (int e = ea; e < eb; ++e, ++g) {
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
             if (q4 == 0) ATTN_TRACE(w, cS - 1, 6);
-            store_out(t_ow, w, q4, p, h, i, row_ok, l, m_used);
+            store_out(t_ow, w, q4, cur.mdl, p, h, i, row_ok, l, m_used);
             if (q4 == 0) ATTN_TRACE(w, cS - 1, 7);
             item_done(k);
         }
@@ -768,7 +776,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             auto publish = [&](int n) {  // fetch item n of this CTA from the global counter
                 tc::mbar_wait(&ring_empty[n & 3], ((n >> 2) & 1) ^ 1);
                 const unsigned v = atomicAdd(a.ctr, 1u) - a.base;
-                const int it = v < (unsigned)a.n_items ? a.order[v] : -1;
+                // queue position v: base item order[v / nm] (longest / head-major first) of model v % nm
+                const int it = v < (unsigned)a.n_items ? (int)(v % a.nm) * a.n_base + a.order[v / a.nm] : -1;
                 ring[n & 3] = it;
                 tc::mbar_arrive(&ring_full[n & 3]);
                 published = n;
@@ -779,14 +788,15 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const int it = a.dyn ? ring[li & 3] : item_at(li);
                 if (it < 0) break;
                 if (a.dyn && !ended && published == li) publish(li + 1);
-                const int p = it / H, h = it % H, qb = li % QB;
+                const int mdl = it / a.n_base, p = (it % a.n_base) / H, h = it % H, qb = li % QB;
+                const CUtensorMap* tm_qkv = &maps.qkv[mdl];
                 tc::mbar_wait(&q_empty[qb], ((li / QB) & 1) ^ 1);
                 tc::mbar_expect_tx(&q_full[qb], 2 * L::TILE);
 #pragma unroll
                 for (int w = 0; w < 2; ++w)
 #pragma unroll
                     for (int r = 0; r < DH / 64; ++r)
-                        tc::tma_load_2d(smem + L::OFF_Q + (qb * 2 + w) * L::TILE + r * 128 * 128, &tm_qkv, &q_full[qb],
+                        tc::tma_load_2d(smem + L::OFF_Q + (qb * 2 + w) * L::TILE + r * 128 * 128, tm_qkv, &q_full[qb],
                                         h * DH + r * 64, (2 * p + w) * 128);
                 for (int e = a.p_ptr[p]; e < a.p_ptr[p + 1]; ++e, ++g) {
                     const int j0 = (a.p_list[e] & 0xffffff) * 128;
@@ -795,9 +805,9 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
 #pragma unroll
                     for (int r = 0; r < DH / 64; ++r) {
-                        tc::tma_load_2d(smem + L::OFF_K + st * L::TILE + r * 128 * 128, &tm_qkv, &kv_full[st],
+                        tc::tma_load_2d(smem + L::OFF_K + st * L::TILE + r * 128 * 128, tm_qkv, &kv_full[st],
                                         a.d + h * DH + r * 64, j0);
-                        tc::tma_load_2d(smem + L::OFF_V + st * L::TILE + r * 128 * 128, &tm_qkv, &kv_full[st],
+                        tc::tma_load_2d(smem + L::OFF_V + st * L::TILE + r * 128 * 128, tm_qkv, &kv_full[st],
                                         2 * a.d + h * DH + r * 64, j0);
                     }
                 }
@@ -821,7 +831,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         int s_it = item_at(0), s_li = 0, s_e = 0, s_end = 0, gS = 0;
         auto s_load_item = [&]() {
             if (s_it >= 0) {
-                const int p = s_it / H;
+                const int p = (s_it % a.n_base) / H;
                 s_e = a.p_ptr[p];
                 s_end = a.p_ptr[p + 1];
             }
@@ -874,7 +884,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int li = 0;; ++li) {
             const int itm = item_at(li);
             if (itm < 0) break;
-            const int p = itm / H, qb = li % QB;
+            const int p = (itm % a.n_base) / H, qb = li % QB;
             const int ea = a.p_ptr[p], eb = a.p_ptr[p + 1];
             bool started = false;
             for (int e = ea; e < eb; ++e, ++g) {
@@ -1022,7 +1032,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
             // item epilogue: O / l -> out (bf16), lse; then release O to the next item
             tc::mbar_wait(&o_done[w], (cS - 1) & 1);
             tc::tc_fence_after();
-            store_out(t_o + w * DH + lane_off, w, q4, p, h, i, row_ok, l, m_used);
+            store_out(t_o + w * DH + lane_off, w, q4, cur.mdl, p, h, i, row_ok, l, m_used);
             item_done(k);
         }
     }
@@ -2010,14 +2020,25 @@ void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
+int device_sms_attn() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 template <int DH>
-void launch_fwd_pair(const CUtensorMap& m, const CUtensorMap& mo, const AttnPairArgs& a, cudaStream_t st) {
+void launch_fwd_pair(const AttnPairMaps& maps, const AttnPairArgs& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_attn_fwd_pair<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairSmem<DH>::TOTAL);
         attr = true;
     }
-    launch_pdl(k_attn_fwd_pair<DH>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<DH>::TOTAL, st, m, mo, a);
+    launch_pdl(k_attn_fwd_pair<DH>, dim3(a.grid), dim3(PAIR_NTHR), PairSmem<DH>::TOTAL, st, maps, a);
     PARL_LAUNCHED();
 }
 
@@ -2126,70 +2147,95 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
 }
 
 // qkv: [T x 3d] bf16; returns false when the head dim / alignment is unsupported.
-bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cudaStream_t st) {
-    if (!(aa.Dh == 64 || aa.Dh == 128)) return false;
-    if (((3L * aa.d * 2) % 16) || (reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
-        (((aa.ldo ? aa.ldo : aa.d) * 2) % 16))
-        return false;
+// qkv: [T x 3d] bf16 per model; the nm models (same packed group, e.g. the tri-model forward)
+// run as one launch when the dynamic queue is on.  false when the head dim / alignment is
+// unsupported.
+bool attn_fwd_tc_multi(const AttnArgs& aa, const bf16* const* qkv, bf16* const* out, float* const* lse, int nm,
+                       cudaStream_t st) {
+    if (!(aa.Dh == 64 || aa.Dh == 128) || nm < 1 || nm > 3) return false;
+    const long ldo = aa.ldo ? aa.ldo : aa.d;
+    if (((3L * aa.d * 2) % 16) || ((ldo * 2) % 16)) return false;
+    for (int k = 0; k < nm; ++k)
+        if ((reinterpret_cast<uintptr_t>(qkv[k]) & 15) || (reinterpret_cast<uintptr_t>(out[k]) & 15)) return false;
     auto fn = encode();
     if (!fn) return false;
-    CUtensorMap m;
-    cuuint64_t dims[2] = {(cuuint64_t)(3 * aa.d), (cuuint64_t)aa.T};
-    cuuint64_t strides[1] = {(cuuint64_t)(3 * aa.d) * 2};
-    cuuint32_t box[2] = {64, 128};
     cuuint32_t es[2] = {1, 1};
-    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(qkv), dims, strides, box, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    AttnTcArgs a;
-    a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
-    a.Peff = aa.Peff;
-    a.seg = aa.seg;
-    a.seg_start = aa.seg_start;
-    a.seg_end = aa.seg_end;
-    a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
-    if (!a.q_ptr) return false;
-    a.scale_log2 = aa.scale * LOG2E;
-    a.out = out;
-    a.ldo = aa.ldo ? aa.ldo : aa.d;
-    a.lse = lse;
+    auto qkv_map = [&](CUtensorMap* m, const bf16* p) {
+        cuuint64_t dims[2] = {(cuuint64_t)(3 * aa.d), (cuuint64_t)aa.T};
+        cuuint64_t strides[1] = {(cuuint64_t)(3 * aa.d) * 2};
+        cuuint32_t box[2] = {64, 128};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(p), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    // output tensor map: [T x d] bf16 with row stride ldo, 32 x 64 boxes, 128B swizzle
+    auto out_map = [&](CUtensorMap* m, bf16* p) {
+        cuuint64_t odims[2] = {(cuuint64_t)aa.d, (cuuint64_t)aa.T};
+        cuuint64_t ostr[1] = {(cuuint64_t)ldo * 2};
+        cuuint32_t obox[2] = {64, 32};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p, odims, ostr, obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+               CUDA_SUCCESS;
+    };
+    if (!aa.sched.q_ptr) return false;
     if (aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
-        AttnPairArgs pa;
-        pa.T = aa.T; pa.H = aa.H; pa.d = aa.d; pa.Peff = aa.Peff;
-        pa.grid = aa.sched.w_grid;
-        pa.seg = aa.seg; pa.seg_start = aa.seg_start;
-        pa.p_ptr = aa.sched.p_ptr; pa.p_list = aa.sched.p_list;
-        pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
-        pa.scale_log2 = aa.scale * LOG2E;
-        pa.out = out; pa.ldo = aa.ldo ? aa.ldo : aa.d; pa.lse = lse;
-        // dynamic work queue (PARL_ATTN_DYN=0: the static per-CTA lists)
+        // dynamic work queue (PARL_ATTN_DYN=0: the static per-CTA lists, one launch per model)
         static const bool dyn_ok = [] {
             const char* e = getenv("PARL_ATTN_DYN");
             return !(e && e[0] == '0');
         }();
-        pa.dyn = dyn_ok && aa.item_ctr && aa.item_base && aa.sched.w_order;
-        pa.n_items = aa.sched.w_n;
-        pa.order = aa.sched.w_order;
-        pa.ctr = aa.item_ctr;
-        pa.base = pa.dyn ? *aa.item_base : 0u;
-        if (pa.dyn) *aa.item_base += (unsigned)(pa.n_items + pa.grid);  // every CTA's last fetch finds the end
-        // output tensor map: [T x d] bf16 with row stride ldo, 32 x 64 boxes, 128B swizzle
-        CUtensorMap mo;
-        cuuint64_t odims[2] = {(cuuint64_t)aa.d, (cuuint64_t)aa.T};
-        cuuint64_t ostr[1] = {(cuuint64_t)pa.ldo * 2};
-        cuuint32_t obox[2] = {64, 32};
-        if (fn(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, odims, ostr, obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-            CUDA_SUCCESS)
-            return false;
-        if (aa.Dh == 64) launch_fwd_pair<64>(m, mo, pa, st);
-        else launch_fwd_pair<128>(m, mo, pa, st);
+        const bool dyn = dyn_ok && aa.item_ctr && aa.item_base && aa.sched.w_order;
+        const int per_launch = dyn ? nm : 1;
+        for (int k0 = 0; k0 < nm; k0 += per_launch) {
+            AttnPairArgs pa;
+            AttnPairMaps maps;
+            pa.T = aa.T; pa.H = aa.H; pa.d = aa.d; pa.Peff = aa.Peff;
+            pa.seg = aa.seg; pa.seg_start = aa.seg_start;
+            pa.p_ptr = aa.sched.p_ptr; pa.p_list = aa.sched.p_list;
+            pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
+            pa.scale_log2 = aa.scale * LOG2E;
+            pa.ldo = ldo;
+            pa.nm = per_launch;
+            pa.n_base = aa.sched.w_n > 0 ? aa.sched.w_n : (1 << 30);
+            for (int k = 0; k < per_launch; ++k) {
+                if (!qkv_map(&maps.qkv[k], qkv[k0 + k]) || !out_map(&maps.out[k], out[k0 + k])) return false;
+                pa.lse[k] = lse[k0 + k];
+            }
+            pa.dyn = dyn;
+            pa.n_items = per_launch * aa.sched.w_n;
+            pa.order = aa.sched.w_order;
+            pa.ctr = aa.item_ctr;
+            // the static lists' grid, or (queue) enough CTAs for all models' items
+            pa.grid = dyn ? std::min(pa.n_items, std::max(aa.sched.w_grid, device_sms_attn())) : aa.sched.w_grid;
+            pa.base = dyn ? *aa.item_base : 0u;
+            if (dyn) *aa.item_base += (unsigned)(pa.n_items + pa.grid);  // every CTA's last fetch finds the end
+            if (aa.Dh == 64) launch_fwd_pair<64>(maps, pa, st);
+            else launch_fwd_pair<128>(maps, pa, st);
+        }
         return true;
     }
-    if (aa.Dh == 64) launch_fwd<64>(m, a, st);
-    else launch_fwd<128>(m, a, st);
+    for (int k = 0; k < nm; ++k) {
+        CUtensorMap m;
+        if (!qkv_map(&m, qkv[k])) return false;
+        AttnTcArgs a;
+        a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
+        a.Peff = aa.Peff;
+        a.seg = aa.seg;
+        a.seg_start = aa.seg_start;
+        a.seg_end = aa.seg_end;
+        a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
+        a.scale_log2 = aa.scale * LOG2E;
+        a.out = out[k];
+        a.ldo = ldo;
+        a.lse = lse[k];
+        if (aa.Dh == 64) launch_fwd<64>(m, a, st);
+        else launch_fwd<128>(m, a, st);
+    }
     return true;
+}
+
+bool attn_fwd_tc(const AttnArgs& aa, const bf16* qkv, bf16* out, float* lse, cudaStream_t st) {
+    return attn_fwd_tc_multi(aa, &qkv, &out, &lse, 1, st);
 }
 
 #ifdef PARL_ATTN_TRACE

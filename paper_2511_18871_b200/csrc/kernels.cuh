@@ -167,6 +167,9 @@ struct AttnArgs {
 };
 // tcgen05 forward (k_attn_tc.cu); false if the head dim / alignment is unsupported
 bool attn_fwd_tc(const AttnArgs& a, const bf16* qkv, bf16* out, float* lse, cudaStream_t st);
+// nm models of one group (tri-model forward) in one launch where possible
+bool attn_fwd_tc_multi(const AttnArgs& a, const bf16* const* qkv, bf16* const* out, float* const* lse, int nm,
+                       cudaStream_t st);
 template <class T>
 void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaStream_t st);
 // tcgen05 backward (k_attn_tc.cu): dqkv from dO, lse and D = rowsum(dO*O)
