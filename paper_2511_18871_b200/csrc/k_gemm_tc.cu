@@ -46,6 +46,7 @@ struct TcArgs {
     int store_logits;      // EPI_LSE: also store bf16 logits (policy, for the backward) by TMA
     bf16* logits_direct;   // EPI_LSE: ... or by plain stores when the row stride is not 16-byte aligned
     long ldl;
+    int raster;            // CTA-pair kernels: 1 = n-tiles fastest (B small, stays in L2; A read once)
 };
 
 template <int BN>
@@ -133,9 +134,18 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
 
     auto coords = [&](int item, int& row, int& col, int& sp) {
         const int t = item % e.tpp;
-        const int mt = t % e.tiles_me, rest = t / e.tiles_me;
-        const int nt = rest % a0.tiles_n;
-        sp = rest / a0.tiles_n;
+        int mt, nt;
+        if (a0.raster) {
+            nt = t % a0.tiles_n;
+            const int rest = t / a0.tiles_n;
+            mt = rest % e.tiles_me;
+            sp = rest / e.tiles_me;
+        } else {
+            mt = t % e.tiles_me;
+            const int rest = t / e.tiles_me;
+            nt = rest % a0.tiles_n;
+            sp = rest / a0.tiles_n;
+        }
         row = mt * e.mrows + e.rank * BM + ew * 32;
         col = nt * BNT + hcol;
     };
@@ -550,8 +560,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const int prob = item / tpp, t = item % tpp;
             const CUtensorMap* tA = &mp.a[prob];
             const CUtensorMap* tB = &mp.b[prob];
-            const int mt = t % tiles_m2, rest = t / tiles_m2;
-            const int nt = rest % a.tiles_n, sp = rest / a.tiles_n;
+            const int mt = a.raster ? (t / a.tiles_n) % tiles_m2 : t % tiles_m2;
+            const int nt = a.raster ? t % a.tiles_n : (t / tiles_m2) % a.tiles_n;
+            const int sp = t / (tiles_m2 * a.tiles_n);
             const int kb0 = sp * a.kbs, kb1 = min(a.nkb, kb0 + a.kbs);
             const int m0 = mt * 2 * BM + (int)rank * BM, n0 = nt * NB + (int)rank * (NB / 2);
             for (int kb = kb0; kb < kb1; ++kb, ++cnt) {
@@ -1007,6 +1018,15 @@ bool plan_gemm(const GemmArgs& g, Plan& P) {
     a.n_parts = g.n_parts;
     a.store_logits = g.logits_act != nullptr;
     const int tiles = pair ? ((g.M + 255) / 256) * a.tiles_n : a.tiles_m * a.tiles_n;
+    // n-fastest tile order when the N-side operand is small (weights: it stays in L2 while the
+    // concurrently running tiles share each A row block, so A streams from HBM once); else
+    // m-fastest (the LM head's 270 MB weight would be re-read per m block).  PARL_GEMM_RASTER=0/1
+    static const int raster_env = [] {
+        const char* e = getenv("PARL_GEMM_RASTER");
+        return e ? atoi(e) : -1;
+    }();
+    const double b_bytes = (double)g.N * g.K * 2, a_bytes = (double)g.M * g.K * 2;
+    a.raster = pair && (raster_env >= 0 ? raster_env == 1 : (b_bytes <= 16e6 && a_bytes >= b_bytes));
     a.splits = 1;
     a.kbs = a.nkb;
     const int slots = pair ? sms / 2 : sms;  // concurrently running tiles
