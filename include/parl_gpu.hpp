@@ -335,6 +335,19 @@ inline ForwardResult forward_logprobs(const ModelParams& params, std::span<const
 }
 
 // model.cpp:587-838: gradient of sum_i upstream[i] * logprobs[i]
+// RolloutService::score_logprobs (rollout.cpp:52-66): response log-probs under a causal forward
+inline std::vector<double> score_logprobs(const ModelParams& params, std::span<const TokenId> prompt,
+                                          std::span<const TokenId> response) {
+    if (response.empty()) return {};
+    std::vector<TokenId> tokens(prompt.begin(), prompt.end());
+    tokens.insert(tokens.end(), response.begin(), response.end());
+    std::vector<int> positions(tokens.size());
+    for (std::size_t i = 0; i < tokens.size(); ++i) positions[i] = static_cast<int>(i);
+    std::vector<std::int32_t> labels(tokens.size(), kIgnoreLabel);
+    for (std::size_t i = 0; i < response.size(); ++i) labels[prompt.size() + i] = response[i];
+    return forward_logprobs(params, tokens, positions, AttentionMaskSpec::causal(), labels).logprobs;
+}
+
 inline GradBuffer backward(const ModelParams& params, const ForwardResult& fwd, std::span<const double> upstream) {
     if (!fwd.cache) throw LifecycleError("backward requires a cached forward result");
     if (upstream.size() != fwd.logprobs.size())

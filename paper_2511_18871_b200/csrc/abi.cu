@@ -187,7 +187,7 @@ struct parl_group_s {
     PackedDev pk{};
     DevBuf ints, seg_se, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
     DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf, work_buf;
-    HostStage sched_stage, work_stage;
+    HostStage sched_stage, work_stage, adv_stage;  // pinned staging: async uploads that never block the host
     AttnSched sched;
     SchedHost sched_h;  // host copies of the schedule's tile pointers (work lists)
     int work_H = -1, work_d = -1;
@@ -207,6 +207,7 @@ struct parl_act_s {
     DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
     bool logits_bf16 = false;  // logits stored bf16 by the fused tcgen05 head
     bool recompute = false;    // only x_0..x_L kept; layers (and bf16 logits) rebuilt in the backward
+    int rc_key[3] = {-1, -1, -1};  // shape the automatic recompute decision was made for
     uintptr_t pad_sig[8] = {};  // buffers / sizes the bias columns were filled for
 };
 
@@ -565,6 +566,8 @@ template <class T>
 bool want_recompute(parl_ctx_s* c, parl_act_s* act, const parl_config& cf, int Tn, int S) {
     if (c->recompute == 1) return true;
     if (c->recompute == 2) return false;
+    // decided once per activation handle and shape (cudaMemGetInfo is a driver round trip)
+    if (act->rc_key[0] == Tn && act->rc_key[1] == S && act->rc_key[2] == cf.d_model) return act->recompute;
     const size_t es = sizeof(T), D = cf.d_model, F = cf.d_ff, V = cf.vocab_size, H = cf.n_heads;
     const size_t stacks = layer_act_bytes(cf, Tn, es) * cf.n_layers + (size_t)S * V * es;
     const size_t held = act->xmid.bytes + act->a.bytes + act->qkv.bytes + act->ctxo.bytes + act->bn.bytes +
@@ -578,6 +581,9 @@ bool want_recompute(parl_ctx_s* c, parl_act_s* act, const parl_config& cf, int T
     size_t free_b = 0, total_b = 0;
     PARL_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t avail = free_b + held, need = stacks + (ws > ws_held ? ws - ws_held : 0) + ((size_t)3 << 30);
+    act->rc_key[0] = Tn;
+    act->rc_key[1] = S;
+    act->rc_key[2] = cf.d_model;
     return need > avail;
 }
 
@@ -2016,12 +2022,12 @@ parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards
         if (rewards) {
             PARL_REQUIRE(G >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
             double* r = g->rewards.as<double>(G);
-            PARL_CUDA(cudaMemcpyAsync(r, rewards, G * sizeof(double), cudaMemcpyHostToDevice, st));
+            g->adv_stage.upload(r, rewards, G * sizeof(double), st);
             launch_advantages(r, G, hp->advantage_mean_only, adv, st);
         } else {
             for (int k = 0; k < G; ++k)
                 PARL_REQUIRE(std::isfinite(advantages[k]), PARL_E_NUMERIC, "advantage is not finite");
-            PARL_CUDA(cudaMemcpyAsync(adv, advantages, G * sizeof(double), cudaMemcpyHostToDevice, st));
+            g->adv_stage.upload(adv, advantages, G * sizeof(double), st);
         }
         const float* lp = static_cast<float*>(g->lp.p);
         double* stats = ctx->stats.as<double>(8);

@@ -253,6 +253,33 @@ TEST_CASE(train_microbatch_matches_oracle) {  // pipeline.cpp:97-141
     CHECK(grads.micro_step_count() == 1);
 }
 
+TEST_CASE(checkpoint_round_trip_and_errors) {  // model.cpp:907-987
+    ModelConfig c = small_config();
+    ModelParams p = ModelParams::init(c, 41);
+    const std::string path = "/tmp/parl_dropin_ckpt.parlckp1";
+    save_checkpoint(path, p);
+    ModelParams q = load_checkpoint(path);
+    CHECK(q.config() == c);
+    CHECK(q.flat() == p.flat());
+    CHECK(q.version() == p.version());
+    CHECK_THROWS_AS(load_checkpoint("/tmp/parl_dropin_missing.parlckp1"), IoError);
+}
+
+TEST_CASE(sample_tokens_and_score_logprobs) {  // model.cpp:843-900, rollout.cpp:52-66
+    ModelConfig c = small_config();
+    ModelParams p = ModelParams::init(c, 41);
+    std::vector<TokenId> prompt{5, 9, 11, 4, 7};
+    auto a = sample_tokens(p, prompt, 12, 0.8, 3);
+    auto b = sample_tokens(p, prompt, 12, 0.8, 3);
+    CHECK(a == b);
+    CHECK(!a.empty() && a.size() <= 12);
+    auto lp = score_logprobs(p, prompt, a);
+    CHECK(lp.size() == a.size());
+    for (double v : lp) CHECK(v <= 0.0);
+    CHECK_THROWS_AS(sample_tokens(p, std::vector<TokenId>{}, 4, 0.0, 0), ShapeError);
+    CHECK_THROWS_AS(sample_tokens(p, prompt, -1, 0.0, 0), ConfigError);
+}
+
 int main() {
     for (auto& [name, fn] : cases()) {
         const int before = g_fail;
