@@ -217,6 +217,9 @@ struct parl_grad_s {
     FlatLayout L{};
     DevBuf g;
     int micro_steps = 0;
+    // tok_emb rows touched by this buffer's backward passes (the other rows are exactly 0), so
+    // the data-parallel exchange of the V x d token-embedding gradient sends only those rows
+    DevBuf touched, sel_idx, sel_rows, sel_count;
     bool overlap = false;  // armed: the next backward allreduces each layer as soon as it is final
     bool streamed = false; // that backward has run: layers and head are in flight on comm_st
 };
@@ -713,14 +716,14 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
 }
 
 }  // namespace
-int nccl_allreduce_raw(void* p, size_t n, int dtype, void* comm, cudaStream_t st);
+int nccl_allreduce_raw(void* p, size_t n, int dtype, int op, void* comm, cudaStream_t st);
 namespace {
 // Allreduce (sum) of n elements at p on the communicator's stream, after everything the
 // compute stream has issued so far.  dtype: ncclFloat32 = 7, ncclFloat64 = 8.
-void comm_allreduce(parl_ctx_s* c, void* p, size_t n, int dtype) {
+void comm_allreduce(parl_ctx_s* c, void* p, size_t n, int dtype, int op = 0 /* ncclSum */) {
     PARL_CUDA(cudaEventRecord(c->ev_comm, c->st));
     PARL_CUDA(cudaStreamWaitEvent(c->comm_st, c->ev_comm, 0));
-    const int r = nccl_allreduce_raw(p, n, dtype, c->comm, c->comm_st);
+    const int r = nccl_allreduce_raw(p, n, dtype, op, c->comm, c->comm_st);
     PARL_REQUIRE(r == 0, PARL_E_NCCL, "ncclAllReduce failed");
 }
 
@@ -928,6 +931,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     }
     // embeddings (model.cpp:826-834), deterministic segmented sums
     ensure_sorted(g);
+    launch_mark_rows(g->pk.tokens, Tn, static_cast<uint8_t*>(gr->touched.p), st);
     launch_embed_grad(static_cast<int32_t*>(g->tok_keys.p), static_cast<int32_t*>(g->tok_idx.p), Tn, dx, D,
                       G + L.tok_emb, st);
     launch_embed_grad(static_cast<int32_t*>(g->pos_keys.p), static_cast<int32_t*>(g->pos_idx.p), Tn, dx, D,
@@ -2095,6 +2099,7 @@ parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out
         gr->L = like->L;
         float* p = gr->g.as<float>(gr->L.total);
         PARL_CUDA(cudaMemsetAsync(p, 0, gr->L.total * sizeof(float), ctx->st));
+        PARL_CUDA(cudaMemsetAsync(gr->touched.as<uint8_t>(gr->cfg.vocab_size), 0, gr->cfg.vocab_size, ctx->st));
         PARL_CUDA(cudaStreamSynchronize(ctx->st));
         *out = gr.release();
     });
@@ -2113,6 +2118,7 @@ parl_status parl_grad_destroy(parl_grad_t gr) {
 parl_status parl_grad_reset(parl_grad_t gr) {
     return guarded(gr->ctx, [&] {
         PARL_CUDA(cudaMemsetAsync(gr->g.p, 0, gr->L.total * sizeof(float), gr->ctx->st));
+        PARL_CUDA(cudaMemsetAsync(gr->touched.p, 0, gr->cfg.vocab_size, gr->ctx->st));
         gr->micro_steps = 0;
     });
 }
@@ -2124,6 +2130,8 @@ parl_status parl_grad_accumulate(parl_grad_t dst, parl_grad_t src) {
         PARL_REQUIRE(same_cfg(dst->cfg, src->cfg), PARL_E_SHAPE, "gradient buffers have incongruent layouts");
         launch_axpy(static_cast<const float*>(src->g.p), static_cast<float*>(dst->g.p), (long)dst->L.total,
                     dst->ctx->st);
+        launch_or_bytes(static_cast<const uint8_t*>(src->touched.p), static_cast<uint8_t*>(dst->touched.p),
+                        dst->cfg.vocab_size, dst->ctx->st);
         check_launch();
         dst->micro_steps += src->micro_steps;
     });
@@ -2198,8 +2206,8 @@ parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr) {
 // ---- NCCL (loaded at run time; data-parallel gradient/stat allreduce) -------------
 static NcclApi& nccl();
 
-extern "C++" int nccl_allreduce_raw(void* p, size_t n, int dtype, void* comm, cudaStream_t st) {
-    return nccl().allReduce(p, p, n, dtype, 0 /* ncclSum */, comm, st);
+extern "C++" int nccl_allreduce_raw(void* p, size_t n, int dtype, int op, void* comm, cudaStream_t st) {
+    return nccl().allReduce(p, p, n, dtype, op, comm, st);
 }
 
 static NcclApi& nccl() {
@@ -2259,8 +2267,39 @@ parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
             return;
         }
         float* G = static_cast<float*>(gr->g.p);
-        if (gr->streamed) comm_allreduce(ctx, G, gr->L.layer0, 7);  // the rest went out during the backward
-        else comm_allreduce(ctx, G, gr->L.total, 7);
+        static const bool sparse = [] {  // PARL_SPARSE_EMB=0: dense exchange of the whole buffer
+            const char* e = std::getenv("PARL_SPARSE_EMB");
+            return !(e && e[0] == '0');
+        }();
+        const int V = gr->cfg.vocab_size, D = gr->cfg.d_model;
+        size_t dense0 = 0;  // first element exchanged densely
+        if (sparse && gr->L.tok_emb == 0 && D % 4 == 0) {
+            // union of the touched rows over the ranks (max of 0/1 bytes), then only those rows
+            cudaStream_t st = ctx->st;
+            uint8_t* flags = static_cast<uint8_t*>(gr->touched.p);
+            comm_allreduce(ctx, flags, V, 1 /* ncclUint8 */, 2 /* ncclMax */);
+            PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
+            PARL_CUDA(cudaStreamWaitEvent(st, ctx->ev_comm_done, 0));
+            int32_t* idx = gr->sel_idx.as<int32_t>(V);
+            int* cnt = gr->sel_count.as<int>(1);
+            select_flagged_rows(flags, V, idx, cnt, st);
+            int n = 0;
+            PARL_CUDA(cudaMemcpyAsync(&n, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaStreamSynchronize(st));
+            float* rows = gr->sel_rows.as<float>((size_t)std::max(n, 1) * D);
+            launch_rows_copy(G + gr->L.tok_emb, idx, n, D, 0, rows, st);
+            comm_allreduce(ctx, rows, (size_t)n * D, 7, 0);
+            PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
+            PARL_CUDA(cudaStreamWaitEvent(st, ctx->ev_comm_done, 0));
+            launch_rows_copy(rows, idx, n, D, 1, G + gr->L.tok_emb, st);
+            check_launch();
+            dense0 = (size_t)V * D;
+        }
+        if (gr->streamed) {  // the layers and the head went out during the backward
+            if (gr->L.layer0 > dense0) comm_allreduce(ctx, G + dense0, gr->L.layer0 - dense0, 7);
+        } else {
+            comm_allreduce(ctx, G + dense0, gr->L.total - dense0, 7);
+        }
         gr->streamed = false;
         // the compute stream continues once every slice is reduced
         PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));

@@ -1339,6 +1339,55 @@ void launch_fill_f64(double* out, long n, double v, cudaStream_t st) {
     PARL_LAUNCHED();
 }
 
+// ---- sparse token-embedding allreduce helpers (rows of tok_emb touched by any rank)
+__global__ void k_mark_rows(const int32_t* __restrict__ ids, int n, uint8_t* __restrict__ flags) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) flags[ids[i]] = 1;
+}
+void launch_mark_rows(const int32_t* ids, int n, uint8_t* flags, cudaStream_t st) {
+    if (n <= 0) return;
+    k_mark_rows<<<std::min(cdiv(n, 256), 1024), 256, 0, st>>>(ids, n, flags);
+    PARL_LAUNCHED();
+}
+__global__ void k_or_bytes(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] |= src[i];
+}
+void launch_or_bytes(const uint8_t* src, uint8_t* dst, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_or_bytes<<<std::min(cdiv(n, 256), 1024), 256, 0, st>>>(src, dst, n);
+    PARL_LAUNCHED();
+}
+// idx[0 .. *count) = the flagged row ids, ascending
+void select_flagged_rows(const uint8_t* flags, int n, int32_t* idx, int* count, cudaStream_t st) {
+    static void* temp = nullptr;
+    static size_t temp_bytes = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    size_t need = 0;
+    cub::DeviceSelect::Flagged(nullptr, need, it, flags, idx, count, n, st);
+    if (need > temp_bytes) {
+        if (temp) cudaFree(temp);
+        PARL_CUDA(cudaMalloc(&temp, need));
+        temp_bytes = need;
+    }
+    PARL_CUDA(cub::DeviceSelect::Flagged(temp, temp_bytes, it, flags, idx, count, n, st));
+}
+// dir 0: dst[i] = src[idx[i]] (gather rows); 1: dst[idx[i]] = src[i] (scatter back)
+__global__ void k_rows_copy(const float* __restrict__ src, const int32_t* __restrict__ idx, int n, int d, int dir,
+                            float* __restrict__ dst) {
+    const int d4 = d >> 2;
+    const long total = (long)n * d4;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / d4), c = (int)(e % d4);
+        const long r = idx[i];
+        if (dir == 0) reinterpret_cast<float4*>(dst)[(long)i * d4 + c] = reinterpret_cast<const float4*>(src)[r * d4 + c];
+        else reinterpret_cast<float4*>(dst)[r * d4 + c] = reinterpret_cast<const float4*>(src)[(long)i * d4 + c];
+    }
+}
+void launch_rows_copy(const float* src, const int32_t* idx, int n, int d, int dir, float* dst, cudaStream_t st) {
+    if (n <= 0) return;
+    k_rows_copy<<<grid_for((long)n * (d / 4)), 256, 0, st>>>(src, idx, n, d, dir, dst);
+    PARL_LAUNCHED();
+}
+
 void launch_axpy(const float* x, float* y, long n, cudaStream_t st) {
     k_axpy<<<grid_for(n), 256, 0, st>>>(x, y, n);
     PARL_LAUNCHED();

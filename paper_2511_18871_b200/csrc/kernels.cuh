@@ -123,6 +123,11 @@ void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double sc
                   cudaStream_t st);
 void launch_fill_f64(double* out, long n, double v, cudaStream_t st);
 void launch_axpy(const float* x, float* y, long n, cudaStream_t st);  // y += x
+// sparse token-embedding gradient exchange (rows touched by any rank)
+void launch_mark_rows(const int32_t* ids, int n, uint8_t* flags, cudaStream_t st);
+void launch_or_bytes(const uint8_t* src, uint8_t* dst, int n, cudaStream_t st);
+void select_flagged_rows(const uint8_t* flags, int n, int32_t* idx, int* count, cudaStream_t st);
+void launch_rows_copy(const float* src, const int32_t* idx, int n, int d, int dir, float* dst, cudaStream_t st);
 void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int phase, cudaStream_t st);
 
 // attention (k_attn.cu).  qkv: [T x 3d] (q | k | v, head h at columns h*Dh);
