@@ -482,14 +482,28 @@ void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs
     const int Dp = D + PAD_COLS, Fp = F + PAD_COLS;
     const size_t TDp = (size_t)Tn * Dp, TFp = (size_t)Tn * Fp;
     GemmArgs gs[3];
-    {
-        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+    // LayerNorm of the nm models in one launch
+    auto ln_multi = [&](int which) {
+        const float* x[3];
+        const float *gg[3], *bb[3];
+        T* y[3];
+        float *mu[3], *rs[3];
         for (int k = 0; k < nm; ++k) {
             const FwdBufs<T>& b = B[k];
-            float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
-            launch_layernorm<T>(b.xin(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln1_g, ms[k]->layers[l].ln1_b,
-                                b.a + b.lay(TDp, l), Dp, st4, st4 + Tn, st);
+            const LayerW& w = ms[k]->layers[l];
+            float* st4 = b.stats + b.lay((size_t)4 * Tn, l) + (which ? 2 * Tn : 0);
+            x[k] = which ? b.xmid + b.lay(TD, l) : b.xin(TD, l);
+            gg[k] = which ? w.ln2_g : w.ln1_g;
+            bb[k] = which ? w.ln2_b : w.ln1_b;
+            y[k] = which ? b.bn + b.lay(TDp, l) : b.a + b.lay(TDp, l);
+            mu[k] = st4;
+            rs[k] = st4 + Tn;
         }
+        launch_layernorm_multi<T>(nm, x, gg, bb, y, Dp, mu, rs, Tn, D, st);
+    };
+    {
+        ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
+        ln_multi(0);
     }
     for (int k = 0; k < nm; ++k) {  // fused Q|K|V projection (model.cpp:464-466)
         const FwdBufs<T>& b = B[k];
@@ -524,12 +538,7 @@ void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs
     gemm_multi<T>(c, gs, nm);
     {
         ProfScope ps(c, PARL_KC_NORM, (double)Tn * D * (4 + sizeof(T)) * nm);
-        for (int k = 0; k < nm; ++k) {
-            const FwdBufs<T>& b = B[k];
-            float* st4 = b.stats + b.lay((size_t)4 * Tn, l);
-            launch_layernorm<T>(b.xmid + b.lay(TD, l), nullptr, Tn, D, ms[k]->layers[l].ln2_g, ms[k]->layers[l].ln2_b,
-                                b.bn + b.lay(TDp, l), Dp, st4 + 2 * Tn, st4 + 3 * Tn, st);
-        }
+        ln_multi(1);
     }
     for (int k = 0; k < nm; ++k) {  // W1 + bias + GELU (model.cpp:509-511)
         const FwdBufs<T>& b = B[k];

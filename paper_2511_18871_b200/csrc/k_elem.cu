@@ -775,15 +775,13 @@ __device__ __forceinline__ void store4<bf16>(bf16* p, float4 v) {
     *reinterpret_cast<uint2*>(p) = u;
 }
 
-// float4 variant of the forward (D % 4 == 0, 16-byte aligned rows)
+// float4 variant of the forward (D % 4 == 0, 16-byte aligned rows): one warp per row
 template <class T, int P4>
-__global__ void __launch_bounds__(256) k_layernorm4(const float* __restrict__ x, const int32_t* __restrict__ rows,
-                                                    int R, int D, const float* __restrict__ gamma,
-                                                    const float* __restrict__ beta, T* __restrict__ y, long ldy,
-                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
-    pdl_wait();
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (r >= R) return;
+__device__ __forceinline__ void ln4_row(const float* __restrict__ x, const int32_t* __restrict__ rows, int r, int D,
+                                        const float* __restrict__ gamma, const float* __restrict__ beta,
+                                        T* __restrict__ y, long ldy, float* __restrict__ mean_out,
+                                        float* __restrict__ rstd_out) {
+    const int lane = threadIdx.x & 31;
     const int D4 = D >> 2;
     const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
     float4 v[P4];
@@ -824,6 +822,33 @@ __global__ void __launch_bounds__(256) k_layernorm4(const float* __restrict__ x,
         mean_out[r] = mean;
         rstd_out[r] = rstd;
     }
+}
+
+template <class T, int P4>
+__global__ void __launch_bounds__(256) k_layernorm4(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                                                    int R, int D, const float* __restrict__ gamma,
+                                                    const float* __restrict__ beta, T* __restrict__ y, long ldy,
+                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    pdl_wait();
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= R) return;
+    ln4_row<T, P4>(x, rows, r, D, gamma, beta, y, ldy, mean_out, rstd_out);
+}
+
+// the same LayerNorm of up to three models (tri-model forward) in one launch: blockIdx.y = model
+template <class T>
+struct LnMulti {
+    const float* x[3];
+    const float *g[3], *b[3];
+    T* y[3];
+    float *mean[3], *rstd[3];
+};
+template <class T, int P4>
+__global__ void __launch_bounds__(256) k_layernorm4_multi(const __grid_constant__ LnMulti<T> a, int R, int D, long ldy) {
+    pdl_wait();
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, m = blockIdx.y;
+    if (r >= R) return;
+    ln4_row<T, P4>(a.x[m], nullptr, r, D, a.g[m], a.b[m], a.y[m], ldy, a.mean[m], a.rstd[m]);
 }
 
 template <class T>
@@ -893,6 +918,35 @@ __global__ void __launch_bounds__(256) k_ln_bwd_rows(const float* __restrict__ d
         }
     }
 }
+
+template <class T>
+void launch_layernorm_multi(int nm, const float* const* x, const float* const* g, const float* const* b, T* const* y,
+                            long ldy, float* const* mean, float* const* rstd, int R, int D, cudaStream_t st) {
+    if (R <= 0) return;
+    bool v4 = D % 4 == 0 && (ldy * (long)sizeof(T)) % 16 == 0 && nm >= 1 && nm <= 3;
+    for (int k = 0; k < nm; ++k) v4 = v4 && (reinterpret_cast<uintptr_t>(y[k]) & 15) == 0;
+    if (!v4 || D > 4096) {
+        for (int k = 0; k < nm; ++k) launch_layernorm<T>(x[k], nullptr, R, D, g[k], b[k], y[k], ldy, mean[k], rstd[k], st);
+        return;
+    }
+    LnMulti<T> a;
+    for (int k = 0; k < nm; ++k) {
+        a.x[k] = x[k]; a.g[k] = g[k]; a.b[k] = b[k]; a.y[k] = y[k]; a.mean[k] = mean[k]; a.rstd[k] = rstd[k];
+    }
+    const dim3 grid(cdiv(R, 8), nm);
+    if (D <= 512) launch_pdl(k_layernorm4_multi<T, 4>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else if (D <= 896) launch_pdl(k_layernorm4_multi<T, 7>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else if (D <= 1024) launch_pdl(k_layernorm4_multi<T, 8>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else if (D <= 1536) launch_pdl(k_layernorm4_multi<T, 12>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else if (D <= 2048) launch_pdl(k_layernorm4_multi<T, 16>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else if (D <= 3584) launch_pdl(k_layernorm4_multi<T, 28>, grid, dim3(256), 0, st, a, R, D, ldy);
+    else launch_pdl(k_layernorm4_multi<T, 32>, grid, dim3(256), 0, st, a, R, D, ldy);
+    PARL_LAUNCHED();
+}
+template void launch_layernorm_multi<float>(int, const float* const*, const float* const*, const float* const*,
+                                            float* const*, long, float* const*, float* const*, int, int, cudaStream_t);
+template void launch_layernorm_multi<bf16>(int, const float* const*, const float* const*, const float* const*,
+                                           bf16* const*, long, float* const*, float* const*, int, int, cudaStream_t);
 
 template <class T, int P4>
 __global__ void __launch_bounds__(256) k_ln_bwd_rows4(const float* __restrict__ dy, const float* __restrict__ x,

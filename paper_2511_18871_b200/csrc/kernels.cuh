@@ -86,6 +86,10 @@ void launch_embed(const float* tok, const float* pos, const int32_t* tokens, con
 template <class T>
 void launch_layernorm(const float* x, const int32_t* rows, int R, int D, const float* g, const float* b, T* y,
                       long ldy, float* mean, float* rstd, cudaStream_t st);
+// the same LayerNorm of nm <= 3 models (tri-model forward) in one launch
+template <class T>
+void launch_layernorm_multi(int nm, const float* const* x, const float* const* g, const float* const* b, T* const* y,
+                            long ldy, float* const* mean, float* const* rstd, int R, int D, cudaStream_t st);
 template <class T>
 void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, const float* mean, const float* rstd,
                           const float* gamma, int R, int D, const float* res, float* dx, T* dx_act, float* dgamma,
