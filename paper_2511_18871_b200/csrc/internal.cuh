@@ -53,6 +53,8 @@ extern uint64_t g_launches;
 // (and memory) before touching its outputs.  pdl_trigger() lets the successor
 // launch before this grid has fully exited.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// pull a line into L2 ahead of its load (memory-level parallelism without registers)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 bool pdl_enabled();  // PARL_PDL=0 disables (diagnostics)

@@ -1020,9 +1020,24 @@ __global__ void __launch_bounds__(256) k_ln_bwd_rows4_cs(const float* __restrict
     float4* sgb = red + (8 + wib) * D4;
     for (int c = lane; c < D4; c += 32) sga[c] = sgb[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* g4 = reinterpret_cast<const float4*>(gamma);
-    for (int r = blockIdx.x * 8 + wib; r < R; r += gridDim.x * 8) {
+    const int rstep = gridDim.x * 8;
+    for (int r = blockIdx.x * 8 + wib; r < R; r += rstep) {
         const float4* xr = reinterpret_cast<const float4*>(x + (long)(rows ? rows[r] : r) * D);
         const float4* dyr = reinterpret_cast<const float4*>(dy + (long)r * D);
+        // L2 prefetch of this row's residual gradient (read after the row reduction) and of
+        // the next row's dy / x: one DRAM latency per row overlaps the current row's work
+        if (res) {
+            const float* rp = res + (long)r * D;
+            for (int c = lane * 32; c < D; c += 32 * 32) prefetch_l2(rp + c);
+        }
+        if (r + rstep < R) {
+            const float* np = dy + (long)(r + rstep) * D;
+            const float* nx = x + (long)(rows ? rows[r + rstep] : r + rstep) * D;
+            for (int c = lane * 32; c < D; c += 32 * 32) {
+                prefetch_l2(np + c);
+                prefetch_l2(nx + c);
+            }
+        }
         float4 vy[P4], vx[P4];
 #pragma unroll
         for (int k = 0; k < P4; ++k) {
