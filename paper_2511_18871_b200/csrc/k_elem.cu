@@ -846,9 +846,26 @@ struct LnMulti {
 template <class T, int P4>
 __global__ void __launch_bounds__(256) k_layernorm4_multi(const __grid_constant__ LnMulti<T> a, int R, int D, long ldy) {
     pdl_wait();
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, m = blockIdx.y;
-    if (r >= R) return;
-    ln4_row<T, P4>(a.x[m], nullptr, r, D, a.g[m], a.b[m], a.y[m], ldy, a.mean[m], a.rstd[m]);
+    // persistent warps over rows; the next row is pulled into L2 while this one is normalised
+    const int m = blockIdx.y, lane = threadIdx.x & 31, rstep = gridDim.x * 8;
+    for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < R; r += rstep) {
+        if (r + rstep < R) {
+            const float* nx = a.x[m] + (long)(r + rstep) * D;
+            for (int c = lane * 32; c < D; c += 32 * 32) prefetch_l2(nx + c);
+        }
+        ln4_row<T, P4>(a.x[m], nullptr, r, D, a.g[m], a.b[m], a.y[m], ldy, a.mean[m], a.rstd[m]);
+    }
+}
+
+// resident blocks per SM of k_layernorm4_multi<T, P4>
+template <class T, int P4>
+int ln_multi_occupancy() {
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_layernorm4_multi<T, P4>, 256, 0);
+        if (occ <= 0) occ = 1;
+    }
+    return occ;
 }
 
 template <class T>
@@ -933,14 +950,20 @@ void launch_layernorm_multi(int nm, const float* const* x, const float* const* g
     for (int k = 0; k < nm; ++k) {
         a.x[k] = x[k]; a.g[k] = g[k]; a.b[k] = b[k]; a.y[k] = y[k]; a.mean[k] = mean[k]; a.rstd[k] = rstd[k];
     }
-    const dim3 grid(cdiv(R, 8), nm);
-    if (D <= 512) launch_pdl(k_layernorm4_multi<T, 4>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else if (D <= 896) launch_pdl(k_layernorm4_multi<T, 7>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else if (D <= 1024) launch_pdl(k_layernorm4_multi<T, 8>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else if (D <= 1536) launch_pdl(k_layernorm4_multi<T, 12>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else if (D <= 2048) launch_pdl(k_layernorm4_multi<T, 16>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else if (D <= 3584) launch_pdl(k_layernorm4_multi<T, 28>, grid, dim3(256), 0, st, a, R, D, ldy);
-    else launch_pdl(k_layernorm4_multi<T, 32>, grid, dim3(256), 0, st, a, R, D, ldy);
+    // all blocks resident at once, split evenly over the models
+#define PARL_LN_MULTI(P4)                                                                                  \
+    do {                                                                                                   \
+        const int gx = std::min(cdiv(R, 8), std::max(1, ln_multi_occupancy<T, P4>() * num_sms() / nm)); \
+        launch_pdl(k_layernorm4_multi<T, P4>, dim3(gx, nm), dim3(256), 0, st, a, R, D, ldy);            \
+    } while (0)
+    if (D <= 512) PARL_LN_MULTI(4);
+    else if (D <= 896) PARL_LN_MULTI(7);
+    else if (D <= 1024) PARL_LN_MULTI(8);
+    else if (D <= 1536) PARL_LN_MULTI(12);
+    else if (D <= 2048) PARL_LN_MULTI(16);
+    else if (D <= 3584) PARL_LN_MULTI(28);
+    else PARL_LN_MULTI(32);
+#undef PARL_LN_MULTI
     PARL_LAUNCHED();
 }
 template void launch_layernorm_multi<float>(int, const float* const*, const float* const*, const float* const*,
@@ -1114,18 +1137,19 @@ int ln_bwd_cs_occupancy(int D) {
     return occ[0];
 }
 
-// out[c] += sum_s part_a[s][c] (out2 likewise) for many partial rows: 32 columns x 8 row
-// groups per block, the groups combined in a fixed order (deterministic)
+// out[c] += sum_s part_a[s][c] (out2 likewise) for many partial rows: 8 columns x 32 row
+// groups per block (enough blocks to cover the SMs at d ~ 1k), the groups combined in a
+// fixed order (deterministic)
 __global__ void __launch_bounds__(256) k_colsum_final8(const float* __restrict__ part_a, const float* __restrict__ part_b,
                                                       int splits, int N, float* __restrict__ out, float* __restrict__ out2) {
-    __shared__ float sa[8][33], sb[8][33];
+    __shared__ float sa[32][9], sb[32][9];
     pdl_wait();
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + tx;
+    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+    const int c = blockIdx.x * 8 + tx;
     float a = 0.f, b = 0.f;
     if (c < N) {
 #pragma unroll 4
-        for (int s0 = ty; s0 < splits; s0 += 8) {
+        for (int s0 = ty; s0 < splits; s0 += 32) {
             a += part_a[(long)s0 * N + c];
             b += part_b[(long)s0 * N + c];
         }
@@ -1136,7 +1160,7 @@ __global__ void __launch_bounds__(256) k_colsum_final8(const float* __restrict__
     if (ty == 0 && c < N) {
         float ta = 0.f, tb = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 32; ++q) {
             ta += sa[q][tx];
             tb += sb[q][tx];
         }
@@ -1216,7 +1240,7 @@ void launch_layernorm_bwd(const float* dy, const float* x, const int32_t* rows, 
         if (D <= 512) launch_ln_bwd_cs<T, 4>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
         else if (D <= 896) launch_ln_bwd_cs<T, 7>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
         else launch_ln_bwd_cs<T, 8>(dy, x, rows, mean, rstd, gamma, R, D, res, dx, dx_act, pa, pb, grid, st);
-        launch_pdl(k_colsum_final8, dim3(cdiv(D, 32)), dim3(256), 0, st, (const float*)pa, (const float*)pb, grid, D,
+        launch_pdl(k_colsum_final8, dim3(cdiv(D, 8)), dim3(256), 0, st, (const float*)pa, (const float*)pb, grid, D,
                    dgamma, dbeta);
         PARL_LAUNCHED();
         return;
