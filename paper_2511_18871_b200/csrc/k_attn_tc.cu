@@ -1078,6 +1078,47 @@ __global__ void k_attn_prep(int T, int H, int d, int Dh, long ldo, const int32_t
     }
 }
 
+// The same prologue with 16-byte loads: thread = 8 consecutive columns of one row, the
+// G = Dh / 8 threads of a head reduce by shuffles (G <= 32, aligned groups of a warp);
+// a block covers whole rows, so every warp streams 512 contiguous bytes of O and dO.
+template <int G>
+__global__ void __launch_bounds__(256) k_attn_prep_v8(int T, int H, int d, long ldo, const int32_t* __restrict__ seg,
+                                                      const int32_t* __restrict__ seg_start,
+                                                      const int32_t* __restrict__ seg_end, const bf16* __restrict__ out,
+                                                      const bf16* __restrict__ dout, const float* __restrict__ lse,
+                                                      float* __restrict__ dsum, float* __restrict__ lse2,
+                                                      int2* __restrict__ meta) {
+    pdl_wait();
+    const int d8 = d >> 3;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = t < (long)T * d8;
+    const int i = ok ? (int)(t / d8) : 0, c8 = ok ? (int)(t % d8) : 0;
+    float acc = 0.f;
+    if (ok) {
+        const uint4 o = *reinterpret_cast<const uint4*>(out + (long)i * ldo + 8 * c8);
+        const uint4 g = *reinterpret_cast<const uint4*>(dout + (long)i * d + 8 * c8);
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 a = __bfloat1622float2(o2[q]), b = __bfloat1622float2(g2[q]);
+            acc = fmaf(a.x, b.x, acc);
+            acc = fmaf(a.y, b.y, acc);
+        }
+    }
+#pragma unroll
+    for (int m = G / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (ok && c8 % G == 0) {
+        const long hi = (long)(c8 / G) * T + i;
+        dsum[hi] = acc;
+        lse2[hi] = lse[hi] * LOG2E;
+    }
+    if (ok && c8 == 0) {
+        const int sg = seg[i];
+        meta[i] = make_int2(sg == 0 ? T : seg_end[sg], sg == 0 ? -1 : seg_start[sg]);
+    }
+}
+
 struct BwdWs {
     void* p = nullptr;
     size_t bytes = 0;
@@ -2121,9 +2162,19 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 8 + 16));
         if (!lse2) return false;
         int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
-        const long warps = (long)aa.T * aa.H;
-        launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, aa.Dh,
-                   (long)(aa.ldo ? aa.ldo : aa.d), aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+        const long warps = (long)aa.T * aa.H, ldo = aa.ldo ? aa.ldo : aa.d;
+        const bool v8 = (aa.Dh == 64 || aa.Dh == 128) && aa.d % 8 == 0 && ldo % 8 == 0 &&
+                        (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (reinterpret_cast<uintptr_t>(dout) & 15) == 0;
+        const long thr = (long)aa.T * (aa.d / 8);
+        if (v8 && aa.Dh == 64)
+            launch_pdl(k_attn_prep_v8<8>, dim3((int)((thr + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, ldo,
+                       aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+        else if (v8)
+            launch_pdl(k_attn_prep_v8<16>, dim3((int)((thr + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, ldo,
+                       aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+        else
+            launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, aa.Dh,
+                       ldo, aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
         PARL_LAUNCHED();
         AttnBwd2Args b;
         b.T = aa.T; b.H = aa.H; b.d = aa.d; b.Peff = aa.Peff;
