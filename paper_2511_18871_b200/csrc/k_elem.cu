@@ -75,6 +75,23 @@ __global__ void k_embed(const float* __restrict__ tok_emb, const float* __restri
     }
 }
 
+// float4 variant (D % 4 == 0, 16-byte aligned rows): one warp per token row, no per-element
+// index division
+__global__ void __launch_bounds__(256) k_embed4(const float4* __restrict__ tok_emb, const float4* __restrict__ pos_emb,
+                                                const int32_t* __restrict__ tokens,
+                                                const int32_t* __restrict__ positions, int T, int D4,
+                                                float4* __restrict__ x) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const float4* a = tok_emb + (long)tokens[t] * D4;
+    const float4* b = pos_emb + (long)positions[t] * D4;
+    float4* y = x + (long)t * D4;
+    for (int c = lane; c < D4; c += 32) {
+        const float4 u = a[c], v = b[c];
+        y[c] = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K5: LayerNorm forward, one warp per row; rows optionally gathered through
 // `rows` (final LN over the head's predecessor rows).  Two-pass mean/variance
@@ -629,6 +646,23 @@ __global__ void k_scatter_rows(const float* __restrict__ dxg, const int32_t* __r
     }
 }
 
+// float4 variant: one warp per position row, its head rows summed in CSR order (as above)
+__global__ void __launch_bounds__(256) k_scatter_rows4(const float4* __restrict__ dxg, const int32_t* __restrict__ row_ptr,
+                                                       const int32_t* __restrict__ row_idx, int T, int D4,
+                                                       float4* __restrict__ dx) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const int r0 = row_ptr[t], r1 = row_ptr[t + 1];
+    for (int c = lane; c < D4; c += 32) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = r0; r < r1; ++r) {
+            const float4 v = dxg[(long)row_idx[r] * D4 + c];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        dx[(long)t * D4 + c] = acc;
+    }
+}
+
 // K11: segmented sum of dx rows over runs of equal keys (keys sorted stably,
 // so each run lists its rows in position order): grad[key] += sum dx[idx].
 __global__ void k_embed_grad(const int32_t* __restrict__ keys, const int32_t* __restrict__ idx, int T,
@@ -757,7 +791,13 @@ void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_
 
 void launch_embed(const float* tok, const float* pos, const int32_t* tokens, const int32_t* positions, int T, int D,
                   float* x, cudaStream_t st) {
-    k_embed<<<grid_for((long)T * D), 256, 0, st>>>(tok, pos, tokens, positions, T, D, x);
+    const bool v4 = D % 4 == 0 && ((reinterpret_cast<uintptr_t>(tok) | reinterpret_cast<uintptr_t>(pos) |
+                                    reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+    if (v4)
+        k_embed4<<<cdiv(T, 8), 256, 0, st>>>(reinterpret_cast<const float4*>(tok), reinterpret_cast<const float4*>(pos),
+                                             tokens, positions, T, D / 4, reinterpret_cast<float4*>(x));
+    else
+        k_embed<<<grid_for((long)T * D), 256, 0, st>>>(tok, pos, tokens, positions, T, D, x);
     PARL_LAUNCHED();
 }
 
@@ -1356,7 +1396,11 @@ void launch_grpo(const float* lp, const float* old, const float* ref, const int3
 
 void launch_scatter_rows(const float* dxg, const int32_t* row_ptr, const int32_t* row_idx, int T, int D, float* dx,
                          cudaStream_t st) {
-    k_scatter_rows<<<grid_for((long)T * D), 256, 0, st>>>(dxg, row_ptr, row_idx, T, D, dx);
+    if (D % 4 == 0 && ((reinterpret_cast<uintptr_t>(dxg) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0)
+        k_scatter_rows4<<<cdiv(T, 8), 256, 0, st>>>(reinterpret_cast<const float4*>(dxg), row_ptr, row_idx, T, D / 4,
+                                                    reinterpret_cast<float4*>(dx));
+    else
+        k_scatter_rows<<<grid_for((long)T * D), 256, 0, st>>>(dxg, row_ptr, row_idx, T, D, dx);
     PARL_LAUNCHED();
 }
 
