@@ -445,11 +445,26 @@ __global__ void k_lse_combine(const float* __restrict__ part, int n_parts, const
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (s >= S) return;
     const float2* p = reinterpret_cast<const float2*>(part + (long)s * n_parts * 2);
-    float m = -INFINITY, sum = 0.f;
-    for (int i = lane; i < n_parts; i += 32) {
+    // two independent online chains per lane (parts i and i + 32), merged before the shuffles
+    float m = -INFINITY, sum = 0.f, m1 = -INFINITY, sum1 = 0.f;
+    int i = lane;
+    for (; i + 32 < n_parts; i += 64) {
+        const float2 v = p[i], w = p[i + 32];
+        const float nm = fmaxf(m, v.x), nm1 = fmaxf(m1, w.x);
+        if (nm > -INFINITY) sum = sum * __expf(m - nm) + v.y * __expf(v.x - nm);
+        if (nm1 > -INFINITY) sum1 = sum1 * __expf(m1 - nm1) + w.y * __expf(w.x - nm1);
+        m = nm;
+        m1 = nm1;
+    }
+    if (i < n_parts) {
         const float2 v = p[i];
         const float nm = fmaxf(m, v.x);
         if (nm > -INFINITY) sum = sum * __expf(m - nm) + v.y * __expf(v.x - nm);
+        m = nm;
+    }
+    {
+        const float nm = fmaxf(m, m1);
+        sum = nm > -INFINITY ? sum * __expf(m - nm) + sum1 * __expf(m1 - nm) : 0.f;
         m = nm;
     }
 #pragma unroll
