@@ -91,17 +91,24 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons during the timed region.
+
+    nvidia-smi takes a few hundred ms to produce its first line, longer than a short timed
+    region, so the sampler is started before the warm-up steps (same load) and `mark()` /
+    `stop()` bracket the timed region; only samples stamped inside it are summarised. If the
+    region was shorter than the 100 ms sampling period, the last warm-up sample stands in
+    and the summary says so (`"window": "warmup"`)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (monotonic time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -116,9 +123,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             p = [x.strip() for x in line.split(",")]
             if len(p) >= 7:
-                self.samples.append(p)
+                self.samples.append((time.monotonic(), p))
 
-    def __exit__(self, *a):
+    def mark(self):
+        self.t0 = time.monotonic()
+
+    def stop(self):
+        self.t1 = time.monotonic()
         if self.proc:
             self.proc.terminate()
             try:
@@ -127,14 +138,21 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        t0 = self.t0 if self.t0 is not None else -1e30
+        t1 = self.t1 if self.t1 is not None else 1e30
+        inside = [p for t, p in self.samples if t0 <= t <= t1]
+        window = "timed"
+        if not inside:
+            before = [p for t, p in self.samples if t < t0]
+            inside, window = before[-1:], "warmup"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        sm = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in inside if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for s in inside for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def dist_setup(n_gpus):
@@ -331,10 +349,12 @@ def run_ours(args, c):
             ctx.stats_allreduce()
         return ctx.stats()
 
+    clk = ClockSampler(local).start()  # running through the warm-up: its first line takes ~0.3 s
     for _ in range(args.warmup):
         step_device()
     ctx.sync()
-    if args.launch_list:  # one step inside an NVTX range for `ncu --nvtx --nvtx-include step/`
+    if args.launch_list:
+        clk.stop()  # one step inside an NVTX range for `ncu --nvtx --nvtx-include step/`
         torch.cuda.nvtx.range_push("step")
         step_device()
         ctx.sync()
@@ -346,12 +366,13 @@ def run_ours(args, c):
     barrier(pg)
     ctx.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step_device()
-        e1.record(stream)
-        ctx.sync()
+    clk.mark()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_device()
+    e1.record(stream)
+    ctx.sync()
+    clk.stop()
     launches = (ctx.launches - l0) // max(args.steps, 1)
     ms = e0.elapsed_time(e1)
     barrier(pg)
