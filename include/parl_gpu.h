@@ -60,6 +60,18 @@ typedef struct {
     double objective_sum, clip_sum, kl_sum, clipped_units, total_units;
 } parl_loss_stats;
 
+/* SampleTerms (scalar part), proj/include/parl/grpo.hpp:64-70 */
+typedef struct {
+    double clip_term, kl;
+    int clipped_units, total_units;
+} parl_sample_terms;
+
+/* LossReport, proj/include/parl/grpo.hpp:41-47 */
+typedef struct {
+    double objective, clip_term_mean, kl_mean, clip_fraction;
+    long token_count;
+} parl_loss_report;
+
 typedef struct parl_ctx_s* parl_ctx_t;     /* device, stream, workspaces, optional NCCL comm */
 typedef struct parl_model_s* parl_model_t; /* one device weight set (ModelParams) */
 typedef struct parl_group_s* parl_group_t; /* one packed sequence (PackedGroup + K1 outputs) */
@@ -122,6 +134,16 @@ parl_status parl_model_copy(parl_model_t dst, parl_model_t src, uint64_t seed, d
 parl_status parl_model_download(parl_model_t m, double* flat, size_t n);
 size_t parl_param_count(const parl_config* cfg);
 uint64_t parl_model_version(parl_model_t m);
+/* ModelParams::init_seed (model.hpp:71): kept by init / copy / checkpoint load; set by callers that
+ * upload weights drawn elsewhere (checkpoint header field). */
+uint64_t parl_model_init_seed(parl_model_t m);
+/* Write counter of the device weights (upload / init / copy / update / load): host mirrors key on it. */
+uint64_t parl_model_epoch(parl_model_t m);
+/* ModelParams::forward_generation (model.hpp:100-101): bumped by every forward on this model. */
+uint64_t parl_model_forward_gen(parl_model_t m);
+parl_status parl_model_set_init_seed(parl_model_t m, uint64_t seed);
+/* ModelParams::all_finite (model.cpp:183-187): *out = 1 when every weight is finite. */
+parl_status parl_model_all_finite(parl_model_t m, int* out);
 
 /* Checkpoints in the reference's PARLCKP1 format (docs/formats.md): save_checkpoint /
  * load_checkpoint (model.cpp:924-987).  IoError on open / magic / truncation / layout
@@ -196,6 +218,7 @@ parl_status parl_stats_reset(parl_ctx_t ctx);
 /* ---- backward: backward (model.cpp:587-838) + GradBuffer::accumulate
  *      (model.cpp:189-194); uses the group's upstream seed --------------- */
 parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out);
+parl_status parl_grad_create_config(parl_ctx_t ctx, const parl_config* cfg, parl_grad_t* out);
 parl_status parl_grad_destroy(parl_grad_t gr);
 parl_status parl_grad_reset(parl_grad_t gr);
 parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl_group_t g,
@@ -203,7 +226,16 @@ parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl
 parl_status parl_grad_download(parl_grad_t gr, double* flat, size_t n);
 /* GradBuffer::accumulate (model.cpp:189-194): dst += src, counts add. */
 parl_status parl_grad_accumulate(parl_grad_t dst, parl_grad_t src);
+/* GradBuffer::micro_step_count / set_micro_step_count / add_micro_steps (model.hpp:124-127).
+ * parl_backward adds 1 per call (backward returns a count-1 buffer that accumulate adds);
+ * the pipeline sets the batch's N*G before apply_update (pipeline.cpp:346-351). */
 int parl_grad_micro_steps(parl_grad_t gr);
+parl_status parl_grad_set_micro_steps(parl_grad_t gr, int n);
+parl_status parl_grad_add_micro_steps(parl_grad_t gr, int n);
+/* GradBuffer::all_finite (model.cpp:196-200) */
+parl_status parl_grad_all_finite(parl_grad_t gr, int* out);
+/* Host fp64 gradient -> device accumulator (GradBuffer::flat_mut() writes of a drop-in caller). */
+parl_status parl_grad_upload(parl_grad_t gr, const double* flat, size_t n);
 
 /* ---- whole micro-step: Pipeline::train_microbatch shared-prompt branch
  *      (pipeline.cpp:97-141) in one call ------------------------------------ */
@@ -211,6 +243,25 @@ parl_status parl_train_microbatch(parl_ctx_t ctx, parl_model_t pol, parl_model_t
                                   parl_model_t ref, parl_group_t g, const double* rewards,
                                   const double* advantages, const parl_hyper* hp,
                                   parl_grad_t gr, parl_loss_stats* stats_out);
+
+/* ---- GRPO operator API (grpo.hpp:50-83) on host arrays, evaluated by the K7 kernels in fp64 ----
+ * group_advantages / group_advantages_mean_only (grpo.cpp:24-48): ConfigError for G < 2. */
+parl_status parl_group_advantages(parl_ctx_t ctx, const double* rewards, int G, int mean_only, double* adv);
+/* clipped_term / kl_term (grpo.cpp:95-108): NumericError on non-finite input, ConfigError on eps. */
+parl_status parl_clipped_term(parl_ctx_t ctx, double lp_new, double lp_old, double adv, double eps, double* out);
+parl_status parl_kl_term(parl_ctx_t ctx, double lp_new, double lp_ref, double* out);
+/* per_sample_terms (grpo.cpp:111-151) for one sample of n tokens: upstream[n] = d(L - beta KL)/d lp. */
+parl_status parl_per_sample_terms(parl_ctx_t ctx, const double* lp, const double* old, const double* ref, int n,
+                                  double adv, double eps, double beta, int granularity, double* upstream,
+                                  parl_sample_terms* out);
+/* grpo_microbatch_loss (grpo.cpp:153-184) over m samples of lengths lens[m] (log-prob vectors and
+ * upstream concatenated in sample order): upstream = -(1/m) per-sample upstream. */
+parl_status parl_grpo_microbatch_loss(parl_ctx_t ctx, int m, const int32_t* lens, const double* lp,
+                                      const double* old, const double* ref, const double* advantages, double eps,
+                                      double beta, int granularity, double* upstream, parl_loss_report* report,
+                                      double* loss);
+/* build_shared_prompt_mask (packing.cpp:47-72): row-major [n x n] 0/1, n = P + sum(lens). */
+parl_status parl_shared_prompt_mask(parl_ctx_t ctx, int P, const int32_t* lens, int G, uint8_t* mask);
 
 /* ---- apply_update (model.cpp:202-219) on the device: W -= lr*g/count,
  *      refusing non-finite gradients/results (weights untouched). ---------- */

@@ -243,6 +243,42 @@ class Oracle:
         self._chk(rc, "train_microbatch")
         return grad_acc, stats, lp3.reshape(3, S)
 
+    def train_iteration(self, cfg: Cfg, w_pol, w_old, w_ref, microbatches, lr, eps=0.2, beta=0.04,
+                        granularity=0, rollout_old=None, total_samples=None):
+        """pipeline.cpp:263-352 (training half): micro-batches [(prompt, responses, advantages)],
+        accumulate, divisor N*G, snapshot, apply_update.  Returns (new_policy, new_old, stats5).
+        The C restatement composes orc_train_microbatch with ModelParams::apply_update's
+        arithmetic (model.cpp:202-219); the reference runs its own TriModel / GradBuffer."""
+        total = total_samples if total_samples is not None else sum(len(mb[2]) for mb in microbatches)
+        w_pol, w_old, w_ref = _f64(w_pol).copy(), _f64(w_old).copy(), _f64(w_ref)
+        stats = np.zeros(5, dtype=np.float64)
+        if self.kind == "ref":
+            pflat = _i32(np.concatenate([np.asarray(mb[0], np.int32) for mb in microbatches]))
+            plens = _i32([len(mb[0]) for mb in microbatches])
+            rlist = [r for mb in microbatches for r in mb[1]]
+            rflat = _i32(np.concatenate([np.asarray(r, np.int32) for r in rlist]))
+            lens = _i32([len(r) for r in rlist])
+            off = _i32(np.concatenate([[0], np.cumsum([len(mb[1]) for mb in microbatches])]))
+            adv = _f64(np.concatenate([np.asarray(mb[2], np.float64) for mb in microbatches]))
+            ro = _f64(rollout_old) if rollout_old is not None else None
+            c = cfg.c()
+            rc = self.lib.ref_train_iteration(C.byref(c), _p(w_pol), _p(w_old), _p(w_ref), len(microbatches),
+                                              _p(pflat), _p(plens), _p(rflat), _p(lens), _p(off), _p(adv), _p(ro),
+                                              C.c_double(eps), C.c_double(beta), granularity, C.c_double(lr),
+                                              int(total), _p(stats))
+            self._chk(rc, "train_iteration")
+            return w_pol, w_old, stats
+        if rollout_old is not None:
+            raise NotImplementedError("rollout_weights iteration: use the reference build")
+        g = np.zeros(len(w_pol), dtype=np.float64)
+        for prompt, responses, adv in microbatches:
+            _, st, _ = self.train_microbatch(cfg, w_pol, w_old, w_ref, prompt, responses, adv, eps, beta,
+                                             granularity, grad_acc=g)
+            stats += st
+        new_old = w_pol.copy()  # snapshot_old_policy before the update (pipeline.cpp:350-351)
+        w_new = w_pol - (lr / float(total)) * g
+        return w_new, new_old, stats
+
     def bench_microbatch(self, cfg: Cfg, seed, P, G, R, reps, threads) -> float:
         assert self.kind == "ref"
         c = cfg.c()

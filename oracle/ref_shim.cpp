@@ -176,10 +176,18 @@ namespace {
 void microbatch(TriModel& tm, const std::vector<TokenId>& prompt,
                 const std::vector<std::vector<TokenId>>& responses,
                 const std::vector<double>& advantages, double eps, double beta,
-                LossGranularity gran, GradBuffer& grads, double* stats5, double* lp3) {
+                LossGranularity gran, GradBuffer& grads, double* stats5, double* lp3,
+                const double* rollout_old = nullptr) {
     PackedGroup packed = pack_group(prompt, responses, tm.policy.config().max_seq_len);
-    TriForwardResult tri =
-        trimodel_forward(tm, packed.tokens, packed.positions, packed.mask, packed.labels);
+    TriForwardResult tri;
+    if (!rollout_old) {  // one_step_delayed (pipeline.cpp:110-112)
+        tri = trimodel_forward(tm, packed.tokens, packed.positions, packed.mask, packed.labels);
+    } else {  // rollout_weights: policy + reference only, old log-probs from the rollout (pipeline.cpp:113-119)
+        tri.policy = forward_logprobs(tm.policy, packed.tokens, packed.positions, packed.mask, packed.labels, true);
+        tri.ref_logprobs =
+            forward_logprobs(tm.reference, packed.tokens, packed.positions, packed.mask, packed.labels).logprobs;
+        tri.old_logprobs.assign(rollout_old, rollout_old + tri.policy.logprobs.size());
+    }
     auto pol = extract_response_logprobs(tri.policy.logprobs, packed);
     auto ref = extract_response_logprobs(tri.ref_logprobs, packed);
     auto old = extract_response_logprobs(tri.old_logprobs, packed);
@@ -238,6 +246,48 @@ int ref_train_microbatch(const CCfg* c, const double* w_pol, const double* w_old
                    gran ? LossGranularity::sequence : LossGranularity::token, grads, stats5, lp3);
         for (size_t i = 0; i < n; ++i) grad_acc[i] += grads.flat()[i];
         return (int)(P + off);
+    });
+}
+
+// The training half of Pipeline::run_iteration (pipeline.cpp:263-352) through the reference API:
+// n_mb shared-prompt micro-batches (micro-batch b: prompt b, lens[mb_off[b] .. mb_off[b+1]),
+// advantages alongside, optional rollout old log-probs), accumulated in order, then
+// set_micro_step_count(N*G) -> snapshot_old_policy -> apply_update(lr).  w_pol / w_old are
+// replaced by the updated policy / snapshot; stats5 summed.
+int ref_train_iteration(const CCfg* c, double* w_pol, double* w_old, const double* w_ref, int n_mb,
+                        const int* prompt_flat, const int* prompt_lens, const int* resp_flat, const int* lens,
+                        const int* mb_off, const double* adv, const double* rollout_old, double eps, double beta,
+                        int gran, double lr, int total_samples, double* stats5) {
+    return guarded([&] {
+        TriModel tm = TriModel::init(to_cfg(c), 0);
+        const size_t n = tm.policy.flat().size();
+        std::memcpy(tm.policy.flat_mut().data(), w_pol, n * sizeof(double));
+        std::memcpy(tm.old_policy.flat_mut().data(), w_old, n * sizeof(double));
+        std::memcpy(tm.reference.flat_mut().data(), w_ref, n * sizeof(double));
+        GradBuffer grad_acc(tm.policy);
+        int po = 0, ro = 0, so = 0;
+        for (int b = 0; b < n_mb; ++b) {
+            std::vector<TokenId> pr(prompt_flat + po, prompt_flat + po + prompt_lens[b]);
+            po += prompt_lens[b];
+            std::vector<std::vector<TokenId>> rs;
+            std::vector<double> a;
+            int S = 0;
+            for (int k = mb_off[b]; k < mb_off[b + 1]; ++k) {
+                rs.emplace_back(resp_flat + ro, resp_flat + ro + lens[k]);
+                ro += lens[k];
+                S += lens[k];
+                a.push_back(adv[k]);
+            }
+            microbatch(tm, pr, rs, a, eps, beta, gran ? LossGranularity::sequence : LossGranularity::token, grad_acc,
+                       stats5, nullptr, rollout_old ? rollout_old + so : nullptr);
+            so += S;
+        }
+        grad_acc.set_micro_step_count(total_samples);
+        tm.snapshot_old_policy();
+        tm.policy.apply_update(grad_acc, lr);
+        std::memcpy(w_pol, tm.policy.flat().data(), n * sizeof(double));
+        std::memcpy(w_old, tm.old_policy.flat().data(), n * sizeof(double));
+        return 0;
     });
 }
 

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-SOURCES = ["abi.cu", "k_elem.cu", "k_gemm_simt.cu", "k_attn.cu", "k_gemm_tc.cu", "k_attn_tc.cu"]
+SOURCES = ["abi.cu", "k_elem.cu", "k_grpo.cu", "k_gemm_simt.cu", "k_attn.cu", "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 
 def _deps(src: str):
@@ -74,6 +74,50 @@ def build_cpp_tests() -> str:
                                "-I/usr/local/cuda/include", src, oracle_o, "-L" + PKG, "-lparl_gpu",
                                "-Wl,-rpath," + PKG, "-lm", "-o", out])
     return out
+
+
+REF_PROJ = os.environ.get("PARL_REF_PROJ", "/root/reference/proj")
+REF_SUITES = {  # suite -> reference sources compiled against the drop-in headers (unmodified)
+    "test_packing": [],
+    "test_grpo": [],
+    "test_model": ["src/gradcheck.cpp"],
+    "test_pipeline": ["src/pipeline.cpp", "src/rollout.cpp", "src/tasks.cpp"],
+}
+
+
+def build_ref_suites() -> list:
+    """The reference's own hot-path test suites (proj/tests/test_*.cpp), compiled UNMODIFIED
+    from where they lie against the drop-in headers (include/parl/*.hpp shadow the reference's
+    model / packing / grpo / errors headers; the rest of its include tree is used as is) with a
+    doctest shim (tests/cpp/doctest), linked with libparl_gpu.so.  The reference caller code the
+    suites need (pipeline.cpp, rollout.cpp, tasks.cpp, gradcheck.cpp) is compiled the same way.
+    Binaries go to build/ref_suites/ (git-ignored; shipped to the GPU box); nothing is copied.
+    Only where /root/reference exists (this container)."""
+    if not os.path.isdir(REF_PROJ):
+        return []
+    build()
+    out_dir = os.path.join(BUILD, "ref_suites")
+    os.makedirs(out_dir, exist_ok=True)
+    inc = ["-I" + os.path.join(ROOT, "tests", "cpp", "doctest"), "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(REF_PROJ, "include")]
+    hdrs = [os.path.join(ROOT, "include", "parl", h) for h in os.listdir(os.path.join(ROOT, "include", "parl"))]
+    hdrs += [os.path.join(ROOT, "include", "parl_gpu.h"), os.path.join(ROOT, "tests", "cpp", "doctest", "doctest.h")]
+
+    def one(name):
+        srcs = [os.path.join(REF_PROJ, "tests", name + ".cpp"), os.path.join(REF_PROJ, "tests", "doctest_main.cpp")]
+        srcs += [os.path.join(REF_PROJ, s) for s in REF_SUITES[name]]
+        exe = os.path.join(out_dir, name)
+        if _stale(exe, srcs + hdrs + [LIB]):
+            cmd = ["g++", "-std=c++20", "-O2", *inc, *srcs, "-L" + PKG, "-lparl_gpu", "-Wl,-rpath,$ORIGIN/../..",
+                   "-lpthread", "-o", exe]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stderr[-4000:])
+                raise RuntimeError(f"reference suite {name} failed to compile against the drop-in")
+        return exe
+
+    with ThreadPoolExecutor(max_workers=len(REF_SUITES)) as ex:
+        return list(ex.map(one, REF_SUITES))
 
 
 if __name__ == "__main__":

@@ -11,6 +11,7 @@
 #include <fstream>
 #include <string>
 #include <memory>
+#include <mutex>
 #include <queue>
 #include <random>
 #include <type_traits>
@@ -114,7 +115,10 @@ struct parl_ctx_s {
     unsigned item_base = 0;
     // backward workspaces
     DevBuf dx, dx2, dx_act, dpre, dbn, dmid, dmid_act, dctx, dqkv, da, dsum, dhf, dxg, dz;
-    DevBuf stats, per_sample, staging, flags;
+    DevBuf stats, per_sample, staging, flags, grpo_slots, g_seq;
+    // one caller at a time per context (the reference allows distinct ModelParams on distinct
+    // threads; they share this context's stream and workspaces)
+    std::recursive_mutex mu;
     // kernel-class profiler (parl_ctx_profile)
     struct ProfRec {
         int cls;
@@ -175,6 +179,7 @@ struct parl_model_s {
     bool has_master = false;
     uint64_t version = 0, forward_gen = 0;
     uint64_t init_seed = 0;  // ModelParams::init_seed (checkpoint header)
+    uint64_t epoch = 0;  // bumped by every write of the weights (host mirrors of the drop-in key on it)
 };
 
 struct parl_group_s {
@@ -196,6 +201,11 @@ struct parl_group_s {
     std::vector<int> lens, span_start, cu;
     std::vector<int> sched_key;  // segment structure the schedule was built for
     int max_seq = 0, vocab = 0;
+    // token-id range of the packed tokens (validate_forward_inputs, model.cpp:413-417): known on
+    // the host for host-packed groups, read once from K1's device reduction for device-packed ones
+    int tok_min = 0, tok_max = 0;
+    bool tok_range_dev = false;  // pending on the device (parl_pack_device)
+    DevBuf tok_range;
 };
 
 struct parl_act_s {
@@ -217,6 +227,10 @@ struct parl_grad_s {
     FlatLayout L{};
     DevBuf g;
     int micro_steps = 0;
+    // after a data-parallel allreduce the count is the sum over ranks, held on the device until
+    // apply_update (which synchronises anyway) reads it
+    DevBuf count_dev;
+    bool count_on_device = false;
     // tok_emb rows touched by this buffer's backward passes (the other rows are exactly 0), so
     // the data-parallel exchange of the V x d token-embedding gradient sends only those rows
     DevBuf touched, sel_idx, sel_rows, sel_count;
@@ -266,6 +280,8 @@ thread_local std::string tl_err;
 
 template <class F>
 parl_status guarded(parl_ctx_s* c, F&& f) {
+    std::unique_lock<std::recursive_mutex> lk;
+    if (c) lk = std::unique_lock<std::recursive_mutex>(c->mu);
     try {
         f();
         return PARL_OK;
@@ -298,6 +314,11 @@ void validate_config(const parl_config& c) {  // ModelConfig::validate, model.cp
                                        std::to_string(c.n_heads) + ")"};
     if (c.d_model / c.n_heads > 128) throw Error{PARL_E_CONFIG, "head dim > 128 not supported by the device path"};
 }
+
+// per-array stride of the group's [T] vectors: a multiple of 4 elements keeps every array
+// 16-byte aligned for the vectorised kernels (K7)
+size_t group_stride(const parl_group_s* g) { return ((size_t)g->max_T + 3) & ~(size_t)3; }
+float* group_lp(parl_group_s* g, int slot) { return static_cast<float*>(g->lp.p) + (size_t)slot * group_stride(g); }
 
 bool same_cfg(const parl_config& a, const parl_config& b) { return std::memcmp(&a, &b, sizeof(a)) == 0; }
 
@@ -374,13 +395,18 @@ void convert_from_master(parl_model_s* m) {
     check_launch();
 }
 
+// Contractions: bf16 runs on the tcgen05 kernels only (a shape they reject is an
+// error, never a silent SIMT fallback); fp32 (BASELINE configs[0]) is the FFMA kernel.
 template <class T>
 void gemm(parl_ctx_s* c, const GemmArgs& g, int cls = PARL_KC_GEMM) {
     ProfScope ps(c, cls, 2.0 * g.M * (double)g.N * g.K);
     if constexpr (std::is_same_v<T, bf16>) {
-        if (gemm_tc(g, c->st)) return;
+        PARL_REQUIRE(gemm_tc(g, c->st), PARL_E_CONFIG,
+                     "tcgen05 GEMM rejected shape " + std::to_string(g.M) + "x" + std::to_string(g.N) + "x" +
+                         std::to_string(g.K) + " (bf16 needs 16-byte aligned rows)");
+    } else {
+        gemm_simt<T>(g, c->st);
     }
-    gemm_simt<T>(g, c->st);
 }
 
 GemmArgs mk(int M, int N, int K, const void* A, long sam, long sak, const void* B, long sbn, long sbk) {
@@ -430,12 +456,10 @@ void gemm_multi(parl_ctx_s* c, const GemmArgs* gs, int n) {
     ProfScope ps(c, PARL_KC_GEMM, fl);
     if constexpr (std::is_same_v<T, bf16>) {
         if (gemm_tc_multi(gs, n, c->st)) return;
-    }
-    for (int q = 0; q < n; ++q) {
-        if constexpr (std::is_same_v<T, bf16>) {
-            if (gemm_tc(gs[q], c->st)) continue;
-        }
-        gemm_simt<T>(gs[q], c->st);
+        for (int q = 0; q < n; ++q)
+            PARL_REQUIRE(gemm_tc(gs[q], c->st), PARL_E_CONFIG, "tcgen05 GEMM rejected a layer shape");
+    } else {
+        for (int q = 0; q < n; ++q) gemm_simt<T>(gs[q], c->st);
     }
 }
 
@@ -523,10 +547,12 @@ void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs
             cl[k] = b.ctxo + b.lay(TDp, l);
             la[k] = b.lse_attn + b.lay((size_t)H * Tn, l);
         }
-        bool done = false;  // the models' attention as one launch (tcgen05 path)
-        if constexpr (std::is_same_v<T, bf16>) done = attn_fwd_tc_multi(aa, ql, cl, la, nm, st);
-        if (!done)
+        if constexpr (std::is_same_v<T, bf16>) {  // the models' attention as one tcgen05 launch
+            PARL_REQUIRE(attn_fwd_tc_multi(aa, ql, cl, la, nm, st), PARL_E_CONFIG,
+                         "tcgen05 attention rejected the head dim / alignment");
+        } else {
             for (int k = 0; k < nm; ++k) launch_attn_fwd<T>(aa, ql[k], cl[k], la[k], st);
+        }
     }
     for (int k = 0; k < nm; ++k) {  // O projection + residual (model.cpp:504-506)
         const FwdBufs<T>& b = B[k];
@@ -695,7 +721,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
         float* lnf_mean = ak ? ak->lnf_mean.as<float>(S) : r.lnf_mean.as<float>(S);
         float* lnf_rstd = ak ? ak->lnf_rstd.as<float>(S) : r.lnf_rstd.as<float>(S);
         float* lse_head = ak ? ak->lse_head.as<float>(S) : r.lse_head.as<float>(S);
-        float* lp = static_cast<float*>(g->lp.p) + (size_t)slots[k] * g->max_T;
+        float* lp = group_lp(g, slots[k]);
         if (S > 0) {
             launch_layernorm<T>(xfin, g->pk.pred_pos, S, D, m->W.lnf_g, m->W.lnf_b, hf, Dp, lnf_mean, lnf_rstd, st);
             bool fused = false;
@@ -715,7 +741,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
                 float* logits = ak ? ak->logits.as<float>((size_t)S * V) : r.logits.as<float>((size_t)S * V);
                 GemmArgs ga = mk(S, V, D, hf, Dp, 1, m->W.head_w_t, D, 1);
                 ga.epi = EPI_F32; ga.bias = m->W.head_b; ga.Cf = logits; ga.ldc = V;
-                gemm_simt<T>(ga, st);
+                gemm<T>(c, ga, PARL_KC_HEAD);
                 launch_row_lse(logits, S, V, g->pk.scored_label, lse_head, lp, st);
             }
             if (ak) ak->logits_bf16 = fused;
@@ -849,7 +875,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             ProfScope ps(c, PARL_KC_GEMM, fl);
             done = gemm_tc_group_dw(dw.data(), (int)dw.size(), st);
         }
-        if (!done)
+        if (!done)  // one tcgen05 launch per problem (N not a multiple of 128)
             for (const auto& ga : dw) gemm<T>(c, ga);
         dw.clear();
     };
@@ -910,11 +936,12 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         // attention (model.cpp:752-786)
         {
             ProfScope ps(c, PARL_KC_ATTN_BWD, 10.0 * g->pairs * D);
-            bool done = false;
-            if constexpr (std::is_same_v<T, bf16>) {
-                done = attn_bwd_tc(aa, ql, cl, dctx, la, dsum, dqkv, st);  // computes D = rowsum(dO O) itself
+            if constexpr (std::is_same_v<T, bf16>) {  // computes D = rowsum(dO O) itself
+                PARL_REQUIRE(attn_bwd_tc(aa, ql, cl, dctx, la, dsum, dqkv, st), PARL_E_CONFIG,
+                             "tcgen05 attention backward rejected the head dim / alignment");
+            } else {
+                launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
             }
-            if (!done) launch_attn_bwd<T>(aa, ql, cl, dctx, la, dsum, dqkv, st);
         }
         // Q/K/V projections (model.cpp:789-817)
         {
@@ -1158,7 +1185,8 @@ void ensure_attn_work(parl_group_s* g, int H, int d) {
 }
 
 void alloc_group_arrays(parl_group_s* g) {
-    const int T = g->max_T, G = g->max_G;
+    const size_t T = group_stride(g);
+    const int G = g->max_G;
     // tokens labels positions seg pred [T] ; scored_pos scored_label pred_pos sample_of [T];
     // row_ptr [T+1]; row_idx [T]
     int32_t* base = g->ints.as<int32_t>((size_t)T * 10 + 1);
@@ -1173,7 +1201,7 @@ void alloc_group_arrays(parl_group_s* g) {
     g->pk.sample_of = base + 8 * (size_t)T;
     g->pk.row_idx = base + 9 * (size_t)T;
     g->seg_se.as<int32_t>(2 * (size_t)(G + 1));               // segment [start, end) bounds
-    g->pk.row_ptr = g->cu_d.as<int32_t>((size_t)T + 1 + (G + 1));  // row_ptr [T+1] | cu [G+1]
+    g->pk.row_ptr = g->cu_d.as<int32_t>((size_t)g->max_T + 1 + (G + 1));  // row_ptr [T+1] | cu [G+1]
     g->lp.as<float>((size_t)3 * T);
     g->upstream.as<float>(T);
     g->rewards.as<double>(G);
@@ -1307,6 +1335,13 @@ size_t parl_param_count(const parl_config* cfg) { return make_layout(*cfg).total
 parl_status parl_model_create(parl_ctx_t ctx, const parl_config* cfg, parl_model_t* out) {
     return guarded(ctx, [&] {
         validate_config(*cfg);
+        if (ctx->prec == PARL_PREC_BF16) {  // shapes the tcgen05 kernels take (no SIMT fallback in bf16)
+            const int dh = cfg->d_model / cfg->n_heads;
+            PARL_REQUIRE(dh == 64 || dh == 128, PARL_E_CONFIG,
+                         "bf16 path needs head dim 64 or 128, got " + std::to_string(dh));
+            PARL_REQUIRE(cfg->d_model % 8 == 0 && cfg->d_ff % 8 == 0 && cfg->vocab_size % 8 == 0, PARL_E_CONFIG,
+                         "bf16 path needs d_model, d_ff and vocab_size divisible by 8 (16-byte TMA rows)");
+        }
         auto m = std::make_unique<parl_model_s>();
         m->ctx = ctx;
         ctx->refs++;
@@ -1343,14 +1378,37 @@ parl_status parl_model_create(parl_ctx_t ctx, const parl_config* cfg, parl_model
 parl_status parl_model_destroy(parl_model_t m) {
     if (m) {
         parl_ctx_s* c = m->ctx;
-        cudaStreamSynchronize(c->st);
-        delete m;
+        {
+            std::lock_guard<std::recursive_mutex> lk(c->mu);
+            cudaStreamSynchronize(c->st);
+            delete m;
+        }
         ctx_release(c);
     }
     return PARL_OK;
 }
 
 uint64_t parl_model_version(parl_model_t m) { return m->version; }
+uint64_t parl_model_init_seed(parl_model_t m) { return m->init_seed; }
+uint64_t parl_model_epoch(parl_model_t m) { return m->epoch; }
+uint64_t parl_model_forward_gen(parl_model_t m) { return m->forward_gen; }
+parl_status parl_model_set_init_seed(parl_model_t m, uint64_t seed) {
+    return guarded(m->ctx, [&] { m->init_seed = seed; });
+}
+
+parl_status parl_model_all_finite(parl_model_t m, int* out) {
+    return guarded(m->ctx, [&] {
+        PARL_REQUIRE(m->has_master, PARL_E_CONFIG, "all_finite needs the fp64 master copy");
+        cudaStream_t st = m->ctx->st;
+        int* flags = m->ctx->flags.as<int>(1);
+        PARL_CUDA(cudaMemsetAsync(flags, 0, 4, st));
+        launch_finite_check_f64(static_cast<const double*>(m->master.p), (long)m->L.total, flags, st);
+        int h = 0;
+        PARL_CUDA(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, st));
+        PARL_CUDA(cudaStreamSynchronize(st));
+        *out = h == 0;
+    });
+}
 
 parl_status parl_model_upload(parl_model_t m, const double* flat, size_t n, uint64_t version) {
     return guarded(m->ctx, [&] {
@@ -1369,6 +1427,7 @@ parl_status parl_model_upload(parl_model_t m, const double* flat, size_t n, uint
         }
         PARL_CUDA(cudaStreamSynchronize(st));
         m->version = version;
+        ++m->epoch;
     });
 }
 
@@ -1431,6 +1490,7 @@ parl_status parl_model_init_device(parl_model_t m, uint64_t seed, double scale) 
         PARL_CUDA(cudaStreamSynchronize(st));
         m->version = 0;
         m->init_seed = seed;
+        ++m->epoch;
     });
 }
 
@@ -1466,6 +1526,8 @@ parl_status parl_model_copy(parl_model_t dst, parl_model_t src, uint64_t seed, d
         }
         PARL_CUDA(cudaStreamSynchronize(st));
         dst->version = src->version;
+        dst->init_seed = src->init_seed;  // ModelParams::clone keeps init_seed_ (model.cpp:172-181)
+        ++dst->epoch;
     });
 }
 
@@ -1641,8 +1703,11 @@ parl_status parl_group_create(parl_ctx_t ctx, int max_tokens, int max_responses,
 parl_status parl_group_destroy(parl_group_t g) {
     if (g) {
         parl_ctx_s* c = g->ctx;
-        cudaStreamSynchronize(c->st);
-        delete g;
+        {
+            std::lock_guard<std::recursive_mutex> lk(c->mu);
+            cudaStreamSynchronize(c->st);
+            delete g;
+        }
         ctx_release(c);
     }
     return PARL_OK;
@@ -1656,6 +1721,11 @@ parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_
     return guarded(g->ctx, [&] {
         check_pack_inputs(g, P, lens, G, max_seq);
         set_pack_meta(g, P, lens, G, max_seq);
+        unsigned umax = 0;  // (unsigned)id >= V <=> id outside [0, V)
+        for (int i = 0; i < P; ++i) umax = std::max(umax, (unsigned)prompt[i]);
+        for (int i = 0; i < g->S; ++i) umax = std::max(umax, (unsigned)resp_flat[i]);
+        g->tok_max = (int)std::min<unsigned>(umax, INT32_MAX);
+        g->tok_range_dev = false;
         cudaStream_t st = g->ctx->st;
         int32_t* dp = g->in_prompt.as<int32_t>(g->max_T);
         int32_t* dr = g->in_resp.as<int32_t>(g->max_T);
@@ -1663,7 +1733,7 @@ parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_
         PARL_CUDA(cudaMemcpyAsync(dr, resp_flat, (size_t)g->S * 4, cudaMemcpyHostToDevice, st));
         upload_meta(g);
         ProfScope ps(g->ctx, PARL_KC_PACK, 24.0 * g->T + 24.0 * g->S);
-        launch_pack(dp, P, dr, group_cu(g), G, g->T, g->pk, st);
+        launch_pack(dp, P, dr, group_cu(g), G, g->T, g->pk, nullptr, st);
         check_launch();
     });
 }
@@ -1675,7 +1745,8 @@ parl_status parl_pack_device(parl_group_t g, const int32_t* d_prompt, int P, con
         set_pack_meta(g, P, lens, G, max_seq);
         upload_meta(g);
         ProfScope ps(g->ctx, PARL_KC_PACK, 24.0 * g->T + 24.0 * g->S);
-        launch_pack(d_prompt, P, d_resp, group_cu(g), G, g->T, g->pk, g->ctx->st);
+        launch_pack(d_prompt, P, d_resp, group_cu(g), G, g->T, g->pk, g->tok_range.as<unsigned>(1), g->ctx->st);
+        g->tok_range_dev = true;  // read (once) by the first forward over this packing
         check_launch();
     });
 }
@@ -1690,6 +1761,9 @@ parl_status parl_set_sequence(parl_group_t g, const int32_t* tokens, const int32
         for (int t = 0; t < T; ++t)
             PARL_REQUIRE(tokens[t] >= 0 && tokens[t] < vocab, PARL_E_VOCAB,
                          "token id " + std::to_string(tokens[t]) + " outside vocab of size " + std::to_string(vocab));
+        g->tok_max = 0;
+        for (int t = 0; t < T; ++t) g->tok_max = std::max(g->tok_max, (int)tokens[t]);
+        g->tok_range_dev = false;
         for (int t = 0; t < T; ++t)
             PARL_REQUIRE(positions[t] >= 0 && positions[t] < max_seq, PARL_E_SHAPE,
                          "position id " + std::to_string(positions[t]) + " outside [0, max_seq_len)");
@@ -1804,6 +1878,16 @@ static void do_forward_n(parl_ctx_s* c, parl_model_s* const* ms, const int* slot
         PARL_REQUIRE(same_cfg(ms[k]->cfg, ms[0]->cfg), PARL_E_CONFIG, "models of one forward must share a config");
     }
     g->vocab = ms[0]->cfg.vocab_size;
+    if (g->tok_range_dev) {  // device-packed: K1's (unsigned) id maximum, read once per packing
+        unsigned u = 0;
+        PARL_CUDA(cudaMemcpyAsync(&u, g->tok_range.p, sizeof(u), cudaMemcpyDeviceToHost, c->st));
+        PARL_CUDA(cudaStreamSynchronize(c->st));
+        g->tok_max = (int)std::min<unsigned>(u, INT32_MAX);
+        g->tok_range_dev = false;
+    }
+    // validate_forward_inputs (model.cpp:413-417): token (and self-aligned label) ids in [0, V)
+    PARL_REQUIRE(g->tok_max < g->vocab, PARL_E_VOCAB,
+                 "token id " + std::to_string(g->tok_max) + " outside vocab of size " + std::to_string(g->vocab));
     parl_act_s* act = nullptr;
     if (act_out) {
         act = *act_out ? *act_out : new parl_act_s();
@@ -1847,7 +1931,7 @@ parl_status parl_group_logprobs(parl_group_t g, int slot, double* out) {
         PARL_REQUIRE(slot >= 0 && slot < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
         std::vector<float> h(g->S);
         if (g->S)
-            PARL_CUDA(cudaMemcpyAsync(h.data(), static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T, g->S * 4,
+            PARL_CUDA(cudaMemcpyAsync(h.data(), group_lp(g, slot), g->S * 4,
                                       cudaMemcpyDeviceToHost, g->ctx->st));
         PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
         for (int s = 0; s < g->S; ++s) out[s] = h[s];
@@ -1856,9 +1940,11 @@ parl_status parl_group_logprobs(parl_group_t g, int slot, double* out) {
 
 parl_status parl_group_set_logprobs(parl_group_t g, int slot, const double* in) {
     return guarded(g->ctx, [&] {
+        PARL_REQUIRE(slot >= 0 && slot < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
+        for (int s = 0; s < g->S; ++s) PARL_REQUIRE(std::isfinite(in[s]), PARL_E_NUMERIC, "log-prob is not finite");
         std::vector<float> h(in, in + g->S);
         if (g->S)
-            PARL_CUDA(cudaMemcpyAsync(static_cast<float*>(g->lp.p) + (size_t)slot * g->max_T, h.data(), g->S * 4,
+            PARL_CUDA(cudaMemcpyAsync(group_lp(g, slot), h.data(), g->S * 4,
                                       cudaMemcpyHostToDevice, g->ctx->st));
         PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
     });
@@ -2028,30 +2114,50 @@ parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards
         const int G = g->n_samples;
         PARL_REQUIRE(hp->epsilon > 0.0 && hp->epsilon < 1.0, PARL_E_CONFIG, "epsilon must be in (0, 1)");
         PARL_REQUIRE(hp->beta >= 0.0, PARL_E_CONFIG, "beta must be >= 0");
+        PARL_REQUIRE(rewards || advantages, PARL_E_CONFIG, "grpo loss needs rewards or advantages");
         for (int k = 0; k < G; ++k)
             PARL_REQUIRE(g->cu[k + 1] > g->cu[k], PARL_E_SHAPE, "sample has empty response");
         cudaStream_t st = ctx->st;
-        double* adv = g->adv.as<double>(G);
-        if (rewards) {
+        GrpoArgs a;
+        a.lp = group_lp(g, 0);
+        a.old = group_lp(g, 1);
+        a.ref = group_lp(g, 2);
+        a.sample_of = g->pk.sample_of;
+        a.cu = group_cu(g);
+        a.S = g->S;
+        a.n = G;
+        if (rewards) {  // group_advantages[_mean_only] over the group's G rewards (grpo.cpp:24-48)
             PARL_REQUIRE(G >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
             double* r = g->rewards.as<double>(G);
             g->adv_stage.upload(r, rewards, G * sizeof(double), st);
-            launch_advantages(r, G, hp->advantage_mean_only, adv, st);
+            a.rewards = r;
+            a.group_size = G;
+            a.mean_only = hp->advantage_mean_only;
         } else {
-            for (int k = 0; k < G; ++k)
+            for (int k = 0; k < G; ++k)  // per_sample_terms: require_finite(advantage), grpo.cpp:117
                 PARL_REQUIRE(std::isfinite(advantages[k]), PARL_E_NUMERIC, "advantage is not finite");
-            g->adv_stage.upload(adv, advantages, G * sizeof(double), st);
+            double* ad = g->rewards.as<double>(G);
+            g->adv_stage.upload(ad, advantages, G * sizeof(double), st);
+            a.adv_in = ad;
         }
-        const float* lp = static_cast<float*>(g->lp.p);
-        double* stats = ctx->stats.as<double>(8);
-        ProfScope ps(ctx, PARL_KC_LOSS, 20.0 * g->S + 16.0 * G);
-        launch_grpo(lp, lp + g->max_T, lp + 2 * (size_t)g->max_T, group_cu(g), G, adv, hp->epsilon, hp->beta,
-                    hp->granularity, static_cast<float*>(g->upstream.p), ctx->per_sample.as<double>(4 * (size_t)G),
-                    stats, st);
+        a.eps = hp->epsilon;
+        a.beta = hp->beta;
+        a.gran = hp->granularity;
+        a.up_scale = -1.0;  // the pipeline backpropagates -d(L - beta KL)/d lp (pipeline.cpp:138)
+        a.up_f32 = static_cast<float*>(g->upstream.p);
+        a.adv_out = g->adv.as<double>(G);
+        a.slots = ctx->grpo_slots.as<double>(grpo_slot_count(a.S, G));
+        a.per_sample = ctx->per_sample.as<double>(4 * (size_t)G);
+        a.g_seq = ctx->g_seq.as<double>(G);
+        a.stats = ctx->stats.as<double>(8);
+        {
+            ProfScope ps(ctx, PARL_KC_LOSS, 20.0 * g->S + 16.0 * G);
+            launch_grpo(a, st);
+        }
         check_launch();
         if (out) {
             double h[5];
-            PARL_CUDA(cudaMemcpyAsync(h, stats, 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            PARL_CUDA(cudaMemcpyAsync(h, a.stats, 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
             PARL_CUDA(cudaStreamSynchronize(st));
             out->objective_sum = h[0];
             out->clip_sum = h[1];
@@ -2059,6 +2165,174 @@ parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards
             out->clipped_units = h[3];
             out->total_units = h[4];
         }
+    });
+}
+
+// ---- GRPO operator API (grpo.hpp:50-83) over host arrays: the same K7 kernels in fp64 ------
+namespace {
+// m samples of lengths lens[] (log-prob vectors concatenated) through K7; upstream (scaled by
+// up_scale), per-sample terms and the summed stats back on the host
+void grpo_host(parl_ctx_s* c, int m, const int32_t* lens, const double* lp, const double* old, const double* ref,
+               const double* rewards, const double* adv, int group_size, int mean_only, double eps, double beta,
+               int gran, double up_scale, double* upstream, double* per_sample, double* stats, double* adv_out) {
+    PARL_REQUIRE(m >= 1, PARL_E_SHAPE, "empty micro-batch");
+    std::vector<int32_t> cu(m + 1, 0);
+    for (int j = 0; j < m; ++j) {
+        PARL_REQUIRE(lens[j] >= 1, PARL_E_SHAPE, "sample has empty response");
+        cu[j + 1] = cu[j] + lens[j];
+    }
+    const long S = cu[m];
+    std::vector<int32_t> so(S);
+    for (int j = 0; j < m; ++j)
+        for (int t = cu[j]; t < cu[j + 1]; ++t) so[t] = j;
+    cudaStream_t st = c->st;
+    // one scratch block: lp | old | ref | upstream (S each) | adv_in / rewards (m) | adv_out (m) |
+    // per_sample (4m) | g_seq (m) | stats (8) | slots, then ints: cu (m+1) | sample_of (S)
+    const size_t nslot = grpo_slot_count(S, m);
+    const size_t nd = 4 * (size_t)S + 8 * (size_t)m + 8 + nslot;
+    double* d = c->staging.as<double>(nd + ((size_t)(m + 1 + S) + 1) / 2 + 1);
+    double *d_lp = d, *d_old = d + S, *d_ref = d + 2 * S, *d_up = d + 3 * S, *d_in = d + 4 * S;
+    double *d_adv = d_in + m, *d_ps = d_adv + m, *d_gs = d_ps + 4 * (size_t)m, *d_st = d_gs + m, *d_sl = d_st + 8;
+    int32_t* d_cu = reinterpret_cast<int32_t*>(d_sl + nslot);
+    int32_t* d_so = d_cu + m + 1;
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) PARL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    up(d_lp, lp, S * 8);
+    up(d_old, old, S * 8);
+    up(d_ref, ref, S * 8);
+    up(d_in, rewards ? rewards : adv, (size_t)m * 8);
+    up(d_cu, cu.data(), (size_t)(m + 1) * 4);
+    up(d_so, so.data(), (size_t)S * 4);
+    PARL_CUDA(cudaMemsetAsync(d_st, 0, 8 * sizeof(double), st));
+    GrpoArgs a;
+    a.lp = d_lp; a.old = d_old; a.ref = d_ref; a.lp_f64 = 1;
+    a.sample_of = d_so; a.cu = d_cu; a.S = S; a.n = m;
+    if (rewards) {
+        a.rewards = d_in;
+        a.group_size = group_size;
+        a.mean_only = mean_only;
+    } else {
+        a.adv_in = d_in;
+    }
+    a.eps = eps; a.beta = beta; a.gran = gran; a.up_scale = up_scale;
+    a.up_f64 = d_up; a.adv_out = d_adv; a.slots = d_sl; a.per_sample = d_ps; a.g_seq = d_gs; a.stats = d_st;
+    launch_grpo(a, st);
+    check_launch();
+    auto dn = [&](void* dst, const void* src, size_t bytes) {
+        if (dst && bytes) PARL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    };
+    dn(upstream, d_up, S * 8);
+    dn(per_sample, d_ps, (size_t)m * 32);
+    dn(stats, d_st, 5 * 8);
+    dn(adv_out, d_adv, (size_t)m * 8);
+    PARL_CUDA(cudaStreamSynchronize(st));
+}
+
+void require_finite(double v, const char* what) {  // grpo.cpp:56-58
+    PARL_REQUIRE(std::isfinite(v), PARL_E_NUMERIC, std::string(what) + " is not finite");
+}
+}  // namespace
+
+parl_status parl_group_advantages(parl_ctx_t ctx, const double* rewards, int G, int mean_only, double* adv) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(G >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
+        // the G rewards as one group of G one-token samples with zero log-probs
+        std::vector<int32_t> lens(G, 1);
+        std::vector<double> z(G, 0.0);
+        grpo_host(ctx, G, lens.data(), z.data(), z.data(), z.data(), rewards, nullptr, G, mean_only, 0.2, 0.0, 0,
+                  1.0, nullptr, nullptr, nullptr, adv);
+    });
+}
+
+parl_status parl_clipped_term(parl_ctx_t ctx, double lp_new, double lp_old, double adv, double eps, double* out) {
+    return guarded(ctx, [&] {
+        require_finite(lp_new, "logp_new");
+        require_finite(lp_old, "logp_old");
+        require_finite(adv, "advantage");
+        PARL_REQUIRE(eps > 0.0 && eps < 1.0, PARL_E_CONFIG, "epsilon must be in (0, 1)");
+        const int32_t one = 1;
+        double ps[4];
+        grpo_host(ctx, 1, &one, &lp_new, &lp_old, &lp_new, nullptr, &adv, 0, 0, eps, 0.0, 0, 1.0, nullptr, ps,
+                  nullptr, nullptr);
+        *out = ps[0];
+    });
+}
+
+parl_status parl_kl_term(parl_ctx_t ctx, double lp_new, double lp_ref, double* out) {
+    return guarded(ctx, [&] {
+        require_finite(lp_new, "logp_new");
+        require_finite(lp_ref, "logp_ref");
+        const int32_t one = 1;
+        const double zero = 0.0;
+        double ps[4];
+        grpo_host(ctx, 1, &one, &lp_new, &lp_new, &lp_ref, nullptr, &zero, 0, 0, 0.2, 0.0, 0, 1.0, nullptr, ps,
+                  nullptr, nullptr);
+        *out = ps[1];
+    });
+}
+
+parl_status parl_per_sample_terms(parl_ctx_t ctx, const double* lp, const double* old, const double* ref, int n,
+                                  double adv, double eps, double beta, int granularity, double* upstream,
+                                  parl_sample_terms* out) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(n >= 1, PARL_E_SHAPE, "sample has empty response");
+        require_finite(adv, "advantage");
+        double ps[4];
+        const int32_t len = n;
+        grpo_host(ctx, 1, &len, lp, old, ref, nullptr, &adv, 0, 0, eps, beta, granularity, 1.0, upstream, ps,
+                  nullptr, nullptr);
+        out->clip_term = ps[0];
+        out->kl = ps[1];
+        out->clipped_units = (int)ps[2];
+        out->total_units = (int)ps[3];
+    });
+}
+
+parl_status parl_grpo_microbatch_loss(parl_ctx_t ctx, int m, const int32_t* lens, const double* lp,
+                                      const double* old, const double* ref, const double* advantages, double eps,
+                                      double beta, int granularity, double* upstream, parl_loss_report* report,
+                                      double* loss) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(m >= 1, PARL_E_SHAPE, "empty micro-batch");
+        for (int j = 0; j < m; ++j) require_finite(advantages[j], "advantage");
+        const double inv_m = 1.0 / m;
+        double st[5];
+        grpo_host(ctx, m, lens, lp, old, ref, nullptr, advantages, 0, 0, eps, beta, granularity, -inv_m, upstream,
+                  nullptr, st, nullptr);
+        long tokens = 0;
+        for (int j = 0; j < m; ++j) tokens += lens[j];
+        if (loss) *loss = -inv_m * st[0];  // grpo.cpp:177-182
+        if (report) {
+            report->objective = inv_m * st[0];
+            report->clip_term_mean = inv_m * st[1];
+            report->kl_mean = inv_m * st[2];
+            report->clip_fraction = st[4] > 0 ? st[3] / st[4] : 0.0;
+            report->token_count = tokens;
+        }
+    });
+}
+
+// build_shared_prompt_mask (packing.cpp:47-72): the dense allowed-pair matrix, evaluated on the
+// device by the rule the attention kernels apply tile by tile (model.cpp:242-245)
+parl_status parl_shared_prompt_mask(parl_ctx_t ctx, int P, const int32_t* lens, int G, uint8_t* mask) {
+    return guarded(ctx, [&] {
+        PARL_REQUIRE(P >= 1, PARL_E_SHAPE, "prompt_len must be >= 1");  // packing.cpp:48-50
+        long n = P;
+        for (int k = 0; k < G; ++k) {
+            PARL_REQUIRE(lens[k] >= 1, PARL_E_SHAPE, "response lengths must be >= 1");
+            n += lens[k];
+        }
+        std::vector<int32_t> seg(n, 0);
+        long t = P;
+        for (int k = 0; k < G; ++k)
+            for (int i = 0; i < lens[k]; ++i) seg[t++] = k + 1;
+        int32_t* d_seg = static_cast<int32_t*>(ctx->staging.get((size_t)n * 4 + (size_t)n * n + 16));
+        uint8_t* d_mask = reinterpret_cast<uint8_t*>(d_seg + n);
+        PARL_CUDA(cudaMemcpyAsync(d_seg, seg.data(), (size_t)n * 4, cudaMemcpyHostToDevice, ctx->st));
+        launch_allowed_mask(d_seg, (int)n, d_mask, ctx->st);
+        PARL_CUDA(cudaMemcpyAsync(mask, d_mask, (size_t)n * n, cudaMemcpyDeviceToHost, ctx->st));
+        PARL_CUDA(cudaStreamSynchronize(ctx->st));
     });
 }
 
@@ -2100,12 +2374,17 @@ parl_status parl_stats_reset(parl_ctx_t ctx) {
 
 // ---- backward -----------------------------------------------------------------
 parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out) {
+    return parl_grad_create_config(ctx, &like->cfg, out);
+}
+
+parl_status parl_grad_create_config(parl_ctx_t ctx, const parl_config* cfg, parl_grad_t* out) {
     return guarded(ctx, [&] {
+        validate_config(*cfg);
         auto gr = std::make_unique<parl_grad_s>();
         gr->ctx = ctx;
         ctx->refs++;
-        gr->cfg = like->cfg;
-        gr->L = like->L;
+        gr->cfg = *cfg;
+        gr->L = make_layout(*cfg);
         float* p = gr->g.as<float>(gr->L.total);
         PARL_CUDA(cudaMemsetAsync(p, 0, gr->L.total * sizeof(float), ctx->st));
         PARL_CUDA(cudaMemsetAsync(gr->touched.as<uint8_t>(gr->cfg.vocab_size), 0, gr->cfg.vocab_size, ctx->st));
@@ -2117,8 +2396,11 @@ parl_status parl_grad_create(parl_ctx_t ctx, parl_model_t like, parl_grad_t* out
 parl_status parl_grad_destroy(parl_grad_t gr) {
     if (gr) {
         parl_ctx_s* c = gr->ctx;
-        cudaStreamSynchronize(c->st);
-        delete gr;
+        {
+            std::lock_guard<std::recursive_mutex> lk(c->mu);
+            cudaStreamSynchronize(c->st);
+            delete gr;
+        }
         ctx_release(c);
     }
     return PARL_OK;
@@ -2129,13 +2411,57 @@ parl_status parl_grad_reset(parl_grad_t gr) {
         PARL_CUDA(cudaMemsetAsync(gr->g.p, 0, gr->L.total * sizeof(float), gr->ctx->st));
         PARL_CUDA(cudaMemsetAsync(gr->touched.p, 0, gr->cfg.vocab_size, gr->ctx->st));
         gr->micro_steps = 0;
+        gr->count_on_device = false;
     });
 }
 
-int parl_grad_micro_steps(parl_grad_t gr) { return gr->micro_steps; }
+int parl_grad_micro_steps(parl_grad_t gr) {
+    if (gr->count_on_device) {  // the data-parallel sum over ranks (parl_grad_allreduce)
+        std::lock_guard<std::recursive_mutex> lk(gr->ctx->mu);
+        double c = 0;
+        if (cudaMemcpyAsync(&c, gr->count_dev.p, sizeof(c), cudaMemcpyDeviceToHost, gr->ctx->st) == cudaSuccess &&
+            cudaStreamSynchronize(gr->ctx->st) == cudaSuccess) {
+            gr->micro_steps = (int)c;
+            gr->count_on_device = false;
+        }
+    }
+    return gr->micro_steps;
+}
+
+// GradBuffer::set_micro_step_count / add_micro_steps (model.hpp:126-127): the pipeline sets the
+// update divisor to the batch's N*G samples before apply_update (pipeline.cpp:346-351)
+parl_status parl_grad_set_micro_steps(parl_grad_t gr, int n) {
+    return guarded(gr->ctx, [&] {
+        gr->micro_steps = n;
+        gr->count_on_device = false;
+    });
+}
+
+parl_status parl_grad_add_micro_steps(parl_grad_t gr, int n) {
+    return guarded(gr->ctx, [&] {
+        parl_grad_micro_steps(gr);
+        gr->micro_steps += n;
+    });
+}
+
+// GradBuffer::all_finite / ModelParams::all_finite
+parl_status parl_grad_all_finite(parl_grad_t gr, int* out) {
+    return guarded(gr->ctx, [&] {
+        cudaStream_t st = gr->ctx->st;
+        int* flags = gr->ctx->flags.as<int>(1);
+        PARL_CUDA(cudaMemsetAsync(flags, 0, 4, st));
+        launch_finite_check_f32(static_cast<const float*>(gr->g.p), (long)gr->L.total, flags, st);
+        int h = 0;
+        PARL_CUDA(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, st));
+        PARL_CUDA(cudaStreamSynchronize(st));
+        *out = h == 0;
+    });
+}
 
 parl_status parl_grad_accumulate(parl_grad_t dst, parl_grad_t src) {
     return guarded(dst->ctx, [&] {
+        parl_grad_micro_steps(dst);
+        parl_grad_micro_steps(src);
         PARL_REQUIRE(same_cfg(dst->cfg, src->cfg), PARL_E_SHAPE, "gradient buffers have incongruent layouts");
         launch_axpy(static_cast<const float*>(src->g.p), static_cast<float*>(dst->g.p), (long)dst->L.total,
                     dst->ctx->st);
@@ -2157,6 +2483,23 @@ parl_status parl_backward(parl_ctx_t ctx, parl_model_t pol, parl_act_t act, parl
         PARL_REQUIRE(same_cfg(gr->cfg, pol->cfg), PARL_E_SHAPE, "gradient buffers have incongruent layouts");
         if (ctx->prec == PARL_PREC_BF16) backward_impl<bf16>(ctx, pol, act, g, gr);
         else backward_impl<float>(ctx, pol, act, g, gr);
+    });
+}
+
+parl_status parl_grad_upload(parl_grad_t gr, const double* flat, size_t n) {
+    return guarded(gr->ctx, [&] {
+        PARL_REQUIRE(n == gr->L.total, PARL_E_SHAPE, "gradient array size does not match the layout");
+        cudaStream_t st = gr->ctx->st;
+        const size_t chunk = (size_t)64 << 20;
+        for (size_t o = 0; o < n; o += chunk) {
+            const size_t cnt = std::min(chunk, n - o);
+            double* stg = gr->ctx->staging.as<double>(cnt);
+            PARL_CUDA(cudaMemcpyAsync(stg, flat + o, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+            launch_f64_to_f32(stg, static_cast<float*>(gr->g.p) + o, (long)cnt, st);
+            PARL_CUDA(cudaStreamSynchronize(st));
+        }
+        // rows of the token embedding that may now be non-zero (sparse data-parallel exchange)
+        PARL_CUDA(cudaMemsetAsync(gr->touched.p, 1, gr->cfg.vocab_size, st));
     });
 }
 
@@ -2192,6 +2535,7 @@ parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr) {
     // ModelParams::apply_update, model.cpp:202-219
     return guarded(m->ctx, [&] {
         PARL_REQUIRE(same_cfg(gr->cfg, m->cfg), PARL_E_SHAPE, "gradient layout not congruent with parameters");
+        parl_grad_micro_steps(gr);
         PARL_REQUIRE(gr->micro_steps > 0, PARL_E_CONFIG, "apply_update requires micro_step_count > 0");
         PARL_REQUIRE(lr >= 0.0 && std::isfinite(lr), PARL_E_CONFIG, "learning rate must be finite and >= 0");
         PARL_REQUIRE(m->has_master, PARL_E_CONFIG, "apply_update needs the fp64 master copy");
@@ -2209,6 +2553,7 @@ parl_status parl_apply_update(parl_model_t m, parl_grad_t gr, double lr) {
         convert_from_master(m);
         PARL_CUDA(cudaStreamSynchronize(st));
         ++m->version;
+        ++m->epoch;
     });
 }
 
@@ -2310,6 +2655,12 @@ parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
             comm_allreduce(ctx, G + dense0, gr->L.total - dense0, 7);
         }
         gr->streamed = false;
+        // counts add across ranks like GradBuffer::accumulate (read back lazily by apply_update)
+        double* cnt_d = gr->count_dev.as<double>(1);
+        const double cnt_h = (double)gr->micro_steps;
+        PARL_CUDA(cudaMemcpyAsync(cnt_d, &cnt_h, sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+        comm_allreduce(ctx, cnt_d, 1, 8);
+        gr->count_on_device = true;
         // the compute stream continues once every slice is reduced
         PARL_CUDA(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
         PARL_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_comm_done, 0));

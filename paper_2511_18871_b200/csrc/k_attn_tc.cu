@@ -1,20 +1,17 @@
 // tcgen05 varlen shared-prompt attention (bf16 in, fp32 accumulate).
 //
-// Forward: one CTA per (128-row query tile, head).  Replaces the attention
-// loops of run_forward (proj/src/model.cpp:468-501) under the shared-prompt
-// rule of model.cpp:242-245:
-//   warp 0      TMA: Q once, then K/V tiles into a 2-stage ring
-//   warp 1      MMA: S_j = Q K_j^T into a double-buffered TMEM S, then
-//               O += P_j V_j (P from smem, V as an MN-major operand)
-//   warps 2..5  softmax, thread = query row: S row from TMEM, online max in
-//               the log2 domain, P = exp2(S - m) to smem (SW128 K-major,
-//               the A operand of the PV MMA); O is rescaled in TMEM only when
-//               a row's max grows by more than 2^8 (exact: every P and O term
-//               uses the same stale max, normalised at the end)
-// Key tiles are visited only when some row of the query tile can see them;
-// response-to-response tiles of different responses are skipped, and only
-// tiles straddling a boundary apply the per-element mask.  The forward saves
-// only the row log-sum-exp.
+// Forward (k_attn_fwd_pair): persistent CTAs, work item = (pair of adjacent 128-row
+// query tiles, head) taken from a global queue; replaces the attention loops of
+// run_forward (proj/src/model.cpp:468-501) under the shared-prompt rule of
+// model.cpp:242-245.  TMA-staged Q/K/V, S = QK^T and O += PV on tcgen05 with TMEM
+// accumulators (P written back to TMEM as the A operand of the PV MMA), online
+// softmax in the log2 domain with a conditional O rescale.  Key tiles are visited
+// only when some row of a query tile can see them: response-to-response tiles of
+// different responses are skipped, and only tiles straddling a boundary apply the
+// per-element mask.  The forward saves only the row log-sum-exp.
+//
+// Backward (k_attn_prep_v8 + k_attn_bwd2<DKV> + k_attn_bwd2<DQ>): D = rowsum(dO*O),
+// then dK/dV per key tile and dQ per query tile, deterministic (no atomics).
 #include <cudaTypedefs.h>
 
 #include <cuda_fp16.h>
@@ -27,285 +24,7 @@ namespace parl_gpu {
 
 namespace {
 
-constexpr int TQ = 128, TK = 128;
-constexpr int NTHR = 192;  // 6 warps
 constexpr float LOG2E = 1.4426950408889634f;
-
-struct AttnTcArgs {
-    int T, H, Dh, d, Peff;
-    const int32_t* seg;
-    const int32_t *seg_start, *seg_end;      // [G+1]: segment k spans [seg_start[k], seg_end[k])
-    const int32_t *q_ptr, *q_list, *q_order;  // tile schedule (see build_attn_schedule)
-    float scale_log2;  // scale * log2(e)
-    bf16* out;         // [T x ldo]
-    long ldo;
-    float* lse;        // [H x T] natural log
-};
-
-template <int DH>
-struct AttnSmem {
-    static constexpr int Q_BYTES = TQ * DH * 2;
-    static constexpr int KV_BYTES = TK * DH * 2;
-    static constexpr int P_BYTES = TQ * TK * 2;
-    static constexpr int OFF_Q = 0;                            // 2 buffers (double-buffered across items)
-    static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;          // 2 stages
-    static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;         // 2 stages
-    static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
-    static constexpr int OFF_SEG = OFF_P + P_BYTES;            // 128 ints (key segments)
-    static constexpr int OFF_BAR = OFF_SEG + TK * 4;
-    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
-};
-
-// Persistent forward: CTA b processes work items b, b+grid, ... of the
-// heavy-first list item -> (q_order[item / H], item % H).  All tiles of all of
-// the CTA's items form one continuous stream (global tile counter n), so the
-// next item's Q load and first QK^T overlap the current item's epilogue.
-template <int DH>
-__global__ void __launch_bounds__(NTHR, 1)
-    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, AttnTcArgs a, int n_items) {
-    using L = AttnSmem<DH>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-    uint64_t* q_full = bar + 0;    // [2]
-    uint64_t* q_empty = bar + 2;   // [2]
-    uint64_t* kv_full = bar + 4;   // [2]
-    uint64_t* kv_empty = bar + 6;  // [2]
-    uint64_t* s_full = bar + 8;    // [2]
-    uint64_t* p_full = bar + 10;
-    uint64_t* o_done = bar + 11;
-    uint64_t* o_free = bar + 12;   // [2]
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 14);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto item_qt = [&](int it) { return a.q_order[it / a.H]; };
-    auto item_h = [&](int it) { return it % a.H; };
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&q_full[s], 1);
-            tc::mbar_init(&q_empty[s], 1);
-            tc::mbar_init(&kv_full[s], 1);
-            tc::mbar_init(&kv_empty[s], 1);
-            tc::mbar_init(&s_full[s], 1);
-            tc::mbar_init(&o_free[s], 128);
-        }
-        tc::mbar_init(p_full, 128);
-        tc::mbar_init(o_done, 1);
-        tc::fence_barrier_init();
-        tc::tma_prefetch(&tm_qkv);
-    }
-    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tbase = *tbase_s;
-    const uint32_t t_s0 = tbase, t_o0 = tbase + 256;  // S buffers at cols 0/128, O buffers at 256 / 256+DH
-
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA
-            int n = 0, li = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-                const int qt = item_qt(it), h = item_h(it), qb = li & 1;
-                tc::mbar_wait(&q_empty[qb], ((li >> 1) & 1) ^ 1);
-                tc::mbar_expect_tx(&q_full[qb], L::Q_BYTES);
-#pragma unroll
-                for (int r = 0; r < DH / 64; ++r)
-                    tc::tma_load_2d(smem + L::OFF_Q + qb * L::Q_BYTES + r * TQ * 128, &tm_qkv, &q_full[qb],
-                                    h * DH + r * 64, qt * TQ);
-                for (int e = a.q_ptr[qt]; e < a.q_ptr[qt + 1]; ++e, ++n) {
-                    const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
-                    const int st = n & 1;
-                    tc::mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
-                    tc::mbar_expect_tx(&kv_full[st], 2 * L::KV_BYTES);
-                    uint8_t* kb = smem + L::OFF_K + st * L::KV_BYTES;
-                    uint8_t* vb = smem + L::OFF_V + st * L::KV_BYTES;
-#pragma unroll
-                    for (int r = 0; r < DH / 64; ++r) {
-                        tc::tma_load_2d(kb + r * TK * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, j0);
-                        tc::tma_load_2d(vb + r * TK * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, j0);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA
-            constexpr uint32_t id_s = tc::idesc_bf16(TQ, TK, 0, 0);
-            constexpr uint32_t id_o = tc::idesc_bf16(TQ, DH, 0, 1);
-            const uint32_t sp = tc::smem_u32(smem + L::OFF_P);
-            // S-iterator (runs one tile ahead of the PV iterator)
-            int s_it = blockIdx.x, s_li = 0, s_e = 0, s_end = 0, s_n = 0;
-            auto s_begin_item = [&]() {
-                if (s_it < n_items) {
-                    const int qt = item_qt(s_it);
-                    s_e = a.q_ptr[qt];
-                    s_end = a.q_ptr[qt + 1];
-                }
-            };
-            s_begin_item();
-            auto issue_s = [&]() -> bool {  // returns false when the stream is exhausted
-                while (s_it < n_items && s_e >= s_end) {
-                    s_it += gridDim.x;
-                    ++s_li;
-                    s_begin_item();
-                }
-                if (s_it >= n_items) return false;
-                const int qb = s_li & 1;
-                if (s_e == a.q_ptr[item_qt(s_it)]) tc::mbar_wait(&q_full[qb], (s_li >> 1) & 1);
-                const int st = s_n & 1;
-                tc::mbar_wait(&kv_full[st], (s_n >> 1) & 1);
-                tc::tc_fence_after();
-                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + qb * L::Q_BYTES);
-                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::KV_BYTES);
-#pragma unroll
-                for (int ks = 0; ks < DH / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_s0 + st * TK, tc::sdesc(sq + off, 16, 1024),
-                                 tc::sdesc(sk + (ks >> 2) * (TK * 128) + (ks & 3) * 32, 16, 1024), id_s, ks > 0);
-                }
-                tc::mma_commit(&s_full[st]);
-                ++s_e;
-                ++s_n;
-                return true;
-            };
-            bool more = issue_s();
-            int n = 0, li = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-                const int qt = item_qt(it), qb = li & 1, ob = li & 1;
-                const int nt = a.q_ptr[qt + 1] - a.q_ptr[qt];
-                for (int t = 0; t < nt; ++t, ++n) {
-                    if (more) more = issue_s();  // S of the next tile (possibly the next item)
-                    tc::mbar_wait(p_full, n & 1);
-                    if (t == 0) tc::mbar_wait(&o_free[ob], ((li >> 1) & 1) ^ 1);
-                    tc::tc_fence_after();
-                    const int st = n & 1;
-                    const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::KV_BYTES);
-#pragma unroll
-                    for (int ks = 0; ks < TK / 16; ++ks) {
-                        const uint32_t pa = sp + (ks >> 2) * (TQ * 128) + (ks & 3) * 32;
-                        tc::mma_bf16(t_o0 + ob * DH, tc::sdesc(pa, 16, 1024),
-                                     tc::sdesc(sv + ks * 2048, TK * 128, 1024), id_o, (t > 0 || ks > 0) ? 1u : 0u);
-                    }
-                    tc::mma_commit(o_done);
-                    tc::mma_commit(&kv_empty[st]);
-                    if (t == nt - 1) tc::mma_commit(&q_empty[qb]);
-                }
-            }
-        }
-    } else {
-        // ---------------- softmax: warps 2..5 -> TMEM lane quarter (warp % 4)
-        const int q4 = warp & 3;
-        const int r = q4 * 32 + lane;  // tile row
-        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        uint8_t* P = smem + L::OFF_P;
-        int n = 0, li = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-            const int qt = item_qt(it), h = item_h(it), ob = li & 1;
-            const int i0 = qt * TQ, i = i0 + r;
-            const bool row_ok = i < a.T;
-            const int seg_i = row_ok ? a.seg[i] : -1;
-            // allowed keys of row i: [0, e0) and [b1, i] (model.cpp:242-245)
-            const int e0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
-            const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, e1 = seg_i > 0 ? i + 1 : 0;
-            float m_used = -INFINITY, l = 0.f;
-            const int ea = a.q_ptr[qt], eb = a.q_ptr[qt + 1];
-            for (int e = ea; e < eb; ++e, ++n) {
-                const int j0 = (a.q_list[e] & 0x3fffffff) * TK;
-                // the row's allowed keys in this tile as local ranges [0, h0) u [l1, h1)
-                const int h0 = min(max(e0 - j0, 0), TK);
-                const int l1 = min(max(b1 - j0, 0), TK), h1 = min(max(e1 - j0, 0), TK);
-                tc::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
-                tc::tc_fence_after();
-                float s[TK];
-                tc::tmem_ld128(t_s0 + (n & 1) * TK + lane_off, s);
-                float mx = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < TK; ++j) {
-                    const bool ok = (j < h0) | ((j >= l1) & (j < h1));
-                    const float v = ok ? s[j] * a.scale_log2 : -INFINITY;
-                    s[j] = v;
-                    mx = fmaxf(mx, v);
-                }
-                // conditional rescale (threshold 8 in log2 units)
-                const bool need = mx > m_used + 8.f;
-                const float m_new = need ? mx : m_used;
-                const float alpha = need ? exp2f(m_used - m_new) : 1.f;  // m_used = -inf -> 0
-                const float mb = m_new == -INFINITY ? 0.f : m_new;
-                float sum = 0.f;
-                uint32_t pk[TK / 2];
-#pragma unroll
-                for (int j = 0; j < TK; j += 2) {
-                    const float p0 = exp2f(s[j] - mb), p1 = exp2f(s[j + 1] - mb);
-                    sum += p0 + p1;
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                    pk[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                // the previous PV (this item's or the previous item's) must be done:
-                // P smem is reused and O is rescaled
-                if (n > 0) {
-                    tc::mbar_wait(o_done, (n - 1) & 1);
-                    tc::tc_fence_after();
-                }
-                if (e > ea && __any_sync(0xffffffffu, need)) {
-#pragma unroll
-                    for (int c = 0; c < DH / 32; ++c) {
-                        float o[32];
-                        tc::tmem_ld32(t_o0 + ob * DH + c * 32 + lane_off, o);
-                        uint32_t w[32];
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) w[q] = __float_as_uint(o[q] * alpha);
-                        tc::tmem_st16(t_o0 + ob * DH + c * 32 + lane_off, w);
-                        tc::tmem_st16(t_o0 + ob * DH + c * 32 + 16 + lane_off, w + 16);
-                    }
-                    tc::tmem_st_wait();
-                }
-                l = l * alpha + sum;
-                m_used = m_new;
-                // P row r -> SW128 K-major tile: 64-key atom columns of [128 rows x 128 B]
-                const uint32_t pbase = tc::smem_u32(P) + r * 128;
-#pragma unroll
-                for (int c = 0; c < TK / 8; ++c) {
-                    const int atom = c >> 3, chunk = c & 7;
-                    tc::sts128(pbase + atom * (TQ * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1],
-                               pk[4 * c + 2], pk[4 * c + 3]);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tc::tc_fence_before();
-                tc::mbar_arrive(p_full);
-            }
-            // item epilogue: O / l -> out (bf16), lse; then release the O buffer
-            tc::mbar_wait(o_done, (n - 1) & 1);
-            tc::tc_fence_after();
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-            for (int c = 0; c < DH / 32; ++c) {
-                float o[32];
-                tc::tmem_ld32(t_o0 + ob * DH + c * 32 + lane_off, o);
-                if (row_ok) {
-                    bf16* dst = a.out + (long)i * a.ldo + h * DH + c * 32;
-#pragma unroll
-                    for (int q = 0; q < 32; q += 8) {
-                        __align__(16) bf16 t[8];
-#pragma unroll
-                        for (int e2 = 0; e2 < 8; ++e2) t[e2] = __float2bfloat16_rn(o[q + e2] * inv);
-                        *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
-                    }
-                }
-            }
-            if (row_ok) a.lse[(long)h * a.T + i] = (m_used + log2f(l)) * 0.69314718055994531f;
-            tc::tc_fence_before();
-            tc::mbar_arrive(&o_free[ob]);
-        }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc::tc_fence_after();
-        tc::tmem_dealloc<512>(tbase);
-    }
-}
-
-
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
@@ -1573,463 +1292,6 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     }
 }
 
-// ===========================================================================
-// Backward (model.cpp:751-786 recomputed flash-style; deterministic, no atomics)
-//   k_attn_dkv_tc : CTA per (key tile, head), loops over the query tiles that
-//                   see it:  S^T = K Q^T, dP^T = V dO^T (TMEM), thread = key row:
-//                   P^T = exp2(S^T*c - lse), dS^T = P^T (dP^T - D) -> smem,
-//                   dV += P^T dO, dK += dS^T Q (TMEM accumulators)
-//   k_attn_dq_tc  : CTA per (query tile, head), loops over visible key tiles:
-//                   S = Q K^T, dP = dO V^T, dS -> smem, dQ += dS K
-struct AttnBwdArgs {
-    int T, H, Dh, d, Peff, n_qt;
-    const int32_t* seg;
-    const int32_t *seg_start, *seg_end;
-    const int32_t *q_ptr, *q_list, *q_order;  // per query tile: visible key tiles
-    const int32_t *k_ptr, *k_list, *k_order;  // per key tile: query tiles that see it
-    float scale, scale_log2;
-    const float* lse;   // [H x T] natural log
-    const float* dsum;  // [H x T]
-    bf16* dqkv;         // [T x 3d]
-};
-
-__device__ __forceinline__ void write_rowtile_sw128(uint8_t* base, int r, const uint32_t* pk /*64 words*/) {
-    // one 128-element bf16 row r of a [128 x 128] K-major SW128 tile (two 64-wide atom columns)
-    const uint32_t b = tc::smem_u32(base) + r * 128;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-        const int atom = c >> 3, chunk = c & 7;
-        tc::sts128(b + atom * (128 * 128) + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                   pk[4 * c + 3]);
-    }
-}
-
-// 32 bf16 columns [c0, c0+32) of row r (16 packed words) into a K-major SW128 tile
-__device__ __forceinline__ void write_row32_sw128(uint8_t* base, int r, int c0, const uint32_t* pk) {
-    const int atom = c0 >> 6, chunk0 = (c0 & 63) >> 3;
-    const uint32_t b = tc::smem_u32(base) + atom * (128 * 128) + r * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        tc::sts128(b + (((chunk0 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-}
-
-template <int DH>
-struct DkvSmem {
-    static constexpr int ST = DH == 128 ? 1 : 2;
-    static constexpr int TILE = 128 * DH * 2;
-    static constexpr int OFF_K = 0, OFF_V = TILE;
-    static constexpr int OFF_Q = 2 * TILE;                 // [ST]
-    static constexpr int OFF_DO = OFF_Q + ST * TILE;       // [ST]
-    static constexpr int OFF_P = OFF_DO + ST * TILE;       // P^T  [128 x 128] bf16
-    static constexpr int OFF_DS = OFF_P + 128 * 128 * 2;   // dS^T
-    static constexpr int OFF_VEC = OFF_DS + 128 * 128 * 2; // lse*log2e, D, seg of the query tile
-    static constexpr int OFF_BAR = OFF_VEC + 3 * 128 * 4;
-    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(NTHR, 1)
-    k_attn_dkv_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                  AttnBwdArgs a) {
-    using L = DkvSmem<DH>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-    uint64_t* kv_full = bar + 0;
-    uint64_t* q_full = bar + 1;   // [2]
-    uint64_t* q_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* p_full = bar + 6;
-    uint64_t* g_done = bar + 7;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 8);
-    float* v_lse = reinterpret_cast<float*>(smem + L::OFF_VEC);
-    float* v_d = v_lse + 128;
-
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kt = a.k_order[blockIdx.x], h = blockIdx.y;
-    const int j0 = kt * 128, j1 = min(a.T, j0 + 128);
-    const int e0 = a.k_ptr[kt], e1 = a.k_ptr[kt + 1];
-
-    if (threadIdx.x == 0) {
-        tc::mbar_init(kv_full, 1);
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&q_full[s], 1);
-            tc::mbar_init(&q_empty[s], 1);
-        }
-        tc::mbar_init(s_full, 1);
-        tc::mbar_init(p_full, 128);
-        tc::mbar_init(g_done, 1);
-        tc::fence_barrier_init();
-        tc::tma_prefetch(&tm_qkv);
-        tc::tma_prefetch(&tm_do);
-    }
-    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tbase = *tbase_s;
-    const uint32_t t_s = tbase, t_dp = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + DH;
-
-    if (warp == 0) {
-        if (lane == 0) {  // TMA
-            tc::mbar_expect_tx(kv_full, 2 * L::TILE);
-#pragma unroll
-            for (int r = 0; r < DH / 64; ++r) {
-                tc::tma_load_2d(smem + L::OFF_K + r * 128 * 128, &tm_qkv, kv_full, a.d + h * DH + r * 64, j0);
-                tc::tma_load_2d(smem + L::OFF_V + r * 128 * 128, &tm_qkv, kv_full, 2 * a.d + h * DH + r * 64, j0);
-            }
-            int n = 0;
-            for (int e = e0; e < e1; ++e) {
-                const int qt = a.k_list[e] & 0x3fffffff;
-                const int st = n % L::ST;
-                tc::mbar_wait(&q_empty[st], ((n / L::ST) & 1) ^ 1);
-                tc::mbar_expect_tx(&q_full[st], 2 * L::TILE);
-                uint8_t* qb = smem + L::OFF_Q + st * L::TILE;
-                uint8_t* db = smem + L::OFF_DO + st * L::TILE;
-#pragma unroll
-                for (int r = 0; r < DH / 64; ++r) {
-                    tc::tma_load_2d(qb + r * 128 * 128, &tm_qkv, &q_full[st], h * DH + r * 64, qt * 128);
-                    tc::tma_load_2d(db + r * 128 * 128, &tm_do, &q_full[st], h * DH + r * 64, qt * 128);
-                }
-                ++n;
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // MMA
-            constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);   // K Q^T, V dO^T
-            constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);    // P^T dO, dS^T Q
-            const uint32_t sk = tc::smem_u32(smem + L::OFF_K), sv = tc::smem_u32(smem + L::OFF_V);
-            const uint32_t sp = tc::smem_u32(smem + L::OFF_P), sds = tc::smem_u32(smem + L::OFF_DS);
-            tc::mbar_wait(kv_full, 0);
-            auto issue_sdp = [&](int n) {
-                const int st = n % L::ST;
-                tc::mbar_wait(&q_full[st], (n / L::ST) & 1);
-                tc::tc_fence_after();
-                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + st * L::TILE);
-                const uint32_t sd = tc::smem_u32(smem + L::OFF_DO + st * L::TILE);
-#pragma unroll
-                for (int ks = 0; ks < DH / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_s, tc::sdesc(sk + off, 16, 1024), tc::sdesc(sq + off, 16, 1024), id_s, ks > 0);
-                    tc::mma_bf16(t_dp, tc::sdesc(sv + off, 16, 1024), tc::sdesc(sd + off, 16, 1024), id_s, ks > 0);
-                }
-                tc::mma_commit(s_full);
-            };
-            auto issue_grad = [&](int n) {
-                const int st = n % L::ST;
-                const uint32_t sq = tc::smem_u32(smem + L::OFF_Q + st * L::TILE);
-                const uint32_t sd = tc::smem_u32(smem + L::OFF_DO + st * L::TILE);
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t aoff = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_dv, tc::sdesc(sp + aoff, 16, 1024), tc::sdesc(sd + ks * 2048, 128 * 128, 1024),
-                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
-                    tc::mma_bf16(t_dk, tc::sdesc(sds + aoff, 16, 1024), tc::sdesc(sq + ks * 2048, 128 * 128, 1024),
-                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
-                }
-                tc::mma_commit(g_done);
-                tc::mma_commit(&q_empty[st]);
-            };
-            const int n_tiles = e1 - e0;
-            if (n_tiles > 0) issue_sdp(0);
-            for (int n = 0; n < n_tiles; ++n) {
-                tc::mbar_wait(p_full, n & 1);
-                tc::tc_fence_after();
-                // with two Q/dO stages the next tile's S/dP overlaps this tile's dV/dK MMAs
-                if (L::ST == 2 && n + 1 < n_tiles) issue_sdp(n + 1);
-                issue_grad(n);
-                if (L::ST == 1 && n + 1 < n_tiles) issue_sdp(n + 1);
-            }
-        }
-    } else {
-        // element-wise: thread = key row
-        const int q4 = warp & 3, r = q4 * 32 + lane, j = j0 + r;
-        const int tid = threadIdx.x - 64;
-        const bool key_ok = j < a.T;
-        const int seg_j = key_ok ? a.seg[j] : -2;
-        // queries that see key j: [j, T) for a prompt key, [j, end_k) for a key of response k
-        const int qhi = !key_ok ? 0 : (seg_j == 0 ? a.T : a.seg_end[seg_j]);
-        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        int n = 0;
-        for (int e = e0; e < e1; ++e) {
-            const int qt = a.k_list[e] & 0x3fffffff;
-            const int i0 = qt * 128;
-            const int lo = min(max(j - i0, 0), 128), hi = min(max(qhi - i0, 0), 128);
-            // per-query vectors of this tile (loads overlap the S/dP MMAs)
-            const int iq = i0 + tid;
-            const float lq = iq < a.T ? a.lse[(long)h * a.T + iq] * LOG2E : 0.f;
-            const float dq = iq < a.T ? a.dsum[(long)h * a.T + iq] : 0.f;
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile done reading the vectors
-            v_lse[tid] = lq;
-            v_d[tid] = dq;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            tc::mbar_wait(s_full, n & 1);
-            tc::tc_fence_after();
-            float sv[128];
-            tc::tmem_ld128(t_s + lane_off, sv);
-            uint32_t pk[64];
-#pragma unroll
-            for (int c = 0; c < 128; c += 2) {
-                float p2[2];
-#pragma unroll
-                for (int e2 = 0; e2 < 2; ++e2) {
-                    const int cc = c + e2;
-                    const float p = exp2f(sv[cc] * a.scale_log2 - v_lse[cc]);
-                    p2[e2] = (cc >= lo) & (cc < hi) ? p : 0.f;
-                    sv[cc] = p2[e2];
-                }
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
-                pk[c / 2] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            // previous tile's dV/dK MMAs must be done before P^T/dS^T are overwritten
-            if (n > 0) tc::mbar_wait(g_done, (n - 1) & 1);
-            write_rowtile_sw128(smem + L::OFF_P, r, pk);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float dp[32];
-                tc::tmem_ld32(t_dp + c * 32 + lane_off, dp);
-                uint32_t w[16];
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const int cc = c * 32 + e;
-                    __nv_bfloat162 b2 =
-                        __floats2bfloat162_rn(sv[cc] * (dp[e] - v_d[cc]), sv[cc + 1] * (dp[e + 1] - v_d[cc + 1]));
-                    w[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                write_row32_sw128(smem + L::OFF_DS, r, c * 32, w);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tc::tc_fence_before();
-            tc::mbar_arrive(p_full);
-            ++n;
-        }
-        if (n > 0) {
-            tc::mbar_wait(g_done, (n - 1) & 1);
-            tc::tc_fence_after();
-        }
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {  // 0: dV, 1: dK (scaled)
-            const uint32_t src = part ? t_dk : t_dv;
-            const float mul = part ? a.scale : 1.f;
-#pragma unroll
-            for (int c = 0; c < DH / 32; ++c) {
-                float o[32];
-                tc::tmem_ld32(src + c * 32 + lane_off, o);
-                if (key_ok) {
-                    bf16* dst = a.dqkv + (long)j * 3 * a.d + (part ? a.d : 2 * a.d) + h * DH + c * 32;
-#pragma unroll
-                    for (int q = 0; q < 32; q += 8) {
-                        __align__(16) bf16 t[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(n > 0 ? o[q + e] * mul : 0.f);
-                        *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
-                    }
-                }
-            }
-        }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc::tc_fence_after();
-        tc::tmem_dealloc<512>(tbase);
-    }
-}
-
-template <int DH>
-struct DqSmem {
-    static constexpr int ST = DH == 128 ? 1 : 2;
-    static constexpr int TILE = 128 * DH * 2;
-    static constexpr int OFF_Q = 0, OFF_DO = TILE;
-    static constexpr int OFF_K = 2 * TILE;            // [ST]
-    static constexpr int OFF_V = OFF_K + ST * TILE;   // [ST]
-    static constexpr int OFF_DS = OFF_V + ST * TILE;  // dS [128 x 128] bf16
-    static constexpr int OFF_SEG = OFF_DS + 128 * 128 * 2;
-    static constexpr int OFF_BAR = OFF_SEG + 128 * 4;
-    static constexpr int TOTAL = OFF_BAR + 256 + 1024;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(NTHR, 1)
-    k_attn_dq_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                 AttnBwdArgs a) {
-    using L = DqSmem<DH>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-    uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;   // [2]
-    uint64_t* kv_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* p_full = bar + 6;
-    uint64_t* g_done = bar + 7;
-    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bar + 8);
-    int* kseg = reinterpret_cast<int*>(smem + L::OFF_SEG);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = a.q_order[blockIdx.x], h = blockIdx.y;
-    const int i0 = qt * 128;
-    const int e0 = a.q_ptr[qt], e1 = a.q_ptr[qt + 1];
-
-    if (threadIdx.x == 0) {
-        tc::mbar_init(q_full, 1);
-        for (int s = 0; s < 2; ++s) {
-            tc::mbar_init(&kv_full[s], 1);
-            tc::mbar_init(&kv_empty[s], 1);
-        }
-        tc::mbar_init(s_full, 1);
-        tc::mbar_init(p_full, 128);
-        tc::mbar_init(g_done, 1);
-        tc::fence_barrier_init();
-        tc::tma_prefetch(&tm_qkv);
-        tc::tma_prefetch(&tm_do);
-    }
-    if (warp == 1) tc::tmem_alloc<512>(tbase_s);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tbase = *tbase_s;
-    const uint32_t t_s = tbase, t_dp = tbase + 128, t_dq = tbase + 256;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            tc::mbar_expect_tx(q_full, 2 * L::TILE);
-#pragma unroll
-            for (int r = 0; r < DH / 64; ++r) {
-                tc::tma_load_2d(smem + L::OFF_Q + r * 128 * 128, &tm_qkv, q_full, h * DH + r * 64, i0);
-                tc::tma_load_2d(smem + L::OFF_DO + r * 128 * 128, &tm_do, q_full, h * DH + r * 64, i0);
-            }
-            int n = 0;
-            for (int e = e0; e < e1; ++e) {
-                const int kt = a.q_list[e] & 0x3fffffff;
-                const int st = n % L::ST;
-                tc::mbar_wait(&kv_empty[st], ((n / L::ST) & 1) ^ 1);
-                tc::mbar_expect_tx(&kv_full[st], 2 * L::TILE);
-                uint8_t* kb = smem + L::OFF_K + st * L::TILE;
-                uint8_t* vb = smem + L::OFF_V + st * L::TILE;
-#pragma unroll
-                for (int r = 0; r < DH / 64; ++r) {
-                    tc::tma_load_2d(kb + r * 128 * 128, &tm_qkv, &kv_full[st], a.d + h * DH + r * 64, kt * 128);
-                    tc::tma_load_2d(vb + r * 128 * 128, &tm_qkv, &kv_full[st], 2 * a.d + h * DH + r * 64, kt * 128);
-                }
-                ++n;
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
-            constexpr uint32_t id_g = tc::idesc_bf16(128, DH, 0, 1);
-            const uint32_t sq = tc::smem_u32(smem + L::OFF_Q), sd = tc::smem_u32(smem + L::OFF_DO);
-            const uint32_t sds = tc::smem_u32(smem + L::OFF_DS);
-            tc::mbar_wait(q_full, 0);
-            auto issue_sdp = [&](int n) {
-                const int st = n % L::ST;
-                tc::mbar_wait(&kv_full[st], (n / L::ST) & 1);
-                tc::tc_fence_after();
-                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
-                const uint32_t sv = tc::smem_u32(smem + L::OFF_V + st * L::TILE);
-#pragma unroll
-                for (int ks = 0; ks < DH / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_s, tc::sdesc(sq + off, 16, 1024), tc::sdesc(sk + off, 16, 1024), id_s, ks > 0);
-                    tc::mma_bf16(t_dp, tc::sdesc(sd + off, 16, 1024), tc::sdesc(sv + off, 16, 1024), id_s, ks > 0);
-                }
-                tc::mma_commit(s_full);
-            };
-            auto issue_grad = [&](int n) {
-                const int st = n % L::ST;
-                const uint32_t sk = tc::smem_u32(smem + L::OFF_K + st * L::TILE);
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t aoff = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
-                    tc::mma_bf16(t_dq, tc::sdesc(sds + aoff, 16, 1024), tc::sdesc(sk + ks * 2048, 128 * 128, 1024),
-                                 id_g, (n > 0 || ks > 0) ? 1u : 0u);
-                }
-                tc::mma_commit(g_done);
-                tc::mma_commit(&kv_empty[st]);
-            };
-            const int n_tiles = e1 - e0;
-            if (n_tiles > 0) issue_sdp(0);
-            for (int n = 0; n < n_tiles; ++n) {
-                tc::mbar_wait(p_full, n & 1);
-                tc::tc_fence_after();
-                if (L::ST == 2 && n + 1 < n_tiles) issue_sdp(n + 1);
-                issue_grad(n);
-                if (L::ST == 1 && n + 1 < n_tiles) issue_sdp(n + 1);
-            }
-        }
-    } else {
-        const int q4 = warp & 3, r = q4 * 32 + lane, i = i0 + r;
-        const bool row_ok = i < a.T;
-        const int seg_i = row_ok ? a.seg[i] : -1;
-        const int ea0 = !row_ok ? 0 : (seg_i == 0 ? i + 1 : a.Peff);
-        const int b1 = seg_i > 0 ? a.seg_start[seg_i] : 0, ea1 = seg_i > 0 ? i + 1 : 0;
-        const float Lr = row_ok ? a.lse[(long)h * a.T + i] * LOG2E : 0.f;
-        const float Dr = row_ok ? a.dsum[(long)h * a.T + i] : 0.f;
-        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        int n = 0;
-        for (int e = e0; e < e1; ++e) {
-            const int j0 = (a.q_list[e] & 0x3fffffff) * 128;
-            const int h0 = min(max(ea0 - j0, 0), 128);
-            const int l1 = min(max(b1 - j0, 0), 128), h1 = min(max(ea1 - j0, 0), 128);
-            tc::mbar_wait(s_full, n & 1);
-            tc::tc_fence_after();
-            float sv[128];
-            tc::tmem_ld128(t_s + lane_off, sv);
-#pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                const bool ok = (c < h0) | ((c >= l1) & (c < h1));
-                const float p = exp2f(sv[c] * a.scale_log2 - Lr);
-                sv[c] = ok ? p : 0.f;
-            }
-            if (n > 0) tc::mbar_wait(g_done, (n - 1) & 1);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float dp[32];
-                tc::tmem_ld32(t_dp + c * 32 + lane_off, dp);
-                uint32_t w[16];
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const int cc = c * 32 + e;
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(sv[cc] * (dp[e] - Dr), sv[cc + 1] * (dp[e + 1] - Dr));
-                    w[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                write_row32_sw128(smem + L::OFF_DS, r, c * 32, w);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tc::tc_fence_before();
-            tc::mbar_arrive(p_full);
-            ++n;
-        }
-        if (n > 0) {
-            tc::mbar_wait(g_done, (n - 1) & 1);
-            tc::tc_fence_after();
-        }
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
-            float o[32];
-            tc::tmem_ld32(t_dq + c * 32 + lane_off, o);
-            if (row_ok) {
-                bf16* dst = a.dqkv + (long)i * 3 * a.d + h * DH + c * 32;
-#pragma unroll
-                for (int q = 0; q < 32; q += 8) {
-                    __align__(16) bf16 t[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) t[e] = __float2bfloat16_rn(n > 0 ? o[q + e] * a.scale : 0.f);
-                    *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<uint4*>(t);
-                }
-            }
-        }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc::tc_fence_after();
-        tc::tmem_dealloc<512>(tbase);
-    }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -2042,24 +1304,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode() {
     return fn;
 }
 
-template <int DH>
-void launch_fwd(const CUtensorMap& m, const AttnTcArgs& a, cudaStream_t st) {
-    using L = AttnSmem<DH>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_attn_fwd_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-        attr = true;
-    }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int n_items = ((a.T + TQ - 1) / TQ) * a.H;
-    k_attn_fwd_tc<DH><<<std::min(n_items, sms), NTHR, L::TOTAL, st>>>(m, a, n_items);
-    PARL_LAUNCHED();
-}
 
 int device_sms_attn() {
     static int n = 0;
@@ -2083,16 +1327,6 @@ void launch_fwd_pair(const AttnPairMaps& maps, const AttnPairArgs& a, cudaStream
     PARL_LAUNCHED();
 }
 
-// PARL_ATTN_PAIR=0 selects the one-query-tile forward (diagnostics)
-bool attn_pair_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PARL_ATTN_PAIR");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
 bool make_qkv_map(CUtensorMap* m, const bf16* base, long cols, long rows) {
     auto fn = encode();
     if (!fn) return false;
@@ -2105,20 +1339,6 @@ bool make_qkv_map(CUtensorMap* m, const bf16* base, long cols, long rows) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DH>
-void launch_bwd(const CUtensorMap& mq, const CUtensorMap& md, const AttnBwdArgs& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_attn_dkv_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem<DH>::TOTAL);
-        cudaFuncSetAttribute(k_attn_dq_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem<DH>::TOTAL);
-        attr = true;
-    }
-    dim3 grid(a.n_qt, a.H);
-    k_attn_dkv_tc<DH><<<grid, NTHR, DkvSmem<DH>::TOTAL, st>>>(mq, md, a);
-    PARL_LAUNCHED();
-    k_attn_dq_tc<DH><<<grid, NTHR, DqSmem<DH>::TOTAL, st>>>(mq, md, a);
-    PARL_LAUNCHED();
-}
 
 }  // namespace
 
@@ -2143,21 +1363,8 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         return false;
     CUtensorMap mq, md;
     if (!make_qkv_map(&mq, qkv, 3L * aa.d, aa.T) || !make_qkv_map(&md, dout, aa.d, aa.T)) return false;
-    AttnBwdArgs a;
-    a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d; a.Peff = aa.Peff;
-    a.n_qt = (aa.T + 127) / 128;
-    a.seg = aa.seg;
-    a.seg_start = aa.seg_start;
-    a.seg_end = aa.seg_end;
-    a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
-    a.k_ptr = aa.sched.k_ptr; a.k_list = aa.sched.k_list; a.k_order = aa.sched.k_order;
-    if (!a.q_ptr || !a.k_ptr) return false;
-    a.scale = aa.scale;
-    a.scale_log2 = aa.scale * LOG2E;
-    a.lse = lse;
-    a.dsum = dsum;
-    a.dqkv = dqkv;
-    if (aa.sched.bk_ptr && aa.sched.bq_ptr && attn_pair_enabled() && out) {
+    if (!aa.sched.q_ptr || !aa.sched.k_ptr || !aa.sched.bk_ptr || !aa.sched.bq_ptr || !out) return false;
+    {
         const size_t ht = (size_t)aa.H * aa.T;
         float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 8 + 16));
         if (!lse2) return false;
@@ -2189,15 +1396,10 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
         b.w_ptr = aa.sched.bq_ptr; b.w_items = aa.sched.bq_items;
         if (aa.Dh == 64) launch_bwd2<64, MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
         else launch_bwd2<128, MODE_DQ>(mq, md, b, aa.sched.bq_grid, st);
-        return true;
     }
-    if (out) launch_attn_dsum<bf16>(aa, out, dout, dsum, st);
-    if (aa.Dh == 64) launch_bwd<64>(mq, md, a, st);
-    else launch_bwd<128>(mq, md, a, st);
     return true;
 }
 
-// qkv: [T x 3d] bf16; returns false when the head dim / alignment is unsupported.
 // qkv: [T x 3d] bf16 per model; the nm models (same packed group, e.g. the tri-model forward)
 // run as one launch when the dynamic queue is on.  false when the head dim / alignment is
 // unsupported.
@@ -2229,7 +1431,8 @@ bool attn_fwd_tc_multi(const AttnArgs& aa, const bf16* const* qkv, bf16* const* 
                CUDA_SUCCESS;
     };
     if (!aa.sched.q_ptr) return false;
-    if (aa.sched.p_ptr && aa.sched.w_ptr && attn_pair_enabled()) {
+    if (!aa.sched.p_ptr || !aa.sched.w_ptr) return false;
+    {
         // dynamic work queue (PARL_ATTN_DYN=0: the static per-CTA lists, one launch per model)
         static const bool dyn_ok = [] {
             const char* e = getenv("PARL_ATTN_DYN");
@@ -2264,23 +1467,6 @@ bool attn_fwd_tc_multi(const AttnArgs& aa, const bf16* const* qkv, bf16* const* 
             else launch_fwd_pair<128>(maps, pa, st);
         }
         return true;
-    }
-    for (int k = 0; k < nm; ++k) {
-        CUtensorMap m;
-        if (!qkv_map(&m, qkv[k])) return false;
-        AttnTcArgs a;
-        a.T = aa.T; a.H = aa.H; a.Dh = aa.Dh; a.d = aa.d;
-        a.Peff = aa.Peff;
-        a.seg = aa.seg;
-        a.seg_start = aa.seg_start;
-        a.seg_end = aa.seg_end;
-        a.q_ptr = aa.sched.q_ptr; a.q_list = aa.sched.q_list; a.q_order = aa.sched.q_order;
-        a.scale_log2 = aa.scale * LOG2E;
-        a.out = out[k];
-        a.ldo = ldo;
-        a.lse = lse[k];
-        if (aa.Dh == 64) launch_fwd<64>(m, a, st);
-        else launch_fwd<128>(m, a, st);
     }
     return true;
 }

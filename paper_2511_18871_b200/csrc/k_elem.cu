@@ -3,7 +3,6 @@
 //   K2  embedding gather       model.cpp:449-455
 //   K5  LayerNorm fwd / bwd    model.cpp:317-369
 //   K6b vocab LSE + gather     model.cpp:523-556 (FFMA mode; the tcgen05 head fuses this)
-//   K7  GRPO loss              grpo.cpp:24-151 + pipeline.cpp:127-139
 //   K8a softmax backward seed  model.cpp:637-650
 //   K11 embedding-grad reduce  model.cpp:825-834 (deterministic: stable sort + segmented sum)
 // plus column reductions (bias / LN parameter grads), weight conversion,
@@ -21,11 +20,15 @@ namespace parl_gpu {
 // ---------------------------------------------------------------------------
 // K1: device packer.  One thread per packed position t.  cu[k] = scored offset
 // of response k (exclusive prefix of resp_lens), cu[G] = S.
+// `id_max` receives max over tokens of (unsigned)id: an id outside [0, V) is exactly
+// one with (unsigned)id >= V (VocabError, model.cpp:413-417), checked before the forward.
 __global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t* __restrict__ resp_flat,
-                       const int32_t* __restrict__ cu, int G, PackedDev pk) {
+                       const int32_t* __restrict__ cu, int G, PackedDev pk, unsigned* __restrict__ id_max) {
     const int T = P + cu[G];
+    unsigned umax = 0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
         if (t < P) {
+            umax = max(umax, (unsigned)prompt[t]);
             pk.tokens[t] = prompt[t];
             pk.labels[t] = -1;
             pk.positions[t] = t;
@@ -41,6 +44,7 @@ __global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t*
             }
             const int k = lo, i = s - cu[k];
             const int tok = resp_flat[s];
+            umax = max(umax, (unsigned)tok);
             pk.tokens[t] = tok;
             pk.labels[t] = tok;  // self-aligned labels, packing.cpp:37
             pk.positions[t] = P + i;
@@ -61,6 +65,9 @@ __global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t*
             for (int k = 0; k < G; ++k) pk.row_idx[k] = cu[k];
         if (t == T - 1) pk.row_ptr[T] = cu[G];
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    if ((threadIdx.x & 31) == 0 && id_max) atomicMax(id_max, umax);
 }
 
 // ---------------------------------------------------------------------------
@@ -533,121 +540,6 @@ __global__ void k_softmax_bwd_v8(const bf16* z, long ldz, bf16* dz,  // may alia
 }
 
 // ---------------------------------------------------------------------------
-// K7: GRPO.  Advantages (grpo.cpp:24-48), one warp.
-__global__ void k_advantages(const double* __restrict__ rewards, int G, int mean_only, double* __restrict__ adv) {
-    const int lane = threadIdx.x;
-    double s = 0.0;
-    for (int i = lane; i < G; i += 32) s += rewards[i];
-    const double mean = warp_sum_d(s) / G;
-    double v = 0.0;
-    for (int i = lane; i < G; i += 32) v += (rewards[i] - mean) * (rewards[i] - mean);
-    const double sd = sqrt(warp_sum_d(v) / G);
-    for (int i = lane; i < G; i += 32)
-        adv[i] = mean_only ? rewards[i] - mean : (sd < 1e-8 ? 0.0 : (rewards[i] - mean) / sd);
-}
-
-__device__ __forceinline__ void clip_eval(double lp, double old, double A, double eps, double& val,
-                                          double& grad, int& clipped) {  // grpo.cpp:64-80
-    const double r = exp(lp - old), lo = 1.0 - eps, hi = 1.0 + eps;
-    const double cl = fmin(fmax(r, lo), hi);
-    const double un = r * A, cv = cl * A;
-    clipped = (r < lo || r > hi);
-    if (un <= cv) {
-        val = un;
-        grad = r * A;
-    } else {
-        val = cv;
-        grad = (r > lo && r < hi) ? r * A : 0.0;
-    }
-}
-
-// One block per response j (tokens [cu[j], cu[j+1])).  Writes the backward
-// seed upstream[t] = -d(L_j - beta KL_j)/d lp_t (pipeline.cpp:138) and the
-// per-sample {clip_term, kl, clipped, units} into per_sample[j][4].
-__global__ void k_grpo_terms(const float* __restrict__ lp, const float* __restrict__ old,
-                             const float* __restrict__ ref, const int32_t* __restrict__ cu,
-                             const double* __restrict__ adv, double eps, double beta, int granularity,
-                             float* __restrict__ upstream, double* __restrict__ per_sample) {
-    __shared__ double red[4][32];
-    const int j = blockIdx.x;
-    const int b = cu[j], e = cu[j + 1], n = e - b;
-    const double A = adv[j], inv = 1.0 / n;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double a0 = 0, a1 = 0, a2 = 0;
-    if (granularity == 0) {
-        for (int t = b + threadIdx.x; t < e; t += blockDim.x) {
-            double cv, cg;
-            int c;
-            clip_eval(lp[t], old[t], A, eps, cv, cg, c);
-            const double d = (double)ref[t] - (double)lp[t];  // grpo.cpp:89-93
-            const double em = expm1(d);
-            a0 += cv;
-            a1 += em - d;
-            a2 += c;
-            upstream[t] = (float)(-inv * (cg + beta * em));
-        }
-    } else {
-        for (int t = b + threadIdx.x; t < e; t += blockDim.x) {
-            a0 += lp[t];
-            a1 += old[t];
-            a2 += ref[t];
-        }
-    }
-    a0 = warp_sum_d(a0);
-    a1 = warp_sum_d(a1);
-    a2 = warp_sum_d(a2);
-    if (lane == 0) {
-        red[0][w] = a0;
-        red[1][w] = a1;
-        red[2][w] = a2;
-    }
-    __syncthreads();
-    __shared__ double g_seq;
-    if (threadIdx.x == 0) {
-        double s0 = 0, s1 = 0, s2 = 0;
-        for (int i = 0; i < nw; ++i) {
-            s0 += red[0][i];
-            s1 += red[1][i];
-            s2 += red[2][i];
-        }
-        double* o = per_sample + 4 * j;
-        if (granularity == 0) {
-            o[0] = s0 * inv;
-            o[1] = s1 * inv;
-            o[2] = s2;
-            o[3] = n;
-        } else {  // grpo.cpp:134-149: one evaluation on the summed log-probs
-            double cv, cg;
-            int c;
-            clip_eval(s0, s1, A, eps, cv, cg, c);
-            const double d = s2 - s0, em = expm1(d);
-            o[0] = cv;
-            o[1] = em - d;
-            o[2] = c;
-            o[3] = 1;
-            g_seq = cg + beta * em;
-        }
-    }
-    __syncthreads();
-    if (granularity == 1)
-        for (int t = b + threadIdx.x; t < e; t += blockDim.x) upstream[t] = (float)(-g_seq);
-}
-
-// Sum per-sample terms in sample order into the running stats
-// (pipeline.cpp:133-137): objective, clip, kl, clipped, units.
-__global__ void k_grpo_stats(const double* __restrict__ per_sample, int G, double beta, double* __restrict__ stats) {
-    if (threadIdx.x != 0) return;
-    for (int j = 0; j < G; ++j) {
-        const double* o = per_sample + 4 * j;
-        stats[0] += o[0] - beta * o[1];
-        stats[1] += o[0];
-        stats[2] += o[1];
-        stats[3] += o[2];
-        stats[4] += o[3];
-    }
-}
-
-// ---------------------------------------------------------------------------
 // dx[t] = sum over gathered head rows r owned by position t of dxg[r]  (CSR;
 // rows of positions without scored successors are zero).
 __global__ void k_scatter_rows(const float* __restrict__ dxg, const int32_t* __restrict__ row_ptr,
@@ -798,9 +690,25 @@ static int grid_for(long n, int bs = 256) {
     return (int)(g < 148L * 16 ? (g < 1 ? 1 : g) : 148L * 16);
 }
 
+// dense shared-prompt mask (build_shared_prompt_mask, packing.cpp:47-72) from the segment ids
+__global__ void k_allowed_mask(const int32_t* __restrict__ seg, int n, uint8_t* __restrict__ mask) {
+    const long nn = (long)n * n;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nn; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e % n);
+        const int si = seg[i], sj = seg[j];
+        mask[e] = si == 0 ? (sj == 0 && j <= i) : (sj == 0 || (sj == si && j <= i));
+    }
+}
+
+void launch_allowed_mask(const int32_t* seg, int n, uint8_t* mask, cudaStream_t st) {
+    k_allowed_mask<<<grid_for((long)n * n), 256, 0, st>>>(seg, n, mask);
+    PARL_LAUNCHED();
+}
+
 void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
-                 const PackedDev& pk, cudaStream_t st) {
-    k_pack<<<grid_for(T), 256, 0, st>>>(prompt, P, resp, cu, G, pk);
+                 const PackedDev& pk, unsigned* id_max, cudaStream_t st) {
+    if (id_max) PARL_CUDA(cudaMemsetAsync(id_max, 0, sizeof(unsigned), st));
+    k_pack<<<grid_for(T), 256, 0, st>>>(prompt, P, resp, cu, G, pk, id_max);
     PARL_LAUNCHED();
 }
 
@@ -1395,20 +1303,6 @@ template void launch_softmax_bwd<bf16, bf16>(const bf16*, long, bf16*, long, int
 template void launch_softmax_bwd<bf16, float>(const bf16*, long, float*, long, int, int, const float*, const float*,
                                               const int32_t*, cudaStream_t);
 
-void launch_advantages(const double* rewards, int G, int mean_only, double* adv, cudaStream_t st) {
-    k_advantages<<<1, 32, 0, st>>>(rewards, G, mean_only, adv);
-    PARL_LAUNCHED();
-}
-
-void launch_grpo(const float* lp, const float* old, const float* ref, const int32_t* cu, int G, const double* adv,
-                 double eps, double beta, int gran, float* upstream, double* per_sample, double* stats,
-                 cudaStream_t st) {
-    k_grpo_terms<<<G, 256, 0, st>>>(lp, old, ref, cu, adv, eps, beta, gran, upstream, per_sample);
-    PARL_LAUNCHED();
-    k_grpo_stats<<<1, 32, 0, st>>>(per_sample, G, beta, stats);
-    PARL_LAUNCHED();
-}
-
 void launch_scatter_rows(const float* dxg, const int32_t* row_ptr, const int32_t* row_idx, int T, int D, float* dx,
                          cudaStream_t st) {
     if (D % 4 == 0 && ((reinterpret_cast<uintptr_t>(dxg) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0)
@@ -1542,6 +1436,31 @@ void launch_rows_copy(const float* src, const int32_t* idx, int n, int d, int di
 
 void launch_axpy(const float* x, float* y, long n, cudaStream_t st) {
     k_axpy<<<grid_for(n), 256, 0, st>>>(x, y, n);
+    PARL_LAUNCHED();
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ x, float* __restrict__ y, long n) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+        y[e] = (float)x[e];
+}
+void launch_f64_to_f32(const double* x, float* y, long n, cudaStream_t st) {
+    k_f64_to_f32<<<grid_for(n), 256, 0, st>>>(x, y, n);
+    PARL_LAUNCHED();
+}
+
+template <class T>
+__global__ void k_finite_check(const T* __restrict__ x, long n, int* __restrict__ flags) {
+    bool bad = false;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[e]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+}
+void launch_finite_check_f32(const float* x, long n, int* flags, cudaStream_t st) {
+    k_finite_check<float><<<grid_for(n), 256, 0, st>>>(x, n, flags);
+    PARL_LAUNCHED();
+}
+void launch_finite_check_f64(const double* x, long n, int* flags, cudaStream_t st) {
+    k_finite_check<double><<<grid_for(n), 256, 0, st>>>(x, n, flags);
     PARL_LAUNCHED();
 }
 

@@ -80,7 +80,8 @@ struct ModelW {
 
 // launchers (k_elem.cu)
 void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
-                 const PackedDev& pk, cudaStream_t st);
+                 const PackedDev& pk, unsigned* id_max, cudaStream_t st);
+void launch_allowed_mask(const int32_t* seg, int n, uint8_t* mask, cudaStream_t st);
 void launch_embed(const float* tok, const float* pos, const int32_t* tokens, const int32_t* positions, int T, int D,
                   float* x, cudaStream_t st);
 template <class T>
@@ -104,10 +105,30 @@ void launch_lse_combine(const float* part, int n_parts, const float* target, int
 template <class Tin, class Tout>
 void launch_softmax_bwd(const Tin* z, long ldz, Tout* dz, long lddz, int S, int V, const float* lse, const float* u,
                         const int32_t* labels, cudaStream_t st);
-void launch_advantages(const double* rewards, int G, int mean_only, double* adv, cudaStream_t st);
-void launch_grpo(const float* lp, const float* old, const float* ref, const int32_t* cu, int G, const double* adv,
-                 double eps, double beta, int gran, float* upstream, double* per_sample, double* stats,
-                 cudaStream_t st);
+// K7 GRPO loss (k_grpo.cu): advantages + per-token terms + per-sample sums + stats
+struct GrpoArgs {
+    const void *lp = nullptr, *old = nullptr, *ref = nullptr;  // [S] each, fp32 or (lp_f64) fp64
+    int lp_f64 = 0;
+    const int32_t* sample_of = nullptr;  // [S] sample of each scored token (non-decreasing)
+    const int32_t* cu = nullptr;         // [n + 1] token offsets of the samples
+    long S = 0;
+    int n = 0;
+    const double* rewards = nullptr;  // [n]: advantages per group of group_size samples (grpo.cpp:24-48)
+    const double* adv_in = nullptr;   // [n]: given advantages (rewards == nullptr)
+    int group_size = 0, mean_only = 0;
+    double eps = 0.2, beta = 0.04;
+    int gran = 0;             // 0 token, 1 sequence
+    double up_scale = -1.0;   // upstream = up_scale * d(L_j - beta KL_j)/d lp  (pipeline.cpp:138: -1)
+    float* up_f32 = nullptr;  // [S] upstream out (one of up_f32 / up_f64 may be null)
+    double* up_f64 = nullptr;
+    double* adv_out = nullptr;     // [n] advantages used (required)
+    double* slots = nullptr;       // grpo_slot_count(S, n) doubles
+    double* per_sample = nullptr;  // [n x 4] {clip_term, kl, clipped_units, total_units} or null
+    double* g_seq = nullptr;       // [n] (sequence granularity)
+    double* stats = nullptr;       // [5] += {objective, clip, kl, clipped, units} or null
+};
+size_t grpo_slot_count(long S, int n);
+void launch_grpo(const GrpoArgs& a, cudaStream_t st);
 void launch_scatter_rows(const float* dxg, const int32_t* row_ptr, const int32_t* row_idx, int T, int D, float* dx,
                          cudaStream_t st);
 size_t sort_temp_bytes(int n);
@@ -123,6 +144,7 @@ void launch_convert_w(const double* src, int rows, int cols, T* dst, long ldd, i
 template <class T>
 void launch_export_w(const T* src, long lds, int rows, int cols, int transposed, double* dst, cudaStream_t st);
 void launch_f32_to_f64(const float* x, double* y, long n, cudaStream_t st);
+void launch_f64_to_f32(const double* x, float* y, long n, cudaStream_t st);
 void launch_randn(double* out, long n, uint64_t seed, uint32_t stream, double scale, const double* base,
                   cudaStream_t st);
 void launch_fill_f64(double* out, long n, double v, cudaStream_t st);
@@ -132,6 +154,8 @@ void launch_mark_rows(const int32_t* ids, int n, uint8_t* flags, cudaStream_t st
 void launch_or_bytes(const uint8_t* src, uint8_t* dst, int n, cudaStream_t st);
 void select_flagged_rows(const uint8_t* flags, int n, int32_t* idx, int* count, cudaStream_t st);
 void launch_rows_copy(const float* src, const int32_t* idx, int n, int d, int dir, float* dst, cudaStream_t st);
+void launch_finite_check_f32(const float* x, long n, int* flags, cudaStream_t st);  // flags |= 1 on NaN/Inf
+void launch_finite_check_f64(const double* x, long n, int* flags, cudaStream_t st);
 void launch_sgd(const float* g, double* w, long n, double scale, int* flags, int phase, cudaStream_t st);
 
 // attention (k_attn.cu).  qkv: [T x 3d] (q | k | v, head h at columns h*Dh);

@@ -97,6 +97,16 @@ class _Stats(C.Structure):
                 ("clipped_units", C.c_double), ("total_units", C.c_double)]
 
 
+class _SampleTerms(C.Structure):
+    _fields_ = [("clip_term", C.c_double), ("kl", C.c_double), ("clipped_units", C.c_int),
+                ("total_units", C.c_int)]
+
+
+class _LossReport(C.Structure):
+    _fields_ = [("objective", C.c_double), ("clip_term_mean", C.c_double), ("kl_mean", C.c_double),
+                ("clip_fraction", C.c_double), ("token_count", C.c_long)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
@@ -133,6 +143,17 @@ def _load():
         "parl_sample_tokens": [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_uint64, vp, C.POINTER(C.c_int)],
         "parl_ctx_profile": [vp, C.c_int], "parl_ctx_set_recompute": [vp, C.c_int], "parl_act_recompute": [vp],
         "parl_ctx_profile_read": [vp, C.c_int, f64p, f64p, C.POINTER(C.c_long)],
+        "parl_grad_set_micro_steps": [vp, C.c_int], "parl_grad_add_micro_steps": [vp, C.c_int],
+        "parl_grad_all_finite": [vp, C.POINTER(C.c_int)], "parl_grad_upload": [vp, f64p, C.c_size_t],
+        "parl_model_all_finite": [vp, C.POINTER(C.c_int)], "parl_model_set_init_seed": [vp, C.c_uint64],
+        "parl_group_advantages": [vp, f64p, C.c_int, C.c_int, f64p],
+        "parl_clipped_term": [vp, C.c_double, C.c_double, C.c_double, C.c_double, f64p],
+        "parl_kl_term": [vp, C.c_double, C.c_double, f64p],
+        "parl_per_sample_terms": [vp, f64p, f64p, f64p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                  f64p, C.POINTER(_SampleTerms)],
+        "parl_grpo_microbatch_loss": [vp, C.c_int, i32p, f64p, f64p, f64p, f64p, C.c_double, C.c_double, C.c_int,
+                                      f64p, C.POINTER(_LossReport), f64p],
+        "parl_shared_prompt_mask": [vp, C.c_int, i32p, C.c_int, C.POINTER(C.c_uint8)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -147,6 +168,8 @@ def _load():
     lib.parl_grad_micro_steps.argtypes = [vp]
     lib.parl_model_version.argtypes = [vp]
     lib.parl_model_version.restype = C.c_uint64
+    lib.parl_model_init_seed.argtypes = [vp]
+    lib.parl_model_init_seed.restype = C.c_uint64
     lib.parl_ctx_stream.argtypes = [vp]
     lib.parl_ctx_stream.restype = C.c_void_p
     lib.parl_ctx_launches.argtypes = [vp]
@@ -326,6 +349,18 @@ class ModelParams:
     def version(self) -> int:
         return int(LIB.parl_model_version(self.h))
 
+    def init_seed(self) -> int:
+        return int(LIB.parl_model_init_seed(self.h))
+
+    def set_init_seed(self, seed: int):
+        _check(LIB.parl_model_set_init_seed(self.h, int(seed)), self.ctx.h)
+
+    def all_finite(self) -> bool:
+        """ModelParams::all_finite (model.cpp:183-187)."""
+        v = C.c_int()
+        _check(LIB.parl_model_all_finite(self.h, C.byref(v)), self.ctx.h)
+        return bool(v.value)
+
     def apply_update(self, grads: "GradBuffer", lr: float):
         _check(LIB.parl_apply_update(self.h, grads.h, lr), self.ctx.h)
 
@@ -371,6 +406,23 @@ class GradBuffer:
 
     def micro_step_count(self) -> int:
         return int(LIB.parl_grad_micro_steps(self.h))
+
+    def set_micro_step_count(self, n: int):
+        """GradBuffer::set_micro_step_count (model.hpp:126): the update divisor."""
+        _check(LIB.parl_grad_set_micro_steps(self.h, int(n)), self.ctx.h)
+
+    def add_micro_steps(self, n: int):
+        _check(LIB.parl_grad_add_micro_steps(self.h, int(n)), self.ctx.h)
+
+    def all_finite(self) -> bool:
+        v = C.c_int()
+        _check(LIB.parl_grad_all_finite(self.h, C.byref(v)), self.ctx.h)
+        return bool(v.value)
+
+    def upload(self, flat):
+        """Host fp64 values into the device accumulator (a GradBuffer::flat_mut() write)."""
+        g = _f64(flat)
+        _check(LIB.parl_grad_upload(self.h, _pd(g), len(g)), self.ctx.h)
 
     def allreduce(self):
         _check(LIB.parl_grad_allreduce(self.ctx.h, self.h), self.ctx.h)
@@ -700,6 +752,155 @@ def train_microbatch(tm: TriModel, group: Group, grads: GradBuffer, hyper: Hyper
     _check(LIB.parl_train_microbatch(ctx.h, tm.policy.h, old, tm.reference.h, group.h, _pd(r), _pd(a), C.byref(h),
                                      grads.h, C.byref(s) if want_stats else None), ctx.h)
     return {k: getattr(s, k) for k, _ in _Stats._fields_} if want_stats else None
+
+
+# --------------------------------------------------------------------------- GRPO operator API (grpo.hpp:50-83)
+def group_advantages(rewards, ctx: Optional[Context] = None, mean_only: bool = False) -> np.ndarray:
+    """grpo.cpp:24-38 (mean_only: 40-48), evaluated by K7 on the device."""
+    ctx = ctx or default_context()
+    r = _f64(rewards)
+    out = np.zeros(max(len(r), 1), np.float64)
+    _check(LIB.parl_group_advantages(ctx.h, _pd(r), len(r), int(mean_only), _pd(out)), ctx.h)
+    return out[:len(r)]
+
+
+def group_advantages_mean_only(rewards, ctx: Optional[Context] = None) -> np.ndarray:
+    return group_advantages(rewards, ctx, mean_only=True)
+
+
+def clipped_term(lp_new: float, lp_old: float, advantage: float, epsilon: float,
+                 ctx: Optional[Context] = None) -> float:
+    """grpo.cpp:95-101."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(LIB.parl_clipped_term(ctx.h, lp_new, lp_old, advantage, epsilon, C.byref(v)), ctx.h)
+    return v.value
+
+
+def kl_term(lp_new: float, lp_ref: float, ctx: Optional[Context] = None) -> float:
+    """grpo.cpp:103-107."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(LIB.parl_kl_term(ctx.h, lp_new, lp_ref, C.byref(v)), ctx.h)
+    return v.value
+
+
+@dataclass
+class Sample:
+    """grpo.hpp:14-27 (fields the loss reads)."""
+
+    response: Sequence[int]
+    advantage: float = 0.0
+    old_logprobs: Sequence[float] = ()
+    ref_logprobs: Sequence[float] = ()
+    prompt: Sequence[int] = ()
+    reward: float = 0.0
+    group_id: int = 0
+    rollout_index: int = 0
+
+
+@dataclass
+class SampleTerms:
+    clip_term: float
+    kl: float
+    clipped_units: int
+    total_units: int
+    upstream: np.ndarray
+
+
+def per_sample_terms(sample: Sample, policy_logprobs, epsilon: float, beta: float, granularity: str = "token",
+                     ctx: Optional[Context] = None) -> SampleTerms:
+    """grpo.cpp:111-151."""
+    ctx = ctx or default_context()
+    n = len(sample.response)
+    lp, old, ref = _f64(policy_logprobs), _f64(sample.old_logprobs), _f64(sample.ref_logprobs)
+    if len(lp) != n or len(old) != n or len(ref) != n:
+        raise ShapeError(f"logprob vectors not aligned with response length {n}")
+    up = np.zeros(max(n, 1), np.float64)
+    st = _SampleTerms()
+    _check(LIB.parl_per_sample_terms(ctx.h, _pd(lp), _pd(old), _pd(ref), n, float(sample.advantage), epsilon, beta,
+                                     0 if granularity == "token" else 1, _pd(up), C.byref(st)), ctx.h)
+    return SampleTerms(st.clip_term, st.kl, st.clipped_units, st.total_units, up[:n])
+
+
+@dataclass
+class LossReport:
+    objective: float
+    clip_term_mean: float
+    kl_mean: float
+    clip_fraction: float
+    token_count: int
+
+
+@dataclass
+class MicrobatchLoss:
+    loss: float
+    upstream: list
+    report: LossReport
+
+
+def grpo_microbatch_loss(samples: Sequence[Sample], policy_logprobs, epsilon: float, beta: float,
+                         granularity: str = "token", ctx: Optional[Context] = None) -> MicrobatchLoss:
+    """grpo.cpp:153-184."""
+    ctx = ctx or default_context()
+    if len(samples) == 0:
+        raise ShapeError("empty micro-batch")
+    if len(policy_logprobs) != len(samples):
+        raise ShapeError("policy logprob count != sample count")
+    lens = _i32([len(s.response) for s in samples])
+    for s, lp in zip(samples, policy_logprobs):
+        n = len(s.response)
+        if len(lp) != n or len(s.old_logprobs) != n or len(s.ref_logprobs) != n:
+            raise ShapeError(f"logprob vectors not aligned with response length {n}")
+    cat = lambda xs: _f64(np.concatenate([np.asarray(x, np.float64) for x in xs]) if len(xs) else [])
+    lp, old = cat(policy_logprobs), cat([s.old_logprobs for s in samples])
+    ref, adv = cat([s.ref_logprobs for s in samples]), _f64([s.advantage for s in samples])
+    up = np.zeros(max(len(lp), 1), np.float64)
+    rep, loss = _LossReport(), C.c_double()
+    _check(LIB.parl_grpo_microbatch_loss(ctx.h, len(samples), _pi(lens), _pd(lp), _pd(old), _pd(ref), _pd(adv),
+                                         epsilon, beta, 0 if granularity == "token" else 1, _pd(up), C.byref(rep),
+                                         C.byref(loss)), ctx.h)
+    ups = np.split(up[:len(lp)], np.cumsum(lens)[:-1])
+    return MicrobatchLoss(loss.value, ups, LossReport(rep.objective, rep.clip_term_mean, rep.kl_mean,
+                                                      rep.clip_fraction, int(rep.token_count)))
+
+
+def build_shared_prompt_mask(prompt_len: int, response_lens, ctx: Optional[Context] = None) -> np.ndarray:
+    """packing.cpp:47-72: dense [n x n] allowed-pair matrix (row i attends to column j)."""
+    ctx = ctx or default_context()
+    lens = _i32(response_lens)
+    n = int(prompt_len) + int(lens.sum())
+    out = np.zeros(max(n * n, 1), np.uint8)
+    _check(LIB.parl_shared_prompt_mask(ctx.h, int(prompt_len), _pi(lens), len(lens),
+                                       out.ctypes.data_as(C.POINTER(C.c_uint8))), ctx.h)
+    return out[:n * n].reshape(n, n).astype(bool)
+
+
+def train_iteration(tm: "TriModel", groups, hyper: "HyperParams", lr: float, grads: Optional[GradBuffer] = None,
+                    old_policy: str = "one_step_delayed", world_samples: Optional[int] = None,
+                    allreduce: bool = False) -> dict:
+    """The training half of Pipeline::run_iteration (pipeline.cpp:263-352), device-resident.
+
+    groups: list of (Group, advantages[m], rollout_old_logprobs or None) micro-batches of this rank, in
+    consumption order.  Accumulates every micro-batch (train_microbatch), then, as pipeline.cpp:346-351:
+    divisor = N*G samples (world_samples when the batch is sharded over ranks), snapshot old <- policy,
+    apply_update.  Returns the summed stats (allreduced across ranks when `allreduce`)."""
+    ctx = tm.policy.ctx
+    gb = grads if grads is not None else GradBuffer(tm.policy)
+    gb.reset()
+    ctx.stats_reset()
+    n_samples = 0
+    for group, adv, old_lp in groups:
+        train_microbatch(tm, group, gb, hyper, advantages=adv,
+                         rollout_old_logprobs=old_lp if old_policy == "rollout_weights" else None, want_stats=False)
+        n_samples += len(adv)
+    if allreduce:
+        gb.allreduce()
+        ctx.stats_allreduce()
+    gb.set_micro_step_count(world_samples if world_samples is not None else n_samples)
+    tm.snapshot_old_policy()
+    tm.policy.apply_update(gb, lr)
+    return ctx.stats()
 
 
 def version() -> str:

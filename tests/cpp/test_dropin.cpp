@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <functional>
 #include <random>
 #include <string>
@@ -94,14 +95,14 @@ TEST_CASE(init_bit_exact_with_oracle) {  // model.cpp:142-164
     orc_cfg oc = ocfg(c);
     std::vector<double> w(orc_param_count(&oc));
     orc_init_params(&oc, 41, w.data());
-    CHECK(p.flat() == w);
+    CHECK(std::ranges::equal(p.flat(), w));
 }
 
 TEST_CASE(packed_logprobs_and_grads_match_oracle) {  // test_packing.cpp:123-200 vs the oracle
     ModelConfig c = small_config();
     ModelParams params = ModelParams::init(c, 41);
     orc_cfg oc = ocfg(c);
-    std::vector<double> w = params.flat();
+    std::vector<double> w(params.flat().begin(), params.flat().end());
     std::mt19937 rng(17);
     for (int trial = 0; trial < 10; ++trial) {
         std::vector<TokenId> prompt(1 + rng() % 5);
@@ -125,7 +126,8 @@ TEST_CASE(packed_logprobs_and_grads_match_oracle) {  // test_packing.cpp:123-200
         double lp_err = 0;
         for (int i = 0; i < n; ++i) lp_err = std::max(lp_err, std::fabs(fwd.logprobs[i] - lref[i]));
         CHECK(lp_err < 2e-5);
-        std::vector<double> g = backward(params, fwd, up).flat();
+        GradBuffer gb = backward(params, fwd, up);
+        std::vector<double> g(gb.flat().begin(), gb.flat().end());
         double num = 0, den = 0;
         for (std::size_t i = 0; i < g.size(); ++i) {
             num += (g[i] - gref[i]) * (g[i] - gref[i]);
@@ -175,11 +177,14 @@ TEST_CASE(backward_linearity_and_lifecycle) {  // test_model.cpp:131-173
     std::vector<TokenId> tokens{1, 5, 6, 7};
     std::vector<std::int32_t> labels{kIgnoreLabel, 5, 9, 2};
     auto f0 = forward_logprobs(p, tokens, iota(4), AttentionMaskSpec::causal(), labels, true);
-    for (double v : backward(p, f0, std::vector<double>{0, 0, 0}).flat()) CHECK(v == 0.0);
+    GradBuffer gz = backward(p, f0, std::vector<double>{0, 0, 0});
+    for (double v : gz.flat()) CHECK(v == 0.0);
     auto f1 = forward_logprobs(p, tokens, iota(4), AttentionMaskSpec::causal(), labels, true);
-    auto g1 = backward(p, f1, std::vector<double>{0.3, -1.1, 0.7}).flat();
+    GradBuffer gb1 = backward(p, f1, std::vector<double>{0.3, -1.1, 0.7});
+    auto g1 = gb1.flat();
     auto f2 = forward_logprobs(p, tokens, iota(4), AttentionMaskSpec::causal(), labels, true);
-    auto g2 = backward(p, f2, std::vector<double>{0.6, -2.2, 1.4}).flat();
+    GradBuffer gb2 = backward(p, f2, std::vector<double>{0.6, -2.2, 1.4});
+    auto g2 = gb2.flat();
     bool exact = true;
     for (std::size_t i = 0; i < g1.size(); ++i) exact = exact && g2[i] == 2 * g1[i];
     CHECK(exact);
@@ -194,7 +199,7 @@ TEST_CASE(backward_linearity_and_lifecycle) {  // test_model.cpp:131-173
 
 TEST_CASE(gradbuffer_accumulate_and_update) {  // test_model.cpp:175-216
     ModelParams p = ModelParams::init(small_config(), 9);
-    auto w0 = p.flat();
+    std::vector<double> w0(p.flat().begin(), p.flat().end());
     std::vector<TokenId> tokens{1, 5, 6, 7};
     std::vector<std::int32_t> labels{kIgnoreLabel, 5, 9, 2};
     auto f = forward_logprobs(p, tokens, iota(4), AttentionMaskSpec::causal(), labels, true);
@@ -203,7 +208,7 @@ TEST_CASE(gradbuffer_accumulate_and_update) {  // test_model.cpp:175-216
     acc.accumulate(g);
     acc.accumulate(g);
     CHECK(acc.micro_step_count() == 2);
-    auto gf = g.flat();
+    std::vector<double> gf(g.flat().begin(), g.flat().end());
     p.apply_update(acc, 0.5);  // W -= 0.5 * (2g) / 2
     CHECK(p.version() == 1);
     auto w1 = p.flat();
@@ -235,7 +240,7 @@ TEST_CASE(train_microbatch_matches_oracle) {  // pipeline.cpp:97-141
     MicrobatchStats stats;
     train_microbatch(tm, prompt, resp, rewards, HyperParams{}, grads, stats);
     orc_cfg oc = ocfg(c);
-    auto w = tm.policy.flat();
+    std::vector<double> w(tm.policy.flat().begin(), tm.policy.flat().end());
     std::vector<double> adv(3), g(w.size(), 0.0), st(5, 0.0);
     orc_group_advantages(rewards.data(), 3, 0, adv.data());
     std::vector<int> flat{5, 6, 2, 7, 9, 10, 11, 3}, lens{3, 1, 4};
@@ -260,7 +265,7 @@ TEST_CASE(checkpoint_round_trip_and_errors) {  // model.cpp:907-987
     save_checkpoint(path, p);
     ModelParams q = load_checkpoint(path);
     CHECK(q.config() == c);
-    CHECK(q.flat() == p.flat());
+    CHECK(std::ranges::equal(q.flat(), p.flat()));
     CHECK(q.version() == p.version());
     CHECK_THROWS_AS(load_checkpoint("/tmp/parl_dropin_missing.parlckp1"), IoError);
 }
