@@ -200,49 +200,53 @@ def cpu_threads(per_thread_bytes: float) -> int:
 def _sample_cfg(c):
     from oracle import Cfg
 
-    # the workload's model dims with a tiny packed group: P=2, G=2, R=1 per worker (T=4)
+    # C1 runs as is; at the large configs' model dims the reference holds fp64 T x V logits and
+    # H x T x T probabilities per layer (C2: ~256 GB), so each worker runs
+    # a tiny packed group of the same model: P=2, G=2, R=1 (T=4)
     sP, sG, sR = (2, 2, 1) if c["vocab"] > 10000 else (c["P"], c["G"], c["R"])
     return Cfg(c["vocab"], c["d"], c["L"], c["H"], c["F"], max(sP + sG * sR, 8)), sP, sG, sR
 
 
-def reference_fits(c):
-    """Whether one reference worker (fp64 params + grads + clones) fits host memory."""
-    from oracle import Oracle
+class RefBaseline:
+    """The reference's own implementation (oracle/_ref, built from its sources) on the host
+    cores: one TriModel per worker thread, built once outside any timing; each step runs one
+    shared-prompt train_microbatch (pipeline.cpp:97-141) per worker, all workers concurrently."""
 
-    try:
-        ref = Oracle("ref")
-    except FileNotFoundError:
-        return False
-    return 6.0 * 8 * ref.param_count(_sample_cfg(c)[0]) <= 0.6 * host_mem_available()
+    def __init__(self, c, threads=None):
+        from oracle import Oracle
 
+        self.ref = Oracle("ref")  # FileNotFoundError when not built
+        self.cfg, self.P, self.G, self.R = _sample_cfg(c)
+        n_params = self.ref.param_count(self.cfg)
+        per_thread = 6.0 * 8 * n_params  # fp64 params x3 + grads + forward caches
+        if per_thread > 0.6 * host_mem_available():
+            raise MemoryError("the reference's fp64 model does not fit host memory")
+        self.threads = threads or cpu_threads(per_thread)
+        self.T = self.P + self.G * self.R
+        self.h = self.ref.bench_open(self.cfg, 7, self.threads)
 
-def reference_sample(c, reps=1, threads=None):
-    """Time the reference (oracle/_ref) on a bounded sample with the workload's
-    model dims; return (tokens/s scaled to the workload by the FLOP model, info)."""
-    from oracle import Cfg, Oracle
+    def step(self) -> float:
+        return self.ref.bench_run(self.h, self.P, self.G, self.R, 1)
 
-    try:
-        ref = Oracle("ref")
-    except FileNotFoundError:
-        return None
-    cfg, sP, sG, sR = _sample_cfg(c)
-    n_params = ref.param_count(cfg)
-    if 6.0 * 8 * n_params > 0.6 * host_mem_available():  # fp64 params + grads + clones per thread
-        return None
-    thr = threads or cpu_threads(6.0 * 8 * n_params)
-    secs = ref.bench_microbatch(cfg, 7, sP, sG, sR, reps, thr)
-    T_s = sP + sG * sR
-    fl_s = flops_per_group(c, sP, [sR] * sG, reference_head=True)
-    fl_w = flops_per_group(c, c["P"], group_lens(c), reference_head=True)
-    T_w = c["P"] + sum(group_lens(c))
-    tok_s_sample = thr * reps * T_s / secs
-    scaled = tok_s_sample * (fl_s / T_s) / (fl_w / T_w)
-    info = {"cores": thr, "sample": f"reference train_microbatch (shared-prompt) at {c['name']} model dims, "
-                                    f"P={sP},G={sG},R={sR} (T={T_s}) x {reps} per thread, {thr} threads, "
-                                    f"{secs:.1f}s wall; {tok_s_sample:.3f} tok/s on the sample, scaled by "
-                                    f"FLOPs/token to T={T_w}",
-            "secs": secs, "sample_tok_s": tok_s_sample}
-    return scaled, info
+    def close(self):
+        self.ref.bench_close(self.h)
+
+    def describe(self, c, secs):
+        T_w = c["P"] + sum(group_lens(c))
+        tok_s = self.threads * self.T * len(secs) / sum(secs)
+        same = self.T == T_w
+        info = {"cores": self.threads, "value": tok_s, "same_config": same,
+                "sample": f"reference Pipeline::train_microbatch (shared-prompt branch) at {c['name']} model dims, "
+                          f"P={self.P} G={self.G} R={self.R} (T={self.T}) per worker, {self.threads} workers "
+                          f"concurrently, {len(secs)} step(s), {np.mean(secs):.2f} s per step (measured, unscaled)"}
+        if not same:  # context only: the FLOP model's per-token cost at the workload's T
+            fl_s = flops_per_group(c, self.P, [self.R] * self.G, reference_head=True)
+            fl_w = flops_per_group(c, c["P"], group_lens(c), reference_head=True)
+            info["extrapolated_to_workload"] = {
+                "value": tok_s * (fl_s / self.T) / (fl_w / T_w), "unit": "packed tokens/s",
+                "method": f"FLOP model per packed token (SURVEY.md 8d, reference head over all rows), T={T_w}; "
+                          f"not executed: needs ~256 GB host memory and hours per micro-step"}
+        return info
 
 
 def run_reference(args, c):
@@ -250,35 +254,34 @@ def run_reference(args, c):
     if rank != 0:
         return
     c["name"] = args.config
-    T_w = c["P"] + sum(group_lens(c))
-    from oracle import Oracle
-
     try:
-        Oracle("ref")
+        rb = RefBaseline(c)
     except FileNotFoundError:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparl_ref.so not built"}))
         return
-    if not reference_fits(c):
+    except MemoryError:
         print(json.dumps({"impl": "reference", "unavailable": f"the reference's fp64 model at {args.config} dims does "
                                                               f"not fit this host's memory"}))
         return
     for _ in range(args.warmup):
-        reference_sample(c)
-    vals, infos = [], []
-    for _ in range(args.steps):
-        v, info = reference_sample(c)
-        vals.append(v)
-        infos.append(info)
-    value = float(np.mean(vals))
+        rb.step()
+    secs = [rb.step() for _ in range(args.steps)]
+    rb.close()
+    info = rb.describe(c, secs)
+    value = info["value"]
     out = {"metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref", "value": value,
            "unit": "packed tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1000.0 * T_w / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
-                                  f"P={c['P']} G={c['G']} R={group_lens(c)} (T={T_w}) per group"},
-           "cpu_baseline": {"value": value, "unit": "packed tokens/s", "cores": infos[0]["cores"],
-                            "kind": "reference", "sample": infos[0]["sample"]},
+           "ms_per_step": 1000.0 * float(np.mean(secs)), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.config} model dims: d={c['d']} H={c['H']} L={c['L']} F={c['F']} "
+                                  f"V={c['vocab']}; executed sample: P={rb.P} G={rb.G} R={rb.R} (T={rb.T}) x "
+                                  f"{rb.threads} workers per step",
+                      "same_config": info["same_config"]},
+           "cpu_baseline": {"value": value, "unit": "packed tokens/s", "cores": rb.threads, "kind": "reference",
+                            "sample": info["sample"]},
            "e2e": {"value": value, "unit": "packed tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if "extrapolated_to_workload" in info:
+        out["extrapolated_to_workload"] = info["extrapolated_to_workload"]
     print(json.dumps(out))
 
 
@@ -413,7 +416,15 @@ def run_ours(args, c):
     traffic, traffic_src = measured_traffic(dom)
     share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
     c["name"] = args.config
-    cpu = reference_sample(c) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:  # one measured step of the reference on the host cores (after both timed regions)
+            rb = RefBaseline(c)
+            secs = [rb.step()]
+            rb.close()
+            cpu = rb.describe(c, secs)
+        except (FileNotFoundError, MemoryError):
+            cpu = None
     out = {
         "metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref",
         "value": value, "unit": "packed tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -442,9 +453,10 @@ def run_ours(args, c):
         "clocks": clk.summary(),
     }
     if cpu is not None:
-        v, info = cpu
-        out["cpu_baseline"] = {"value": v, "unit": "packed tokens/s", "cores": info["cores"], "kind": "reference",
-                               "sample": info["sample"]}
+        out["cpu_baseline"] = {"value": cpu["value"], "unit": "packed tokens/s", "cores": cpu["cores"],
+                               "kind": "reference", "sample": cpu["sample"], "same_config": cpu["same_config"]}
+        if "extrapolated_to_workload" in cpu:
+            out["cpu_baseline"]["extrapolated_to_workload"] = cpu["extrapolated_to_workload"]
     print(json.dumps(out))
 
 

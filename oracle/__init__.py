@@ -88,6 +88,11 @@ class Oracle:
             self.lib.ref_bench_microbatch.restype = C.c_double
             self.lib.ref_bench_microbatch.argtypes = [C.c_void_p, C.c_ulonglong] + [C.c_int] * 5
             self.lib.ref_param_count.restype = C.c_long
+            self.lib.ref_bench_open.restype = C.c_void_p
+            self.lib.ref_bench_open.argtypes = [C.c_void_p, C.c_ulonglong, C.c_int]
+            self.lib.ref_bench_run.restype = C.c_double
+            self.lib.ref_bench_run.argtypes = [C.c_void_p] + [C.c_int] * 4
+            self.lib.ref_bench_close.argtypes = [C.c_void_p]
         else:
             self.lib.orc_param_count.restype = C.c_size_t
         self.lib[self.px + "init_params"].argtypes = [C.c_void_p, C.c_ulonglong, C.c_void_p]
@@ -278,6 +283,19 @@ class Oracle:
         new_old = w_pol.copy()  # snapshot_old_policy before the update (pipeline.cpp:350-351)
         w_new = w_pol - (lr / float(total)) * g
         return w_new, new_old, stats
+
+    def bench_open(self, cfg: Cfg, seed: int, threads: int):
+        """Persistent CPU-baseline workers (one TriModel each, built once, outside any timing)."""
+        assert self.kind == "ref"
+        c = cfg.c()
+        return self.lib.ref_bench_open(C.byref(c), C.c_ulonglong(seed), threads)
+
+    def bench_run(self, h, P, G, R, reps) -> float:
+        """Max wall seconds over the workers for `reps` shared-prompt micro-batches each."""
+        return float(self.lib.ref_bench_run(h, P, G, R, reps))
+
+    def bench_close(self, h):
+        self.lib.ref_bench_close(h)
 
     def bench_microbatch(self, cfg: Cfg, seed, P, G, R, reps, threads) -> float:
         assert self.kind == "ref"

@@ -374,4 +374,62 @@ double ref_bench_microbatch(const CCfg* c, unsigned long long seed, int P, int G
     return mx;
 }
 
+// Persistent CPU-baseline workers (bench.py --impl reference): the TriModels are built once
+// (ref_bench_open, in parallel), then every ref_bench_run times `reps` shared-prompt
+// micro-batches per worker, all workers concurrently; returns the max wall seconds.
+struct RefBench {
+    ModelConfig mc;
+    std::vector<std::unique_ptr<TriModel>> tms;
+    std::vector<Rng> rngs;
+};
+
+void* ref_bench_open(const CCfg* c, unsigned long long seed, int threads) {
+    auto* b = new RefBench();
+    b->mc = to_cfg(c);
+    b->tms.resize(threads);
+    for (int th = 0; th < threads; ++th) b->rngs.emplace_back(mix_seed(seed, 123 + th));
+    std::vector<std::thread> pool;
+    for (int th = 0; th < threads; ++th)
+        pool.emplace_back([b, th, seed] { b->tms[th] = std::make_unique<TriModel>(TriModel::init(b->mc, seed)); });
+    for (auto& t : pool) t.join();
+    return b;
+}
+
+double ref_bench_run(void* h, int P, int G, int R, int reps) {
+    auto* b = static_cast<RefBench*>(h);
+    const int threads = (int)b->tms.size();
+    std::vector<std::thread> pool;
+    std::vector<double> secs(threads, 0.0);
+    std::atomic<int> ready{0};
+    for (int th = 0; th < threads; ++th) {
+        pool.emplace_back([=, &ready, &secs] {
+            TriModel& tm = *b->tms[th];
+            Rng& rng = b->rngs[th];
+            const ModelConfig& mc = b->mc;
+            ready.fetch_add(1);
+            while (ready.load() < threads) std::this_thread::yield();
+            auto t0 = std::chrono::steady_clock::now();
+            for (int rep = 0; rep < reps; ++rep) {
+                std::vector<TokenId> prompt(P);
+                for (auto& t : prompt) t = rng.uniform_int(4, mc.vocab_size - 1);
+                std::vector<std::vector<TokenId>> rs(G, std::vector<TokenId>(R));
+                for (auto& r : rs)
+                    for (auto& t : r) t = rng.uniform_int(4, mc.vocab_size - 1);
+                std::vector<double> rewards(G);
+                for (auto& r : rewards) r = rng.uniform();
+                std::vector<double> adv = group_advantages(rewards);
+                GradBuffer grads(tm.policy);
+                microbatch(tm, prompt, rs, adv, 0.2, 0.04, LossGranularity::token, grads, nullptr, nullptr);
+            }
+            secs[th] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        });
+    }
+    for (auto& t : pool) t.join();
+    double mx = 0.0;
+    for (double v : secs) mx = v > mx ? v : mx;
+    return mx;
+}
+
+void ref_bench_close(void* h) { delete static_cast<RefBench*>(h); }
+
 }  // extern "C"

@@ -1998,7 +1998,8 @@ parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, do
         PARL_CUDA(cudaMemcpyAsync(lse.data(), ctx->scr[0].lse_head.p, T * 4, cudaMemcpyDeviceToHost, ctx->st));
         PARL_CUDA(cudaStreamSynchronize(ctx->st));
         for (int t = 0; t < T; ++t)
-            for (int v = 0; v < V; ++v) rows[(size_t)t * V + v] = (double)z[(size_t)t * V + v] - (double)lse[t];
+            for (int v = 0; v < V; ++v)  // the LSE kernel's own rounding: lp = z - lse in fp32, so a row
+                rows[(size_t)t * V + v] = (double)(z[(size_t)t * V + v] - lse[t]);  // entry == forward_logprobs
     });
 }
 

@@ -8,7 +8,8 @@
 // doctest::Contains.  main() (DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN) runs every
 // case, or the cases named by -tc=<a,b,...>, and prints one line per case:
 //   CASE <PASS|FAIL> <asserts> <failed> <name>
-// followed by the first failed assertions of each failing case.
+// followed by one "FAILED_AT <file>:<line> x<count>" line per failing assertion
+// site and the first failure messages.
 #pragma once
 
 #include <cmath>
@@ -16,6 +17,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <map>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -63,6 +65,7 @@ struct State {
     long asserts = 0, failed = 0;
     std::vector<std::string> msgs;
     std::vector<std::string> info;
+    std::map<std::string, long> sites;
 };
 inline State& state() {
     static State s;
@@ -74,6 +77,7 @@ inline void record(bool ok, const char* file, int line, const char* what, bool r
     ++s.asserts;
     if (ok) return;
     ++s.failed;
+    ++s.sites[std::string(file) + ":" + std::to_string(line)];
     if (s.msgs.size() < 8) {
         std::string m = std::string(file) + ":" + std::to_string(line) + ": " + what;
         for (const auto& i : s.info) m += "  [" + i + "]";
@@ -186,6 +190,7 @@ int main(int argc, char** argv) {
             s.msgs.push_back("unexpected exception");
         }
         std::printf("CASE %s %ld %ld %s\n", s.failed ? "FAIL" : "PASS", s.asserts, s.failed, c.name);
+        for (const auto& [site, n] : s.sites) std::printf("    FAILED_AT %s x%ld\n", site.c_str(), n);
         for (const auto& m : s.msgs) std::printf("    %s\n", m.c_str());
         std::fflush(stdout);
         n_fail += s.failed ? 1 : 0;

@@ -371,3 +371,16 @@ def test_model_copy_keeps_init_seed(P, ctx32, tmp_path):
     p.save(str(tmp_path / "a.ckpt"))
     q.save(str(tmp_path / "b.ckpt"))
     assert (tmp_path / "a.ckpt").read_bytes() == (tmp_path / "b.ckpt").read_bytes()
+
+
+def test_logprob_rows_normalized(P, ctx32):
+    """test_model.cpp:72-93 at fp32: rows normalised, log-probs <= 0, and a forward_logprobs value
+    equals its forward_logprob_rows entry bit for bit (the same LSE kernel and rounding)."""
+    cfg = P.ModelConfig(16, 16, 2, 2, 24, 32)
+    p = P.ModelParams.init(cfg, 3, ctx32)
+    tokens = [1, 5, 9, 4, 2]
+    rows = P.forward_logprob_rows(p, tokens, np.arange(5), P.AttentionMaskSpec.causal())
+    assert np.abs(np.exp(rows).sum(1) - 1).max() < 1e-5 and rows.max() <= 0
+    labels = [-1, -1, 9, -1, -1]
+    out = P.forward_logprobs(p, tokens, np.arange(5), P.AttentionMaskSpec.causal(), labels)
+    assert out.logprobs[0] == rows[1, 9]
