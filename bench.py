@@ -4,9 +4,11 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
-A step = every rank processes `groups_per_rank` prompt groups (pack -> tri-model
-forward -> GRPO loss -> policy backward -> accumulate), then the gradient and the
-loss scalars are allreduced over NCCL (N>1).  Weak scaling: per-GPU work is fixed.
+A step = one global batch of prompt groups (C2 N=64 groups), split
+over the ranks (pack -> tri-model forward -> GRPO loss -> policy backward ->
+accumulate per group), then the gradient and the loss scalars are allreduced over
+NCCL (N>1).  Strong scaling: the global batch is fixed as N grows.  The SGD update
+(set N*G, snapshot, apply_update) is timed separately, outside the metric.
 
 Prints ONE JSON line (rank 0).  `value` = device-resident inputs, CUDA-event
 timed; `e2e` = the same through the public C-ABI from pinned host buffers with
@@ -32,16 +34,16 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # BASELINE.json configs[0]: tiny decoder, fp32 (CPU-runnable oracle case)
-    "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=4),
+    "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=8),
     # BASELINE.json configs[1]: Qwen2.5-0.5B-shaped random-init tri-model, G=8, 512+1k, bf16, single B200
-    "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=2),
+    "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=64),
     # configs[2]: Qwen2.5-7B-shaped tri-model, G=16, 1k prompt + 4k responses (T=66,560 per group),
     # one group per rank (prompt groups sharded over the GPUs); runs with activation recomputation
     "c3": dict(vocab=152064, d=3584, L=28, H=28, F=18944, max_seq=66560, P=1024, G=16, R=4096, prec="bf16",
-               groups=1),
+               groups=16),
     # configs[3]: long-CoT ragged batch, Qwen2.5-1.5B shape, 2k prompt + 8 responses of 1k-16k tokens
     # (SURVEY.md 8d seed: random.Random(20251118).randint(1024, 16384), group 0; T=87,893)
-    "c4": dict(vocab=151936, d=1536, L=28, H=12, F=8960, max_seq=90112, P=2048, G=8, R=None, prec="bf16", groups=1,
+    "c4": dict(vocab=151936, d=1536, L=28, H=12, F=8960, max_seq=90112, P=2048, G=8, R=None, prec="bf16", groups=16,
                lens=[15781, 14233, 10574, 3139, 3977, 14992, 13452, 9697]),
 }
 
@@ -304,14 +306,19 @@ def run_ours(args, c):
     grads = P.GradBuffer(pol)
     hyper = P.HyperParams(0.2, 0.04, "token")
 
-    Pn, G, ng = c["P"], c["G"], args.groups or c["groups"]
+    Pn, G = c["P"], c["G"]
+    n_global = args.groups or c["groups"]  # global batch of prompt groups (strong scaling)
+    mine = list(range(rank, n_global, world))  # this rank's groups (identical global batch at every N)
+    ng = len(mine)
     lens = np.array(group_lens(c), np.int32)
     offs = np.concatenate([[0], np.cumsum(lens)])
     T = Pn + int(lens.sum())
-    rng = np.random.default_rng(123 + rank)
-    prompts = [rng.integers(4, c["vocab"], Pn).astype(np.int32) for _ in range(ng)]
-    resps = [rng.integers(4, c["vocab"], T - Pn).astype(np.int32) for _ in range(ng)]
-    rewards = [rng.random(G) for _ in range(ng)]
+    prompts, resps, rewards = [], [], []
+    for gi in mine:  # per-group seeds: the same synthetic batch however it is split
+        rng = np.random.default_rng([123, gi])
+        prompts.append(rng.integers(4, c["vocab"], Pn).astype(np.int32))
+        resps.append(rng.integers(4, c["vocab"], T - Pn).astype(np.int32))
+        rewards.append(rng.random(G))
     group = P.Group(T, G, ctx)
 
     import torch
@@ -381,11 +388,23 @@ def run_ours(args, c):
     barrier(pg)
     ms_max = allmax(pg, ms)
 
-    # ---- the same K steps again with per-launch CUDA events on the launch
-    # stream for every kernel class (roofline); kept out of `value`.
+    # ---- the SGD update, timed separately (outside the metric): divisor = the
+    # global batch's N*G samples (pipeline.cpp:346-351), snapshot old <- policy, apply_update
+    upd0, upd1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    upd0.record(stream)
+    grads.set_micro_step_count(n_global * G)
+    tm.snapshot_old_policy()
+    tm.policy.apply_update(grads, 1e-4)
+    upd1.record(stream)
+    ctx.sync()
+    update_ms = upd0.elapsed_time(upd1)
+
+    # ---- again with per-launch CUDA events on the launch stream for every kernel class
+    # (roofline), over min(K, 4) steps; kept out of `value`.
+    prof_steps = min(args.steps, 4)
     ctx.profile(True)
     ctx.sync()
-    for _ in range(args.steps):
+    for _ in range(prof_steps):
         step_device()
     ctx.sync()
     ctx.profile(False)
@@ -403,7 +422,7 @@ def run_ours(args, c):
 
     if rank != 0:
         return
-    tokens_per_step = world * ng * T
+    tokens_per_step = n_global * T
     value = tokens_per_step * args.steps / (ms_max / 1000.0)
     e2e_val = tokens_per_step * args.steps / e2e_max
     hbm, bf16, bf16_sus, src = peaks()
@@ -414,7 +433,7 @@ def run_ours(args, c):
     achieved = dp["work"] / (dp["ms"] / 1000.0) / 1e12 if dp["ms"] > 0 else 0.0
     step_ms = ms_max / args.steps
     traffic, traffic_src = measured_traffic(dom)
-    share = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
+    share = {k: round(v["ms"] / prof_steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
     c["name"] = args.config
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -428,22 +447,24 @@ def run_ours(args, c):
     out = {
         "metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref",
         "value": value, "unit": "packed tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": c["prec"], "data": "synthetic (random-init weights, uniform tokens in [4,V), U[0,1) rewards)",
         "config": {"workload": f"{args.config}: d={c['d']} H={c['H']} L={c['L']} F={c['F']} V={c['vocab']}, "
-                               f"P={Pn} G={G} R={c['R'] or lens.tolist()} (T={T}) x {ng} groups per rank per step",
-                   "groups_per_rank": ng, "packed_tokens_per_group": T,
+                               f"P={Pn} G={G} R={c['R'] or lens.tolist()} (T={T}); global batch {n_global} groups "
+                               f"per step, {ng} on rank 0",
+                   "global_groups": n_global, "groups_per_rank": ng, "packed_tokens_per_group": T,
                    "l2": "working set (weights+activations, GBs) exceeds the 126 MB L2; no explicit flush",
-                   "roofline_timing": "per-launch CUDA events over a second identical K-step region",
+                   "roofline_timing": f"per-launch CUDA events over {prof_steps} further identical steps",
+                   "update_ms": update_ms,
                    "parallelism": f"dp{world} over prompt groups"},
-        "e2e": {"value": e2e_val, "unit": "packed tokens/s", "h2d_bytes_per_step": ng * (T * 4 + G * 8),
+        "e2e": {"value": e2e_val, "unit": "packed tokens/s", "h2d_bytes_per_step": ng * (T * 4 + G * 8 + G * 4),
                 "d2h_bytes_per_step": 40},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": achieved / bf16_sus, "peak_kind": f"{src} bf16 sustained",
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, read + write)",
                      "traffic_source": traffic_src, "share_of_step": share},
-        "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+        "kernel_classes": {k: {"ms_per_step": v["ms"] / prof_steps, "launches_per_step": v["launches"] / prof_steps,
                                "achieved": (v["work"] / (v["ms"] / 1e3) / (1e12 if k in tc else 1e9))
                                if v["ms"] > 0 else None,
                                "unit": "TFLOP/s" if k in ("gemm", "head", "attn_fwd", "attn_bwd") else "GB/s"}

@@ -100,7 +100,8 @@ typedef enum {
     PARL_KC_LOSS = 4,      /* K7 GRPO loss */
     PARL_KC_PACK = 5,      /* K1 packer */
     PARL_KC_NORM = 6,      /* LayerNorm fwd/bwd, embeddings, reductions */
-    PARL_KC_COUNT = 7
+    PARL_KC_SEED = 7,      /* softmax backward seed dZ = u (onehot - softmax) over the policy logits */
+    PARL_KC_COUNT = 8
 } parl_kernel_class;
 parl_status parl_ctx_profile(parl_ctx_t ctx, int enable);
 /* ms = summed event time, work = summed algorithmic FLOPs (or bytes for HBM

@@ -781,22 +781,28 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
         T* dz = c->dz.as<T>((size_t)S * V);
         {
-            ProfScope ps_sm(c, PARL_KC_HEAD, 4.0 * S * (double)V);
             if (act->logits_bf16 && act->recompute) {
                 if constexpr (std::is_same_v<T, bf16>) {
                     // logits were not kept: the same head GEMM rebuilds them (bit-identical)
                     // into dZ, which the softmax backward then overwrites in place
                     GemmArgs ga = head_lse_args(c, m, g, static_cast<const bf16*>(act->hf.p), dz);
-                    PARL_REQUIRE(gemm_tc(ga, st), PARL_E_CUDA, "head recompute: tcgen05 GEMM unavailable");
+                    {
+                        ProfScope ps_h(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
+                        PARL_REQUIRE(gemm_tc(ga, st), PARL_E_CUDA, "head recompute: tcgen05 GEMM unavailable");
+                    }
+                    ProfScope ps_sm(c, PARL_KC_SEED, 4.0 * S * (double)V);  // bf16 z in, bf16 dZ out
                     launch_softmax_bwd<bf16, T>(dz, V, dz, V, S, V, static_cast<float*>(act->lse_head.p), u,
                                                 g->pk.scored_label, st);
                 }
-            } else if (act->logits_bf16)
+            } else if (act->logits_bf16) {
+                ProfScope ps_sm(c, PARL_KC_SEED, 4.0 * S * (double)V);
                 launch_softmax_bwd<bf16, T>(static_cast<bf16*>(act->logits.p), V, dz, V, S, V,
                                             static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
-            else
+            } else {
+                ProfScope ps_sm(c, PARL_KC_SEED, (4.0 + sizeof(T)) * S * (double)V);
                 launch_softmax_bwd<float, T>(static_cast<float*>(act->logits.p), V, dz, V, S, V,
                                              static_cast<float*>(act->lse_head.p), u, g->pk.scored_label, st);
+            }
         }
         T* hf = static_cast<T*>(act->hf.p);
         float* dhf = c->dhf.as<float>((size_t)S * D);
@@ -814,7 +820,10 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         float* dxg = c->dxg.as<float>((size_t)S * D);
         float* xfin = static_cast<float*>(act->xs.p) + TD * NL;
         {
-            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+            // algorithmic bytes: final-LN backward over the S gathered rows (dH, x in, dX out, fp32),
+            // the scatter onto positions (dX rows in, dx out) and the compute-dtype copy of dx
+            ProfScope ps_(c, PARL_KC_NORM,
+                          (double)S * D * 12 + (double)S * D * 4 + (double)Tn * D * 4 + (double)Tn * D * (4 + sizeof(T)));
             launch_layernorm_bwd<T>(dhf, xfin, g->pk.pred_pos, static_cast<float*>(act->lnf_mean.p),
                                     static_cast<float*>(act->lnf_rstd.p), m->W.lnf_g, S, D, nullptr, dxg,
                                     static_cast<T*>(nullptr), G + L.lnf_g, G + L.lnf_b, st);
@@ -917,8 +926,8 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
             add_dw(ga);
         }
         // LN2 (model.cpp:729-730): dmid = dx + LN2^T(dbn), plus its compute-dtype copy
-        {
-            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+        {  // bytes: dy, x, residual grad in (fp32), dx out (fp32) + its compute-dtype copy, per row
+            ProfScope ps_(c, PARL_KC_NORM, (double)Tn * D * (16 + sizeof(T)));
             launch_layernorm_bwd<T>(dbn, xm, nullptr, st4 + 2 * Tn, st4 + 3 * Tn, w.ln2_g, Tn, D, dx, dmid, dmid_act,
                                     G + o.ln2g, G + o.ln2b, st);
         }
@@ -958,7 +967,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         flush_dw();  // dx_act is overwritten next
         // LN1 (model.cpp:820-822): dx <- dmid + LN1^T(da), plus the next layer's compute-dtype copy
         {
-            ProfScope ps_(c, PARL_KC_NORM, 0.0);
+            ProfScope ps_(c, PARL_KC_NORM, (double)Tn * D * (16 + sizeof(T)));
             launch_layernorm_bwd<T>(da, xin, nullptr, st4, st4 + Tn, w.ln1_g, Tn, D, dmid, dx2, dx_act, G + o.ln1g,
                                     G + o.ln1b, st);
         }

@@ -5,8 +5,10 @@ sequence; pipeline.cpp:42-45 keeps a micro-batch inside one group).  Each rank
 holds replicated tri-model weights, runs pack -> tri-model forward -> GRPO loss
 -> backward for the groups assigned to it with no communication, and the only
 exchange per optimizer step is an NCCL allreduce (sum) of the fp32 gradient and
-of the five loss scalars (Pipeline::MicrobatchStats).  The update divisor stays
-the global N*G (pipeline.cpp:350), so every rank applies the identical update.
+of the five loss scalars (Pipeline::MicrobatchStats).  The caller then sets the
+update divisor to the GLOBAL batch's N*G samples (GradBuffer.set_micro_step_count,
+pipeline.cpp:350; parl.train_iteration(world_samples=...)) before apply_update, so
+every rank applies the identical update.
 
 Host-side logic here (no GPU needed, tested with gloo on CPU):
   * group_cost / lpt_assign  : longest-processing-time assignment of ragged

@@ -225,7 +225,7 @@ class Context:
     def launches(self) -> int:
         return LIB.parl_ctx_launches(self.h)
 
-    KC = {"gemm": 0, "head": 1, "attn_fwd": 2, "attn_bwd": 3, "loss": 4, "pack": 5, "norm": 6}
+    KC = {"gemm": 0, "head": 1, "attn_fwd": 2, "attn_bwd": 3, "loss": 4, "pack": 5, "norm": 6, "seed": 7}
 
     def set_recompute(self, mode: int):
         """Activation recomputation: 0 auto, 1 always, 2 never (parl_ctx_set_recompute)."""
