@@ -172,6 +172,19 @@ parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_
 parl_status parl_pack_device(parl_group_t g, const int32_t* d_prompt, int P,
                              const int32_t* d_resp_flat, const int32_t* resp_lens_host, int G,
                              int max_seq_len);
+/* Several prompt groups in ONE packed sequence (f4; SPEC.md:278 lifted): group q is
+ * prompt q (prompt_lens[q] tokens, concatenated in `prompts`) followed by its group_sizes[q]
+ * responses (concatenated in resp_flat, lengths resp_lens[]), each group laid out as
+ * pack_group lays out one (positions restart per group, max_seq_len bounds each group);
+ * attention never crosses groups.  One forward / backward then covers every group; the
+ * GRPO loss takes per-group rewards (equal group sizes) or per-sample advantages. */
+parl_status parl_pack_multi(parl_group_t g, const int32_t* prompts, const int32_t* prompt_lens,
+                            const int32_t* resp_flat, const int32_t* resp_lens, const int32_t* group_sizes, int n,
+                            int max_seq_len);
+/* Device-resident token arrays (lengths on the host). */
+parl_status parl_pack_multi_device(parl_group_t g, const int32_t* d_prompts, const int32_t* prompt_lens,
+                                   const int32_t* d_resp, const int32_t* resp_lens, const int32_t* group_sizes, int n,
+                                   int max_seq_len);
 /* General forward_logprobs input (model.hpp:153-158): arbitrary tokens,
  * positions and self-aligned labels (-1 = unscored) under a causal mask
  * (prompt_len == 0) or a shared-prompt mask (prompt_len, resp_lens[G]).

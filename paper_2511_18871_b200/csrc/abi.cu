@@ -156,6 +156,11 @@ struct parl_ctx_s {
     }
     // activation recomputation: 0 auto (when the stacks do not fit), 1 always, 2 never
     int recompute = 0;
+    // the policy's bf16 logits: 0 keep them for the backward's softmax seed (S x V x 2 B of HBM,
+    // written once, read once), 1 never write them and rebuild them in the backward with the same
+    // head GEMM into dZ (one more 2 S V d contraction); activation recomputation implies 1.
+    // $PARL_HEAD_RECOMPUTE (the A/B of DESIGN.md §4, K8)
+    int head_recompute = 0;
     // activation handle reused by parl_train_microbatch (no per-call allocation)
     parl_act_s* act_cache = nullptr;
     // lifetime: objects created on this context keep it alive
@@ -182,6 +187,52 @@ struct parl_model_s {
     uint64_t epoch = 0;  // bumped by every write of the weights (host mirrors of the drop-in key on it)
 };
 
+// Segment layout of one packed sequence (host): contiguous token ranges, each a prompt or a
+// response of some prompt group, with the shared-prompt visibility rule (model.cpp:242-245)
+// generalised to several groups per sequence: rows of a prompt segment see [A, i], rows of a
+// response see their group's prompt [A, B) and their own prefix [C, i]; keys of a segment are
+// seen by queries up to Q (the group's end for a prompt, the response's end for a response).
+// One group: segment 0 = prompt [0, P), segments 1..G = responses; causal: one prompt [0, T).
+struct SegLayout {
+    std::vector<int> start, end;
+    std::vector<int4> info;  // {A, B (-1: prompt segment), C, Q} == AttnArgs::seg_info
+    int n_groups = 0;
+    void clear() {
+        start.clear();
+        end.clear();
+        info.clear();
+        n_groups = 0;
+    }
+    // appends one group: prompt [p0, p0 + P), then the responses back to back
+    void add_group(int p0, int P, const int* lens, int G) {
+        int t = p0 + P;
+        for (int k = 0; k < G; ++k) t += lens[k];
+        const int gend = t;
+        start.push_back(p0);
+        end.push_back(p0 + P);
+        info.push_back(make_int4(p0, -1, p0, gend));
+        t = p0 + P;
+        for (int k = 0; k < G; ++k) {
+            start.push_back(t);
+            end.push_back(t + lens[k]);
+            info.push_back(make_int4(p0, p0 + P, t, t + lens[k]));
+            t += lens[k];
+        }
+        ++n_groups;
+    }
+    int T() const { return end.empty() ? 0 : end.back(); }
+    // allowed (query, key) pairs: the algorithmic attention work
+    double pairs() const {
+        double s = 0;
+        for (size_t k = 0; k < start.size(); ++k) {
+            const double n = end[k] - start[k];
+            s += n * (n + 1) / 2;
+            if (info[k].y >= 0) s += n * (info[k].y - info[k].x);
+        }
+        return s;
+    }
+};
+
 struct parl_group_s {
     parl_ctx_s* ctx = nullptr;
     int max_T = 0, max_G = 0;
@@ -190,16 +241,19 @@ struct parl_group_s {
     double pairs = 0;  // allowed attention pairs (algorithmic attention work)
     uint64_t epoch = 0;
     PackedDev pk{};
-    DevBuf ints, seg_se, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
+    DevBuf ints, seg_info, cu_d, in_prompt, in_resp, lp, upstream, rewards, adv;
+    SegLayout segs;
     DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf, work_buf;
-    HostStage sched_stage, work_stage, adv_stage;  // pinned staging: async uploads that never block the host
+    HostStage sched_stage, work_stage, adv_stage, multi_stage;  // pinned staging: async uploads, no host block
+    int n_groups = 1, group_G = 0;  // prompt groups in the sequence; responses per group (0: not uniform)
+    DevBuf multi_tab, multi_prompts, multi_resp;
     AttnSched sched;
     SchedHost sched_h;  // host copies of the schedule's tile pointers (work lists)
     int work_H = -1, work_d = -1;
     uint64_t work_epoch = ~0ull;
     uint64_t sorted_epoch = ~0ull;
     std::vector<int> lens, span_start, cu;
-    std::vector<int> sched_key;  // segment structure the schedule was built for
+    std::vector<int> sched_key;  // segment structure (starts) the schedule was built for
     int max_seq = 0, vocab = 0;
     // token-id range of the packed tokens (validate_forward_inputs, model.cpp:413-417): known on
     // the host for host-packed groups, read once from K1's device reduction for device-packed ones
@@ -216,6 +270,7 @@ struct parl_act_s {
     DevBuf xs, xmid, a, qkv, ctxo, bn, pre, actv, stats, lse_attn;  // per-layer stacks
     DevBuf hf, lnf_mean, lnf_rstd, logits, lse_head;
     bool logits_bf16 = false;  // logits stored bf16 by the fused tcgen05 head
+    bool logits_rc = false;    // logits not kept: the backward rebuilds them into dZ (head recompute)
     bool recompute = false;    // only x_0..x_L kept; layers (and bf16 logits) rebuilt in the backward
     int rc_key[3] = {-1, -1, -1};  // shape the automatic recompute decision was made for
     uintptr_t pad_sig[8] = {};  // buffers / sizes the bias columns were filled for
@@ -482,10 +537,8 @@ AttnArgs attn_args(parl_group_s* g, const parl_config& cf) {
     AttnArgs aa;
     aa.T = g->T; aa.H = cf.n_heads; aa.Dh = cf.d_model / cf.n_heads; aa.d = cf.d_model;
     aa.seg = g->pk.seg;
-    aa.seg_start = static_cast<int32_t*>(g->seg_se.p);
-    aa.seg_end = aa.seg_start + (g->max_G + 1);
+    aa.seg_info = static_cast<const int4*>(g->seg_info.p);
     aa.scale = 1.0f / std::sqrt((float)aa.Dh);
-    aa.Peff = g->Peff;
     aa.sched = g->sched;
     aa.ldo = cf.d_model + PAD_COLS;
     aa.item_ctr = static_cast<unsigned*>(g->ctx->item_ctr.p);
@@ -729,7 +782,8 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
                 // tcgen05 head with the vocab log-sum-exp and target gather fused
                 // into the epilogue: logits reach HBM only for the policy (bf16,
                 // kept for the backward unless it recomputes them), never for old/ref.
-                bf16* keep = (ak && !ak->recompute) ? ak->logits.as<bf16>((size_t)S * V) : nullptr;
+                if (ak) ak->logits_rc = ak->recompute || c->head_recompute;
+                bf16* keep = (ak && !ak->logits_rc) ? ak->logits.as<bf16>((size_t)S * V) : nullptr;
                 GemmArgs ga = head_lse_args(c, m, g, hf, keep);
                 {
                     ProfScope ps(c, PARL_KC_HEAD, 2.0 * S * (double)V * D);
@@ -781,7 +835,7 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
         // dZ = u (onehot - softmax) at the head rows (model.cpp:637-650)
         T* dz = c->dz.as<T>((size_t)S * V);
         {
-            if (act->logits_bf16 && act->recompute) {
+            if (act->logits_bf16 && act->logits_rc) {
                 if constexpr (std::is_same_v<T, bf16>) {
                     // logits were not kept: the same head GEMM rebuilds them (bit-identical)
                     // into dZ, which the softmax backward then overwrites in place
@@ -989,28 +1043,48 @@ void backward_impl(parl_ctx_s* c, parl_model_s* m, parl_act_s* act, parl_group_s
     }
 }
 
-// Host-side attention tile schedule (see AttnSched in kernels.cuh): the same
-// visibility rule as the shared-prompt mask (model.cpp:242-245) at tile level.
-AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const std::vector<int>& lens, DevBuf& buf,
-                         HostStage& stage, cudaStream_t st, SchedHost* host_out = nullptr) {
+// Host-side attention tile schedule (see AttnSched in kernels.cuh): the visibility rule of
+// SegLayout (model.cpp:242-245, per prompt group) at 128 x 128 tile level.  The rows of a
+// query tile fall into at most a few segments ("pieces"); a key tile is visible when some
+// piece sees one of its keys and full (no per-element mask) when every row sees all of them.
+AttnSched build_schedule(const SegLayout& L, DevBuf& buf, HostStage& stage, cudaStream_t st,
+                         SchedHost* host_out = nullptr) {
+    const int T = L.T();
     const int nt = (T + 127) / 128;
-    auto seg_at = [&](int i) -> int {
-        if (i < Peff) return 0;
-        int k = (int)(std::upper_bound(starts.begin(), starts.end(), i) - starts.begin()) - 1;
-        return k + 1;
+    struct Piece {
+        int s, r0, r1;  // segment, rows [r0, r1)
     };
-    auto visible = [&](int i0, int i1, int j0, int j1) {
-        if (j0 > i1 - 1) return false;
-        if (j0 < Peff) return true;
-        const int sq_lo = seg_at(i0), sq_hi = seg_at(i1 - 1), sk_lo = seg_at(j0), sk_hi = seg_at(j1 - 1);
-        return sq_hi >= 1 && std::max(sq_lo, sk_lo) <= std::min(sq_hi, sk_hi);
+    std::vector<std::vector<Piece>> pieces(nt);
+    for (size_t s = 0; s < L.start.size(); ++s)
+        for (int r = L.start[s]; r < L.end[s];) {
+            const int qt = r / 128, r1 = std::min(L.end[s], (qt + 1) * 128);
+            pieces[qt].push_back({(int)s, r, r1});
+            r = r1;
+        }
+    // rows [r0, r1) of segment s against keys [j0, j1)
+    auto piece_visible = [&](const Piece& p, int j0, int j1) {
+        const int4 f = L.info[p.s];
+        if (f.y < 0) return std::max(f.x, j0) <= std::min(p.r1 - 1, j1 - 1);  // [A, i]
+        return std::max(f.x, j0) < std::min(f.y, j1) || std::max(f.z, j0) <= std::min(p.r1 - 1, j1 - 1);
     };
-    auto full = [&](int i0, int i1, int j0) {
+    auto piece_full = [&](const Piece& p, int j0, int j1) {  // the piece's first row sees the least
+        const int4 f = L.info[p.s];
+        if (f.y < 0) return f.x <= j0 && j1 - 1 <= p.r0;
+        if (f.z <= f.y)  // prompt and own prefix touch: one range [A, max(B, r0 + 1))
+            return f.x <= j0 && j1 <= std::max(f.y, p.r0 + 1);
+        return (f.x <= j0 && j1 <= f.y) || (f.z <= j0 && j1 - 1 <= p.r0);
+    };
+    auto visible = [&](int qt, int j0, int j1) {
+        for (const auto& p : pieces[qt])
+            if (piece_visible(p, j0, j1)) return true;
+        return false;
+    };
+    auto full = [&](int qt, int j0) {
         const int j1 = j0 + 128;
-        if (j1 > T || i1 - i0 < 128) return false;
-        if (j1 <= Peff) return seg_at(i0) >= 1 || j1 - 1 <= i0;
-        const int s = seg_at(j0);
-        return s >= 1 && seg_at(j1 - 1) == s && seg_at(i0) == s && seg_at(i1 - 1) == s && j1 - 1 <= i0;
+        if (j1 > T || (qt + 1) * 128 > T) return false;
+        for (const auto& p : pieces[qt])
+            if (!piece_full(p, j0, j1)) return false;
+        return true;
     };
     std::vector<int32_t> q_ptr(nt + 1, 0), q_list, k_ptr(nt + 1, 0), k_list;
     std::vector<std::vector<int32_t>> per_k(nt);
@@ -1018,8 +1092,8 @@ AttnSched build_schedule(int T, int Peff, const std::vector<int>& starts, const 
         const int i0 = qt * 128, i1 = std::min(T, i0 + 128);
         for (int kt = 0; kt <= (i1 - 1) / 128; ++kt) {
             const int j0 = kt * 128, j1 = std::min(T, j0 + 128);
-            if (!visible(i0, i1, j0, j1)) continue;
-            const int32_t e = (full(i0, i1, j0) ? (1 << 30) : 0);
+            if (!visible(qt, j0, j1)) continue;
+            const int32_t e = (full(qt, j0) ? (1 << 30) : 0);
             q_list.push_back(kt | e);
             per_k[kt].push_back(qt | e);
         }
@@ -1209,7 +1283,7 @@ void alloc_group_arrays(parl_group_s* g) {
     g->pk.pred_pos = base + 7 * (size_t)T;
     g->pk.sample_of = base + 8 * (size_t)T;
     g->pk.row_idx = base + 9 * (size_t)T;
-    g->seg_se.as<int32_t>(2 * (size_t)(G + 1));               // segment [start, end) bounds
+    g->seg_info.as<int4>((size_t)G + 1);                       // per-segment visibility (SegLayout)
     g->pk.row_ptr = g->cu_d.as<int32_t>((size_t)g->max_T + 1 + (G + 1));  // row_ptr [T+1] | cu [G+1]
     g->lp.as<float>((size_t)3 * T);
     g->upstream.as<float>(T);
@@ -1219,25 +1293,19 @@ void alloc_group_arrays(parl_group_s* g) {
 
 int32_t* group_cu(parl_group_s* g) { return static_cast<int32_t*>(g->cu_d.p) + g->max_T + 1; }
 
-// upload segment bounds / response offsets computed on the host
+// upload the segment layout / response offsets computed on the host
 void upload_meta(parl_group_s* g) {
-    std::vector<int32_t> se(2 * (size_t)(g->max_G + 1), 0);
-    se[0] = 0;
-    se[g->max_G + 1] = g->Peff;
-    for (int k = 0; k < g->G; ++k) {
-        se[k + 1] = g->span_start[k];
-        se[g->max_G + 1 + k + 1] = g->span_start[k] + g->lens[k];
-    }
-    PARL_CUDA(cudaMemcpyAsync(g->seg_se.p, se.data(), se.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
+    const SegLayout& L = g->segs;
+    int4* si = g->seg_info.as<int4>(L.info.size());
+    PARL_CUDA(cudaMemcpyAsync(si, L.info.data(), L.info.size() * sizeof(int4), cudaMemcpyHostToDevice, g->ctx->st));
     PARL_CUDA(cudaMemcpyAsync(group_cu(g), g->cu.data(), g->cu.size() * 4, cudaMemcpyHostToDevice, g->ctx->st));
     // the tile schedule and the attention work lists depend only on the segment structure:
     // a group re-packed with the same lengths (every step of a fixed-shape run) keeps them
-    std::vector<int> key = {g->T, g->Peff, g->G};
-    key.insert(key.end(), g->lens.begin(), g->lens.end());
-    key.insert(key.end(), g->span_start.begin(), g->span_start.end());
+    std::vector<int> key = L.start;
+    key.insert(key.end(), L.end.begin(), L.end.end());
+    for (const auto& f : L.info) key.insert(key.end(), {f.x, f.y, f.z, f.w});
     if (key == g->sched_key && g->sched.q_ptr) return;
-    g->sched = build_schedule(g->T, g->Peff, g->span_start, g->lens, g->sched_buf, g->sched_stage, g->ctx->st,
-                              &g->sched_h);
+    g->sched = build_schedule(L, g->sched_buf, g->sched_stage, g->ctx->st, &g->sched_h);
     g->sched_key = std::move(key);
     g->work_H = -1;
 }
@@ -1273,8 +1341,11 @@ void set_pack_meta(parl_group_s* g, int P, const int32_t* lens, int G, int max_s
     g->T = t;
     g->S = t - P;
     g->Peff = P;
-    g->pairs = 0.5 * P * (P + 1.0);
-    for (int k = 0; k < G; ++k) g->pairs += (double)lens[k] * P + 0.5 * lens[k] * (lens[k] + 1.0);
+    g->n_groups = 1;
+    g->group_G = G;
+    g->segs.clear();
+    g->segs.add_group(0, P, lens, G);
+    g->pairs = g->segs.pairs();
     g->max_seq = max_seq;
     g->epoch++;
 }
@@ -1299,6 +1370,7 @@ parl_status parl_ctx_create(int device, parl_precision prec, parl_ctx_t* out) {
         PARL_CUDA(cudaMemsetAsync(s, 0, 8 * sizeof(double), c->st));
         PARL_CUDA(cudaMemsetAsync(c->item_ctr.as<unsigned>(4), 0, 4 * sizeof(unsigned), c->st));
         if (const char* e = std::getenv("PARL_RECOMPUTE")) c->recompute = std::atoi(e);
+        if (const char* e = std::getenv("PARL_HEAD_RECOMPUTE")) c->head_recompute = std::atoi(e) != 0;
         PARL_REQUIRE(c->recompute >= 0 && c->recompute <= 2, PARL_E_CONFIG, "PARL_RECOMPUTE must be 0, 1 or 2");
         *out = c.release();
     });
@@ -1747,6 +1819,115 @@ parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_
     });
 }
 
+// ---- several prompt groups per packed sequence (f4) -------------------------------
+namespace {
+// validate each group as pack_group does (packing.cpp:7-19; positions restart per group, so
+// max_seq_len bounds every group's own packed length), then set the host meta and return the
+// K1 tables gstart [n+1] | pstart [n] | r0 [n+1] | rcu [R+1] | rstart [R]
+std::vector<int32_t> set_multi_meta(parl_group_s* g, const int32_t* prompt_lens, const int32_t* resp_lens,
+                                    const int32_t* group_sizes, int n, int max_seq) {
+    PARL_REQUIRE(n >= 1, PARL_E_SHAPE, "pack: no prompt groups");
+    long T = 0;
+    int R = 0, uniform = group_sizes[0];
+    for (int q = 0; q < n; ++q) {
+        const int P = prompt_lens[q], G = group_sizes[q];
+        PARL_REQUIRE(P >= 1, PARL_E_SHAPE, "pack_group: empty prompt");
+        PARL_REQUIRE(G >= 1, PARL_E_SHAPE, "pack_group: no responses");
+        long tg = P;
+        for (int k = 0; k < G; ++k) {
+            PARL_REQUIRE(resp_lens[R + k] >= 1, PARL_E_SHAPE, "pack_group: empty response");
+            tg += resp_lens[R + k];
+        }
+        PARL_REQUIRE(tg <= max_seq, PARL_E_SHAPE,
+                     "pack_group: packed length " + std::to_string(tg) + " for group of " + std::to_string(G) +
+                         " responses exceeds max_seq_len " + std::to_string(max_seq));
+        T += tg;
+        R += G;
+        if (G != uniform) uniform = 0;
+    }
+    PARL_REQUIRE(T <= g->max_T && R <= g->max_G, PARL_E_SHAPE,
+                 "packed groups exceed the capacity this group was created with");
+    std::vector<int32_t> gstart(n + 1), pstart(n), r0(n + 1), rcu(R + 1), rstart(R);
+    g->segs.clear();
+    g->lens.assign(resp_lens, resp_lens + R);
+    g->span_start.assign(R, 0);
+    int t = 0, po = 0, k = 0;
+    rcu[0] = 0;
+    for (int q = 0; q < n; ++q) {
+        gstart[q] = t;
+        pstart[q] = po;
+        r0[q] = k;
+        g->segs.add_group(t, prompt_lens[q], resp_lens + k, group_sizes[q]);
+        t += prompt_lens[q];
+        po += prompt_lens[q];
+        for (int j = 0; j < group_sizes[q]; ++j, ++k) {
+            rstart[k] = t;
+            g->span_start[k] = t;
+            rcu[k + 1] = rcu[k] + resp_lens[k];
+            t += resp_lens[k];
+        }
+    }
+    gstart[n] = t;
+    r0[n] = R;
+    g->T = t;
+    g->S = rcu[R];
+    g->P = prompt_lens[0];
+    g->G = R;
+    g->n_samples = R;
+    g->n_groups = n;
+    g->group_G = uniform;
+    g->Peff = n == 1 ? prompt_lens[0] : 0;
+    g->cu.assign(rcu.begin(), rcu.end());
+    g->pairs = g->segs.pairs();
+    g->max_seq = max_seq;
+    g->epoch++;
+    std::vector<int32_t> tab;
+    for (const auto* v : {&gstart, &pstart, &r0, &rcu, &rstart}) tab.insert(tab.end(), v->begin(), v->end());
+    return tab;
+}
+
+void pack_multi_launch(parl_group_s* g, const int32_t* d_prompts, const int32_t* d_resp, const std::vector<int32_t>& tab,
+                       unsigned* id_max) {
+    upload_meta(g);
+    int32_t* d_tab = g->multi_tab.as<int32_t>(tab.size());
+    g->multi_stage.upload(d_tab, tab.data(), tab.size() * 4, g->ctx->st);
+    ProfScope ps(g->ctx, PARL_KC_PACK, 28.0 * g->T + 20.0 * g->S);
+    launch_pack_multi(d_prompts, d_resp, d_tab, g->n_groups, g->G, g->T, g->pk, id_max, g->ctx->st);
+    check_launch();
+}
+}  // namespace
+
+parl_status parl_pack_multi(parl_group_t g, const int32_t* prompts, const int32_t* prompt_lens,
+                            const int32_t* resp_flat, const int32_t* resp_lens, const int32_t* group_sizes, int n,
+                            int max_seq) {
+    return guarded(g->ctx, [&] {
+        auto tab = set_multi_meta(g, prompt_lens, resp_lens, group_sizes, n, max_seq);
+        long np = 0;
+        for (int q = 0; q < n; ++q) np += prompt_lens[q];
+        unsigned umax = 0;
+        for (long i = 0; i < np; ++i) umax = std::max(umax, (unsigned)prompts[i]);
+        for (long i = 0; i < g->S; ++i) umax = std::max(umax, (unsigned)resp_flat[i]);
+        g->tok_max = (int)std::min<unsigned>(umax, INT32_MAX);
+        g->tok_range_dev = false;
+        cudaStream_t st = g->ctx->st;
+        int32_t* dp = g->multi_prompts.as<int32_t>(np);
+        int32_t* dr = g->multi_resp.as<int32_t>(g->S);
+        PARL_CUDA(cudaMemcpyAsync(dp, prompts, (size_t)np * 4, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaMemcpyAsync(dr, resp_flat, (size_t)g->S * 4, cudaMemcpyHostToDevice, st));
+        pack_multi_launch(g, dp, dr, tab, nullptr);
+    });
+}
+
+parl_status parl_pack_multi_device(parl_group_t g, const int32_t* d_prompts, const int32_t* prompt_lens,
+                                   const int32_t* d_resp, const int32_t* resp_lens, const int32_t* group_sizes, int n,
+                                   int max_seq) {
+    return guarded(g->ctx, [&] {
+        auto tab = set_multi_meta(g, prompt_lens, resp_lens, group_sizes, n, max_seq);
+        pack_multi_launch(g, d_prompts, d_resp, tab, g->tok_range.as<unsigned>(1));
+        g->tok_range_dev = true;
+    });
+}
+
 parl_status parl_pack_device(parl_group_t g, const int32_t* d_prompt, int P, const int32_t* d_resp,
                              const int32_t* lens, int G, int max_seq) {
     return guarded(g->ctx, [&] {
@@ -1827,8 +2008,11 @@ parl_status parl_set_sequence(parl_group_t g, const int32_t* tokens, const int32
         g->T = T;
         g->P = prompt_len;
         g->G = prompt_len > 0 ? G : 0;
-        g->pairs = 0.5 * Peff * (Peff + 1.0);
-        for (int k = 0; k < g->G; ++k) g->pairs += (double)resp_lens[k] * Peff + 0.5 * resp_lens[k] * (resp_lens[k] + 1.0);
+        g->segs.clear();
+        g->segs.add_group(0, Peff, prompt_len > 0 ? resp_lens : nullptr, g->G);
+        g->pairs = g->segs.pairs();
+        g->n_groups = 1;
+        g->group_G = std::max(g->G, 1);
         g->S = S;
         g->Peff = Peff;
         g->n_samples = std::max(G, 1);
@@ -1984,6 +2168,7 @@ parl_status parl_logprob_rows(parl_ctx_t ctx, parl_model_t m, parl_group_t g, do
         rp[T] = T;
         tmp.T = T; tmp.P = g->P; tmp.G = g->G; tmp.S = T; tmp.Peff = g->Peff; tmp.n_samples = 1;
         tmp.lens = g->lens; tmp.span_start = g->span_start; tmp.cu = {0, T};
+        tmp.segs = g->segs;
         tmp.vocab = V; tmp.max_seq = m->cfg.max_seq_len;
         auto up = [&](int32_t* dst, const void* src, size_t n) {
             PARL_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, ctx->st));
@@ -2069,6 +2254,8 @@ parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* pr
             g.T = T; g.P = T; g.G = 0; g.S = 1; g.Peff = T; g.n_samples = 1;
             g.pairs = (double)T * (T + 1) / 2;
             g.lens.clear(); g.span_start.clear(); g.cu = {0, 1};
+            g.segs.clear();
+            g.segs.add_group(0, T, nullptr, 0);
             g.vocab = V; g.max_seq = c.max_seq_len;
             ++g.epoch;
             upload_meta(&g);
@@ -2136,12 +2323,14 @@ parl_status parl_grpo_loss(parl_ctx_t ctx, parl_group_t g, const double* rewards
         a.cu = group_cu(g);
         a.S = g->S;
         a.n = G;
-        if (rewards) {  // group_advantages[_mean_only] over the group's G rewards (grpo.cpp:24-48)
-            PARL_REQUIRE(G >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
+        if (rewards) {  // group_advantages[_mean_only] over each group's rewards (grpo.cpp:24-48)
+            const int gs = g->n_groups > 1 ? g->group_G : G;
+            PARL_REQUIRE(gs > 0, PARL_E_CONFIG, "rewards need groups of equal size; pass advantages instead");
+            PARL_REQUIRE(gs >= 2, PARL_E_CONFIG, "group_advantages needs G >= 2 rewards");
             double* r = g->rewards.as<double>(G);
             g->adv_stage.upload(r, rewards, G * sizeof(double), st);
             a.rewards = r;
-            a.group_size = G;
+            a.group_size = gs;
             a.mean_only = hp->advantage_mean_only;
         } else {
             for (int k = 0; k < G; ++k)  // per_sample_terms: require_finite(advantage), grpo.cpp:117
@@ -2724,56 +2913,65 @@ extern "C" parl_status parl_debug_gemm_bf16(int path, int M, int N, int K, const
     });
 }
 
+namespace {
+// The debug hooks' layout: one group from the device seg_start / seg_end arrays the tests pass
+// ([prompt, r1, ..] when Peff < T, else a causal sequence), its seg_info and tile schedule /
+// work lists (cached across the timing loops' repeated calls of one shape).
+struct DebugLayout {
+    DevBuf info, sched, work;
+    HostStage stage, wstage;
+    AttnSched cached;
+    long key[5] = {-1, -1, -1, -1, -1};
+};
+
+void debug_layout(DebugLayout& D, AttnArgs& aa, int path, int T, int H, int Dh, int Peff, const int32_t* seg_start,
+                  const int32_t* seg_end) {
+    const long k5[5] = {T, Peff, (long)(uintptr_t)seg_start, (long)(uintptr_t)seg_end, H};
+    if (path == 2 && std::memcmp(D.key, k5, sizeof(k5)) == 0) {  // timing loops reuse the schedule
+        aa.sched = D.cached;
+        aa.seg_info = static_cast<const int4*>(D.info.p);
+        return;
+    }
+    std::vector<int> lens;
+    if (Peff < T) {  // count the responses: walk the segment ends until T
+        std::vector<int32_t> s1(T + 1), e1(T + 1);
+        int n = 1;
+        while (true) {
+            PARL_CUDA(cudaMemcpy(e1.data() + n - 1, seg_end + n - 1, 4, cudaMemcpyDeviceToHost));
+            if (e1[n - 1] >= T) break;
+            ++n;
+        }
+        PARL_CUDA(cudaMemcpy(s1.data(), seg_start, 4 * n, cudaMemcpyDeviceToHost));
+        for (int k = 1; k < n; ++k) lens.push_back(e1[k] - s1[k]);
+    }
+    SegLayout L;
+    L.add_group(0, Peff, lens.data(), (int)lens.size());
+    int4* si = D.info.as<int4>(L.info.size());
+    PARL_CUDA(cudaMemcpy(si, L.info.data(), L.info.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    aa.seg_info = si;
+    SchedHost hs;
+    aa.sched = build_schedule(L, D.sched, D.stage, 0, &hs);
+    build_attn_work(aa.sched, hs, H, H * Dh, D.work, D.wstage, 0);
+    D.cached = aa.sched;
+    std::memcpy(D.key, k5, sizeof(k5));
+}
+}  // namespace
+
 extern "C" parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
                                             const int32_t* seg_start, const int32_t* seg_end, const void* qkv,
                                             void* out, float* lse) {
     return guarded(nullptr, [&] {
         AttnArgs aa;
-        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
-        aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
+        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh;
+        aa.seg = seg;
         aa.scale = 1.0f / std::sqrt((float)Dh);
         static DevBuf dbg_ctr;
         static unsigned dbg_base = 0;
         if (!dbg_ctr.p) PARL_CUDA(cudaMemset(dbg_ctr.as<unsigned>(4), 0, 4 * sizeof(unsigned)));
         aa.item_ctr = static_cast<unsigned*>(dbg_ctr.p);
         aa.item_base = &dbg_base;
-        static DevBuf dbg_sched;
-        static HostStage dbg_stage;
-        static AttnSched cached;
-        static long key[4] = {-1, -1, -1, -1};
-        const long k4[4] = {T, Peff, (long)(uintptr_t)seg_start, (long)(uintptr_t)seg_end};
-        if (path == 2 && std::memcmp(key, k4, sizeof(k4)) == 0) {  // timing loops reuse the schedule
-            aa.sched = cached;
-        } else {
-            int G = 0;
-            std::vector<int32_t> st_h, en_h;
-            if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
-                G = 0;
-                std::vector<int32_t> tmp(2 * (T + 1));
-                PARL_CUDA(cudaMemcpy(tmp.data(), seg_end, 4, cudaMemcpyDeviceToHost));
-                // count responses: walk ends until T
-                std::vector<int32_t> s1(T + 1), e1(T + 1);
-                int n = 1;
-                while (true) {
-                    PARL_CUDA(cudaMemcpy(e1.data() + n - 1, seg_end + n - 1, 4, cudaMemcpyDeviceToHost));
-                    if (e1[n - 1] >= T) break;
-                    ++n;
-                }
-                PARL_CUDA(cudaMemcpy(s1.data(), seg_start, 4 * n, cudaMemcpyDeviceToHost));
-                for (int k = 1; k < n; ++k) {
-                    st_h.push_back(s1[k]);
-                    en_h.push_back(e1[k] - s1[k]);
-                }
-            }
-            std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            SchedHost hs;
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
-            static DevBuf dbg_work;
-            static HostStage dbg_wstage;
-            build_attn_work(aa.sched, hs, H, H * Dh, dbg_work, dbg_wstage, 0);
-            cached = aa.sched;
-            std::memcpy(key, k4, sizeof(k4));
-        }
+        static DebugLayout D;
+        debug_layout(D, aa, path, T, H, Dh, Peff, seg_start, seg_end);
         if (path == 0 || path == 2) {  // 2: no device sync (timing loops)
             PARL_REQUIRE(attn_fwd_tc(aa, static_cast<const bf16*>(qkv), static_cast<bf16*>(out), lse, 0), PARL_E_CONFIG,
                          "head dim not supported by the tcgen05 attention");
@@ -2791,46 +2989,11 @@ extern "C" parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, 
                                                 void* dqkv) {
     return guarded(nullptr, [&] {
         AttnArgs aa;
-        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh; aa.Peff = Peff;
-        aa.seg = seg; aa.seg_start = seg_start; aa.seg_end = seg_end;
+        aa.T = T; aa.H = H; aa.Dh = Dh; aa.d = H * Dh;
+        aa.seg = seg;
         aa.scale = 1.0f / std::sqrt((float)Dh);
-        static DevBuf dbg_sched;
-        static HostStage dbg_stage;
-        static AttnSched cached;
-        static long key[4] = {-1, -1, -1, -1};
-        const long k4[4] = {T, Peff, (long)(uintptr_t)seg_start, (long)(uintptr_t)seg_end};
-        if (path == 2 && std::memcmp(key, k4, sizeof(k4)) == 0) {  // timing loops reuse the schedule
-            aa.sched = cached;
-        } else {
-            int G = 0;
-            std::vector<int32_t> st_h, en_h;
-            if (Peff < T) {  // responses present: seg_start/seg_end hold [prompt, r1, ..]
-                G = 0;
-                std::vector<int32_t> tmp(2 * (T + 1));
-                PARL_CUDA(cudaMemcpy(tmp.data(), seg_end, 4, cudaMemcpyDeviceToHost));
-                // count responses: walk ends until T
-                std::vector<int32_t> s1(T + 1), e1(T + 1);
-                int n = 1;
-                while (true) {
-                    PARL_CUDA(cudaMemcpy(e1.data() + n - 1, seg_end + n - 1, 4, cudaMemcpyDeviceToHost));
-                    if (e1[n - 1] >= T) break;
-                    ++n;
-                }
-                PARL_CUDA(cudaMemcpy(s1.data(), seg_start, 4 * n, cudaMemcpyDeviceToHost));
-                for (int k = 1; k < n; ++k) {
-                    st_h.push_back(s1[k]);
-                    en_h.push_back(e1[k] - s1[k]);
-                }
-            }
-            std::vector<int> sv(st_h.begin(), st_h.end()), lv(en_h.begin(), en_h.end());
-            SchedHost hs;
-            aa.sched = build_schedule(T, Peff, sv, lv, dbg_sched, dbg_stage, 0, &hs);
-            static DevBuf dbg_work;
-            static HostStage dbg_wstage;
-            build_attn_work(aa.sched, hs, H, H * Dh, dbg_work, dbg_wstage, 0);
-            cached = aa.sched;
-            std::memcpy(key, k4, sizeof(k4));
-        }
+        static DebugLayout D;
+        debug_layout(D, aa, path, T, H, Dh, Peff, seg_start, seg_end);
         const bf16* q = static_cast<const bf16*>(qkv);
         if (path == 0 || path == 2) {  // 2: no device sync (timing loops)
             PARL_REQUIRE(attn_bwd_tc(aa, q, static_cast<const bf16*>(out), static_cast<const bf16*>(dout), lse, dsum,

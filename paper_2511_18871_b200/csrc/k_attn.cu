@@ -5,10 +5,11 @@
 // (model.cpp:242-245) makes every row's allowed set a union of at most two
 // contiguous ranges, so masked pairs are never visited (no -inf masking, no
 // leakage: a response's result cannot depend on another response's values).
-//   query i in the prompt  (seg 0): keys [0, i]
-//   query i in response k  (seg k): keys [0, P) and [start_k, i]
-//   key j in the prompt           : queries [j, T)
-//   key j in response k           : queries [j, end_k)
+//   query i in a prompt            : keys [group start, i]
+//   query i in response k          : keys [its group's prompt) and [start_k, i]
+//   key j in a prompt              : queries [j, group end)
+//   key j in response k            : queries [j, end_k)
+// (AttnArgs::seg_info; one group: the prompt is [0, P) and the group ends at T)
 // Forward saves only the per-row log-sum-exp (no T x T probabilities); the
 // backward recomputes probabilities and is deterministic (dQ and dK/dV are
 // produced by separate row-owning passes, no float atomics).
@@ -27,12 +28,12 @@ struct Ranges {
 };
 
 __device__ __forceinline__ Ranges key_ranges(const AttnArgs& a, int i) {
-    const int s = a.seg[i];
+    const int4 f = a.seg_info[a.seg[i]];
     Ranges r;
-    if (s == 0) {
-        r.b0 = 0; r.e0 = i + 1; r.b1 = 0; r.e1 = 0;
-    } else {
-        r.b0 = 0; r.e0 = a.seg_end[0]; r.b1 = a.seg_start[s]; r.e1 = i + 1;
+    if (f.y < 0) {  // prompt row: its group's prompt prefix
+        r.b0 = f.x; r.e0 = i + 1; r.b1 = 0; r.e1 = 0;
+    } else {        // response row: its group's prompt, then its own prefix
+        r.b0 = f.x; r.e0 = f.y; r.b1 = f.z; r.e1 = i + 1;
     }
     return r;
 }
@@ -189,8 +190,7 @@ __global__ void __launch_bounds__(WPB * 32) k_attn_bwd_dkv(AttnArgs a, const T* 
         vs[e] = to_f<T>(qkv[(long)j * ld + 2 * a.d + h * Dh + e]);
     }
     __syncwarp();
-    const int sj = a.seg[j];
-    const int ie = sj == 0 ? a.T : a.seg_end[sj];
+    const int ie = a.seg_info[a.seg[j]].w;  // queries [j, ie) see key j
     float dk[MAXE] = {0.f, 0.f, 0.f, 0.f}, dv[MAXE] = {0.f, 0.f, 0.f, 0.f};
     for (int i0 = j; i0 < ie; i0 += 32) {
         const int i = i0 + lane;

@@ -47,9 +47,9 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 // TMEM: S0 | S1 | O0 | O1 | P0 | P1  (128 | 128 | 64 | 64 | 64 | 64 columns) at Dh = 64;
 // S0 | S1 | O0 | O1 (128 each, P_w over S_w) at Dh = 128.
 struct AttnPairArgs {
-    int T, H, d, Peff, grid;
+    int T, H, d, grid;
     const int32_t* seg;
-    const int32_t* seg_start;
+    const int4* seg_info;
     const int32_t *p_ptr, *p_list;
     const int32_t *w_ptr, *w_items;  // per-CTA item lists (item = pair * H + head)
     // dynamic work queue (dyn): CTAs take items from `order` (n_items, longest or head-major
@@ -193,15 +193,15 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
     };
 
     // Per-row metadata of a softmax item (prefetched one item ahead): pair p, head h, row i,
-    // the row's allowed key ranges [0, e0) u [b1, e1) (model.cpp:242-245), the pair's entry
+    // the row's allowed key ranges [l0, e0) u [b1, e1) (model.cpp:242-245), the pair's entry
     // range and its first entry
     struct ItemMeta {
-        int p, h, i, e0, b1, e1, ea, eb;
+        int p, h, i, l0, e0, b1, e1, ea, eb;
         uint32_t f0;
         int mdl;
     };
     auto fetch_item = [&](int li, int w, int r) -> ItemMeta {  // p < 0: no item li
-        ItemMeta m{-1, 0, a.T, 0, 0, 0, 0, 0, 0u, 0};
+        ItemMeta m{-1, 0, a.T, 0, 0, 0, 0, 0, 0, 0u, 0};
         const int it = item_at(li);
         if (it < 0) return m;
         m.mdl = it / a.n_base;
@@ -209,10 +209,12 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         m.h = it % H;
         m.i = (2 * m.p + w) * 128 + r;
         const bool row_ok = m.i < a.T;
-        const int seg_i = row_ok ? a.seg[m.i] : -1;
-        m.e0 = !row_ok ? 0 : (seg_i == 0 ? m.i + 1 : a.Peff);
-        m.b1 = seg_i > 0 ? a.seg_start[seg_i] : 0;
-        m.e1 = seg_i > 0 ? m.i + 1 : 0;
+        const int4 f = row_ok ? a.seg_info[a.seg[m.i]] : make_int4(0, 0, 0, 0);
+        const bool resp = row_ok && f.y >= 0;
+        m.l0 = f.x;
+        m.e0 = !row_ok ? 0 : (resp ? f.y : m.i + 1);
+        m.b1 = resp ? f.z : 0;
+        m.e1 = resp ? m.i + 1 : 0;
         m.ea = a.p_ptr[m.p];
         m.eb = a.p_ptr[m.p + 1];
         m.f0 = m.ea < m.eb ? (uint32_t)a.p_list[m.ea] : 0u;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int k = 0; nx.p >= 0; ++k) {
             const ItemMeta cur = nx;
             nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
-            const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
+            const int p = cur.p, h = cur.h, i = cur.i, l0 = cur.l0, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
             bool first = true;
@@ -405,11 +407,11 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     if (q4 == 0) ATTN_TRACE(w, cS, 2);
                     if (!(f & FULL)) {
                         const int j0 = (int)(f & 0xffffff) * 128 + hc * 64;
-                        const int h0 = min(max(e0 - j0, 0), 64);
+                        const int lo0 = min(max(l0 - j0, 0), 64), h0 = min(max(e0 - j0, 0), 64);
                         const int l1 = min(max(b1 - j0, 0), 64), h1 = min(max(e1 - j0, 0), 64);
 #pragma unroll
                         for (int j = 0; j < 64; ++j) {
-                            const bool ok = (j < h0) | ((j >= l1) & (j < h1));
+                            const bool ok = ((j >= lo0) & (j < h0)) | ((j >= l1) & (j < h1));
                             sv[j] = ok ? sv[j] : -INFINITY;
                         }
                     }
@@ -659,7 +661,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int k = 0; nx.p >= 0; ++k) {
             const ItemMeta cur = nx;
             nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
-            const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
+            const int p = cur.p, h = cur.h, i = cur.i, l0 = cur.l0, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
             bool first = true;
@@ -678,11 +680,11 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 if (q4 == 0) ATTN_TRACE(w, cS, 2);
                 if (!(f & FULL)) {
                     const int j0 = (int)(f & 0xffffff) * 128;
-                    const int h0 = min(max(e0 - j0, 0), 128);
+                    const int lo0 = min(max(l0 - j0, 0), 128), h0 = min(max(e0 - j0, 0), 128);
                     const int l1 = min(max(b1 - j0, 0), 128), h1 = min(max(e1 - j0, 0), 128);
 #pragma unroll
                     for (int j = 0; j < 128; ++j) {
-                        const bool ok = (j < h0) | ((j >= l1) & (j < h1));
+                        const bool ok = ((j >= lo0) & (j < h0)) | ((j >= l1) & (j < h1));
                         sv[j] = ok ? sv[j] : -INFINITY;
                     }
                 }
@@ -767,14 +769,17 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
 
 
 // Backward prologue for the v2 kernels: D = rowsum(dO * O) per (head, row),
-// lse in log2 units, and per-row visibility bounds {qhi, b1} (b1 = -1 for
-// prompt rows): key j is seen by queries [j, qhi_j); query i sees keys
-// [0, e0) u [b1, i] with e0 = i + 1 (prompt row) or Peff (response row).
+// lse in log2 units, and per-row visibility bounds {qhi, b1, l0, e0} (b1 = -1
+// for prompt rows): key j is seen by queries [j, qhi_j); query i sees keys
+// [l0, e0) u [b1, i] with e0 = i + 1 (prompt row) or its group's prompt end.
+__device__ __forceinline__ int4 row_meta(const int4 f) {
+    return make_int4(f.w, f.y < 0 ? -1 : f.z, f.x, f.y);
+}
+
 __global__ void k_attn_prep(int T, int H, int d, int Dh, long ldo, const int32_t* __restrict__ seg,
-                            const int32_t* __restrict__ seg_start, const int32_t* __restrict__ seg_end,
-                            const bf16* __restrict__ out, const bf16* __restrict__ dout,
-                            const float* __restrict__ lse, float* __restrict__ dsum, float* __restrict__ lse2,
-                            int2* __restrict__ meta) {
+                            const int4* __restrict__ seg_info, const bf16* __restrict__ out,
+                            const bf16* __restrict__ dout, const float* __restrict__ lse, float* __restrict__ dsum,
+                            float* __restrict__ lse2, int4* __restrict__ meta) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
     const long gw = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -791,10 +796,7 @@ __global__ void k_attn_prep(int T, int H, int d, int Dh, long ldo, const int32_t
         dsum[(long)h * T + i] = acc;
         lse2[(long)h * T + i] = lse[(long)h * T + i] * LOG2E;
     }
-    if (h == 0 && lane == 1) {
-        const int sg = seg[i];
-        meta[i] = make_int2(sg == 0 ? T : seg_end[sg], sg == 0 ? -1 : seg_start[sg]);
-    }
+    if (h == 0 && lane == 1) meta[i] = row_meta(seg_info[seg[i]]);
 }
 
 // The same prologue with 16-byte loads: thread = 8 consecutive columns of one row, the
@@ -802,11 +804,10 @@ __global__ void k_attn_prep(int T, int H, int d, int Dh, long ldo, const int32_t
 // a block covers whole rows, so every warp streams 512 contiguous bytes of O and dO.
 template <int G>
 __global__ void __launch_bounds__(256) k_attn_prep_v8(int T, int H, int d, long ldo, const int32_t* __restrict__ seg,
-                                                      const int32_t* __restrict__ seg_start,
-                                                      const int32_t* __restrict__ seg_end, const bf16* __restrict__ out,
+                                                      const int4* __restrict__ seg_info, const bf16* __restrict__ out,
                                                       const bf16* __restrict__ dout, const float* __restrict__ lse,
                                                       float* __restrict__ dsum, float* __restrict__ lse2,
-                                                      int2* __restrict__ meta) {
+                                                      int4* __restrict__ meta) {
     pdl_wait();
     const int d8 = d >> 3;
     const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -832,10 +833,7 @@ __global__ void __launch_bounds__(256) k_attn_prep_v8(int T, int H, int d, long 
         dsum[hi] = acc;
         lse2[hi] = lse[hi] * LOG2E;
     }
-    if (ok && c8 == 0) {
-        const int sg = seg[i];
-        meta[i] = make_int2(sg == 0 ? T : seg_end[sg], sg == 0 ? -1 : seg_start[sg]);
-    }
+    if (ok && c8 == 0) meta[i] = row_meta(seg_info[seg[i]]);
 }
 
 struct BwdWs {
@@ -874,15 +872,13 @@ BwdWs g_bwd_ws;
 enum { MODE_DKV = 0, MODE_DQ = 1 };
 
 struct AttnBwd2Args {
-    int T, H, d, Peff;
-    const int32_t* seg;
-    const int32_t *seg_start, *seg_end;
+    int T, H, d;
     const int32_t *lst_ptr, *lst;    // per item tile: partner tiles (k_ptr/k_list or q_ptr/q_list)
     const int32_t *w_ptr, *w_items;  // per-CTA items (tile * H + head)
     float scale, scale_log2;
     const float* lse2;  // [H x T] log-sum-exp in log2 units
     const float* dsum;  // [H x T]
-    const int2* meta;   // [T] {qhi, b1} (k_attn_prep)
+    const int4* meta;   // [T] {qhi, b1, l0, e0} (k_attn_prep)
     bf16* dqkv;         // [T x 3d]
 };
 
@@ -1125,7 +1121,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
         const float c2 = a.scale_log2;
         int cS = 0, na = 0, g = 0;
         // per-row data of an item (prefetched one item ahead)
-        int2 nmeta = make_int2(0, -1);
+        int4 nmeta = make_int4(0, -1, 0, 0);
         float nlr = 0.f, ndr = 0.f;
         auto fetch = [&](int k) {
             if (k >= k_end) return;
@@ -1143,12 +1139,13 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             const int it = a.w_items[k], t = it / H, h = it % H;
             const int x = t * 128 + r;  // this thread's row: key j (DKV) or query i (DQ)
             const bool row_ok = x < a.T;
-            const int2 meta = nmeta;
+            const int4 meta = nmeta;
             const float lr = nlr, dr = ndr;
             fetch(k + 1);
-            // DKV: queries that see key j are [j, qhi); DQ: keys seen by query i are [0, e0) u [b1, e1)
+            // DKV: queries that see key j are [j, qhi); DQ: keys seen by query i are [l0, e0) u [b1, e1)
             const int qhi = row_ok ? meta.x : 0;
-            const int e0 = !row_ok ? 0 : (meta.y < 0 ? x + 1 : a.Peff);
+            const int l0 = meta.z;
+            const int e0 = !row_ok ? 0 : (meta.y < 0 ? x + 1 : meta.w);
             const int b1 = meta.y < 0 ? 0 : meta.y, e1 = (row_ok && meta.y >= 0) ? x + 1 : 0;
             const int ea = a.lst_ptr[t], eb = a.lst_ptr[t + 1];
             for (int e = ea; e < eb; ++e, ++g) {
@@ -1209,7 +1206,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                             hi = min(max(qhi - cu, 0), 32);
                             l2 = h2 = 32;
                         } else {
-                            lo = 0;
+                            lo = min(max(l0 - cu, 0), 32);
                             hi = min(max(e0 - cu, 0), 32);
                             l2 = min(max(b1 - cu, 0), 32);
                             h2 = min(max(e1 - cu, 0), 32);
@@ -1366,26 +1363,25 @@ bool attn_bwd_tc(const AttnArgs& aa, const bf16* qkv, const bf16* out, const bf1
     if (!aa.sched.q_ptr || !aa.sched.k_ptr || !aa.sched.bk_ptr || !aa.sched.bq_ptr || !out) return false;
     {
         const size_t ht = (size_t)aa.H * aa.T;
-        float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 8 + 16));
+        float* lse2 = static_cast<float*>(g_bwd_ws.get(ht * 4 + (size_t)aa.T * 16 + 16));
         if (!lse2) return false;
-        int2* meta = reinterpret_cast<int2*>(lse2 + ((ht + 3) & ~size_t(3)));
+        int4* meta = reinterpret_cast<int4*>(lse2 + ((ht + 3) & ~size_t(3)));
         const long warps = (long)aa.T * aa.H, ldo = aa.ldo ? aa.ldo : aa.d;
         const bool v8 = (aa.Dh == 64 || aa.Dh == 128) && aa.d % 8 == 0 && ldo % 8 == 0 &&
                         (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (reinterpret_cast<uintptr_t>(dout) & 15) == 0;
         const long thr = (long)aa.T * (aa.d / 8);
         if (v8 && aa.Dh == 64)
             launch_pdl(k_attn_prep_v8<8>, dim3((int)((thr + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, ldo,
-                       aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+                       aa.seg, aa.seg_info, out, dout, lse, dsum, lse2, meta);
         else if (v8)
             launch_pdl(k_attn_prep_v8<16>, dim3((int)((thr + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, ldo,
-                       aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+                       aa.seg, aa.seg_info, out, dout, lse, dsum, lse2, meta);
         else
             launch_pdl(k_attn_prep, dim3((int)((warps * 32 + 255) / 256)), dim3(256), 0, st, aa.T, aa.H, aa.d, aa.Dh,
-                       ldo, aa.seg, aa.seg_start, aa.seg_end, out, dout, lse, dsum, lse2, meta);
+                       ldo, aa.seg, aa.seg_info, out, dout, lse, dsum, lse2, meta);
         PARL_LAUNCHED();
         AttnBwd2Args b;
-        b.T = aa.T; b.H = aa.H; b.d = aa.d; b.Peff = aa.Peff;
-        b.seg = aa.seg; b.seg_start = aa.seg_start; b.seg_end = aa.seg_end;
+        b.T = aa.T; b.H = aa.H; b.d = aa.d;
         b.scale = aa.scale; b.scale_log2 = aa.scale * LOG2E;
         b.lse2 = lse2; b.dsum = dsum; b.meta = meta; b.dqkv = dqkv;
         b.lst_ptr = aa.sched.k_ptr; b.lst = aa.sched.k_list;
@@ -1443,8 +1439,8 @@ bool attn_fwd_tc_multi(const AttnArgs& aa, const bf16* const* qkv, bf16* const* 
         for (int k0 = 0; k0 < nm; k0 += per_launch) {
             AttnPairArgs pa;
             AttnPairMaps maps;
-            pa.T = aa.T; pa.H = aa.H; pa.d = aa.d; pa.Peff = aa.Peff;
-            pa.seg = aa.seg; pa.seg_start = aa.seg_start;
+            pa.T = aa.T; pa.H = aa.H; pa.d = aa.d;
+            pa.seg = aa.seg; pa.seg_info = aa.seg_info;
             pa.p_ptr = aa.sched.p_ptr; pa.p_list = aa.sched.p_list;
             pa.w_ptr = aa.sched.w_ptr; pa.w_items = aa.sched.w_items;
             pa.scale_log2 = aa.scale * LOG2E;

@@ -70,6 +70,71 @@ __global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t*
     if ((threadIdx.x & 31) == 0 && id_max) atomicMax(id_max, umax);
 }
 
+// K1, several prompt groups in one packed sequence (f4: several prompts per launch):
+// [P_0 | R_0,0 .. R_0,G0-1 | P_1 | R_1,0 ..], each group laid out as pack_group lays out
+// one (packing.cpp:27-43): positions restart at 0 for every group, the responses of a group
+// restart at its P, labels self-aligned, the first token of a response scored from its
+// group's last prompt position.  Segments: group g's prompt is segment g + r0[g] (r0 =
+// first response of the group), its responses follow.  One thread per packed position;
+// the group by binary search over gstart[n + 1], the response over rcu (scored offsets).
+__global__ void k_pack_multi(const int32_t* __restrict__ prompts, const int32_t* __restrict__ resp_flat,
+                             const int32_t* __restrict__ gstart, const int32_t* __restrict__ pstart,
+                             const int32_t* __restrict__ r0, const int32_t* __restrict__ rcu,
+                             const int32_t* __restrict__ rstart, int n, PackedDev pk, unsigned* __restrict__ id_max) {
+    const int T = gstart[n], S = rcu[r0[n]];
+    unsigned umax = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+        int lo = 0, hi = n - 1;  // group g with gstart[g] <= t < gstart[g + 1]
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (gstart[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int g = lo, gs = gstart[g], kr0 = r0[g], kr1 = r0[g + 1];
+        const int P = (kr1 > kr0 ? rstart[kr0] : gstart[g + 1]) - gs;
+        const int pe = gs + P - 1;                     // the group's last prompt position
+        const int S_before = rcu[kr0];                 // rows owned by earlier groups' positions
+        const int sp = g + kr0;                        // the group's prompt segment
+        if (t < gs + P) {
+            const int tok = prompts[pstart[g] + (t - gs)];
+            umax = max(umax, (unsigned)tok);
+            pk.tokens[t] = tok;
+            pk.labels[t] = -1;
+            pk.positions[t] = t - gs;
+            pk.seg[t] = sp;
+            pk.pred[t] = t > gs ? t - 1 : -1;
+            pk.row_ptr[t] = S_before;
+            if (t == pe)
+                for (int k = kr0; k < kr1; ++k) pk.row_idx[S_before + (k - kr0)] = rcu[k];
+        } else {
+            int a = kr0, b = kr1 - 1;  // response k with rstart[k] <= t
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (rstart[mid] <= t) a = mid; else b = mid - 1;
+            }
+            const int k = a, i = t - rstart[k], s = rcu[k] + i;
+            const int tok = resp_flat[s];
+            umax = max(umax, (unsigned)tok);
+            pk.tokens[t] = tok;
+            pk.labels[t] = tok;
+            pk.positions[t] = P + i;
+            pk.seg[t] = sp + 1 + (k - kr0);
+            const int pr = i == 0 ? pe : t - 1;
+            pk.pred[t] = pr;
+            pk.scored_pos[s] = t;
+            pk.scored_label[s] = tok;
+            pk.pred_pos[s] = pr;
+            pk.sample_of[s] = k;
+            const int rp = S_before + (kr1 - kr0) + (s - rcu[kr0]) - (k - kr0);
+            pk.row_ptr[t] = rp;
+            if (i != rcu[k + 1] - rcu[k] - 1) pk.row_idx[rp] = s + 1;
+        }
+        if (t == T - 1) pk.row_ptr[T] = S;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    if ((threadIdx.x & 31) == 0 && id_max) atomicMax(id_max, umax);
+}
+
 // ---------------------------------------------------------------------------
 // K2: x[t] = tok_emb[tokens[t]] + pos_emb[positions[t]]  (fp32 residual stream)
 __global__ void k_embed(const float* __restrict__ tok_emb, const float* __restrict__ pos_emb,
@@ -702,6 +767,19 @@ __global__ void k_allowed_mask(const int32_t* __restrict__ seg, int n, uint8_t* 
 
 void launch_allowed_mask(const int32_t* seg, int n, uint8_t* mask, cudaStream_t st) {
     k_allowed_mask<<<grid_for((long)n * n), 256, 0, st>>>(seg, n, mask);
+    PARL_LAUNCHED();
+}
+
+void launch_pack_multi(const int32_t* prompts, const int32_t* resp, const int32_t* tables, int n, int n_resp, int T,
+                       const PackedDev& pk, unsigned* id_max, cudaStream_t st) {
+    // tables: gstart [n + 1] | pstart [n] | r0 [n + 1] | rcu [n_resp + 1] | rstart [n_resp]
+    const int32_t* gstart = tables;
+    const int32_t* pstart = gstart + n + 1;
+    const int32_t* r0 = pstart + n;
+    const int32_t* rcu = r0 + n + 1;
+    const int32_t* rstart = rcu + n_resp + 1;
+    if (id_max) PARL_CUDA(cudaMemsetAsync(id_max, 0, sizeof(unsigned), st));
+    k_pack_multi<<<grid_for(T), 256, 0, st>>>(prompts, resp, gstart, pstart, r0, rcu, rstart, n, pk, id_max);
     PARL_LAUNCHED();
 }
 

@@ -62,8 +62,8 @@ struct SegOp {
     }
 };
 
-template <class LP>
-__device__ __forceinline__ void load8(const LP* __restrict__ p, long t, int S, double* v) {
+template <class LP, class R>
+__device__ __forceinline__ void load8(const LP* __restrict__ p, long t, long S, R* v) {
     if constexpr (std::is_same_v<LP, float>) {
         if (t + GR_ITEMS <= S && ((reinterpret_cast<uintptr_t>(p + t) & 15) == 0)) {
             const float4 x = *reinterpret_cast<const float4*>(p + t), y = *reinterpret_cast<const float4*>(p + t + 4);
@@ -73,11 +73,11 @@ __device__ __forceinline__ void load8(const LP* __restrict__ p, long t, int S, d
         }
     }
 #pragma unroll
-    for (int i = 0; i < GR_ITEMS; ++i) v[i] = (t + i < S) ? (double)p[t + i] : 0.0;
+    for (int i = 0; i < GR_ITEMS; ++i) v[i] = (t + i < S) ? (R)p[t + i] : R(0);
 }
 
 template <class LP>
-__global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, 3) k_grpo_tokens(const GrpoArgs a) {
     using Scan = cub::BlockScan<SegAgg, GR_THREADS>;
     using R = std::conditional_t<std::is_same_v<LP, float>, float, double>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
 
     const long t0 = c0 + (long)tid * GR_ITEMS;
     int s[GR_ITEMS];
-    double x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];
+    R x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];  // per-token values in the arithmetic type (fp32 hot path)
     if (t0 + GR_ITEMS <= c1 && ((reinterpret_cast<uintptr_t>(a.sample_of + t0) & 15) == 0)) {
         const int4 p = *reinterpret_cast<const int4*>(a.sample_of + t0), q = *reinterpret_cast<const int4*>(a.sample_of + t0 + 4);
         s[0] = p.x; s[1] = p.y; s[2] = p.z; s[3] = p.w; s[4] = q.x; s[5] = q.y; s[6] = q.z; s[7] = q.w;
@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
 #pragma unroll
         for (int i = 0; i < GR_ITEMS; ++i) s[i] = (t0 + i < c1) ? a.sample_of[t0 + i] : -1;
     }
-    load8(static_cast<const LP*>(a.lp), t0, (int)c1, x0);
-    load8(static_cast<const LP*>(a.old), t0, (int)c1, x1);
-    load8(static_cast<const LP*>(a.ref), t0, (int)c1, x2);
+    load8(static_cast<const LP*>(a.lp), t0, c1, x0);
+    load8(static_cast<const LP*>(a.old), t0, c1, x1);
+    load8(static_cast<const LP*>(a.ref), t0, c1, x2);
     const int nv = (int)max(0L, min((long)GR_ITEMS, c1 - t0));  // valid items of this thread
     const R eps = (R)a.eps, beta = (R)a.beta;
     if (a.gran == 0) {  // token granularity (grpo.cpp:119-131)
@@ -133,20 +133,20 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
 #pragma unroll
         for (int i = 0; i < GR_ITEMS; ++i) {
             if (i >= nv) {
-                x0[i] = x1[i] = x2[i] = 0.0;
+                x0[i] = x1[i] = x2[i] = R(0);
                 up4[i] = 0.f;
                 continue;
             }
-            const R lp = (R)x0[i], old = (R)x1[i], ref = (R)x2[i];
+            const R lp = x0[i], old = x1[i], ref = x2[i];
             const int jl = s[i] - j_lo;
             R cv, cg;
             int c;
             clip_eval<R>(lp, old, (R)s_adv[jl], eps, cv, cg, c);
             const R d = ref - lp, em = expm1(d);  // eval_kl, grpo.cpp:89-93
             const double g = s_inv[jl] * ((double)cg + (double)beta * (double)em);
-            x0[i] = (double)cv;
-            x1[i] = (double)(em - d);
-            x2[i] = (double)c;
+            x0[i] = cv;
+            x1[i] = em - d;
+            x2[i] = (R)c;
             up4[i] = (float)(a.up_scale * g);
             if (a.up_f64) a.up_f64[t0 + i] = a.up_scale * g;
         }
@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
     SegAgg agg{0.0, 0.0, 0.0, (tid == 0 || first != prev_last || first != last) ? 1 : 0};
     for (int i = 0; i < nv; ++i)
         if (s[i] == last) {
-            agg.a += x0[i];
-            agg.b += x1[i];
-            agg.c += x2[i];
+            agg.a += (double)x0[i];
+            agg.b += (double)x1[i];
+            agg.c += (double)x2[i];
         }
     SegAgg carry;
     Scan(scan_tmp).ExclusiveScan(agg, carry, SegOp());
@@ -183,9 +183,9 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
         r2 = carry.c;
     }
     for (int i = 0; i < nv; ++i) {
-        r0 += x0[i];
-        r1 += x1[i];
-        r2 += x2[i];
+        r0 += (double)x0[i];
+        r1 += (double)x1[i];
+        r2 += (double)x2[i];
         const bool end = (i + 1 < nv) ? (s[i + 1] != s[i]) : (next_first != s[i]);
         if (end) {
             double* o = a.slots + 3 * ((long)s[i] + blockIdx.x);
@@ -197,21 +197,27 @@ __global__ void __launch_bounds__(GR_THREADS) k_grpo_tokens(const GrpoArgs a) {
     }
 }
 
-// Per-sample terms + stats, one block (fixed-order reductions).
+// Per-sample terms + stats, one block: warp w takes samples w, w + 32, ...; its lanes add the
+// sample's (sample, block) partials in a fixed strided order (a sample spanning many chunks is
+// not a serial chain of dependent loads), then a fixed-order tree over the warps.
 __global__ void __launch_bounds__(1024) k_grpo_finish(const GrpoArgs a) {
-    __shared__ double red[5][1024];
-    const int tid = threadIdx.x;
+    __shared__ double red[5][32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     double acc[5] = {0, 0, 0, 0, 0};
-    for (int j = tid; j < a.n; j += blockDim.x) {
+    for (int j = wid; j < a.n; j += nw) {
         const int b = a.cu[j], e = a.cu[j + 1], n = e - b;
         const int b0 = b / GR_CHUNK, b1 = (e - 1) / GR_CHUNK;
         double s0 = 0, s1 = 0, s2 = 0;
-        for (int k = b0; k <= b1; ++k) {
+        for (int k = b0 + lane; k <= b1; k += 32) {
             const double* o = a.slots + 3 * ((long)j + k);
             s0 += o[0];
             s1 += o[1];
             s2 += o[2];
         }
+        s0 = warp_sum_d(s0);
+        s1 = warp_sum_d(s1);
+        s2 = warp_sum_d(s2);
+        if (lane != 0) continue;
         double t[4];
         if (a.gran == 0) {
             const double inv = 1.0 / n;
@@ -238,15 +244,16 @@ __global__ void __launch_bounds__(1024) k_grpo_finish(const GrpoArgs a) {
         acc[3] += t[2];
         acc[4] += t[3];
     }
-    for (int q = 0; q < 5; ++q) red[q][tid] = acc[q];
+    if (lane == 0)
+        for (int q = 0; q < 5; ++q) red[q][wid] = acc[q];
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (tid < w)
-            for (int q = 0; q < 5; ++q) red[q][tid] += red[q][tid + w];
-        __syncthreads();
+    if (tid == 0 && a.stats) {
+        for (int q = 0; q < 5; ++q) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += red[q][w];
+            a.stats[q] += s;
+        }
     }
-    if (tid == 0 && a.stats)
-        for (int q = 0; q < 5; ++q) a.stats[q] += red[q][0];
 }
 
 __global__ void __launch_bounds__(256) k_grpo_bcast(const GrpoArgs a) {

@@ -81,6 +81,9 @@ struct ModelW {
 // launchers (k_elem.cu)
 void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
                  const PackedDev& pk, unsigned* id_max, cudaStream_t st);
+// several prompt groups per sequence; tables: gstart [n+1] | pstart [n] | r0 [n+1] | rcu [R+1] | rstart [R]
+void launch_pack_multi(const int32_t* prompts, const int32_t* resp, const int32_t* tables, int n, int n_resp, int T,
+                       const PackedDev& pk, unsigned* id_max, cudaStream_t st);
 void launch_allowed_mask(const int32_t* seg, int n, uint8_t* mask, cudaStream_t st);
 void launch_embed(const float* tok, const float* pos, const int32_t* tokens, const int32_t* positions, int T, int D,
                   float* x, cudaStream_t st);
@@ -188,10 +191,11 @@ struct AttnArgs {
     AttnSched sched;
     int T, H, Dh, d;
     long ldo = 0;              // row stride of the attention output O (0: d)
-    int Peff;                  // end of segment 0 (prompt length, or T when causal)
-    const int32_t* seg;        // [T]
-    const int32_t* seg_start;  // [G+1]
-    const int32_t* seg_end;    // [G+1]
+    const int32_t* seg;        // [T] segment of each position
+    // per segment {A, B, C, Q}: rows of a prompt segment (B = -1) see keys [A, i]; rows of a
+    // response segment see their group's prompt [A, B) and their own prefix [C, i]; keys of the
+    // segment are seen by queries [j, Q) (model.cpp:242-245, several prompt groups per sequence)
+    const int4* seg_info;
     float scale;
     // dynamic work queue of the forward: a device counter and the host-side running base
     // (each launch consumes n_items + grid counter values); null: static per-CTA lists

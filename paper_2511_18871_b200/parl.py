@@ -122,6 +122,8 @@ def _load():
         "parl_group_create": [vp, C.c_int, C.c_int, C.POINTER(vp)], "parl_group_destroy": [vp],
         "parl_pack": [vp, i32p, C.c_int, i32p, i32p, C.c_int, C.c_int],
         "parl_pack_device": [vp, vp, C.c_int, vp, i32p, C.c_int, C.c_int],
+        "parl_pack_multi": [vp, i32p, i32p, i32p, i32p, i32p, C.c_int, C.c_int],
+        "parl_pack_multi_device": [vp, vp, i32p, vp, i32p, i32p, C.c_int, C.c_int],
         "parl_set_sequence": [vp, i32p, i32p, i32p, C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int],
         "parl_group_download": [vp, i32p, i32p, i32p, i32p, i32p, i32p, i32p],
         "parl_forward": [vp, vp, vp, C.c_int, C.POINTER(vp)],
@@ -495,6 +497,26 @@ class Group:
         _check(LIB.parl_pack_device(self.h, C.c_void_p(d_prompt), P, C.c_void_p(d_resp), _pi(lens), len(lens),
                                     max_seq_len), self.ctx.h)
         self.prompt_len, self.response_lens = P, tuple(int(x) for x in lens)
+        return self
+
+    def pack_multi(self, prompts, groups, max_seq_len: int):
+        """Several prompt groups in one packed sequence (parl_pack_multi): prompts[q] with its
+        responses groups[q]; each group laid out as pack_group, no attention across groups."""
+        pl = _i32([len(p) for p in prompts])
+        gs = _i32([len(r) for r in groups])
+        rl = _i32([len(x) for r in groups for x in r])
+        pf = _i32(np.concatenate([np.asarray(p, np.int32) for p in prompts]))
+        rf = _i32(np.concatenate([np.asarray(x, np.int32) for r in groups for x in r]))
+        _check(LIB.parl_pack_multi(self.h, _pi(pf), _pi(pl), _pi(rf), _pi(rl), _pi(gs), len(pl), max_seq_len),
+               self.ctx.h)
+        self.prompt_len, self.response_lens = int(pl[0]), tuple(int(x) for x in rl)
+        return self
+
+    def pack_multi_device(self, d_prompts: int, prompt_lens, d_resp: int, resp_lens, group_sizes, max_seq_len: int):
+        pl, rl, gs = _i32(prompt_lens), _i32(resp_lens), _i32(group_sizes)
+        _check(LIB.parl_pack_multi_device(self.h, C.c_void_p(d_prompts), _pi(pl), C.c_void_p(d_resp), _pi(rl),
+                                          _pi(gs), len(pl), max_seq_len), self.ctx.h)
+        self.prompt_len, self.response_lens = int(pl[0]), tuple(int(x) for x in rl)
         return self
 
     def set_sequence(self, tokens, positions, labels, mask: AttentionMaskSpec, vocab_size: int, max_seq_len: int):

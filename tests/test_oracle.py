@@ -258,3 +258,40 @@ def test_parlckp1_reference_round_trip(ref_orc, tmp_path):
     cfg, version, seed, w2 = ref_orc.load_checkpoint(path)
     assert cfg == TINY_CKPT and version == 0 and seed == 5 and np.array_equal(w, w2)
     assert np.array_equal(read_parlckp1(path)[4], w)
+
+
+def test_torch_ref_pinned(orc):
+    """oracle/torch_ref.py (exact mode) == the C restatement on a shared-prompt micro-step:
+    log-probs of the three roles, the gradient and the loss stats, to fp64 rounding."""
+    from oracle import Cfg
+    from oracle import torch_ref as TR
+
+    for cfg, P, lens in ((Cfg(16, 16, 2, 2, 24, 64), 5, [3, 4, 1, 2]), (Cfg(64, 32, 1, 4, 48, 64), 9, [7, 1, 12])):
+        w = orc.init_params(cfg, 41)
+        rng = np.random.default_rng(0)
+        wo, wr = w + 0.01 * rng.standard_normal(len(w)), w - 0.01 * rng.standard_normal(len(w))
+        prompt = rng.integers(4, cfg.vocab, P)
+        resp = [rng.integers(4, cfg.vocab, n) for n in lens]
+        adv = orc.group_advantages(rng.random(len(lens)))
+        g, st, lp3 = orc.train_microbatch(cfg, w, wo, wr, prompt, resp, adv)
+        lp3_t, g_t, st_t = TR.microstep(cfg, w, wo, wr, prompt, resp, adv)
+        assert np.abs(lp3 - lp3_t).max() < 1e-13
+        assert np.abs(g - g_t).max() <= 1e-12 * np.abs(g).max()
+        assert np.abs(st - st_t).max() < 1e-13
+
+
+def test_torch_ref_pinned_c2_width_fixture():
+    """The restatement at C2's layer width against the reference-generated fixture
+    (tests/golden/c2w_micro.npz: log-probs, per-tensor gradient sums / norms, 4096 sampled entries)."""
+    from oracle import Cfg, Oracle
+    from oracle import torch_ref as TR
+    from oracle.make_golden import C2W, perturb
+
+    z = np.load(os.path.join(GOLDEN, "c2w_micro.npz"))
+    w = Oracle("c").init_params(C2W, int(z["seed"]))
+    wo, wr = perturb(w, int(z["old_seed"]), float(z["scale"])), perturb(w, int(z["ref_seed"]), float(z["scale"]))
+    resp = np.split(z["resp_flat"], np.cumsum(z["lens"])[:-1])
+    lp3, g, st = TR.microstep(C2W, w, wo, wr, z["prompt"], resp, z["advantages"])
+    assert np.abs(lp3 - z["lp3"]).max() < 1e-11
+    assert np.abs(st - z["stats"]).max() < 1e-11
+    assert np.allclose(g[z["grad_idx"]], z["grad_vals"], rtol=1e-9, atol=1e-14)
