@@ -319,23 +319,34 @@ def run_ours(args, c):
         prompts.append(rng.integers(4, c["vocab"], Pn).astype(np.int32))
         resps.append(rng.integers(4, c["vocab"], T - Pn).astype(np.int32))
         rewards.append(rng.random(G))
-    group = P.Group(T, G, ctx)
+    K = max(1, args.pack)  # prompt groups packed into one sequence per micro-step (f4)
+    chunks = [list(range(i, min(i + K, ng))) for i in range(0, ng, K)]
+    group = P.Group(T * K, G * K, ctx)
 
     import torch
 
     torch.cuda.set_device(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
-    d_prompts = [torch.from_numpy(p).cuda(local) for p in prompts]
-    d_resps = [torch.from_numpy(r).cuda(local) for r in resps]
+    d_prompts = [torch.from_numpy(np.concatenate([prompts[i] for i in ch])).cuda(local) for ch in chunks]
+    d_resps = [torch.from_numpy(np.concatenate([resps[i] for i in ch])).cuda(local) for ch in chunks]
+    rew_ch = [np.concatenate([rewards[i] for i in ch]) for ch in chunks]
     torch.cuda.synchronize(local)
+
+    def pack_chunk(q):
+        n = len(chunks[q])
+        if n == 1:
+            group.pack_device(d_prompts[q].data_ptr(), Pn, d_resps[q].data_ptr(), lens, c["max_seq"])
+        else:
+            group.pack_multi_device(d_prompts[q].data_ptr(), [Pn] * n, d_resps[q].data_ptr(), np.tile(lens, n),
+                                    [G] * n, c["max_seq"])
 
     def step_device():
         grads.reset()
-        for i in range(ng):
-            group.pack_device(d_prompts[i].data_ptr(), Pn, d_resps[i].data_ptr(), lens, c["max_seq"])
-            if world > 1 and i == ng - 1:
+        for q in range(len(chunks)):
+            pack_chunk(q)
+            if world > 1 and q == len(chunks) - 1:
                 grads.allreduce_overlap()  # the last backward streams its gradient slices to NCCL
-            P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=False)
+            P.train_microbatch(tm, group, grads, hyper, rewards=rew_ch[q], want_stats=False)
         if world > 1:
             grads.allreduce()
             ctx.stats_allreduce()
@@ -349,11 +360,16 @@ def run_ours(args, c):
         # after the last micro-batch; the statistics accumulate on the device)
         grads.reset()
         ctx.stats_reset()
-        for i in range(ng):
-            group.pack(h_prompts[i], [h_resps[i][offs[k]:offs[k + 1]] for k in range(G)], c["max_seq"])
-            if world > 1 and i == ng - 1:
+        for q, ch in enumerate(chunks):
+            if len(ch) == 1:
+                i = ch[0]
+                group.pack(h_prompts[i], [h_resps[i][offs[k]:offs[k + 1]] for k in range(G)], c["max_seq"])
+            else:
+                group.pack_multi([h_prompts[i] for i in ch],
+                                 [[h_resps[i][offs[k]:offs[k + 1]] for k in range(G)] for i in ch], c["max_seq"])
+            if world > 1 and q == len(chunks) - 1:
                 grads.allreduce_overlap()
-            P.train_microbatch(tm, group, grads, hyper, rewards=rewards[i], want_stats=False)
+            P.train_microbatch(tm, group, grads, hyper, rewards=rew_ch[q], want_stats=False)
         if world > 1:
             grads.allreduce()
             ctx.stats_allreduce()
@@ -453,6 +469,7 @@ def run_ours(args, c):
                                f"P={Pn} G={G} R={c['R'] or lens.tolist()} (T={T}); global batch {n_global} groups "
                                f"per step, {ng} on rank 0",
                    "global_groups": n_global, "groups_per_rank": ng, "packed_tokens_per_group": T,
+                   "groups_per_packed_sequence": K,
                    "l2": "working set (weights+activations, GBs) exceeds the 126 MB L2; no explicit flush",
                    "roofline_timing": f"per-launch CUDA events over {prof_steps} further identical steps",
                    "update_ms": update_ms,
@@ -488,7 +505,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--groups", type=int, default=0, help="prompt groups per rank per step")
+    ap.add_argument("--groups", type=int, default=0, help="global batch: prompt groups per step (all ranks)")
+    ap.add_argument("--pack", type=int, default=1, help="prompt groups packed into one sequence per micro-step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--launch-list", action="store_true",
                     help="run one step inside an NVTX range 'step' (for ncu launch lists) and exit")

@@ -187,6 +187,31 @@ inline void finish_iteration(TriModel& tm, GradBuffer& grads, int total_samples,
     tm.policy.apply_update(grads, lr);
 }
 
+// The G rollouts of one prompt on the KV-cached decoder (parl_sample_group): the prompt's K/V
+// prefilled once and shared; sequence k == sample_tokens(params, prompt, max_new_tokens,
+// temperature, seeds[k]).  old_logprobs (optional): each sampled token's log-prob under params.
+inline std::vector<std::vector<TokenId>> sample_group(const ModelParams& params, std::span<const TokenId> prompt,
+                                                      int max_new_tokens, double temperature,
+                                                      std::span<const std::uint64_t> seeds,
+                                                      std::vector<std::vector<double>>* old_logprobs = nullptr) {
+    const int n = (int)seeds.size(), mx = std::max(max_new_tokens, 1);
+    std::vector<TokenId> out((std::size_t)n * mx);
+    std::vector<int> lens(n);
+    std::vector<double> lp(old_logprobs ? (std::size_t)n * mx : 0);
+    detail::check(parl_sample_group(params.device().ctx(), params.handle(), prompt.data(), (int)prompt.size(), n,
+                                    max_new_tokens, temperature, seeds.data(), out.data(), lens.data(),
+                                    old_logprobs ? lp.data() : nullptr),
+                  params.device().ctx());
+    std::vector<std::vector<TokenId>> r(n);
+    if (old_logprobs) old_logprobs->assign(n, {});
+    for (int k = 0; k < n; ++k) {
+        r[k].assign(out.begin() + (std::size_t)k * mx, out.begin() + (std::size_t)k * mx + lens[k]);
+        if (old_logprobs)
+            (*old_logprobs)[k].assign(lp.begin() + (std::size_t)k * mx, lp.begin() + (std::size_t)k * mx + lens[k]);
+    }
+    return r;
+}
+
 // RolloutService::score_logprobs (rollout.cpp:52-66): response log-probs under a causal forward
 inline std::vector<double> score_logprobs(const ModelParams& params, std::span<const TokenId> prompt,
                                           std::span<const TokenId> response) {

@@ -156,6 +156,15 @@ parl_status parl_model_all_finite(parl_model_t m, int* out);
  * reference (ShapeError / ConfigError / VocabError). */
 parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int prompt_len,
                                int max_new_tokens, double temperature, uint64_t rng_seed, int32_t* out, int* n_out);
+/* The G rollouts of one prompt at once (RolloutService::run's sample_tokens calls,
+ * rollout.cpp:140-160) on a KV-cached decoder: the prompt is prefilled once and its K/V shared
+ * by the n_seq sequences; sequence k follows sample_tokens(prompt, max_new_tokens, temperature,
+ * seeds[k]) exactly (the reference's token choice and RNG stream).  out[k * max_new_tokens ..],
+ * n_out[k]; logprobs_out (may be NULL) gets each sampled token's log-prob under the model, the
+ * old_logprobs of rollout_weights mode (score_logprobs, rollout.cpp:52-66). */
+parl_status parl_sample_group(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int prompt_len, int n_seq,
+                              int max_new_tokens, double temperature, const uint64_t* seeds, int32_t* out, int* n_out,
+                              double* logprobs_out);
 parl_status parl_checkpoint_save(parl_model_t m, const char* path);
 parl_status parl_model_config(parl_model_t m, parl_config* out);
 parl_status parl_checkpoint_load(parl_ctx_t ctx, const char* path, parl_model_t* out);

@@ -116,6 +116,8 @@ struct parl_ctx_s {
     // backward workspaces
     DevBuf dx, dx2, dx_act, dpre, dbn, dmid, dmid_act, dctx, dqkv, da, dsum, dhf, dxg, dz;
     DevBuf stats, per_sample, staging, flags, grpo_slots, g_seq;
+    // KV-cached decoder (parl_sample_group): prompt / per-sequence caches and one step's rows
+    DevBuf kv_prompt, kv_own, dec_x, dec_x2, dec_xm, dec_a, dec_qkv, dec_ctx, dec_act, dec_st, dec_logits, dec_tok;
     // one caller at a time per context (the reference allows distinct ModelParams on distinct
     // threads; they share this context's stream and workspaces)
     std::recursive_mutex mu;
@@ -221,6 +223,12 @@ struct SegLayout {
         ++n_groups;
     }
     int T() const { return end.empty() ? 0 : end.back(); }
+    int max_group_len() const {  // the longest prompt group (info.w of a prompt segment = group end)
+        int m = 0;
+        for (size_t k = 0; k < info.size(); ++k)
+            if (info[k].y < 0) m = std::max(m, info[k].w - info[k].x);
+        return m;
+    }
     // allowed (query, key) pairs: the algorithmic attention work
     double pairs() const {
         double s = 0;
@@ -333,8 +341,17 @@ namespace {
 
 thread_local std::string tl_err;
 
+// Every entry point runs under its context's lock and the process lock: the reference lets
+// distinct ModelParams instances run on distinct threads (rollout.cpp:178), and
+// contexts share a few process-wide workspaces (the split-K and attention-backward scratch).
+std::recursive_mutex& process_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+
 template <class F>
 parl_status guarded(parl_ctx_s* c, F&& f) {
+    std::lock_guard<std::recursive_mutex> glk(process_mutex());
     std::unique_lock<std::recursive_mutex> lk;
     if (c) lk = std::unique_lock<std::recursive_mutex>(c->mu);
     try {
@@ -529,6 +546,7 @@ struct FwdBufs {
     float* xmid = nullptr;  // x_mid
     T *a = nullptr, *qkv = nullptr, *ctxo = nullptr, *bn = nullptr, *pre = nullptr, *actv = nullptr;
     float *stats = nullptr, *lse_attn = nullptr;
+    T* kv = nullptr;  // prefill of the KV-cached decoder: every layer's K | V rows kept, [L][T][2d]
     size_t lay(size_t per, int l) const { return stack_layers ? per * (size_t)l : 0; }
     float* xin(size_t TD, int l) const { return xs + (stack_x ? TD * l : TD * (l & 1)); }
 };
@@ -589,6 +607,10 @@ void layer_forward(parl_ctx_s* c, parl_model_s* const* ms, int nm, const FwdBufs
         gs[k].epi = EPI_ACT; gs[k].bias = w.bqkv; gs[k].Ca = b.qkv + b.lay(3 * TD, l); gs[k].ldca = 3 * D;
     }
     gemm_multi<T>(c, gs, nm);
+    if (B[0].kv)  // K | V columns of this layer's projection into the decoder's cache
+        PARL_CUDA(cudaMemcpy2DAsync(B[0].kv + (size_t)l * Tn * 2 * D, (size_t)2 * D * sizeof(T),
+                                    B[0].qkv + B[0].lay(3 * TD, l) + D, (size_t)3 * D * sizeof(T),
+                                    (size_t)2 * D * sizeof(T), Tn, cudaMemcpyDeviceToDevice, st));
     {
         ProfScope ps(c, PARL_KC_ATTN_FWD, 4.0 * g->pairs * D * nm);
         T* ql[3];
@@ -695,7 +717,7 @@ GemmArgs head_lse_args(parl_ctx_s* c, parl_model_s* m, parl_group_s* g, const bf
 
 template <class T>
 void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int nm, parl_group_s* g,
-                  parl_act_s* act, bool full_logits = false) {
+                  parl_act_s* act, bool full_logits = false, T* kv_out = nullptr) {
     cudaStream_t st = c->st;
     const auto& cf = ms[0]->cfg;
     const int Tn = g->T, D = cf.d_model, H = cf.n_heads, F = cf.d_ff, V = cf.vocab_size, S = g->S;
@@ -741,6 +763,7 @@ void forward_impl(parl_ctx_s* c, parl_model_s* const* ms, const int* slots, int 
         }
     }
 
+    B[0].kv = kv_out;
     if constexpr (std::is_same_v<T, bf16>) ensure_attn_work(g, H, D);
     const AttnArgs aa = attn_args(g, cf);
     {
@@ -2067,7 +2090,9 @@ static void do_forward_n(parl_ctx_s* c, parl_model_s* const* ms, const int* slot
     PARL_REQUIRE(g->T > 0, PARL_E_SHAPE, "group is empty (pack or set a sequence first)");
     for (int k = 0; k < nm; ++k) {
         PARL_REQUIRE(slots[k] >= 0 && slots[k] < 3, PARL_E_CONFIG, "slot must be 0, 1 or 2");
-        PARL_REQUIRE(g->T <= ms[k]->cfg.max_seq_len, PARL_E_SHAPE, "sequence length exceeds max_seq_len");
+        // positions restart per prompt group: max_seq_len bounds each group's own length
+        PARL_REQUIRE(g->segs.max_group_len() <= ms[k]->cfg.max_seq_len, PARL_E_SHAPE,
+                     "sequence length exceeds max_seq_len");
         PARL_REQUIRE(same_cfg(ms[k]->cfg, ms[0]->cfg), PARL_E_CONFIG, "models of one forward must share a config");
     }
     g->vocab = ms[0]->cfg.vocab_size;
@@ -2206,96 +2231,211 @@ parl_status parl_ctx_set_recompute(parl_ctx_t ctx, int mode) {
 
 int parl_act_recompute(parl_act_t a) { return a && a->recompute ? 1 : 0; }
 
-// sample_tokens (model.cpp:843-900): autoregressive sampling from the model.  Each step
-// runs the causal forward over the sequence so far (as the reference does) with the LM
-// head on the last row only (fp32 logits of the compute path), and chooses the token on
-// the host with the reference's own fp64 arithmetic and RNG stream: greedy argmax (lowest
-// id on ties) at temperature 0, else inverse-CDF sampling of softmax(logits / temperature)
-// with Rng(mix_seed(seed, "sample")).uniform() (rng.hpp).  Stops after kEosToken.
-parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int P, int max_new_tokens,
-                               double temperature, uint64_t rng_seed, int32_t* out, int* n_out) {
-    return guarded(ctx, [&] {
-        const auto& c = m->cfg;
-        PARL_REQUIRE(P > 0, PARL_E_SHAPE, "empty prompt");
-        PARL_REQUIRE(max_new_tokens >= 0, PARL_E_CONFIG, "max_new_tokens must be >= 0");
-        PARL_REQUIRE(temperature >= 0.0, PARL_E_CONFIG, "temperature must be >= 0");
-        PARL_REQUIRE(P + max_new_tokens <= c.max_seq_len, PARL_E_SHAPE, "prompt + max_new_tokens exceeds max_seq_len");
-        for (int t = 0; t < P; ++t)
-            PARL_REQUIRE(prompt[t] >= 0 && prompt[t] < c.vocab_size, PARL_E_VOCAB, "token id out of vocabulary");
-        *n_out = 0;
-        if (max_new_tokens == 0) return;
+// ---- rollout side: the KV-cached decoder ------------------------------------------------
+// sample_tokens (model.cpp:843-900) for n sequences that share one prompt (the G rollouts of
+// a group): the prompt runs once through the causal forward with every layer's K | V kept
+// (prefill), then each step embeds the n newest tokens, runs every layer on those n rows
+// (tensor-core GEMMs with M = n, decode attention over the shared prompt cache plus each
+// sequence's own cache) and the LM head on n rows.  Token choice stays with the reference's
+// own fp64 arithmetic and RNG stream per sequence (Rng(mix_seed(seed, "sample")), rng.hpp):
+// greedy argmax (lowest id on ties) at temperature 0, else inverse-CDF sampling of
+// softmax(logits / temperature); a sequence stops after kEosToken.  Optionally returns each
+// sampled token's log-prob under the model (what score_logprobs recomputes, rollout.cpp:52-66).
+extern "C++" {
+namespace {
+struct Sampler {
+    std::mt19937_64 eng;
+    explicit Sampler(uint64_t seed) {
         auto sm64 = [](uint64_t x) {
             x += 0x9e3779b97f4a7c15ull;
             x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
             x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
             return x ^ (x >> 31);
         };
-        std::mt19937_64 eng(sm64(sm64(sm64(rng_seed) ^ (0x9e3779b97f4a7c15ull + 0x73616d706c65ull))));
-        const int V = c.vocab_size, maxT = P + max_new_tokens;
-        parl_group_s g;
-        g.ctx = ctx;
-        g.max_T = maxT;
-        g.max_G = 1;
-        alloc_group_arrays(&g);
-        std::vector<int32_t> seq(prompt, prompt + P);
-        std::vector<int32_t> pos(maxT), zeros(maxT, 0);
-        for (int t = 0; t < maxT; ++t) pos[t] = t;
-        cudaStream_t st = ctx->st;
-        PARL_CUDA(cudaMemcpyAsync(g.pk.positions, pos.data(), maxT * 4, cudaMemcpyHostToDevice, st));
-        PARL_CUDA(cudaMemcpyAsync(g.pk.seg, zeros.data(), maxT * 4, cudaMemcpyHostToDevice, st));
-        PARL_CUDA(cudaMemcpyAsync(g.pk.scored_label, zeros.data(), 4, cudaMemcpyHostToDevice, st));
-        std::vector<float> row(V);
-        std::vector<double> w(V);
-        for (int step = 0; step < max_new_tokens; ++step) {
-            const int T = (int)seq.size();
-            const int32_t last = T - 1;
-            PARL_CUDA(cudaMemcpyAsync(g.pk.tokens, seq.data(), T * 4, cudaMemcpyHostToDevice, st));
-            PARL_CUDA(cudaMemcpyAsync(g.pk.pred_pos, &last, 4, cudaMemcpyHostToDevice, st));
-            g.T = T; g.P = T; g.G = 0; g.S = 1; g.Peff = T; g.n_samples = 1;
-            g.pairs = (double)T * (T + 1) / 2;
-            g.lens.clear(); g.span_start.clear(); g.cu = {0, 1};
-            g.segs.clear();
-            g.segs.add_group(0, T, nullptr, 0);
-            g.vocab = V; g.max_seq = c.max_seq_len;
-            ++g.epoch;
-            upload_meta(&g);
-            int slot = 0;
-            if (ctx->prec == PARL_PREC_BF16) forward_impl<bf16>(ctx, &m, &slot, 1, &g, nullptr, true);
-            else forward_impl<float>(ctx, &m, &slot, 1, &g, nullptr, true);
-            ++m->forward_gen;  // bump_forward_generation (model.cpp:865)
-            PARL_CUDA(cudaMemcpyAsync(row.data(), ctx->scr[0].logits.p, (size_t)V * 4, cudaMemcpyDeviceToHost, st));
-            PARL_CUDA(cudaStreamSynchronize(st));
-            int32_t chosen = 0;
-            if (temperature == 0.0) {
-                double best = row[0];
-                for (int v = 1; v < V; ++v)
-                    if ((double)row[v] > best) {  // strict: lowest id wins ties
-                        best = row[v];
-                        chosen = v;
-                    }
-            } else {
-                double maxv = row[0];
-                for (int v = 1; v < V; ++v) maxv = std::max(maxv, (double)row[v]);
-                double z = 0.0;
-                for (int v = 0; v < V; ++v) {
-                    w[v] = std::exp(((double)row[v] - maxv) / temperature);
-                    z += w[v];
+        eng.seed(sm64(sm64(sm64(seed) ^ (0x9e3779b97f4a7c15ull + 0x73616d706c65ull))));
+    }
+    // model.cpp:868-893 on one fp32 logit row; *lp = log softmax(row)[chosen]
+    int32_t choose(const float* row, int V, double temperature, std::vector<double>& w, double* lp) {
+        int32_t chosen = 0;
+        double maxv = row[0];
+        for (int v = 1; v < V; ++v) maxv = std::max(maxv, (double)row[v]);
+        if (temperature == 0.0) {
+            double best = row[0];
+            for (int v = 1; v < V; ++v)
+                if ((double)row[v] > best) {  // strict: lowest id wins ties
+                    best = row[v];
+                    chosen = v;
                 }
-                const double target = (double)(eng() >> 11) * 0x1.0p-53 * z;
-                double acc = 0.0;
-                chosen = V - 1;
-                for (int v = 0; v < V; ++v) {
-                    acc += w[v];
-                    if (target < acc) {
-                        chosen = v;
-                        break;
-                    }
+        } else {
+            double z = 0.0;
+            for (int v = 0; v < V; ++v) {
+                w[v] = std::exp(((double)row[v] - maxv) / temperature);
+                z += w[v];
+            }
+            const double target = (double)(eng() >> 11) * 0x1.0p-53 * z;
+            double acc = 0.0;
+            chosen = V - 1;
+            for (int v = 0; v < V; ++v) {
+                acc += w[v];
+                if (target < acc) {
+                    chosen = v;
+                    break;
                 }
             }
-            out[(*n_out)++] = chosen;
-            seq.push_back(chosen);
-            if (chosen == 2) break;  // kEosToken (model.hpp:18)
         }
+        if (lp) {
+            double s = 0.0;
+            for (int v = 0; v < V; ++v) s += std::exp((double)row[v] - maxv);
+            *lp = (double)row[chosen] - maxv - std::log(s);
+        }
+        return chosen;
+    }
+};
+
+template <class T>
+void sample_group_impl(parl_ctx_s* c, parl_model_s* m, const int32_t* prompt, int P, int n, int max_new,
+                       double temperature, const uint64_t* seeds, int32_t* out, int* n_out, double* lp_out) {
+    const auto& cf = m->cfg;
+    const int V = cf.vocab_size, D = cf.d_model, F = cf.d_ff, H = cf.n_heads, NL = cf.n_layers;
+    cudaStream_t st = c->st;
+    for (int k = 0; k < n; ++k) n_out[k] = 0;
+    if (max_new == 0) return;
+    // prefill: the causal forward over the prompt, K | V of every layer kept, logits of row P - 1
+    parl_group_s g;
+    g.ctx = c;
+    g.max_T = P;
+    g.max_G = 1;
+    alloc_group_arrays(&g);
+    std::vector<int32_t> pos(P), zeros(P, 0);
+    for (int t = 0; t < P; ++t) pos[t] = t;
+    const int32_t last = P - 1;
+    PARL_CUDA(cudaMemcpyAsync(g.pk.tokens, prompt, (size_t)P * 4, cudaMemcpyHostToDevice, st));
+    PARL_CUDA(cudaMemcpyAsync(g.pk.positions, pos.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
+    PARL_CUDA(cudaMemcpyAsync(g.pk.seg, zeros.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
+    PARL_CUDA(cudaMemcpyAsync(g.pk.scored_label, zeros.data(), 4, cudaMemcpyHostToDevice, st));
+    PARL_CUDA(cudaMemcpyAsync(g.pk.pred_pos, &last, 4, cudaMemcpyHostToDevice, st));
+    g.T = P; g.P = P; g.G = 0; g.S = 1; g.Peff = P; g.n_samples = 1;
+    g.cu = {0, 1};
+    g.segs.add_group(0, P, nullptr, 0);
+    g.pairs = g.segs.pairs();
+    g.vocab = V; g.max_seq = cf.max_seq_len;
+    ++g.epoch;
+    upload_meta(&g);
+    const size_t row2 = (size_t)2 * D;
+    T* kvp = c->kv_prompt.as<T>((size_t)NL * P * row2);
+    int slot = 0;
+    forward_impl<T>(c, &m, &slot, 1, &g, nullptr, true, kvp);
+    ++m->forward_gen;
+    // decode state: n rows
+    const long own_stride = (long)max_new * row2;  // per sequence, per layer
+    T* kvo = c->kv_own.as<T>((size_t)NL * n * own_stride);
+    float* x = c->dec_x.as<float>((size_t)n * D);
+    float* x2 = c->dec_x2.as<float>((size_t)n * D);
+    float* xm = c->dec_xm.as<float>((size_t)n * D);
+    T* a = c->dec_a.as<T>((size_t)n * D);
+    T* qkv = c->dec_qkv.as<T>((size_t)n * 3 * D);
+    T* cx = c->dec_ctx.as<T>((size_t)n * D);
+    T* act = c->dec_act.as<T>((size_t)n * F);
+    float* stv = c->dec_st.as<float>((size_t)2 * n);
+    float* logits = c->dec_logits.as<float>((size_t)n * V);
+    int32_t* dtok = c->dec_tok.as<int32_t>((size_t)2 * n);
+    std::vector<float> rows((size_t)n * V);
+    PARL_CUDA(cudaMemcpyAsync(rows.data(), c->scr[0].logits.p, (size_t)V * 4, cudaMemcpyDeviceToHost, st));
+    PARL_CUDA(cudaStreamSynchronize(st));
+    for (int k = 1; k < n; ++k) std::copy(rows.begin(), rows.begin() + V, rows.begin() + (size_t)k * V);
+    std::vector<Sampler> smp;
+    for (int k = 0; k < n; ++k) smp.emplace_back(seeds[k]);
+    std::vector<double> w(V);
+    std::vector<char> done(n, 0);
+    std::vector<int32_t> tok(n), tpos(n);
+    const float scale = 1.0f / std::sqrt((float)(D / H));
+    for (int step = 0;; ++step) {
+        bool any = false;
+        for (int k = 0; k < n; ++k) {
+            if (done[k]) continue;
+            double lp = 0.0;
+            tok[k] = smp[k].choose(rows.data() + (size_t)k * V, V, temperature, w, lp_out ? &lp : nullptr);
+            if (lp_out) lp_out[(size_t)k * max_new + step] = lp;
+            out[(size_t)k * max_new + step] = tok[k];
+            n_out[k] = step + 1;
+            if (tok[k] == 2 || step + 1 == max_new) done[k] = 1;  // kEosToken (model.hpp:18)
+            else any = true;
+        }
+        if (!any) break;
+        // one decode step over the n newest tokens at position P + step
+        for (int k = 0; k < n; ++k) tpos[k] = P + step;
+        std::vector<int32_t> io(tok);
+        io.insert(io.end(), tpos.begin(), tpos.end());
+        PARL_CUDA(cudaMemcpyAsync(dtok, io.data(), io.size() * 4, cudaMemcpyHostToDevice, st));
+        launch_embed(m->W.tok_emb, m->W.pos_emb, dtok, dtok + n, n, D, x, st);
+        for (int l = 0; l < NL; ++l) {
+            const LayerW& lw = m->layers[l];
+            launch_layernorm<T>(x, nullptr, n, D, lw.ln1_g, lw.ln1_b, a, D, stv, stv + n, st);
+            GemmArgs gq = mk(n, 3 * D, D, a, D, 1, lw.wqkv_t, D, 1);
+            gq.epi = EPI_ACT; gq.bias = lw.bqkv; gq.Ca = qkv; gq.ldca = 3 * D;
+            gemm<T>(c, gq);
+            T* own = kvo + (size_t)l * n * own_stride;
+            PARL_CUDA(cudaMemcpy2DAsync(own + (size_t)step * row2, own_stride * sizeof(T), qkv + D, 3 * D * sizeof(T),
+                                        row2 * sizeof(T), n, cudaMemcpyDeviceToDevice, st));
+            launch_decode_attn<T>(qkv, 3 * D, kvp + (size_t)l * P * row2, own, own_stride, P, step + 1, n, H, D, scale,
+                                  cx, D, st);
+            GemmArgs go = mk(n, D, D, cx, D, 1, lw.wo_t, D, 1);
+            go.epi = EPI_RESID; go.bias = lw.bo; go.resid = x; go.Cf = xm; go.ldc = D;
+            gemm<T>(c, go);
+            launch_layernorm<T>(xm, nullptr, n, D, lw.ln2_g, lw.ln2_b, a, D, stv, stv + n, st);
+            GemmArgs g1 = mk(n, F, D, a, D, 1, lw.w1_t, D, 1);
+            g1.epi = EPI_GELU_ACT; g1.bias = lw.b1; g1.Ca = act; g1.ldca = F;
+            gemm<T>(c, g1);
+            GemmArgs g2 = mk(n, D, F, act, F, 1, lw.w2_t, F, 1);
+            g2.epi = EPI_RESID; g2.bias = lw.b2; g2.resid = xm; g2.Cf = x2; g2.ldc = D;
+            gemm<T>(c, g2);
+            std::swap(x, x2);
+        }
+        launch_layernorm<T>(x, nullptr, n, D, m->W.lnf_g, m->W.lnf_b, a, D, stv, stv + n, st);
+        GemmArgs gh = mk(n, V, D, a, D, 1, m->W.head_w_t, D, 1);
+        gh.epi = EPI_F32; gh.bias = m->W.head_b; gh.Cf = logits; gh.ldc = V;
+        gemm<T>(c, gh, PARL_KC_HEAD);
+        check_launch();
+        PARL_CUDA(cudaMemcpyAsync(rows.data(), logits, (size_t)n * V * 4, cudaMemcpyDeviceToHost, st));
+        PARL_CUDA(cudaStreamSynchronize(st));
+    }
+    ++m->forward_gen;  // bump_forward_generation (model.cpp:865)
+}
+
+void check_sample_args(const parl_config& c, const int32_t* prompt, int P, int max_new, double temperature) {
+    PARL_REQUIRE(P > 0, PARL_E_SHAPE, "empty prompt");
+    PARL_REQUIRE(max_new >= 0, PARL_E_CONFIG, "max_new_tokens must be >= 0");
+    PARL_REQUIRE(temperature >= 0.0, PARL_E_CONFIG, "temperature must be >= 0");
+    PARL_REQUIRE(P + max_new <= c.max_seq_len, PARL_E_SHAPE, "prompt + max_new_tokens exceeds max_seq_len");
+    for (int t = 0; t < P; ++t)
+        PARL_REQUIRE(prompt[t] >= 0 && prompt[t] < c.vocab_size, PARL_E_VOCAB, "token id out of vocabulary");
+}
+}  // namespace
+}  // extern "C++"
+
+parl_status parl_sample_tokens(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int P, int max_new_tokens,
+                               double temperature, uint64_t rng_seed, int32_t* out, int* n_out) {
+    return guarded(ctx, [&] {
+        check_sample_args(m->cfg, prompt, P, max_new_tokens, temperature);
+        if (ctx->prec == PARL_PREC_BF16)
+            sample_group_impl<bf16>(ctx, m, prompt, P, 1, max_new_tokens, temperature, &rng_seed, out, n_out, nullptr);
+        else
+            sample_group_impl<float>(ctx, m, prompt, P, 1, max_new_tokens, temperature, &rng_seed, out, n_out, nullptr);
+    });
+}
+
+parl_status parl_sample_group(parl_ctx_t ctx, parl_model_t m, const int32_t* prompt, int P, int n_seq,
+                              int max_new_tokens, double temperature, const uint64_t* seeds, int32_t* out, int* n_out,
+                              double* logprobs_out) {
+    return guarded(ctx, [&] {
+        check_sample_args(m->cfg, prompt, P, max_new_tokens, temperature);
+        PARL_REQUIRE(n_seq >= 1, PARL_E_CONFIG, "n_seq must be >= 1");
+        if (ctx->prec == PARL_PREC_BF16)
+            sample_group_impl<bf16>(ctx, m, prompt, P, n_seq, max_new_tokens, temperature, seeds, out, n_out,
+                                    logprobs_out);
+        else
+            sample_group_impl<float>(ctx, m, prompt, P, n_seq, max_new_tokens, temperature, seeds, out, n_out,
+                                     logprobs_out);
     });
 }
 

@@ -263,6 +263,82 @@ void launch_attn_bwd(const AttnArgs& a, const T* qkv, const T* out, const T* dou
     PARL_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// KV-cached decoding (the rollout side, sample_tokens model.cpp:843-900): one new query row
+// per sequence against the shared prompt's cached K/V (prefilled once for all sequences of
+// a group) and the sequence's own generated K/V.  Block = (sequence, head), 4 warps stride
+// over the keys with an online softmax each, combined at the end; lane holds Dh/32 elements.
+template <class T>
+__global__ void __launch_bounds__(128) k_decode_attn(const T* __restrict__ q, long ldq, const T* __restrict__ kv_prompt,
+                                                     const T* __restrict__ kv_own, long own_stride, int P, int n_own,
+                                                     int d, int Dh, float scale, T* __restrict__ out, long ldo) {
+    __shared__ float sm_m[4], sm_l[4], sm_o[4][128];
+    const int seq = blockIdx.x, h = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float qv[MAXE], o[MAXE] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k) {
+        const int e = lane + 32 * k;
+        qv[k] = e < Dh ? to_f<T>(q[(long)seq * ldq + h * Dh + e]) : 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = w; j < P + n_own; j += 4) {
+        const T* kr = j < P ? kv_prompt + (long)j * 2 * d + h * Dh : kv_own + seq * own_stride + (long)(j - P) * 2 * d + h * Dh;
+        const T* vr = kr + d;
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < MAXE; ++k) {
+            const int e = lane + 32 * k;
+            if (e < Dh) s = fmaf(qv[k], to_f<T>(kr[e]), s);
+        }
+        s = warp_sum(s) * scale;
+        const float mn = fmaxf(m, s), corr = __expf(m - mn), p = __expf(s - mn);
+        l = l * corr + p;
+#pragma unroll
+        for (int k = 0; k < MAXE; ++k) {
+            const int e = lane + 32 * k;
+            o[k] = o[k] * corr + (e < Dh ? p * to_f<T>(vr[e]) : 0.f);
+        }
+        m = mn;
+    }
+    if (lane == 0) {
+        sm_m[w] = m;
+        sm_l[w] = l;
+    }
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k)
+        if (lane + 32 * k < Dh) sm_o[w][lane + 32 * k] = o[k];
+    __syncthreads();
+    if (w != 0) return;
+    const float mm = fmaxf(fmaxf(sm_m[0], sm_m[1]), fmaxf(sm_m[2], sm_m[3]));
+    float lt = 0.f, c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        c[u] = sm_m[u] == -INFINITY ? 0.f : __expf(sm_m[u] - mm);
+        lt += sm_l[u] * c[u];
+    }
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k) {
+        const int e = lane + 32 * k;
+        if (e >= Dh) continue;
+        float v = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v += sm_o[u][e] * c[u];
+        out[(long)seq * ldo + h * Dh + e] = from_f<T>(v / lt);
+    }
+}
+
+template <class T>
+void launch_decode_attn(const T* q, long ldq, const T* kv_prompt, const T* kv_own, long own_stride, int P, int n_own,
+                        int n_seq, int H, int d, float scale, T* out, long ldo, cudaStream_t st) {
+    k_decode_attn<T><<<dim3(n_seq, H), 128, 0, st>>>(q, ldq, kv_prompt, kv_own, own_stride, P, n_own, d, d / H, scale,
+                                                     out, ldo);
+    PARL_LAUNCHED();
+}
+template void launch_decode_attn<float>(const float*, long, const float*, const float*, long, int, int, int, int, int,
+                                        float, float*, long, cudaStream_t);
+template void launch_decode_attn<bf16>(const bf16*, long, const bf16*, const bf16*, long, int, int, int, int, int,
+                                       float, bf16*, long, cudaStream_t);
+
 template void launch_attn_fwd<float>(const AttnArgs&, const float*, float*, float*, cudaStream_t);
 template void launch_attn_fwd<bf16>(const AttnArgs&, const bf16*, bf16*, float*, cudaStream_t);
 template void launch_attn_bwd<float>(const AttnArgs&, const float*, const float*, const float*, const float*, float*,

@@ -77,42 +77,17 @@ __device__ __forceinline__ void load8(const LP* __restrict__ p, long t, long S, 
 }
 
 template <class LP>
-__global__ void __launch_bounds__(GR_THREADS, 3) k_grpo_tokens(const GrpoArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, 2) k_grpo_tokens(const GrpoArgs a) {
     using Scan = cub::BlockScan<SegAgg, GR_THREADS>;
     using R = std::conditional_t<std::is_same_v<LP, float>, float, double>;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ double s_adv[GR_CHUNK], s_inv[GR_CHUNK];
+    __shared__ R s_adv[GR_CHUNK], s_inv[GR_CHUNK];
     __shared__ int s_first[GR_THREADS], s_last[GR_THREADS];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long c0 = (long)blockIdx.x * GR_CHUNK;
     const long c1 = min((long)a.S, c0 + GR_CHUNK);
-    const int j_lo = a.sample_of[c0], j_hi = a.sample_of[c1 - 1];
-    // per-sample advantage and 1/n_j for the samples this chunk touches
-    if (a.adv_in) {
-        for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) s_adv[j - j_lo] = a.adv_in[j];
-    } else {
-        const int G = a.group_size, g_lo = j_lo / G, g_hi = j_hi / G;
-        for (int grp = g_lo + wid; grp <= g_hi; grp += GR_THREADS / 32) {  // group_advantages[_mean_only]
-            const double* r = a.rewards + (long)grp * G;
-            double s = 0.0;
-            for (int i = lane; i < G; i += 32) s += r[i];
-            const double mean = warp_sum_d(s) / G;
-            double v = 0.0;
-            for (int i = lane; i < G; i += 32) v += (r[i] - mean) * (r[i] - mean);
-            const double sd = sqrt(warp_sum_d(v) / G);
-            for (int i = lane; i < G; i += 32) {
-                const int j = grp * G + i;
-                if (j < j_lo || j > j_hi) continue;
-                s_adv[j - j_lo] = a.mean_only ? r[i] - mean : (sd < 1e-8 ? 0.0 : (r[i] - mean) / sd);
-            }
-        }
-    }
-    for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) {
-        s_inv[j - j_lo] = 1.0 / (double)(a.cu[j + 1] - a.cu[j]);
-        if (a.adv_out && a.cu[j] >= c0) a.adv_out[j] = s_adv[j - j_lo];  // one writer: the sample's first chunk
-    }
-    __syncthreads();
-
+    // this thread's tokens first: their loads are in flight while the prologue below walks its
+    // chain of dependent loads (sample range -> advantages / lengths)
     const long t0 = c0 + (long)tid * GR_ITEMS;
     int s[GR_ITEMS];
     R x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];  // per-token values in the arithmetic type (fp32 hot path)
@@ -126,6 +101,45 @@ __global__ void __launch_bounds__(GR_THREADS, 3) k_grpo_tokens(const GrpoArgs a)
     load8(static_cast<const LP*>(a.lp), t0, c1, x0);
     load8(static_cast<const LP*>(a.old), t0, c1, x1);
     load8(static_cast<const LP*>(a.ref), t0, c1, x2);
+    const int j_lo = a.sample_of[c0], j_hi = a.sample_of[c1 - 1];
+    // per-sample advantage and 1/n_j for the samples this chunk touches
+    if (a.adv_in) {
+        for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) s_adv[j - j_lo] = (R)a.adv_in[j];
+    } else {
+        const int G = a.group_size, g_lo = j_lo / G, g_hi = j_hi / G;
+        for (int grp = g_lo + wid; grp <= g_hi; grp += GR_THREADS / 32) {  // group_advantages[_mean_only]
+            const double* r = a.rewards + (long)grp * G;
+            double s = 0.0;
+            for (int i = lane; i < G; i += 32) s += r[i];
+            const double mean = warp_sum_d(s) / G;
+            double v = 0.0;
+            for (int i = lane; i < G; i += 32) v += (r[i] - mean) * (r[i] - mean);
+            const double sd = sqrt(warp_sum_d(v) / G);
+            for (int i = lane; i < G; i += 32) {
+                const int j = grp * G + i;
+                if (j < j_lo || j > j_hi) continue;
+                s_adv[j - j_lo] = (R)(a.mean_only ? r[i] - mean : (sd < 1e-8 ? 0.0 : (r[i] - mean) / sd));
+            }
+        }
+    }
+    for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) {
+        s_inv[j - j_lo] = R(1) / (R)(a.cu[j + 1] - a.cu[j]);
+        if (a.adv_out && a.cu[j] >= c0) {  // one writer: the sample's first chunk (fp64 advantage)
+            if (a.adv_in) a.adv_out[j] = a.adv_in[j];
+            else {
+                const int G = a.group_size, grp = j / G;
+                const double* r = a.rewards + (long)grp * G;
+                double s = 0.0, v = 0.0;
+                for (int i = 0; i < G; ++i) s += r[i];
+                const double mean = s / G;
+                for (int i = 0; i < G; ++i) v += (r[i] - mean) * (r[i] - mean);
+                const double sd = sqrt(v / G), rj = r[j - grp * G];
+                a.adv_out[j] = a.mean_only ? rj - mean : (sd < 1e-8 ? 0.0 : (rj - mean) / sd);
+            }
+        }
+    }
+    __syncthreads();
+
     const int nv = (int)max(0L, min((long)GR_ITEMS, c1 - t0));  // valid items of this thread
     const R eps = (R)a.eps, beta = (R)a.beta;
     if (a.gran == 0) {  // token granularity (grpo.cpp:119-131)
@@ -143,12 +157,12 @@ __global__ void __launch_bounds__(GR_THREADS, 3) k_grpo_tokens(const GrpoArgs a)
             int c;
             clip_eval<R>(lp, old, (R)s_adv[jl], eps, cv, cg, c);
             const R d = ref - lp, em = expm1(d);  // eval_kl, grpo.cpp:89-93
-            const double g = s_inv[jl] * ((double)cg + (double)beta * (double)em);
+            const R g = s_inv[jl] * (cg + beta * em);
             x0[i] = cv;
             x1[i] = em - d;
             x2[i] = (R)c;
-            up4[i] = (float)(a.up_scale * g);
-            if (a.up_f64) a.up_f64[t0 + i] = a.up_scale * g;
+            up4[i] = (float)((R)a.up_scale * g);
+            if (a.up_f64) a.up_f64[t0 + i] = a.up_scale * (double)g;
         }
         if (a.up_f32) {
             if (nv == GR_ITEMS && ((reinterpret_cast<uintptr_t>(a.up_f32 + t0) & 15) == 0)) {
@@ -167,32 +181,36 @@ __global__ void __launch_bounds__(GR_THREADS, 3) k_grpo_tokens(const GrpoArgs a)
     __syncthreads();
     const int prev_last = tid > 0 ? s_last[tid - 1] : -2;
     const int next_first = tid + 1 < GR_THREADS ? s_first[tid + 1] : -2;
-    SegAgg agg{0.0, 0.0, 0.0, (tid == 0 || first != prev_last || first != last) ? 1 : 0};
+    // the thread's last run (in R, at most 8 terms), widened once
+    R t0a = 0, t0b = 0, t0c = 0;
     for (int i = 0; i < nv; ++i)
         if (s[i] == last) {
-            agg.a += (double)x0[i];
-            agg.b += (double)x1[i];
-            agg.c += (double)x2[i];
+            t0a += x0[i];
+            t0b += x1[i];
+            t0c += x2[i];
         }
+    SegAgg agg{(double)t0a, (double)t0b, (double)t0c, (tid == 0 || first != prev_last || first != last) ? 1 : 0};
     SegAgg carry;
     Scan(scan_tmp).ExclusiveScan(agg, carry, SegOp());
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    double c0a = 0.0, c0b = 0.0, c0c = 0.0;  // carried into the thread's first run
     if (tid > 0 && nv > 0 && first == prev_last) {
-        r0 = carry.a;
-        r1 = carry.b;
-        r2 = carry.c;
+        c0a = carry.a;
+        c0b = carry.b;
+        c0c = carry.c;
     }
+    R r0 = 0, r1 = 0, r2 = 0;
     for (int i = 0; i < nv; ++i) {
-        r0 += (double)x0[i];
-        r1 += (double)x1[i];
-        r2 += (double)x2[i];
+        r0 += x0[i];
+        r1 += x1[i];
+        r2 += x2[i];
         const bool end = (i + 1 < nv) ? (s[i + 1] != s[i]) : (next_first != s[i]);
         if (end) {
             double* o = a.slots + 3 * ((long)s[i] + blockIdx.x);
-            o[0] = r0;
-            o[1] = r1;
-            o[2] = r2;
-            r0 = r1 = r2 = 0.0;
+            o[0] = c0a + (double)r0;
+            o[1] = c0b + (double)r1;
+            o[2] = c0c + (double)r2;
+            r0 = r1 = r2 = 0;
+            c0a = c0b = c0c = 0.0;
         }
     }
 }

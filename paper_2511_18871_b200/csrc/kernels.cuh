@@ -212,6 +212,12 @@ void launch_attn_fwd(const AttnArgs& a, const T* qkv, T* out, float* lse, cudaSt
 // tcgen05 backward (k_attn_tc.cu): dqkv from dO, lse and D = rowsum(dO*O)
 bool attn_bwd_tc(const AttnArgs& a, const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dsum,
                  bf16* dqkv, cudaStream_t st);
+// KV-cached decode attention: n_seq query rows (q, row stride ldq, head h at h*Dh) against
+// the shared prompt cache kv_prompt [P x 2d] (K | V) and each sequence's own cache
+// kv_own + seq * own_stride [n_own x 2d]
+template <class T>
+void launch_decode_attn(const T* q, long ldq, const T* kv_prompt, const T* kv_own, long own_stride, int P, int n_own,
+                        int n_seq, int H, int d, float scale, T* out, long ldo, cudaStream_t st);
 template <class T>
 void launch_attn_dsum(const AttnArgs& a, const T* out, const T* dout, float* dsum, cudaStream_t st);
 template <class T>

@@ -143,6 +143,7 @@ def _load():
         "parl_checkpoint_save": [vp, C.c_char_p], "parl_checkpoint_load": [vp, C.c_char_p, C.POINTER(vp)],
         "parl_model_config": [vp, C.POINTER(_Config)],
         "parl_sample_tokens": [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_uint64, vp, C.POINTER(C.c_int)],
+        "parl_sample_group": [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_double, vp, vp, vp, vp],
         "parl_ctx_profile": [vp, C.c_int], "parl_ctx_set_recompute": [vp, C.c_int], "parl_act_recompute": [vp],
         "parl_ctx_profile_read": [vp, C.c_int, f64p, f64p, C.POINTER(C.c_long)],
         "parl_grad_set_micro_steps": [vp, C.c_int], "parl_grad_add_micro_steps": [vp, C.c_int],
@@ -610,6 +611,30 @@ def sample_tokens(params: "ModelParams", prompt, max_new_tokens: int, temperatur
                                   float(temperature), int(rng_seed), out.ctypes.data_as(C.c_void_p), C.byref(n)),
            params.ctx.h)
     return out[:n.value]
+
+
+def sample_group(params: "ModelParams", prompt, n_seq: int, max_new_tokens: int, temperature: float, seeds,
+                 want_logprobs: bool = False):
+    """The G rollouts of one prompt on the KV-cached decoder (parl_sample_group): sequence k is
+    sample_tokens(prompt, max_new_tokens, temperature, seeds[k]); with want_logprobs also each
+    sampled token's log-prob (the rollout-side old_logprobs).  Returns a list of token arrays
+    (and of log-prob arrays)."""
+    pr = np.ascontiguousarray(np.asarray(prompt, dtype=np.int32))
+    sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    if len(sd) != n_seq:
+        raise ShapeError("one seed per sequence")
+    mx = max(int(max_new_tokens), 1)
+    out = np.zeros(n_seq * mx, np.int32)
+    n = np.zeros(n_seq, np.int32)
+    lp = np.zeros(n_seq * mx, np.float64) if want_logprobs else None
+    _check(LIB.parl_sample_group(params.ctx.h, params.h, pr.ctypes.data_as(C.c_void_p), len(pr), int(n_seq),
+                                 int(max_new_tokens), float(temperature), sd.ctypes.data_as(C.c_void_p),
+                                 out.ctypes.data_as(C.c_void_p), n.ctypes.data_as(C.c_void_p),
+                                 lp.ctypes.data_as(C.c_void_p) if lp is not None else None), params.ctx.h)
+    toks = [out[k * mx:k * mx + n[k]] for k in range(n_seq)]
+    if not want_logprobs:
+        return toks
+    return toks, [lp[k * mx:k * mx + n[k]] for k in range(n_seq)]
 
 
 def extract_response_logprobs(logprobs, packed: PackedGroup):

@@ -63,3 +63,24 @@ def test_comm_unique_id_without_gpu(lib):
     buf = C.create_string_buffer(128)
     rc = lib.parl_comm_unique_id(buf)
     assert rc in (0, 10)
+
+
+def test_dropin_headers_compile():
+    """include/parl/*.hpp and parl_gpu.hpp compile as C++20 on their own (no CUDA headers)."""
+    src = '#include "parl_gpu.hpp"\nint main() { parl::ModelConfig c; c.validate(); return 0; }\n'
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), "-x", "c++", "-"],
+                       input=src, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj"), reason="needs the reference sources")
+def test_reference_code_compiles_against_dropin():
+    """The reference's pipeline / rollout / tasks / gradcheck sources and its test suites compile
+    UNMODIFIED with include/parl/ shadowing model.hpp / packing.hpp / grpo.hpp / errors.hpp."""
+    inc = ["-I" + os.path.join(ROOT, "tests", "cpp", "doctest"), "-I" + os.path.join(ROOT, "include"),
+           "-I/root/reference/proj/include"]
+    for f in ("src/pipeline.cpp", "src/rollout.cpp", "src/gradcheck.cpp", "tests/test_pipeline.cpp",
+              "tests/test_model.cpp", "tests/test_packing.cpp", "tests/test_grpo.cpp"):
+        r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", *inc, "/root/reference/proj/" + f],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, (f, r.stderr[-3000:])

@@ -66,3 +66,33 @@ def test_score_logprobs_matches_oracle(P, orc):
     labels[len(prompt):] = resp
     want = orc.forward(Cfg(*CFGS["tiny"]), pm.flat(), toks, np.arange(len(toks)), labels)
     assert len(lp) == len(resp) and np.abs(lp - want).max() < 2e-5
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_kv_cached_group_decoder(P, prec):
+    """parl_sample_group: the G rollouts of one prompt on one shared prompt cache give, sequence
+    by sequence, what sample_tokens gives with that sequence's seed (fp32: the reference's own
+    tokens, checked above); the returned log-probs are score_logprobs of the sampled tokens."""
+    ctx = P.Context(0, P.PREC_FP32 if prec == "fp32" else P.PREC_BF16)
+    cfg = CFGS["tiny"] if prec == "fp32" else CFGS["c1"]
+    z = load("sample_tokens.npz")
+    name = "tiny" if prec == "fp32" else "c1"
+    pm = P.ModelParams.init(P.ModelConfig(*cfg), 41 if name == "tiny" else 7, ctx)
+    prompt = [5, 9, 11, 4, 7, 3, 12]
+    seeds = [11, 12, 13, 99, 7]
+    for temp in (0.0, 0.8):
+        toks, lps = P.sample_group(pm, prompt, len(seeds), 20, temp, seeds, want_logprobs=True)
+        for k, s in enumerate(seeds):
+            want = P.sample_tokens(pm, prompt, 20, temp, s)
+            if prec == "fp32":
+                assert np.array_equal(toks[k], want), (temp, k, toks[k], want)
+            ref_lp = P.score_logprobs(pm, prompt, toks[k])
+            tol = 1e-4 if prec == "fp32" else 0.1
+            assert np.abs(lps[k] - ref_lp).max() < tol
+    if prec == "fp32":  # the fixture's reference runs, now through the cached decoder
+        for k in range(len(z["names"])):
+            if str(z["names"][k]) != "tiny" or int(z["wseeds"][k]) != 41:
+                continue
+            want = z["tokens"][k][z["tokens"][k] >= 0]
+            got = P.sample_group(pm, z["prompts"][k], 1, 24, float(z["temps"][k]), [int(z["seeds"][k])])[0]
+            assert np.array_equal(got, want)

@@ -84,4 +84,6 @@ def test_bf16_parity_at_width(P, ctx16, case):
     assert m["grad_rel_global"] <= tol("grad_rel_global"), m
     assert 1 - m["grad_cos"] <= TOL_FACTOR * (1 - floor["grad_cos"]), m
     assert m["bk_abs"] <= max(tol("bk_abs"), 1e-2), m  # attn.bk <= 1e-2 absolute in bf16
-    assert m["obj_rel"] <= max(tol("obj_rel"), 1e-3), m
+    # the objective sums advantage-weighted ratios whose advantages sum to zero: its relative error
+    # is ill-conditioned (cancellation), so SURVEY §8c's 1e-2 bound holds when it exceeds 3x floor
+    assert m["obj_rel"] <= max(tol("obj_rel"), 1e-2), m
