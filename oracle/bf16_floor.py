@@ -93,15 +93,28 @@ def measure(name, device="cpu"):
 
 
 def main():
-    names = sys.argv[1:] or list(CASES)
+    """python -m oracle.bf16_floor [case ...] [--device cuda] [--out path]: the widest case (c3w)
+    needs ~60 GB for its fp64 weights and gradients and runs on a GPU box's fp64 torch."""
+    args, device, out = [], "cpu", OUT
+    argv = sys.argv[1:]
+    while argv:
+        a = argv.pop(0)
+        if a == "--device":
+            device = argv.pop(0)
+        elif a == "--out":
+            out = argv.pop(0)
+        else:
+            args.append(a)
+    names = args or list(CASES)
     res = {}
-    if os.path.exists(OUT):
-        with open(OUT) as f:
+    if os.path.exists(out):
+        with open(out) as f:
             res = json.load(f)
     for n in names:
-        res[n] = measure(n)
+        res[n] = measure(n, device)
+        res[n]["device"] = device
         print(n, json.dumps(res[n]), flush=True)
-        with open(OUT, "w") as f:
+        with open(out, "w") as f:
             json.dump(res, f, indent=1)
 
 

@@ -2960,9 +2960,13 @@ parl_status parl_grad_allreduce(parl_ctx_t ctx, parl_grad_t gr) {
             return;
         }
         float* G = static_cast<float*>(gr->g.p);
-        static const bool sparse = [] {  // PARL_SPARSE_EMB=0: dense exchange of the whole buffer
+        // PARL_SPARSE_EMB=1: exchange only the token-embedding rows some rank touched (a union of
+        // row flags, then a compacted allreduce).  Its row count must reach the host to size the
+        // NCCL call, a stream synchronisation mid-exchange, so the default is one dense allreduce
+        // of the whole buffer (no host round trip; the rows are ~28% of the C2 gradient).
+        static const bool sparse = [] {
             const char* e = std::getenv("PARL_SPARSE_EMB");
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         const int V = gr->cfg.vocab_size, D = gr->cfg.d_model;
         size_t dense0 = 0;  // first element exchanged densely

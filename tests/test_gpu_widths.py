@@ -52,7 +52,10 @@ def test_bf16_parity_at_width(P, ctx16, case):
     from oracle import bf16_floor as BF
     from oracle import torch_ref as TR
 
-    floor = _floors()[case]
+    floors = _floors()
+    if case not in floors:
+        pytest.skip(f"no measured floor for {case} (python -m oracle.bf16_floor {case} --device cuda)")
+    floor = floors[case]
     cfg_o, Pn, lens = BF.CASES[case]
     w, wo, wr, prompt, resp, adv = BF.case_inputs(case, cfg_o, Pn, lens)
     cfg = P.ModelConfig(cfg_o.vocab, cfg_o.d_model, cfg_o.n_layers, cfg_o.n_heads, cfg_o.d_ff, cfg_o.max_seq)
