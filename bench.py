@@ -15,7 +15,8 @@ timed; `e2e` = the same through the public C-ABI from pinned host buffers with
 H2D/D2H inside the timed region; `roofline` = dominant kernel class timed with
 CUDA events on its launch stream during the timed region; `cpu_baseline` = the
 reference (oracle/_ref, built from the reference's own sources) on a bounded
-sample, FLOP-scaled to this workload.
+sample it really executes, measured tokens/s (a FLOP-model extrapolation to this
+workload is reported separately).  C2 packs 4 prompt groups per sequence (--pack).
 """
 from __future__ import annotations
 
@@ -34,9 +35,11 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # BASELINE.json configs[0]: tiny decoder, fp32 (CPU-runnable oracle case)
-    "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=8),
+    "c1": dict(vocab=4096, d=256, L=2, H=4, F=1024, max_seq=576, P=64, G=4, R=128, prec="fp32", groups=8, pack=4),
     # BASELINE.json configs[1]: Qwen2.5-0.5B-shaped random-init tri-model, G=8, 512+1k, bf16, single B200
-    "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=64),
+    # 4 prompt groups per packed sequence (each group shared-prompt packed as pack_group does)
+    "c2": dict(vocab=151936, d=896, L=24, H=14, F=4864, max_seq=16384, P=512, G=8, R=1024, prec="bf16", groups=64,
+               pack=4),
     # configs[2]: Qwen2.5-7B-shaped tri-model, G=16, 1k prompt + 4k responses (T=66,560 per group),
     # one group per rank (prompt groups sharded over the GPUs); runs with activation recomputation
     "c3": dict(vocab=152064, d=3584, L=28, H=28, F=18944, max_seq=66560, P=1024, G=16, R=4096, prec="bf16",
@@ -319,7 +322,7 @@ def run_ours(args, c):
         prompts.append(rng.integers(4, c["vocab"], Pn).astype(np.int32))
         resps.append(rng.integers(4, c["vocab"], T - Pn).astype(np.int32))
         rewards.append(rng.random(G))
-    K = max(1, args.pack)  # prompt groups packed into one sequence per micro-step (f4)
+    K = max(1, args.pack or c.get("pack", 1))  # prompt groups packed into one sequence per micro-step (f4)
     chunks = [list(range(i, min(i + K, ng))) for i in range(0, ng, K)]
     group = P.Group(T * K, G * K, ctx)
 
@@ -506,7 +509,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--groups", type=int, default=0, help="global batch: prompt groups per step (all ranks)")
-    ap.add_argument("--pack", type=int, default=1, help="prompt groups packed into one sequence per micro-step")
+    ap.add_argument("--pack", type=int, default=0,
+                    help="prompt groups packed into one sequence per micro-step (0: the config's default)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--launch-list", action="store_true",
                     help="run one step inside an NVTX range 'step' (for ncu launch lists) and exit")

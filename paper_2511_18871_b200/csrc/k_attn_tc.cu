@@ -85,8 +85,7 @@ struct PairSmem {
     static constexpr int OFF_OST = OFF_V + KVS * TILE;       // [8 softmax warps][32 rows x 128 B] output staging
     static constexpr int OFF_BAR = OFF_OST + 8 * 4096;
     static constexpr int OFF_RING = OFF_BAR + 256;           // [4] item ids of the dynamic queue
-    static constexpr int OFF_META = OFF_RING + 64;           // [256 softmax threads] next item's row metadata (Dh 64)
-    static constexpr int TOTAL = OFF_META + (DH == 64 ? 256 * 48 : 0) + 1024;
+    static constexpr int TOTAL = OFF_RING + 64 + 1024;
 };
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
@@ -658,14 +657,10 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const uint32_t VIS = w ? VIS1 : VIS0, FULL = w ? FULL1 : FULL0;
         const float c2 = a.scale_log2;
         int cS = 0;
-        // the next item's metadata is prefetched (its chain of dependent loads off the critical
-        // path) into this thread's shared-memory slot, not registers: the score row needs them
-        ItemMeta* my_meta = reinterpret_cast<ItemMeta*>(smem + L::OFF_META) + (warp * 32 + lane);
-        *my_meta = fetch_item(0, w, r);
-        for (int k = 0;; ++k) {
-            const ItemMeta cur = *my_meta;
-            if (cur.p < 0) break;
-            *my_meta = fetch_item(k + 1, w, r);
+        ItemMeta nx = fetch_item(0, w, r);
+        for (int k = 0; nx.p >= 0; ++k) {
+            const ItemMeta cur = nx;
+            nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
             const int p = cur.p, h = cur.h, i = cur.i, l0 = cur.l0, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
@@ -707,7 +702,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 const float m_new = need ? mxl : m_used;
                 const float alpha = need ? tc::ex2_approx(m_used - m_new) : 1.f;
                 const float mb = m_new == -INFINITY ? 0.f : m_new;
-                // P = exp2(S * c - m) -> bf16 in registers, while the previous PV still runs
+                // P = exp2(S * c - m) -> bf16 (registers)
                 float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
                 uint32_t pk[64];
 #pragma unroll
@@ -726,21 +721,21 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     tc::mbar_wait(&o_done[w], (cS - 1) & 1);
                     tc::tc_fence_after();
                 }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tc::tmem_st16(t_p + w * PCOL + c * 16 + lane_off, pk + 16 * c);
-                // O *= alpha (rare: the max grew by more than 2^8), 16 columns at a time in place;
-                // before p_full, i.e. before the next PV accumulates
+                if (q4 == 0) ATTN_TRACE(w, cS, 4);
                 if (!first && __any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-                    for (int c = 0; c < DH / 16; ++c) {
-                        uint32_t o[16];
-                        tc::tmem_ld16(t_o + w * DH + c * 16 + lane_off, o);
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
-                        tc::tmem_st16(t_o + w * DH + c * 16 + lane_off, o);
+                    for (int c = 0; c < DH / 32; ++c) {
+                        float o[32];
+                        tc::tmem_ld32(t_o + w * DH + c * 32 + lane_off, o);
+                        uint32_t wv[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) wv[q] = __float_as_uint(o[q] * alpha);
+                        tc::tmem_st16(t_o + w * DH + c * 32 + lane_off, wv);
+                        tc::tmem_st16(t_o + w * DH + c * 32 + 16 + lane_off, wv + 16);
                     }
                 }
-                if (q4 == 0) ATTN_TRACE(w, cS, 4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tc::tmem_st16(t_p + w * PCOL + c * 16 + lane_off, pk + 16 * c);
                 tc::tmem_st_wait();
                 tc::tc_fence_before();
                 __syncwarp();

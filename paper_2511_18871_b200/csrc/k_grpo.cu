@@ -1,7 +1,7 @@
 // K7: the GRPO loss over every scored token of a micro-batch, one coalesced,
 // vectorised pass (grpo.cpp:24-151 + pipeline.cpp:127-139).
 //
-//   k_grpo_tokens  grid over the S scored tokens, CHUNK tokens per block (8 per
+//   k_grpo_tokens  grid over the S scored tokens, CHUNK tokens per block (4 per
 //                  thread, 16-byte loads of the three log-prob vectors and the
 //                  token -> sample map).  Group advantages (grpo.cpp:24-48) are
 //                  rebuilt in shared memory by every block for the samples its
@@ -32,7 +32,7 @@ namespace parl_gpu {
 
 namespace {
 
-constexpr int GR_THREADS = 256, GR_ITEMS = 8, GR_CHUNK = GR_THREADS * GR_ITEMS;
+constexpr int GR_THREADS = 256, GR_ITEMS = 4, GR_CHUNK = GR_THREADS * GR_ITEMS;
 
 // eval_clip (grpo.cpp:64-80) in the arithmetic of R
 template <class R>
@@ -66,9 +66,11 @@ template <class LP, class R>
 __device__ __forceinline__ void load8(const LP* __restrict__ p, long t, long S, R* v) {
     if constexpr (std::is_same_v<LP, float>) {
         if (t + GR_ITEMS <= S && ((reinterpret_cast<uintptr_t>(p + t) & 15) == 0)) {
-            const float4 x = *reinterpret_cast<const float4*>(p + t), y = *reinterpret_cast<const float4*>(p + t + 4);
-            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-            v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+#pragma unroll
+            for (int q = 0; q < GR_ITEMS; q += 4) {
+                const float4 x = *reinterpret_cast<const float4*>(p + t + q);
+                v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+            }
             return;
         }
     }
@@ -77,7 +79,7 @@ __device__ __forceinline__ void load8(const LP* __restrict__ p, long t, long S, 
 }
 
 template <class LP>
-__global__ void __launch_bounds__(GR_THREADS, 2) k_grpo_tokens(const GrpoArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, 4) k_grpo_tokens(const GrpoArgs a) {
     using Scan = cub::BlockScan<SegAgg, GR_THREADS>;
     using R = std::conditional_t<std::is_same_v<LP, float>, float, double>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -92,8 +94,11 @@ __global__ void __launch_bounds__(GR_THREADS, 2) k_grpo_tokens(const GrpoArgs a)
     int s[GR_ITEMS];
     R x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];  // per-token values in the arithmetic type (fp32 hot path)
     if (t0 + GR_ITEMS <= c1 && ((reinterpret_cast<uintptr_t>(a.sample_of + t0) & 15) == 0)) {
-        const int4 p = *reinterpret_cast<const int4*>(a.sample_of + t0), q = *reinterpret_cast<const int4*>(a.sample_of + t0 + 4);
-        s[0] = p.x; s[1] = p.y; s[2] = p.z; s[3] = p.w; s[4] = q.x; s[5] = q.y; s[6] = q.z; s[7] = q.w;
+#pragma unroll
+        for (int q = 0; q < GR_ITEMS; q += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(a.sample_of + t0 + q);
+            s[q] = v.x; s[q + 1] = v.y; s[q + 2] = v.z; s[q + 3] = v.w;
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < GR_ITEMS; ++i) s[i] = (t0 + i < c1) ? a.sample_of[t0 + i] : -1;
@@ -166,8 +171,9 @@ __global__ void __launch_bounds__(GR_THREADS, 2) k_grpo_tokens(const GrpoArgs a)
         }
         if (a.up_f32) {
             if (nv == GR_ITEMS && ((reinterpret_cast<uintptr_t>(a.up_f32 + t0) & 15) == 0)) {
-                *reinterpret_cast<float4*>(a.up_f32 + t0) = make_float4(up4[0], up4[1], up4[2], up4[3]);
-                *reinterpret_cast<float4*>(a.up_f32 + t0 + 4) = make_float4(up4[4], up4[5], up4[6], up4[7]);
+#pragma unroll
+                for (int q = 0; q < GR_ITEMS; q += 4)
+                    *reinterpret_cast<float4*>(a.up_f32 + t0 + q) = make_float4(up4[q], up4[q + 1], up4[q + 2], up4[q + 3]);
             } else {
                 for (int i = 0; i < nv; ++i) a.up_f32[t0 + i] = up4[i];
             }

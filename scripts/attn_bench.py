@@ -3,7 +3,12 @@
 import ctypes as C, os, sys, math
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2511_18871_b200 import parl as P
+# the library directly (PARL_LIB: A/B of another build; no dependency on parl.py's symbol list)
+LIB = C.CDLL(os.environ.get("PARL_LIB") or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                          "paper_2511_18871_b200", "libparl_gpu.so"))
+LIB.parl_last_error.restype = C.c_char_p
+class P:  # noqa: N801
+    LIB = LIB
 f = P.LIB.parl_debug_attn_bf16
 f.restype = C.c_int
 f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 6
