@@ -85,10 +85,18 @@ struct PairSmem {
     static constexpr int OFF_OST = OFF_V + KVS * TILE;       // [8 softmax warps][32 rows x 128 B] output staging
     static constexpr int OFF_BAR = OFF_OST + 8 * 4096;
     static constexpr int OFF_RING = OFF_BAR + 256;           // [4] item ids of the dynamic queue
-    static constexpr int TOTAL = OFF_RING + 64 + 1024;
+    static constexpr int OFF_L0 = OFF_RING + 64;             // Dh 64: [2 items][256 softmax threads] row range start
+    static constexpr int TOTAL = OFF_L0 + (DH == 64 ? 2 * 256 * 4 : 0) + 1024;
 };
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+
+// bits [lo, hi) of the 32-column word starting at column c0 (lo / hi relative to the tile)
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int c0) {
+    const int a = min(max(lo - c0, 0), 32), b = min(max(hi - c0, 0), 32);
+    const uint32_t ub = b >= 32 ? 0xffffffffu : ((1u << b) - 1u), ua = a >= 32 ? 0xffffffffu : ((1u << a) - 1u);
+    return ub & ~ua;
+}
 
 #ifdef PARL_ATTN_TRACE
 // phase timestamps of CTA 0 (build with -DPARL_ATTN_TRACE; read by parl_debug_attn_trace)
@@ -212,6 +220,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         const int4 f = row_ok ? a.seg_info[a.seg[m.i]] : make_int4(0, 0, 0, 0);
         const bool resp = row_ok && f.y >= 0;
         m.l0 = f.x;
+        // Dh 64: the score row leaves no register for it; kept in shared memory by item parity
+        if constexpr (DH == 64) reinterpret_cast<int*>(smem + L::OFF_L0)[(li & 1) * 256 + warp * 32 + lane] = f.x;
         m.e0 = !row_ok ? 0 : (resp ? f.y : m.i + 1);
         m.b1 = resp ? f.z : 0;
         m.e1 = resp ? m.i + 1 : 0;
@@ -406,14 +416,14 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     tc::tmem_ld_wait();
                     if (q4 == 0) ATTN_TRACE(w, cS, 2);
                     if (!(f & FULL)) {
+                        // allowed keys [l0, e0) u [b1, e1) as a column bitmask (no per-element range math)
                         const int j0 = (int)(f & 0xffffff) * 128 + hc * 64;
-                        const int lo0 = min(max(l0 - j0, 0), 64), h0 = min(max(e0 - j0, 0), 64);
-                        const int l1 = min(max(b1 - j0, 0), 64), h1 = min(max(e1 - j0, 0), 64);
+                        uint32_t mw[2];
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) {
-                            const bool ok = ((j >= lo0) & (j < h0)) | ((j >= l1) & (j < h1));
-                            sv[j] = ok ? sv[j] : -INFINITY;
-                        }
+                        for (int q = 0; q < 2; ++q)
+                            mw[q] = range_bits(l0 - j0, e0 - j0, 32 * q) | range_bits(b1 - j0, e1 - j0, 32 * q);
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) sv[j] = ((mw[j >> 5] >> (j & 31)) & 1u) ? sv[j] : -INFINITY;
                     }
                     float mq[4];
 #pragma unroll
@@ -661,7 +671,8 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
         for (int k = 0; nx.p >= 0; ++k) {
             const ItemMeta cur = nx;
             nx = fetch_item(k + 1, w, r);  // the next item's chain of dependent loads, off the critical path
-            const int p = cur.p, h = cur.h, i = cur.i, l0 = cur.l0, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
+            const int p = cur.p, h = cur.h, i = cur.i, e0 = cur.e0, b1 = cur.b1, e1 = cur.e1;
+            const int* l0_slot = reinterpret_cast<const int*>(smem + L::OFF_L0) + (k & 1) * 256 + warp * 32 + lane;
             const bool row_ok = i < a.T;
             float m_used = -INFINITY, l = 0.f;
             bool first = true;
@@ -679,14 +690,14 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 if (lane == 0) tc::mbar_arrive(&s_free[w]);  // the next S of this tile may be issued
                 if (q4 == 0) ATTN_TRACE(w, cS, 2);
                 if (!(f & FULL)) {
-                    const int j0 = (int)(f & 0xffffff) * 128;
-                    const int lo0 = min(max(l0 - j0, 0), 128), h0 = min(max(e0 - j0, 0), 128);
-                    const int l1 = min(max(b1 - j0, 0), 128), h1 = min(max(e1 - j0, 0), 128);
+                    // allowed keys [l0, e0) u [b1, e1) as a column bitmask (no per-element range math)
+                    const int j0 = (int)(f & 0xffffff) * 128, l0 = *l0_slot;
+                    uint32_t mw[4];
 #pragma unroll
-                    for (int j = 0; j < 128; ++j) {
-                        const bool ok = ((j >= lo0) & (j < h0)) | ((j >= l1) & (j < h1));
-                        sv[j] = ok ? sv[j] : -INFINITY;
-                    }
+                    for (int q = 0; q < 4; ++q)
+                        mw[q] = range_bits(l0 - j0, e0 - j0, 32 * q) | range_bits(b1 - j0, e1 - j0, 32 * q);
+#pragma unroll
+                    for (int j = 0; j < 128; ++j) sv[j] = ((mw[j >> 5] >> (j & 31)) & 1u) ? sv[j] : -INFINITY;
                 }
                 float mq[4];  // four independent max chains
 #pragma unroll
