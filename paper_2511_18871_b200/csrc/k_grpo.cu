@@ -1,30 +1,32 @@
 // K7: the GRPO loss over every scored token of a micro-batch, one coalesced,
 // vectorised pass (grpo.cpp:24-151 + pipeline.cpp:127-139).
 //
-//   k_grpo_tokens  grid over the S scored tokens, CHUNK tokens per block (4 per
-//                  thread, 16-byte loads of the three log-prob vectors and the
-//                  token -> sample map).  Group advantages (grpo.cpp:24-48) are
-//                  rebuilt in shared memory by every block for the samples its
-//                  chunk touches, so the rewards never take a separate launch.
-//                  Token granularity writes the backward seed
-//                      upstream[t] = up_scale * (1/n_j) (clip_grad - beta kl_grad)
+//   k_grpo_tokens  warp-autonomous: each warp walks a contiguous range of
+//                  warp_tokens scored tokens in spans of 128 (4 per lane,
+//                  16-byte loads of the three log-prob vectors and the
+//                  token -> sample map); no block barrier anywhere.  The group
+//                  advantages (grpo.cpp:24-48) and 1/n_j of the samples a span
+//                  touches are rebuilt by the warp's lanes into a per-warp
+//                  table only when the span leaves the samples already there
+//                  (once per sample boundary), so the rewards take no separate
+//                  launch.  Token granularity writes the backward seed
+//                      upstream[t] = up_scale * (1/n_j) (clip_grad + beta kl_grad)
 //                  (pipeline.cpp:138 pushes up_scale = -1) and reduces the
 //                  per-sample sums {clip value, kl value, clipped} with a
-//                  segmented block scan; each (sample, block) partial goes to
-//                  its own slot (index sample + block), so the finisher adds them
-//                  in a fixed order: deterministic, no atomics.
-//   k_grpo_finish  one block: per-sample terms (SampleTerms, grpo.hpp:64-70) and
-//                  the running stats (pipeline.cpp:131-137), fixed-order tree.
+//                  segmented warp scan whose open run carries from span to span;
+//                  each (sample, warp range) partial goes to its own slot (index
+//                  sample + range), so the finisher adds them in a fixed order:
+//                  deterministic, no atomics.
+//   k_grpo_finish  warp per sample: per-sample terms (SampleTerms, grpo.hpp:64-70); the
+//                  last block adds the running stats (pipeline.cpp:131-137), fixed order.
 //   k_grpo_bcast   sequence granularity only: broadcast g_j to every token.
 //
 // Hot path inputs are the fp32 device log-probs: the ratio / KL terms are then
-// evaluated in fp32 (expf / expm1f, full precision) and every sum in fp64, which
-// keeps the pass on the HBM roofline (fp64 exp + expm1 per token would bound it
-// on the fp64 pipe at stress sizes).  The operator API
+// evaluated in fp32 (expf / expm1f, full precision) and every cross-lane sum in
+// fp64, which keeps the pass on the HBM roofline (fp64 exp + expm1 per token would
+// bound it on the fp64 pipe at stress sizes).  The operator API
 // (parl_per_sample_terms / parl_grpo_microbatch_loss) passes fp64 inputs and runs
 // the same kernels with fp64 arithmetic throughout.
-#include <cub/block/block_scan.cuh>
-
 #include "internal.cuh"
 #include "kernels.cuh"
 
@@ -32,7 +34,7 @@ namespace parl_gpu {
 
 namespace {
 
-constexpr int GR_THREADS = 256, GR_ITEMS = 4, GR_CHUNK = GR_THREADS * GR_ITEMS;
+constexpr int GR_ITEMS = 4, GR_SPAN = 32 * GR_ITEMS, GR_WARPS = 8, GR_MAX_ITERS = 8;
 
 // eval_clip (grpo.cpp:64-80) in the arithmetic of R
 template <class R>
@@ -50,188 +52,273 @@ __device__ __forceinline__ void clip_eval(R lp, R old, R A, R eps, R& val, R& gr
     }
 }
 
-struct SegAgg {
-    double a, b, c;
-    int reset;  // a segment boundary lies in (or at the start of) this span: earlier values do not carry in
-};
-
-struct SegOp {
-    __device__ __forceinline__ SegAgg operator()(const SegAgg& x, const SegAgg& y) const {
-        if (y.reset) return y;
-        return {x.a + y.a, x.b + y.b, x.c + y.c, x.reset};
-    }
-};
-
+// GR_ITEMS consecutive values from t (zero beyond the range end e); one or two 16-byte loads
 template <class LP, class R>
-__device__ __forceinline__ void load8(const LP* __restrict__ p, long t, long S, R* v) {
-    if constexpr (std::is_same_v<LP, float>) {
-        if (t + GR_ITEMS <= S && ((reinterpret_cast<uintptr_t>(p + t) & 15) == 0)) {
-#pragma unroll
-            for (int q = 0; q < GR_ITEMS; q += 4) {
-                const float4 x = *reinterpret_cast<const float4*>(p + t + q);
-                v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
-            }
-            return;
+__device__ __forceinline__ void load_items(const LP* __restrict__ p, long t, long e, R* v) {
+    if (t + GR_ITEMS <= e && ((reinterpret_cast<uintptr_t>(p + t) & 15) == 0)) {
+        if constexpr (std::is_same_v<LP, float>) {
+            const float4 x = __ldcs(reinterpret_cast<const float4*>(p + t));
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+            const double2 x = __ldcs(reinterpret_cast<const double2*>(p + t));
+            const double2 y = __ldcs(reinterpret_cast<const double2*>(p + t + 2));
+            v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
         }
+        return;
     }
 #pragma unroll
-    for (int i = 0; i < GR_ITEMS; ++i) v[i] = (t + i < S) ? (R)p[t + i] : R(0);
+    for (int i = 0; i < GR_ITEMS; ++i) v[i] = (t + i < e) ? (R)p[t + i] : R(0);
 }
 
-template <class LP>
-__global__ void __launch_bounds__(GR_THREADS, 4) k_grpo_tokens(const GrpoArgs a) {
-    using Scan = cub::BlockScan<SegAgg, GR_THREADS>;
-    using R = std::conditional_t<std::is_same_v<LP, float>, float, double>;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ R s_adv[GR_CHUNK], s_inv[GR_CHUNK];
-    __shared__ int s_first[GR_THREADS], s_last[GR_THREADS];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long c0 = (long)blockIdx.x * GR_CHUNK;
-    const long c1 = min((long)a.S, c0 + GR_CHUNK);
-    // this thread's tokens first: their loads are in flight while the prologue below walks its
-    // chain of dependent loads (sample range -> advantages / lengths)
-    const long t0 = c0 + (long)tid * GR_ITEMS;
-    int s[GR_ITEMS];
-    R x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];  // per-token values in the arithmetic type (fp32 hot path)
-    if (t0 + GR_ITEMS <= c1 && ((reinterpret_cast<uintptr_t>(a.sample_of + t0) & 15) == 0)) {
-#pragma unroll
-        for (int q = 0; q < GR_ITEMS; q += 4) {
-            const int4 v = *reinterpret_cast<const int4*>(a.sample_of + t0 + q);
-            s[q] = v.x; s[q + 1] = v.y; s[q + 2] = v.z; s[q + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < GR_ITEMS; ++i) s[i] = (t0 + i < c1) ? a.sample_of[t0 + i] : -1;
-    }
-    load8(static_cast<const LP*>(a.lp), t0, c1, x0);
-    load8(static_cast<const LP*>(a.old), t0, c1, x1);
-    load8(static_cast<const LP*>(a.ref), t0, c1, x2);
-    const int j_lo = a.sample_of[c0], j_hi = a.sample_of[c1 - 1];
-    // per-sample advantage and 1/n_j for the samples this chunk touches
-    if (a.adv_in) {
-        for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) s_adv[j - j_lo] = (R)a.adv_in[j];
-    } else {
-        const int G = a.group_size, g_lo = j_lo / G, g_hi = j_hi / G;
-        for (int grp = g_lo + wid; grp <= g_hi; grp += GR_THREADS / 32) {  // group_advantages[_mean_only]
-            const double* r = a.rewards + (long)grp * G;
-            double s = 0.0;
-            for (int i = lane; i < G; i += 32) s += r[i];
-            const double mean = warp_sum_d(s) / G;
-            double v = 0.0;
-            for (int i = lane; i < G; i += 32) v += (r[i] - mean) * (r[i] - mean);
-            const double sd = sqrt(warp_sum_d(v) / G);
-            for (int i = lane; i < G; i += 32) {
-                const int j = grp * G + i;
-                if (j < j_lo || j > j_hi) continue;
-                s_adv[j - j_lo] = (R)(a.mean_only ? r[i] - mean : (sd < 1e-8 ? 0.0 : (r[i] - mean) / sd));
-            }
-        }
-    }
-    for (int j = j_lo + tid; j <= j_hi; j += GR_THREADS) {
-        s_inv[j - j_lo] = R(1) / (R)(a.cu[j + 1] - a.cu[j]);
-        if (a.adv_out && a.cu[j] >= c0) {  // one writer: the sample's first chunk (fp64 advantage)
-            if (a.adv_in) a.adv_out[j] = a.adv_in[j];
-            else {
-                const int G = a.group_size, grp = j / G;
-                const double* r = a.rewards + (long)grp * G;
-                double s = 0.0, v = 0.0;
-                for (int i = 0; i < G; ++i) s += r[i];
-                const double mean = s / G;
-                for (int i = 0; i < G; ++i) v += (r[i] - mean) * (r[i] - mean);
-                const double sd = sqrt(v / G), rj = r[j - grp * G];
-                a.adv_out[j] = a.mean_only ? rj - mean : (sd < 1e-8 ? 0.0 : (rj - mean) / sd);
-            }
-        }
-    }
-    __syncthreads();
+// the advantage of sample j (grpo.cpp:24-48: group mean / population std, mean-only variant)
+__device__ __forceinline__ double sample_advantage(const GrpoArgs& a, int j) {
+    if (a.adv_in) return a.adv_in[j];
+    const int G = a.group_size, grp = j / G;
+    const double* r = a.rewards + (long)grp * G;
+    double s = 0.0, v = 0.0;
+    for (int i = 0; i < G; ++i) s += r[i];
+    const double mean = s / G;
+    for (int i = 0; i < G; ++i) v += (r[i] - mean) * (r[i] - mean);
+    const double sd = sqrt(v / G), rj = r[j - grp * G];
+    return a.mean_only ? rj - mean : (sd < 1e-8 ? 0.0 : (rj - mean) / sd);
+}
 
-    const int nv = (int)max(0L, min((long)GR_ITEMS, c1 - t0));  // valid items of this thread
-    const R eps = (R)a.eps, beta = (R)a.beta;
-    if (a.gran == 0) {  // token granularity (grpo.cpp:119-131)
-        float up4[GR_ITEMS];
+// The per-token part of one span: loads (FULL: one 16-byte load per vector and lane, no
+// bounds), the sample table refresh, the GRPO terms (token granularity, grpo.cpp:119-131) and
+// the upstream store.  On return x0 / x1 / x2 hold the values to reduce per sample (zero past
+// the range end): {clip value, kl value, clipped} or, for sequence granularity, the raw
+// {lp, old, ref} (grpo.cpp:134-140).
+template <class LP, class R, int GRAN, bool FULL>
+__device__ __forceinline__ void span_terms(const GrpoArgs& a, long b, long e, long r0, long r1, int lane,
+                                           R (*tab)[2], int& tab_lo, int& tab_hi, int* s, R* x0, R* x1, R* x2,
+                                           int& nv, int& j_first, int& j_last, int& last_lane, int& first,
+                                           int& last) {
+    const long t0 = b + lane * GR_ITEMS;
+    if constexpr (FULL) {
+        const int4 v = __ldcs(reinterpret_cast<const int4*>(a.sample_of + t0));
+        s[0] = v.x; s[1] = v.y; s[2] = v.z; s[3] = v.w;
+        nv = GR_ITEMS;
+        last_lane = 31;
+        first = s[0];
+        last = s[GR_ITEMS - 1];
+    } else {
+#pragma unroll
+        for (int i = 0; i < GR_ITEMS; ++i) s[i] = (t0 + i < e) ? a.sample_of[t0 + i] : -1;
+        nv = (int)max(0L, min((long)GR_ITEMS, e - t0));
+        last_lane = (int)((e - b - 1) / GR_ITEMS);
+        first = nv > 0 ? s[0] : -1;
+        last = first;
+#pragma unroll
+        for (int i = 1; i < GR_ITEMS; ++i) last = i < nv ? s[i] : last;
+    }
+    load_items<LP, R>(static_cast<const LP*>(a.lp), t0, FULL ? t0 + GR_ITEMS : e, x0);
+    load_items<LP, R>(static_cast<const LP*>(a.old), t0, FULL ? t0 + GR_ITEMS : e, x1);
+    load_items<LP, R>(static_cast<const LP*>(a.ref), t0, FULL ? t0 + GR_ITEMS : e, x2);
+    j_first = __shfl_sync(0xffffffffu, first, 0);
+    j_last = __shfl_sync(0xffffffffu, last, last_lane);
+    if constexpr (GRAN == 0) {
+        if (j_first < tab_lo || j_last > tab_hi) {  // refresh the sample table (warp-uniform)
+            __syncwarp();
+            // [j_first, j_last] is at most GR_SPAN samples (every sample holds >= 1 token); one lane
+            // round fills up to 32 of them, so short samples refresh once per 32
+            tab_lo = j_first;
+            tab_hi = max(j_last, min(a.n - 1, j_first + 31));
+            for (int j = tab_lo + lane; j <= tab_hi; j += 32) {
+                const double adv = sample_advantage(a, j);
+                const int cj = a.cu[j];
+                tab[j - tab_lo][0] = (R)adv;
+                tab[j - tab_lo][1] = R(1) / (R)(a.cu[j + 1] - cj);
+                if (a.adv_out && cj >= r0 && cj < r1) a.adv_out[j] = adv;  // the range holding the first token
+            }
+            __syncwarp();
+        }
+        const R eps = (R)a.eps, beta = (R)a.beta, ups = (R)a.up_scale;
+        R up4[GR_ITEMS];
 #pragma unroll
         for (int i = 0; i < GR_ITEMS; ++i) {
-            if (i >= nv) {
-                x0[i] = x1[i] = x2[i] = R(0);
-                up4[i] = 0.f;
-                continue;
-            }
-            const R lp = x0[i], old = x1[i], ref = x2[i];
-            const int jl = s[i] - j_lo;
+            const bool ok = FULL || i < nv;
+            const int jl = ok ? s[i] - tab_lo : 0;
             R cv, cg;
             int c;
-            clip_eval<R>(lp, old, (R)s_adv[jl], eps, cv, cg, c);
-            const R d = ref - lp, em = expm1(d);  // eval_kl, grpo.cpp:89-93
-            const R g = s_inv[jl] * (cg + beta * em);
-            x0[i] = cv;
-            x1[i] = em - d;
-            x2[i] = (R)c;
-            up4[i] = (float)((R)a.up_scale * g);
-            if (a.up_f64) a.up_f64[t0 + i] = a.up_scale * (double)g;
+            clip_eval<R>(x0[i], x1[i], tab[jl][0], eps, cv, cg, c);
+            const R d = x2[i] - x0[i], em = expm1(d);  // eval_kl, grpo.cpp:89-93
+            const R g = tab[jl][1] * (cg + beta * em);
+            x0[i] = ok ? cv : R(0);
+            x1[i] = ok ? em - d : R(0);
+            x2[i] = ok ? (R)c : R(0);
+            up4[i] = ups * g;
         }
         if (a.up_f32) {
-            if (nv == GR_ITEMS && ((reinterpret_cast<uintptr_t>(a.up_f32 + t0) & 15) == 0)) {
-#pragma unroll
-                for (int q = 0; q < GR_ITEMS; q += 4)
-                    *reinterpret_cast<float4*>(a.up_f32 + t0 + q) = make_float4(up4[q], up4[q + 1], up4[q + 2], up4[q + 3]);
+            if (FULL || nv == GR_ITEMS) {
+                __stcs(reinterpret_cast<float4*>(a.up_f32 + t0),
+                       make_float4((float)up4[0], (float)up4[1], (float)up4[2], (float)up4[3]));
             } else {
-                for (int i = 0; i < nv; ++i) a.up_f32[t0 + i] = up4[i];
+                for (int i = 0; i < nv; ++i) a.up_f32[t0 + i] = (float)up4[i];
             }
         }
-    }  // sequence granularity: sum the raw log-probs (grpo.cpp:134-140)
-
-    // segmented reduction of (x0, x1, x2) by sample over the block's chunk
-    const int first = nv > 0 ? s[0] : -1, last = nv > 0 ? s[nv - 1] : -1;
-    s_first[tid] = first;
-    s_last[tid] = last;
-    __syncthreads();
-    const int prev_last = tid > 0 ? s_last[tid - 1] : -2;
-    const int next_first = tid + 1 < GR_THREADS ? s_first[tid + 1] : -2;
-    // the thread's last run (in R, at most 8 terms), widened once
-    R t0a = 0, t0b = 0, t0c = 0;
-    for (int i = 0; i < nv; ++i)
-        if (s[i] == last) {
-            t0a += x0[i];
-            t0b += x1[i];
-            t0c += x2[i];
-        }
-    SegAgg agg{(double)t0a, (double)t0b, (double)t0c, (tid == 0 || first != prev_last || first != last) ? 1 : 0};
-    SegAgg carry;
-    Scan(scan_tmp).ExclusiveScan(agg, carry, SegOp());
-    double c0a = 0.0, c0b = 0.0, c0c = 0.0;  // carried into the thread's first run
-    if (tid > 0 && nv > 0 && first == prev_last) {
-        c0a = carry.a;
-        c0b = carry.b;
-        c0c = carry.c;
-    }
-    R r0 = 0, r1 = 0, r2 = 0;
-    for (int i = 0; i < nv; ++i) {
-        r0 += x0[i];
-        r1 += x1[i];
-        r2 += x2[i];
-        const bool end = (i + 1 < nv) ? (s[i + 1] != s[i]) : (next_first != s[i]);
-        if (end) {
-            double* o = a.slots + 3 * ((long)s[i] + blockIdx.x);
-            o[0] = c0a + (double)r0;
-            o[1] = c0b + (double)r1;
-            o[2] = c0c + (double)r2;
-            r0 = r1 = r2 = 0;
-            c0a = c0b = c0c = 0.0;
+        if (a.up_f64)
+            for (int i = 0; i < nv; ++i) a.up_f64[t0 + i] = (double)up4[i];
+    } else if (a.adv_out) {  // sequence granularity: the advantage, written by the span holding the first token
+        for (int j = j_first + lane; j <= j_last; j += 32) {
+            const int cj = a.cu[j];
+            if (cj >= b && cj < e) a.adv_out[j] = sample_advantage(a, j);
         }
     }
 }
 
-// Per-sample terms + stats, one block: warp w takes samples w, w + 32, ...; its lanes add the
-// sample's (sample, block) partials in a fixed strided order (a sample spanning many chunks is
-// not a serial chain of dependent loads), then a fixed-order tree over the warps.
+// Warp-autonomous pass over the range [r0, r1) of scored tokens.  The open run (sample cs,
+// the one the previous span ended in) is held as per-lane fp64 partials la / lb / lc: a span
+// wholly inside it (the common case: samples are hundreds of tokens) only adds each lane's
+// items, with no cross-lane traffic.  A span holding a sample boundary folds the partials
+// into a carry, runs a segmented warp scan, writes every run that ends inside it to its
+// (sample, range) slot and leaves the new open run's total in lane 0.
+template <class LP, int GRAN>
+__global__ void __launch_bounds__(GR_WARPS * 32) k_grpo_tokens(const GrpoArgs a) {
+    using R = std::conditional_t<std::is_same_v<LP, float>, float, double>;
+    __shared__ R s_tab[GR_WARPS][GR_SPAN][2];  // per warp: {advantage, 1/n} of samples [tab_lo, tab_hi]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long rng = (long)blockIdx.x * GR_WARPS + wid;  // this warp's range of scored tokens
+    const long r0 = rng * a.warp_tokens, r1 = min((long)a.S, r0 + a.warp_tokens);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.ticket = 0u;  // k_grpo_finish's ticket (stream-ordered)
+    if (r0 >= r1) return;
+    // 16-byte vector loads / stores need 16-byte aligned bases (t0 is a multiple of 4 elements)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.lp) | reinterpret_cast<uintptr_t>(a.old) |
+                           reinterpret_cast<uintptr_t>(a.ref) | reinterpret_cast<uintptr_t>(a.sample_of) |
+                           reinterpret_cast<uintptr_t>(a.up_f32)) & 15) == 0;
+    R(*tab)[2] = s_tab[wid];
+    int tab_lo = 0, tab_hi = -1;
+    int cs = -1;                    // the open run's sample
+    double la = 0.0, lb = 0.0, lc = 0.0;  // its per-lane partials
+    for (long b = r0; b < r1; b += GR_SPAN) {
+        const long e = min(r1, b + GR_SPAN);
+        int s[GR_ITEMS], nv, j_first, j_last, last_lane, first, last;
+        R x0[GR_ITEMS], x1[GR_ITEMS], x2[GR_ITEMS];
+        if (aligned && e - b == GR_SPAN)
+            span_terms<LP, R, GRAN, true>(a, b, e, r0, r1, lane, tab, tab_lo, tab_hi, s, x0, x1, x2, nv, j_first,
+                                          j_last, last_lane, first, last);
+        else
+            span_terms<LP, R, GRAN, false>(a, b, e, r0, r1, lane, tab, tab_lo, tab_hi, s, x0, x1, x2, nv, j_first,
+                                           j_last, last_lane, first, last);
+        if (j_first == j_last && (cs == j_first || cs < 0)) {  // inside the open run (warp-uniform)
+            cs = j_first;
+            if constexpr (GRAN == 0) {  // token terms: a 4-term fp32 sum per lane, then fp64
+                la += (double)((x0[0] + x0[1]) + (x0[2] + x0[3]));
+                lb += (double)((x1[0] + x1[1]) + (x1[2] + x1[3]));
+                lc += (double)((x2[0] + x2[1]) + (x2[2] + x2[3]));
+            } else {  // raw log-probs: exact fp64 sums
+#pragma unroll
+                for (int i = 0; i < GR_ITEMS; ++i) {
+                    la += (double)x0[i];
+                    lb += (double)x1[i];
+                    lc += (double)x2[i];
+                }
+            }
+            continue;
+        }
+        // a sample boundary: the open run's total, flushed if the span does not continue it
+        double ca = warp_sum_d(la), cb = warp_sum_d(lb), cc = warp_sum_d(lc);
+        if (cs >= 0 && j_first != cs) {
+            if (lane == 0) {
+                double* o = a.slots + 3 * ((long)cs + rng);
+                o[0] = ca;
+                o[1] = cb;
+                o[2] = cc;
+            }
+            cs = -1;
+            ca = cb = cc = 0.0;
+        }
+        const int up_last = __shfl_up_sync(0xffffffffu, last, 1);
+        const int prev_last = lane == 0 ? cs : up_last;
+        const int next_first = __shfl_down_sync(0xffffffffu, first, 1);
+        double ta = 0, tb = 0, tc = 0;  // the lane's last run
+#pragma unroll
+        for (int i = 0; i < GR_ITEMS; ++i)
+            if (i < nv && s[i] == last) {
+                ta += (double)x0[i];
+                tb += (double)x1[i];
+                tc += (double)x2[i];
+            }
+        double va = ta, vb = tb, vc = tc;
+        int reset = (lane == 0 || first != prev_last || first != last) ? 1 : 0;
+        if (lane == 0 && nv > 0 && first == last && first == cs) {  // the carried run continues through lane 0
+            va += ca;
+            vb += cb;
+            vc += cc;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive segmented scan over the lanes
+            const double ua = __shfl_up_sync(0xffffffffu, va, o), ub = __shfl_up_sync(0xffffffffu, vb, o),
+                         uc = __shfl_up_sync(0xffffffffu, vc, o);
+            const int ur = __shfl_up_sync(0xffffffffu, reset, o);
+            if (lane >= o && !reset) {
+                va += ua;
+                vb += ub;
+                vc += uc;
+                reset = ur;
+            }
+        }
+        // carried into the lane's first run: the previous lane's inclusive value (lane 0: the open run)
+        const double pa = __shfl_up_sync(0xffffffffu, va, 1), pb = __shfl_up_sync(0xffffffffu, vb, 1),
+                     pc = __shfl_up_sync(0xffffffffu, vc, 1);
+        double c0a = 0.0, c0b = 0.0, c0c = 0.0;
+        if (nv > 0 && first == prev_last) {
+            c0a = lane == 0 ? ca : pa;
+            c0b = lane == 0 ? cb : pb;
+            c0c = lane == 0 ? cc : pc;
+        }
+        double q0 = 0, q1 = 0, q2 = 0;
+#pragma unroll
+        for (int i = 0; i < GR_ITEMS; ++i) {
+            if (i >= nv) break;
+            q0 += (double)x0[i];
+            q1 += (double)x1[i];
+            q2 += (double)x2[i];
+            const bool open = (lane == last_lane) && (i == nv - 1);  // continues into the next span
+            const bool end = (i + 1 < nv) ? (s[i + 1] != s[i]) : (!open && next_first != s[i]);
+            if (end) {
+                double* o = a.slots + 3 * ((long)s[i] + rng);
+                o[0] = c0a + q0;
+                o[1] = c0b + q1;
+                o[2] = c0c + q2;
+                q0 = q1 = q2 = 0;
+                c0a = c0b = c0c = 0.0;
+            }
+        }
+        // the span's last run stays open: its inclusive value, held by lane 0
+        cs = j_last;
+        ca = __shfl_sync(0xffffffffu, va, last_lane);
+        cb = __shfl_sync(0xffffffffu, vb, last_lane);
+        cc = __shfl_sync(0xffffffffu, vc, last_lane);
+        la = lane == 0 ? ca : 0.0;
+        lb = lane == 0 ? cb : 0.0;
+        lc = lane == 0 ? cc : 0.0;
+    }
+    // flush the open run at the range end
+    const double ca = warp_sum_d(la), cb = warp_sum_d(lb), cc = warp_sum_d(lc);
+    if (lane == 0) {
+        double* o = a.slots + 3 * ((long)cs + rng);
+        o[0] = ca;
+        o[1] = cb;
+        o[2] = cc;
+    }
+}
+
+// Per-sample terms: warp w of the grid takes sample w; its lanes add the sample's (sample,
+// range) partials in a fixed strided order, then a fixed-order butterfly.  Terms go to
+// a.terms (and per_sample when requested).  The last block to finish (a ticket that
+// k_grpo_tokens zeroed) adds the running stats (pipeline.cpp:131-137): thread-strided
+// sums over the samples in index order, then a fixed-order tree -- deterministic whichever
+// block draws the last ticket.
 __global__ void __launch_bounds__(1024) k_grpo_finish(const GrpoArgs a) {
     __shared__ double red[5][32];
+    __shared__ unsigned ticket;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    double acc[5] = {0, 0, 0, 0, 0};
-    for (int j = wid; j < a.n; j += nw) {
+    const int j = (int)(((long)blockIdx.x * blockDim.x + tid) >> 5);
+    if (j < a.n) {
         const int b = a.cu[j], e = a.cu[j + 1], n = e - b;
-        const int b0 = b / GR_CHUNK, b1 = (e - 1) / GR_CHUNK;
+        const int b0 = b / a.warp_tokens, b1 = (e - 1) / a.warp_tokens;
         double s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll 4
         for (int k = b0 + lane; k <= b1; k += 32) {
             const double* o = a.slots + 3 * ((long)j + k);
             s0 += o[0];
@@ -241,42 +328,55 @@ __global__ void __launch_bounds__(1024) k_grpo_finish(const GrpoArgs a) {
         s0 = warp_sum_d(s0);
         s1 = warp_sum_d(s1);
         s2 = warp_sum_d(s2);
-        if (lane != 0) continue;
-        double t[4];
-        if (a.gran == 0) {
-            const double inv = 1.0 / n;
-            t[0] = s0 * inv;
-            t[1] = s1 * inv;
-            t[2] = s2;
-            t[3] = n;
-        } else {  // one evaluation on the summed log-probs (grpo.cpp:134-149)
-            double cv, cg;
-            int c;
-            clip_eval<double>(s0, s1, a.adv_out[j], a.eps, cv, cg, c);
-            const double d = s2 - s0, em = expm1(d);
-            t[0] = cv;
-            t[1] = em - d;
-            t[2] = c;
-            t[3] = 1;
-            a.g_seq[j] = a.up_scale * (cg + a.beta * em);
+        if (lane == 0) {
+            double t[4];
+            if (a.gran == 0) {
+                const double inv = 1.0 / n;
+                t[0] = s0 * inv;
+                t[1] = s1 * inv;
+                t[2] = s2;
+                t[3] = n;
+            } else {  // one evaluation on the summed log-probs (grpo.cpp:134-149)
+                double cv, cg;
+                int c;
+                clip_eval<double>(s0, s1, a.adv_out[j], a.eps, cv, cg, c);
+                const double d = s2 - s0, em = expm1(d);
+                t[0] = cv;
+                t[1] = em - d;
+                t[2] = c;
+                t[3] = 1;
+                a.g_seq[j] = a.up_scale * (cg + a.beta * em);
+            }
+            for (int q = 0; q < 4; ++q) a.terms[4 * (long)j + q] = t[q];
+            if (a.per_sample)
+                for (int q = 0; q < 4; ++q) a.per_sample[4 * (long)j + q] = t[q];
         }
-        if (a.per_sample)
-            for (int q = 0; q < 4; ++q) a.per_sample[4 * (long)j + q] = t[q];
-        acc[0] += t[0] - a.beta * t[1];
-        acc[1] += t[0];
-        acc[2] += t[1];
-        acc[3] += t[2];
-        acc[4] += t[3];
     }
+    if (!a.stats) return;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) ticket = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    if (ticket != gridDim.x - 1) return;
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int k = tid; k < a.n; k += blockDim.x) {
+        const double* t = a.terms + 4 * (long)k;
+        const double t0 = __ldcg(t), t1 = __ldcg(t + 1);
+        acc[0] += t0 - a.beta * t1;
+        acc[1] += t0;
+        acc[2] += t1;
+        acc[3] += __ldcg(t + 2);
+        acc[4] += __ldcg(t + 3);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) acc[q] = warp_sum_d(acc[q]);
     if (lane == 0)
         for (int q = 0; q < 5; ++q) red[q][wid] = acc[q];
     __syncthreads();
-    if (tid == 0 && a.stats) {
-        for (int q = 0; q < 5; ++q) {
-            double s = 0.0;
-            for (int w = 0; w < nw; ++w) s += red[q][w];
-            a.stats[q] += s;
-        }
+    if (tid < 5) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[tid][w];
+        a.stats[tid] += s;
     }
 }
 
@@ -290,15 +390,32 @@ __global__ void __launch_bounds__(256) k_grpo_bcast(const GrpoArgs a) {
 
 }  // namespace
 
-size_t grpo_slot_count(long S, int n) { return 3 * ((size_t)n + (size_t)((S + GR_CHUNK - 1) / GR_CHUNK) + 1); }
+// slots for the finest warp range (one span): enough for any range length launch_grpo picks
+// (+ 4 per sample: the per-sample terms, + 1: k_grpo_finish's ticket)
+size_t grpo_slot_count(long S, int n) {
+    return 3 * ((size_t)n + (size_t)((S + GR_SPAN - 1) / GR_SPAN) + 1) + 4 * (size_t)n + 1;
+}
 
-void launch_grpo(const GrpoArgs& a, cudaStream_t st) {
-    if (a.S <= 0 || a.n <= 0) return;
-    const int grid = (int)((a.S + GR_CHUNK - 1) / GR_CHUNK);
-    if (a.lp_f64) k_grpo_tokens<double><<<grid, GR_THREADS, 0, st>>>(a);
-    else k_grpo_tokens<float><<<grid, GR_THREADS, 0, st>>>(a);
+void launch_grpo(const GrpoArgs& a_in, cudaStream_t st) {
+    if (a_in.S <= 0 || a_in.n <= 0) return;
+    GrpoArgs a = a_in;
+    a.terms = a.slots + 3 * ((size_t)a.n + (size_t)((a.S + GR_SPAN - 1) / GR_SPAN) + 1);
+    a.ticket = reinterpret_cast<unsigned*>(a.terms + 4 * (size_t)a.n);
+    // spans per warp: as many as keep >= ~48 warps per SM busy (fewer slots, longer carried runs)
+    const long spans = (a.S + GR_SPAN - 1) / GR_SPAN;
+    const int iters = (int)std::max(1L, std::min((long)GR_MAX_ITERS, spans / (148L * 48)));
+    a.warp_tokens = GR_SPAN * iters;
+    const long warps = (a.S + a.warp_tokens - 1) / a.warp_tokens;
+    const int grid = (int)((warps + GR_WARPS - 1) / GR_WARPS);
+    if (a.lp_f64) {
+        if (a.gran == 0) k_grpo_tokens<double, 0><<<grid, GR_WARPS * 32, 0, st>>>(a);
+        else k_grpo_tokens<double, 1><<<grid, GR_WARPS * 32, 0, st>>>(a);
+    } else {
+        if (a.gran == 0) k_grpo_tokens<float, 0><<<grid, GR_WARPS * 32, 0, st>>>(a);
+        else k_grpo_tokens<float, 1><<<grid, GR_WARPS * 32, 0, st>>>(a);
+    }
     PARL_LAUNCHED();
-    k_grpo_finish<<<1, 1024, 0, st>>>(a);
+    k_grpo_finish<<<cdiv(a.n, 32), 1024, 0, st>>>(a);
     PARL_LAUNCHED();
     if (a.gran == 1) {
         k_grpo_bcast<<<std::min(cdiv(a.S, 256), 148 * 8), 256, 0, st>>>(a);

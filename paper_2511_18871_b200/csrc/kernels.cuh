@@ -129,6 +129,9 @@ struct GrpoArgs {
     double* per_sample = nullptr;  // [n x 4] {clip_term, kl, clipped_units, total_units} or null
     double* g_seq = nullptr;       // [n] (sequence granularity)
     double* stats = nullptr;       // [5] += {objective, clip, kl, clipped, units} or null
+    int warp_tokens = 0;           // set by launch_grpo: tokens per warp range (slot granularity)
+    double* terms = nullptr;       // set by launch_grpo: [n x 4] per-sample terms (in the slots block)
+    unsigned* ticket = nullptr;    // set by launch_grpo: k_grpo_finish's last-block ticket (in the slots block)
 };
 size_t grpo_slot_count(long S, int n);
 void launch_grpo(const GrpoArgs& a, cudaStream_t st);

@@ -282,6 +282,44 @@ def test_microbatch_loss_matches_oracle_terms(P, ctx32, orc):
         assert ml.report.objective == pytest.approx(obj / len(lens), rel=1e-9)
 
 
+@pytest.mark.parametrize("gran", ["token", "sequence"])
+def test_microbatch_loss_ragged_at_scale(P, ctx32, gran):
+    """K7 with 3M scored tokens (several spans per warp range, runs carried across them) and
+    hundreds of 1-3 token samples (more samples than fit one warp's sample table), vs the fp64
+    GRPO terms of torch_ref (grpo.cpp:111-184)."""
+    from oracle import torch_ref as TR
+
+    rng = np.random.default_rng(11)
+    lens = [1] * 300 + [2, 3] * 100 + [1_000_003, 77, 1_400_000, 1] + [int(x) for x in rng.integers(1, 9, 200)] \
+        + [600_000]
+    S = sum(lens)
+    lp = -3 * rng.random(S)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    # sequence granularity exponentiates differences of sums: per-token noise ~ 1/sqrt(n_j) there
+    sc = 1.0 if gran == "token" else np.repeat(1.0 / np.sqrt(lens), lens)
+    old = lp + 0.3 * sc * rng.standard_normal(S)
+    ref = lp + 0.1 * sc * rng.standard_normal(S)
+    adv = rng.standard_normal(len(lens))
+    samples = [P.Sample(response=np.full(n, 6, np.int32), advantage=float(adv[j]),
+                        old_logprobs=old[cu[j]:cu[j + 1]], ref_logprobs=ref[cu[j]:cu[j + 1]])
+               for j, n in enumerate(lens)]
+    ml = P.grpo_microbatch_loss(samples, [lp[cu[j]:cu[j + 1]] for j in range(len(lens))], 0.2, 0.04, gran, ctx32)
+    n = len(lens)
+    if gran == "token":
+        up, st = TR.grpo_terms(lp, old, ref, lens, adv)
+        assert np.allclose(np.concatenate(ml.upstream), up / n, rtol=1e-12, atol=1e-18)
+        assert ml.report.objective == pytest.approx(st[0] / n, rel=1e-10)
+        assert ml.report.clip_fraction == pytest.approx(st[3] / st[4], rel=1e-12)
+    else:  # one evaluation per sample on the summed log-probs (grpo.cpp:134-149)
+        sl, so, sr = (np.add.reduceat(x, cu[:-1]) for x in (lp, old, ref))
+        up, st = TR.grpo_terms(sl, so, sr, [1] * n, adv)
+        got = np.array([u[0] for u in ml.upstream])
+        assert np.allclose(got, up / n, rtol=1e-8, atol=1e-18)
+        for u in ml.upstream:
+            assert np.all(u == u[0])
+        assert ml.report.objective == pytest.approx(st[0] / n, rel=1e-8)
+
+
 def test_shared_prompt_mask(P, ctx32):  # test_packing.cpp:79-107
     m = P.build_shared_prompt_mask(2, [1, 1], ctx32)
     assert m.astype(int).ravel().tolist() == [1, 0, 0, 0, 1, 1, 0, 0, 1, 1, 1, 0, 1, 1, 0, 1]
