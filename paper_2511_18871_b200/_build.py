@@ -19,6 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+FLAGS += os.environ.get("PARL_NVCC_EXTRA", "").split()  # A/B builds (e.g. -DATTN_POLY_MASK=0x11)
 SOURCES = ["abi.cu", "k_elem.cu", "k_grpo.cu", "k_gemm_simt.cu", "k_attn.cu", "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 

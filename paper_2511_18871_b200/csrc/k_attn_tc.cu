@@ -89,6 +89,13 @@ struct PairSmem {
     static constexpr int TOTAL = OFF_L0 + (DH == 64 ? 2 * 256 * 4 : 0) + 1024;
 };
 
+#ifndef ATTN_POLY_MASK
+// which of every 8 exps of a full tile run on the FMA pipe (Dh 64 forward, FA4-style).  Measured
+// at C2: 0x00 0.067 ms, 0x80 0.068, 0x88 0.069, 0x8a 0.071 per 2 groups -- the softmax is not
+// MUFU-bound here (XU 43%, stalls on fixed-latency waits), so the default keeps MUFU only.
+#define ATTN_POLY_MASK 0x00
+#endif
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 
 // bits [lo, hi) of the 32-column word starting at column c0 (lo / hi relative to the tile)
@@ -716,15 +723,30 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 // P = exp2(S * c - m) -> bf16 (registers)
                 float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
                 uint32_t pk[64];
+                if (ATTN_POLY_MASK != 0 && (f & FULL)) {  // a share of the exps on the FMA pipe, the rest on MUFU
+                    float pe[8];
 #pragma unroll
-                for (int j = 0; j < 128; j += 4) {
-                    const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
-                    const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
-                    const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
-                    const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
-                    sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
-                    pk[j / 2] = pack2(p0, p1);
-                    pk[j / 2 + 1] = pack2(p2, p3);
+                    for (int j = 0; j < 128; j += 8) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float x = fmaf(sv[j + q], c2, -mb);
+                            pe[q] = ((ATTN_POLY_MASK >> q) & 1) ? tc::exp2_fma(x) : tc::ex2_approx(x);
+                        }
+                        sm0 += pe[0] + pe[4]; sm1 += pe[1] + pe[5]; sm2 += pe[2] + pe[6]; sm3 += pe[3] + pe[7];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) pk[j / 2 + q] = pack2(pe[2 * q], pe[2 * q + 1]);
+                    }
+                } else {  // masked scores are -inf: MUFU gives their exact zero
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
+                        const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
+                        const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
+                        const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
+                        sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
+                        pk[j / 2] = pack2(p0, p1);
+                        pk[j / 2 + 1] = pack2(p2, p3);
+                    }
                 }
                 if (q4 == 0) ATTN_TRACE(w, cS, 3);
                 // the previous PV of this tile has finished reading P and writing O
