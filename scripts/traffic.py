@@ -5,7 +5,7 @@ dram__bytes_write.sum --csv`):
     python scripts/traffic.py gpurun_out/launches_dram.csv > profiles/r01_traffic.json
 
 Classes follow bench.py's kernel classes (parl_ctx_profile): gemm, head, attn_fwd,
-attn_bwd, norm, loss, pack.  ncu replays each kernel with cold caches, so times are
+attn_bwd, norm, loss, pack, seed (the head GEMMs fold into gemm here).  ncu replays each kernel with cold caches, so times are
 serialised / cold; the DRAM bytes are the measured traffic per launch."""
 import collections
 import csv
@@ -24,7 +24,9 @@ def klass(name, grid):
         return "attn_bwd"
     if "k_gemm" in n or "splitk" in n:
         return "gemm"
-    if "lse_combine" in n or "softmax_bwd" in n:
+    if "softmax_bwd" in n:
+        return "seed"
+    if "lse_combine" in n:
         return "head"
     if "grpo" in n or "advantages" in n:
         return "loss"
