@@ -86,6 +86,14 @@ def measured_traffic(cls):
         return None, None
 
 
+def sm_max_mhz():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -452,6 +460,13 @@ def run_ours(args, c):
     achieved = dp["work"] / (dp["ms"] / 1000.0) / 1e12 if dp["ms"] > 0 else 0.0
     step_ms = ms_max / args.steps
     traffic, traffic_src = measured_traffic(dom)
+    if args.config != "c2":  # the committed capture is of a C2 step: no traffic figure for other configs
+        traffic, traffic_src = None, "no ncu capture of this config"
+    if c["prec"] == "fp32":  # the fp32 build runs SIMT (FFMA): its roofline is the FP32 pipe, not the tensor core
+        peak_t, peak_kind = 148 * 128 * 2 * (sm_max_mhz() or 1965.0) * 1e6 / 1e12, \
+            "nominal fp32 FFMA (148 SMs x 128 lanes x 2 x max SM clock; the fp32 build runs SIMT)"
+    else:
+        peak_t, peak_kind = bf16_sus, f"{src} bf16 sustained"
     share = {k: round(v["ms"] / prof_steps / step_ms, 4) for k, v in prof.items() if v["ms"] > 0}
     c["name"] = args.config
     cpu = None
@@ -480,8 +495,8 @@ def run_ours(args, c):
         "e2e": {"value": e2e_val, "unit": "packed tokens/s", "h2d_bytes_per_step": ng * (T * 4 + G * 8 + G * 4),
                 "d2h_bytes_per_step": 40},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved, "peak": bf16_sus,
-                     "unit": "TFLOP/s", "frac": achieved / bf16_sus, "peak_kind": f"{src} bf16 sustained",
+        "roofline": {"bound": "tensor" if c["prec"] != "fp32" else "fp32", "kernel_class": dom, "achieved": achieved,
+                     "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t, "peak_kind": peak_kind,
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, read + write)",
                      "traffic_source": traffic_src, "share_of_step": share},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / prof_steps, "launches_per_step": v["launches"] / prof_steps,
