@@ -30,6 +30,10 @@ parl_status parl_debug_attn_bf16(int path, int T, int H, int Dh, int Peff, const
 parl_status parl_debug_attn_bwd_bf16(int path, int T, int H, int Dh, int Peff, const int32_t* seg,
                                      const int32_t* seg_start, const int32_t* seg_end, const void* qkv,
                                      const void* out, const void* dout, const float* lse, float* dsum, void* dqkv);
+/* Every array K1 wrote for a packed group, concatenated into out (host, int32):
+ * tokens, labels, positions, seg, pred [T each], row_ptr [T + 1], scored_pos, scored_label,
+ * pred_pos, sample_of, row_idx [S each]  (6T + 1 + 5S entries). */
+parl_status parl_debug_group_arrays(parl_group_t g, int32_t* out);
 #ifdef __cplusplus
 }
 #endif

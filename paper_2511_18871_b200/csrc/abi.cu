@@ -3156,6 +3156,21 @@ namespace parl_gpu {
 bool attn_trace_read(unsigned long long* out);
 }
 // phase timestamps of the attention forward's CTA 0 (builds with -DPARL_ATTN_TRACE only)
+extern "C" parl_status parl_debug_group_arrays(parl_group_t g, int32_t* out) {
+    return guarded(g->ctx, [&] {
+        const long T = g->T, S = g->S;
+        const int32_t* src[11] = {g->pk.tokens, g->pk.labels, g->pk.positions, g->pk.seg, g->pk.pred, g->pk.row_ptr,
+                                  g->pk.scored_pos, g->pk.scored_label, g->pk.pred_pos, g->pk.sample_of,
+                                  g->pk.row_idx};
+        const long n[11] = {T, T, T, T, T, T + 1, S, S, S, S, S};
+        for (int a = 0; a < 11; ++a) {
+            if (n[a]) PARL_CUDA(cudaMemcpyAsync(out, src[a], n[a] * 4, cudaMemcpyDeviceToHost, g->ctx->st));
+            out += n[a];
+        }
+        PARL_CUDA(cudaStreamSynchronize(g->ctx->st));
+    });
+}
+
 extern "C" parl_status parl_debug_attn_trace(unsigned long long* out) {
     return parl_gpu::attn_trace_read(out) ? PARL_OK : PARL_E_CONFIG;
 }

@@ -22,7 +22,113 @@ namespace parl_gpu {
 // of response k (exclusive prefix of resp_lens), cu[G] = S.
 // `id_max` receives max over tokens of (unsigned)id: an id outside [0, V) is exactly
 // one with (unsigned)id >= V (VocabError, model.cpp:413-417), checked before the forward.
+__device__ __forceinline__ void st4(int32_t* p, const int* v) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+}
+
+// One thread per 4 consecutive positions (P a multiple of 4, so the [T] and [S] arrays are
+// both 16-byte aligned): one binary search over cu[] per thread (the following positions
+// advance the response index), 16-byte stores of all the arrays.
 __global__ void k_pack(const int32_t* __restrict__ prompt, int P, const int32_t* __restrict__ resp_flat,
+                       const int32_t* __restrict__ cu, int G, PackedDev pk, unsigned* __restrict__ id_max) {
+    const int T = P + cu[G];
+    const bool vt = ((reinterpret_cast<uintptr_t>(pk.tokens) | reinterpret_cast<uintptr_t>(pk.labels) |
+                      reinterpret_cast<uintptr_t>(pk.positions) | reinterpret_cast<uintptr_t>(pk.seg) |
+                      reinterpret_cast<uintptr_t>(pk.pred) | reinterpret_cast<uintptr_t>(pk.row_ptr)) & 15) == 0;
+    const bool vs = (P & 3) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(pk.scored_pos) | reinterpret_cast<uintptr_t>(pk.scored_label) |
+                      reinterpret_cast<uintptr_t>(pk.pred_pos) | reinterpret_cast<uintptr_t>(pk.sample_of)) & 15) == 0;
+    unsigned umax = 0;
+    for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; 4 * q < T; q += (long)gridDim.x * blockDim.x) {
+        const int t0 = (int)(4 * q);
+        int tk[4], lb[4], ps[4], sg[4], pr[4], rp[4], sp[4], sk[4];
+        int k = -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u;
+            tk[u] = lb[u] = ps[u] = sg[u] = pr[u] = rp[u] = sp[u] = sk[u] = 0;
+            if (t >= T) continue;
+            if (t < P) {
+                const int tok = prompt[t];
+                umax = max(umax, (unsigned)tok);
+                tk[u] = tok;
+                lb[u] = -1;
+                ps[u] = t;
+                pr[u] = t - 1;
+            } else {
+                const int s = t - P;
+                if (k < 0) {  // response k with cu[k] <= s < cu[k+1]
+                    int lo = 0, hi = G - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (cu[mid] <= s) lo = mid; else hi = mid - 1;
+                    }
+                    k = lo;
+                } else {
+                    while (cu[k + 1] <= s) ++k;
+                }
+                const int i = s - cu[k];
+                const int tok = resp_flat[s];
+                umax = max(umax, (unsigned)tok);
+                tk[u] = tok;
+                lb[u] = tok;  // self-aligned labels, packing.cpp:37
+                ps[u] = P + i;
+                sg[u] = k + 1;
+                pr[u] = (i == 0) ? P - 1 : t - 1;  // model.cpp:251
+                // position -> gathered head rows (CSR): P-1 owns the G response starts, every
+                // non-final response token owns row t+1-P
+                rp[u] = G + s - k;
+                sp[u] = t;
+                sk[u] = k;
+                const bool last = (i == cu[k + 1] - cu[k] - 1);
+                if (!last) pk.row_idx[G + s - k] = s + 1;
+            }
+            if (t == P - 1)
+                for (int r = 0; r < G; ++r) pk.row_idx[r] = cu[r];
+            if (t == T - 1) pk.row_ptr[T] = cu[G];
+        }
+        if (vt && t0 + 4 <= T) {
+            st4(pk.tokens + t0, tk);
+            st4(pk.labels + t0, lb);
+            st4(pk.positions + t0, ps);
+            st4(pk.seg + t0, sg);
+            st4(pk.pred + t0, pr);
+            st4(pk.row_ptr + t0, rp);
+        } else {
+            for (int u = 0; u < 4 && t0 + u < T; ++u) {
+                pk.tokens[t0 + u] = tk[u];
+                pk.labels[t0 + u] = lb[u];
+                pk.positions[t0 + u] = ps[u];
+                pk.seg[t0 + u] = sg[u];
+                pk.pred[t0 + u] = pr[u];
+                pk.row_ptr[t0 + u] = rp[u];
+            }
+        }
+        if (vs && t0 >= P && t0 + 4 <= T) {  // s0 = t0 - P is a multiple of 4
+            const int s0 = t0 - P;
+            st4(pk.scored_pos + s0, sp);
+            st4(pk.scored_label + s0, tk);
+            st4(pk.pred_pos + s0, pr);
+            st4(pk.sample_of + s0, sk);
+        } else {
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u;
+                if (t < P || t >= T) continue;
+                pk.scored_pos[t - P] = sp[u];
+                pk.scored_label[t - P] = tk[u];
+                pk.pred_pos[t - P] = pr[u];
+                pk.sample_of[t - P] = sk[u];
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    if ((threadIdx.x & 31) == 0 && id_max) atomicMax(id_max, umax);
+}
+
+// K1 when P is not a multiple of 4 (the [T] and [S] arrays cannot both be 16-byte aligned):
+// one thread per position, every store instruction 128 contiguous bytes of one array.
+__global__ void k_pack_scalar(const int32_t* __restrict__ prompt, int P, const int32_t* __restrict__ resp_flat,
                        const int32_t* __restrict__ cu, int G, PackedDev pk, unsigned* __restrict__ id_max) {
     const int T = P + cu[G];
     unsigned umax = 0;
@@ -786,7 +892,8 @@ void launch_pack_multi(const int32_t* prompts, const int32_t* resp, const int32_
 void launch_pack(const int32_t* prompt, int P, const int32_t* resp, const int32_t* cu, int G, int T,
                  const PackedDev& pk, unsigned* id_max, cudaStream_t st) {
     if (id_max) PARL_CUDA(cudaMemsetAsync(id_max, 0, sizeof(unsigned), st));
-    k_pack<<<grid_for(T), 256, 0, st>>>(prompt, P, resp, cu, G, pk, id_max);
+    if (P & 3) k_pack_scalar<<<grid_for(T), 256, 0, st>>>(prompt, P, resp, cu, G, pk, id_max);
+    else k_pack<<<grid_for(cdiv(T, 4)), 256, 0, st>>>(prompt, P, resp, cu, G, pk, id_max);
     PARL_LAUNCHED();
 }
 

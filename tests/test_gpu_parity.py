@@ -77,6 +77,55 @@ def test_pack_large_bit_exact(P, ctx32, orc):
         assert np.array_equal(d[k], o[k]), k
 
 
+def _pack_arrays_np(prompt, resp):
+    """Every K1 array restated (packing.cpp:7-45, model.cpp:230-253; head-row CSR of kernels.cuh)."""
+    Pn, G = len(prompt), len(resp)
+    lens = np.array([len(r) for r in resp])
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    S, T = int(cu[-1]), Pn + int(cu[-1])
+    k = np.repeat(np.arange(G), lens)
+    s = np.arange(S)
+    i = s - cu[k]
+    rt = np.concatenate(resp) if S else np.zeros(0, int)
+    t = Pn + s
+    pred_r = np.where(i == 0, Pn - 1, t - 1)
+    out = {"tokens": np.concatenate([prompt, rt]), "labels": np.concatenate([np.full(Pn, -1), rt]),
+           "positions": np.concatenate([np.arange(Pn), Pn + i]), "seg": np.concatenate([np.zeros(Pn), k + 1]),
+           "pred": np.concatenate([np.arange(Pn) - 1, pred_r]),
+           "row_ptr": np.concatenate([np.zeros(Pn), G + s - k, [S]]),
+           "scored_pos": t, "scored_label": rt, "pred_pos": pred_r, "sample_of": k}
+    row_idx = np.zeros(S, np.int64)
+    row_idx[:G] = cu[:G]
+    nl = i != lens[k] - 1
+    row_idx[(G + s - k)[nl]] = (s + 1)[nl]
+    out["row_idx"] = row_idx
+    return out, T, S
+
+
+@pytest.mark.parametrize("Pn", [1, 2, 3, 4, 5, 511, 513, 1023])
+def test_pack_every_array_bit_exact(P, ctx32, Pn):
+    """All eleven K1 arrays (incl. the scored-row gathers and the head-row CSR) against a numpy
+    restatement, for every prompt length mod 4 (the 16-byte store paths), over several blocks of
+    the grid-stride loop and with many short responses."""
+    import ctypes as C
+
+    f = P.LIB.parl_debug_group_arrays
+    f.restype, f.argtypes = C.c_int, [C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(Pn)
+    for G, hi in ((1, 300), (3, 2000), (64, 40), (200, 9000)):
+        prompt = rng.integers(4, 151936, Pn).astype(np.int32)
+        resp = [rng.integers(4, 151936, int(rng.integers(1, hi))).astype(np.int32) for _ in range(G)]
+        pk = P.pack_group(prompt, resp, 1 << 22, ctx32)
+        ref, T, S = _pack_arrays_np(prompt, resp)
+        buf = np.zeros(6 * T + 1 + 5 * S, np.int32)
+        assert f(pk.group.h, buf.ctypes.data) == 0
+        off = 0
+        for name, n in (("tokens", T), ("labels", T), ("positions", T), ("seg", T), ("pred", T), ("row_ptr", T + 1),
+                        ("scored_pos", S), ("scored_label", S), ("pred_pos", S), ("sample_of", S), ("row_idx", S)):
+            assert np.array_equal(buf[off:off + n], ref[name]), (Pn, G, name)
+            off += n
+
+
 # --------------------------------------------------------------------------- init parity
 def test_init_bit_exact(P, ctx32, orc):
     cfg = tiny(P)
