@@ -79,6 +79,24 @@ struct HostStage {
         PARL_CUDA(cudaEventRecord(ev, st));
         pending = true;
     }
+    // two host ranges into one pinned buffer, two copies, one completion event
+    void upload2(void* dst1, const void* src1, size_t n1, void* dst2, const void* src2, size_t n2, cudaStream_t st) {
+        if (pending) PARL_CUDA(cudaEventSynchronize(ev));
+        const size_t n1a = (n1 + 15) & ~size_t(15), n = n1a + n2;
+        if (n > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            PARL_CUDA(cudaMallocHost(&p, n));
+            bytes = n;
+        }
+        if (!ev) PARL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        std::memcpy(p, src1, n1);
+        std::memcpy(static_cast<char*>(p) + n1a, src2, n2);
+        if (n1) PARL_CUDA(cudaMemcpyAsync(dst1, p, n1, cudaMemcpyHostToDevice, st));
+        if (n2) PARL_CUDA(cudaMemcpyAsync(dst2, static_cast<char*>(p) + n1a, n2, cudaMemcpyHostToDevice, st));
+        PARL_CUDA(cudaEventRecord(ev, st));
+        pending = true;
+    }
     ~HostStage() {
         if (pending) cudaEventSynchronize(ev);
         if (ev) cudaEventDestroy(ev);
@@ -253,6 +271,10 @@ struct parl_group_s {
     SegLayout segs;
     DevBuf tok_keys, tok_idx, pos_keys, pos_idx, iota, sort_tmp, sched_buf, work_buf;
     HostStage sched_stage, work_stage, adv_stage, multi_stage;  // pinned staging: async uploads, no host block
+    // host token inputs (parl_pack / parl_pack_multi): a pageable copy above 64 KB would block the
+    // host until the stream drains; two pinned stages let the host run a micro-batch ahead
+    HostStage in_stage[2];
+    int in_flip = 0;
     int n_groups = 1, group_G = 0;  // prompt groups in the sequence; responses per group (0: not uniform)
     DevBuf multi_tab, multi_prompts, multi_resp;
     AttnSched sched;
@@ -1833,8 +1855,8 @@ parl_status parl_pack(parl_group_t g, const int32_t* prompt, int P, const int32_
         cudaStream_t st = g->ctx->st;
         int32_t* dp = g->in_prompt.as<int32_t>(g->max_T);
         int32_t* dr = g->in_resp.as<int32_t>(g->max_T);
-        PARL_CUDA(cudaMemcpyAsync(dp, prompt, (size_t)P * 4, cudaMemcpyHostToDevice, st));
-        PARL_CUDA(cudaMemcpyAsync(dr, resp_flat, (size_t)g->S * 4, cudaMemcpyHostToDevice, st));
+        g->in_flip ^= 1;
+        g->in_stage[g->in_flip].upload2(dp, prompt, (size_t)P * 4, dr, resp_flat, (size_t)g->S * 4, st);
         upload_meta(g);
         ProfScope ps(g->ctx, PARL_KC_PACK, 24.0 * g->T + 24.0 * g->S);
         launch_pack(dp, P, dr, group_cu(g), G, g->T, g->pk, nullptr, st);
@@ -1935,8 +1957,8 @@ parl_status parl_pack_multi(parl_group_t g, const int32_t* prompts, const int32_
         cudaStream_t st = g->ctx->st;
         int32_t* dp = g->multi_prompts.as<int32_t>(np);
         int32_t* dr = g->multi_resp.as<int32_t>(g->S);
-        PARL_CUDA(cudaMemcpyAsync(dp, prompts, (size_t)np * 4, cudaMemcpyHostToDevice, st));
-        PARL_CUDA(cudaMemcpyAsync(dr, resp_flat, (size_t)g->S * 4, cudaMemcpyHostToDevice, st));
+        g->in_flip ^= 1;
+        g->in_stage[g->in_flip].upload2(dp, prompts, (size_t)np * 4, dr, resp_flat, (size_t)g->S * 4, st);
         pack_multi_launch(g, dp, dr, tab, nullptr);
     });
 }
