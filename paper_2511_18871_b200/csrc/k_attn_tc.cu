@@ -956,6 +956,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
     uint64_t* p_full = s_full + 2;
     uint64_t* g_done = s_full + 3;
     uint64_t* acc_full = s_full + 4;
+    uint64_t* dp_full = s_full + 5;  // dP of the current tile (S is committed first, on s_full)
     uint32_t* tbase_s = reinterpret_cast<uint32_t*>(s_full + 6);
     float* vec = reinterpret_cast<float*>(smem + L::OFF_VEC);
 
@@ -978,6 +979,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
             tc::mbar_init(&b_empty[s], 1);
         }
         tc::mbar_init(s_full, 1);
+        tc::mbar_init(dp_full, 1);
         tc::mbar_init(s_free, 8);
         tc::mbar_init(p_full, 8);
         tc::mbar_init(g_done, 1);
@@ -1076,14 +1078,21 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 tc::tc_fence_after();
                 const uint32_t f0 = tc::smem_u32(smem + L::OFF_A + (ab * 2) * L::TILE);
                 const uint32_t s0 = tc::smem_u32(smem + L::OFF_B + (st * 2) * L::TILE);
+                // Dh 128: S first, on its own barrier, so the element-wise warps start the exponentials
+                // while dP is still in the tensor pipe
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
                     tc::mma_bf16_e(t_s, tc::sdesc(f0 + off, 16, 1024), tc::sdesc(s0 + off, 16, 1024), id_s, ks > 0);
+                }
+                if (DH == 128) tc::mma_commit_e(s_full);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * (128 * 128) + (ks & 3) * 32;
                     tc::mma_bf16_e(t_dp, tc::sdesc(f0 + L::TILE + off, 16, 1024),
                                  tc::sdesc(s0 + L::TILE + off, 16, 1024), id_s, ks > 0);
                 }
-                tc::mma_commit_e(s_full);
+                tc::mma_commit_e(DH == 128 ? dp_full : s_full);  // Dh 64: S and dP on one barrier
                 if (MODE == MODE_DKV) ATTN_TRACE(2, cS, 0);
                 ++cS;
                 ++gS;
@@ -1191,6 +1200,89 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                 tc::tc_fence_after();
                 if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 1);
                 uint32_t pp[32], pd[32];  // packed bf16 P / dS of this thread's 64 columns
+                if constexpr (DH == 128) {  // measured: +4% at Dh 128, -7% at Dh 64 (profiles/r02_ab_attn_bwd_split.txt)
+                // S (both 32-column chunks) first; P = exp2(S c - lse) runs while dP is still being
+                // computed; then dP, after which S / dP are released so the next tile's MMAs overlap
+                float pv[64], dall[64];
+                tc::tmem_ld32_nowait(t_s + half * 64 + lane_off, reinterpret_cast<uint32_t*>(pv));
+                tc::tmem_ld32_nowait(t_s + half * 64 + 32 + lane_off, reinterpret_cast<uint32_t*>(pv) + 32);
+                tc::tmem_ld_wait();
+                if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 2);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int cb = half * 64 + c * 32;  // first tile column of the chunk
+                    float* sv = pv + 32 * c;
+                    // exponent argument (log2 units); -inf where the pair is masked
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float l4[4];
+                        if (MODE == MODE_DKV) {
+                            uint32_t w0, w1, w2, w3;
+                            tc::lds128(vl + (cb + j) * 4, w0, w1, w2, w3);
+                            l4[0] = __uint_as_float(w0); l4[1] = __uint_as_float(w1);
+                            l4[2] = __uint_as_float(w2); l4[3] = __uint_as_float(w3);
+                        } else {
+                            l4[0] = l4[1] = l4[2] = l4[3] = lr;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) sv[j + q] = fmaf(sv[j + q], c2, -l4[q]);
+                    }
+                    if (!full) {
+                        const int cu = u0 + cb;
+                        int lo, hi, l2, h2;
+                        if (MODE == MODE_DKV) {
+                            lo = min(max(x - cu, 0), 32);
+                            hi = min(max(qhi - cu, 0), 32);
+                            l2 = h2 = 32;
+                        } else {
+                            lo = min(max(l0 - cu, 0), 32);
+                            hi = min(max(e0 - cu, 0), 32);
+                            l2 = min(max(b1 - cu, 0), 32);
+                            h2 = min(max(e1 - cu, 0), 32);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = ((j >= lo) & (j < hi)) | ((j >= l2) & (j < h2));
+                            sv[j] = ok ? sv[j] : -INFINITY;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        sv[j] = tc::ex2_approx(sv[j]);
+                        sv[j + 1] = tc::ex2_approx(sv[j + 1]);
+                        pp[c * 16 + j / 2] = pack2(sv[j], sv[j + 1]);
+                    }
+                }
+                tc::mbar_wait(dp_full, cS & 1);
+                tc::tc_fence_after();
+                tc::tmem_ld32_nowait(t_dp + half * 64 + lane_off, reinterpret_cast<uint32_t*>(dall));
+                tc::tmem_ld32_nowait(t_dp + half * 64 + 32 + lane_off, reinterpret_cast<uint32_t*>(dall) + 32);
+                tc::tmem_ld_wait();
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(s_free);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int cb = half * 64 + c * 32;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float d4[4];
+                        if (MODE == MODE_DKV) {
+                            uint32_t w0, w1, w2, w3;
+                            tc::lds128(vl + (128 + cb + j) * 4, w0, w1, w2, w3);
+                            d4[0] = __uint_as_float(w0); d4[1] = __uint_as_float(w1);
+                            d4[2] = __uint_as_float(w2); d4[3] = __uint_as_float(w3);
+                        } else {
+                            d4[0] = d4[1] = d4[2] = d4[3] = dr;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; q += 2) {
+                            const int jj = 32 * c + j + q;
+                            pd[jj / 2] = pack2(pv[jj] * (dall[jj] - d4[q]), pv[jj + 1] * (dall[jj + 1] - d4[q + 1]));
+                        }
+                    }
+                }
+                } else {
                 // all four TMEM loads (S and dP, both 32-column chunks) in flight at once, then
                 // S/dP are released so the next tile's S/dP MMAs overlap this tile's math
                 float sall[64], dall[64];
@@ -1256,6 +1348,7 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                         pp[c * 16 + j / 2] = pack2(p0, p1);
                         pd[c * 16 + j / 2] = pack2(p0 * dd[j], p1 * dd[j + 1]);
                     }
+                }
                 }
                 if (MODE == MODE_DKV) ATTN_TRACE(4 + warp, cS, 3);
                 // the previous tile's gradient MMAs have read P / dS
