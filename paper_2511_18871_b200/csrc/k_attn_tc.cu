@@ -89,6 +89,9 @@ struct PairSmem {
     static constexpr int TOTAL = OFF_L0 + (DH == 64 ? 2 * 256 * 4 : 0) + 1024;
 };
 
+#ifndef ATTN_F32X2
+#define ATTN_F32X2 1  // packed fp32 pair arithmetic (FFMA2 / FADD2) in the Dh 64 forward softmax
+#endif
 #ifndef ATTN_POLY_MASK
 // which of every 8 exps of a full tile run on the FMA pipe (Dh 64 forward, FA4-style).  Measured
 // at C2: 0x00 0.067 ms, 0x80 0.068, 0x88 0.069, 0x8a 0.071 per 2 groups -- the softmax is not
@@ -448,15 +451,21 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     const float mb = m_new == -INFINITY ? 0.f : m_new;
                     float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
                     uint32_t pk[32];
+                    {  // packed fp32 pairs (FFMA2 / FADD2), the same per-lane arithmetic and sum order
+                        const float2 c22 = make_float2(c2, c2), mb2 = make_float2(-mb, -mb);
+                        float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < 64; j += 4) {
-                        const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
-                        const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
-                        const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
-                        const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
-                        sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
-                        pk[j / 2] = pack2(p0, p1);
-                        pk[j / 2 + 1] = pack2(p2, p3);
+                        for (int j = 0; j < 64; j += 4) {
+                            const float2 a01 = tc::ffma2(make_float2(sv[j], sv[j + 1]), c22, mb2);
+                            const float2 a23 = tc::ffma2(make_float2(sv[j + 2], sv[j + 3]), c22, mb2);
+                            const float2 p01 = make_float2(tc::ex2_approx(a01.x), tc::ex2_approx(a01.y));
+                            const float2 p23 = make_float2(tc::ex2_approx(a23.x), tc::ex2_approx(a23.y));
+                            s01 = tc::fadd2(s01, p01);
+                            s23 = tc::fadd2(s23, p23);
+                            pk[j / 2] = pack2(p01.x, p01.y);
+                            pk[j / 2 + 1] = pack2(p23.x, p23.y);
+                        }
+                        sm0 = s01.x; sm1 = s01.y; sm2 = s23.x; sm3 = s23.y;
                     }
                     if (q4 == 0) ATTN_TRACE(w, cS, 3);
                     // the previous chunk's PV has finished writing O
@@ -737,6 +746,23 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                         for (int q = 0; q < 4; ++q) pk[j / 2 + q] = pack2(pe[2 * q], pe[2 * q + 1]);
                     }
                 } else {  // masked scores are -inf: MUFU gives their exact zero
+#if ATTN_F32X2
+                    // packed fp32 pairs: one FFMA2 per two arguments, one FADD2 per two row-sum terms
+                    const float2 c22 = make_float2(c2, c2), mb2 = make_float2(-mb, -mb);
+                    float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        const float2 a01 = tc::ffma2(make_float2(sv[j], sv[j + 1]), c22, mb2);
+                        const float2 a23 = tc::ffma2(make_float2(sv[j + 2], sv[j + 3]), c22, mb2);
+                        const float2 p01 = make_float2(tc::ex2_approx(a01.x), tc::ex2_approx(a01.y));
+                        const float2 p23 = make_float2(tc::ex2_approx(a23.x), tc::ex2_approx(a23.y));
+                        s01 = tc::fadd2(s01, p01);
+                        s23 = tc::fadd2(s23, p23);
+                        pk[j / 2] = pack2(p01.x, p01.y);
+                        pk[j / 2 + 1] = pack2(p23.x, p23.y);
+                    }
+                    sm0 = s01.x; sm1 = s01.y; sm2 = s23.x; sm3 = s23.y;
+#else
 #pragma unroll
                     for (int j = 0; j < 128; j += 4) {
                         const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
@@ -747,6 +773,7 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                         pk[j / 2] = pack2(p0, p1);
                         pk[j / 2 + 1] = pack2(p2, p3);
                     }
+#endif
                 }
                 if (q4 == 0) ATTN_TRACE(w, cS, 3);
                 // the previous PV of this tile has finished reading P and writing O
@@ -1224,8 +1251,10 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                         } else {
                             l4[0] = l4[1] = l4[2] = l4[3] = lr;
                         }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) sv[j + q] = fmaf(sv[j + q], c2, -l4[q]);
+                        const float2 c22 = make_float2(c2, c2);
+                        const float2 a01 = tc::ffma2(make_float2(sv[j], sv[j + 1]), c22, make_float2(-l4[0], -l4[1]));
+                        const float2 a23 = tc::ffma2(make_float2(sv[j + 2], sv[j + 3]), c22, make_float2(-l4[2], -l4[3]));
+                        sv[j] = a01.x; sv[j + 1] = a01.y; sv[j + 2] = a23.x; sv[j + 3] = a23.y;
                     }
                     if (!full) {
                         const int cu = u0 + cb;
@@ -1278,7 +1307,9 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
 #pragma unroll
                         for (int q = 0; q < 4; q += 2) {
                             const int jj = 32 * c + j + q;
-                            pd[jj / 2] = pack2(pv[jj] * (dall[jj] - d4[q]), pv[jj + 1] * (dall[jj + 1] - d4[q + 1]));
+                            const float2 dd = tc::fadd2(make_float2(dall[jj], dall[jj + 1]), make_float2(-d4[q], -d4[q + 1]));
+                            const float2 ds = tc::fmul2(make_float2(pv[jj], pv[jj + 1]), dd);
+                            pd[jj / 2] = pack2(ds.x, ds.y);
                         }
                     }
                 }
@@ -1317,11 +1348,13 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                             l4[0] = l4[1] = l4[2] = l4[3] = lr;
                             d4[0] = d4[1] = d4[2] = d4[3] = dr;
                         }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            arg[j + q] = fmaf(sv[j + q], c2, -l4[q]);
-                            dd[j + q] = dp[j + q] - d4[q];
-                        }
+                        const float2 c22 = make_float2(c2, c2);
+                        const float2 a01 = tc::ffma2(make_float2(sv[j], sv[j + 1]), c22, make_float2(-l4[0], -l4[1]));
+                        const float2 a23 = tc::ffma2(make_float2(sv[j + 2], sv[j + 3]), c22, make_float2(-l4[2], -l4[3]));
+                        const float2 d01 = tc::fadd2(make_float2(dp[j], dp[j + 1]), make_float2(-d4[0], -d4[1]));
+                        const float2 d23 = tc::fadd2(make_float2(dp[j + 2], dp[j + 3]), make_float2(-d4[2], -d4[3]));
+                        arg[j] = a01.x; arg[j + 1] = a01.y; arg[j + 2] = a23.x; arg[j + 3] = a23.y;
+                        dd[j] = d01.x; dd[j + 1] = d01.y; dd[j + 2] = d23.x; dd[j + 3] = d23.y;
                     }
                     if (!full) {
                         const int cu = u0 + cb;
@@ -1344,9 +1377,10 @@ __global__ void __launch_bounds__(BWD_NTHR, 1)
                     }
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) {
-                        const float p0 = tc::ex2_approx(arg[j]), p1 = tc::ex2_approx(arg[j + 1]);
-                        pp[c * 16 + j / 2] = pack2(p0, p1);
-                        pd[c * 16 + j / 2] = pack2(p0 * dd[j], p1 * dd[j + 1]);
+                        const float2 p = make_float2(tc::ex2_approx(arg[j]), tc::ex2_approx(arg[j + 1]));
+                        const float2 ds = tc::fmul2(p, make_float2(dd[j], dd[j + 1]));
+                        pp[c * 16 + j / 2] = pack2(p.x, p.y);
+                        pd[c * 16 + j / 2] = pack2(ds.x, ds.y);
                     }
                 }
                 }
