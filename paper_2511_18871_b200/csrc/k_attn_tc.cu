@@ -98,6 +98,13 @@ struct PairSmem {
 // MUFU-bound here (XU 43%, stalls on fixed-latency waits), so the default keeps MUFU only.
 #define ATTN_POLY_MASK 0x00
 #endif
+#ifndef ATTN_POLY_PAIRS
+// of every 8 exp pairs of a full tile, how many run on the FMA pipe (packed-pair math).  With the
+// FFMA2 / FADD2 softmax the Dh 64 forward is MUFU-bound: 1 pair +0.8%, 2 pairs +2.3% at C2
+// (profiles/r02_ab_attn_poly_pairs.txt).  Off by default: a tile's exps then depend on whether it is
+// full, so regrouping sequences (several prompt groups per sequence) would no longer be bit-identical.
+#define ATTN_POLY_PAIRS 0
+#endif
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 
@@ -732,19 +739,29 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                 // P = exp2(S * c - m) -> bf16 (registers)
                 float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;
                 uint32_t pk[64];
-                if (ATTN_POLY_MASK != 0 && (f & FULL)) {  // a share of the exps on the FMA pipe, the rest on MUFU
-                    float pe[8];
+                if (ATTN_POLY_PAIRS != 0 && (f & FULL)) {
+                    // FA4-style: the last ATTN_POLY_PAIRS pairs of every 16 exps on the FMA pipe, the rest on
+                    // MUFU (full tiles only: masked -inf scores need MUFU's exact zero)
+                    const float2 c22 = make_float2(c2, c2), mb2 = make_float2(-mb, -mb);
+                    float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int j = 0; j < 128; j += 8) {
+                    for (int j = 0; j < 128; j += 16) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float x = fmaf(sv[j + q], c2, -mb);
-                            pe[q] = ((ATTN_POLY_MASK >> q) & 1) ? tc::exp2_fma(x) : tc::ex2_approx(x);
+                        for (int q = 0; q < 16; q += 4) {
+                            const float2 a01 = tc::ffma2(make_float2(sv[j + q], sv[j + q + 1]), c22, mb2);
+                            const float2 a23 = tc::ffma2(make_float2(sv[j + q + 2], sv[j + q + 3]), c22, mb2);
+                            const bool poly01 = (q / 2) >= 8 - ATTN_POLY_PAIRS, poly23 = (q / 2 + 1) >= 8 - ATTN_POLY_PAIRS;
+                            const float2 p01 = poly01 ? tc::exp2_fma2(a01)
+                                                      : make_float2(tc::ex2_approx(a01.x), tc::ex2_approx(a01.y));
+                            const float2 p23 = poly23 ? tc::exp2_fma2(a23)
+                                                      : make_float2(tc::ex2_approx(a23.x), tc::ex2_approx(a23.y));
+                            s01 = tc::fadd2(s01, p01);
+                            s23 = tc::fadd2(s23, p23);
+                            pk[(j + q) / 2] = pack2(p01.x, p01.y);
+                            pk[(j + q) / 2 + 1] = pack2(p23.x, p23.y);
                         }
-                        sm0 += pe[0] + pe[4]; sm1 += pe[1] + pe[5]; sm2 += pe[2] + pe[6]; sm3 += pe[3] + pe[7];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) pk[j / 2 + q] = pack2(pe[2 * q], pe[2 * q + 1]);
                     }
+                    sm0 = s01.x; sm1 = s01.y; sm2 = s23.x; sm3 = s23.y;
                 } else {  // masked scores are -inf: MUFU gives their exact zero
 #if ATTN_F32X2
                     // packed fp32 pairs: one FFMA2 per two arguments, one FADD2 per two row-sum terms

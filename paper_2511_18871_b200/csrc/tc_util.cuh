@@ -98,6 +98,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return r;
 }
 
+// exp2_fma on a pair, in packed-pair arithmetic (FADD2 / FFMA2, one LEA per lane for the
+// exponent field): 10 issue slots for two exponentials, none of them on MUFU
+__device__ __forceinline__ float2 exp2_fma2(float2 x);
+
 // packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2): one issue slot for two lanes' worth
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     float2 d;
@@ -123,6 +127,19 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
         : "=f"(d.x), "=f"(d.y)
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
+}
+
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 C = make_float2(12582912.f, 12582912.f);
+    const float2 tt = fadd2(x, C);
+    const float2 f = ffma2(fadd2(tt, make_float2(-12582912.f, -12582912.f)), make_float2(-1.f, -1.f), x);
+    float2 p = ffma2(make_float2(0.05500898f, 0.05500898f), f, make_float2(0.24221104f, 0.24221104f));
+    p = ffma2(p, f, make_float2(0.6932829f, 0.6932829f));
+    p = ffma2(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(tt.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(tt.y) << 23)));
 }
 
 // 2^x on the FMA / ALU pipes (no MUFU): round-to-nearest split through the 1.5 * 2^23
