@@ -90,6 +90,31 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// The same GELU / GELU' on a pair in packed fp32 arithmetic (FFMA2 / FMUL2: the per-lane
+// operations and rounding of gelu_dev / gelu_grad_dev, half the issue slots)
+__device__ __forceinline__ float2 erf_arg2(float2 x, float2 x2) {
+    x2.x = fminf(x2.x, 72.f);
+    x2.y = fminf(x2.y, 72.f);
+    const float2 p = tc::ffma2(x2, tc::ffma2(x2, make_float2(-0.000315806263f, -0.000315806263f),
+                                             make_float2(0.0367982576f, 0.0367982576f)),
+                               make_float2(0.797717834f, 0.797717834f));
+    return tc::fmul2(x, p);
+}
+__device__ __forceinline__ float2 gelu_dev2(float2 x) {
+    const float2 h = tc::fmul2(make_float2(0.5f, 0.5f), x);
+    const float2 y = erf_arg2(x, tc::fmul2(x, x));
+    return tc::ffma2(h, make_float2(tanh_approx(y.x), tanh_approx(y.y)), h);
+}
+__device__ __forceinline__ float2 gelu_grad_dev2(float2 x) {
+    const float2 x2 = tc::fmul2(x, x);
+    const float2 y = erf_arg2(x, x2);
+    const float2 phi = tc::ffma2(make_float2(0.5f, 0.5f), make_float2(tanh_approx(y.x), tanh_approx(y.y)),
+                                 make_float2(0.5f, 0.5f));
+    const float2 ea = tc::fmul2(x2, make_float2(-0.72134752044448170368f, -0.72134752044448170368f));
+    const float2 e = make_float2(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
+    return tc::ffma2(tc::fmul2(x, make_float2(0.39894228040143267794f, 0.39894228040143267794f)), e, phi);
+}
 // byte offset of 16-byte chunk j of row r in a [32 x 128 B] SWIZZLE_128B / [32 x 64 B] SWIZZLE_64B tile
 __device__ __forceinline__ uint32_t sw128(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 __device__ __forceinline__ uint32_t sw64(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
@@ -132,7 +157,7 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
     const uint32_t in_bytes = a0.epi == EPI_RESID ? 4096u : 2048u;
     const bool do_store = a0.epi != EPI_LSE || a0.store_logits;
 
-    auto coords = [&](int item, int& row, int& col, int& sp) {
+    auto coords_calc = [&](int item, int& row, int& col, int& sp) {
         const int t = item % e.tpp;
         int mt, nt;
         if (a0.raster) {
@@ -148,6 +173,27 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
         }
         row = mt * e.mrows + e.rank * BM + ew * 32;
         col = nt * BNT + hcol;
+    };
+    // the chunk streams (prefetch, bias, current) ask for the same item NCH times in a row, and the
+    // integer divisions above cost ~60 instructions: keep the last two items' coordinates
+    int ci0 = -1, cr0 = 0, cc0 = 0, cs0 = 0, ci1 = -1, cr1 = 0, cc1 = 0, cs1 = 0;
+    bool c_next = false;
+    auto coords = [&](int item, int& row, int& col, int& sp) {
+        if (ci0 == item) {
+            row = cr0; col = cc0; sp = cs0;
+            return;
+        }
+        if (ci1 == item) {
+            row = cr1; col = cc1; sp = cs1;
+            return;
+        }
+        coords_calc(item, row, col, sp);
+        if (c_next) {
+            ci1 = item; cr1 = row; cc1 = col; cs1 = sp;
+        } else {
+            ci0 = item; cr0 = row; cc0 = col; cs0 = sp;
+        }
+        c_next = !c_next;
     };
     // chunk stream: (item, c) -> the next chunk; item >= n_items when exhausted
     auto next = [&](int& item, int& c) {
@@ -238,18 +284,21 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
                         tc::sts128(sb + sw128(lane, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
                                    __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
                     break;
-                case EPI_RESID:
+                case EPI_RESID: {  // all inputs first: the shared loads are ordered behind the stores
+                    uint32_t r[32];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) tc::lds128(sb + sw128(lane, j), r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        uint32_t r0, r1, r2, r3;
-                        const uint32_t ad = sb + sw128(lane, j);
-                        tc::lds128(ad, r0, r1, r2, r3);
-                        tc::sts128(ad, __float_as_uint(__uint_as_float(r0) + v[4 * j]),
-                                   __float_as_uint(__uint_as_float(r1) + v[4 * j + 1]),
-                                   __float_as_uint(__uint_as_float(r2) + v[4 * j + 2]),
-                                   __float_as_uint(__uint_as_float(r3) + v[4 * j + 3]));
+                        const float2 s0 = tc::fadd2(make_float2(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1])),
+                                                    make_float2(v[4 * j], v[4 * j + 1]));
+                        const float2 s1 = tc::fadd2(make_float2(__uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])),
+                                                    make_float2(v[4 * j + 2], v[4 * j + 3]));
+                        tc::sts128(sb + sw128(lane, j), __float_as_uint(s0.x), __float_as_uint(s0.y), __float_as_uint(s1.x),
+                                   __float_as_uint(s1.y));
                     }
                     break;
+                }
                 case EPI_ACT:
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
@@ -257,44 +306,47 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
                                    pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
                                    pack_bf16(v[8 * j + 6], v[8 * j + 7]));
                     break;
-                case EPI_GELU:
+                case EPI_GELU: {  // 16 independent pairs, then the stores
+                    uint32_t u[16], g[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        u[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
+                        const float2 gg = gelu_dev2(make_float2(bf_lo(u[q]), bf_hi(u[q])));
+                        g[q] = pack_bf16(gg.x, gg.y);
+                    }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        uint32_t u[4], g[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            u[q] = pack_bf16(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
-                            g[q] = pack_bf16(gelu_dev(bf_lo(u[q])), gelu_dev(bf_hi(u[q])));
-                        }
-                        tc::sts128(sb + sw64(lane, j), u[0], u[1], u[2], u[3]);
-                        tc::sts128(sb + 2048 + sw64(lane, j), g[0], g[1], g[2], g[3]);
+                        tc::sts128(sb + sw64(lane, j), u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+                        tc::sts128(sb + 2048 + sw64(lane, j), g[4 * j], g[4 * j + 1], g[4 * j + 2], g[4 * j + 3]);
                     }
                     break;
-                case EPI_GELU_ACT:  // activation only (no backward will need the pre-activation)
+                }
+                case EPI_GELU_ACT: {  // activation only (no backward will need the pre-activation)
+                    uint32_t g[16];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint32_t g[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t u = pack_bf16(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
-                            g[q] = pack_bf16(gelu_dev(bf_lo(u)), gelu_dev(bf_hi(u)));
-                        }
-                        tc::sts128(sb + sw64(lane, j), g[0], g[1], g[2], g[3]);
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t u = pack_bf16(v[2 * q], v[2 * q + 1]);
+                        const float2 gg = gelu_dev2(make_float2(bf_lo(u), bf_hi(u)));
+                        g[q] = pack_bf16(gg.x, gg.y);
                     }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) tc::sts128(sb + sw64(lane, j), g[4 * j], g[4 * j + 1], g[4 * j + 2], g[4 * j + 3]);
                     break;
-                case EPI_GELU_BWD:
+                }
+                case EPI_GELU_BWD: {  // all inputs first, then 16 independent pairs, then the stores
+                    uint32_t x[16];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint32_t x[4];
-                        const uint32_t ad = sb + sw64(lane, j);
-                        tc::lds128(ad, x[0], x[1], x[2], x[3]);
+                    for (int j = 0; j < 4; ++j) tc::lds128(sb + sw64(lane, j), x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            x[q] = pack_bf16(v[8 * j + 2 * q] * gelu_grad_dev(bf_lo(x[q])),
-                                             v[8 * j + 2 * q + 1] * gelu_grad_dev(bf_hi(x[q])));
-                        tc::sts128(ad, x[0], x[1], x[2], x[3]);
+                    for (int q = 0; q < 16; ++q) {
+                        const float2 gd = tc::fmul2(make_float2(v[2 * q], v[2 * q + 1]),
+                                                    gelu_grad_dev2(make_float2(bf_lo(x[q]), bf_hi(x[q]))));
+                        x[q] = pack_bf16(gd.x, gd.y);
                     }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) tc::sts128(sb + sw64(lane, j), x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
                     break;
+                }
                 case EPI_LSE: {
                     const int ncol = min(32, a.N - col);
                     float cm = -INFINITY;
