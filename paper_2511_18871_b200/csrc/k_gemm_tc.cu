@@ -392,6 +392,8 @@ __device__ __forceinline__ void epilogue_warps(const TcArgs* av, const CUtensorM
                     if (epi == EPI_F32_ACC) {
                         if (a.splits > 1) tc::tma_store_3d(mo + prob, sb, col, row0, sp);
                         else tc::tma_reduce_add_2d(mo + prob, sb, col, row0);
+                    } else if (epi == EPI_LSE) {  // the policy's logits: written once, read by the backward
+                        tc::tma_store_2d_hint(mo + prob, sb, col, row0, tc::l2_evict_first_policy());
                     } else {
                         tc::tma_store_2d(mo + prob, sb, col, row0);
                         if (epi == EPI_GELU) tc::tma_store_2d(mo2 + prob, sb + 2048, col, row0);
@@ -607,6 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer (both CTAs, completing on the leader's barrier)
+        const uint64_t pol_keep = tc::l2_evict_last_policy();
         uint32_t cnt = 0;
         for (int item = cid; item < n_items; item += ncl) {
             const int prob = item / tpp, t = item % tpp;
@@ -626,7 +629,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 uint8_t* sa = smem + s * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
                 if (!A_MN) {
-                    tc::tma_load_2d_pair(sa, tA, fb, kb * BK, m0);
+                    // m-fastest sweeps re-read all of A once per n-tile column: keep it in L2 (the LM head,
+                    // where the 10 GB logits stream would otherwise evict it)
+                    if (a.epi == EPI_LSE && !a.raster) tc::tma_load_2d_pair_hint(sa, tA, fb, kb * BK, m0, pol_keep);
+                    else tc::tma_load_2d_pair(sa, tA, fb, kb * BK, m0);
                 } else {
                     tc::tma_load_2d_pair(sa, tA, fb, m0, kb * BK);
                     tc::tma_load_2d_pair(sa + 8192, tA, fb, m0 + 64, kb * BK);
