@@ -17,8 +17,9 @@
 //                  each (sample, warp range) partial goes to its own slot (index
 //                  sample + range), so the finisher adds them in a fixed order:
 //                  deterministic, no atomics.
-//   k_grpo_finish  warp per sample: per-sample terms (SampleTerms, grpo.hpp:64-70); the
-//                  last block adds the running stats (pipeline.cpp:131-137), fixed order.
+//   k_grpo_finish  warp (long samples) or thread (short ones) per sample: per-sample terms
+//                  (SampleTerms, grpo.hpp:64-70); block partials of the running stats, added
+//                  in index order by the last block (pipeline.cpp:131-137).
 //   k_grpo_bcast   sequence granularity only: broadcast g_j to every token.
 //
 // Hot path inputs are the fp32 device log-probs: the ratio / KL terms are then
@@ -303,75 +304,99 @@ __global__ void __launch_bounds__(GR_WARPS * 32) k_grpo_tokens(const GrpoArgs a)
     }
 }
 
-// Per-sample terms: warp w of the grid takes sample w; its lanes add the sample's (sample,
-// range) partials in a fixed strided order, then a fixed-order butterfly.  Terms go to
-// a.terms (and per_sample when requested).  The last block to finish (a ticket that
-// k_grpo_tokens zeroed) adds the running stats (pipeline.cpp:131-137): thread-strided
-// sums over the samples in index order, then a fixed-order tree -- deterministic whichever
-// block draws the last ticket.
-__global__ void __launch_bounds__(1024) k_grpo_finish(const GrpoArgs a) {
+// Per-sample terms (SampleTerms, grpo.hpp:64-70) from the (sample, range) partials, then the
+// running stats (pipeline.cpp:131-137).  Two shapes, chosen per launch from S / n:
+//   WPS (long samples, many partials each): warp w takes sample w, its lanes add the partials in
+//        a fixed strided order, then a fixed butterfly;
+//   TPS (short samples, a few partials): thread t takes sample t and adds them in order.
+// Each block reduces its samples' stats contributions in a fixed tree into a block partial; the
+// last block to finish (a ticket k_grpo_tokens zeroed) adds the block partials in index order.
+// Deterministic for a given (S, n): the shape and both trees depend on nothing else.
+template <bool WPS>
+__global__ void __launch_bounds__(WPS ? 1024 : 256) k_grpo_finish(const GrpoArgs a) {
     __shared__ double red[5][32];
     __shared__ unsigned ticket;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const int j = (int)(((long)blockIdx.x * blockDim.x + tid) >> 5);
+    const int j = WPS ? (int)(((long)blockIdx.x * blockDim.x + tid) >> 5) : blockIdx.x * blockDim.x + tid;
+    double acc[5] = {0, 0, 0, 0, 0};
     if (j < a.n) {
         const int b = a.cu[j], e = a.cu[j + 1], n = e - b;
         const int b0 = b / a.warp_tokens, b1 = (e - 1) / a.warp_tokens;
         double s0 = 0, s1 = 0, s2 = 0;
+        if constexpr (WPS) {
 #pragma unroll 4
-        for (int k = b0 + lane; k <= b1; k += 32) {
-            const double* o = a.slots + 3 * ((long)j + k);
-            s0 += o[0];
-            s1 += o[1];
-            s2 += o[2];
+            for (int k = b0 + lane; k <= b1; k += 32) {
+                const double* o = a.slots + 3 * ((long)j + k);
+                s0 += o[0];
+                s1 += o[1];
+                s2 += o[2];
+            }
+            s0 = warp_sum_d(s0);
+            s1 = warp_sum_d(s1);
+            s2 = warp_sum_d(s2);
+        } else {
+            for (int k = b0; k <= b1; ++k) {
+                const double* o = a.slots + 3 * ((long)j + k);
+                s0 += o[0];
+                s1 += o[1];
+                s2 += o[2];
+            }
         }
-        s0 = warp_sum_d(s0);
-        s1 = warp_sum_d(s1);
-        s2 = warp_sum_d(s2);
-        if (lane == 0) {
-            double t[4];
+        if (!WPS || lane == 0) {
+            double tm[4];
             if (a.gran == 0) {
                 const double inv = 1.0 / n;
-                t[0] = s0 * inv;
-                t[1] = s1 * inv;
-                t[2] = s2;
-                t[3] = n;
+                tm[0] = s0 * inv;
+                tm[1] = s1 * inv;
+                tm[2] = s2;
+                tm[3] = n;
             } else {  // one evaluation on the summed log-probs (grpo.cpp:134-149)
                 double cv, cg;
                 int c;
                 clip_eval<double>(s0, s1, a.adv_out[j], a.eps, cv, cg, c);
                 const double d = s2 - s0, em = expm1(d);
-                t[0] = cv;
-                t[1] = em - d;
-                t[2] = c;
-                t[3] = 1;
+                tm[0] = cv;
+                tm[1] = em - d;
+                tm[2] = c;
+                tm[3] = 1;
                 a.g_seq[j] = a.up_scale * (cg + a.beta * em);
             }
-            for (int q = 0; q < 4; ++q) a.terms[4 * (long)j + q] = t[q];
             if (a.per_sample)
-                for (int q = 0; q < 4; ++q) a.per_sample[4 * (long)j + q] = t[q];
+                for (int q = 0; q < 4; ++q) a.per_sample[4 * (long)j + q] = tm[q];
+            acc[0] = tm[0] - a.beta * tm[1];
+            acc[1] = tm[0];
+            acc[2] = tm[1];
+            acc[3] = tm[2];
+            acc[4] = tm[3];
         }
     }
     if (!a.stats) return;
+    // the block's contribution: a fixed tree (lanes, then warps in order)
+    if constexpr (!WPS) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[q] = warp_sum_d(acc[q]);
+    }
+    if (lane == 0)
+        for (int q = 0; q < 5; ++q) red[q][wid] = acc[q];
+    __syncthreads();
+    if (tid < 5) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[tid][w];
+        a.terms[5 * (long)blockIdx.x + tid] = s;  // block partials
+    }
     __threadfence();
     __syncthreads();
     if (tid == 0) ticket = atomicAdd(a.ticket, 1u);
     __syncthreads();
     if (ticket != gridDim.x - 1) return;
-    double acc[5] = {0, 0, 0, 0, 0};
-    for (int k = tid; k < a.n; k += blockDim.x) {
-        const double* t = a.terms + 4 * (long)k;
-        const double t0 = __ldcg(t), t1 = __ldcg(t + 1);
-        acc[0] += t0 - a.beta * t1;
-        acc[1] += t0;
-        acc[2] += t1;
-        acc[3] += __ldcg(t + 2);
-        acc[4] += __ldcg(t + 3);
-    }
+    double tot[5] = {0, 0, 0, 0, 0};
+    for (int k = tid; k < (int)gridDim.x; k += blockDim.x)
+        for (int q = 0; q < 5; ++q) tot[q] += __ldcg(a.terms + 5 * (long)k + q);
 #pragma unroll
-    for (int q = 0; q < 5; ++q) acc[q] = warp_sum_d(acc[q]);
+    for (int q = 0; q < 5; ++q) tot[q] = warp_sum_d(tot[q]);
+    __syncthreads();
     if (lane == 0)
-        for (int q = 0; q < 5; ++q) red[q][wid] = acc[q];
+        for (int q = 0; q < 5; ++q) red[q][wid] = tot[q];
     __syncthreads();
     if (tid < 5) {
         double s = 0.0;
@@ -391,16 +416,16 @@ __global__ void __launch_bounds__(256) k_grpo_bcast(const GrpoArgs a) {
 }  // namespace
 
 // slots for the finest warp range (one span): enough for any range length launch_grpo picks
-// (+ 4 per sample: the per-sample terms, + 1: k_grpo_finish's ticket)
+// (+ 5 per finisher block of at most 32 samples: the block partials, + 1: k_grpo_finish's ticket)
 size_t grpo_slot_count(long S, int n) {
-    return 3 * ((size_t)n + (size_t)((S + GR_SPAN - 1) / GR_SPAN) + 1) + 4 * (size_t)n + 1;
+    return 3 * ((size_t)n + (size_t)((S + GR_SPAN - 1) / GR_SPAN) + 1) + 5 * (size_t)((n + 31) / 32) + 1;
 }
 
 void launch_grpo(const GrpoArgs& a_in, cudaStream_t st) {
     if (a_in.S <= 0 || a_in.n <= 0) return;
     GrpoArgs a = a_in;
     a.terms = a.slots + 3 * ((size_t)a.n + (size_t)((a.S + GR_SPAN - 1) / GR_SPAN) + 1);
-    a.ticket = reinterpret_cast<unsigned*>(a.terms + 4 * (size_t)a.n);
+    a.ticket = reinterpret_cast<unsigned*>(a.terms + 5 * (size_t)((a.n + 31) / 32));
     // spans per warp: as many as keep >= ~48 warps per SM busy (fewer slots, longer carried runs)
     const long spans = (a.S + GR_SPAN - 1) / GR_SPAN;
     const int iters = (int)std::max(1L, std::min((long)GR_MAX_ITERS, spans / (148L * 48)));
@@ -415,7 +440,9 @@ void launch_grpo(const GrpoArgs& a_in, cudaStream_t st) {
         else k_grpo_tokens<float, 1><<<grid, GR_WARPS * 32, 0, st>>>(a);
     }
     PARL_LAUNCHED();
-    k_grpo_finish<<<cdiv(a.n, 32), 1024, 0, st>>>(a);
+    // a thread per sample while samples hold a few (sample, range) partials, else a warp
+    if (a.S / a.n > 4L * a.warp_tokens) k_grpo_finish<true><<<cdiv(a.n, 32), 1024, 0, st>>>(a);
+    else k_grpo_finish<false><<<cdiv(a.n, 256), 256, 0, st>>>(a);
     PARL_LAUNCHED();
     if (a.gran == 1) {
         k_grpo_bcast<<<std::min(cdiv(a.S, 256), 148 * 8), 256, 0, st>>>(a);

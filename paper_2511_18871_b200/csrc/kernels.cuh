@@ -130,7 +130,7 @@ struct GrpoArgs {
     double* g_seq = nullptr;       // [n] (sequence granularity)
     double* stats = nullptr;       // [5] += {objective, clip, kl, clipped, units} or null
     int warp_tokens = 0;           // set by launch_grpo: tokens per warp range (slot granularity)
-    double* terms = nullptr;       // set by launch_grpo: [n x 4] per-sample terms (in the slots block)
+    double* terms = nullptr;       // set by launch_grpo: the finisher's block partials of the stats (slots block)
     unsigned* ticket = nullptr;    // set by launch_grpo: k_grpo_finish's last-block ticket (in the slots block)
 };
 size_t grpo_slot_count(long S, int n);
