@@ -12,8 +12,10 @@ NCCL (N>1).  Strong scaling: the global batch is fixed as N grows.  The SGD upda
 
 Prints ONE JSON line (rank 0).  `value` = device-resident inputs, CUDA-event
 timed; `e2e` = the same through the public C-ABI from pinned host buffers with
-H2D/D2H inside the timed region; `roofline` = dominant kernel class timed with
-CUDA events on its launch stream during the timed region; `cpu_baseline` = the
+H2D/D2H inside the timed region, measured right after `value`'s leg; `roofline` =
+the dominant kernel class, every launch timed with CUDA events on its launch
+stream over min(K, 4) further identical steps (a profiling leg kept out of
+`value` and `e2e`); `cpu_baseline` = the
 reference (oracle/_ref, built from the reference's own sources) on a bounded
 sample it really executes, measured tokens/s (a FLOP-model extrapolation to this
 workload is reported separately).  C2 packs 4 prompt groups per sequence (--pack).
