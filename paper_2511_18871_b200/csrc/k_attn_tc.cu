@@ -89,15 +89,6 @@ struct PairSmem {
     static constexpr int TOTAL = OFF_L0 + (DH == 64 ? 2 * 256 * 4 : 0) + 1024;
 };
 
-#ifndef ATTN_F32X2
-#define ATTN_F32X2 1  // packed fp32 pair arithmetic (FFMA2 / FADD2) in the Dh 64 forward softmax
-#endif
-#ifndef ATTN_POLY_MASK
-// which of every 8 exps of a full tile run on the FMA pipe (Dh 64 forward, FA4-style).  Measured
-// at C2: 0x00 0.067 ms, 0x80 0.068, 0x88 0.069, 0x8a 0.071 per 2 groups -- the softmax is not
-// MUFU-bound here (XU 43%, stalls on fixed-latency waits), so the default keeps MUFU only.
-#define ATTN_POLY_MASK 0x00
-#endif
 #ifndef ATTN_POLY_PAIRS
 // of every 8 exp pairs of a full tile, how many run on the FMA pipe (packed-pair math).  With the
 // FFMA2 / FADD2 softmax the Dh 64 forward is MUFU-bound: 1 pair +0.8%, 2 pairs +2.3% at C2
@@ -763,7 +754,6 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                     }
                     sm0 = s01.x; sm1 = s01.y; sm2 = s23.x; sm3 = s23.y;
                 } else {  // masked scores are -inf: MUFU gives their exact zero
-#if ATTN_F32X2
                     // packed fp32 pairs: one FFMA2 per two arguments, one FADD2 per two row-sum terms
                     const float2 c22 = make_float2(c2, c2), mb2 = make_float2(-mb, -mb);
                     float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
@@ -779,18 +769,6 @@ __global__ void __launch_bounds__(PAIR_NTHR, 1)
                         pk[j / 2 + 1] = pack2(p23.x, p23.y);
                     }
                     sm0 = s01.x; sm1 = s01.y; sm2 = s23.x; sm3 = s23.y;
-#else
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        const float p0 = tc::ex2_approx(fmaf(sv[j], c2, -mb));
-                        const float p1 = tc::ex2_approx(fmaf(sv[j + 1], c2, -mb));
-                        const float p2 = tc::ex2_approx(fmaf(sv[j + 2], c2, -mb));
-                        const float p3 = tc::ex2_approx(fmaf(sv[j + 3], c2, -mb));
-                        sm0 += p0; sm1 += p1; sm2 += p2; sm3 += p3;
-                        pk[j / 2] = pack2(p0, p1);
-                        pk[j / 2 + 1] = pack2(p2, p3);
-                    }
-#endif
                 }
                 if (q4 == 0) ATTN_TRACE(w, cS, 3);
                 // the previous PV of this tile has finished reading P and writing O

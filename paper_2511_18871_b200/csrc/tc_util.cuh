@@ -115,8 +115,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return r;
 }
 
-// exp2_fma on a pair, in packed-pair arithmetic (FADD2 / FFMA2, one LEA per lane for the
-// exponent field): 10 issue slots for two exponentials, none of them on MUFU
+// 2^x on a pair without MUFU: round-to-nearest split through the 1.5 * 2^23 magic constant, a
+// degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (relative error 1.0e-4, below bf16's half
+// ulp) and the integer part added into the exponent field; packed-pair arithmetic (FADD2 /
+// FFMA2): 10 issue slots for two exponentials.  x is clamped at -125 (no denormals / zero:
+// callers feed it only finite, unmasked scores).
 __device__ __forceinline__ float2 exp2_fma2(float2 x);
 
 // packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2): one issue slot for two lanes' worth
@@ -159,17 +162,6 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(tt.y) << 23)));
 }
 
-// 2^x on the FMA / ALU pipes (no MUFU): round-to-nearest split through the 1.5 * 2^23
-// magic constant, a degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (relative error
-// 1.0e-4, below bf16's half ulp) and the integer part added into the exponent field.
-// x is clamped at -125 (no denormals / zero: callers feed it only finite, unmasked scores).
-__device__ __forceinline__ float exp2_fma(float x) {
-    x = fmaxf(x, -125.f);
-    const float t = x + 12582912.f;
-    const float f = x - (t - 12582912.f);
-    const float p = fmaf(fmaf(fmaf(0.05500898f, f, 0.24221104f), f, 0.6932829f), f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 // ---- tcgen05 / TMEM ----------------------------------------------------------
 __device__ __forceinline__ void tma_load_2d_pair_hint(void* smem, const CUtensorMap* map, uint32_t leader_bar, int c0,
