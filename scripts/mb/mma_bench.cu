@@ -11,7 +11,7 @@
 
 using namespace parl_gpu;
 
-template <int N, bool TS>
+template <int N, bool TS, int BMN = 0>
 __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int iters) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -31,13 +31,14 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int iters) 
     tc::tc_fence_after();
     const uint32_t tb = tbase_s;
     if (threadIdx.x == 0) {
-        constexpr uint32_t id = tc::idesc_bf16(128, N, 0, 0);
+        constexpr uint32_t id = tc::idesc_bf16(128, N, 0, BMN);
         const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(B);
         const unsigned long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {  // K = 64: four K = 16 steps inside the 128-byte swizzle atom
-                const uint64_t bd = tc::sdesc(b0 + ks * 32, 16, 1024);
+                // B MN-major (N contiguous): K = 16 rows of 128 B per step, as the backward's dV / dK B operands
+                const uint64_t bd = BMN ? tc::sdesc(b0 + ks * 2048, 128 * 128, 1024) : tc::sdesc(b0 + ks * 32, 16, 1024);
                 if (TS) tc::mma_bf16_ts(tb, tb + 256 + ks * 8, bd, id, 1);
                 else tc::mma_bf16(tb, tc::sdesc(a0 + ks * 32, 16, 1024), bd, id, 1);
             }
@@ -55,12 +56,12 @@ __global__ void __launch_bounds__(128, 1) k(unsigned long long* out, int iters) 
     }
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int BMN = 0>
 void run(const char* name, unsigned long long* d, int sms) {
     const int iters = 4096, smem = 16384 + 32768 + 1024;
-    cudaFuncSetAttribute(k<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<N, TS><<<sms, 128, smem>>>(d, 16);  // warm-up
-    k<N, TS><<<sms, 128, smem>>>(d, iters);
+    cudaFuncSetAttribute(k<N, TS, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<N, TS, BMN><<<sms, 128, smem>>>(d, 16);  // warm-up
+    k<N, TS, BMN><<<sms, 128, smem>>>(d, iters);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long clk = 0;
     cudaMemcpy(&clk, d, 8, cudaMemcpyDeviceToHost);
@@ -80,5 +81,8 @@ int main() {
     run<64, true>("TS M=128 N=64", d, sms);
     run<128, true>("TS M=128 N=128", d, sms);
     run<256, true>("TS M=128 N=256", d, sms);
+    run<64, true, 1>("TS M=128 N=64 B MN-major", d, sms);
+    run<128, true, 1>("TS M=128 N=128 B MN-major", d, sms);
+    run<64, false, 1>("SS M=128 N=64 B MN-major", d, sms);
     return 0;
 }
