@@ -286,7 +286,7 @@ def run_reference(args, c):
     value = info["value"]
     out = {"metric": "packed tokens/s, tri-model logprob+GRPO loss at 1/2/4/8 B200 vs CPU ref", "value": value,
            "unit": "packed tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1000.0 * float(np.mean(secs)), "higher_is_better": True, "scaling": "weak",
+           "ms_per_step": 1000.0 * float(np.mean(secs)), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.config} model dims: d={c['d']} H={c['H']} L={c['L']} F={c['F']} "
                                   f"V={c['vocab']}; executed sample: P={rb.P} G={rb.G} R={rb.R} (T={rb.T}) x "
