@@ -94,3 +94,52 @@ def test_multi_group_equals_per_group(P, orc, prec):
             assert np.abs(lp_m[s] - lp_s[s]).max() < 0.05
         assert rel < 2e-2, rel
     assert st_m["total_units"] == st_s["total_units"]
+
+
+def test_multi_pack_every_array_bit_exact(P):
+    """All eleven K1 arrays of a several-group sequence with ragged group sizes and prompt lengths
+    of every residue mod 4: each group is laid out exactly as a single pack_group of its own,
+    shifted by its packed offset (positions restart; segments, scored rows, head-row CSR and the
+    sample ids continue across groups; a group's first position has no predecessor)."""
+    import ctypes as C
+
+    from tests.test_gpu_parity import _pack_arrays_np
+
+    f = P.LIB.parl_debug_group_arrays
+    f.restype, f.argtypes = C.c_int, [C.c_void_p, C.c_void_p]
+    ctx = P.Context(0, P.PREC_FP32)
+    rng = np.random.default_rng(9)
+    for trial in range(4):
+        n = int(rng.integers(2, 7))
+        sizes = [int(rng.integers(1, 7)) for _ in range(n)]
+        prompts = [rng.integers(4, 151936, int(rng.integers(1, 200))).astype(np.int32) for _ in range(n)]
+        resps = [[rng.integers(4, 151936, int(rng.integers(1, 300))).astype(np.int32) for _ in range(G)] for G in sizes]
+        T = sum(len(p) + sum(len(r) for r in rs) for p, rs in zip(prompts, resps))
+        g = P.Group(T, sum(sizes), ctx).pack_multi(prompts, resps, 4096)
+        S = g.S
+        exp = {k: [] for k in ("tokens", "labels", "positions", "seg", "pred", "row_ptr", "scored_pos", "scored_label",
+                               "pred_pos", "sample_of", "row_idx")}
+        gs = s0 = k0 = 0
+        for q, (p, rs) in enumerate(zip(prompts, resps)):
+            ref, Tq, Sq = _pack_arrays_np(p, rs)
+            exp["tokens"].append(ref["tokens"])
+            exp["labels"].append(ref["labels"])
+            exp["positions"].append(ref["positions"])
+            exp["seg"].append(ref["seg"] + q + k0)
+            exp["pred"].append(np.where(ref["pred"] < 0, -1, ref["pred"] + gs))
+            exp["row_ptr"].append(ref["row_ptr"][:Tq] + s0)
+            exp["scored_pos"].append(ref["scored_pos"] + gs)
+            exp["scored_label"].append(ref["scored_label"])
+            exp["pred_pos"].append(ref["pred_pos"] + gs)
+            exp["sample_of"].append(ref["sample_of"] + k0)
+            exp["row_idx"].append(ref["row_idx"] + s0)
+            gs, s0, k0 = gs + Tq, s0 + Sq, k0 + len(rs)
+        exp["row_ptr"].append(np.array([S]))
+        exp = {k: np.concatenate(v) for k, v in exp.items()}
+        buf = np.zeros(6 * T + 1 + 5 * S, np.int32)
+        assert f(g.h, buf.ctypes.data) == 0
+        off = 0
+        for name, m in (("tokens", T), ("labels", T), ("positions", T), ("seg", T), ("pred", T), ("row_ptr", T + 1),
+                        ("scored_pos", S), ("scored_label", S), ("pred_pos", S), ("sample_of", S), ("row_idx", S)):
+            assert np.array_equal(buf[off:off + m], exp[name]), (trial, name)
+            off += m
