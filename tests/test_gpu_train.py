@@ -422,3 +422,40 @@ def test_logprob_rows_normalized(P, ctx32):
     labels = [-1, -1, 9, -1, -1]
     out = P.forward_logprobs(p, tokens, np.arange(5), P.AttentionMaskSpec.causal(), labels)
     assert out.logprobs[0] == rows[1, 9]
+
+
+@pytest.mark.parametrize("mean_only", [False, True])
+def test_grpo_device_path_rewards_at_scale(P, ctx32, mean_only):
+    """K7 on the device path (fp32 log-probs in the group, advantages rebuilt in-kernel from the
+    rewards per prompt group, grpo.cpp:24-48) over ~0.8M scored tokens of 24 groups x 8 ragged
+    responses packed into one sequence, against the fp64 GRPO terms of the same fp32 inputs."""
+    from oracle import torch_ref as TR
+
+    rng = np.random.default_rng(21)
+    n, G = 24, 8
+    prompts = [rng.integers(4, 4096, int(rng.integers(1, 64))).astype(np.int32) for _ in range(n)]
+    resps = [[rng.integers(4, 4096, int(rng.integers(1, 8000))).astype(np.int32) for _ in range(G)] for _ in range(n)]
+    T = sum(len(p) + sum(len(r) for r in rs) for p, rs in zip(prompts, resps))
+    g = P.Group(T, n * G, ctx32).pack_multi(prompts, resps, 1 << 16)
+    S = g.S
+    lens = [len(r) for rs in resps for r in rs]
+    lp = (-3 * rng.random(S)).astype(np.float32).astype(np.float64)  # the group holds fp32 log-probs
+    old = (lp + 0.3 * rng.standard_normal(S)).astype(np.float32).astype(np.float64)
+    ref = (lp + 0.1 * rng.standard_normal(S)).astype(np.float32).astype(np.float64)
+    for slot, v in enumerate((lp, old, ref)):
+        g.set_logprobs(slot, v)
+    rewards = rng.random(n * G)
+    ctx32.stats_reset()
+    st = P.grpo_loss(ctx32, g, P.HyperParams(0.2, 0.04, "token", mean_only), rewards=rewards)
+    adv = np.concatenate([TR.group_advantages(rewards[q * G:(q + 1) * G], mean_only) for q in range(n)])
+    up, st_x = TR.grpo_terms(lp, old, ref, lens, adv)
+    # the clipped gradient is discontinuous at r = 1 +- eps: a ratio within fp32 rounding of the
+    # boundary may take the other branch (the clipped value itself is continuous there)
+    r = np.exp(lp - old)
+    edge = (np.abs(r - 0.8) < 2e-6) | (np.abs(r - 1.2) < 2e-6)
+    assert edge.sum() <= max(8, 1e-5 * S)
+    assert np.allclose(g.upstream()[~edge], up[~edge], rtol=2e-5, atol=1e-10)
+    scale = np.abs(adv).sum() + abs(st_x[0])
+    assert abs(st["objective_sum"] - st_x[0]) <= 1e-5 * scale
+    assert abs(st["kl_sum"] - st_x[2]) <= 1e-5 * (abs(st_x[2]) + 1)
+    assert abs(st["clipped_units"] - st_x[3]) <= edge.sum() and st["total_units"] == st_x[4]
